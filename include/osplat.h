@@ -1,0 +1,190 @@
+/* osplat.h — C ABI of the B200-native ERP Gaussian-splatting hot path (libosplat_b200.so).
+ *
+ * Part 1 re-exports the reference C interface for this path with byte-identical signatures and
+ * semantics (reference: /root/reference/proj/include/omnisplat/capi.h). Every call returns
+ * osplat_status; on failure osplat_last_error() holds "<ErrorCode>: message" for the calling
+ * thread (capi.cpp:39,68-81). Handles are opaque and freed with their _free function (NULL OK).
+ *
+ * Part 2 adds the device-resident render / backward / step interface the reference exposes only
+ * in C++ (rasterizer.hpp:85-86 render, gradients.hpp:43-44 backward, trainer.hpp:80-81
+ * adam_step), as plain-pointer C entry points. No torch or CUDA types appear in any signature;
+ * streams and device buffers cross the boundary as void* / typed device pointers.
+ *
+ * Threading contract (same as the reference, SPEC.md exclusivity): an osplat_gpu context and the
+ * frames it produced must not be used concurrently from two host threads. Calls are ordered on
+ * the context's CUDA stream; every call that returns host data synchronizes that stream.
+ */
+#ifndef OSPLAT_B200_H
+#define OSPLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define OSPLAT_API __attribute__((visibility("default")))
+#else
+#define OSPLAT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ======================================================================================
+ * Part 1 — reference C ABI (capi.h)
+ * ====================================================================================== */
+
+/* capi.h:15-23 */
+typedef enum osplat_status {
+    OSPLAT_OK = 0,
+    OSPLAT_ERR_INVALID_ARGUMENT = 1,
+    OSPLAT_ERR_IO = 2,
+    OSPLAT_ERR_PARSE = 3,
+    OSPLAT_ERR_VALIDATION = 4,
+    OSPLAT_ERR_UNSUPPORTED = 5,
+    OSPLAT_ERR_RUNTIME = 6
+} osplat_status;
+
+typedef struct osplat_cloud osplat_cloud;   /* capi.h:25 — host GaussianCloud (scene.hpp:31-55) */
+typedef struct osplat_config osplat_config; /* capi.h:27 — TrainConfig (trainer.hpp:19-51) */
+typedef struct osplat_image osplat_image;   /* capi.h:28 — H x W x 3 double image (image.hpp) */
+
+OSPLAT_API const char* osplat_version(void);     /* capi.h:31 */
+OSPLAT_API const char* osplat_last_error(void);  /* capi.h:33 */
+/* capi.h:36 — accepted for compatibility; the GPU path has no CPU worker pool. */
+OSPLAT_API void osplat_set_threads(int n);
+
+/* capi.h:39-42 — checkpoint PLY (dataio.cpp:347-453 format: binary little-endian float32). */
+OSPLAT_API osplat_status osplat_cloud_load(const char* path, osplat_cloud** out);
+OSPLAT_API osplat_status osplat_cloud_save(const osplat_cloud* cloud, const char* path);
+OSPLAT_API size_t osplat_cloud_count(const osplat_cloud* cloud);
+OSPLAT_API void osplat_cloud_free(osplat_cloud* cloud);
+
+/* capi.h:56-60 — training configuration (set_train_config_field keys, dataio.cpp:570-605). */
+OSPLAT_API osplat_status osplat_config_create(osplat_config** out);
+OSPLAT_API osplat_status osplat_config_set(osplat_config* config, const char* key, const char* value);
+OSPLAT_API void osplat_config_free(osplat_config* config);
+
+/* capi.h:73-74 — renders on the GPU (device OSPLAT_DEVICE, default 0), tile 16, black
+ * background, the cloud's active SH degree; synchronous; *out owns an H x W x 3 double image. */
+OSPLAT_API osplat_status osplat_render(const osplat_cloud* cloud, const double transform_cw[16], int width, int height,
+                            osplat_image** out);
+
+/* capi.h:84-88 */
+OSPLAT_API int osplat_image_width(const osplat_image* image);
+OSPLAT_API int osplat_image_height(const osplat_image* image);
+OSPLAT_API const double* osplat_image_pixels(const osplat_image* image);
+OSPLAT_API void osplat_image_free(osplat_image* image);
+
+/* ======================================================================================
+ * Part 2 — device-resident render / backward / step interface
+ * ====================================================================================== */
+
+/* Build a host cloud from reference-layout arrays (GaussianCloud fields, scene.hpp:35-39):
+ * positions n*3, sh n*(sh_degree+1)^2*3, rotations n*4 (w,x,y,z), log_scales n*3, opacity n. */
+OSPLAT_API osplat_status osplat_cloud_create(size_t n, int sh_degree, int active_sh_degree, const double* positions,
+                                  const double* sh, const double* rotations, const double* log_scales,
+                                  const double* opacity_logits, osplat_cloud** out);
+/* Copy a host cloud back out (any pointer may be NULL). */
+OSPLAT_API osplat_status osplat_cloud_read(const osplat_cloud* cloud, double* positions, double* sh, double* rotations,
+                                double* log_scales, double* opacity_logits, int* sh_degree,
+                                int* active_sh_degree);
+
+typedef struct osplat_gpu osplat_gpu;     /* device context: parameters, gradients, Adam moments */
+typedef struct osplat_frame osplat_frame; /* retained forward state of one render (RenderOutput) */
+
+/* Create a context on `device`, ordering all work on `cuda_stream` (a cudaStream_t; NULL = the
+ * context creates its own non-blocking stream), and upload `cloud` to FP32 SoA planes. */
+OSPLAT_API osplat_status osplat_gpu_create(int device, void* cuda_stream, const osplat_cloud* cloud, osplat_gpu** out);
+OSPLAT_API void osplat_gpu_free(osplat_gpu* ctx);
+OSPLAT_API size_t osplat_gpu_count(const osplat_gpu* ctx);
+OSPLAT_API osplat_status osplat_gpu_set_active_sh_degree(osplat_gpu* ctx, int degree);
+/* Download the current parameters into a new host cloud. */
+OSPLAT_API osplat_status osplat_gpu_download(osplat_gpu* ctx, osplat_cloud** out);
+OSPLAT_API osplat_status osplat_gpu_synchronize(osplat_gpu* ctx);
+
+/* render (rasterizer.hpp:85-86): K1 preprocess -> K2 sort -> K3 blend. transform_cw is the
+ * row-major 4x4 world->camera matrix (capi.cpp:88-95); background may be NULL (black). */
+OSPLAT_API osplat_status osplat_gpu_render(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
+                                const double background[3], osplat_frame** out);
+OSPLAT_API void osplat_frame_free(osplat_frame* frame);
+OSPLAT_API int osplat_frame_width(const osplat_frame* frame);
+OSPLAT_API int osplat_frame_height(const osplat_frame* frame);
+/* Host copies of the RenderOutput pixel state (rasterizer.hpp:52-57); NULL pointers skipped.
+ * rgb is H x W x 3 (interleaved, like Image), the rest H x W. */
+OSPLAT_API osplat_status osplat_frame_image(const osplat_frame* frame, double* rgb);
+OSPLAT_API osplat_status osplat_frame_pixels(const osplat_frame* frame, float* rgb, float* transmittance,
+                                  int* contributors, int* last_contrib);
+/* Per-Gaussian projection state indexed by Gaussian id (n entries): visible flag, FP64 centre
+ * (2), FP64 conic (3), opacity, FP32 colour (3), tile rect {tx0,tx1,ty0,ty1} (4), instances. */
+OSPLAT_API osplat_status osplat_frame_projections(const osplat_frame* frame, uint8_t* visible, double* p, double* conic,
+                                       double* opacity, float* color, int32_t* rect, uint32_t* touched);
+/* Sorted tile lists: *instances = M; ranges (2 per tile, [begin, end)) and gaussian ids (M).
+ * Call with NULL arrays first to size them. */
+OSPLAT_API osplat_status osplat_frame_tiles(const osplat_frame* frame, int* tiles_x, int* tiles_y, size_t* instances,
+                                 uint32_t* ranges, uint32_t* gaussian_ids);
+
+/* Device views for zero-copy interop (e.g. wrapping as torch tensors for NCCL). */
+typedef struct osplat_frame_view {
+    float* rgb;           /* 3 planes of H*W (R, G, B) */
+    float* transmittance; /* H*W */
+    int* contributors;    /* H*W */
+    int* last_contrib;    /* H*W */
+    int width, height;
+} osplat_frame_view;
+OSPLAT_API osplat_status osplat_frame_device(const osplat_frame* frame, osplat_frame_view* view);
+
+typedef struct osplat_gpu_view {
+    float* params;    /* planes * stride FP32: pos 3 | SH 3*bc | rot 4 | log-scale 3 | opacity 1 */
+    float* grads;     /* same layout; the buffer NCCL allreduces */
+    float* adam_m;
+    float* adam_v;
+    float* d_screen;  /* n * 2 */
+    double* screen_norm_sum;
+    int32_t* screen_hits;
+    size_t n, stride;
+    int planes, sh_degree, active_sh_degree;
+    long adam_step;
+} osplat_gpu_view;
+OSPLAT_API osplat_status osplat_gpu_view_buffers(osplat_gpu* ctx, osplat_gpu_view* view);
+
+/* backward (gradients.hpp:43-44). d_image is dL/dC: host H x W x 3 double (reference Image
+ * layout) for osplat_gpu_backward, device planar FP32 (3 planes of H*W) for _device. With
+ * accumulate = 0 the raw-parameter gradients are overwritten (reference semantics); with 1 they
+ * are added (multi-view batches). Screen statistics always accumulate (GradientBuffer). */
+OSPLAT_API osplat_status osplat_gpu_backward(osplat_gpu* ctx, const osplat_frame* frame, const double* d_image, int accumulate);
+OSPLAT_API osplat_status osplat_gpu_backward_device(osplat_gpu* ctx, const osplat_frame* frame, const float* d_image_planar,
+                                         int accumulate);
+/* Raw-parameter gradients in reference GradientBuffer layout (gradients.hpp:16-36). */
+OSPLAT_API osplat_status osplat_gpu_gradients(osplat_gpu* ctx, double* d_position, double* d_sh, double* d_rotation,
+                                   double* d_log_scale, double* d_opacity_logit, double* d_screen,
+                                   double* screen_norm_sum, long* screen_hits);
+OSPLAT_API osplat_status osplat_gpu_zero_grad(osplat_gpu* ctx);
+OSPLAT_API osplat_status osplat_gpu_reset_screen_stats(osplat_gpu* ctx);
+
+/* adam_step (trainer.hpp:80-81): one fused launch over all planes; config may be NULL
+ * (reference defaults). zero_grad != 0 clears the consumed gradients in the same pass. */
+OSPLAT_API osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_config* config, double scene_extent,
+                                   long iteration, int zero_grad);
+
+/* L1 term of loss() (trainer.cpp:25-71, lambda_ssim = 0) against a device planar FP32 target:
+ * writes dL/dC into the context's d_image buffer (returned through *d_image_planar) and the
+ * loss value (host, synchronizes) into *loss unless loss is NULL. */
+OSPLAT_API osplat_status osplat_gpu_l1_loss(osplat_gpu* ctx, const osplat_frame* frame, const float* gt_planar_device,
+                                 double mask_bottom_fraction, const float** d_image_planar, double* loss);
+
+/* One training view: render -> L1 loss -> backward (accumulate) against `gt` (host or device
+ * planar FP32, 3*H*W), returning the loss in *loss (host) — the per-view part of
+ * Trainer::run (trainer.cpp:360-363). The caller follows with osplat_gpu_adam_step. */
+OSPLAT_API osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
+                                    const float* gt_planar, int gt_on_device, double mask_bottom_fraction,
+                                    double* loss);
+
+/* Kernel launches issued by this library since load (evidence for the benchmark). */
+OSPLAT_API long long osplat_gpu_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OSPLAT_B200_H */

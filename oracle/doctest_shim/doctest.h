@@ -1,0 +1,115 @@
+// Minimal doctest-compatible harness — TEST INFRASTRUCTURE ONLY.
+// The reference's unit tests (/root/reference/proj/tests/*.cpp) include <doctest.h>, which the
+// reference does not ship (vendor/ is git-ignored, proj/.gitignore:2). This header implements just
+// the subset those files use (TEST_CASE, CHECK, CHECK_FALSE, REQUIRE, CHECK_THROWS_AS,
+// doctest::Approx with epsilon/scale) so they compile unmodified and pin the oracle.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <limits>
+#include <string>
+#include <vector>
+
+namespace doctest {
+
+class Approx {
+public:
+    explicit Approx(double v) : value_(v) {}
+    Approx& epsilon(double e) { eps_ = e; return *this; }
+    Approx& scale(double s) { scale_ = s; return *this; }
+    bool matches(double lhs) const {
+        return std::fabs(lhs - value_) < eps_ * (scale_ + std::max(std::fabs(lhs), std::fabs(value_)));
+    }
+    double value() const { return value_; }
+
+private:
+    double value_;
+    double eps_ = static_cast<double>(std::numeric_limits<float>::epsilon()) * 100;
+    double scale_ = 1.0;
+};
+
+inline bool operator==(double lhs, const Approx& rhs) { return rhs.matches(lhs); }
+inline bool operator==(const Approx& lhs, double rhs) { return lhs.matches(rhs); }
+inline bool operator!=(double lhs, const Approx& rhs) { return !rhs.matches(lhs); }
+
+namespace detail {
+
+struct Case {
+    const char* name;
+    const char* file;
+    void (*fn)();
+};
+
+inline std::vector<Case>& registry() {
+    static std::vector<Case> r;
+    return r;
+}
+inline int& failures() {
+    static int f = 0;
+    return f;
+}
+struct Registrar {
+    Registrar(const char* name, const char* file, void (*fn)()) { registry().push_back({name, file, fn}); }
+};
+struct RequireFailed {};
+
+inline void report(bool ok, const char* expr, const char* file, int line, bool fatal) {
+    if (ok) return;
+    ++failures();
+    std::printf("%s:%d: CHECK FAILED: %s\n", file, line, expr);
+    if (fatal) throw RequireFailed{};
+}
+
+inline int run_all() {
+    int cases_failed = 0, cases = 0;
+    for (const Case& c : registry()) {
+        ++cases;
+        int before = failures();
+        try {
+            c.fn();
+        } catch (const RequireFailed&) {
+        } catch (const std::exception& e) {
+            ++failures();
+            std::printf("%s: exception in \"%s\": %s\n", c.file, c.name, e.what());
+        }
+        bool ok = failures() == before;
+        if (!ok) ++cases_failed;
+        std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", c.name);
+    }
+    std::printf("[doctest] test cases: %d | %d passed | %d failed\n", cases, cases - cases_failed,
+                cases_failed);
+    return cases_failed == 0 ? 0 : 1;
+}
+
+}  // namespace detail
+}  // namespace doctest
+
+#define DOCTEST_CAT_(a, b) a##b
+#define DOCTEST_CAT(a, b) DOCTEST_CAT_(a, b)
+#define DOCTEST_TEST_CASE_IMPL(fn, name)                                                    \
+    static void fn();                                                                       \
+    static ::doctest::detail::Registrar DOCTEST_CAT(fn, _reg)(name, __FILE__, &fn);         \
+    static void fn()
+#define TEST_CASE(name) DOCTEST_TEST_CASE_IMPL(DOCTEST_CAT(doctest_case_, __COUNTER__), name)
+
+#define CHECK(...) ::doctest::detail::report(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, false)
+#define CHECK_FALSE(...) ::doctest::detail::report(!static_cast<bool>(__VA_ARGS__), "!(" #__VA_ARGS__ ")", __FILE__, __LINE__, false)
+#define REQUIRE(...) ::doctest::detail::report(static_cast<bool>(__VA_ARGS__), #__VA_ARGS__, __FILE__, __LINE__, true)
+#define CHECK_THROWS_AS(expr, type)                                                         \
+    do {                                                                                    \
+        bool caught_ = false;                                                               \
+        try {                                                                               \
+            (void)(expr);                                                                   \
+        } catch (const type&) {                                                             \
+            caught_ = true;                                                                 \
+        } catch (...) {                                                                     \
+        }                                                                                   \
+        ::doctest::detail::report(caught_, "THROWS_AS(" #expr ", " #type ")", __FILE__, __LINE__, false); \
+    } while (0)
+
+#ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
+int main() { return ::doctest::detail::run_all(); }
+#endif

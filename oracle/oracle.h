@@ -1,0 +1,111 @@
+/* oracle.h — TEST INFRASTRUCTURE ONLY (the parity checker, never the product).
+ *
+ * One C interface, two implementations:
+ *   oracle/oracle.c      -> oracle/build/liboracle.so      (our FP64 C restatement)
+ *   oracle/ref_shim.cpp  -> oracle/_ref/libref_oracle.so   (the reference's own C++ sources,
+ *                                                           compiled from /root/reference)
+ * Both export exactly these symbols so tests can diff them bit-for-bit.  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may load them.
+ *
+ * Layouts follow the reference GaussianCloud (proj/include/omnisplat/scene.hpp:31-55):
+ *   positions  n x 3, sh n x bc x 3 (bc = (sh_degree+1)^2, RGB triples per basis function),
+ *   rotations  n x 4 (w, x, y, z raw), log_scales n x 3, opacity_logits n.
+ * Poses are 12 doubles: row-major 3x3 world->camera rotation, then translation
+ * (proj/include/omnisplat/camera.hpp:21-30). */
+#ifndef OSPLAT_ORACLE_H
+#define OSPLAT_ORACLE_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct oracle_cloud {
+    int n;
+    int sh_degree;
+    int active_sh_degree;
+    double* positions;
+    double* sh;
+    double* rotations;
+    double* log_scales;
+    double* opacity_logits;
+} oracle_cloud;
+
+/* GradientBuffer (proj/include/omnisplat/gradients.hpp:16-36); caller-owned arrays. */
+typedef struct oracle_grads {
+    double* d_position;      /* n x 3 */
+    double* d_sh;            /* n x bc x 3 */
+    double* d_rotation;      /* n x 4 */
+    double* d_log_scale;     /* n x 3 */
+    double* d_opacity_logit; /* n */
+    double* d_screen;        /* n x 2 */
+    double* screen_norm_sum; /* n, accumulated across calls */
+    long* screen_hits;       /* n, accumulated across calls */
+} oracle_grads;
+
+/* AdamState (proj/include/omnisplat/trainer.hpp:64-75), same flat layouts. */
+typedef struct oracle_adam {
+    double *m_position, *v_position;
+    double *m_sh, *v_sh;
+    double *m_rotation, *v_rotation;
+    double *m_scale, *v_scale;
+    double *m_opacity, *v_opacity;
+    long step;
+} oracle_adam;
+
+/* The TrainConfig fields adam_step reads (proj/include/omnisplat/trainer.hpp:19-51). */
+typedef struct oracle_adam_cfg {
+    long iterations;
+    double lr_position_init, lr_position_final;
+    double lr_sh_dc, lr_sh_rest, lr_opacity, lr_scale, lr_rotation;
+} oracle_adam_cfg;
+
+typedef struct oracle_frame oracle_frame;
+
+/* render(): project -> bin -> blend (proj/src/rasterizer.cpp:159-175). NULL on error. */
+oracle_frame* oracle_render(const oracle_cloud* cloud, const double pose[12], int width, int height,
+                            const double background[3]);
+/* reference_render(): brute-force oracle (proj/src/rasterizer.cpp:177-235). */
+oracle_frame* oracle_reference_render(const oracle_cloud* cloud, const double pose[12], int width,
+                                      int height, const double background[3]);
+void oracle_frame_free(oracle_frame* frame);
+
+int oracle_frame_num_projections(const oracle_frame* frame);
+/* SplatProjection fields (proj/include/omnisplat/rasterizer.hpp:31-41); any pointer may be NULL. */
+void oracle_frame_projections(const oracle_frame* frame, int* gaussian_id, double* p /*2*/,
+                              double* cov /*3*/, double* conic /*3*/, double* radius,
+                              double* depth, double* color /*3*/, double* alpha_base,
+                              double* t /*3*/);
+/* Tile grid: returns the instance count M. */
+long oracle_frame_tile_count(const oracle_frame* frame, int* tiles_x, int* tiles_y);
+/* CSR tile lists: offsets[tiles+1], items[M] = projection indices in blend order. */
+void oracle_frame_tile_lists(const oracle_frame* frame, long* offsets, int* items);
+/* RenderOutput pixel planes: rgb H x W x 3, T / contributors / last_contrib H x W. */
+void oracle_frame_pixels(const oracle_frame* frame, double* rgb, double* transmittance,
+                         int* contributors, int* last_contrib);
+
+/* backward() (proj/src/gradients.cpp:72-296). Overwrites the gradients, accumulates the
+ * screen statistics. Returns 0 on success, nonzero on StateMismatch. */
+int oracle_backward(const oracle_frame* frame, const double* d_image, const oracle_cloud* cloud,
+                    const double pose[12], int width, int height, oracle_grads* grads);
+
+/* adam_step() (proj/src/trainer.cpp:143-178); mutates cloud and state. */
+void oracle_adam_step(oracle_cloud* cloud, const oracle_grads* grads, oracle_adam* state,
+                      const oracle_adam_cfg* cfg, double scene_extent, long iteration);
+
+/* loss() (proj/src/trainer.cpp:25-71): (1-l)L1 + l(1-SSIM) with bottom-row masking.
+ * d_image (H x W x 3) receives dL/dC; returns the loss value. */
+double oracle_loss(const double* rendered, const double* gt, int width, int height,
+                   double lambda_ssim, double mask_bottom_fraction, double* d_image);
+
+/* Thread count of the implementation (reference: OMNISPLAT_THREADS; restatement: 1). */
+void oracle_set_threads(int n);
+int oracle_threads(void);
+const char* oracle_kind(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

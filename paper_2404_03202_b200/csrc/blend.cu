@@ -1,0 +1,129 @@
+// blend.cu — K3: per-tile front-to-back alpha blending (proj/src/rasterizer.cpp:100-157).
+//
+// One 256-thread CTA per 16x16 tile, one pixel per thread. The tile list is walked in chunks of
+// 256 entries staged cooperatively into shared memory (FP64 centre -> tile-relative FP32 offsets,
+// seam-wrapped once per (entry, tile)); every thread then reads the chunk with broadcast LDS.128.
+// The CTA leaves the list as soon as all 256 pixels have terminated (__syncthreads_count).
+// FP32 fast path + FP64 guard (pair.cuh): power/alpha decisions near a threshold and T near the
+// 1e-4 stop are decided in FP64 exactly like the reference; a T decision inside the band replays
+// the pixel's prefix in FP64 and the pixel continues in FP64 ("exact mode").
+#include "kernels.h"
+#include "pair.cuh"
+
+namespace osb {
+
+namespace {
+
+__global__ void __launch_bounds__(kStage) k_blend(const uint32_t* __restrict__ inst_gid, const uint2* __restrict__ ranges,
+                                                  PreprocessOut pp, int W, int H, int tiles_x, float bg0, float bg1,
+                                                  float bg2, FrameBuffers fb) {
+    __shared__ StageSmem sm;
+    const int tile = blockIdx.x;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const int px = tx * kTile + lx, py = ty * kTile + ly;
+    const bool inside = px < W && py < H;
+    const uint2 range = ranges[tile];
+    const double width = W;
+    const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
+    const float lxo = lx - 7.5f, lyo = ly - 7.5f;
+    const float halfW = 0.5f * W, fW = static_cast<float>(W);
+
+    float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
+    double T64 = 1.0;
+    bool exact = false;
+    int contrib = 0, last = 0;
+    bool done = !inside;
+
+    for (uint32_t base = range.x; base < range.y; base += kStage) {
+        __syncthreads();
+        const uint32_t idx = base + threadIdx.x;
+        if (idx < range.y) stage_splat(sm, threadIdx.x, inst_gid[idx], pp.pxy, pp.splat, pp.delta, xc, yc, width);
+        if (__syncthreads_count(done) == kStage) break;
+        const int cnt = min(kStage, static_cast<int>(range.y - base));
+        for (int j = 0; j < cnt && !done; ++j) {
+            const float4 A = sm.a[j];
+            const float4 B = sm.b[j];
+            float dx, dy, power;
+            bool unc;
+            if (!pair_power(A, B, lxo, lyo, halfW, fW, dx, dy, power, unc)) continue;
+            const float4 Cc = sm.c[j];
+            const uint32_t k = base + j;
+            float alpha;
+            double a64 = 0.0;
+            if (unc || exact) {
+                Pair64 p;
+                if (!pair_slow(sm.gid[j], px, py, width, pp.pxy, pp.conic_o, &p)) continue;
+                a64 = p.alpha;
+                alpha = static_cast<float>(a64);
+            } else {
+                alpha = fminf(0.99f, Cc.w * ex2_approx(-power * kLog2e));
+            }
+            float w;
+            if (!exact) {
+                const float Tn = T * (1.0f - alpha);
+                if (Tn < kTHi) {
+                    if (Tn < kTLo) {
+                        done = true;
+                        break;
+                    }
+                    // Inside the band: decide in FP64 from an exact replay of the prefix.
+                    T64 = replay_T(inst_gid, range.x, k, px, py, width, pp.pxy, pp.conic_o);
+                    if (!unc) {
+                        Pair64 p;
+                        pair_slow(sm.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
+                        a64 = p.alpha;
+                    }
+                    const double Tn64 = T64 * (1.0 - a64);
+                    if (Tn64 < kTStop) {
+                        done = true;
+                        break;
+                    }
+                    exact = true;
+                    w = static_cast<float>(a64 * T64);
+                    T64 = Tn64;
+                    T = static_cast<float>(Tn64);
+                } else {
+                    w = alpha * T;
+                    T = Tn;
+                }
+            } else {
+                const double Tn64 = T64 * (1.0 - a64);
+                if (Tn64 < kTStop) {
+                    done = true;
+                    break;
+                }
+                w = static_cast<float>(a64 * T64);
+                T64 = Tn64;
+                T = static_cast<float>(Tn64);
+            }
+            c0 = __fmaf_rn(Cc.x, w, c0);
+            c1 = __fmaf_rn(Cc.y, w, c1);
+            c2 = __fmaf_rn(Cc.z, w, c2);
+            ++contrib;
+            last = static_cast<int>(k - range.x) + 1;
+        }
+    }
+    if (inside) {
+        const size_t pix = static_cast<size_t>(py) * W + px;
+        const size_t plane = static_cast<size_t>(W) * H;
+        fb.rgb[pix] = __fmaf_rn(T, bg0, c0);
+        fb.rgb[plane + pix] = __fmaf_rn(T, bg1, c1);
+        fb.rgb[2 * plane + pix] = __fmaf_rn(T, bg2, c2);
+        fb.T[pix] = T;
+        fb.contrib[pix] = contrib;
+        fb.last[pix] = last;
+    }
+}
+
+}  // namespace
+
+void launch_blend(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H, int tiles_x,
+                  int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s) {
+    const int tiles = tiles_x * tiles_y;
+    if (tiles <= 0) return;
+    k_blend<<<tiles, kStage, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb);
+    OSB_LAUNCHED(1);
+}
+
+}  // namespace osb

@@ -1,0 +1,782 @@
+// capi.cpp — the C ABI (include/osplat.h): the reference osplat_* symbols for this path
+// (proj/src/capi.cpp) plus the device-resident extension. Error mapping follows
+// capi.cpp:41-81: typed errors -> osplat_status, "<ErrorCode>: message" in a thread-local
+// buffer that is cleared on success.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/osplat.h"
+#include "engine.h"
+
+using osb::Engine;
+using osb::HostCloud;
+
+struct osplat_cloud {
+    HostCloud cloud;
+    mutable std::shared_ptr<Engine> render_cache;  // device copy used by osplat_render
+};
+struct osplat_image {
+    int width = 0, height = 0;
+    std::vector<double> data;
+};
+struct osplat_config {
+    // TrainConfig (trainer.hpp:19-51) with the reference defaults
+    double lambda_ssim = 0.2;
+    long iterations = 7000, densify_until = 15000, densify_interval = 100, opacity_reset_interval = 3000;
+    double densify_grad_threshold = 2e-4, scale_split_threshold = 0.01, split_factor = 1.6, prune_opacity = 0.005;
+    double prune_scale_world = 0.1, prune_radius_px = 20.0, opacity_reset_ceiling = 0.01;
+    double lr_position_init = 1.6e-4, lr_position_final = 1.6e-6, lr_sh_dc = 2.5e-3, lr_sh_rest = 2.5e-3 / 20.0;
+    double lr_opacity = 5e-2, lr_scale = 5e-3, lr_rotation = 1e-3, mask_bottom_fraction = 0.0;
+    int sh_degree = 3;
+    long sh_warmup_interval = 1000;
+    unsigned long long seed = 0;
+    long checkpoint_interval = 0, log_interval = 100;
+};
+struct osplat_gpu {
+    std::shared_ptr<Engine> engine;
+};
+struct osplat_frame {
+    std::shared_ptr<Engine> engine;
+    osb::Frame* frame = nullptr;
+};
+
+namespace {
+
+// Reference ErrorCode subset used on this path (error.hpp:8-25) and its status mapping.
+enum class Code { ValidationError, StateMismatch, DimensionMismatch, ParseError, UnsupportedFormat, MissingProperty,
+                  VersionMismatch, IoError, InvalidArgument };
+
+struct ApiError : std::runtime_error {
+    Code code;
+    ApiError(Code c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+const char* code_name(Code c) {
+    switch (c) {
+        case Code::ValidationError: return "ValidationError";
+        case Code::StateMismatch: return "StateMismatch";
+        case Code::DimensionMismatch: return "DimensionMismatch";
+        case Code::ParseError: return "ParseError";
+        case Code::UnsupportedFormat: return "UnsupportedFormat";
+        case Code::MissingProperty: return "MissingProperty";
+        case Code::VersionMismatch: return "VersionMismatch";
+        case Code::IoError: return "IoError";
+        case Code::InvalidArgument: return "InvalidArgument";
+    }
+    return "Unknown";
+}
+
+osplat_status map_code(Code c) {  // capi.cpp:41-66
+    switch (c) {
+        case Code::ParseError:
+        case Code::MissingProperty: return OSPLAT_ERR_PARSE;
+        case Code::ValidationError:
+        case Code::DimensionMismatch:
+        case Code::StateMismatch: return OSPLAT_ERR_VALIDATION;
+        case Code::UnsupportedFormat:
+        case Code::VersionMismatch: return OSPLAT_ERR_UNSUPPORTED;
+        case Code::IoError: return OSPLAT_ERR_IO;
+        case Code::InvalidArgument: return OSPLAT_ERR_INVALID_ARGUMENT;
+    }
+    return OSPLAT_ERR_RUNTIME;
+}
+
+thread_local std::string t_last_error;
+
+template <typename Fn>
+osplat_status wrap(Fn&& fn) {
+    try {
+        fn();
+        t_last_error.clear();
+        return OSPLAT_OK;
+    } catch (const ApiError& e) {
+        t_last_error = std::string(code_name(e.code)) + ": " + e.what();
+        return map_code(e.code);
+    } catch (const std::invalid_argument& e) {
+        t_last_error = std::string("InvalidArgument: ") + e.what();
+        return OSPLAT_ERR_INVALID_ARGUMENT;
+    } catch (const std::exception& e) {
+        t_last_error = e.what();
+        return OSPLAT_ERR_RUNTIME;
+    }
+}
+
+osplat_status invalid(const char* message) {
+    t_last_error = message;
+    return OSPLAT_ERR_INVALID_ARGUMENT;
+}
+
+// Row-major 4x4 -> pose (capi.cpp:88-95) and Pose::is_valid (camera.cpp:7-19).
+void pose_from_rowmajor(const double t[16], double p12[12]) {
+    for (int r = 0; r < 3; ++r) {
+        for (int c = 0; c < 3; ++c) p12[r * 3 + c] = t[r * 4 + c];
+        p12[9 + r] = t[r * 4 + 3];
+    }
+}
+
+bool pose_is_valid(const double* w, double tol = 1e-6) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < 3; ++k) s += w[k * 3 + i] * w[k * 3 + j];
+            double expect = i == j ? 1.0 : 0.0;
+            if (std::abs(s - expect) > tol) return false;
+        }
+    double det = w[0] * (w[4] * w[8] - w[5] * w[7]) - w[1] * (w[3] * w[8] - w[5] * w[6]) +
+                 w[2] * (w[3] * w[7] - w[4] * w[6]);
+    return std::abs(det - 1.0) <= tol;
+}
+
+void checked_pose(const double t[16], double p12[12]) {
+    pose_from_rowmajor(t, p12);
+    if (!pose_is_valid(p12)) throw ApiError(Code::ValidationError, "pose rotation is not orthonormal");
+}
+
+int default_device() {
+    const char* env = std::getenv("OSPLAT_DEVICE");
+    return env ? std::atoi(env) : 0;
+}
+
+// ------------------------------------------------------------------ checkpoint PLY (dataio.cpp:347-453)
+
+constexpr int kCheckpointVersion = 1;
+
+void save_checkpoint(const HostCloud& c, const std::string& path) {
+    const int bc = c.bc();
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw ApiError(Code::IoError, "cannot write " + path);
+    out << "ply\nformat binary_little_endian 1.0\n";
+    out << "comment format_version " << kCheckpointVersion << "\n";
+    out << "comment sh_degree " << c.sh_degree << "\n";
+    out << "element vertex " << c.n() << "\n";
+    for (const char* p : {"x", "y", "z", "nx", "ny", "nz", "f_dc_0", "f_dc_1", "f_dc_2"})
+        out << "property float " << p << "\n";
+    for (int i = 0; i < (bc - 1) * 3; ++i) out << "property float f_rest_" << i << "\n";
+    out << "property float opacity\n";
+    for (int i = 0; i < 3; ++i) out << "property float scale_" << i << "\n";
+    for (int i = 0; i < 4; ++i) out << "property float rot_" << i << "\n";
+    out << "end_header\n";
+    std::vector<float> row;
+    for (size_t i = 0; i < c.n(); ++i) {
+        row.clear();
+        for (int k = 0; k < 3; ++k) row.push_back(static_cast<float>(c.positions[3 * i + k]));
+        for (int k = 0; k < 3; ++k) row.push_back(0.0f);
+        const double* sh = &c.sh[i * bc * 3];
+        for (int ch = 0; ch < 3; ++ch) row.push_back(static_cast<float>(sh[ch]));
+        for (int ch = 0; ch < 3; ++ch)  // f_rest channel-major (dataio.cpp:374-376)
+            for (int j = 1; j < bc; ++j) row.push_back(static_cast<float>(sh[j * 3 + ch]));
+        row.push_back(static_cast<float>(c.opacity[i]));
+        for (int k = 0; k < 3; ++k) row.push_back(static_cast<float>(c.log_scales[3 * i + k]));
+        for (int k = 0; k < 4; ++k) row.push_back(static_cast<float>(c.rotations[4 * i + k]));
+        out.write(reinterpret_cast<const char*>(row.data()), static_cast<std::streamsize>(row.size() * 4));
+    }
+    if (!out) throw ApiError(Code::IoError, "write failed for " + path);
+}
+
+HostCloud load_checkpoint(const std::string& path) {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw ApiError(Code::IoError, "cannot open " + path);
+    std::string line;
+    std::getline(in, line);
+    if (line != "ply") throw ApiError(Code::ParseError, path + ": not a PLY file");
+    bool binary_le = false;
+    size_t count = 0;
+    int sh_degree = -1;
+    std::vector<std::string> props;
+    while (std::getline(in, line)) {
+        if (!line.empty() && line.back() == '\r') line.pop_back();
+        std::istringstream ls(line);
+        std::string key;
+        ls >> key;
+        if (key == "format") {
+            std::string fmt;
+            ls >> fmt;
+            binary_le = fmt == "binary_little_endian";
+            if (!binary_le) throw ApiError(Code::UnsupportedFormat, path + ": only binary_little_endian checkpoints");
+        } else if (key == "comment") {
+            std::string k2;
+            ls >> k2;
+            if (k2 == "format_version") {
+                int v = -1;
+                ls >> v;
+                if (v != kCheckpointVersion)
+                    throw ApiError(Code::VersionMismatch, path + ": checkpoint format version " + std::to_string(v));
+            } else if (k2 == "sh_degree") {
+                ls >> sh_degree;
+            }
+        } else if (key == "element") {
+            std::string name;
+            ls >> name >> count;
+            if (name != "vertex") throw ApiError(Code::UnsupportedFormat, path + ": unexpected element " + name);
+        } else if (key == "property") {
+            std::string type, name;
+            ls >> type >> name;
+            if (type != "float" && type != "float32")
+                throw ApiError(Code::UnsupportedFormat, path + ": property " + name + " is not float32");
+            props.push_back(name);
+        } else if (key == "end_header") {
+            break;
+        }
+    }
+    if (!binary_le) throw ApiError(Code::ParseError, path + ": missing format line");
+    auto find = [&](const std::string& n) -> int {
+        for (size_t i = 0; i < props.size(); ++i)
+            if (props[i] == n) return static_cast<int>(i);
+        return -1;
+    };
+    int rest = 0;
+    while (find("f_rest_" + std::to_string(rest)) >= 0) ++rest;
+    if (rest % 3 != 0) throw ApiError(Code::ParseError, path + ": f_rest count not divisible by 3");
+    const int bc_rest = rest / 3 + 1;
+    if (sh_degree < 0) {
+        int d = 0;
+        while ((d + 1) * (d + 1) < bc_rest) ++d;
+        sh_degree = d;
+    }
+    const int bc = (sh_degree + 1) * (sh_degree + 1);
+    if (bc != bc_rest) throw ApiError(Code::ParseError, path + ": sh_degree does not match f_rest count");
+    for (const char* r : {"x", "y", "z", "f_dc_0", "f_dc_1", "f_dc_2", "opacity", "scale_0", "scale_1", "scale_2",
+                          "rot_0", "rot_1", "rot_2", "rot_3"})
+        if (find(r) < 0) throw ApiError(Code::MissingProperty, path + ": missing property " + r);
+    std::vector<float> data(count * props.size());
+    if (!in.read(reinterpret_cast<char*>(data.data()), static_cast<std::streamsize>(data.size() * 4)))
+        throw ApiError(Code::ParseError, path + ": truncated vertex data");
+    HostCloud c;
+    c.sh_degree = sh_degree;
+    c.active_sh_degree = sh_degree;
+    c.positions.resize(count * 3);
+    c.sh.resize(count * bc * 3);
+    c.rotations.resize(count * 4);
+    c.log_scales.resize(count * 3);
+    c.opacity.resize(count);
+    const size_t np = props.size();
+    auto col = [&](const std::string& n, size_t i) { return static_cast<double>(data[i * np + find(n)]); };
+    for (size_t i = 0; i < count; ++i) {
+        c.positions[3 * i] = col("x", i);
+        c.positions[3 * i + 1] = col("y", i);
+        c.positions[3 * i + 2] = col("z", i);
+        for (int ch = 0; ch < 3; ++ch) c.sh[i * bc * 3 + ch] = col("f_dc_" + std::to_string(ch), i);
+        for (int ch = 0; ch < 3; ++ch)
+            for (int j = 1; j < bc; ++j)
+                c.sh[(i * bc + j) * 3 + ch] = col("f_rest_" + std::to_string(ch * (bc - 1) + (j - 1)), i);
+        c.opacity[i] = col("opacity", i);
+        for (int k = 0; k < 3; ++k) c.log_scales[3 * i + k] = col("scale_" + std::to_string(k), i);
+        for (int k = 0; k < 4; ++k) c.rotations[4 * i + k] = col("rot_" + std::to_string(k), i);
+    }
+    return c;
+}
+
+void set_config_field(osplat_config& c, const std::string& key, const std::string& value) {
+    auto as_double = [&] { return std::stod(value); };
+    auto as_long = [&] { return std::stol(value); };
+    try {
+        if (key == "lambda_ssim") c.lambda_ssim = as_double();
+        else if (key == "iterations") c.iterations = as_long();
+        else if (key == "densify_until") c.densify_until = as_long();
+        else if (key == "densify_interval") c.densify_interval = as_long();
+        else if (key == "opacity_reset_interval") c.opacity_reset_interval = as_long();
+        else if (key == "densify_grad_threshold") c.densify_grad_threshold = as_double();
+        else if (key == "scale_split_threshold") c.scale_split_threshold = as_double();
+        else if (key == "split_factor") c.split_factor = as_double();
+        else if (key == "prune_opacity") c.prune_opacity = as_double();
+        else if (key == "prune_scale_world") c.prune_scale_world = as_double();
+        else if (key == "prune_radius_px") c.prune_radius_px = as_double();
+        else if (key == "opacity_reset_ceiling") c.opacity_reset_ceiling = as_double();
+        else if (key == "lr_position_init") c.lr_position_init = as_double();
+        else if (key == "lr_position_final") c.lr_position_final = as_double();
+        else if (key == "lr_sh_dc") c.lr_sh_dc = as_double();
+        else if (key == "lr_sh_rest") c.lr_sh_rest = as_double();
+        else if (key == "lr_opacity") c.lr_opacity = as_double();
+        else if (key == "lr_scale") c.lr_scale = as_double();
+        else if (key == "lr_rotation") c.lr_rotation = as_double();
+        else if (key == "mask_bottom_fraction") c.mask_bottom_fraction = as_double();
+        else if (key == "sh_degree") c.sh_degree = static_cast<int>(as_long());
+        else if (key == "sh_warmup_interval") c.sh_warmup_interval = as_long();
+        else if (key == "seed") c.seed = std::stoull(value);
+        else if (key == "checkpoint_interval") c.checkpoint_interval = as_long();
+        else if (key == "log_interval") c.log_interval = as_long();
+        else throw ApiError(Code::ParseError, "unknown config key: " + key);
+    } catch (const std::invalid_argument&) {
+        throw ApiError(Code::ParseError, "config value for " + key + " is not a number: " + value);
+    } catch (const std::out_of_range&) {
+        throw ApiError(Code::ParseError, "config value for " + key + " is out of range: " + value);
+    }
+}
+
+osb::TrainHyper hyper_from(const osplat_config* c) {
+    osb::TrainHyper h;
+    if (!c) return h;
+    h.iterations = c->iterations;
+    h.lr_position_init = c->lr_position_init;
+    h.lr_position_final = c->lr_position_final;
+    h.lr_sh_dc = c->lr_sh_dc;
+    h.lr_sh_rest = c->lr_sh_rest;
+    h.lr_opacity = c->lr_opacity;
+    h.lr_scale = c->lr_scale;
+    h.lr_rotation = c->lr_rotation;
+    return h;
+}
+
+void check_dims(int w, int h) {
+    if (w < 2 || h < 2) throw ApiError(Code::InvalidArgument, "image size must be >= 2x2");
+    if (static_cast<long long>(w) * h > (1ll << 30)) throw ApiError(Code::InvalidArgument, "image too large");
+}
+
+// planar FP32 (3 x H*W) -> interleaved H x W x 3 double
+void planar_to_hwc(const std::vector<float>& planar, int w, int h, double* out) {
+    const size_t plane = static_cast<size_t>(w) * h;
+    for (size_t i = 0; i < plane; ++i)
+        for (int c = 0; c < 3; ++c) out[i * 3 + c] = planar[c * plane + i];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* osplat_version(void) { return "0.1.0"; }
+const char* osplat_last_error(void) { return t_last_error.c_str(); }
+void osplat_set_threads(int) {}
+
+osplat_status osplat_cloud_load(const char* path, osplat_cloud** out) {
+    if (!path || !out) return invalid("osplat_cloud_load: null argument");
+    return wrap([&] { *out = new osplat_cloud{load_checkpoint(path), nullptr}; });
+}
+
+osplat_status osplat_cloud_save(const osplat_cloud* cloud, const char* path) {
+    if (!cloud || !path) return invalid("osplat_cloud_save: null argument");
+    return wrap([&] { save_checkpoint(cloud->cloud, path); });
+}
+
+size_t osplat_cloud_count(const osplat_cloud* cloud) { return cloud ? cloud->cloud.n() : 0; }
+void osplat_cloud_free(osplat_cloud* cloud) { delete cloud; }
+
+osplat_status osplat_cloud_create(size_t n, int sh_degree, int active, const double* positions, const double* sh,
+                                  const double* rotations, const double* log_scales, const double* opacity,
+                                  osplat_cloud** out) {
+    if (!out || (n > 0 && (!positions || !sh || !rotations || !log_scales || !opacity)))
+        return invalid("osplat_cloud_create: null argument");
+    if (sh_degree < 0 || sh_degree > 3) return invalid("osplat_cloud_create: sh_degree must be in 0..3");
+    return wrap([&] {
+        auto* c = new osplat_cloud;
+        HostCloud& h = c->cloud;
+        h.sh_degree = sh_degree;
+        h.active_sh_degree = active < 0 ? 0 : (active > sh_degree ? sh_degree : active);
+        const size_t bc = static_cast<size_t>(h.bc());
+        h.positions.assign(positions, positions + 3 * n);
+        h.sh.assign(sh, sh + 3 * bc * n);
+        h.rotations.assign(rotations, rotations + 4 * n);
+        h.log_scales.assign(log_scales, log_scales + 3 * n);
+        h.opacity.assign(opacity, opacity + n);
+        *out = c;
+    });
+}
+
+osplat_status osplat_cloud_read(const osplat_cloud* cloud, double* positions, double* sh, double* rotations,
+                                double* log_scales, double* opacity, int* sh_degree, int* active) {
+    if (!cloud) return invalid("osplat_cloud_read: null cloud");
+    const HostCloud& h = cloud->cloud;
+    auto cp = [](const std::vector<double>& v, double* dst) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * 8);
+    };
+    cp(h.positions, positions);
+    cp(h.sh, sh);
+    cp(h.rotations, rotations);
+    cp(h.log_scales, log_scales);
+    cp(h.opacity, opacity);
+    if (sh_degree) *sh_degree = h.sh_degree;
+    if (active) *active = h.active_sh_degree;
+    t_last_error.clear();
+    return OSPLAT_OK;
+}
+
+osplat_status osplat_config_create(osplat_config** out) {
+    if (!out) return invalid("osplat_config_create: null argument");
+    return wrap([&] { *out = new osplat_config{}; });
+}
+
+osplat_status osplat_config_set(osplat_config* config, const char* key, const char* value) {
+    if (!config || !key || !value) return invalid("osplat_config_set: null argument");
+    return wrap([&] { set_config_field(*config, key, value); });
+}
+
+void osplat_config_free(osplat_config* config) { delete config; }
+
+osplat_status osplat_render(const osplat_cloud* cloud, const double transform_cw[16], int width, int height,
+                            osplat_image** out) {
+    if (!cloud || !transform_cw || !out) return invalid("osplat_render: null argument");
+    if (width < 2 || height < 2) return invalid("osplat_render: image size must be >= 2x2");
+    return wrap([&] {
+        double p12[12];
+        checked_pose(transform_cw, p12);
+        if (!cloud->render_cache) {
+            auto e = std::make_shared<Engine>(default_device(), nullptr);
+            e->upload(cloud->cloud);
+            cloud->render_cache = e;
+        }
+        Engine& e = *cloud->render_cache;
+        const double bg[3] = {0.0, 0.0, 0.0};
+        osb::Frame* f = e.render(p12, width, height, bg);
+        const size_t plane = static_cast<size_t>(width) * height;
+        std::vector<float> host(plane * 3);
+        try {
+            OSB_CUDA_CHECK(cudaMemcpyAsync(host.data(), f->rgb.as<float>(), plane * 12, cudaMemcpyDeviceToHost,
+                                           e.stream()));
+            OSB_CUDA_CHECK(cudaStreamSynchronize(e.stream()));
+        } catch (...) {
+            e.release(f);
+            throw;
+        }
+        e.release(f);
+        auto img = std::make_unique<osplat_image>();
+        img->width = width;
+        img->height = height;
+        img->data.resize(plane * 3);
+        planar_to_hwc(host, width, height, img->data.data());
+        *out = img.release();
+    });
+}
+
+int osplat_image_width(const osplat_image* image) { return image ? image->width : 0; }
+int osplat_image_height(const osplat_image* image) { return image ? image->height : 0; }
+const double* osplat_image_pixels(const osplat_image* image) { return image ? image->data.data() : nullptr; }
+void osplat_image_free(osplat_image* image) { delete image; }
+
+// ------------------------------------------------------------------ device-resident extension
+
+osplat_status osplat_gpu_create(int device, void* stream, const osplat_cloud* cloud, osplat_gpu** out) {
+    if (!cloud || !out) return invalid("osplat_gpu_create: null argument");
+    return wrap([&] {
+        auto g = std::make_unique<osplat_gpu>();
+        g->engine = std::make_shared<Engine>(device, static_cast<cudaStream_t>(stream));
+        g->engine->upload(cloud->cloud);
+        *out = g.release();
+    });
+}
+
+void osplat_gpu_free(osplat_gpu* ctx) { delete ctx; }
+size_t osplat_gpu_count(const osplat_gpu* ctx) { return ctx ? ctx->engine->n() : 0; }
+
+osplat_status osplat_gpu_set_active_sh_degree(osplat_gpu* ctx, int degree) {
+    if (!ctx) return invalid("osplat_gpu_set_active_sh_degree: null context");
+    return wrap([&] { ctx->engine->set_active_sh_degree(degree); });
+}
+
+osplat_status osplat_gpu_download(osplat_gpu* ctx, osplat_cloud** out) {
+    if (!ctx || !out) return invalid("osplat_gpu_download: null argument");
+    return wrap([&] { *out = new osplat_cloud{ctx->engine->download(), nullptr}; });
+}
+
+osplat_status osplat_gpu_synchronize(osplat_gpu* ctx) {
+    if (!ctx) return invalid("osplat_gpu_synchronize: null context");
+    return wrap([&] { ctx->engine->synchronize(); });
+}
+
+osplat_status osplat_gpu_render(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
+                                const double background[3], osplat_frame** out) {
+    if (!ctx || !transform_cw || !out) return invalid("osplat_gpu_render: null argument");
+    return wrap([&] {
+        check_dims(width, height);
+        double p12[12];
+        checked_pose(transform_cw, p12);
+        const double zero[3] = {0, 0, 0};
+        auto fr = std::make_unique<osplat_frame>();
+        fr->engine = ctx->engine;
+        fr->frame = ctx->engine->render(p12, width, height, background ? background : zero);
+        *out = fr.release();
+    });
+}
+
+void osplat_frame_free(osplat_frame* frame) {
+    if (!frame) return;
+    frame->engine->release(frame->frame);
+    delete frame;
+}
+
+int osplat_frame_width(const osplat_frame* f) { return f ? f->frame->W : 0; }
+int osplat_frame_height(const osplat_frame* f) { return f ? f->frame->H : 0; }
+
+osplat_status osplat_frame_image(const osplat_frame* frame, double* rgb) {
+    if (!frame || !rgb) return invalid("osplat_frame_image: null argument");
+    return wrap([&] {
+        const osb::Frame& f = *frame->frame;
+        osb::DeviceGuard g(frame->engine->device());
+        const size_t plane = static_cast<size_t>(f.W) * f.H;
+        std::vector<float> host(plane * 3);
+        OSB_CUDA_CHECK(cudaMemcpyAsync(host.data(), f.rgb.as<float>(), plane * 12, cudaMemcpyDeviceToHost,
+                                       frame->engine->stream()));
+        OSB_CUDA_CHECK(cudaStreamSynchronize(frame->engine->stream()));
+        planar_to_hwc(host, f.W, f.H, rgb);
+    });
+}
+
+osplat_status osplat_frame_pixels(const osplat_frame* frame, float* rgb, float* T, int* contrib, int* last) {
+    if (!frame) return invalid("osplat_frame_pixels: null frame");
+    return wrap([&] {
+        const osb::Frame& f = *frame->frame;
+        osb::DeviceGuard g(frame->engine->device());
+        cudaStream_t s = frame->engine->stream();
+        const size_t plane = static_cast<size_t>(f.W) * f.H;
+        std::vector<float> host;
+        if (rgb) {
+            host.resize(plane * 3);
+            OSB_CUDA_CHECK(cudaMemcpyAsync(host.data(), f.rgb.as<float>(), plane * 12, cudaMemcpyDeviceToHost, s));
+        }
+        if (T) OSB_CUDA_CHECK(cudaMemcpyAsync(T, f.T.as<float>(), plane * 4, cudaMemcpyDeviceToHost, s));
+        if (contrib) OSB_CUDA_CHECK(cudaMemcpyAsync(contrib, f.contrib.as<int>(), plane * 4, cudaMemcpyDeviceToHost, s));
+        if (last) OSB_CUDA_CHECK(cudaMemcpyAsync(last, f.last.as<int>(), plane * 4, cudaMemcpyDeviceToHost, s));
+        OSB_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (rgb)
+            for (size_t i = 0; i < plane; ++i)
+                for (int c = 0; c < 3; ++c) rgb[i * 3 + c] = host[c * plane + i];
+    });
+}
+
+osplat_status osplat_frame_projections(const osplat_frame* frame, uint8_t* visible, double* p, double* conic,
+                                       double* opacity, float* color, int32_t* rect, uint32_t* touched) {
+    if (!frame) return invalid("osplat_frame_projections: null frame");
+    return wrap([&] {
+        const osb::Frame& f = *frame->frame;
+        osb::DeviceGuard g(frame->engine->device());
+        cudaStream_t s = frame->engine->stream();
+        const size_t n = static_cast<size_t>(f.n);
+        std::vector<uint64_t> key(n);
+        std::vector<double2> pxy(n);
+        std::vector<double4> co(n);
+        std::vector<osb::Splat32> sp(n);
+        std::vector<int4> rc(n);
+        std::vector<uint32_t> tc(n);
+        if (n) {
+            OSB_CUDA_CHECK(cudaMemcpyAsync(key.data(), f.depth_key.as<void>(), n * 8, cudaMemcpyDeviceToHost, s));
+            OSB_CUDA_CHECK(cudaMemcpyAsync(pxy.data(), f.pxy.as<void>(), n * 16, cudaMemcpyDeviceToHost, s));
+            OSB_CUDA_CHECK(cudaMemcpyAsync(co.data(), f.conic_o.as<void>(), n * 32, cudaMemcpyDeviceToHost, s));
+            OSB_CUDA_CHECK(cudaMemcpyAsync(sp.data(), f.splat.as<void>(), n * sizeof(osb::Splat32),
+                                           cudaMemcpyDeviceToHost, s));
+            OSB_CUDA_CHECK(cudaMemcpyAsync(rc.data(), f.rect.as<void>(), n * 16, cudaMemcpyDeviceToHost, s));
+            OSB_CUDA_CHECK(cudaMemcpyAsync(tc.data(), f.touched.as<void>(), n * 4, cudaMemcpyDeviceToHost, s));
+            OSB_CUDA_CHECK(cudaStreamSynchronize(s));
+        }
+        for (size_t i = 0; i < n; ++i) {
+            const bool vis = key[i] != ~0ull;
+            if (visible) visible[i] = vis ? 1 : 0;
+            if (p) { p[2 * i] = vis ? pxy[i].x : 0.0; p[2 * i + 1] = vis ? pxy[i].y : 0.0; }
+            if (conic) {
+                conic[3 * i] = vis ? co[i].x : 0.0;
+                conic[3 * i + 1] = vis ? co[i].y : 0.0;
+                conic[3 * i + 2] = vis ? co[i].z : 0.0;
+            }
+            if (opacity) opacity[i] = vis ? co[i].w : 0.0;
+            if (color) {
+                color[3 * i] = vis ? sp[i].r : 0.0f;
+                color[3 * i + 1] = vis ? sp[i].g : 0.0f;
+                color[3 * i + 2] = vis ? sp[i].bl : 0.0f;
+            }
+            if (rect) {
+                rect[4 * i] = vis ? rc[i].x : 0;
+                rect[4 * i + 1] = vis ? rc[i].y : 0;
+                rect[4 * i + 2] = vis ? rc[i].z : 0;
+                rect[4 * i + 3] = vis ? rc[i].w : 0;
+            }
+            if (touched) touched[i] = vis ? tc[i] : 0;
+        }
+    });
+}
+
+osplat_status osplat_frame_tiles(const osplat_frame* frame, int* tiles_x, int* tiles_y, size_t* instances,
+                                 uint32_t* ranges, uint32_t* gaussian_ids) {
+    if (!frame) return invalid("osplat_frame_tiles: null frame");
+    return wrap([&] {
+        const osb::Frame& f = *frame->frame;
+        osb::DeviceGuard g(frame->engine->device());
+        cudaStream_t s = frame->engine->stream();
+        if (tiles_x) *tiles_x = f.tiles_x;
+        if (tiles_y) *tiles_y = f.tiles_y;
+        if (instances) *instances = f.M;
+        const size_t tiles = static_cast<size_t>(f.tiles_x) * f.tiles_y;
+        if (ranges) OSB_CUDA_CHECK(cudaMemcpyAsync(ranges, f.ranges.as<void>(), tiles * 8, cudaMemcpyDeviceToHost, s));
+        if (gaussian_ids && f.M)
+            OSB_CUDA_CHECK(cudaMemcpyAsync(gaussian_ids, f.inst_gid(), static_cast<size_t>(f.M) * 4,
+                                           cudaMemcpyDeviceToHost, s));
+        OSB_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+osplat_status osplat_frame_device(const osplat_frame* frame, osplat_frame_view* v) {
+    if (!frame || !v) return invalid("osplat_frame_device: null argument");
+    const osb::Frame& f = *frame->frame;
+    v->rgb = f.rgb.as<float>();
+    v->transmittance = f.T.as<float>();
+    v->contributors = f.contrib.as<int>();
+    v->last_contrib = f.last.as<int>();
+    v->width = f.W;
+    v->height = f.H;
+    t_last_error.clear();
+    return OSPLAT_OK;
+}
+
+osplat_status osplat_gpu_view_buffers(osplat_gpu* ctx, osplat_gpu_view* v) {
+    if (!ctx || !v) return invalid("osplat_gpu_view_buffers: null argument");
+    Engine& e = *ctx->engine;
+    v->params = e.params();
+    v->grads = e.grads();
+    v->adam_m = e.adam_m();
+    v->adam_v = e.adam_v();
+    v->d_screen = reinterpret_cast<float*>(e.d_screen());
+    v->screen_norm_sum = e.norm_sum();
+    v->screen_hits = e.hits();
+    v->n = e.n();
+    v->stride = e.stride();
+    v->planes = e.planes();
+    v->sh_degree = e.sh_degree();
+    v->active_sh_degree = e.active_sh_degree();
+    v->adam_step = e.adam_step_count();
+    t_last_error.clear();
+    return OSPLAT_OK;
+}
+
+static void validate_frame(osplat_gpu* ctx, const osplat_frame* frame) {
+    if (frame->engine.get() != ctx->engine.get())
+        throw ApiError(Code::StateMismatch, "frame was rendered by another context");
+    if (static_cast<size_t>(frame->frame->n) != ctx->engine->n())
+        throw ApiError(Code::StateMismatch, "render output does not match the given scene");
+}
+
+osplat_status osplat_gpu_backward(osplat_gpu* ctx, const osplat_frame* frame, const double* d_image, int accumulate) {
+    if (!ctx || !frame || !d_image) return invalid("osplat_gpu_backward: null argument");
+    return wrap([&] {
+        validate_frame(ctx, frame);
+        Engine& e = *ctx->engine;
+        osb::DeviceGuard g(e.device());
+        const osb::Frame& f = *frame->frame;
+        const size_t plane = static_cast<size_t>(f.W) * f.H;
+        std::vector<float> planar(plane * 3);
+        for (size_t i = 0; i < plane; ++i)
+            for (int c = 0; c < 3; ++c) planar[c * plane + i] = static_cast<float>(d_image[i * 3 + c]);
+        float* dev = e.d_image_buffer(plane);
+        OSB_CUDA_CHECK(cudaMemcpyAsync(dev, planar.data(), plane * 12, cudaMemcpyHostToDevice, e.stream()));
+        e.backward(&f, dev, accumulate != 0);
+        OSB_CUDA_CHECK(cudaStreamSynchronize(e.stream()));  // `planar` is pageable host memory
+    });
+}
+
+osplat_status osplat_gpu_backward_device(osplat_gpu* ctx, const osplat_frame* frame, const float* d_image_planar,
+                                         int accumulate) {
+    if (!ctx || !frame || !d_image_planar) return invalid("osplat_gpu_backward_device: null argument");
+    return wrap([&] {
+        validate_frame(ctx, frame);
+        ctx->engine->backward(frame->frame, d_image_planar, accumulate != 0);
+    });
+}
+
+osplat_status osplat_gpu_gradients(osplat_gpu* ctx, double* d_position, double* d_sh, double* d_rotation,
+                                   double* d_log_scale, double* d_opacity, double* d_screen, double* norm_sum,
+                                   long* hits) {
+    if (!ctx) return invalid("osplat_gpu_gradients: null context");
+    return wrap([&] {
+        Engine& e = *ctx->engine;
+        osb::DeviceGuard g(e.device());
+        const size_t n = e.n(), stride = e.stride();
+        const int bc = (e.sh_degree() + 1) * (e.sh_degree() + 1);
+        const osb::Planes pl{bc};
+        std::vector<float> G(static_cast<size_t>(e.planes()) * stride);
+        std::vector<float2> ds(stride);
+        std::vector<double> ns(stride);
+        std::vector<int> hs(stride);
+        cudaStream_t s = e.stream();
+        OSB_CUDA_CHECK(cudaMemcpyAsync(G.data(), e.grads(), G.size() * 4, cudaMemcpyDeviceToHost, s));
+        OSB_CUDA_CHECK(cudaMemcpyAsync(ds.data(), e.d_screen(), stride * 8, cudaMemcpyDeviceToHost, s));
+        OSB_CUDA_CHECK(cudaMemcpyAsync(ns.data(), e.norm_sum(), stride * 8, cudaMemcpyDeviceToHost, s));
+        OSB_CUDA_CHECK(cudaMemcpyAsync(hs.data(), e.hits(), stride * 4, cudaMemcpyDeviceToHost, s));
+        OSB_CUDA_CHECK(cudaStreamSynchronize(s));
+        for (size_t i = 0; i < n; ++i) {
+            for (int k = 0; k < 3; ++k)
+                if (d_position) d_position[3 * i + k] = G[k * stride + i];
+            for (int b = 0; b < bc; ++b)
+                for (int k = 0; k < 3; ++k)
+                    if (d_sh) d_sh[(i * bc + b) * 3 + k] = G[pl.sh(b, k) * stride + i];
+            for (int k = 0; k < 4; ++k)
+                if (d_rotation) d_rotation[4 * i + k] = G[pl.rot(k) * stride + i];
+            for (int k = 0; k < 3; ++k)
+                if (d_log_scale) d_log_scale[3 * i + k] = G[pl.lscale(k) * stride + i];
+            if (d_opacity) d_opacity[i] = G[pl.opacity() * stride + i];
+            if (d_screen) { d_screen[2 * i] = ds[i].x; d_screen[2 * i + 1] = ds[i].y; }
+            if (norm_sum) norm_sum[i] = ns[i];
+            if (hits) hits[i] = hs[i];
+        }
+    });
+}
+
+osplat_status osplat_gpu_zero_grad(osplat_gpu* ctx) {
+    if (!ctx) return invalid("osplat_gpu_zero_grad: null context");
+    return wrap([&] { ctx->engine->zero_grad(); });
+}
+
+osplat_status osplat_gpu_reset_screen_stats(osplat_gpu* ctx) {
+    if (!ctx) return invalid("osplat_gpu_reset_screen_stats: null context");
+    return wrap([&] { ctx->engine->reset_screen_stats(); });
+}
+
+osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_config* config, double extent, long iteration,
+                                   int zero_grad) {
+    if (!ctx) return invalid("osplat_gpu_adam_step: null context");
+    return wrap([&] { ctx->engine->adam_step(hyper_from(config), extent, iteration, zero_grad != 0); });
+}
+
+osplat_status osplat_gpu_l1_loss(osplat_gpu* ctx, const osplat_frame* frame, const float* gt, double mask,
+                                 const float** d_image, double* loss) {
+    if (!ctx || !frame || !gt) return invalid("osplat_gpu_l1_loss: null argument");
+    if (mask < 0.0 || mask >= 1.0) return invalid("osplat_gpu_l1_loss: mask_bottom_fraction must be in [0, 1)");
+    return wrap([&] {
+        validate_frame(ctx, frame);
+        Engine& e = *ctx->engine;
+        double v = e.l1_loss(frame->frame, gt, mask, loss != nullptr);
+        if (loss) *loss = v;
+        if (d_image) *d_image = e.d_image_buffer(static_cast<size_t>(frame->frame->W) * frame->frame->H);
+    });
+}
+
+osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
+                                    const float* gt, int gt_on_device, double mask, double* loss) {
+    if (!ctx || !transform_cw || !gt) return invalid("osplat_gpu_train_view: null argument");
+    if (mask < 0.0 || mask >= 1.0) return invalid("osplat_gpu_train_view: mask_bottom_fraction must be in [0, 1)");
+    return wrap([&] {
+        check_dims(width, height);
+        double p12[12];
+        checked_pose(transform_cw, p12);
+        Engine& e = *ctx->engine;
+        osb::DeviceGuard g(e.device());
+        const size_t plane = static_cast<size_t>(width) * height;
+        const float* gt_dev = gt;
+        if (!gt_on_device) {
+            float* buf = e.gt_buffer(plane);
+            OSB_CUDA_CHECK(cudaMemcpyAsync(buf, gt, plane * 12, cudaMemcpyHostToDevice, e.stream()));
+            gt_dev = buf;
+        }
+        const double zero[3] = {0, 0, 0};
+        osb::Frame* f = e.render(p12, width, height, zero);
+        try {
+            const double v = e.l1_loss(f, gt_dev, mask, false);
+            (void)v;
+            const size_t pixels = plane;
+            e.backward(f, e.d_image_buffer(pixels), true);
+            if (loss) {
+                // the L1 sum lives on the device; one 8-byte read completes the step
+                *loss = e.l1_loss_value(f, mask);
+            }
+        } catch (...) {
+            e.release(f);
+            throw;
+        }
+        e.release(f);
+    });
+}
+
+long long osplat_gpu_launch_count(void) { return osb::launches_total(); }
+
+}  // extern "C"

@@ -1,0 +1,350 @@
+// engine.cu — host orchestration of K1..K5 on one device and one CUDA stream.
+//
+// Memory layout in HBM: parameters, gradients and Adam moments are four
+// planes x stride FP32 buffers (SoA planes, stride = n rounded up to 32 -> every plane starts on
+// a 128-B line); per-frame workspaces are pooled and grow monotonically, so steady-state frames
+// allocate nothing.
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "engine.h"
+
+namespace osb {
+
+namespace {
+long long g_launches = 0;
+}
+
+void count_launches(int k) { __atomic_add_fetch(&g_launches, k, __ATOMIC_RELAXED); }
+long long launches_total() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
+DevBuf::~DevBuf() {
+    if (p_) cudaFree(p_);
+}
+
+void DevBuf::ensure(size_t bytes) {
+    if (bytes <= cap_ && p_) return;
+    if (p_) {
+        OSB_CUDA_CHECK(cudaFree(p_));
+        p_ = nullptr;
+        cap_ = 0;
+    }
+    size_t want = bytes < 256 ? 256 : bytes;
+    want = (want + 255) & ~size_t(255);
+    OSB_CUDA_CHECK(cudaMalloc(&p_, want));
+    cap_ = want;
+}
+
+DeviceGuard::DeviceGuard(int dev) {
+    OSB_CUDA_CHECK(cudaGetDevice(&prev));
+    if (prev != dev) OSB_CUDA_CHECK(cudaSetDevice(dev));
+}
+DeviceGuard::~DeviceGuard() { cudaSetDevice(prev); }
+
+PreprocessOut Frame::pp() const {
+    PreprocessOut o;
+    o.depth_key = depth_key.as<uint64_t>();
+    o.touched = touched.as<uint32_t>();
+    o.rect = rect.as<int4>();
+    o.pxy = pxy.as<double2>();
+    o.conic_o = conic_o.as<double4>();
+    o.splat = splat.as<Splat32>();
+    o.delta = delta.as<float>();
+    return o;
+}
+
+FrameBuffers Frame::fb() const {
+    FrameBuffers b;
+    b.rgb = rgb.as<float>();
+    b.T = T.as<float>();
+    b.contrib = contrib.as<int>();
+    b.last = last.as<int>();
+    return b;
+}
+
+Engine::Engine(int device, cudaStream_t stream) : device_(device), stream_(stream), own_stream_(stream == nullptr) {
+    int count = 0;
+    OSB_CUDA_CHECK(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw std::invalid_argument("no CUDA device " + std::to_string(device));
+    DeviceGuard g(device_);
+    if (own_stream_) OSB_CUDA_CHECK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    cudaStreamSynchronize(stream_);
+    pool_.clear();
+    if (own_stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::upload(const HostCloud& c) {
+    DeviceGuard g(device_);
+    if (c.sh_degree < 0 || c.sh_degree > 3) throw std::invalid_argument("sh_degree must be in 0..3");
+    n_ = c.n();
+    sh_degree_ = c.sh_degree;
+    active_ = c.active_sh_degree < 0 ? 0 : (c.active_sh_degree > c.sh_degree ? c.sh_degree : c.active_sh_degree);
+    const int bc = c.bc();
+    const Planes pl{bc};
+    planes_ = pl.count();
+    stride_ = ((n_ > 0 ? n_ : 1) + 31) & ~size_t(31);
+    const size_t elems = static_cast<size_t>(planes_) * stride_;
+    std::vector<float> host(elems, 0.0f);
+    for (size_t i = 0; i < n_; ++i) {
+        for (int k = 0; k < 3; ++k) host[k * stride_ + i] = static_cast<float>(c.positions[3 * i + k]);
+        for (int b = 0; b < bc; ++b)
+            for (int k = 0; k < 3; ++k)
+                host[pl.sh(b, k) * stride_ + i] = static_cast<float>(c.sh[(i * bc + b) * 3 + k]);
+        for (int k = 0; k < 4; ++k) host[pl.rot(k) * stride_ + i] = static_cast<float>(c.rotations[4 * i + k]);
+        for (int k = 0; k < 3; ++k) host[pl.lscale(k) * stride_ + i] = static_cast<float>(c.log_scales[3 * i + k]);
+        host[pl.opacity() * stride_ + i] = static_cast<float>(c.opacity[i]);
+    }
+    params_.ensure(elems * 4);
+    grads_.ensure(elems * 4);
+    m_.ensure(elems * 4);
+    v_.ensure(elems * 4);
+    acc_.ensure(stride_ * 48);
+    d_screen_.ensure(stride_ * 8);
+    norm_sum_.ensure(stride_ * 8);
+    hits_.ensure(stride_ * 4);
+    loss_sum_.ensure(64);
+    OSB_CUDA_CHECK(cudaMemcpyAsync(params_.as<float>(), host.data(), elems * 4, cudaMemcpyHostToDevice, stream_));
+    OSB_CUDA_CHECK(cudaMemsetAsync(grads_.as<float>(), 0, elems * 4, stream_));
+    OSB_CUDA_CHECK(cudaMemsetAsync(m_.as<float>(), 0, elems * 4, stream_));
+    OSB_CUDA_CHECK(cudaMemsetAsync(v_.as<float>(), 0, elems * 4, stream_));
+    OSB_CUDA_CHECK(cudaMemsetAsync(d_screen_.as<float>(), 0, stride_ * 8, stream_));
+    OSB_CUDA_CHECK(cudaMemsetAsync(norm_sum_.as<double>(), 0, stride_ * 8, stream_));
+    OSB_CUDA_CHECK(cudaMemsetAsync(hits_.as<int>(), 0, stride_ * 4, stream_));
+    adam_step_ = 0;
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+HostCloud Engine::download() {
+    DeviceGuard g(device_);
+    HostCloud c;
+    c.sh_degree = sh_degree_;
+    c.active_sh_degree = active_;
+    const int bc = c.bc();
+    const Planes pl{bc};
+    const size_t elems = static_cast<size_t>(planes_) * stride_;
+    std::vector<float> host(elems);
+    OSB_CUDA_CHECK(cudaMemcpyAsync(host.data(), params_.as<float>(), elems * 4, cudaMemcpyDeviceToHost, stream_));
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    c.positions.resize(n_ * 3);
+    c.sh.resize(n_ * bc * 3);
+    c.rotations.resize(n_ * 4);
+    c.log_scales.resize(n_ * 3);
+    c.opacity.resize(n_);
+    for (size_t i = 0; i < n_; ++i) {
+        for (int k = 0; k < 3; ++k) c.positions[3 * i + k] = host[k * stride_ + i];
+        for (int b = 0; b < bc; ++b)
+            for (int k = 0; k < 3; ++k) c.sh[(i * bc + b) * 3 + k] = host[pl.sh(b, k) * stride_ + i];
+        for (int k = 0; k < 4; ++k) c.rotations[4 * i + k] = host[pl.rot(k) * stride_ + i];
+        for (int k = 0; k < 3; ++k) c.log_scales[3 * i + k] = host[pl.lscale(k) * stride_ + i];
+        c.opacity[i] = host[pl.opacity() * stride_ + i];
+    }
+    return c;
+}
+
+void Engine::set_active_sh_degree(int d) {
+    if (d < 0 || d > sh_degree_) throw std::invalid_argument("active_sh_degree out of range");
+    active_ = d;
+}
+
+static int bits_for(uint64_t v) {
+    int b = 0;
+    while (b < 64 && (1ull << b) < v) ++b;
+    return b;
+}
+
+Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3]) {
+    DeviceGuard g(device_);
+    Frame* f;
+    if (!free_.empty()) {
+        f = free_.back();
+        free_.pop_back();
+    } else {
+        pool_.emplace_back(new Frame());
+        f = pool_.back().get();
+    }
+    try {
+        f->W = W;
+        f->H = H;
+        f->tiles_x = (W + kTile - 1) / kTile;
+        f->tiles_y = (H + kTile - 1) / kTile;
+        f->n = static_cast<int>(n_);
+        f->active_degree = active_;
+        std::memcpy(f->pose12, pose12, sizeof(double) * 12);
+        for (int i = 0; i < 9; ++i) f->pose.R[i] = pose12[i];
+        for (int i = 0; i < 3; ++i) f->pose.t[i] = pose12[9 + i];
+        for (int i = 0; i < 3; ++i) f->bg[i] = static_cast<float>(bg ? bg[i] : 0.0);
+        const size_t n = n_ > 0 ? n_ : 1;
+        const size_t pixels = static_cast<size_t>(W) * H;
+        const int tiles = f->tiles_x * f->tiles_y;
+        f->depth_key.ensure(n * 8);
+        f->touched.ensure(n * 4);
+        f->rect.ensure(n * 16);
+        f->pxy.ensure(n * 16);
+        f->conic_o.ensure(n * 32);
+        f->splat.ensure(n * sizeof(Splat32));
+        f->delta.ensure(n * 4);
+        for (int k = 0; k < 2; ++k) {
+            f->okeys[k].ensure(n * 8);
+            f->ovals[k].ensure(n * 4);
+        }
+        f->offsets.ensure(n * 4);
+        f->total.ensure(16);
+        f->ranges.ensure(static_cast<size_t>(tiles) * 8);
+        f->rgb.ensure(pixels * 12);
+        f->T.ensure(pixels * 4);
+        f->contrib.ensure(pixels * 4);
+        f->last.ensure(pixels * 4);
+        f->scan_ws.ensure(scan_workspace_bytes(static_cast<int>(n)));
+
+        const PreprocessOut pp = f->pp();
+        const int N = static_cast<int>(n_);
+        // K1
+        launch_preprocess(params_.as<float>(), N, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
+                          active_, f->pose, W, H, pp, stream_);
+        // K2a: depth rank (stable by id)
+        f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(n), 8));
+        OSB_CUDA_CHECK(cudaMemcpyAsync(f->okeys[0].as<uint64_t>(), pp.depth_key, n_ * 8, cudaMemcpyDeviceToDevice,
+                                       stream_));
+        launch_iota(f->ovals[0].as<uint32_t>(), N, stream_);
+        const bool flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(),
+                                            f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N, 64,
+                                            f->sort_ws.as<void>(), stream_);
+        const uint32_t* order = f->ovals[flipped ? 1 : 0].as<uint32_t>();
+        // K2b: instance offsets in depth order
+        launch_gather_scan(pp.touched, order, f->offsets.as<uint32_t>(), f->total.as<uint32_t>(), N,
+                           f->scan_ws.as<void>(), stream_);
+        uint32_t M = 0;
+        OSB_CUDA_CHECK(cudaMemcpyAsync(&M, f->total.as<uint32_t>(), 4, cudaMemcpyDeviceToHost, stream_));
+        OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+        if (N == 0) M = 0;
+        f->M = M;
+        const size_t m = M > 0 ? M : 1;
+        for (int k = 0; k < 2; ++k) {
+            f->ikeys[k].ensure(m * 4);
+            f->ivals[k].ensure(m * 4);
+        }
+        // K2c: emit (tile, gid) in depth order, stable sort by tile, ranges
+        launch_emit(order, f->offsets.as<uint32_t>(), pp.touched, pp.rect, N, f->tiles_x, f->ikeys[0].as<uint32_t>(),
+                    f->ivals[0].as<uint32_t>(), stream_);
+        f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(m), 4));
+        f->inst_in_alt = radix_sort_u32(f->ikeys[0].as<uint32_t>(), f->ikeys[1].as<uint32_t>(),
+                                        f->ivals[0].as<uint32_t>(), f->ivals[1].as<uint32_t>(),
+                                        static_cast<int>(M), bits_for(static_cast<uint64_t>(tiles)),
+                                        f->sort_ws.as<void>(), stream_);
+        OSB_CUDA_CHECK(cudaMemsetAsync(f->ranges.as<uint2>(), 0, static_cast<size_t>(tiles) * 8, stream_));
+        launch_ranges(f->ikeys[f->inst_in_alt ? 1 : 0].as<uint32_t>(), static_cast<int>(M), f->ranges.as<uint2>(),
+                      stream_);
+        // K3
+        launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(), stream_);
+    } catch (...) {
+        free_.push_back(f);
+        throw;
+    }
+    return f;
+}
+
+void Engine::release(Frame* f) {
+    if (f) free_.push_back(f);
+}
+
+void Engine::backward(const Frame* f, const float* d_image, bool accumulate) {
+    DeviceGuard g(device_);
+    if (static_cast<size_t>(f->n) != n_) throw std::logic_error("StateMismatch: render output does not match the cloud");
+    const size_t elems = static_cast<size_t>(planes_) * stride_;
+    if (!accumulate) OSB_CUDA_CHECK(cudaMemsetAsync(grads_.as<float>(), 0, elems * 4, stream_));
+    OSB_CUDA_CHECK(cudaMemsetAsync(acc_.as<float4>(), 0, stride_ * 48, stream_));
+    const PreprocessOut pp = f->pp();
+    launch_backward_pixels(f->inst_gid(), f->ranges.as<uint2>(), pp, f->W, f->H, f->tiles_x, f->tiles_y, f->bg,
+                           f->fb(), d_image, acc_.as<float4>(), stream_);
+    ScreenStats st{d_screen_.as<float2>(), norm_sum_.as<double>(), hits_.as<int>()};
+    if (!accumulate) OSB_CUDA_CHECK(cudaMemsetAsync(d_screen_.as<float2>(), 0, stride_ * 8, stream_));
+    launch_backward_gaussians(params_.as<float>(), f->n, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
+                              f->active_degree, f->pose, f->W, f->H, pp.depth_key, acc_.as<float4>(), grads_.as<float>(),
+                              st, stream_);
+}
+
+float* Engine::d_image_buffer(size_t pixels) {
+    d_image_.ensure(pixels * 12);
+    return d_image_.as<float>();
+}
+
+float* Engine::gt_buffer(size_t pixels) {
+    gt_.ensure(pixels * 12);
+    return gt_.as<float>();
+}
+
+double Engine::l1_loss(const Frame* f, const float* gt, double mask_bottom_fraction, bool want_value) {
+    DeviceGuard g(device_);
+    const size_t pixels = static_cast<size_t>(f->W) * f->H;
+    float* dimg = d_image_buffer(pixels);
+    const int masked = static_cast<int>(std::floor(mask_bottom_fraction * f->H));
+    const int keep = f->H - masked;
+    const double n = static_cast<double>(f->W) * keep * 3.0;
+    OSB_CUDA_CHECK(cudaMemsetAsync(loss_sum_.as<double>(), 0, 8, stream_));
+    launch_l1_loss(f->fb().rgb, gt, f->W, f->H, keep, 1.0 / n, dimg, loss_sum_.as<double>(), stream_);
+    if (!want_value) return 0.0;
+    return l1_loss_value(f, mask_bottom_fraction);
+}
+
+double Engine::l1_loss_value(const Frame* f, double mask_bottom_fraction) {
+    DeviceGuard g(device_);
+    const int masked = static_cast<int>(std::floor(mask_bottom_fraction * f->H));
+    const double n = static_cast<double>(f->W) * (f->H - masked) * 3.0;
+    double s = 0.0;
+    OSB_CUDA_CHECK(cudaMemcpyAsync(&s, loss_sum_.as<double>(), 8, cudaMemcpyDeviceToHost, stream_));
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    return s / n;
+}
+
+void Engine::adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad) {
+    DeviceGuard g(device_);
+    adam_step_ += 1;
+    const double bias1 = 1.0 - std::pow(0.9, static_cast<double>(adam_step_));
+    const double bias2 = 1.0 - std::pow(0.999, static_cast<double>(adam_step_));
+    double t = 1.0;
+    if (h.iterations > 0) {
+        t = static_cast<double>(iteration) / h.iterations;
+        t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+    }
+    const double lr_pos = std::exp((1.0 - t) * std::log(h.lr_position_init * extent) +
+                                   t * std::log(h.lr_position_final * extent));
+    AdamArgs a;
+    const int bc = (sh_degree_ + 1) * (sh_degree_ + 1);
+    const Planes pl{bc};
+    for (int i = 0; i < 64; ++i) a.lr_plane[i] = 0.0f;
+    for (int k = 0; k < 3; ++k) a.lr_plane[k] = static_cast<float>(lr_pos);
+    for (int b = 0; b < bc; ++b)
+        for (int k = 0; k < 3; ++k) a.lr_plane[pl.sh(b, k)] = static_cast<float>(b == 0 ? h.lr_sh_dc : h.lr_sh_rest);
+    for (int k = 0; k < 4; ++k) a.lr_plane[pl.rot(k)] = static_cast<float>(h.lr_rotation);
+    for (int k = 0; k < 3; ++k) a.lr_plane[pl.lscale(k)] = static_cast<float>(h.lr_scale);
+    a.lr_plane[pl.opacity()] = static_cast<float>(h.lr_opacity);
+    a.inv_bias1 = static_cast<float>(1.0 / bias1);
+    a.inv_bias2 = static_cast<float>(1.0 / bias2);
+    a.planes = planes_;
+    a.stride = static_cast<int>(stride_);
+    a.zero_grad = zero_grad ? 1 : 0;
+    launch_adam(params_.as<float>(), grads_.as<float>(), m_.as<float>(), v_.as<float>(), a, stream_);
+}
+
+void Engine::zero_grad() {
+    DeviceGuard g(device_);
+    OSB_CUDA_CHECK(cudaMemsetAsync(grads_.as<float>(), 0, static_cast<size_t>(planes_) * stride_ * 4, stream_));
+}
+
+void Engine::reset_screen_stats() {
+    DeviceGuard g(device_);
+    OSB_CUDA_CHECK(cudaMemsetAsync(norm_sum_.as<double>(), 0, stride_ * 8, stream_));
+    OSB_CUDA_CHECK(cudaMemsetAsync(hits_.as<int>(), 0, stride_ * 4, stream_));
+}
+
+void Engine::synchronize() {
+    DeviceGuard g(device_);
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+}  // namespace osb

@@ -1,0 +1,128 @@
+// engine.h — device context (parameters, gradients, Adam state) and frame workspaces.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <vector>
+
+#include "kernels.h"
+
+namespace osb {
+
+// Host mirror of the reference GaussianCloud (proj/include/omnisplat/scene.hpp:31-55).
+struct HostCloud {
+    int sh_degree = 3;
+    int active_sh_degree = 0;
+    std::vector<double> positions, sh, rotations, log_scales, opacity;
+    size_t n() const { return positions.size() / 3; }
+    int bc() const { return (sh_degree + 1) * (sh_degree + 1); }
+};
+
+// Growable device allocation (never shrinks; reused across frames).
+class DevBuf {
+public:
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf();
+    void ensure(size_t bytes);
+    template <typename T>
+    T* as() const { return static_cast<T*>(p_); }
+    size_t capacity() const { return cap_; }
+
+private:
+    void* p_ = nullptr;
+    size_t cap_ = 0;
+};
+
+// Hyper-parameters adam_step reads (trainer.hpp:19-51 TrainConfig subset) + loss settings.
+struct TrainHyper {
+    long iterations = 7000;
+    double lr_position_init = 1.6e-4, lr_position_final = 1.6e-6;
+    double lr_sh_dc = 2.5e-3, lr_sh_rest = 2.5e-3 / 20.0;
+    double lr_opacity = 5e-2, lr_scale = 5e-3, lr_rotation = 1e-3;
+};
+
+struct Frame {
+    int W = 0, H = 0, tiles_x = 0, tiles_y = 0, n = 0, active_degree = 0;
+    uint32_t M = 0;
+    double pose12[12];
+    Pose pose;
+    float bg[3] = {0, 0, 0};
+    bool inst_in_alt = false;  // sorted instance gids live in inst_vals[1]
+    // per Gaussian (K1 outputs)
+    DevBuf depth_key, touched, rect, pxy, conic_o, splat, delta;
+    // depth sort
+    DevBuf okeys[2], ovals[2], offsets, total;
+    // instances
+    DevBuf ikeys[2], ivals[2], ranges;
+    // pixels
+    DevBuf rgb, T, contrib, last;
+    DevBuf sort_ws, scan_ws;
+    const uint32_t* inst_gid() const { return ivals[inst_in_alt ? 1 : 0].as<uint32_t>(); }
+    PreprocessOut pp() const;
+    FrameBuffers fb() const;
+};
+
+class Engine {
+public:
+    Engine(int device, cudaStream_t stream);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    void upload(const HostCloud& cloud);
+    HostCloud download();
+    void set_active_sh_degree(int d);
+
+    Frame* render(const double pose12[12], int W, int H, const double bg[3]);
+    void release(Frame* f);
+    void backward(const Frame* f, const float* d_image_planar_dev, bool accumulate);
+    double l1_loss(const Frame* f, const float* gt_planar_dev, double mask_bottom_fraction, bool want_value);
+    // Reads back the value of the last l1_loss() launch (synchronizes the stream).
+    double l1_loss_value(const Frame* f, double mask_bottom_fraction);
+    void adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad);
+    void zero_grad();
+    void reset_screen_stats();
+    void synchronize();
+
+    // accessors
+    cudaStream_t stream() const { return stream_; }
+    int device() const { return device_; }
+    size_t n() const { return n_; }
+    size_t stride() const { return stride_; }
+    int planes() const { return planes_; }
+    int sh_degree() const { return sh_degree_; }
+    int active_sh_degree() const { return active_; }
+    long adam_step_count() const { return adam_step_; }
+    float* params() const { return params_.as<float>(); }
+    float* grads() const { return grads_.as<float>(); }
+    float* adam_m() const { return m_.as<float>(); }
+    float* adam_v() const { return v_.as<float>(); }
+    float2* d_screen() const { return d_screen_.as<float2>(); }
+    double* norm_sum() const { return norm_sum_.as<double>(); }
+    int* hits() const { return hits_.as<int>(); }
+    float* d_image_buffer(size_t pixels);
+    float* gt_buffer(size_t pixels);
+
+private:
+    int device_;
+    cudaStream_t stream_;
+    bool own_stream_;
+    size_t n_ = 0, stride_ = 0;
+    int planes_ = 0, sh_degree_ = 0, active_ = 0;
+    long adam_step_ = 0;
+    DevBuf params_, grads_, m_, v_, acc_, d_screen_, norm_sum_, hits_, loss_sum_, d_image_, gt_;
+    std::vector<std::unique_ptr<Frame>> pool_;
+    std::vector<Frame*> free_;
+};
+
+// RAII device guard.
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev);
+    ~DeviceGuard();
+};
+
+}  // namespace osb

@@ -1,0 +1,104 @@
+// kernels.h — host-side launchers for the sm_100a kernels (one TU per kernel family).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace osb {
+
+// Kernel launches issued by this library (reported by bench.py as gpu_launches).
+void count_launches(int k);
+long long launches_total();
+
+// ---- K1 preprocess (preprocess.cu) --------------------------------------------------------
+struct PreprocessOut {
+    uint64_t* depth_key;   // N: bit pattern of t_r (monotone), ~0 when culled
+    uint32_t* touched;     // N: tile instances this Gaussian emits
+    int4* rect;            // N: {tx0, tx1, ty0, ty1} (tx may wrap)
+    double2* pxy;          // N: FP64 pixel centre
+    double4* conic_o;      // N: FP64 conic a, b, c and opacity
+    Splat32* splat;        // N: FP32 blend record
+    float* delta;          // N: FP32 power guard band
+};
+void launch_preprocess(const float* params, int n, int stride, int bc, int active_degree, const Pose& pose,
+                       int W, int H, const PreprocessOut& out, cudaStream_t s);
+
+// ---- K2 duplicate + sort (sort.cu) ----------------------------------------------------------
+struct SortWorkspace;  // opaque, owned by the context
+size_t radix_workspace_bytes(int n_max, int key_bytes);
+// Stable LSD radix sort of (key, value) pairs on bits [0, bits). keys/vals are double-buffered:
+// the result ends up in *_out when the function returns true, in *_in otherwise.
+bool radix_sort_u64(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
+                    int bits, void* ws, cudaStream_t s);
+bool radix_sort_u32(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
+                    int bits, void* ws, cudaStream_t s);
+void launch_iota(uint32_t* v, int n, cudaStream_t s);
+// offsets[r] = exclusive scan of touched[order[r]]; *total = sum (device).
+size_t scan_workspace_bytes(int n);
+void launch_gather_scan(const uint32_t* touched, const uint32_t* order, uint32_t* offsets, uint32_t* total,
+                        int n, void* ws, cudaStream_t s);
+void launch_emit(const uint32_t* order, const uint32_t* offsets, const uint32_t* touched, const int4* rect,
+                 int n, int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s);
+
+// ---- K3 blend (blend.cu) --------------------------------------------------------------------
+struct FrameBuffers {
+    float* rgb;        // 3 planes of H*W
+    float* T;          // H*W
+    int* contrib;      // H*W
+    int* last;         // H*W
+};
+void launch_blend(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H,
+                  int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s);
+
+// ---- K4 backward (backward.cu) --------------------------------------------------------------
+void launch_backward_pixels(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W,
+                            int H, int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb,
+                            const float* d_image, float4* acc, cudaStream_t s);
+struct ScreenStats {
+    float2* d_screen;       // N (latest view, overwritten for visible Gaussians)
+    double* norm_sum;       // N (accumulated)
+    int* hits;              // N (accumulated)
+};
+void launch_backward_gaussians(const float* params, int n, int stride, int bc, int active_degree,
+                               const Pose& pose, int W, int H, const uint64_t* depth_key, const float4* acc,
+                               float* grads, const ScreenStats& st, cudaStream_t s);
+
+// ---- K5 Adam + loss (adam.cu) ---------------------------------------------------------------
+struct AdamArgs {
+    float lr_plane[64];  // learning rate per plane (planes <= 59)
+    float inv_bias1, inv_bias2;
+    int planes, stride;
+    int zero_grad;
+};
+void launch_adam(float* params, float* grads, float* m, float* v, const AdamArgs& a, cudaStream_t s);
+// L1 part of loss() (trainer.cpp:25-71) on planar FP32 images; writes d_image planes and
+// atomically accumulates sum|d| (FP64) into *abs_sum.
+void launch_l1_loss(const float* rgb, const float* gt, int W, int H, int keep_rows, double scale,
+                    float* d_image, double* abs_sum, cudaStream_t s);
+
+}  // namespace osb
+
+#define OSB_CUDA_CHECK(expr)                                                                    \
+    do {                                                                                        \
+        cudaError_t err__ = (expr);                                                             \
+        if (err__ != cudaSuccess) throw ::osb::CudaError(err__, #expr, __FILE__, __LINE__);    \
+    } while (0)
+
+#define OSB_LAUNCHED(k)                          \
+    do {                                         \
+        OSB_CUDA_CHECK(cudaGetLastError());      \
+        ::osb::count_launches(k);                \
+    } while (0)
+
+#include <stdexcept>
+#include <string>
+namespace osb {
+struct CudaError : std::runtime_error {
+    CudaError(cudaError_t e, const char* expr, const char* file, int line)
+        : std::runtime_error(std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+                             ") at " + file + ":" + std::to_string(line) + ": " + expr) {}
+};
+}  // namespace osb

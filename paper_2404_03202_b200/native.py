@@ -1,0 +1,368 @@
+"""ctypes binding of the product library ``libosplat_b200.so`` (include/osplat.h).
+
+This module is the Python-side mirror of the reference interface for the hot path:
+
+* ``render(cloud, pose, W, H)``         -> proj/include/omnisplat/rasterizer.hpp:85-86
+* ``Context.backward(frame, d_image)``  -> proj/include/omnisplat/gradients.hpp:43-44
+* ``Context.adam_step(cfg, extent, it)``-> proj/include/omnisplat/trainer.hpp:80-81
+* ``osplat_render`` / ``osplat_cloud_*`` reference C ABI (proj/include/omnisplat/capi.h)
+
+There is no fallback: if the shared library is missing the import fails, and every call that
+reaches a CUDA error raises :class:`OsplatError`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .scenes import Cloud
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libosplat_b200.so")
+
+OK, INVALID_ARGUMENT, IO, PARSE, VALIDATION, UNSUPPORTED, RUNTIME = range(7)
+STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "IO", 3: "PARSE", 4: "VALIDATION", 5: "UNSUPPORTED",
+                6: "RUNTIME"}
+
+
+class OsplatError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"osplat status {STATUS_NAMES.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+_dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
+_ip = C.POINTER(C.c_int)
+_u8p = C.POINTER(C.c_uint8)
+_i32p = C.POINTER(C.c_int32)
+_u32p = C.POINTER(C.c_uint32)
+_lp = C.POINTER(C.c_long)
+_vp = C.c_void_p
+
+
+class FrameView(C.Structure):
+    _fields_ = [("rgb", _vp), ("transmittance", _vp), ("contributors", _vp), ("last_contrib", _vp),
+                ("width", C.c_int), ("height", C.c_int)]
+
+
+class GpuView(C.Structure):
+    _fields_ = [("params", _vp), ("grads", _vp), ("adam_m", _vp), ("adam_v", _vp), ("d_screen", _vp),
+                ("screen_norm_sum", _vp), ("screen_hits", _vp), ("n", C.c_size_t), ("stride", C.c_size_t),
+                ("planes", C.c_int), ("sh_degree", C.c_int), ("active_sh_degree", C.c_int),
+                ("adam_step", C.c_long)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() (make -C paper_2404_03202_b200)")
+    lib = C.CDLL(LIB_PATH)
+    S = C.c_int  # osplat_status
+    sig = {
+        "osplat_version": (C.c_char_p, []),
+        "osplat_last_error": (C.c_char_p, []),
+        "osplat_set_threads": (None, [C.c_int]),
+        "osplat_cloud_load": (S, [C.c_char_p, C.POINTER(_vp)]),
+        "osplat_cloud_save": (S, [_vp, C.c_char_p]),
+        "osplat_cloud_count": (C.c_size_t, [_vp]),
+        "osplat_cloud_free": (None, [_vp]),
+        "osplat_config_create": (S, [C.POINTER(_vp)]),
+        "osplat_config_set": (S, [_vp, C.c_char_p, C.c_char_p]),
+        "osplat_config_free": (None, [_vp]),
+        "osplat_render": (S, [_vp, _dp, C.c_int, C.c_int, C.POINTER(_vp)]),
+        "osplat_image_width": (C.c_int, [_vp]),
+        "osplat_image_height": (C.c_int, [_vp]),
+        "osplat_image_pixels": (_dp, [_vp]),
+        "osplat_image_free": (None, [_vp]),
+        "osplat_cloud_create": (S, [C.c_size_t, C.c_int, C.c_int, _dp, _dp, _dp, _dp, _dp, C.POINTER(_vp)]),
+        "osplat_cloud_read": (S, [_vp, _dp, _dp, _dp, _dp, _dp, _ip, _ip]),
+        "osplat_gpu_create": (S, [C.c_int, _vp, _vp, C.POINTER(_vp)]),
+        "osplat_gpu_free": (None, [_vp]),
+        "osplat_gpu_count": (C.c_size_t, [_vp]),
+        "osplat_gpu_set_active_sh_degree": (S, [_vp, C.c_int]),
+        "osplat_gpu_download": (S, [_vp, C.POINTER(_vp)]),
+        "osplat_gpu_synchronize": (S, [_vp]),
+        "osplat_gpu_render": (S, [_vp, _dp, C.c_int, C.c_int, _dp, C.POINTER(_vp)]),
+        "osplat_frame_free": (None, [_vp]),
+        "osplat_frame_width": (C.c_int, [_vp]),
+        "osplat_frame_height": (C.c_int, [_vp]),
+        "osplat_frame_image": (S, [_vp, _dp]),
+        "osplat_frame_pixels": (S, [_vp, _fp, _fp, _ip, _ip]),
+        "osplat_frame_projections": (S, [_vp, _u8p, _dp, _dp, _dp, _fp, _i32p, _u32p]),
+        "osplat_frame_tiles": (S, [_vp, _ip, _ip, C.POINTER(C.c_size_t), _u32p, _u32p]),
+        "osplat_frame_device": (S, [_vp, C.POINTER(FrameView)]),
+        "osplat_gpu_view_buffers": (S, [_vp, C.POINTER(GpuView)]),
+        "osplat_gpu_backward": (S, [_vp, _vp, _dp, C.c_int]),
+        "osplat_gpu_backward_device": (S, [_vp, _vp, _vp, C.c_int]),
+        "osplat_gpu_gradients": (S, [_vp, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _lp]),
+        "osplat_gpu_zero_grad": (S, [_vp]),
+        "osplat_gpu_reset_screen_stats": (S, [_vp]),
+        "osplat_gpu_adam_step": (S, [_vp, _vp, C.c_double, C.c_long, C.c_int]),
+        "osplat_gpu_l1_loss": (S, [_vp, _vp, _vp, C.c_double, C.POINTER(_vp), _dp]),
+        "osplat_gpu_train_view": (S, [_vp, _dp, C.c_int, C.c_int, _vp, C.c_int, C.c_double, _dp]),
+        "osplat_gpu_launch_count": (C.c_longlong, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+lib = _load()
+EXPORTED = ("osplat_version osplat_last_error osplat_set_threads osplat_cloud_load osplat_cloud_save "
+            "osplat_cloud_count osplat_cloud_free osplat_config_create osplat_config_set osplat_config_free "
+            "osplat_render osplat_image_width osplat_image_height osplat_image_pixels osplat_image_free").split()
+
+
+def check(status: int):
+    if status != OK:
+        raise OsplatError(status, lib.osplat_last_error().decode())
+
+
+def _p(a, t=_dp):
+    return a.ctypes.data_as(t)
+
+
+def version() -> str:
+    return lib.osplat_version().decode()
+
+
+def launch_count() -> int:
+    return int(lib.osplat_gpu_launch_count())
+
+
+def transform_of(pose12: np.ndarray) -> np.ndarray:
+    """12-double pose (R row-major, t) -> row-major 4x4 world->camera (capi.cpp:88-95)."""
+    t = np.eye(4)
+    t[:3, :3] = np.asarray(pose12[:9], dtype=np.float64).reshape(3, 3)
+    t[:3, 3] = pose12[9:12]
+    return np.ascontiguousarray(t)
+
+
+# --------------------------------------------------------------------------- host handles
+
+class HostCloud:
+    """Owning wrapper of an ``osplat_cloud`` handle (reference GaussianCloud on the host)."""
+
+    def __init__(self, handle):
+        self.handle = handle
+
+    @staticmethod
+    def from_cloud(cloud: Cloud) -> "HostCloud":
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                (cloud.positions, cloud.sh, cloud.rotations, cloud.log_scales, cloud.opacity_logits)]
+        h = _vp()
+        check(lib.osplat_cloud_create(cloud.n, cloud.sh_degree, cloud.active_sh_degree,
+                                      *[_p(a) for a in arrs], C.byref(h)))
+        return HostCloud(h)
+
+    @staticmethod
+    def load(path: str) -> "HostCloud":
+        h = _vp()
+        check(lib.osplat_cloud_load(path.encode(), C.byref(h)))
+        return HostCloud(h)
+
+    def save(self, path: str):
+        check(lib.osplat_cloud_save(self.handle, path.encode()))
+
+    def __len__(self):
+        return int(lib.osplat_cloud_count(self.handle))
+
+    def to_cloud(self) -> Cloud:
+        deg, act = C.c_int(0), C.c_int(0)
+        check(lib.osplat_cloud_read(self.handle, None, None, None, None, None, C.byref(deg), C.byref(act)))
+        n = len(self)
+        bc = (deg.value + 1) ** 2
+        pos, sh, rot = np.zeros((n, 3)), np.zeros((n, bc, 3)), np.zeros((n, 4))
+        ls, op = np.zeros((n, 3)), np.zeros(n)
+        check(lib.osplat_cloud_read(self.handle, _p(pos), _p(sh), _p(rot), _p(ls), _p(op), None, None))
+        return Cloud(pos, sh, rot, ls, op, deg.value, act.value)
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib.osplat_cloud_free(self.handle)
+            self.handle = None
+
+
+def osplat_render(cloud: HostCloud, pose12, width: int, height: int) -> np.ndarray:
+    """The reference drop-in entry point (capi.h:73-74): host cloud in, H x W x 3 double out."""
+    t = transform_of(pose12)
+    img = _vp()
+    check(lib.osplat_render(cloud.handle, _p(t), width, height, C.byref(img)))
+    try:
+        w, h = lib.osplat_image_width(img), lib.osplat_image_height(img)
+        px = lib.osplat_image_pixels(img)
+        return np.ctypeslib.as_array(px, shape=(h, w, 3)).copy()
+    finally:
+        lib.osplat_image_free(img)
+
+
+class Config:
+    """``osplat_config`` (TrainConfig) with string setters (dataio.cpp:570-605)."""
+
+    def __init__(self, **fields):
+        self.handle = _vp()
+        check(lib.osplat_config_create(C.byref(self.handle)))
+        for k, v in fields.items():
+            self.set(k, v)
+
+    def set(self, key: str, value):
+        check(lib.osplat_config_set(self.handle, key.encode(), str(value).encode()))
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            lib.osplat_config_free(self.handle)
+            self.handle = None
+
+
+# --------------------------------------------------------------------------- device context
+
+class Frame:
+    """Retained forward state of one render (the reference RenderOutput)."""
+
+    def __init__(self, ctx: "Context", handle):
+        self.ctx = ctx
+        self.handle = handle
+        self.width = lib.osplat_frame_width(handle)
+        self.height = lib.osplat_frame_height(handle)
+
+    def image(self) -> np.ndarray:
+        out = np.zeros((self.height, self.width, 3))
+        check(lib.osplat_frame_image(self.handle, _p(out)))
+        return out
+
+    def pixels(self):
+        H, W = self.height, self.width
+        rgb = np.zeros((H, W, 3), dtype=np.float32)
+        T = np.zeros((H, W), dtype=np.float32)
+        con = np.zeros((H, W), dtype=np.int32)
+        last = np.zeros((H, W), dtype=np.int32)
+        check(lib.osplat_frame_pixels(self.handle, _p(rgb, _fp), _p(T, _fp), _p(con, _ip), _p(last, _ip)))
+        return rgb, T, con, last
+
+    def projections(self):
+        n = self.ctx.n
+        vis = np.zeros(n, dtype=np.uint8)
+        p, conic, op = np.zeros((n, 2)), np.zeros((n, 3)), np.zeros(n)
+        col = np.zeros((n, 3), dtype=np.float32)
+        rect = np.zeros((n, 4), dtype=np.int32)
+        touched = np.zeros(n, dtype=np.uint32)
+        check(lib.osplat_frame_projections(self.handle, _p(vis, _u8p), _p(p), _p(conic), _p(op), _p(col, _fp),
+                                           _p(rect, _i32p), _p(touched, _u32p)))
+        return dict(visible=vis.astype(bool), p=p, conic=conic, opacity=op, color=col, rect=rect,
+                    touched=touched)
+
+    def tiles(self):
+        tx, ty, m = C.c_int(0), C.c_int(0), C.c_size_t(0)
+        check(lib.osplat_frame_tiles(self.handle, C.byref(tx), C.byref(ty), C.byref(m), None, None))
+        ranges = np.zeros((tx.value * ty.value, 2), dtype=np.uint32)
+        ids = np.zeros(max(m.value, 1), dtype=np.uint32)
+        check(lib.osplat_frame_tiles(self.handle, None, None, None, _p(ranges, _u32p), _p(ids, _u32p)))
+        return tx.value, ty.value, ranges, ids[:m.value]
+
+    def device(self) -> FrameView:
+        v = FrameView()
+        check(lib.osplat_frame_device(self.handle, C.byref(v)))
+        return v
+
+    def free(self):
+        if self.handle:
+            lib.osplat_frame_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.free()
+
+
+class Context:
+    """``osplat_gpu``: device-resident parameters, gradients and Adam state on one GPU."""
+
+    def __init__(self, cloud: Cloud | HostCloud, device: int = 0, stream: int | None = None):
+        hc = cloud if isinstance(cloud, HostCloud) else HostCloud.from_cloud(cloud)
+        self.handle = _vp()
+        check(lib.osplat_gpu_create(device, C.c_void_p(stream) if stream else None, hc.handle,
+                                    C.byref(self.handle)))
+        self.device = device
+        v = self.view()
+        self.n, self.stride, self.planes, self.sh_degree = v.n, v.stride, v.planes, v.sh_degree
+        self.basis_count = (v.sh_degree + 1) ** 2
+
+    def view(self) -> GpuView:
+        v = GpuView()
+        check(lib.osplat_gpu_view_buffers(self.handle, C.byref(v)))
+        return v
+
+    def set_active_sh_degree(self, d: int):
+        check(lib.osplat_gpu_set_active_sh_degree(self.handle, d))
+
+    def render(self, pose12, width: int, height: int, background=(0.0, 0.0, 0.0)) -> Frame:
+        t = transform_of(pose12)
+        bg = np.ascontiguousarray(background, dtype=np.float64)
+        h = _vp()
+        check(lib.osplat_gpu_render(self.handle, _p(t), width, height, _p(bg), C.byref(h)))
+        return Frame(self, h)
+
+    def backward(self, frame: Frame, d_image: np.ndarray, accumulate: bool = False):
+        d = np.ascontiguousarray(d_image, dtype=np.float64)
+        assert d.shape == (frame.height, frame.width, 3)
+        check(lib.osplat_gpu_backward(self.handle, frame.handle, _p(d), int(accumulate)))
+
+    def backward_device(self, frame: Frame, d_image_ptr: int, accumulate: bool = False):
+        check(lib.osplat_gpu_backward_device(self.handle, frame.handle, C.c_void_p(d_image_ptr), int(accumulate)))
+
+    def gradients(self):
+        n, bc = self.n, self.basis_count
+        out = dict(d_position=np.zeros((n, 3)), d_sh=np.zeros((n, bc, 3)), d_rotation=np.zeros((n, 4)),
+                   d_log_scale=np.zeros((n, 3)), d_opacity_logit=np.zeros(n), d_screen=np.zeros((n, 2)),
+                   screen_norm_sum=np.zeros(n), screen_hits=np.zeros(n, dtype=np.int64))
+        check(lib.osplat_gpu_gradients(self.handle, *[_p(out[k]) for k in (
+            "d_position", "d_sh", "d_rotation", "d_log_scale", "d_opacity_logit", "d_screen",
+            "screen_norm_sum")], _p(out["screen_hits"], _lp)))
+        return out
+
+    def zero_grad(self):
+        check(lib.osplat_gpu_zero_grad(self.handle))
+
+    def reset_screen_stats(self):
+        check(lib.osplat_gpu_reset_screen_stats(self.handle))
+
+    def adam_step(self, config: Config | None, extent: float, iteration: int, zero_grad: bool = False):
+        check(lib.osplat_gpu_adam_step(self.handle, config.handle if config else None, extent, iteration,
+                                       int(zero_grad)))
+
+    def l1_loss(self, frame: Frame, gt_ptr: int, mask_bottom_fraction: float = 0.0, want_value=True):
+        d = _vp()
+        val = C.c_double(0.0)
+        check(lib.osplat_gpu_l1_loss(self.handle, frame.handle, C.c_void_p(gt_ptr), mask_bottom_fraction,
+                                     C.byref(d), C.byref(val) if want_value else None))
+        return val.value, d.value
+
+    def train_view(self, pose12, width: int, height: int, gt, gt_on_device: bool, mask: float = 0.0) -> float:
+        """render -> L1 loss -> backward(accumulate); gt is a host numpy array (3,H,W) float32
+        or a device pointer (int)."""
+        t = transform_of(pose12)
+        loss = C.c_double(0.0)
+        ptr = C.c_void_p(gt) if gt_on_device else gt.ctypes.data_as(C.c_void_p)
+        check(lib.osplat_gpu_train_view(self.handle, _p(t), width, height, ptr, int(gt_on_device), mask,
+                                        C.byref(loss)))
+        return loss.value
+
+    def download(self) -> Cloud:
+        h = _vp()
+        check(lib.osplat_gpu_download(self.handle, C.byref(h)))
+        return HostCloud(h).to_cloud()
+
+    def synchronize(self):
+        check(lib.osplat_gpu_synchronize(self.handle))
+
+    def free(self):
+        if getattr(self, "handle", None):
+            lib.osplat_gpu_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.free()

@@ -1,0 +1,143 @@
+"""GPU parity: the CUDA path (through the C ABI) against the FP64 oracle on identical inputs.
+
+Bars (BASELINE.json north_star): tile assignments / sorted keys / per-tile ranges bit-exact,
+images within 1e-4 absolute, gradients within 1e-3 relative (norm-relative floor).
+"""
+import numpy as np
+import pytest
+
+from paper_2404_03202_b200 import native, scenes
+
+from parity import IMAGE_ATOL, compare_projections, compare_tiles, grads_close
+
+pytestmark = pytest.mark.gpu
+
+
+def _scene(kind, n, seed=1):
+    return scenes.synthetic_cloud(n, seed=seed, variant=kind)
+
+
+CASES = [
+    # (name, cloud factory, pose, W, H)
+    ("c1_uniform", lambda: _scene("uniform", 10_000, 1), scenes.identity_pose(), 512, 256),
+    ("pole_small", lambda: _scene("pole", 3_000, 3), scenes.identity_pose(), 256, 128),
+    ("seam_small", lambda: _scene("seam", 3_000, 4), scenes.identity_pose(), 256, 128),
+    ("random_pose", lambda: _scene("uniform", 5_000, 5), scenes.random_pose(np.random.default_rng(7)), 384, 192),
+    ("odd_size", lambda: _scene("uniform", 2_000, 6), scenes.identity_pose(), 200, 100),
+]
+
+
+@pytest.mark.parametrize("name,make,pose,W,H", CASES, ids=[c[0] for c in CASES])
+def test_forward_parity(name, make, pose, W, H, oracle_port):
+    cloud = make()
+    ctx = native.Context(cloud)
+    fr = ctx.render(pose, W, H)
+    of = oracle_port.render(cloud, pose, W, H)
+
+    proj = compare_projections(fr, of, cloud.n)
+    assert proj["p_rel"] < 1e-12, proj
+    assert proj["conic_rel"] < 1e-12, proj
+    assert proj["opacity_rel"] < 1e-14, proj
+    assert proj["color_abs"] < 1e-6, proj
+    assert proj["touched_mismatch"] == 0, proj
+
+    nbad, first = compare_tiles(fr, of)
+    assert nbad == 0, f"{nbad} tile lists differ (first {first})"
+
+    rgb, T, con, last = fr.pixels()
+    img = fr.image()
+    err = np.max(np.abs(img - of.rgb))
+    assert err <= IMAGE_ATOL, err
+    assert np.array_equal(last, of.last_contrib), int(np.sum(last != of.last_contrib))
+    assert np.array_equal(con, of.contributors), int(np.sum(con != of.contributors))
+    assert np.max(np.abs(T - of.T)) < 1e-5
+
+
+@pytest.mark.parametrize("name,make,pose,W,H", CASES[:4], ids=[c[0] for c in CASES[:4]])
+def test_backward_parity(name, make, pose, W, H, oracle_port):
+    cloud = make()
+    rng = np.random.default_rng(11)
+    d_image = rng.uniform(-1.0, 1.0, size=(H, W, 3)) / (W * H)
+    ctx = native.Context(cloud)
+    fr = ctx.render(pose, W, H)
+    ctx.backward(fr, d_image)
+    g = ctx.gradients()
+    of = oracle_port.render(cloud, pose, W, H, keep_handle=True)
+    go = oracle_port.backward(of, d_image, cloud, pose)
+    oracle_port.free(of)
+    rep = grads_close(g, go)
+    for k, (nbad, total, maxrel) in rep.items():
+        assert nbad <= max(2, total // 20000), (k, nbad, total, maxrel)
+    assert np.array_equal(g["screen_hits"], go.screen_hits)
+    ds_scale = np.max(np.abs(go.d_screen))
+    assert np.max(np.abs(g["d_screen"] - go.d_screen)) <= 1e-3 * ds_scale + 1e-12
+
+
+def test_adam_parity(oracle_port):
+    """adam_step over the GPU's own FP32 gradients vs the oracle fed the same gradients."""
+    import pyoracle
+    cloud = _scene("uniform", 4_000, 9)
+    W, H, pose = 256, 128, scenes.identity_pose()
+    ctx = native.Context(cloud)
+    ref = cloud.copy()
+    st = pyoracle.AdamState.zeros(cloud.n, cloud.basis_count)
+    cfg = pyoracle.AdamConfig(iterations=100)
+    ncfg = native.Config(iterations=100)
+    rng = np.random.default_rng(3)
+    for it in range(1, 11):
+        fr = ctx.render(pose, W, H)
+        d_image = rng.uniform(-1.0, 1.0, size=(H, W, 3)) / (W * H)
+        ctx.backward(fr, d_image)
+        g = ctx.gradients()
+        go = pyoracle.Grads(g["d_position"], g["d_sh"], g["d_rotation"], g["d_log_scale"], g["d_opacity_logit"],
+                            g["d_screen"], np.zeros(cloud.n), np.zeros(cloud.n, dtype=np.int64))
+        ctx.adam_step(ncfg, 1.5, it)
+        oracle_port.adam_step(ref, go, st, cfg, 1.5, it)
+        fr.free()
+        got = ctx.download()
+        # oracle keeps FP64 params; the device keeps FP32 planes -> compare within FP32 rounding of
+        # the accumulated update (lr-scaled)
+        for name, lr in (("positions", 1.6e-4 * 1.5), ("sh", 2.5e-3), ("rotations", 1e-3), ("log_scales", 5e-3),
+                         ("opacity_logits", 5e-2)):
+            a, b = getattr(got, name), getattr(ref, name)
+            tol = 1e-6 * np.abs(b) + 1e-3 * lr * it
+            assert np.all(np.abs(a - b) <= tol + 1e-7), (name, it, float(np.max(np.abs(a - b))))
+        # resync the oracle to the device's FP32 parameters so FP32 rounding does not compound
+        ref = got.copy()
+
+
+def test_tiled_matches_bruteforce_compact(oracle_port):
+    """test_rasterizer.cpp:171-185 through the GPU: 50 compact scenes, |tiled - brute| < 1e-5."""
+    rng = np.random.default_rng(43)
+    worst = 0.0
+    for scene in range(50):
+        cloud = scenes.random_cloud(rng, count=20 + scene % 80, min_opacity=0.05, max_opacity=0.3)
+        pose = scenes.random_pose(rng)
+        ctx = native.Context(cloud)
+        img = ctx.render(pose, 128, 64).image()
+        ref = oracle_port.render(cloud, pose, 128, 64, brute_force=True)
+        worst = max(worst, float(np.max(np.abs(img - ref.rgb))))
+    assert worst < 1e-5, worst
+
+
+def test_osplat_render_c_abi_matches_frame(oracle_port):
+    cloud = _scene("uniform", 3_000, 12)
+    pose = scenes.random_pose(np.random.default_rng(1))
+    hc = native.HostCloud.from_cloud(cloud)
+    img = native.osplat_render(hc, pose, 256, 128)
+    of = oracle_port.render(cloud, pose, 256, 128)
+    assert img.shape == (128, 256, 3)
+    assert np.max(np.abs(img - of.rgb)) <= IMAGE_ATOL
+
+
+def test_empty_and_culled_clouds():
+    empty = scenes.synthetic_cloud(0, seed=1)
+    ctx = native.Context(empty)
+    img = ctx.render(scenes.identity_pose(), 128, 64, background=(0.2, 0.3, 0.4)).image()
+    assert np.allclose(img[..., 0], 0.2) and np.allclose(img[..., 2], 0.4)
+    faint = scenes.synthetic_cloud(100, seed=2)
+    faint.opacity_logits[:] = -10.0  # sigmoid < 1/255 -> every Gaussian culled
+    ctx = native.Context(faint)
+    fr = ctx.render(scenes.identity_pose(), 128, 64)
+    assert np.all(fr.image() == 0.0)
+    assert fr.tiles()[3].size == 0

@@ -1,0 +1,138 @@
+"""CPU: pin the C restatement (oracle/oracle.c) against the reference's own sources
+(oracle/_ref, compiled from /root/reference) and against the committed golden fixtures.
+
+Every output must be BIT-identical: the restatement keeps the reference's FP64 operation order
+and both are compiled with -ffp-contract=off.
+"""
+import os
+import subprocess
+import zlib
+
+import numpy as np
+import pytest
+
+from paper_2404_03202_b200 import scenes
+
+import pyoracle
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _frame_fields(f):
+    return dict(gid=f.gaussian_id, p=f.p, cov=f.cov, conic=f.conic, radius=f.radius, depth=f.depth,
+                color=f.color, alpha=f.alpha, t=f.t, offsets=f.offsets, items=f.items, rgb=f.rgb, T=f.T,
+                contributors=f.contributors, last=f.last_contrib)
+
+
+def _assert_same(a: dict, b: dict, ctx=""):
+    for k in a:
+        assert np.array_equal(a[k], b[k]), f"{ctx}: {k} differs"
+
+
+SCENES = [
+    ("random40", lambda rng: scenes.random_cloud(rng, count=40), 128, 64),
+    ("random_poles", lambda rng: scenes.random_cloud(rng, count=60, avoid_poles=False), 128, 64),
+    ("sh0", lambda rng: scenes.random_cloud(rng, count=50, sh_degree=0), 96, 48),
+    ("sh1", lambda rng: scenes.random_cloud(rng, count=50, sh_degree=1), 100, 50),
+    ("sh2", lambda rng: scenes.random_cloud(rng, count=50, sh_degree=2), 64, 32),
+    ("synthetic2k", lambda rng: scenes.synthetic_cloud(2000, seed=5), 256, 128),
+    ("pole2k", lambda rng: scenes.synthetic_cloud(2000, seed=6, variant="pole"), 256, 128),
+    ("seam2k", lambda rng: scenes.synthetic_cloud(2000, seed=7, variant="seam"), 256, 128),
+]
+
+
+@pytest.mark.parametrize("name,make,W,H", SCENES, ids=[s[0] for s in SCENES])
+def test_restatement_bit_exact_vs_reference(name, make, W, H, oracle_port, oracle_ref):
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
+    cloud = make(rng)
+    if cloud.sh_degree > 0:
+        cloud.active_sh_degree = max(0, cloud.sh_degree - 1) if name == "sh2" else cloud.sh_degree
+    pose = scenes.random_pose(rng)
+    bg = (0.1, 0.2, 0.3)
+    fp = oracle_port.render(cloud, pose, W, H, bg, keep_handle=True)
+    fr = oracle_ref.render(cloud, pose, W, H, bg, keep_handle=True)
+    _assert_same(_frame_fields(fp), _frame_fields(fr), name)
+
+    d_image = rng.uniform(-1, 1, size=(H, W, 3))
+    gp = oracle_port.backward(fp, d_image, cloud, pose)
+    gr = oracle_ref.backward(fr, d_image, cloud, pose)
+    for k in gp.__dataclass_fields__:
+        assert np.array_equal(getattr(gp, k), getattr(gr, k)), f"{name}: grad {k}"
+
+    cfg = pyoracle.AdamConfig(iterations=50)
+    c1, c2 = cloud.copy(), cloud.copy()
+    s1 = pyoracle.AdamState.zeros(cloud.n, cloud.basis_count)
+    s2 = pyoracle.AdamState.zeros(cloud.n, cloud.basis_count)
+    for it in range(1, 4):
+        oracle_port.adam_step(c1, gp, s1, cfg, 1.7, it)
+        oracle_ref.adam_step(c2, gr, s2, cfg, 1.7, it)
+    for k in ("positions", "sh", "rotations", "log_scales", "opacity_logits"):
+        assert np.array_equal(getattr(c1, k), getattr(c2, k)), f"{name}: adam {k}"
+    assert s1.step == s2.step == 3
+
+    gt = rng.uniform(0, 1, size=(H, W, 3))
+    for lam, mask in ((0.0, 0.0), (0.2, 0.0), (0.2, 0.1)):
+        vp, dp = oracle_port.loss(fp.rgb, gt, lam, mask)
+        vr, dr = oracle_ref.loss(fr.rgb, gt, lam, mask)
+        assert vp == vr and np.array_equal(dp, dr), f"{name}: loss lambda={lam} mask={mask}"
+    oracle_port.free(fp)
+    oracle_ref.free(fr)
+
+
+def test_brute_force_bit_exact_vs_reference(oracle_port, oracle_ref):
+    rng = np.random.default_rng(99)
+    cloud = scenes.random_cloud(rng, count=30, min_opacity=0.05, max_opacity=0.3)
+    pose = scenes.random_pose(rng)
+    a = oracle_port.render(cloud, pose, 64, 32, brute_force=True)
+    b = oracle_ref.render(cloud, pose, 64, 32, brute_force=True)
+    assert np.array_equal(a.rgb, b.rgb) and np.array_equal(a.contributors, b.contributors)
+
+
+def _golden_files():
+    return sorted(f for f in os.listdir(GOLDEN) if f.endswith(".npz"))
+
+
+@pytest.mark.parametrize("fname", _golden_files())
+def test_restatement_matches_golden(fname, oracle_port):
+    """Golden vectors were produced by the reference sources (tests/golden/make_golden.py)."""
+    z = np.load(os.path.join(GOLDEN, fname))
+    cloud = scenes.Cloud(z["positions"], z["sh"], z["rotations"], z["log_scales"], z["opacity_logits"],
+                         int(z["sh_degree"]), int(z["active_sh_degree"]))
+    pose, W, H = z["pose"], int(z["width"]), int(z["height"])
+    f = oracle_port.render(cloud, pose, W, H, tuple(z["background"]), keep_handle=True)
+    got = _frame_fields(f)
+    for k in ("gid", "p", "conic", "radius", "depth", "color", "offsets", "items", "rgb", "T", "contributors",
+              "last"):
+        assert np.array_equal(got[k], z["f_" + k]), f"{fname}: {k}"
+    g = oracle_port.backward(f, z["d_image"], cloud, pose)
+    for k in ("d_position", "d_sh", "d_rotation", "d_log_scale", "d_opacity_logit", "d_screen"):
+        assert np.array_equal(getattr(g, k), z["g_" + k]), f"{fname}: {k}"
+    oracle_port.free(f)
+    c = cloud.copy()
+    st = pyoracle.AdamState.zeros(c.n, c.basis_count)
+    cfg = pyoracle.AdamConfig(iterations=int(z["adam_iterations"]))
+    for it in range(1, 11):
+        oracle_port.adam_step(c, g, st, cfg, float(z["extent"]), it)
+        if it in (1, 10):
+            for k in ("positions", "sh", "rotations", "log_scales", "opacity_logits"):
+                assert np.array_equal(getattr(c, k), z[f"adam{it}_{k}"]), f"{fname}: adam step {it} {k}"
+
+
+REF_TESTS = os.path.join(os.path.dirname(os.path.dirname(__file__)), "oracle", "_ref", "tests")
+
+
+@pytest.mark.parametrize("name", ["test_camera", "test_scene", "test_metrics", "test_rasterizer"])
+def test_reference_unit_tests_pin_oracle(name):
+    """The reference's own doctest files, compiled unmodified against its sources through
+    oracle/doctest_shim. Known result: 33/34 pass; the failing case is
+    test_rasterizer.cpp:80 (a splat on a tile boundary emits 4 instances, not 1)."""
+    exe = os.path.join(REF_TESTS, name)
+    if not os.path.exists(exe):
+        pytest.skip("reference unit tests not built")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    fails = [l for l in r.stdout.splitlines() if l.startswith("[FAIL]")]
+    if name == "test_rasterizer":
+        assert fails == ["[FAIL] bin_to_tiles basics and seam wrap"], r.stdout
+        assert "test_rasterizer.cpp:80" in r.stdout
+    else:
+        assert r.returncode == 0 and not fails, r.stdout
