@@ -180,6 +180,19 @@ OSPLAT_API osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double tra
                                     const float* gt_planar, int gt_on_device, double mask_bottom_fraction,
                                     double* loss);
 
+/* Profiling (bench.py roofline evidence). With timing on, every kernel family is bracketed by a
+ * CUDA event pair on the context stream; with count_work on, K3 also writes per-pixel visited
+ * list entries so osplat_frame_work can report the algorithmic pair counts. */
+#define OSPLAT_KERNEL_COUNT 11
+OSPLAT_API osplat_status osplat_gpu_profile(osplat_gpu* ctx, int timing, int count_work);
+/* ms[k] / launches[k] for k < OSPLAT_KERNEL_COUNT (synchronizes); reset != 0 clears them. */
+OSPLAT_API osplat_status osplat_gpu_profile_read(osplat_gpu* ctx, double* ms, long* launches, int reset);
+OSPLAT_API const char* osplat_kernel_name(int id);
+/* Work of one frame: forward pairs visited (sum over pixels of list entries evaluated before the
+ * T stop), backward pairs (sum of last_contrib), tile instances M. Needs count_work at render. */
+OSPLAT_API osplat_status osplat_frame_work(const osplat_frame* frame, uint64_t* fwd_pairs, uint64_t* bwd_pairs,
+                                           uint64_t* instances);
+
 /* Kernel launches issued by this library since load (evidence for the benchmark). */
 OSPLAT_API long long osplat_gpu_launch_count(void);
 

@@ -13,6 +13,7 @@
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #define K_PI 3.14159265358979323846            /* vecmath.hpp:191 */
 #define K_ALPHA_MIN (1.0 / 255.0)              /* rasterizer.hpp:18 */
@@ -30,6 +31,13 @@ static const double kShC2[5] = {1.0925484305920792, -1.0925484305920792, 0.31539
 static const double kShC3[7] = {-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
                                 0.3731763325901154, -0.4570457994644658, 1.445305721320277,
                                 -0.5900435899266435};
+
+static double g_last_seconds = 0.0;
+static double now_s(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
+}
 
 /* ------------------------------------------------------------------ small math (vecmath.hpp) */
 
@@ -426,9 +434,11 @@ static void blend(oracle_frame* f) {
 
 oracle_frame* oracle_render(const oracle_cloud* c, const double pose[12], int W, int H, const double bg[3]) {
     if (!c || !pose || W < 1 || H < 1) return NULL;
+    double t0 = now_s();
     oracle_frame* f = frame_new(c, pose, W, H, bg);
     bin_tiles(f);
     blend(f);
+    g_last_seconds = now_s() - t0;
     return f;
 }
 
@@ -540,8 +550,19 @@ static void quat_rotation_grad(const double* q, double out[4][9]) {
     memcpy(out[2], g2, sizeof g2); memcpy(out[3], g3, sizeof g3);
 }
 
+static int backward_impl(const oracle_frame* f, const double* d_image, const oracle_cloud* c,
+                         const double pose[12], int W, int H, oracle_grads* gb);
+
 int oracle_backward(const oracle_frame* f, const double* d_image, const oracle_cloud* c,
                     const double pose[12], int W, int H, oracle_grads* gb) {
+    double t0 = now_s();
+    int rc = backward_impl(f, d_image, c, pose, W, H, gb);
+    g_last_seconds = now_s() - t0;
+    return rc;
+}
+
+static int backward_impl(const oracle_frame* f, const double* d_image, const oracle_cloud* c,
+                         const double pose[12], int W, int H, oracle_grads* gb) {
     /* state checks (gradients.cpp:74-80): only the rotation is compared */
     if (f->cloud_size != c->n || f->width != W || f->height != H ||
         memcmp(f->pose, pose, sizeof(double) * 9) != 0)
@@ -769,6 +790,7 @@ static void adam_update(double* param, double grad, double* m, double* v, double
 
 void oracle_adam_step(oracle_cloud* c, const oracle_grads* g, oracle_adam* st, const oracle_adam_cfg* cfg,
                       double extent, long iteration) {
+    const double t0 = now_s();
     const int n = c->n, bc = bc_of(c->sh_degree);
     st->step += 1;
     double bias1 = 1.0 - pow(0.9, (double)st->step);
@@ -800,6 +822,7 @@ void oracle_adam_step(oracle_cloud* c, const oracle_grads* g, oracle_adam* st, c
         adam_update(&c->opacity_logits[i], g->d_opacity_logit[i], &st->m_opacity[i], &st->v_opacity[i],
                     cfg->lr_opacity, bias1, bias2);
     }
+    g_last_seconds = now_s() - t0;
 }
 
 /* ------------------------------------------------------------------ loss (trainer.cpp, metrics.cpp) */
@@ -937,5 +960,6 @@ double oracle_loss(const double* r, const double* gt, int w, int h, double lambd
 }
 
 void oracle_set_threads(int n) { (void)n; }
+double oracle_last_seconds(void) { return g_last_seconds; }
 int oracle_threads(void) { return 1; }
 const char* oracle_kind(void) { return "port"; }

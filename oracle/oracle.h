@@ -99,6 +99,10 @@ void oracle_adam_step(oracle_cloud* cloud, const oracle_grads* grads, oracle_ada
 double oracle_loss(const double* rendered, const double* gt, int width, int height,
                    double lambda_ssim, double mask_bottom_fraction, double* d_image);
 
+/* Wall time (steady clock, like eval.cpp:84-87) of the last render / backward / adam_step / loss
+ * call, excluding the marshalling between these flat arrays and the implementation's types. */
+double oracle_last_seconds(void);
+
 /* Thread count of the implementation (reference: OMNISPLAT_THREADS; restatement: 1). */
 void oracle_set_threads(int n);
 int oracle_threads(void);

@@ -164,6 +164,7 @@ class Oracle:
         lib.oracle_set_threads.argtypes = [C.c_int]
         lib.oracle_threads.restype = C.c_int
         lib.oracle_kind.restype = C.c_char_p
+        lib.oracle_last_seconds.restype = C.c_double
 
     # ------------------------------------------------------------------ helpers
     @staticmethod
@@ -178,6 +179,10 @@ class Oracle:
 
     def threads(self) -> int:
         return int(self.lib.oracle_threads())
+
+    def last_seconds(self) -> float:
+        """Steady-clock time of the last render/backward/adam_step/loss call (no marshalling)."""
+        return float(self.lib.oracle_last_seconds())
 
     # ------------------------------------------------------------------ API
     def render(self, cloud, pose, width, height, background=(0.0, 0.0, 0.0), brute_force=False,

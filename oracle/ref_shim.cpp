@@ -3,6 +3,7 @@
 // through oracle/oracle.h so tests can diff the C restatement and the CUDA product against
 // the unmodified reference code. Built by oracle/Makefile into oracle/_ref/libref_oracle.so;
 // the reference sources are compiled where they lie and never copied into this repo.
+#include <chrono>
 #include <cstring>
 #include <vector>
 
@@ -53,6 +54,15 @@ void from_cloud(const GaussianCloud& g, oracle_cloud* c) {
     }
 }
 
+double g_last_seconds = 0.0;
+
+struct Stopwatch {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    ~Stopwatch() {
+        g_last_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
+
 Pose to_pose(const double* p) {
     Pose pose;
     for (int i = 0; i < 9; ++i) pose.rotation.m[i] = p[i];
@@ -69,7 +79,12 @@ oracle_frame* oracle_render(const oracle_cloud* c, const double pose[12], int w,
         RenderSettings s;
         if (bg) s.background = {bg[0], bg[1], bg[2]};
         auto* f = new oracle_frame;
-        f->out = render(to_cloud(c), to_pose(pose), EquirectCamera{w, h}, s);
+        GaussianCloud cloud = to_cloud(c);
+        Pose p = to_pose(pose);
+        {
+            Stopwatch sw;
+            f->out = render(cloud, p, EquirectCamera{w, h}, s);
+        }
         return f;
     } catch (...) {
         return nullptr;
@@ -160,7 +175,10 @@ int oracle_backward(const oracle_frame* f, const double* d_image, const oracle_c
             buf.screen_norm_sum[i] = g->screen_norm_sum[i];
             buf.screen_hits[i] = g->screen_hits[i];
         }
-        backward(f->out, di, cloud, to_pose(pose), EquirectCamera{w, h}, buf);
+        {
+            Stopwatch sw;
+            backward(f->out, di, cloud, to_pose(pose), EquirectCamera{w, h}, buf);
+        }
         const int bc = cloud.basis_count();
         for (int i = 0; i < c->n; ++i) {
             for (int k = 0; k < 3; ++k) g->d_position[3 * i + k] = buf.d_position[i][k];
@@ -222,7 +240,10 @@ void oracle_adam_step(oracle_cloud* c, const oracle_grads* g, oracle_adam* st, c
     tc.lr_opacity = cfg->lr_opacity;
     tc.lr_scale = cfg->lr_scale;
     tc.lr_rotation = cfg->lr_rotation;
-    adam_step(cloud, buf, state, tc, extent, iteration);
+    {
+        Stopwatch sw;
+        adam_step(cloud, buf, state, tc, extent, iteration);
+    }
     from_cloud(cloud, c);
     st->step = state.step;
     auto store = [](const std::vector<double>& v, double* dst) { std::memcpy(dst, v.data(), v.size() * 8); };
@@ -243,12 +264,17 @@ double oracle_loss(const double* r, const double* gt, int w, int h, double lambd
     Image a(w, h), b(w, h);
     std::memcpy(a.data.data(), r, a.data.size() * 8);
     std::memcpy(b.data.data(), gt, b.data.size() * 8);
-    LossResult lr = loss(a, b, lambda, mask);
+    LossResult lr;
+    {
+        Stopwatch sw;
+        lr = loss(a, b, lambda, mask);
+    }
     if (d_image) std::memcpy(d_image, lr.d_image.data.data(), lr.d_image.data.size() * 8);
     return lr.value;
 }
 
 void oracle_set_threads(int n) { set_thread_count(n); }
+double oracle_last_seconds(void) { return g_last_seconds; }
 int oracle_threads(void) { return thread_count(); }
 const char* oracle_kind(void) { return "reference"; }
 

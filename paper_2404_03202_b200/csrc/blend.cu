@@ -33,6 +33,7 @@ __global__ void __launch_bounds__(kStage) k_blend(const uint32_t* __restrict__ i
     double T64 = 1.0;
     bool exact = false;
     int contrib = 0, last = 0;
+    int stop_at = static_cast<int>(range.y - range.x);  // entries evaluated (work counting)
     bool done = !inside;
 
     for (uint32_t base = range.x; base < range.y; base += kStage) {
@@ -65,6 +66,7 @@ __global__ void __launch_bounds__(kStage) k_blend(const uint32_t* __restrict__ i
                 if (Tn < kTHi) {
                     if (Tn < kTLo) {
                         done = true;
+                        stop_at = static_cast<int>(k - range.x) + 1;
                         break;
                     }
                     // Inside the band: decide in FP64 from an exact replay of the prefix.
@@ -77,6 +79,7 @@ __global__ void __launch_bounds__(kStage) k_blend(const uint32_t* __restrict__ i
                     const double Tn64 = T64 * (1.0 - a64);
                     if (Tn64 < kTStop) {
                         done = true;
+                        stop_at = static_cast<int>(k - range.x) + 1;
                         break;
                     }
                     exact = true;
@@ -91,6 +94,7 @@ __global__ void __launch_bounds__(kStage) k_blend(const uint32_t* __restrict__ i
                 const double Tn64 = T64 * (1.0 - a64);
                 if (Tn64 < kTStop) {
                     done = true;
+                    stop_at = static_cast<int>(k - range.x) + 1;
                     break;
                 }
                 w = static_cast<float>(a64 * T64);
@@ -113,10 +117,36 @@ __global__ void __launch_bounds__(kStage) k_blend(const uint32_t* __restrict__ i
         fb.T[pix] = T;
         fb.contrib[pix] = contrib;
         fb.last[pix] = last;
+        if (fb.visited) fb.visited[pix] = stop_at;
+    }
+}
+
+__global__ void k_work_count(const int* __restrict__ visited, const int* __restrict__ last, int pixels,
+                             unsigned long long* __restrict__ out) {
+    unsigned long long a = 0, b = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < pixels; i += gridDim.x * blockDim.x) {
+        a += static_cast<unsigned long long>(visited[i]);
+        b += static_cast<unsigned long long>(last[i]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, off);
+        b += __shfl_down_sync(0xffffffffu, b, off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out, a);
+        atomicAdd(out + 1, b);
     }
 }
 
 }  // namespace
+
+void launch_work_count(const FrameBuffers& fb, int pixels, unsigned long long* out, cudaStream_t s) {
+    OSB_CUDA_CHECK(cudaMemsetAsync(out, 0, 16, s));
+    if (pixels <= 0 || !fb.visited) return;
+    k_work_count<<<296, 256, 0, s>>>(fb.visited, fb.last, pixels, out);
+    OSB_LAUNCHED(1);
+}
 
 void launch_blend(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H, int tiles_x,
                   int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s) {

@@ -777,6 +777,35 @@ osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[1
     });
 }
 
+osplat_status osplat_gpu_profile(osplat_gpu* ctx, int timing, int count_work) {
+    if (!ctx) return invalid("osplat_gpu_profile: null context");
+    return wrap([&] { ctx->engine->set_profiling(timing != 0, count_work != 0); });
+}
+
+osplat_status osplat_gpu_profile_read(osplat_gpu* ctx, double* ms, long* launches, int reset) {
+    if (!ctx) return invalid("osplat_gpu_profile_read: null context");
+    return wrap([&] { ctx->engine->profile_read(ms, launches, reset != 0); });
+}
+
+const char* osplat_kernel_name(int id) { return osb::kernel_name(id); }
+
+osplat_status osplat_frame_work(const osplat_frame* frame, uint64_t* fwd, uint64_t* bwd, uint64_t* instances) {
+    if (!frame) return invalid("osplat_frame_work: null frame");
+    return wrap([&] {
+        const osb::Frame& f = *frame->frame;
+        if (!f.count_work) throw ApiError(Code::StateMismatch, "frame was rendered without work counting");
+        osb::DeviceGuard g(frame->engine->device());
+        cudaStream_t s = frame->engine->stream();
+        unsigned long long host[2] = {0, 0};
+        osb::launch_work_count(f.fb(), f.W * f.H, f.work.as<unsigned long long>(), s);
+        OSB_CUDA_CHECK(cudaMemcpyAsync(host, f.work.as<void>(), 16, cudaMemcpyDeviceToHost, s));
+        OSB_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (fwd) *fwd = host[0];
+        if (bwd) *bwd = host[1];
+        if (instances) *instances = f.M;
+    });
+}
+
 long long osplat_gpu_launch_count(void) { return osb::launches_total(); }
 
 }  // extern "C"

@@ -60,7 +60,72 @@ FrameBuffers Frame::fb() const {
     b.T = T.as<float>();
     b.contrib = contrib.as<int>();
     b.last = last.as<int>();
+    b.visited = count_work ? visited.as<int>() : nullptr;
     return b;
+}
+
+const char* kernel_name(int id) {
+    static const char* names[kKernelCount] = {"preprocess", "depth_sort", "scan",  "emit",
+                                              "tile_sort",  "ranges",     "blend", "loss",
+                                              "bwd_pixels", "bwd_gauss",  "adam"};
+    return id >= 0 && id < kKernelCount ? names[id] : "";
+}
+
+cudaEvent_t Engine::ev_get() {
+    if (!events_.empty()) {
+        cudaEvent_t e = events_.back();
+        events_.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    OSB_CUDA_CHECK(cudaEventCreate(&e));
+    return e;
+}
+
+Engine::Span::Span(Engine& eng, int kind) : e(eng), k(kind) {
+    if (!e.timing_) return;
+    a = e.ev_get();
+    OSB_CUDA_CHECK(cudaEventRecord(a, e.stream_));
+}
+
+Engine::Span::~Span() {
+    if (!a) return;
+    cudaEvent_t b = e.ev_get();
+    cudaEventRecord(b, e.stream_);
+    e.pending_.push_back({k, a, b});
+}
+
+void Engine::collect() {
+    for (const Ev& ev : pending_) {
+        float ms = 0.0f;
+        OSB_CUDA_CHECK(cudaEventSynchronize(ev.b));
+        OSB_CUDA_CHECK(cudaEventElapsedTime(&ms, ev.a, ev.b));
+        prof_ms_[ev.k] += ms;
+        prof_n_[ev.k] += 1;
+        events_.push_back(ev.a);
+        events_.push_back(ev.b);
+    }
+    pending_.clear();
+}
+
+void Engine::set_profiling(bool timing, bool count_work) {
+    DeviceGuard g(device_);
+    collect();
+    timing_ = timing;
+    count_work_ = count_work;
+}
+
+void Engine::profile_read(double* ms, long* launches, bool reset) {
+    DeviceGuard g(device_);
+    collect();
+    for (int i = 0; i < kKernelCount; ++i) {
+        if (ms) ms[i] = prof_ms_[i];
+        if (launches) launches[i] = prof_n_[i];
+        if (reset) {
+            prof_ms_[i] = 0.0;
+            prof_n_[i] = 0;
+        }
+    }
 }
 
 Engine::Engine(int device, cudaStream_t stream) : device_(device), stream_(stream), own_stream_(stream == nullptr) {
@@ -75,6 +140,11 @@ Engine::~Engine() {
     cudaSetDevice(device_);
     cudaStreamSynchronize(stream_);
     pool_.clear();
+    for (const Ev& ev : pending_) {
+        cudaEventDestroy(ev.a);
+        cudaEventDestroy(ev.b);
+    }
+    for (cudaEvent_t e : events_) cudaEventDestroy(e);
     if (own_stream_) cudaStreamDestroy(stream_);
 }
 
@@ -199,25 +269,40 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
         f->T.ensure(pixels * 4);
         f->contrib.ensure(pixels * 4);
         f->last.ensure(pixels * 4);
+        f->count_work = count_work_;
+        if (count_work_) {
+            f->visited.ensure(pixels * 4);
+            f->work.ensure(16);
+        }
         f->scan_ws.ensure(scan_workspace_bytes(static_cast<int>(n)));
 
         const PreprocessOut pp = f->pp();
         const int N = static_cast<int>(n_);
         // K1
-        launch_preprocess(params_.as<float>(), N, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
-                          active_, f->pose, W, H, pp, stream_);
+        {
+            Span sp(*this, kPreprocess);
+            launch_preprocess(params_.as<float>(), N, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
+                              active_, f->pose, W, H, pp, stream_);
+        }
         // K2a: depth rank (stable by id)
         f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(n), 8));
-        OSB_CUDA_CHECK(cudaMemcpyAsync(f->okeys[0].as<uint64_t>(), pp.depth_key, n_ * 8, cudaMemcpyDeviceToDevice,
-                                       stream_));
-        launch_iota(f->ovals[0].as<uint32_t>(), N, stream_);
-        const bool flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(),
-                                            f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N, 64,
-                                            f->sort_ws.as<void>(), stream_);
+        bool flipped;
+        {
+            Span sp(*this, kDepthSort);
+            OSB_CUDA_CHECK(cudaMemcpyAsync(f->okeys[0].as<uint64_t>(), pp.depth_key, n_ * 8,
+                                           cudaMemcpyDeviceToDevice, stream_));
+            launch_iota(f->ovals[0].as<uint32_t>(), N, stream_);
+            flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(),
+                                     f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N, 64,
+                                     f->sort_ws.as<void>(), stream_);
+        }
         const uint32_t* order = f->ovals[flipped ? 1 : 0].as<uint32_t>();
         // K2b: instance offsets in depth order
-        launch_gather_scan(pp.touched, order, f->offsets.as<uint32_t>(), f->total.as<uint32_t>(), N,
-                           f->scan_ws.as<void>(), stream_);
+        {
+            Span sp(*this, kScan);
+            launch_gather_scan(pp.touched, order, f->offsets.as<uint32_t>(), f->total.as<uint32_t>(), N,
+                               f->scan_ws.as<void>(), stream_);
+        }
         uint32_t M = 0;
         OSB_CUDA_CHECK(cudaMemcpyAsync(&M, f->total.as<uint32_t>(), 4, cudaMemcpyDeviceToHost, stream_));
         OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -229,18 +314,31 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
             f->ivals[k].ensure(m * 4);
         }
         // K2c: emit (tile, gid) in depth order, stable sort by tile, ranges
-        launch_emit(order, f->offsets.as<uint32_t>(), pp.touched, pp.rect, N, f->tiles_x, f->ikeys[0].as<uint32_t>(),
-                    f->ivals[0].as<uint32_t>(), stream_);
         f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(m), 4));
-        f->inst_in_alt = radix_sort_u32(f->ikeys[0].as<uint32_t>(), f->ikeys[1].as<uint32_t>(),
-                                        f->ivals[0].as<uint32_t>(), f->ivals[1].as<uint32_t>(),
-                                        static_cast<int>(M), bits_for(static_cast<uint64_t>(tiles)),
-                                        f->sort_ws.as<void>(), stream_);
-        OSB_CUDA_CHECK(cudaMemsetAsync(f->ranges.as<uint2>(), 0, static_cast<size_t>(tiles) * 8, stream_));
-        launch_ranges(f->ikeys[f->inst_in_alt ? 1 : 0].as<uint32_t>(), static_cast<int>(M), f->ranges.as<uint2>(),
-                      stream_);
+        {
+            Span sp(*this, kEmit);
+            launch_emit(order, f->offsets.as<uint32_t>(), pp.touched, pp.rect, N, f->tiles_x,
+                        f->ikeys[0].as<uint32_t>(), f->ivals[0].as<uint32_t>(), stream_);
+        }
+        {
+            Span sp(*this, kTileSort);
+            f->inst_in_alt = radix_sort_u32(f->ikeys[0].as<uint32_t>(), f->ikeys[1].as<uint32_t>(),
+                                            f->ivals[0].as<uint32_t>(), f->ivals[1].as<uint32_t>(),
+                                            static_cast<int>(M), bits_for(static_cast<uint64_t>(tiles)),
+                                            f->sort_ws.as<void>(), stream_);
+        }
+        {
+            Span sp(*this, kRanges);
+            OSB_CUDA_CHECK(cudaMemsetAsync(f->ranges.as<uint2>(), 0, static_cast<size_t>(tiles) * 8, stream_));
+            launch_ranges(f->ikeys[f->inst_in_alt ? 1 : 0].as<uint32_t>(), static_cast<int>(M),
+                          f->ranges.as<uint2>(), stream_);
+        }
         // K3
-        launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(), stream_);
+        {
+            Span sp(*this, kBlend);
+            launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(),
+                         stream_);
+        }
     } catch (...) {
         free_.push_back(f);
         throw;
@@ -259,13 +357,19 @@ void Engine::backward(const Frame* f, const float* d_image, bool accumulate) {
     if (!accumulate) OSB_CUDA_CHECK(cudaMemsetAsync(grads_.as<float>(), 0, elems * 4, stream_));
     OSB_CUDA_CHECK(cudaMemsetAsync(acc_.as<float4>(), 0, stride_ * 48, stream_));
     const PreprocessOut pp = f->pp();
-    launch_backward_pixels(f->inst_gid(), f->ranges.as<uint2>(), pp, f->W, f->H, f->tiles_x, f->tiles_y, f->bg,
-                           f->fb(), d_image, acc_.as<float4>(), stream_);
+    {
+        Span sp(*this, kBwdPixels);
+        launch_backward_pixels(f->inst_gid(), f->ranges.as<uint2>(), pp, f->W, f->H, f->tiles_x, f->tiles_y, f->bg,
+                               f->fb(), d_image, acc_.as<float4>(), stream_);
+    }
     ScreenStats st{d_screen_.as<float2>(), norm_sum_.as<double>(), hits_.as<int>()};
     if (!accumulate) OSB_CUDA_CHECK(cudaMemsetAsync(d_screen_.as<float2>(), 0, stride_ * 8, stream_));
-    launch_backward_gaussians(params_.as<float>(), f->n, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
-                              f->active_degree, f->pose, f->W, f->H, pp.depth_key, acc_.as<float4>(), grads_.as<float>(),
-                              st, stream_);
+    {
+        Span sp(*this, kBwdGauss);
+        launch_backward_gaussians(params_.as<float>(), f->n, static_cast<int>(stride_),
+                                  (sh_degree_ + 1) * (sh_degree_ + 1), f->active_degree, f->pose, f->W, f->H,
+                                  pp.depth_key, acc_.as<float4>(), grads_.as<float>(), st, stream_);
+    }
 }
 
 float* Engine::d_image_buffer(size_t pixels) {
@@ -285,8 +389,11 @@ double Engine::l1_loss(const Frame* f, const float* gt, double mask_bottom_fract
     const int masked = static_cast<int>(std::floor(mask_bottom_fraction * f->H));
     const int keep = f->H - masked;
     const double n = static_cast<double>(f->W) * keep * 3.0;
-    OSB_CUDA_CHECK(cudaMemsetAsync(loss_sum_.as<double>(), 0, 8, stream_));
-    launch_l1_loss(f->fb().rgb, gt, f->W, f->H, keep, 1.0 / n, dimg, loss_sum_.as<double>(), stream_);
+    {
+        Span sp(*this, kLoss);
+        OSB_CUDA_CHECK(cudaMemsetAsync(loss_sum_.as<double>(), 0, 8, stream_));
+        launch_l1_loss(f->fb().rgb, gt, f->W, f->H, keep, 1.0 / n, dimg, loss_sum_.as<double>(), stream_);
+    }
     if (!want_value) return 0.0;
     return l1_loss_value(f, mask_bottom_fraction);
 }
@@ -328,6 +435,7 @@ void Engine::adam_step(const TrainHyper& h, double extent, long iteration, bool 
     a.planes = planes_;
     a.stride = static_cast<int>(stride_);
     a.zero_grad = zero_grad ? 1 : 0;
+    Span sp(*this, kAdam);
     launch_adam(params_.as<float>(), grads_.as<float>(), m_.as<float>(), v_.as<float>(), a, stream_);
 }
 

@@ -44,6 +44,11 @@ struct TrainHyper {
     double lr_opacity = 5e-2, lr_scale = 5e-3, lr_rotation = 1e-3;
 };
 
+// Kernel families timed by the optional CUDA-event profiler (osplat_gpu_profile).
+enum KernelId { kPreprocess, kDepthSort, kScan, kEmit, kTileSort, kRanges, kBlend, kLoss, kBwdPixels, kBwdGauss,
+                kAdam, kKernelCount };
+const char* kernel_name(int id);
+
 struct Frame {
     int W = 0, H = 0, tiles_x = 0, tiles_y = 0, n = 0, active_degree = 0;
     uint32_t M = 0;
@@ -58,7 +63,8 @@ struct Frame {
     // instances
     DevBuf ikeys[2], ivals[2], ranges;
     // pixels
-    DevBuf rgb, T, contrib, last;
+    DevBuf rgb, T, contrib, last, visited, work;
+    bool count_work = false;
     DevBuf sort_ws, scan_ws;
     const uint32_t* inst_gid() const { return ivals[inst_in_alt ? 1 : 0].as<uint32_t>(); }
     PreprocessOut pp() const;
@@ -86,6 +92,9 @@ public:
     void zero_grad();
     void reset_screen_stats();
     void synchronize();
+    // CUDA-event timing per kernel family on the context stream, and per-pixel work counting.
+    void set_profiling(bool timing, bool count_work);
+    void profile_read(double* ms, long* launches, bool reset);
 
     // accessors
     cudaStream_t stream() const { return stream_; }
@@ -116,6 +125,29 @@ private:
     DevBuf params_, grads_, m_, v_, acc_, d_screen_, norm_sum_, hits_, loss_sum_, d_image_, gt_;
     std::vector<std::unique_ptr<Frame>> pool_;
     std::vector<Frame*> free_;
+
+    // profiler
+    struct Ev {
+        int k;
+        cudaEvent_t a, b;
+    };
+    bool timing_ = false, count_work_ = false;
+    std::vector<Ev> pending_;
+    std::vector<cudaEvent_t> events_;
+    double prof_ms_[kKernelCount] = {};
+    long prof_n_[kKernelCount] = {};
+    cudaEvent_t ev_get();
+    void collect();
+
+public:
+    // RAII span: records a start/stop event pair around a kernel family when timing is on.
+    struct Span {
+        Engine& e;
+        int k;
+        cudaEvent_t a = nullptr;
+        Span(Engine& eng, int kind);
+        ~Span();
+    };
 };
 
 // RAII device guard.

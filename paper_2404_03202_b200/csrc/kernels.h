@@ -49,7 +49,10 @@ struct FrameBuffers {
     float* T;          // H*W
     int* contrib;      // H*W
     int* last;         // H*W
+    int* visited;      // H*W or nullptr: list entries evaluated per pixel (work counting only)
 };
+// Sums of per-pixel visited (forward pairs) and last_contrib (backward pairs) -> out[0], out[1].
+void launch_work_count(const FrameBuffers& fb, int pixels, unsigned long long* out, cudaStream_t s);
 void launch_blend(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H,
                   int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s);
 

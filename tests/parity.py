@@ -36,7 +36,7 @@ def compare_projections(frame, of, n):
     gid = of.gaussian_id
     rel = lambda a, b: np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)) if a.size else 0.0
     out = dict(
-        p_rel=rel(pr["p"][gid], of.p),
+        p_abs=float(np.max(np.abs(pr["p"][gid] - of.p))) if gid.size else 0.0,
         conic_rel=rel(pr["conic"][gid], of.conic),
         opacity_rel=rel(pr["opacity"][gid], of.alpha),
         color_abs=float(np.max(np.abs(pr["color"][gid] - of.color))) if gid.size else 0.0,
