@@ -1,0 +1,451 @@
+#!/usr/bin/env python
+"""bench.py — "ERP render FPS + fwd/bwd train iters/s, 1M Gaussians at 2048x1024" (BASELINE.json).
+
+One step = one training iteration of the hot path on every GPU: per view, render (K1 preprocess ->
+K2 depth/tile sort -> K3 blend) -> L1 loss -> backward (K4a pixels -> K4b Gaussians, accumulate),
+then the NCCL allreduce of the flat gradient buffer (N > 1) and the fused Adam step (K5).
+Weak scaling: every GPU trains `--views-per-gpu` views of its own per iteration on the replicated
+1M-Gaussian scene; `value` = views trained per second over the whole job (= iterations/s at N=1).
+
+    python bench.py [--gpus N --steps K --warmup W]          # our arm (torchrun for N > 1)
+    python bench.py --impl reference [...]                    # the reference CPU code, host cores
+
+Prints ONE JSON line on rank 0. Inputs are synthetic (scenes.synthetic_cloud, seed 1; the loss
+target is a render of the seed-2 scene from the same view).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ERP render FPS + fwd/bwd train iters/s, 1M Gaussians at 2048x1024"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+
+# Algorithmic work per unit: FP32-pipe instructions per visited
+# (pixel, splat) pair for K3/K4a; bytes per Gaussian / element for the HBM-bound kernels.
+INSTR_PER_FWD_PAIR = 21
+INSTR_PER_BWD_PAIR = 48
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--gaussians", type=int, default=1_000_000)
+    p.add_argument("--width", type=int, default=2048)
+    p.add_argument("--height", type=int, default=1024)
+    p.add_argument("--views-per-gpu", type=int, default=1)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return dict(PEAKS_FALLBACK)
+
+
+def load_traffic():
+    """Per-launch DRAM bytes from the committed ncu capture summary (profiles/), if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f)
+    return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [x.strip() for x in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------------
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def cpu_reference_step(oracle, cloud, pose, gt, W, H, cfg, it):
+    """One reference train step (render + L1 loss + backward + adam_step), summing the reference's
+    own steady-clock times (marshalling excluded)."""
+    import pyoracle
+    f = oracle.render(cloud, pose, W, H, keep_handle=True)
+    t = oracle.last_seconds()
+    _, d = oracle.loss(f.rgb, gt, 0.0, 0.0)
+    t += oracle.last_seconds()
+    g = oracle.backward(f, d, cloud, pose)
+    t += oracle.last_seconds()
+    oracle.free(f)
+    st = pyoracle.AdamState.zeros(cloud.n, cloud.basis_count)
+    oracle.adam_step(cloud, g, st, cfg, 1.0, it)
+    t += oracle.last_seconds()
+    return t, f.rgb
+
+
+def reference_oracle():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    kind = "reference" if pyoracle.available("reference") else "port"
+    o = pyoracle.load(kind)
+    cores = os.cpu_count() or 1
+    o.set_threads(cores)
+    return o, kind, o.threads()
+
+
+def workload_config(args, world):
+    return {"workload": f"{args.gaussians // 1000}k Gaussians, {args.width}x{args.height} ERP, train step "
+                        f"(render + L1 loss + backward + Adam), {args.views_per_gpu} view/GPU/iter",
+            "gaussians": args.gaussians, "width": args.width, "height": args.height,
+            "views_per_gpu_per_step": args.views_per_gpu, "sh_degree": 3, "scene": "synthetic uniform shell, seed 1",
+            "parallelism": f"dp{world} (views split, Gaussians replicated, NCCL allreduce)",
+            "l2": "inputs larger than L2: params + grads + Adam moments = 4 x 236 MB resident"}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2404_03202_b200 import scenes
+    import pyoracle
+    oracle, kind, cores = reference_oracle()
+    N, W, H = args.gaussians, args.width, args.height
+    cloud = scenes.synthetic_cloud(N, seed=1)
+    poses = scenes.ring_poses(16, seed=2)
+    gt = np.zeros((H, W, 3))
+    cfg = pyoracle.AdamConfig(iterations=30000)
+    steps_run, times = 0, []
+    warm = min(args.warmup, 1)
+    budget = 240.0
+    t_start = time.time()
+    for i in range(warm + args.steps):
+        t, _ = cpu_reference_step(oracle, cloud, poses[i % 16], gt, W, H, cfg, i + 1)
+        if i >= warm:
+            times.append(t)
+            steps_run += 1
+        if time.time() - t_start > budget and steps_run >= 1:
+            break
+    sec = float(np.mean(times))
+    value = args.views_per_gpu / sec * 1.0
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world,
+            "steps": args.steps, "steps_run": steps_run, "warmup": warm, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, 1),
+            "cpu_baseline": {"value": value, "unit": "views/s", "cores": cores, "kind": kind,
+                             "sample": f"{steps_run} full train step(s) of the workload on the host "
+                                       f"(reference render + L1 loss + backward + adam_step, steady clock)"},
+            "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+
+class CudaArray:
+    """Minimal __cuda_array_interface__ wrapper so torch can view our device buffers zero-copy."""
+
+    def __init__(self, ptr, n, typestr="<f4"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2404_03202_b200 import native, scenes
+
+    rank, world, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    N, W, H, V = args.gaussians, args.width, args.height, args.views_per_gpu
+    peaks = load_peaks()
+
+    cloud = scenes.synthetic_cloud(N, seed=1)
+    target_cloud = scenes.synthetic_cloud(N, seed=2)
+    poses = scenes.ring_poses(16, seed=2)
+    my_views = [(rank + world * v) % 16 for v in range(V)]
+
+    # loss targets: renders of the seed-2 scene from each view, device resident
+    gts = {}
+    tctx = native.Context(target_cloud, device=local, stream=stream.cuda_stream)
+    plane = W * H
+    for vi in set(my_views):
+        fr = tctx.render(poses[vi], W, H)
+        t = torch.empty(3 * plane, dtype=torch.float32, device="cuda")
+        rgb = fr.device().rgb
+        t.copy_(torch.as_tensor(CudaArray(rgb, 3 * plane), device="cuda"))
+        gts[vi] = t
+        fr.free()
+    tctx.synchronize()
+    del tctx
+
+    ctx = native.Context(cloud, device=local, stream=stream.cuda_stream)
+    cfg = native.Config(iterations=30000)
+    view = ctx.view()
+    grads = torch.as_tensor(CudaArray(view.grads, view.planes * view.stride), device="cuda")
+    extent = 1.0
+    it = [0]
+    from paper_2404_03202_b200 import dp
+    engine = dp.GpuViewEngine(ctx, poses, gts, W, H, cfg, extent)
+    trainer = dp.DataParallelTrainer(engine, rank, world, allreduce=(lambda t: dist.all_reduce(t)) if world > 1
+                                     else None)
+
+    def train_step():
+        it[0] += 1
+        trainer.step(it[0], my_views)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # work counts of this workload (one untimed profiled frame)
+    ctx.profile(timing=False, count_work=True)
+    fr = ctx.render(poses[my_views[0]], W, H)
+    fwd_pairs, bwd_pairs, instances = fr.work()
+    fr.free()
+    ctx.profile(timing=False, count_work=False)
+    ctx.zero_grad()
+
+    for _ in range(max(args.warmup, 3)):
+        train_step()
+    barrier()
+    # clocks are sampled from here to the end of the profiled pass; keep the GPU busy for ~0.6 s
+    # first so the sampler sees the steady state of this load
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_warm = time.perf_counter()
+    while time.perf_counter() - t_warm < 0.6:
+        train_step()
+        torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed train steps (device time, CUDA events on the launching stream, no profiler)
+    launches0 = native.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        train_step()
+    e1.record(stream)
+    barrier()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    launches = native.launch_count() - launches0
+    ms_per_step = ms_total / args.steps
+    value = world * V * args.steps / (ms_total / 1e3)
+
+    # ---- the same steps again with per-kernel CUDA events (roofline evidence)
+    ctx.profile(timing=True, count_work=False)
+    ctx.profile_read(reset=True)
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        train_step()
+    p1.record(stream)
+    barrier()
+    ms_profiled = p0.elapsed_time(p1)
+    prof = ctx.profile_read(reset=True)
+    ctx.profile(timing=False)
+    clk = clocks.stop()
+
+    # ---- render-only FPS (K1 -> K3), same scene, device time
+    barrier()
+    nframes = max(args.steps, 10)
+    ctx.profile(timing=True)
+    ctx.profile_read(reset=True)
+    r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
+    for k in range(nframes):
+        ctx.render(poses[(my_views[0] + k) % 16], W, H).free()
+    r1.record(stream)
+    barrier()
+    render_ms = max_over_ranks(r0.elapsed_time(r1)) / nframes
+    rprof = ctx.profile_read(reset=True)
+    ctx.profile(timing=False)
+
+    # ---- end to end through the public C ABI with host buffers
+    e2e = None
+    render_e2e = None
+    if not args.no_e2e:
+        host_gt = {vi: torch.empty(3 * plane, dtype=torch.float32, pin_memory=True) for vi in my_views}
+        for vi in my_views:
+            host_gt[vi].copy_(gts[vi].cpu())
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            it[0] += 1
+            for vi in my_views:
+                ctx.train_view(poses[vi], W, H, host_gt[vi].data_ptr(), gt_on_device=False)
+            if world > 1:
+                dist.all_reduce(grads)
+            ctx.adam_step(cfg, extent, it[0], zero_grad=True)
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": world * V * args.steps / e2e_s, "unit": "views/s",
+               "h2d_bytes_per_step": V * 3 * plane * 4, "d2h_bytes_per_step": V * 8,
+               "api": "osplat_gpu_train_view (pinned host target in, loss out) + osplat_gpu_adam_step"}
+        if rank == 0:
+            hc = native.HostCloud.from_cloud(cloud)
+            native.osplat_render(hc, poses[0], W, H)  # upload + warm
+            t0 = time.perf_counter()
+            nf = max(3, min(args.steps, 10))
+            for k in range(nf):
+                native.osplat_render(hc, poses[k % 16], W, H)
+            render_e2e = {"value": nf / (time.perf_counter() - t0), "unit": "FPS",
+                          "api": "osplat_render (reference C ABI: host cloud -> host H x W x 3 double image)",
+                          "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 3 * plane * 4}
+
+    # ---- roofline of the dominant kernel family in the timed train steps
+    clk_mhz = peaks["sm_max_mhz"]
+    fp32_peak = 148 * 128 * clk_mhz * 1e6 / 1e12  # T instr/s
+    traffic = load_traffic()
+    n_launch = lambda name: max(prof[name][1], 1)
+    per_launch_ms = {k: v[0] / max(v[1], 1) for k, v in prof.items()}
+    planes = view.planes
+    work = {
+        "blend": ("fp32", fwd_pairs * INSTR_PER_FWD_PAIR / 1e12, "Tinstr/s", fp32_peak),
+        "bwd_pixels": ("fp32", bwd_pairs * INSTR_PER_BWD_PAIR / 1e12, "Tinstr/s", fp32_peak),
+        "preprocess": ("hbm", N * (44 + 12 * 16) / 1e9 + N * 44 / 1e9, "GB/s", peaks["hbm_gbs"]),
+        "adam": ("hbm", 32.0 * planes * view.stride / 1e9, "GB/s", peaks["hbm_gbs"]),
+        "bwd_gauss": ("hbm", N * 520 / 1e9, "GB/s", peaks["hbm_gbs"]),
+        "tile_sort": ("hbm", instances * 32 / 1e9, "GB/s", peaks["hbm_gbs"]),
+        "depth_sort": ("hbm", N * 12 * 2 * 8 / 1e9, "GB/s", peaks["hbm_gbs"]),
+    }
+    rooflines = {}
+    for name, (bound, units, unit, peak) in work.items():
+        if name not in per_launch_ms or prof[name][1] == 0:
+            continue
+        achieved = units / (per_launch_ms[name] / 1e3)
+        rooflines[name] = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                           "frac": achieved / peak, "ms_per_launch": per_launch_ms[name],
+                           "share_of_step": prof[name][0] / max(ms_profiled, 1e-9),
+                           "traffic": traffic.get(name)}
+    dominant = max(prof, key=lambda k: prof[k][0])
+    roof = dict(rooflines.get(dominant, {}))
+    roof["kernel"] = dominant
+    roof["peak_source"] = (f"FP32 issue 148 SMs x 128 lanes x {clk_mhz:.0f} MHz (derived)" if roof.get("bound") ==
+                           "fp32" else peaks["source"])
+
+    # ---- CPU baseline (rank 0, N == 1): the reference code on this host's cores
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            oracle, kind, cores = reference_oracle()
+            import pyoracle
+            gt_host = gts[my_views[0]].cpu().numpy().reshape(3, H, W).transpose(1, 2, 0).astype(np.float64)
+            secs, _ = cpu_reference_step(oracle, scenes.synthetic_cloud(N, seed=1), poses[my_views[0]], gt_host, W, H,
+                                         pyoracle.AdamConfig(iterations=30000), 1)
+            cpu = {"value": 1.0 / secs, "unit": "views/s", "cores": cores, "kind": kind,
+                   "sample": "1 full train step of the same workload (reference render + L1 loss + backward + "
+                             "adam_step, steady clock, marshalling excluded)", "seconds": secs}
+        except Exception as exc:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "views/s", "cores": os.cpu_count(), "kind": "unavailable",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "views/s", "n_gpus": world, "steps": args.steps,
+                "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 geometry + guard)",
+                "data": "synthetic", "config": workload_config(args, world),
+                "render_fps": {"value": 1e3 / render_ms, "ms_per_frame": render_ms, "frames": nframes,
+                               "kernels_ms_per_frame": {k: v[0] / nframes for k, v in rprof.items() if v[1]},
+                               "e2e": render_e2e},
+                "work": {"fwd_pairs": fwd_pairs, "bwd_pairs": bwd_pairs, "instances": instances},
+                "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
+                "ms_per_step_profiled": ms_profiled / args.steps,
+                "roofline": roof, "rooflines": rooflines, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -65,7 +65,7 @@ FrameBuffers Frame::fb() const {
 }
 
 const char* kernel_name(int id) {
-    static const char* names[kKernelCount] = {"preprocess", "depth_sort", "scan",  "emit",
+    static const char* names[kKernelCount] = {"preprocess", "depth_sort", "scan_emit", "emit",
                                               "tile_sort",  "ranges",     "blend", "loss",
                                               "bwd_pixels", "bwd_gauss",  "adam"};
     return id >= 0 && id < kKernelCount ? names[id] : "";
@@ -297,29 +297,31 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
                                      f->sort_ws.as<void>(), stream_);
         }
         const uint32_t* order = f->ovals[flipped ? 1 : 0].as<uint32_t>();
-        // K2b: instance offsets in depth order
-        {
-            Span sp(*this, kScan);
-            launch_gather_scan(pp.touched, order, f->offsets.as<uint32_t>(), f->total.as<uint32_t>(), N,
-                               f->scan_ws.as<void>(), stream_);
-        }
+        // K2b: scan of tiles_touched in depth order fused with the (tile, gid) emission. The
+        // instance buffers keep their capacity across frames; only a frame that outgrows them pays
+        // a second pass.
         uint32_t M = 0;
-        OSB_CUDA_CHECK(cudaMemcpyAsync(&M, f->total.as<uint32_t>(), 4, cudaMemcpyDeviceToHost, stream_));
-        OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
-        if (N == 0) M = 0;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            const uint32_t cap = static_cast<uint32_t>(f->ikeys[0].capacity() / 4);
+            {
+                Span sp(*this, kScan);
+                launch_scan_emit(pp.touched, order, pp.rect, N, f->tiles_x, f->ikeys[0].as<uint32_t>(),
+                                 f->ivals[0].as<uint32_t>(), cap, f->total.as<uint32_t>(), f->scan_ws.as<void>(),
+                                 stream_);
+            }
+            OSB_CUDA_CHECK(cudaMemcpyAsync(&M, f->total.as<uint32_t>(), 4, cudaMemcpyDeviceToHost, stream_));
+            OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+            if (N == 0) M = 0;
+            if (M <= cap && f->ikeys[0].capacity() > 0) break;
+            const size_t want = (static_cast<size_t>(M) + M / 4 + 1024) * 4;
+            for (int k = 0; k < 2; ++k) {
+                f->ikeys[k].ensure(want);
+                f->ivals[k].ensure(want);
+            }
+        }
         f->M = M;
         const size_t m = M > 0 ? M : 1;
-        for (int k = 0; k < 2; ++k) {
-            f->ikeys[k].ensure(m * 4);
-            f->ivals[k].ensure(m * 4);
-        }
-        // K2c: emit (tile, gid) in depth order, stable sort by tile, ranges
         f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(m), 4));
-        {
-            Span sp(*this, kEmit);
-            launch_emit(order, f->offsets.as<uint32_t>(), pp.touched, pp.rect, N, f->tiles_x,
-                        f->ikeys[0].as<uint32_t>(), f->ivals[0].as<uint32_t>(), stream_);
-        }
         {
             Span sp(*this, kTileSort);
             f->inst_in_alt = radix_sort_u32(f->ikeys[0].as<uint32_t>(), f->ikeys[1].as<uint32_t>(),

@@ -35,12 +35,11 @@ bool radix_sort_u64(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, ui
 bool radix_sort_u32(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
                     int bits, void* ws, cudaStream_t s);
 void launch_iota(uint32_t* v, int n, cudaStream_t s);
-// offsets[r] = exclusive scan of touched[order[r]]; *total = sum (device).
+// Exclusive scan of touched[order[r]] fused with the emission of (tile, gid) instances in depth
+// order; writes only instances below `capacity`; *total = M (device).
 size_t scan_workspace_bytes(int n);
-void launch_gather_scan(const uint32_t* touched, const uint32_t* order, uint32_t* offsets, uint32_t* total,
-                        int n, void* ws, cudaStream_t s);
-void launch_emit(const uint32_t* order, const uint32_t* offsets, const uint32_t* touched, const int4* rect,
-                 int n, int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t s);
+void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
+                      uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws, cudaStream_t s);
 void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s);
 
 // ---- K3 blend (blend.cu) --------------------------------------------------------------------

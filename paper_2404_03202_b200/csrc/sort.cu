@@ -2,18 +2,18 @@
 //
 // Replaces bin_to_tiles (proj/src/rasterizer.cpp:57-98): the serial duplication loop and the
 // per-tile std::sort by (depth, gaussian_id). Exactness argument:
-//   1. visible Gaussians are stably radix-sorted by the 64-bit pattern of t_r (positive doubles
-//      order like their bit patterns), with ids as values in ascending order -> (depth, id) order;
-//   2. instances are emitted in that order (exclusive scan of tiles_touched over it);
+//   1. all Gaussians are stably radix-sorted by the 64-bit pattern of t_r (positive doubles order
+//      like their bit patterns; culled ones carry ~0 and sink to the end), with ids as values in
+//      ascending order -> (depth, id) order;
+//   2. instances are emitted in that order (exclusive scan of tiles_touched over it, fused with a
+//      load-balanced emission: every lane writes consecutive instances -> coalesced stores);
 //   3. a STABLE radix sort by tile id keeps the (depth, id) order inside every tile.
 // So each tile list equals the reference's sorted list element for element.
 //
 // Radix sort: LSD, 8-bit digits, one "onesweep" kernel per digit: per-warp match_any ranking,
-// per-block digit counts, decoupled look-back across blocks for the global digit offsets
-// (dynamic block ids guarantee forward progress). Digits that are constant over all keys are
-// skipped (their counts are known from the up-front histogram).
-#include <vector>
-
+// per-block digit counts, decoupled look-back across blocks for the global digit offsets (dynamic
+// block ids guarantee forward progress), then a block-local sort in shared memory so the global
+// scatter writes runs of consecutive addresses. No host synchronization inside a sort.
 #include "kernels.h"
 
 namespace osb {
@@ -24,25 +24,35 @@ constexpr int kRadixBits = 8;
 constexpr int kBins = 1 << kRadixBits;
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kItems = 16;
-constexpr int kTileKeys = kSortThreads * kItems;
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kCountMask = (1u << 30) - 1;
+constexpr int kMaxPasses = 8;
+
+template <typename K>
+struct SortCfg;
+template <>
+struct SortCfg<uint64_t> {
+    static constexpr int kItems = 8;
+};
+template <>
+struct SortCfg<uint32_t> {
+    static constexpr int kItems = 16;
+};
 
 template <typename K>
 __global__ void __launch_bounds__(256) k_histogram(const K* __restrict__ keys, int n, int passes,
                                                    uint32_t* __restrict__ hist /* passes x 256 */) {
-    __shared__ uint32_t s_hist[8][kBins];
+    __shared__ uint32_t s_hist[kMaxPasses][kBins];
     for (int i = threadIdx.x; i < passes * kBins; i += blockDim.x) (&s_hist[0][0])[i] = 0;
     __syncthreads();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        K k = keys[i];
+        const K k = keys[i];
         for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (p * kRadixBits)) & (kBins - 1)], 1u);
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kBins; i += blockDim.x) {
-        uint32_t v = (&s_hist[0][0])[i];
+        const uint32_t v = (&s_hist[0][0])[i];
         if (v) atomicAdd(&hist[i], v);
     }
 }
@@ -55,12 +65,62 @@ __global__ void k_scan_hist(const uint32_t* __restrict__ hist, uint32_t* __restr
     s[d] = hist[p * kBins + d];
     __syncthreads();
     for (int off = 1; off < kBins; off <<= 1) {
-        uint32_t v = d >= off ? s[d - off] : 0;
+        const uint32_t v = d >= off ? s[d - off] : 0;
         __syncthreads();
         s[d] += v;
         __syncthreads();
     }
     base[p * kBins + d] = s[d] - hist[p * kBins + d];
+}
+
+// 256-thread exclusive scan (returns exclusive prefix, *total = block sum).
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += t;
+    }
+    if (lane == 31) s_warp[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t w = lane < kSortWarps ? s_warp[lane] : 0u;
+        uint32_t wi = w;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, wi, off);
+            if (lane >= off) wi += t;
+        }
+        if (lane < kSortWarps) s_warp[lane] = wi - w;
+        if (lane == kSortWarps - 1) s_warp[kSortWarps] = wi;
+    }
+    __syncthreads();
+    const uint32_t r = s_warp[warp] + inc - v;
+    *total = s_warp[kSortWarps];
+    return r;
+}
+
+// Decoupled look-back: publish this block's aggregate for `slot`, return the exclusive prefix.
+__device__ __forceinline__ uint32_t lookback(uint32_t* status, uint32_t bid, size_t stride, size_t slot, uint32_t agg) {
+    uint32_t* my = status + static_cast<size_t>(bid) * stride + slot;
+    if (bid == 0) {
+        st_release(my, kFlagPrefix | agg);
+        return 0;
+    }
+    st_release(my, kFlagAgg | agg);
+    uint32_t exclusive = 0;
+    long p = static_cast<long>(bid) - 1;
+    while (true) {
+        const uint32_t s = ld_acquire(status + static_cast<size_t>(p) * stride + slot);
+        const uint32_t flag = s & ~kCountMask;
+        if (flag == 0) continue;
+        exclusive += s & kCountMask;
+        if (flag == kFlagPrefix) break;
+        --p;
+    }
+    st_release(my, kFlagPrefix | (exclusive + agg));
+    return exclusive;
 }
 
 template <typename K>
@@ -69,19 +129,28 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K* __restrict__
                                                            K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                                                            int n, int shift, const uint32_t* __restrict__ digit_base,
                                                            uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
+    constexpr int kItems = SortCfg<K>::kItems;
+    constexpr int kTile = kSortThreads * kItems;
     __shared__ uint32_t s_bid;
     __shared__ uint32_t s_warp[kSortWarps][kBins];
-    __shared__ uint32_t s_prefix[kBins];
+    __shared__ uint32_t s_local[kBins];   // block-local start of each digit
+    __shared__ int s_global[kBins];       // global position - local position, per digit
+    __shared__ uint32_t s_scan[kSortWarps + 1];
+    __shared__ K s_keys[kTile];
+    __shared__ uint32_t s_vals[kTile];
+
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) s_bid = atomicAdd(counter, 1u);
     for (int i = tid; i < kSortWarps * kBins; i += kSortThreads) (&s_warp[0][0])[i] = 0;
     __syncthreads();
     const uint32_t bid = s_bid;
-    const long base = static_cast<long>(bid) * kTileKeys + static_cast<long>(warp) * 32 * kItems;
+    const long block_base = static_cast<long>(bid) * kTile;
+    const long base = block_base + static_cast<long>(warp) * 32 * kItems;
+    const int count = static_cast<int>(min(static_cast<long>(kTile), static_cast<long>(n) - block_base));
 
     K key[kItems];
     uint32_t val[kItems];
-    uint32_t rank[kItems];
+    uint16_t rank[kItems];
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
@@ -89,6 +158,11 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K* __restrict__
         const bool valid = idx < n;
         key[i] = valid ? keys_in[idx] : K(0);
         val[i] = valid ? vals_in[idx] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const long idx = base + i * 32 + lane;
+        const bool valid = idx < n;
         const uint32_t d = valid ? static_cast<uint32_t>((key[i] >> shift) & (kBins - 1)) : kBins;
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         const int leader = __ffs(peers) - 1;
@@ -98,155 +172,128 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K* __restrict__
             s_warp[warp][d] = prev + __popc(peers);
         }
         prev = __shfl_sync(0xffffffffu, prev, leader);
-        rank[i] = prev + __popc(peers & lt);
+        rank[i] = static_cast<uint16_t>(prev + __popc(peers & lt));
         __syncwarp();
     }
     __syncthreads();
 
-    // Per digit: exclusive prefix over warps, block total, then look-back across blocks.
-    {
-        const int d = tid;
-        uint32_t sum = 0;
+    // Per digit (thread = digit): exclusive prefix over warps and the block count.
+    const int d = tid;
+    uint32_t cnt = 0;
 #pragma unroll
-        for (int w = 0; w < kSortWarps; ++w) {
-            uint32_t t = s_warp[w][d];
-            s_warp[w][d] = sum;
-            sum += t;
-        }
-        uint32_t* my = status + static_cast<size_t>(bid) * kBins + d;
-        uint32_t exclusive = 0;
-        if (bid == 0) {
-            st_release(my, kFlagPrefix | sum);
-        } else {
-            st_release(my, kFlagAgg | sum);
-            long p = static_cast<long>(bid) - 1;
-            while (true) {
-                uint32_t s = ld_acquire(status + static_cast<size_t>(p) * kBins + d);
-                uint32_t flag = s & ~kCountMask;
-                if (flag == 0) continue;
-                exclusive += s & kCountMask;
-                if (flag == kFlagPrefix) break;
-                --p;
-            }
-            st_release(my, kFlagPrefix | (exclusive + sum));
-        }
-        s_prefix[d] = digit_base[d] + exclusive;
+    for (int w = 0; w < kSortWarps; ++w) {
+        const uint32_t t = s_warp[w][d];
+        s_warp[w][d] = cnt;
+        cnt += t;
     }
+    uint32_t total;
+    const uint32_t local = block_exclusive_scan(cnt, s_scan, &total);
+    s_local[d] = local;
+    const uint32_t excl = lookback(status, bid, kBins, d, cnt);
+    s_global[d] = static_cast<int>(digit_base[d] + excl) - static_cast<int>(local);
     __syncthreads();
 
+    // Block-local sort into shared memory.
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         const long idx = base + i * 32 + lane;
         if (idx < n) {
-            const uint32_t d = static_cast<uint32_t>((key[i] >> shift) & (kBins - 1));
-            const uint32_t dst = s_prefix[d] + s_warp[warp][d] + rank[i];
-            keys_out[dst] = key[i];
-            vals_out[dst] = val[i];
+            const uint32_t dd = static_cast<uint32_t>((key[i] >> shift) & (kBins - 1));
+            const uint32_t pos = s_local[dd] + s_warp[warp][dd] + rank[i];
+            s_keys[pos] = key[i];
+            s_vals[pos] = val[i];
         }
+    }
+    __syncthreads();
+    // Coalesced scatter: consecutive local positions of one digit are consecutive globally.
+    for (int i = tid; i < count; i += kSortThreads) {
+        const K k = s_keys[i];
+        const uint32_t dd = static_cast<uint32_t>((k >> shift) & (kBins - 1));
+        const int dst = s_global[dd] + i;
+        keys_out[dst] = k;
+        vals_out[dst] = s_vals[i];
     }
 }
 
 __global__ void k_iota(uint32_t* v, int n) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) v[i] = static_cast<uint32_t>(i);
 }
 
-// Single-pass exclusive scan with decoupled look-back over touched[order[r]].
+// ---- fused exclusive scan of tiles_touched (depth order) + load-balanced instance emission ----
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
-constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int kScanTile = kScanThreads * kScanItems;  // ranks per block
+constexpr int kWarpRanks = 32 * kScanItems;            // ranks per warp
 
-__global__ void __launch_bounds__(kScanThreads) k_gather_scan(const uint32_t* __restrict__ touched,
-                                                              const uint32_t* __restrict__ order,
-                                                              uint32_t* __restrict__ out, uint32_t* __restrict__ total,
-                                                              int n, uint32_t* __restrict__ status,
-                                                              uint32_t* __restrict__ counter) {
+__global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __restrict__ touched,
+                                                            const uint32_t* __restrict__ order,
+                                                            const int4* __restrict__ rect, int n, int tiles_x,
+                                                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                            uint32_t capacity, uint32_t* __restrict__ total,
+                                                            uint32_t* __restrict__ status,
+                                                            uint32_t* __restrict__ counter) {
     __shared__ uint32_t s_bid;
-    __shared__ uint32_t s_warp[kScanThreads / 32];
+    __shared__ uint32_t s_scan[kSortWarps + 1];
     __shared__ uint32_t s_excl;
+    __shared__ uint32_t s_off[kScanTile + kSortWarps];  // per warp: kWarpRanks offsets + warp end
+    __shared__ uint32_t s_gid[kScanTile];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_bid = atomicAdd(counter, 1u);
     __syncthreads();
     const uint32_t bid = s_bid;
-    const long base = static_cast<long>(bid) * kScanTile + static_cast<long>(tid) * kScanItems;
+    // thread owns ranks [r0, r0 + kScanItems) inside its warp's contiguous 256-rank chunk
+    const long r0 = static_cast<long>(bid) * kScanTile + warp * kWarpRanks + lane * kScanItems;
     uint32_t v[kScanItems];
+    uint32_t g[kScanItems];
     uint32_t local = 0;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
-        long idx = base + i;
-        v[i] = idx < n ? touched[order[idx]] : 0u;
+        const long r = r0 + i;
+        g[i] = r < n ? order[r] : 0u;
+        v[i] = r < n ? touched[g[i]] : 0u;
         local += v[i];
     }
-    // block exclusive scan of per-thread sums
-    uint32_t inc = local;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        uint32_t t = __shfl_up_sync(0xffffffffu, inc, off);
-        if (lane >= off) inc += t;
-    }
-    if (lane == 31) s_warp[warp] = inc;
+    uint32_t agg;
+    const uint32_t thread_excl = block_exclusive_scan(local, s_scan, &agg);
+    if (tid == 0) s_excl = lookback(status, bid, 1, 0, agg);
     __syncthreads();
-    if (warp == 0) {
-        uint32_t w = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
-        uint32_t wi = w;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            uint32_t t = __shfl_up_sync(0xffffffffu, wi, off);
-            if (lane >= off) wi += t;
-        }
-        if (lane < kScanThreads / 32) s_warp[lane] = wi - w;
-        if (lane == kScanThreads / 32 - 1) {
-            // block aggregate = wi (inclusive of the last warp); look back
-            const uint32_t agg = wi;
-            uint32_t excl = 0;
-            if (bid == 0) {
-                st_release(status + bid, kFlagPrefix | agg);
-            } else {
-                st_release(status + bid, kFlagAgg | agg);
-                long p = static_cast<long>(bid) - 1;
-                while (true) {
-                    uint32_t s = ld_acquire(status + p);
-                    uint32_t flag = s & ~kCountMask;
-                    if (flag == 0) continue;
-                    excl += s & kCountMask;
-                    if (flag == kFlagPrefix) break;
-                    --p;
-                }
-                st_release(status + bid, kFlagPrefix | (excl + agg));
-            }
-            s_excl = excl;
-            if (static_cast<long>(bid + 1) * kScanTile >= n) *total = excl + agg;
-        }
-    }
-    __syncthreads();
-    uint32_t run = s_excl + s_warp[warp] + (inc - local);
+    const uint32_t block_excl = s_excl;
+    if (static_cast<long>(bid + 1) * kScanTile >= n && tid == 0) *total = block_excl + agg;
+
+    // offsets (block-relative) of this thread's ranks, staged per warp
+    uint32_t run = thread_excl;
+    uint32_t* w_off = s_off + warp * (kWarpRanks + 1);
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
-        long idx = base + i;
-        if (idx < n) out[idx] = run;
+        w_off[lane * kScanItems + i] = run;
+        s_gid[warp * kWarpRanks + lane * kScanItems + i] = g[i];
         run += v[i];
     }
-}
-
-// One thread per depth-sorted Gaussian: writes (tile, gid) for every tile of its rectangle.
-__global__ void __launch_bounds__(256) k_emit(const uint32_t* __restrict__ order, const uint32_t* __restrict__ offsets,
-                                              const uint32_t* __restrict__ touched, const int4* __restrict__ rect,
-                                              int n, int tiles_x, uint32_t* __restrict__ keys,
-                                              uint32_t* __restrict__ vals) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n) return;
-    const uint32_t gid = order[r];
-    const uint32_t cnt = touched[gid];
-    if (cnt == 0) return;
-    const int4 rc = rect[gid];
-    uint32_t o = offsets[r];
-    for (int ty = rc.z; ty <= rc.w; ++ty)
-        for (int k = rc.x; k <= rc.y; ++k) {
-            int tx = ((k % tiles_x) + tiles_x) % tiles_x;
-            keys[o] = static_cast<uint32_t>(ty * tiles_x + tx);
-            vals[o] = gid;
-            ++o;
+    if (lane == 31) w_off[kWarpRanks] = run;  // warp end
+    __syncwarp();
+    const uint32_t w_begin = w_off[0], w_end = w_off[kWarpRanks];
+    for (uint32_t j = w_begin + lane; j < w_end; j += 32) {
+        // owner: last q with w_off[q] <= j (binary search over the warp's 256 offsets)
+        int lo = 0, hi = kWarpRanks - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (w_off[mid] <= j) lo = mid;
+            else hi = mid - 1;
         }
+        const uint32_t gid = s_gid[warp * kWarpRanks + lo];
+        const int4 rc = rect[gid];
+        const uint32_t li = j - w_off[lo];
+        const uint32_t wt = static_cast<uint32_t>(rc.y - rc.x + 1);
+        const uint32_t row = li / wt;
+        int kx = rc.x + static_cast<int>(li - row * wt);
+        kx = kx < 0 ? kx + tiles_x : (kx >= tiles_x ? kx - tiles_x : kx);
+        const uint32_t out = block_excl + j;
+        if (out < capacity) {
+            keys[out] = static_cast<uint32_t>((rc.z + static_cast<int>(row)) * tiles_x + kx);
+            vals[out] = gid;
+        }
+    }
 }
 
 __global__ void k_ranges(const uint32_t* __restrict__ keys, int m, uint2* __restrict__ ranges) {
@@ -257,56 +304,36 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, int m, uint2* __rest
     if (i == m - 1 || keys[i + 1] != k) ranges[k].y = i + 1;
 }
 
-struct RadixWs {
-    uint32_t* hist;     // 8 x 256
-    uint32_t* base;     // 8 x 256
-    uint32_t* counter;  // 8
-    uint32_t* status;   // 8 x blocks x 256
-};
-
-RadixWs carve(void* ws, int n_max) {
-    const int blocks = (n_max + kTileKeys - 1) / kTileKeys;
-    uint32_t* p = static_cast<uint32_t*>(ws);
-    RadixWs r;
-    r.hist = p;
-    r.base = p + 8 * kBins;
-    r.counter = p + 16 * kBins;
-    r.status = p + 16 * kBins + 64;
-    (void)blocks;
-    return r;
+template <typename K>
+constexpr int tile_keys() {
+    return kSortThreads * SortCfg<K>::kItems;
 }
 
+// Workspace: hist[8][256] | base[8][256] | counters[64] | status[passes][blocks][256]
 template <typename K>
 bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n, int bits, void* ws,
                 cudaStream_t s) {
     if (n <= 1) return false;
     const int passes = (bits + kRadixBits - 1) / kRadixBits;
-    const int blocks = (n + kTileKeys - 1) / kTileKeys;
-    RadixWs w = carve(ws, n);
+    const int blocks = (n + tile_keys<K>() - 1) / tile_keys<K>();
+    uint32_t* hist = static_cast<uint32_t*>(ws);
+    uint32_t* base = hist + kMaxPasses * kBins;
+    uint32_t* counter = base + kMaxPasses * kBins;
+    uint32_t* status = counter + 64;
     const size_t status_words = static_cast<size_t>(passes) * blocks * kBins;
-    OSB_CUDA_CHECK(cudaMemsetAsync(w.hist, 0, sizeof(uint32_t) * (16 * kBins + 64), s));
-    OSB_CUDA_CHECK(cudaMemsetAsync(w.status, 0, sizeof(uint32_t) * status_words, s));
-    const int hblocks = blocks < 1184 ? blocks : 1184;
-    k_histogram<K><<<hblocks, 256, 0, s>>>(keys_in, n, passes, w.hist);
-    k_scan_hist<<<passes, kBins, 0, s>>>(w.hist, w.base);
+    OSB_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (2 * kMaxPasses * kBins + 64 + status_words), s));
+    const int hblocks = blocks < 148 * 4 ? blocks : 148 * 4;
+    k_histogram<K><<<hblocks, 256, 0, s>>>(keys_in, n, passes, hist);
+    k_scan_hist<<<passes, kBins, 0, s>>>(hist, base);
     OSB_LAUNCHED(2);
-    // Constant digits would be a pure copy; detect them on the host from the histogram.
-    std::vector<uint32_t> h(static_cast<size_t>(passes) * kBins);
-    OSB_CUDA_CHECK(cudaMemcpyAsync(h.data(), w.hist, h.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    OSB_CUDA_CHECK(cudaStreamSynchronize(s));
     bool flipped = false;
     for (int p = 0; p < passes; ++p) {
-        bool constant = false;
-        for (int d = 0; d < kBins; ++d)
-            if (h[static_cast<size_t>(p) * kBins + d] == static_cast<uint32_t>(n)) constant = true;
-        if (constant) continue;
         K* ki = flipped ? keys_out : keys_in;
         K* ko = flipped ? keys_in : keys_out;
         uint32_t* vi = flipped ? vals_out : vals_in;
         uint32_t* vo = flipped ? vals_in : vals_out;
-        k_onesweep<K><<<blocks, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, p * kRadixBits, w.base + p * kBins,
-                                                       w.status + static_cast<size_t>(p) * blocks * kBins,
-                                                       w.counter + p);
+        k_onesweep<K><<<blocks, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, p * kRadixBits, base + p * kBins,
+                                                       status + static_cast<size_t>(p) * blocks * kBins, counter + p);
         OSB_LAUNCHED(1);
         flipped = !flipped;
     }
@@ -315,9 +342,10 @@ bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, 
 
 }  // namespace
 
-size_t radix_workspace_bytes(int n_max, int /*key_bytes*/) {
-    const size_t blocks = (static_cast<size_t>(n_max) + kTileKeys - 1) / kTileKeys;
-    return sizeof(uint32_t) * (16 * kBins + 64 + 8 * blocks * kBins) + 256;
+size_t radix_workspace_bytes(int n_max, int key_bytes) {
+    const int tk = key_bytes == 8 ? tile_keys<uint64_t>() : tile_keys<uint32_t>();
+    const size_t blocks = (static_cast<size_t>(n_max) + tk - 1) / tk;
+    return sizeof(uint32_t) * (2 * kMaxPasses * kBins + 64 + kMaxPasses * blocks * kBins) + 256;
 }
 
 bool radix_sort_u64(uint64_t* ki, uint64_t* ko, uint32_t* vi, uint32_t* vo, int n, int bits, void* ws,
@@ -340,8 +368,8 @@ size_t scan_workspace_bytes(int n) {
     return sizeof(uint32_t) * (blocks + 64);
 }
 
-void launch_gather_scan(const uint32_t* touched, const uint32_t* order, uint32_t* offsets, uint32_t* total, int n,
-                        void* ws, cudaStream_t s) {
+void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
+                      uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws, cudaStream_t s) {
     if (n <= 0) {
         OSB_CUDA_CHECK(cudaMemsetAsync(total, 0, sizeof(uint32_t), s));
         return;
@@ -350,14 +378,8 @@ void launch_gather_scan(const uint32_t* touched, const uint32_t* order, uint32_t
     uint32_t* counter = static_cast<uint32_t*>(ws);
     uint32_t* status = counter + 64;
     OSB_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * (blocks + 64), s));
-    k_gather_scan<<<blocks, kScanThreads, 0, s>>>(touched, order, offsets, total, n, status, counter);
-    OSB_LAUNCHED(1);
-}
-
-void launch_emit(const uint32_t* order, const uint32_t* offsets, const uint32_t* touched, const int4* rect, int n,
-                 int tiles_x, uint32_t* keys, uint32_t* vals, cudaStream_t s) {
-    if (n <= 0) return;
-    k_emit<<<(n + 255) / 256, 256, 0, s>>>(order, offsets, touched, rect, n, tiles_x, keys, vals);
+    k_scan_emit<<<blocks, kScanThreads, 0, s>>>(touched, order, rect, n, tiles_x, keys, vals, capacity, total, status,
+                                                 counter);
     OSB_LAUNCHED(1);
 }
 

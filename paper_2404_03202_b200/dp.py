@@ -1,0 +1,100 @@
+"""Multi-view data parallelism for training.
+
+One process per GPU. Every rank holds all N Gaussians, their gradients and Adam moments. A
+training iteration over a batch of B views gives each rank its share of the views; each rank
+accumulates the raw-parameter gradients of its views into its flat FP32 plane buffer (K4b adds,
+never overwrites), the buffers are summed with ONE allreduce (NCCL over NVLink on the GPU box,
+gloo in the CPU tests), and every rank applies the identical fused Adam step, so replicas stay
+bit-identical.
+
+Batch semantics (the reference trains one view per iteration, trainer.cpp:353-381): a batch of B
+views = B reference backward() calls with their gradients summed, followed by one adam_step.
+
+The single-view path has no exchange step and is never split across GPUs ("replicas only").
+"""
+from __future__ import annotations
+
+from typing import Callable, Protocol, Sequence
+
+
+def batch_views(step: int, views_per_step: int, n_views: int) -> list[int]:
+    """The global batch of view ids for iteration `step` (0-based), cycling over the dataset."""
+    return [(step * views_per_step + j) % n_views for j in range(views_per_step)]
+
+
+def views_for_rank(step: int, views_per_step: int, n_views: int, rank: int, world: int) -> list[int]:
+    """This rank's share of the batch: view j of the batch goes to rank j % world."""
+    return batch_views(step, views_per_step, n_views)[rank::world]
+
+
+class ViewEngine(Protocol):
+    def accumulate_view(self, view_id: int) -> float | None: ...
+
+    def grad_tensor(self): ...
+
+    def adam_step(self, iteration: int) -> None: ...
+
+
+class DataParallelTrainer:
+    """Drives ViewEngine replicas: accumulate local views -> allreduce(sum) -> Adam."""
+
+    def __init__(self, engine: ViewEngine, rank: int, world: int, allreduce: Callable | None = None):
+        if world > 1 and allreduce is None:
+            raise ValueError("world > 1 needs an allreduce")
+        self.engine = engine
+        self.rank = rank
+        self.world = world
+        self.allreduce = allreduce
+
+    def step(self, iteration: int, view_ids: Sequence[int]) -> float:
+        loss = 0.0
+        for v in view_ids:
+            out = self.engine.accumulate_view(v)
+            if out is not None:
+                loss += out
+        if self.world > 1:
+            self.allreduce(self.engine.grad_tensor())
+        self.engine.adam_step(iteration)
+        return loss
+
+
+class GpuViewEngine:
+    """ViewEngine over a native.Context: render -> L1 loss -> backward(accumulate) per view on the
+    device; the target images stay resident. Adam zeroes the gradients it consumes."""
+
+    def __init__(self, ctx, poses, targets: dict, width: int, height: int, config, extent: float = 1.0,
+                 mask_bottom_fraction: float = 0.0):
+        import torch
+
+        self.ctx = ctx
+        self.poses = poses
+        self.targets = targets  # view id -> device tensor (3*H*W float32, planar)
+        self.W, self.H = width, height
+        self.config = config
+        self.extent = extent
+        self.mask = mask_bottom_fraction
+        v = ctx.view()
+        self._grads = torch.as_tensor(_CudaArray(v.grads, v.planes * v.stride), device="cuda")
+
+    def accumulate_view(self, view_id: int):
+        fr = self.ctx.render(self.poses[view_id], self.W, self.H)
+        try:
+            _, dimg = self.ctx.l1_loss(fr, self.targets[view_id].data_ptr(), self.mask, want_value=False)
+            self.ctx.backward_device(fr, dimg, accumulate=True)
+        finally:
+            fr.free()
+        return None
+
+    def grad_tensor(self):
+        return self._grads
+
+    def adam_step(self, iteration: int):
+        self.ctx.adam_step(self.config, self.extent, iteration, zero_grad=True)
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a device pointer (zero-copy torch interop)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str = "<f4"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
+                                         "strides": None}

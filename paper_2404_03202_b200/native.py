@@ -104,6 +104,10 @@ def _load():
         "osplat_gpu_l1_loss": (S, [_vp, _vp, _vp, C.c_double, C.POINTER(_vp), _dp]),
         "osplat_gpu_train_view": (S, [_vp, _dp, C.c_int, C.c_int, _vp, C.c_int, C.c_double, _dp]),
         "osplat_gpu_launch_count": (C.c_longlong, []),
+        "osplat_gpu_profile": (S, [_vp, C.c_int, C.c_int]),
+        "osplat_gpu_profile_read": (S, [_vp, _dp, _lp, C.c_int]),
+        "osplat_kernel_name": (C.c_char_p, [C.c_int]),
+        "osplat_frame_work": (S, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -113,6 +117,7 @@ def _load():
 
 
 lib = _load()
+KERNEL_COUNT = 11  # OSPLAT_KERNEL_COUNT
 EXPORTED = ("osplat_version osplat_last_error osplat_set_threads osplat_cloud_load osplat_cloud_save "
             "osplat_cloud_count osplat_cloud_free osplat_config_create osplat_config_set osplat_config_free "
             "osplat_render osplat_image_width osplat_image_height osplat_image_pixels osplat_image_free").split()
@@ -264,6 +269,12 @@ class Frame:
         check(lib.osplat_frame_tiles(self.handle, None, None, None, _p(ranges, _u32p), _p(ids, _u32p)))
         return tx.value, ty.value, ranges, ids[:m.value]
 
+    def work(self):
+        """(forward pairs visited, backward pairs, tile instances) — needs count_work profiling."""
+        f, b, m = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        check(lib.osplat_frame_work(self.handle, C.byref(f), C.byref(b), C.byref(m)))
+        return f.value, b.value, m.value
+
     def device(self) -> FrameView:
         v = FrameView()
         check(lib.osplat_frame_device(self.handle, C.byref(v)))
@@ -346,10 +357,20 @@ class Context:
         or a device pointer (int)."""
         t = transform_of(pose12)
         loss = C.c_double(0.0)
-        ptr = C.c_void_p(gt) if gt_on_device else gt.ctypes.data_as(C.c_void_p)
+        ptr = C.c_void_p(gt) if isinstance(gt, int) else gt.ctypes.data_as(C.c_void_p)
         check(lib.osplat_gpu_train_view(self.handle, _p(t), width, height, ptr, int(gt_on_device), mask,
                                         C.byref(loss)))
         return loss.value
+
+    def profile(self, timing: bool = True, count_work: bool = False):
+        check(lib.osplat_gpu_profile(self.handle, int(timing), int(count_work)))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        """{kernel family: (total ms, launches)} since the last reset (synchronizes)."""
+        ms = np.zeros(KERNEL_COUNT)
+        cnt = np.zeros(KERNEL_COUNT, dtype=np.int64)
+        check(lib.osplat_gpu_profile_read(self.handle, _p(ms), _p(cnt, _lp), int(reset)))
+        return {lib.osplat_kernel_name(i).decode(): (float(ms[i]), int(cnt[i])) for i in range(KERNEL_COUNT)}
 
     def download(self) -> Cloud:
         h = _vp()
