@@ -227,7 +227,11 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    stream = torch.cuda.current_stream()
+    # one dedicated stream for everything: our kernels (the context adopts it), NCCL (torch waits on
+    # the current stream) and the timing events
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     N, W, H, V = args.gaussians, args.width, args.height, args.views_per_gpu
     peaks = load_peaks()
 
@@ -301,13 +305,15 @@ def run_ours(args):
 
     # ---- timed train steps (device time, CUDA events on the launching stream, no profiler)
     launches0 = native.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record(stream)
+    for k in range(args.steps):
         train_step()
-    e1.record(stream)
+        ev[k + 1].record(stream)
     barrier()
-    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    ms_total = max_over_ranks(ev[0].elapsed_time(ev[-1]))
+    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    print(f"[bench] step ms: {['%.2f' % x for x in step_ms]}", file=sys.stderr, flush=True)
     launches = native.launch_count() - launches0
     ms_per_step = ms_total / args.steps
     value = world * V * args.steps / (ms_total / 1e3)
@@ -431,6 +437,7 @@ def run_ours(args):
                 "work": {"fwd_pairs": fwd_pairs, "bwd_pairs": bwd_pairs, "instances": instances},
                 "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
                 "ms_per_step_profiled": ms_profiled / args.steps,
+                "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms), "max": max(step_ms)},
                 "roofline": roof, "rooflines": rooflines, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line), flush=True)

@@ -1,10 +1,12 @@
 // backward.cu — K4a (per-pixel, reverse order) and K4b (per-Gaussian chain rule, FP64).
 //
 // K4a replaces backward() pass 1 + pass 2 (proj/src/gradients.cpp:96-169): same CTA/tile layout
-// as K3, list walked back to front from each pixel's last_contrib, the 9 per-instance
-// accumulators (d_colour 3, d_opacity, d_p 2, d_conic 3) reduced across the warp with shuffles and
-// added with one vector red.global.add.v4.f32 per 4 values. Pair decisions are the forward's
-// (pair.cuh); the 0.99 clamp gate (gradients.cpp:146) has its own FP64 guard.
+// as K3 (warp-compacted entry lists, pair.cuh), list walked back to front from each pixel's
+// last_contrib. The 9 per-entry accumulators (d_colour 3, d_opacity, d_p 2, d_conic 3) of the
+// warp's pixels are combined with a reduce-scatter shuffle tree (12 shuffles instead of 45) and
+// added by one warp-wide red.global.add.f32 (9 lanes, 9 consecutive floats); an entry touched by
+// a single pixel of the warp is added directly by that lane. Pair decisions are the forward's;
+// the 0.99 clamp gate (gradients.cpp:146) has its own FP64 guard.
 //
 // K4b replaces pass 3 (gradients.cpp:173-295): one thread per visible Gaussian, FP64 internals,
 // re-derives t, J, Sigma and the conic with the same device code as K1 and accumulates the raw
@@ -21,20 +23,57 @@ __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
 }
+__device__ __forceinline__ void red_add(float* addr, float a) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
+}
 
-__global__ void __launch_bounds__(kStage) k_backward_pixels(const uint32_t* __restrict__ inst_gid,
-                                                            const uint2* __restrict__ ranges, PreprocessOut pp,
-                                                            int W, int H, int tiles_x, float bg0, float bg1,
-                                                            float bg2, FrameBuffers fb,
-                                                            const float* __restrict__ d_image,
-                                                            float4* __restrict__ acc) {
+// Reduce-scatter of 9 values over the warp. Afterwards the lane pair (l, l^1) holds the full sum
+// of value *idx (or idx = -1 for a padding slot); levels split 9 -> 5 -> 3 -> 2 -> 1.
+__device__ __forceinline__ float warp_reduce9(const float (&v)[9], int lane, int* idx) {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+    float a[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const float lo = v[i];
+        const float hi = i + 5 < 9 ? v[i + 5] : 0.0f;
+        a[i] = (b4 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b4 ? lo : hi, 16);
+    }
+    float c[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float lo = a[i];
+        const float hi = i + 3 < 5 ? a[i + 3] : 0.0f;
+        c[i] = (b3 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b3 ? lo : hi, 8);
+    }
+    float e[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float lo = c[i];
+        const float hi = i + 2 < 3 ? c[i + 2] : 0.0f;
+        e[i] = (b2 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b2 ? lo : hi, 4);
+    }
+    float f = (b1 ? e[1] : e[0]) + __shfl_xor_sync(0xffffffffu, b1 ? e[0] : e[1], 2);
+    f += __shfl_xor_sync(0xffffffffu, f, 1);
+    const int i2 = (b2 ? 2 : 0) + (b1 ? 1 : 0);
+    const int i1 = (b3 ? 3 : 0) + i2;
+    const bool pad = (b2 && b1) || (b3 && i2 == 2) || (b4 && i1 == 4);
+    *idx = pad ? -1 : (b4 ? 5 : 0) + i1;
+    return f;
+}
+
+__global__ void __launch_bounds__(kStage, 3) k_backward_pixels(const uint32_t* __restrict__ inst_gid,
+                                                               const uint2* __restrict__ ranges, PreprocessOut pp,
+                                                               int W, int H, int tiles_x, float bg0, float bg1,
+                                                               float bg2, FrameBuffers fb,
+                                                               const float* __restrict__ d_image,
+                                                               float4* __restrict__ acc) {
     __shared__ StageSmem sm;
     __shared__ int s_max_last;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
     const int px = tx * kTile + lx, py = ty * kTile + ly;
-    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool inside = px < W && py < H;
     const uint2 range = ranges[tile];
     const double width = W;
@@ -67,12 +106,13 @@ __global__ void __launch_bounds__(kStage) k_backward_pixels(const uint32_t* __re
         const int cnt = hi - lo;
         __syncthreads();
         if (threadIdx.x < cnt)
-            stage_splat(sm, threadIdx.x, inst_gid[range.x + lo + threadIdx.x], pp.pxy, pp.splat, pp.delta, xc, yc,
-                        width);
+            stage_splat(sm, threadIdx.x, inst_gid[range.x + lo + threadIdx.x], pp.pxy, pp.splat, xc, yc, width);
         __syncthreads();
-        for (int j = cnt - 1; j >= 0; --j) {
+        const int n_act = compact_for_warp(sm, cnt, warp, lane);
+        for (int t = n_act - 1; t >= 0; --t) {
+            const int j = sm.list[warp][t];
             const int k = lo + j;
-            float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f, v5 = 0.f, v6 = 0.f, v7 = 0.f, v8 = 0.f;
+            float v[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             bool has = false;
             if (k < last) {
                 const float4 A = sm.a[j];
@@ -109,9 +149,9 @@ __global__ void __launch_bounds__(kStage) k_backward_pixels(const uint32_t* __re
                         const float inv = __fdividef(1.0f, one_m);
                         T_acc = T_acc * inv;
                         const float wb = alpha * T_acc;
-                        v0 = dl0 * wb;
-                        v1 = dl1 * wb;
-                        v2 = dl2 * wb;
+                        v[0] = dl0 * wb;
+                        v[1] = dl1 * wb;
+                        v[2] = dl2 * wb;
                         const float oml = 1.0f - last_a;
                         s0 = __fmaf_rn(lc0, last_a, s0 * oml);
                         s1 = __fmaf_rn(lc1, last_a, s1 * oml);
@@ -123,74 +163,36 @@ __global__ void __launch_bounds__(kStage) k_backward_pixels(const uint32_t* __re
                         lc0 = Cc.x; lc1 = Cc.y; lc2 = Cc.z;
                         last_a = alpha;
                         if (gate) {
-                            v3 = g * d_alpha;
+                            v[3] = g * d_alpha;
                             const float d_power = -g * Cc.w * d_alpha;
                             const float qx = __fmaf_rn(2.0f * A.z, dx, B.x * dy);
                             const float qy = __fmaf_rn(B.x, dx, 2.0f * A.w * dy);
-                            v4 = d_power * qx;
-                            v5 = d_power * qy;
+                            v[4] = d_power * qx;
+                            v[5] = d_power * qy;
                             const float hp = 0.5f * d_power;
-                            v6 = hp * dx * dx;
-                            v7 = d_power * dx * dy;
-                            v8 = hp * dy * dy;
+                            v[6] = hp * dx * dx;
+                            v[7] = d_power * dx * dy;
+                            v[8] = hp * dy * dy;
                         }
                     }
                 }
             }
-            if (__any_sync(0xffffffffu, has)) {
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) {
-                    v0 += __shfl_down_sync(0xffffffffu, v0, off);
-                    v1 += __shfl_down_sync(0xffffffffu, v1, off);
-                    v2 += __shfl_down_sync(0xffffffffu, v2, off);
-                    v3 += __shfl_down_sync(0xffffffffu, v3, off);
-                    v4 += __shfl_down_sync(0xffffffffu, v4, off);
-                    v5 += __shfl_down_sync(0xffffffffu, v5, off);
-                    v6 += __shfl_down_sync(0xffffffffu, v6, off);
-                    v7 += __shfl_down_sync(0xffffffffu, v7, off);
-                    v8 += __shfl_down_sync(0xffffffffu, v8, off);
+            const uint32_t bal = __ballot_sync(0xffffffffu, has);
+            if (bal == 0u) continue;
+            float* a = reinterpret_cast<float*>(acc + 3 * static_cast<size_t>(sm.gid[j]));
+            if ((bal & (bal - 1u)) == 0u) {
+                if (has) {
+                    red_add_v4(reinterpret_cast<float4*>(a), v[0], v[1], v[2], v[3]);
+                    red_add_v4(reinterpret_cast<float4*>(a) + 1, v[4], v[5], v[6], v[7]);
+                    red_add(a + 8, v[8]);
                 }
-                if (lane == 0) {
-                    float4* a = acc + 3 * static_cast<size_t>(sm.gid[j]);
-                    red_add_v4(a, v0, v1, v2, v3);
-                    red_add_v4(a + 1, v4, v5, v6, v7);
-                    red_add_v4(a + 2, v8, 0.f, 0.f, 0.f);
-                }
+            } else {
+                int idx;
+                const float s = warp_reduce9(v, lane, &idx);
+                if (idx >= 0 && !(lane & 1)) red_add(a + idx, s);
             }
         }
     }
-}
-
-// Real SH basis gradients w.r.t. the direction (scene.cpp:69-92); g is 16 x 3.
-__device__ __forceinline__ void sh_basis_grad(const double* d, int degree, double* b, double* g) {
-    constexpr double C1 = 0.4886025119029199;
-    constexpr double C20 = 1.0925484305920792, C21 = -1.0925484305920792, C22 = 0.31539156525252005,
-                     C23 = -1.0925484305920792, C24 = 0.5462742152960396;
-    constexpr double C30 = -0.5900435899266435, C31 = 2.890611442640554, C32 = -0.4570457994644658,
-                     C33 = 0.3731763325901154, C34 = -0.4570457994644658, C35 = 1.445305721320277,
-                     C36 = -0.5900435899266435;
-    sh_basis(d, degree, b);
-    g[0] = 0.0; g[1] = 0.0; g[2] = 0.0;
-    if (degree < 1) return;
-    const double x = d[0], y = d[1], z = d[2];
-    g[3] = 0.0; g[4] = -C1; g[5] = 0.0;
-    g[6] = 0.0; g[7] = 0.0; g[8] = C1;
-    g[9] = -C1; g[10] = 0.0; g[11] = 0.0;
-    if (degree < 2) return;
-    const double xx = x * x, yy = y * y, zz = z * z;
-    g[12] = C20 * y; g[13] = C20 * x; g[14] = 0.0;
-    g[15] = 0.0; g[16] = C21 * z; g[17] = C21 * y;
-    g[18] = -2.0 * C22 * x; g[19] = -2.0 * C22 * y; g[20] = 4.0 * C22 * z;
-    g[21] = C23 * z; g[22] = 0.0; g[23] = C23 * x;
-    g[24] = 2.0 * C24 * x; g[25] = -2.0 * C24 * y; g[26] = 0.0;
-    if (degree < 3) return;
-    g[27] = C30 * 6.0 * x * y; g[28] = C30 * (3.0 * xx - 3.0 * yy); g[29] = 0.0;
-    g[30] = C31 * y * z; g[31] = C31 * x * z; g[32] = C31 * x * y;
-    g[33] = -2.0 * C32 * x * y; g[34] = C32 * (4.0 * zz - xx - 3.0 * yy); g[35] = 8.0 * C32 * y * z;
-    g[36] = -6.0 * C33 * x * z; g[37] = -6.0 * C33 * y * z; g[38] = C33 * (6.0 * zz - 3.0 * xx - 3.0 * yy);
-    g[39] = C34 * (4.0 * zz - 3.0 * xx - yy); g[40] = -2.0 * C34 * x * y; g[41] = 8.0 * C34 * x * z;
-    g[42] = 2.0 * C35 * x * z; g[43] = -2.0 * C35 * y * z; g[44] = C35 * (xx - yy);
-    g[45] = C36 * (3.0 * xx - 3.0 * yy); g[46] = -6.0 * C36 * x * y; g[47] = 0.0;
 }
 
 __device__ __forceinline__ void add_grad(float* __restrict__ G, int stride, int plane, int gid, double v) {
@@ -198,24 +200,81 @@ __device__ __forceinline__ void add_grad(float* __restrict__ G, int stride, int 
     *p = *p + static_cast<float>(v);
 }
 
+// One SH basis function of the backward (gradients.cpp:202-207): d_sh_i = dl_color * b_i and
+// d_dir += db_i * (c_i . dl_color), with b_i / db_i from scene.cpp:45-92.
+struct ShBack {
+    const float* P;
+    float* G;
+    int stride, gid;
+    Planes pl;
+    double dlc[3];
+    double dd[3];
+    __device__ __forceinline__ void basis(int i, double b, double gx, double gy, double gz) {
+        const double c0 = load_param(P, stride, pl.sh(i, 0), gid);
+        const double c1 = load_param(P, stride, pl.sh(i, 1), gid);
+        const double c2 = load_param(P, stride, pl.sh(i, 2), gid);
+        add_grad(G, stride, pl.sh(i, 0), gid, dlc[0] * b);
+        add_grad(G, stride, pl.sh(i, 1), gid, dlc[1] * b);
+        add_grad(G, stride, pl.sh(i, 2), gid, dlc[2] * b);
+        const double cdot = c0 * dlc[0] + c1 * dlc[1] + c2 * dlc[2];
+        dd[0] += gx * cdot;
+        dd[1] += gy * cdot;
+        dd[2] += gz * cdot;
+    }
+};
+
+template <int DEG>
+__device__ __forceinline__ void sh_backward(ShBack& s, const double* d) {
+    constexpr double C1 = 0.4886025119029199;
+    constexpr double C20 = 1.0925484305920792, C21 = -1.0925484305920792, C22 = 0.31539156525252005,
+                     C23 = -1.0925484305920792, C24 = 0.5462742152960396;
+    constexpr double C30 = -0.5900435899266435, C31 = 2.890611442640554, C32 = -0.4570457994644658,
+                     C33 = 0.3731763325901154, C34 = -0.4570457994644658, C35 = 1.445305721320277,
+                     C36 = -0.5900435899266435;
+    const double x = d[0], y = d[1], z = d[2];
+    s.basis(0, kShC0, 0.0, 0.0, 0.0);
+    if (DEG < 1) return;
+    s.basis(1, -C1 * y, 0.0, -C1, 0.0);
+    s.basis(2, C1 * z, 0.0, 0.0, C1);
+    s.basis(3, -C1 * x, -C1, 0.0, 0.0);
+    if (DEG < 2) return;
+    const double xx = x * x, yy = y * y, zz = z * z;
+    s.basis(4, C20 * x * y, C20 * y, C20 * x, 0.0);
+    s.basis(5, C21 * y * z, 0.0, C21 * z, C21 * y);
+    s.basis(6, C22 * (2.0 * zz - xx - yy), -2.0 * C22 * x, -2.0 * C22 * y, 4.0 * C22 * z);
+    s.basis(7, C23 * x * z, C23 * z, 0.0, C23 * x);
+    s.basis(8, C24 * (xx - yy), 2.0 * C24 * x, -2.0 * C24 * y, 0.0);
+    if (DEG < 3) return;
+    s.basis(9, C30 * y * (3.0 * xx - yy), C30 * 6.0 * x * y, C30 * (3.0 * xx - 3.0 * yy), 0.0);
+    s.basis(10, C31 * x * y * z, C31 * y * z, C31 * x * z, C31 * x * y);
+    s.basis(11, C32 * y * (4.0 * zz - xx - yy), -2.0 * C32 * x * y, C32 * (4.0 * zz - xx - 3.0 * yy),
+            8.0 * C32 * y * z);
+    s.basis(12, C33 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy), -6.0 * C33 * x * z, -6.0 * C33 * y * z,
+            C33 * (6.0 * zz - 3.0 * xx - 3.0 * yy));
+    s.basis(13, C34 * x * (4.0 * zz - xx - yy), C34 * (4.0 * zz - 3.0 * xx - yy), -2.0 * C34 * x * y,
+            8.0 * C34 * x * z);
+    s.basis(14, C35 * z * (xx - yy), 2.0 * C35 * x * z, -2.0 * C35 * y * z, C35 * (xx - yy));
+    s.basis(15, C36 * x * (xx - 3.0 * yy), C36 * (3.0 * xx - 3.0 * yy), -6.0 * C36 * x * y, 0.0);
+}
+
+// K4b. Uses K1's FP64 conic and opacity (conic_o) and its pre-clamp colour sign bits instead of
+// re-deriving them; re-derives t, J, W-rotated J, Sigma3 and the rotation with K1's device code.
+template <int DEG>
 __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restrict__ P, int n, int stride, int bc,
-                                                            int active_degree, Pose pose, int W, int H,
+                                                            Pose pose, int W, int H,
                                                             const uint64_t* __restrict__ depth_key,
+                                                            const double4* __restrict__ conic_o,
+                                                            const Splat32* __restrict__ splat,
                                                             const float4* __restrict__ acc, float* __restrict__ G,
                                                             ScreenStats st) {
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= n || depth_key[gid] == ~0ull) return;
     const Planes pl{bc};
-    Proj64 pr;
-    project64(P, stride, pl, gid, pose, W, H, pr);  // visible by construction (same code as K1)
 
     const float4 a0 = acc[3 * static_cast<size_t>(gid)];
     const float4 a1 = acc[3 * static_cast<size_t>(gid) + 1];
     const float4 a2 = acc[3 * static_cast<size_t>(gid) + 2];
-    const double d_color[3] = {a0.x, a0.y, a0.z};
-    const double d_opacity = a0.w;
     const double d_p[2] = {a1.x, a1.y};
-    const double dca_in = a1.z, dcb_in = a1.w, dcc_in = a2.x;
 
     // screen-space gradient and densification statistics (gradients.cpp:180-183)
     const double ds0 = d_p[0] * W * 0.5, ds1 = d_p[1] * H * 0.5;
@@ -224,58 +283,64 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
     st.hits[gid] += 1;
 
     // opacity through the sigmoid (gradients.cpp:186-187)
-    const double o = pr.o;
-    add_grad(G, stride, pl.opacity(), gid, d_opacity * o * (1.0 - o));
+    const double4 co = conic_o[gid];
+    const double o = co.w;
+    add_grad(G, stride, pl.opacity(), gid, static_cast<double>(a0.w) * o * (1.0 - o));
 
-    // colour: SH coefficients and the view-direction path (gradients.cpp:190-209)
-    double dir[3];
-    view_dir(pose, pr.t, pr.t_r, dir);
-    double basis[16], dbasis[48];
-    sh_basis_grad(dir, active_degree, basis, dbasis);
-    const int active_n = (active_degree + 1) * (active_degree + 1);
-    double raw[3] = {0.5, 0.5, 0.5};
-    for (int i = 0; i < active_n; ++i)
-        for (int c = 0; c < 3; ++c) raw[c] += load_param(P, stride, pl.sh(i, c), gid) * basis[i];
-    double dlc[3];
-    for (int c = 0; c < 3; ++c) dlc[c] = raw[c] < 0.0 ? 0.0 : d_color[c];
-    double d_dir[3] = {0.0, 0.0, 0.0};
-    for (int i = 0; i < active_n; ++i) {
-        double co[3];
-        for (int c = 0; c < 3; ++c) {
-            co[c] = load_param(P, stride, pl.sh(i, c), gid);
-            add_grad(G, stride, pl.sh(i, c), gid, dlc[c] * basis[i]);
-        }
-        const double cdot = co[0] * dlc[0] + co[1] * dlc[1] + co[2] * dlc[2];
-        for (int c = 0; c < 3; ++c) d_dir[c] += dbasis[3 * i + c] * cdot;
-    }
-    const double dd = dot3(dir, d_dir);
+    // camera-space centre (camera.cpp:21-23)
+    double m[3] = {load_param(P, stride, 0, gid), load_param(P, stride, 1, gid), load_param(P, stride, 2, gid)};
+    double t[3], t_r;
+    world_to_camera(pose, m, t, &t_r);
+
+    // colour: SH coefficients and the view-direction path (gradients.cpp:190-209); the
+    // pre-clamp sign gate (:197-200) comes from K1 (same basis, same summation order)
     double d_m_sh[3];
-    for (int c = 0; c < 3; ++c) d_m_sh[c] = (d_dir[c] - dir[c] * dd) * (1.0 / pr.t_r);
+    {
+        const uint32_t neg = __float_as_uint(splat[gid].pad);
+        ShBack sb{P, G, stride, gid, pl,
+                  {(neg & 1u) ? 0.0 : static_cast<double>(a0.x), (neg & 2u) ? 0.0 : static_cast<double>(a0.y),
+                   (neg & 4u) ? 0.0 : static_cast<double>(a0.z)},
+                  {0.0, 0.0, 0.0}};
+        double dir[3];
+        view_dir(pose, t, t_r, dir);
+        sh_backward<DEG>(sb, dir);
+        const double dd = dot3(dir, sb.dd);
+        for (int c = 0; c < 3; ++c) d_m_sh[c] = (sb.dd[c] - dir[c] * dd) * (1.0 / t_r);
+    }
 
     // mean path: dL/dt = J^T dL/dp (gradients.cpp:212-213)
-    const double* jac = pr.jac;
+    double jac[6];
+    jacobian_equirect(t, t_r, W, H, jac);
     double d_t[3] = {jac[0] * d_p[0] + jac[3] * d_p[1], jac[1] * d_p[0] + jac[4] * d_p[1],
                      jac[2] * d_p[0] + jac[5] * d_p[1]};
 
     // covariance path (gradients.cpp:216-254)
-    const double qa = pr.conic[0], qb = pr.conic[1], qc = pr.conic[2];
-    const double da = dca_in, db = 0.5 * dcb_in, dc = dcc_in;
+    const double qa = co.x, qb = co.y, qc = co.z;
+    const double da = a1.z, db = 0.5 * static_cast<double>(a1.w), dc = a2.x;
     const double m00 = qa * da + qb * db, m01 = qa * db + qb * dc;
     const double m10 = qb * da + qc * db, m11 = qb * db + qc * dc;
     const double dva = -(m00 * qa + m01 * qb);
     const double dvb = -(m00 * qb + m01 * qc);
     const double dvc = -(m10 * qb + m11 * qc);
-    const double* m0 = pr.m23;
-    const double* m1 = pr.m23 + 3;
+    double m23[6];
+    m23_mul(jac, pose.R, m23);
+    const double* m0 = m23;
+    const double* m1 = m23 + 3;
     double dsig[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
 #pragma unroll
         for (int c = 0; c < 3; ++c)
             dsig[r * 3 + c] = dva * m0[r] * m0[c] + dvb * (m0[r] * m1[c] + m1[r] * m0[c]) + dvc * m1[r] * m1[c];
+    double s[3], q[4], s3[9];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) s[k] = exp(load_param(P, stride, pl.lscale(k), gid));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = load_param(P, stride, pl.rot(k), gid);
+    covariance3d(q, s, s3);
     double sm0[3], sm1[3];
-    m3v(pr.s3, m0, sm0);
-    m3v(pr.s3, m1, sm1);
+    m3v(s3, m0, sm0);
+    m3v(s3, m1, sm1);
     double dm[6];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -290,7 +355,7 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
     double djac[6];
     m23_mul(dm, Rt, djac);
     double jg[18];
-    jacobian_equirect_grad(pr.t, pr.t_r, W, H, jg);
+    jacobian_equirect_grad(t, t_r, W, H, jg);
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
         const double dj = djac[r];
@@ -304,9 +369,8 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
 
     // Sigma3 -> quaternion (through normalisation) and log-scales (gradients.cpp:260-293)
     double qu[4], rot[9];
-    qnormalize(pr.q, qu);
+    qnormalize(q, qu);
     quat_rot(qu, rot);
-    const double* s = pr.s;
     double drot[9];
 #pragma unroll
     for (int r = 0; r < 3; ++r)
@@ -330,9 +394,11 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
         for (int i = 0; i < 9; ++i) v += drot[i] * rg[k][i];
         dqu[k] = v;
     }
-    const double qn = qnorm(pr.q);
+    const double qn = qnorm(q);
     const double qdot = qu[0] * dqu[0] + qu[1] * dqu[1] + qu[2] * dqu[2] + qu[3] * dqu[3];
+#pragma unroll
     for (int k = 0; k < 4; ++k) add_grad(G, stride, pl.rot(k), gid, (dqu[k] - qu[k] * qdot) / qn);
+#pragma unroll
     for (int k = 0; k < 3; ++k) {
         const double rk[3] = {rot[k], rot[3 + k], rot[6 + k]};
         double srk[3];
@@ -355,11 +421,20 @@ void launch_backward_pixels(const uint32_t* inst_gid, const uint2* ranges, const
 }
 
 void launch_backward_gaussians(const float* params, int n, int stride, int bc, int active_degree, const Pose& pose,
-                               int W, int H, const uint64_t* depth_key, const float4* acc, float* grads,
+                               int W, int H, const PreprocessOut& pp, const float4* acc, float* grads,
                                const ScreenStats& st, cudaStream_t s) {
     if (n <= 0) return;
-    k_backward_gaussians<<<(n + 127) / 128, 128, 0, s>>>(params, n, stride, bc, active_degree, pose, W, H, depth_key,
-                                                          acc, grads, st);
+    const int blocks = (n + 127) / 128;
+#define OSB_K4B(D)                                                                                               \
+    k_backward_gaussians<D><<<blocks, 128, 0, s>>>(params, n, stride, bc, pose, W, H, pp.depth_key, pp.conic_o, \
+                                                   pp.splat, acc, grads, st)
+    switch (active_degree) {
+        case 0: OSB_K4B(0); break;
+        case 1: OSB_K4B(1); break;
+        case 2: OSB_K4B(2); break;
+        default: OSB_K4B(3); break;
+    }
+#undef OSB_K4B
     OSB_LAUNCHED(1);
 }
 

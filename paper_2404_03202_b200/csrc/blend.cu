@@ -2,8 +2,10 @@
 //
 // One 256-thread CTA per 16x16 tile, one pixel per thread. The tile list is walked in chunks of
 // 256 entries staged cooperatively into shared memory (FP64 centre -> tile-relative FP32 offsets,
-// seam-wrapped once per (entry, tile)); every thread then reads the chunk with broadcast LDS.128.
-// The CTA leaves the list as soon as all 256 pixels have terminated (__syncthreads_count).
+// seam-wrapped once per (entry, tile)). Each warp (2 pixel rows) then compacts the chunk to the
+// entries whose conservative alpha >= 1/255 extent reaches its rows and walks only those; the
+// dropped pairs are certain skips, so every decision is unchanged. The CTA leaves the list as soon
+// as all 256 pixels have terminated (__syncthreads_count).
 // FP32 fast path + FP64 guard (pair.cuh): power/alpha decisions near a threshold and T near the
 // 1e-4 stop are decided in FP64 exactly like the reference; a T decision inside the band replays
 // the pixel's prefix in FP64 and the pixel continues in FP64 ("exact mode").
@@ -14,13 +16,14 @@ namespace osb {
 
 namespace {
 
-__global__ void __launch_bounds__(kStage) k_blend(const uint32_t* __restrict__ inst_gid, const uint2* __restrict__ ranges,
-                                                  PreprocessOut pp, int W, int H, int tiles_x, float bg0, float bg1,
-                                                  float bg2, FrameBuffers fb) {
+__global__ void __launch_bounds__(kStage, 3) k_blend(const uint32_t* __restrict__ inst_gid,
+                                                     const uint2* __restrict__ ranges, PreprocessOut pp, int W, int H,
+                                                     int tiles_x, float bg0, float bg1, float bg2, FrameBuffers fb) {
     __shared__ StageSmem sm;
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int px = tx * kTile + lx, py = ty * kTile + ly;
     const bool inside = px < W && py < H;
     const uint2 range = ranges[tile];
@@ -39,10 +42,12 @@ __global__ void __launch_bounds__(kStage) k_blend(const uint32_t* __restrict__ i
     for (uint32_t base = range.x; base < range.y; base += kStage) {
         __syncthreads();
         const uint32_t idx = base + threadIdx.x;
-        if (idx < range.y) stage_splat(sm, threadIdx.x, inst_gid[idx], pp.pxy, pp.splat, pp.delta, xc, yc, width);
+        if (idx < range.y) stage_splat(sm, threadIdx.x, inst_gid[idx], pp.pxy, pp.splat, xc, yc, width);
         if (__syncthreads_count(done) == kStage) break;
         const int cnt = min(kStage, static_cast<int>(range.y - base));
-        for (int j = 0; j < cnt && !done; ++j) {
+        const int n_act = compact_for_warp(sm, cnt, warp, lane);
+        for (int t = 0; t < n_act && !done; ++t) {
+            const int j = sm.list[warp][t];
             const float4 A = sm.a[j];
             const float4 B = sm.b[j];
             float dx, dy, power;

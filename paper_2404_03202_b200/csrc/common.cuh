@@ -48,10 +48,13 @@ struct Pose {
     double t[3];
 };
 
-// Per-Gaussian blend record (FP32, 32 B) staged into shared memory by K3/K4a.
+// Per-Gaussian blend record (FP32, 48 B) staged into shared memory by K3/K4a.
 struct __align__(16) Splat32 {
     float ha, b, hc, o;          // 0.5*conic.a, conic.b, 0.5*conic.c, opacity
     float r, g, bl, pthr;        // SH colour, ln(255 * o)
+    float dl, ext_x, ext_y, pad; // power guard band; half-extents (px) of the region where the
+                                 // FP32 power can be <= pthr + dl (conservative, for culling);
+                                 // pad = bits of "pre-clamp colour < 0" per channel (for K4b)
 };
 
 // ---------------------------------------------------------------- FP64 helpers (vecmath.hpp)

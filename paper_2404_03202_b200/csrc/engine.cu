@@ -50,7 +50,6 @@ PreprocessOut Frame::pp() const {
     o.pxy = pxy.as<double2>();
     o.conic_o = conic_o.as<double4>();
     o.splat = splat.as<Splat32>();
-    o.delta = delta.as<float>();
     return o;
 }
 
@@ -257,7 +256,6 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
         f->pxy.ensure(n * 16);
         f->conic_o.ensure(n * 32);
         f->splat.ensure(n * sizeof(Splat32));
-        f->delta.ensure(n * 4);
         for (int k = 0; k < 2; ++k) {
             f->okeys[k].ensure(n * 8);
             f->ovals[k].ensure(n * 4);
@@ -370,7 +368,7 @@ void Engine::backward(const Frame* f, const float* d_image, bool accumulate) {
         Span sp(*this, kBwdGauss);
         launch_backward_gaussians(params_.as<float>(), f->n, static_cast<int>(stride_),
                                   (sh_degree_ + 1) * (sh_degree_ + 1), f->active_degree, f->pose, f->W, f->H,
-                                  pp.depth_key, acc_.as<float4>(), grads_.as<float>(), st, stream_);
+                                  pp, acc_.as<float4>(), grads_.as<float>(), st, stream_);
     }
 }
 

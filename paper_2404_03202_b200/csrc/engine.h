@@ -57,7 +57,7 @@ struct Frame {
     float bg[3] = {0, 0, 0};
     bool inst_in_alt = false;  // sorted instance gids live in inst_vals[1]
     // per Gaussian (K1 outputs)
-    DevBuf depth_key, touched, rect, pxy, conic_o, splat, delta;
+    DevBuf depth_key, touched, rect, pxy, conic_o, splat;
     // depth sort
     DevBuf okeys[2], ovals[2], offsets, total;
     // instances

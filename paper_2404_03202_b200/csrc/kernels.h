@@ -19,8 +19,7 @@ struct PreprocessOut {
     int4* rect;            // N: {tx0, tx1, ty0, ty1} (tx may wrap)
     double2* pxy;          // N: FP64 pixel centre
     double4* conic_o;      // N: FP64 conic a, b, c and opacity
-    Splat32* splat;        // N: FP32 blend record
-    float* delta;          // N: FP32 power guard band
+    Splat32* splat;        // N: FP32 blend record (conic, opacity, colour, guard band, extents)
 };
 void launch_preprocess(const float* params, int n, int stride, int bc, int active_degree, const Pose& pose,
                        int W, int H, const PreprocessOut& out, cudaStream_t s);
@@ -65,7 +64,7 @@ struct ScreenStats {
     int* hits;              // N (accumulated)
 };
 void launch_backward_gaussians(const float* params, int n, int stride, int bc, int active_degree,
-                               const Pose& pose, int W, int H, const uint64_t* depth_key, const float4* acc,
+                               const Pose& pose, int W, int H, const PreprocessOut& pp, const float4* acc,
                                float* grads, const ScreenStats& st, cudaStream_t s);
 
 // ---- K5 Adam + loss (adam.cu) ---------------------------------------------------------------

@@ -12,9 +12,10 @@ namespace osb {
 
 namespace {
 
-__global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P, int n, int stride, int bc,
-                                                    int active_degree, Pose pose, int W, int H,
-                                                    PreprocessOut out) {
+template <int DEG>
+__global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P, int n, int stride, int bc, Pose pose,
+                                                    int W, int H, PreprocessOut out) {
+    constexpr int active_degree = DEG;  // compile-time: the SH loop unrolls into registers
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= n) return;
     const Planes pl{bc};
@@ -30,13 +31,19 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
     view_dir(pose, pr.t, pr.t_r, dir);
     double basis[16];
     sh_basis(dir, active_degree, basis);
-    const int nb = (active_degree + 1) * (active_degree + 1);
+    constexpr int nb = (active_degree + 1) * (active_degree + 1);
     double col[3] = {0.0, 0.0, 0.0};
+    double raw_b[3] = {0.5, 0.5, 0.5};  // backward's pre-clamp sum order (gradients.cpp:197-198)
+#pragma unroll
     for (int k = 0; k < nb; ++k) {
-        col[0] += load_param(P, stride, pl.sh(k, 0), gid) * basis[k];
-        col[1] += load_param(P, stride, pl.sh(k, 1), gid) * basis[k];
-        col[2] += load_param(P, stride, pl.sh(k, 2), gid) * basis[k];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double term = load_param(P, stride, pl.sh(k, c), gid) * basis[k];
+            col[c] += term;
+            raw_b[c] += term;
+        }
     }
+    const uint32_t neg_bits = (raw_b[0] < 0.0 ? 1u : 0u) | (raw_b[1] < 0.0 ? 2u : 0u) | (raw_b[2] < 0.0 ? 4u : 0u);
     col[0] += 0.5; col[1] += 0.5; col[2] += 0.5;
     col[0] = col[0] > 0.0 ? col[0] : 0.0;
     col[1] = col[1] > 0.0 ? col[1] : 0.0;
@@ -91,8 +98,17 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
     s.g = static_cast<float>(col[1]);
     s.bl = static_cast<float>(col[2]);
     s.pthr = static_cast<float>(pthr);
+    s.dl = static_cast<float>(delta);
+    // Bounding box of {d : 0.5 d^T Q d <= P} is |dx| <= sqrt(2 P cov_a), |dy| <= sqrt(2 P cov_c)
+    // (cov = Q^-1). With P = pthr + 3 delta (+ slack) every pixel outside has FP32 power
+    // > pthr + delta, i.e. a certain skip, so culling by these extents preserves every decision.
+    const double Pext = (pthr + 3.0 * delta) * (1.0 + 1e-4) + 1e-3;
+    const double ex = sqrt(2.0 * Pext * (a > 0.0 ? a : 0.0)) * (1.0 + 1e-5) + 0.02;
+    const double ey = sqrt(2.0 * Pext * (c > 0.0 ? c : 0.0)) * (1.0 + 1e-5) + 0.02;
+    s.ext_x = ex < 1e30 ? static_cast<float>(ex) : 1e30f;
+    s.ext_y = ey < 1e30 ? static_cast<float>(ey) : 1e30f;
+    s.pad = __uint_as_float(neg_bits);  // K4b's colour-clamp gate
     out.splat[gid] = s;
-    out.delta[gid] = static_cast<float>(delta);
 }
 
 }  // namespace
@@ -100,7 +116,13 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
 void launch_preprocess(const float* params, int n, int stride, int bc, int active_degree, const Pose& pose,
                        int W, int H, const PreprocessOut& out, cudaStream_t s) {
     if (n <= 0) return;
-    k_preprocess<<<(n + 255) / 256, 256, 0, s>>>(params, n, stride, bc, active_degree, pose, W, H, out);
+    const int blocks = (n + 255) / 256;
+    switch (active_degree) {
+        case 0: k_preprocess<0><<<blocks, 256, 0, s>>>(params, n, stride, bc, pose, W, H, out); break;
+        case 1: k_preprocess<1><<<blocks, 256, 0, s>>>(params, n, stride, bc, pose, W, H, out); break;
+        case 2: k_preprocess<2><<<blocks, 256, 0, s>>>(params, n, stride, bc, pose, W, H, out); break;
+        default: k_preprocess<3><<<blocks, 256, 0, s>>>(params, n, stride, bc, pose, W, H, out); break;
+    }
     OSB_LAUNCHED(1);
 }
 

@@ -76,6 +76,7 @@ __device__ __forceinline__ void jacobian_equirect_grad(const double* t, double t
 
 // project_gaussian (rasterizer.cpp:17-55) minus the SH colour. Returns false when culled
 // (t_r < 0.01, pole-degenerate, opacity < 1/255).
+template <bool kPixel = true>
 __device__ __forceinline__ bool project64(const float* __restrict__ P, int stride, const Planes& pl, int gid,
                                           const Pose& pose, int W, int H, Proj64& pr) {
     double m[3] = {load_param(P, stride, 0, gid), load_param(P, stride, 1, gid), load_param(P, stride, 2, gid)};
@@ -88,15 +89,16 @@ __device__ __forceinline__ bool project64(const float* __restrict__ P, int strid
     pr.o = 1.0 / (1.0 + exp(-logit));
     if (pr.o < kAlphaMin) return false;
 
-    // project_equirect (camera.cpp:25-39)
-    double lon = atan2(t[0], t[2]);
-    if (lon >= kPi) lon -= 2.0 * kPi;
-    double sine = t[1] / pr.t_r;
-    sine = sine < -1.0 ? -1.0 : (sine > 1.0 ? 1.0 : sine);
-    double lat = asin(sine);
-    double sx = lon / kPi, sy = 2.0 * lat / kPi;
-    pr.p[0] = (sx + 1.0) * W * 0.5;
-    pr.p[1] = (sy + 1.0) * H * 0.5;
+    if (kPixel) {  // project_equirect (camera.cpp:25-39); the backward does not need p
+        double lon = atan2(t[0], t[2]);
+        if (lon >= kPi) lon -= 2.0 * kPi;
+        double sine = t[1] / pr.t_r;
+        sine = sine < -1.0 ? -1.0 : (sine > 1.0 ? 1.0 : sine);
+        double lat = asin(sine);
+        double sx = lon / kPi, sy = 2.0 * lat / kPi;
+        pr.p[0] = (sx + 1.0) * W * 0.5;
+        pr.p[1] = (sy + 1.0) * H * 0.5;
+    }
 
     jacobian_equirect(t, pr.t_r, W, H, pr.jac);
     m23_mul(pr.jac, pose.R, pr.m23);

@@ -295,8 +295,13 @@ class Context:
     def __init__(self, cloud: Cloud | HostCloud, device: int = 0, stream: int | None = None):
         hc = cloud if isinstance(cloud, HostCloud) else HostCloud.from_cloud(cloud)
         self.handle = _vp()
-        check(lib.osplat_gpu_create(device, C.c_void_p(stream) if stream else None, hc.handle,
-                                    C.byref(self.handle)))
+        # stream: None -> the library creates its own stream; an int is a cudaStream_t handle, where
+        # 0 (torch's default stream) means the legacy default stream (cudaStreamLegacy = 0x1).
+        if stream is None:
+            s = None
+        else:
+            s = C.c_void_p(stream if stream != 0 else 0x1)
+        check(lib.osplat_gpu_create(device, s, hc.handle, C.byref(self.handle)))
         self.device = device
         v = self.view()
         self.n, self.stride, self.planes, self.sh_degree = v.n, v.stride, v.planes, v.sh_degree

@@ -18,7 +18,8 @@ def main():
     W, H = int(os.environ.get("W", "2048")), int(os.environ.get("H", "1024"))
     steps = int(os.environ.get("STEPS", "3"))
     variant = os.environ.get("VARIANT", "uniform")
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     cloud = scenes.synthetic_cloud(n, seed=1, variant=variant)
     target = scenes.synthetic_cloud(n, seed=2, variant=variant)
     poses = scenes.ring_poses(16, seed=2)

@@ -143,3 +143,24 @@ def test_empty_and_culled_clouds():
     fr = ctx.render(scenes.identity_pose(), 128, 64)
     assert np.all(fr.image() == 0.0)
     assert fr.tiles()[3].size == 0
+
+
+@pytest.mark.parametrize("legacy", [False, True])
+def test_context_adopts_caller_stream(legacy):
+    """Kernels run on the caller's stream (torch events on it bracket them; NCCL ordering)."""
+    import torch
+    s = torch.cuda.default_stream() if legacy else torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx = native.Context(_scene("uniform", 50_000, 2), stream=s.cuda_stream)
+        ctx.profile(timing=True)
+        ctx.render(scenes.identity_pose(), 1024, 512).free()  # warm
+        ctx.profile_read(reset=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(3):
+            ctx.render(scenes.identity_pose(), 1024, 512).free()
+        e1.record(s)
+        torch.cuda.synchronize()
+        kern = sum(v[0] for v in ctx.profile_read().values())
+        assert kern > 0.0
+        assert e0.elapsed_time(e1) >= 0.9 * kern, (e0.elapsed_time(e1), kern)
