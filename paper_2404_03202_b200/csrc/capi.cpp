@@ -752,17 +752,15 @@ osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[1
         Engine& e = *ctx->engine;
         osb::DeviceGuard g(e.device());
         const size_t plane = static_cast<size_t>(width) * height;
-        const float* gt_dev = gt;
-        if (!gt_on_device) {
-            float* buf = e.gt_buffer(plane);
-            OSB_CUDA_CHECK(cudaMemcpyAsync(buf, gt, plane * 12, cudaMemcpyHostToDevice, e.stream()));
-            gt_dev = buf;
-        }
+        // a host target is uploaded on the copy stream while K1-K3 run (overlapped H2D)
+        const float* gt_dev = gt_on_device ? gt : e.upload_target_async(gt, plane);
         const double zero[3] = {0, 0, 0};
         osb::Frame* f = e.render(p12, width, height, zero);
         try {
+            if (!gt_on_device) e.wait_target();
             const double v = e.l1_loss(f, gt_dev, mask, false);
             (void)v;
+            if (!gt_on_device) e.release_target();
             const size_t pixels = plane;
             e.backward(f, e.d_image_buffer(pixels), true);
             if (loss) {

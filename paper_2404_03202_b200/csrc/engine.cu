@@ -144,6 +144,12 @@ Engine::~Engine() {
         cudaEventDestroy(ev.b);
     }
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
+    if (copy_stream_) {
+        cudaStreamSynchronize(copy_stream_);
+        cudaEventDestroy(target_ready_);
+        cudaEventDestroy(target_free_);
+        cudaStreamDestroy(copy_stream_);
+    }
     if (own_stream_) cudaStreamDestroy(stream_);
 }
 
@@ -381,6 +387,29 @@ float* Engine::gt_buffer(size_t pixels) {
     gt_.ensure(pixels * 12);
     return gt_.as<float>();
 }
+
+const float* Engine::upload_target_async(const float* host, size_t pixels) {
+    DeviceGuard g(device_);
+    if (!copy_stream_) {
+        OSB_CUDA_CHECK(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+        OSB_CUDA_CHECK(cudaEventCreateWithFlags(&target_ready_, cudaEventDisableTiming));
+        OSB_CUDA_CHECK(cudaEventCreateWithFlags(&target_free_, cudaEventDisableTiming));
+        OSB_CUDA_CHECK(cudaEventRecord(target_free_, stream_));
+    }
+    if (gt_.capacity() < pixels * 12) {
+        OSB_CUDA_CHECK(cudaStreamSynchronize(copy_stream_));
+        OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    }
+    float* buf = gt_buffer(pixels);
+    OSB_CUDA_CHECK(cudaStreamWaitEvent(copy_stream_, target_free_, 0));  // previous consumer done
+    OSB_CUDA_CHECK(cudaMemcpyAsync(buf, host, pixels * 12, cudaMemcpyHostToDevice, copy_stream_));
+    OSB_CUDA_CHECK(cudaEventRecord(target_ready_, copy_stream_));
+    return buf;
+}
+
+void Engine::wait_target() { OSB_CUDA_CHECK(cudaStreamWaitEvent(stream_, target_ready_, 0)); }
+
+void Engine::release_target() { OSB_CUDA_CHECK(cudaEventRecord(target_free_, stream_)); }
 
 double Engine::l1_loss(const Frame* f, const float* gt, double mask_bottom_fraction, bool want_value) {
     DeviceGuard g(device_);

@@ -114,6 +114,11 @@ public:
     int* hits() const { return hits_.as<int>(); }
     float* d_image_buffer(size_t pixels);
     float* gt_buffer(size_t pixels);
+    // Host target upload on a side stream (overlaps the render): upload -> wait_target() on the
+    // main stream before the first consumer -> release_target() after the last consumer.
+    const float* upload_target_async(const float* host, size_t pixels);
+    void wait_target();
+    void release_target();
 
 private:
     int device_;
@@ -125,6 +130,8 @@ private:
     DevBuf params_, grads_, m_, v_, acc_, d_screen_, norm_sum_, hits_, loss_sum_, d_image_, gt_;
     std::vector<std::unique_ptr<Frame>> pool_;
     std::vector<Frame*> free_;
+    cudaStream_t copy_stream_ = nullptr;
+    cudaEvent_t target_ready_ = nullptr, target_free_ = nullptr;
 
     // profiler
     struct Ev {
