@@ -2,7 +2,7 @@
 """bench.py — "ERP render FPS + fwd/bwd train iters/s, 1M Gaussians at 2048x1024" (BASELINE.json).
 
 One step = one training iteration of the hot path on every GPU: per view, render (K1 preprocess ->
-K2 depth/tile sort -> K3 blend) -> L1 loss -> backward (K4a pixels -> K4b Gaussians, accumulate),
+K2 depth/tile sort -> K3 blend) -> loss (L1 + SSIM, lambda 0.2) -> backward (K4a pixels -> K4b Gaussians, accumulate),
 then the NCCL allreduce of the flat gradient buffer (N > 1) and the fused Adam step (K5).
 Weak scaling: every GPU trains `--views-per-gpu` views of its own per iteration on the replicated
 1M-Gaussian scene; `value` = views trained per second over the whole job (= iterations/s at N=1).
@@ -36,6 +36,7 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (
 # (pixel, splat) pair for K3/K4a; bytes per Gaussian / element for the HBM-bound kernels.
 INSTR_PER_FWD_PAIR = 21
 INSTR_PER_BWD_PAIR = 48
+LAMBDA_SSIM = 0.2  # TrainConfig default (trainer.hpp:20), both arms
 
 
 def parse():
@@ -135,12 +136,12 @@ def dist_env():
 
 
 def cpu_reference_step(oracle, cloud, pose, gt, W, H, cfg, it):
-    """One reference train step (render + L1 loss + backward + adam_step), summing the reference's
+    """One reference train step (render + loss + backward + adam_step), summing the reference's
     own steady-clock times (marshalling excluded)."""
     import pyoracle
     f = oracle.render(cloud, pose, W, H, keep_handle=True)
     t = oracle.last_seconds()
-    _, d = oracle.loss(f.rgb, gt, 0.0, 0.0)
+    _, d = oracle.loss(f.rgb, gt, LAMBDA_SSIM, 0.0)
     t += oracle.last_seconds()
     g = oracle.backward(f, d, cloud, pose)
     t += oracle.last_seconds()
@@ -163,9 +164,10 @@ def reference_oracle():
 
 def workload_config(args, world):
     return {"workload": f"{args.gaussians // 1000}k Gaussians, {args.width}x{args.height} ERP, train step "
-                        f"(render + L1 loss + backward + Adam), {args.views_per_gpu} view/GPU/iter",
+                        f"(render + L1+SSIM loss + backward + Adam), {args.views_per_gpu} view/GPU/iter",
             "gaussians": args.gaussians, "width": args.width, "height": args.height,
             "views_per_gpu_per_step": args.views_per_gpu, "sh_degree": 3, "scene": "synthetic uniform shell, seed 1",
+            "lambda_ssim": LAMBDA_SSIM,
             "parallelism": f"dp{world} (views split, Gaussians replicated, NCCL allreduce)",
             "l2": "inputs larger than L2: params + grads + Adam moments = 4 x 236 MB resident"}
 
@@ -201,7 +203,7 @@ def run_reference_arm(args):
             "config": workload_config(args, 1),
             "cpu_baseline": {"value": value, "unit": "views/s", "cores": cores, "kind": kind,
                              "sample": f"{steps_run} full train step(s) of the workload on the host "
-                                       f"(reference render + L1 loss + backward + adam_step, steady clock)"},
+                                       f"(reference render + loss + backward + adam_step, steady clock)"},
             "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -261,7 +263,7 @@ def run_ours(args):
     extent = 1.0
     it = [0]
     from paper_2404_03202_b200 import dp
-    engine = dp.GpuViewEngine(ctx, poses, gts, W, H, cfg, extent)
+    engine = dp.GpuViewEngine(ctx, poses, gts, W, H, cfg, extent, lambda_ssim=LAMBDA_SSIM)
     trainer = dp.DataParallelTrainer(engine, rank, world, allreduce=(lambda t: dist.all_reduce(t)) if world > 1
                                      else None)
 
@@ -359,7 +361,7 @@ def run_ours(args):
         for _ in range(args.steps):
             it[0] += 1
             for vi in my_views:
-                ctx.train_view(poses[vi], W, H, host_gt[vi].data_ptr(), gt_on_device=False)
+                ctx.train_view(poses[vi], W, H, host_gt[vi].data_ptr(), gt_on_device=False, lambda_ssim=LAMBDA_SSIM)
             if world > 1:
                 dist.all_reduce(grads)
             ctx.adam_step(cfg, extent, it[0], zero_grad=True)
@@ -420,7 +422,7 @@ def run_ours(args):
             secs, _ = cpu_reference_step(oracle, scenes.synthetic_cloud(N, seed=1), poses[my_views[0]], gt_host, W, H,
                                          pyoracle.AdamConfig(iterations=30000), 1)
             cpu = {"value": 1.0 / secs, "unit": "views/s", "cores": cores, "kind": kind,
-                   "sample": "1 full train step of the same workload (reference render + L1 loss + backward + "
+                   "sample": "1 full train step of the same workload (reference render + loss + backward + "
                              "adam_step, steady clock, marshalling excluded)", "seconds": secs}
         except Exception as exc:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "views/s", "cores": os.cpu_count(), "kind": "unavailable",

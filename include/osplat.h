@@ -167,18 +167,23 @@ OSPLAT_API osplat_status osplat_gpu_reset_screen_stats(osplat_gpu* ctx);
 OSPLAT_API osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_config* config, double scene_extent,
                                    long iteration, int zero_grad);
 
-/* L1 term of loss() (trainer.cpp:25-71, lambda_ssim = 0) against a device planar FP32 target:
+/* loss() (trainer.cpp:25-71): (1 - lambda_ssim) L1 + lambda_ssim (1 - SSIM), SSIM 11x11 sigma 1.5
+ * zero-padded (metrics.cpp:17-153), bottom rows masked, against a device planar FP32 target:
  * writes dL/dC into the context's d_image buffer (returned through *d_image_planar) and the
- * loss value (host, synchronizes) into *loss unless loss is NULL. */
+ * loss value (host, synchronizes) into *loss unless loss is NULL. _l1_loss = lambda_ssim 0. */
+OSPLAT_API osplat_status osplat_gpu_loss(osplat_gpu* ctx, const osplat_frame* frame, const float* gt_planar_device,
+                                         double lambda_ssim, double mask_bottom_fraction,
+                                         const float** d_image_planar, double* loss);
 OSPLAT_API osplat_status osplat_gpu_l1_loss(osplat_gpu* ctx, const osplat_frame* frame, const float* gt_planar_device,
                                  double mask_bottom_fraction, const float** d_image_planar, double* loss);
 
-/* One training view: render -> L1 loss -> backward (accumulate) against `gt` (host or device
- * planar FP32, 3*H*W), returning the loss in *loss (host) — the per-view part of
- * Trainer::run (trainer.cpp:360-363). The caller follows with osplat_gpu_adam_step. */
+/* One training view: render -> loss -> backward (accumulate) against `gt` (host or device
+ * planar FP32, 3*H*W; a host target is uploaded on a side stream, overlapped with the render),
+ * returning the loss in *loss (host) — the per-view part of Trainer::run (trainer.cpp:360-363).
+ * The caller follows with osplat_gpu_adam_step. */
 OSPLAT_API osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
-                                    const float* gt_planar, int gt_on_device, double mask_bottom_fraction,
-                                    double* loss);
+                                    const float* gt_planar, int gt_on_device, double lambda_ssim,
+                                    double mask_bottom_fraction, double* loss);
 
 /* Profiling (bench.py roofline evidence). With timing on, every kernel family is bracketed by a
  * CUDA event pair on the context stream; with count_work on, K3 also writes per-pixel visited

@@ -195,13 +195,18 @@ __global__ void __launch_bounds__(kStage, 3) k_backward_pixels(const uint32_t* _
     }
 }
 
-__device__ __forceinline__ void add_grad(float* __restrict__ G, int stride, int plane, int gid, double v) {
+// Gradient plane update: OVERWRITE (the buffer is logically zero: first view after Adam or a
+// non-accumulating backward) stores, otherwise read-modify-write (multi-view accumulation).
+template <bool OVERWRITE>
+__device__ __forceinline__ void put_grad(float* __restrict__ G, int stride, int plane, int gid, double v) {
     float* p = G + static_cast<size_t>(plane) * stride + gid;
-    *p = *p + static_cast<float>(v);
+    if (OVERWRITE) *p = static_cast<float>(v);
+    else *p = *p + static_cast<float>(v);
 }
 
 // One SH basis function of the backward (gradients.cpp:202-207): d_sh_i = dl_color * b_i and
 // d_dir += db_i * (c_i . dl_color), with b_i / db_i from scene.cpp:45-92.
+template <bool OVERWRITE>
 struct ShBack {
     const float* P;
     float* G;
@@ -213,9 +218,9 @@ struct ShBack {
         const double c0 = load_param(P, stride, pl.sh(i, 0), gid);
         const double c1 = load_param(P, stride, pl.sh(i, 1), gid);
         const double c2 = load_param(P, stride, pl.sh(i, 2), gid);
-        add_grad(G, stride, pl.sh(i, 0), gid, dlc[0] * b);
-        add_grad(G, stride, pl.sh(i, 1), gid, dlc[1] * b);
-        add_grad(G, stride, pl.sh(i, 2), gid, dlc[2] * b);
+        put_grad<OVERWRITE>(G, stride, pl.sh(i, 0), gid, dlc[0] * b);
+        put_grad<OVERWRITE>(G, stride, pl.sh(i, 1), gid, dlc[1] * b);
+        put_grad<OVERWRITE>(G, stride, pl.sh(i, 2), gid, dlc[2] * b);
         const double cdot = c0 * dlc[0] + c1 * dlc[1] + c2 * dlc[2];
         dd[0] += gx * cdot;
         dd[1] += gy * cdot;
@@ -223,8 +228,8 @@ struct ShBack {
     }
 };
 
-template <int DEG>
-__device__ __forceinline__ void sh_backward(ShBack& s, const double* d) {
+template <int DEG, bool OVERWRITE>
+__device__ __forceinline__ void sh_backward(ShBack<OVERWRITE>& s, const double* d) {
     constexpr double C1 = 0.4886025119029199;
     constexpr double C20 = 1.0925484305920792, C21 = -1.0925484305920792, C22 = 0.31539156525252005,
                      C23 = -1.0925484305920792, C24 = 0.5462742152960396;
@@ -259,7 +264,7 @@ __device__ __forceinline__ void sh_backward(ShBack& s, const double* d) {
 
 // K4b. Uses K1's FP64 conic and opacity (conic_o) and its pre-clamp colour sign bits instead of
 // re-deriving them; re-derives t, J, W-rotated J, Sigma3 and the rotation with K1's device code.
-template <int DEG>
+template <int DEG, bool OVERWRITE>
 __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restrict__ P, int n, int stride, int bc,
                                                             Pose pose, int W, int H,
                                                             const uint64_t* __restrict__ depth_key,
@@ -268,8 +273,17 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
                                                             const float4* __restrict__ acc, float* __restrict__ G,
                                                             ScreenStats st) {
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= n || depth_key[gid] == ~0ull) return;
+    if (gid >= n) return;
     const Planes pl{bc};
+    if (depth_key[gid] == ~0ull) {  // culled: zero gradient (gradients.cpp:82-86), nothing to add
+        if (OVERWRITE)
+            for (int q = 0; q < pl.count(); ++q) G[static_cast<size_t>(q) * stride + gid] = 0.0f;
+        return;
+    }
+    if (OVERWRITE) {  // SH bands above the active degree carry no gradient (gradients.cpp:202-203)
+        constexpr int active_n = (DEG + 1) * (DEG + 1);
+        for (int q = pl.sh(active_n, 0); q < pl.sh(bc, 0); ++q) G[static_cast<size_t>(q) * stride + gid] = 0.0f;
+    }
 
     const float4 a0 = acc[3 * static_cast<size_t>(gid)];
     const float4 a1 = acc[3 * static_cast<size_t>(gid) + 1];
@@ -285,7 +299,7 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
     // opacity through the sigmoid (gradients.cpp:186-187)
     const double4 co = conic_o[gid];
     const double o = co.w;
-    add_grad(G, stride, pl.opacity(), gid, static_cast<double>(a0.w) * o * (1.0 - o));
+    put_grad<OVERWRITE>(G, stride, pl.opacity(), gid, static_cast<double>(a0.w) * o * (1.0 - o));
 
     // camera-space centre (camera.cpp:21-23)
     double m[3] = {load_param(P, stride, 0, gid), load_param(P, stride, 1, gid), load_param(P, stride, 2, gid)};
@@ -297,13 +311,13 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
     double d_m_sh[3];
     {
         const uint32_t neg = __float_as_uint(splat[gid].pad);
-        ShBack sb{P, G, stride, gid, pl,
+        ShBack<OVERWRITE> sb{P, G, stride, gid, pl,
                   {(neg & 1u) ? 0.0 : static_cast<double>(a0.x), (neg & 2u) ? 0.0 : static_cast<double>(a0.y),
                    (neg & 4u) ? 0.0 : static_cast<double>(a0.z)},
                   {0.0, 0.0, 0.0}};
         double dir[3];
         view_dir(pose, t, t_r, dir);
-        sh_backward<DEG>(sb, dir);
+        sh_backward<DEG, OVERWRITE>(sb, dir);
         const double dd = dot3(dir, sb.dd);
         for (int c = 0; c < 3; ++c) d_m_sh[c] = (sb.dd[c] - dir[c] * dd) * (1.0 / t_r);
     }
@@ -365,7 +379,7 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
     }
     double dpos[3];
     m3tv(pose.R, d_t, dpos);
-    for (int c = 0; c < 3; ++c) add_grad(G, stride, c, gid, dpos[c] + d_m_sh[c]);
+    for (int c = 0; c < 3; ++c) put_grad<OVERWRITE>(G, stride, c, gid, dpos[c] + d_m_sh[c]);
 
     // Sigma3 -> quaternion (through normalisation) and log-scales (gradients.cpp:260-293)
     double qu[4], rot[9];
@@ -397,14 +411,14 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
     const double qn = qnorm(q);
     const double qdot = qu[0] * dqu[0] + qu[1] * dqu[1] + qu[2] * dqu[2] + qu[3] * dqu[3];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) add_grad(G, stride, pl.rot(k), gid, (dqu[k] - qu[k] * qdot) / qn);
+    for (int k = 0; k < 4; ++k) put_grad<OVERWRITE>(G, stride, pl.rot(k), gid, (dqu[k] - qu[k] * qdot) / qn);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const double rk[3] = {rot[k], rot[3 + k], rot[6 + k]};
         double srk[3];
         m3v(dsig, rk, srk);
         const double rr = dot3(rk, srk);
-        add_grad(G, stride, pl.lscale(k), gid, 2.0 * s[k] * rr * s[k]);
+        put_grad<OVERWRITE>(G, stride, pl.lscale(k), gid, 2.0 * s[k] * rr * s[k]);
     }
 }
 
@@ -422,17 +436,21 @@ void launch_backward_pixels(const uint32_t* inst_gid, const uint2* ranges, const
 
 void launch_backward_gaussians(const float* params, int n, int stride, int bc, int active_degree, const Pose& pose,
                                int W, int H, const PreprocessOut& pp, const float4* acc, float* grads,
-                               const ScreenStats& st, cudaStream_t s) {
+                               const ScreenStats& st, bool overwrite, cudaStream_t s) {
     if (n <= 0) return;
     const int blocks = (n + 127) / 128;
-#define OSB_K4B(D)                                                                                               \
-    k_backward_gaussians<D><<<blocks, 128, 0, s>>>(params, n, stride, bc, pose, W, H, pp.depth_key, pp.conic_o, \
-                                                   pp.splat, acc, grads, st)
-    switch (active_degree) {
-        case 0: OSB_K4B(0); break;
-        case 1: OSB_K4B(1); break;
-        case 2: OSB_K4B(2); break;
-        default: OSB_K4B(3); break;
+#define OSB_K4B(D, O)                                                                                               \
+    k_backward_gaussians<D, O><<<blocks, 128, 0, s>>>(params, n, stride, bc, pose, W, H, pp.depth_key, pp.conic_o, \
+                                                      pp.splat, acc, grads, st)
+    switch (active_degree * 2 + (overwrite ? 1 : 0)) {
+        case 0: OSB_K4B(0, false); break;
+        case 1: OSB_K4B(0, true); break;
+        case 2: OSB_K4B(1, false); break;
+        case 3: OSB_K4B(1, true); break;
+        case 4: OSB_K4B(2, false); break;
+        case 5: OSB_K4B(2, true); break;
+        case 6: OSB_K4B(3, false); break;
+        default: OSB_K4B(3, true); break;
     }
 #undef OSB_K4B
     OSB_LAUNCHED(1);

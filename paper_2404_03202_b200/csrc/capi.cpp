@@ -623,6 +623,13 @@ osplat_status osplat_frame_device(const osplat_frame* frame, osplat_frame_view* 
 osplat_status osplat_gpu_view_buffers(osplat_gpu* ctx, osplat_gpu_view* v) {
     if (!ctx || !v) return invalid("osplat_gpu_view_buffers: null argument");
     Engine& e = *ctx->engine;
+    try {
+        osb::DeviceGuard g(e.device());
+        e.materialize_grads();  // the caller may read the gradient planes directly
+    } catch (const std::exception& ex) {
+        t_last_error = ex.what();
+        return OSPLAT_ERR_RUNTIME;
+    }
     v->params = e.params();
     v->grads = e.grads();
     v->adam_m = e.adam_m();
@@ -684,6 +691,7 @@ osplat_status osplat_gpu_gradients(osplat_gpu* ctx, double* d_position, double* 
         const size_t n = e.n(), stride = e.stride();
         const int bc = (e.sh_degree() + 1) * (e.sh_degree() + 1);
         const osb::Planes pl{bc};
+        e.materialize_grads();
         std::vector<float> G(static_cast<size_t>(e.planes()) * stride);
         std::vector<float2> ds(stride);
         std::vector<double> ns(stride);
@@ -728,22 +736,30 @@ osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_config* config,
     return wrap([&] { ctx->engine->adam_step(hyper_from(config), extent, iteration, zero_grad != 0); });
 }
 
-osplat_status osplat_gpu_l1_loss(osplat_gpu* ctx, const osplat_frame* frame, const float* gt, double mask,
-                                 const float** d_image, double* loss) {
-    if (!ctx || !frame || !gt) return invalid("osplat_gpu_l1_loss: null argument");
-    if (mask < 0.0 || mask >= 1.0) return invalid("osplat_gpu_l1_loss: mask_bottom_fraction must be in [0, 1)");
+osplat_status osplat_gpu_loss(osplat_gpu* ctx, const osplat_frame* frame, const float* gt, double lambda_ssim,
+                              double mask, const float** d_image, double* loss) {
+    if (!ctx || !frame || !gt) return invalid("osplat_gpu_loss: null argument");
+    if (mask < 0.0 || mask >= 1.0) return invalid("osplat_gpu_loss: mask_bottom_fraction must be in [0, 1)");
+    if (lambda_ssim < 0.0 || lambda_ssim > 1.0) return invalid("osplat_gpu_loss: lambda_ssim must be in [0, 1]");
     return wrap([&] {
         validate_frame(ctx, frame);
         Engine& e = *ctx->engine;
-        double v = e.l1_loss(frame->frame, gt, mask, loss != nullptr);
+        double v = e.loss(frame->frame, gt, lambda_ssim, mask, loss != nullptr);
         if (loss) *loss = v;
         if (d_image) *d_image = e.d_image_buffer(static_cast<size_t>(frame->frame->W) * frame->frame->H);
     });
 }
 
+osplat_status osplat_gpu_l1_loss(osplat_gpu* ctx, const osplat_frame* frame, const float* gt, double mask,
+                                 const float** d_image, double* loss) {
+    return osplat_gpu_loss(ctx, frame, gt, 0.0, mask, d_image, loss);
+}
+
 osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
-                                    const float* gt, int gt_on_device, double mask, double* loss) {
+                                    const float* gt, int gt_on_device, double lambda_ssim, double mask,
+                                    double* loss) {
     if (!ctx || !transform_cw || !gt) return invalid("osplat_gpu_train_view: null argument");
+    if (lambda_ssim < 0.0 || lambda_ssim > 1.0) return invalid("osplat_gpu_train_view: lambda_ssim must be in [0, 1]");
     if (mask < 0.0 || mask >= 1.0) return invalid("osplat_gpu_train_view: mask_bottom_fraction must be in [0, 1)");
     return wrap([&] {
         check_dims(width, height);
@@ -758,14 +774,14 @@ osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[1
         osb::Frame* f = e.render(p12, width, height, zero);
         try {
             if (!gt_on_device) e.wait_target();
-            const double v = e.l1_loss(f, gt_dev, mask, false);
+            const double v = e.loss(f, gt_dev, lambda_ssim, mask, false);
             (void)v;
             if (!gt_on_device) e.release_target();
             const size_t pixels = plane;
             e.backward(f, e.d_image_buffer(pixels), true);
             if (loss) {
                 // the L1 sum lives on the device; one 8-byte read completes the step
-                *loss = e.l1_loss_value(f, mask);
+                *loss = e.loss_value(f, mask);
             }
         } catch (...) {
             e.release(f);

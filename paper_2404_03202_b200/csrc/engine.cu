@@ -359,8 +359,9 @@ void Engine::release(Frame* f) {
 void Engine::backward(const Frame* f, const float* d_image, bool accumulate) {
     DeviceGuard g(device_);
     if (static_cast<size_t>(f->n) != n_) throw std::logic_error("StateMismatch: render output does not match the cloud");
-    const size_t elems = static_cast<size_t>(planes_) * stride_;
-    if (!accumulate) OSB_CUDA_CHECK(cudaMemsetAsync(grads_.as<float>(), 0, elems * 4, stream_));
+    // K4b overwrites (no read of the gradient planes, zeros for culled Gaussians) when the buffer is
+    // logically zero or the caller asks for reference overwrite semantics.
+    const bool overwrite = !accumulate || grads_zero_;
     OSB_CUDA_CHECK(cudaMemsetAsync(acc_.as<float4>(), 0, stride_ * 48, stream_));
     const PreprocessOut pp = f->pp();
     {
@@ -374,8 +375,14 @@ void Engine::backward(const Frame* f, const float* d_image, bool accumulate) {
         Span sp(*this, kBwdGauss);
         launch_backward_gaussians(params_.as<float>(), f->n, static_cast<int>(stride_),
                                   (sh_degree_ + 1) * (sh_degree_ + 1), f->active_degree, f->pose, f->W, f->H,
-                                  pp, acc_.as<float4>(), grads_.as<float>(), st, stream_);
+                                  pp, acc_.as<float4>(), grads_.as<float>(), st, overwrite, stream_);
     }
+    grads_zero_ = false;
+}
+
+void Engine::materialize_grads() {
+    if (!grads_zero_) return;
+    OSB_CUDA_CHECK(cudaMemsetAsync(grads_.as<float>(), 0, static_cast<size_t>(planes_) * stride_ * 4, stream_));
 }
 
 float* Engine::d_image_buffer(size_t pixels) {
@@ -411,30 +418,35 @@ void Engine::wait_target() { OSB_CUDA_CHECK(cudaStreamWaitEvent(stream_, target_
 
 void Engine::release_target() { OSB_CUDA_CHECK(cudaEventRecord(target_free_, stream_)); }
 
-double Engine::l1_loss(const Frame* f, const float* gt, double mask_bottom_fraction, bool want_value) {
+double Engine::loss(const Frame* f, const float* gt, double lambda, double mask_bottom_fraction, bool want_value) {
     DeviceGuard g(device_);
     const size_t pixels = static_cast<size_t>(f->W) * f->H;
     float* dimg = d_image_buffer(pixels);
     const int masked = static_cast<int>(std::floor(mask_bottom_fraction * f->H));
     const int keep = f->H - masked;
-    const double n = static_cast<double>(f->W) * keep * 3.0;
+    if (lambda > 0.0) ssim_planes_.ensure(pixels * 9 * sizeof(float));
     {
         Span sp(*this, kLoss);
-        OSB_CUDA_CHECK(cudaMemsetAsync(loss_sum_.as<double>(), 0, 8, stream_));
-        launch_l1_loss(f->fb().rgb, gt, f->W, f->H, keep, 1.0 / n, dimg, loss_sum_.as<double>(), stream_);
+        launch_loss(f->fb().rgb, gt, f->W, f->H, keep, lambda, dimg, ssim_planes_.as<float>(), loss_sum_.as<double>(),
+                    stream_);
     }
+    last_lambda_ = lambda;
     if (!want_value) return 0.0;
-    return l1_loss_value(f, mask_bottom_fraction);
+    return loss_value(f, mask_bottom_fraction);
 }
 
-double Engine::l1_loss_value(const Frame* f, double mask_bottom_fraction) {
+double Engine::loss_value(const Frame* f, double mask_bottom_fraction) {
     DeviceGuard g(device_);
     const int masked = static_cast<int>(std::floor(mask_bottom_fraction * f->H));
-    const double n = static_cast<double>(f->W) * (f->H - masked) * 3.0;
-    double s = 0.0;
-    OSB_CUDA_CHECK(cudaMemcpyAsync(&s, loss_sum_.as<double>(), 8, cudaMemcpyDeviceToHost, stream_));
+    const double npx = static_cast<double>(f->W) * (f->H - masked);
+    const double n = npx * 3.0;
+    double s[4] = {0, 0, 0, 0};
+    OSB_CUDA_CHECK(cudaMemcpyAsync(s, loss_sum_.as<double>(), 32, cudaMemcpyDeviceToHost, stream_));
     OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
-    return s / n;
+    // trainer.cpp:54-63: (1 - l) * L1 + l * (1 - SSIM), SSIM = mean over channels of the pixel mean
+    double value = (1.0 - last_lambda_) * (s[0] / n);
+    if (last_lambda_ > 0.0) value += last_lambda_ * (1.0 - ((s[1] + s[2] + s[3]) / npx) / 3.0);
+    return value;
 }
 
 void Engine::adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad) {
@@ -463,15 +475,17 @@ void Engine::adam_step(const TrainHyper& h, double extent, long iteration, bool 
     a.inv_bias2 = static_cast<float>(1.0 / bias2);
     a.planes = planes_;
     a.stride = static_cast<int>(stride_);
-    a.zero_grad = zero_grad ? 1 : 0;
-    Span sp(*this, kAdam);
-    launch_adam(params_.as<float>(), grads_.as<float>(), m_.as<float>(), v_.as<float>(), a, stream_);
+    // Consumed gradients are not cleared in memory: the flag makes the next backward overwrite them.
+    a.zero_grad = 0;
+    materialize_grads();
+    {
+        Span sp(*this, kAdam);
+        launch_adam(params_.as<float>(), grads_.as<float>(), m_.as<float>(), v_.as<float>(), a, stream_);
+    }
+    if (zero_grad) grads_zero_ = true;
 }
 
-void Engine::zero_grad() {
-    DeviceGuard g(device_);
-    OSB_CUDA_CHECK(cudaMemsetAsync(grads_.as<float>(), 0, static_cast<size_t>(planes_) * stride_ * 4, stream_));
-}
+void Engine::zero_grad() { grads_zero_ = true; }
 
 void Engine::reset_screen_stats() {
     DeviceGuard g(device_);

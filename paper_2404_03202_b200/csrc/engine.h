@@ -85,11 +85,18 @@ public:
     Frame* render(const double pose12[12], int W, int H, const double bg[3]);
     void release(Frame* f);
     void backward(const Frame* f, const float* d_image_planar_dev, bool accumulate);
-    double l1_loss(const Frame* f, const float* gt_planar_dev, double mask_bottom_fraction, bool want_value);
-    // Reads back the value of the last l1_loss() launch (synchronizes the stream).
-    double l1_loss_value(const Frame* f, double mask_bottom_fraction);
+    // loss() of trainer.cpp:25-71 on the device: d_image into d_image_buffer(); the value is read
+    // back only when want_value (one 32-byte read, synchronizes the stream).
+    double loss(const Frame* f, const float* gt_planar_dev, double lambda_ssim, double mask_bottom_fraction,
+                bool want_value);
+    double loss_value(const Frame* f, double mask_bottom_fraction);
     void adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad);
+    // Gradients are tracked as "logically zero" after zero_grad / a consuming Adam step, so the next
+    // backward stores instead of read-modify-writes; materialize_grads() writes the zeros when the
+    // buffer itself is about to be read (download, external views, Adam without a backward).
     void zero_grad();
+    void materialize_grads();
+    bool grads_zero() const { return grads_zero_; }
     void reset_screen_stats();
     void synchronize();
     // CUDA-event timing per kernel family on the context stream, and per-pixel work counting.
@@ -127,7 +134,9 @@ private:
     size_t n_ = 0, stride_ = 0;
     int planes_ = 0, sh_degree_ = 0, active_ = 0;
     long adam_step_ = 0;
-    DevBuf params_, grads_, m_, v_, acc_, d_screen_, norm_sum_, hits_, loss_sum_, d_image_, gt_;
+    DevBuf params_, grads_, m_, v_, acc_, d_screen_, norm_sum_, hits_, loss_sum_, d_image_, gt_, ssim_planes_;
+    double last_lambda_ = 0.0;
+    bool grads_zero_ = true;
     std::vector<std::unique_ptr<Frame>> pool_;
     std::vector<Frame*> free_;
     cudaStream_t copy_stream_ = nullptr;

@@ -65,7 +65,7 @@ struct ScreenStats {
 };
 void launch_backward_gaussians(const float* params, int n, int stride, int bc, int active_degree,
                                const Pose& pose, int W, int H, const PreprocessOut& pp, const float4* acc,
-                               float* grads, const ScreenStats& st, cudaStream_t s);
+                               float* grads, const ScreenStats& st, bool overwrite, cudaStream_t s);
 
 // ---- K5 Adam + loss (adam.cu) ---------------------------------------------------------------
 struct AdamArgs {
@@ -75,10 +75,12 @@ struct AdamArgs {
     int zero_grad;
 };
 void launch_adam(float* params, float* grads, float* m, float* v, const AdamArgs& a, cudaStream_t s);
-// L1 part of loss() (trainer.cpp:25-71) on planar FP32 images; writes d_image planes and
-// atomically accumulates sum|d| (FP64) into *abs_sum.
-void launch_l1_loss(const float* rgb, const float* gt, int W, int H, int keep_rows, double scale,
-                    float* d_image, double* abs_sum, cudaStream_t s);
+// loss() of trainer.cpp:25-71 (loss.cu): (1 - lambda) L1 + lambda (1 - SSIM) over the top
+// keep_rows rows of planar FP32 images; writes dL/dC planes (0 in masked rows) and accumulates
+// sums[0] = sum |r - g| (FP64), sums[1..3] = per-channel SSIM map sums. g_planes: 9 * W * H floats
+// of scratch (only used when lambda > 0).
+void launch_loss(const float* rgb, const float* gt, int W, int H, int keep_rows, double lambda, float* d_image,
+                 float* g_planes, double* sums, cudaStream_t s);
 
 }  // namespace osb
 

@@ -1,0 +1,204 @@
+// loss.cu — the photometric loss of the training step on the device:
+//   L = (1 - lambda) * L1 + lambda * (1 - SSIM)         (proj/src/trainer.cpp:25-71)
+// with SSIM = 11x11, sigma 1.5, zero-padded separable Gaussian windows (proj/src/metrics.cpp:17-55,
+// 81-153), evaluated on the top `keep` rows (bottom-row mask) and its exact gradient.
+//
+// Two tiled kernels per image, one CTA per 32x32 output tile and colour channel:
+//   S1: x, y tile + 5-px halo -> smem; horizontal then vertical 11-tap passes for the five maps
+//       (mu_x, mu_y, E[xx], E[yy], E[xy]); per-pixel SSIM (block-reduced into one FP64 sum per
+//       channel) and its partials g_mu, g_sxx, g_sxy written as three planes.
+//   S2: the three partial planes + halo -> smem; the same separable window (it is its own adjoint)
+//       -> dSSIM/dx; fused with the L1 sign gradient and the FP64 |r - g| sum -> d_image.
+// HBM-bound: ~6 plane reads + 3 plane writes per channel.
+#include "kernels.h"
+
+namespace osb {
+
+namespace {
+
+constexpr int kT = 32;              // output tile
+constexpr int kR = 5;               // window radius
+constexpr int kS = kT + 2 * kR;     // staged tile with halo
+constexpr int kLossThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* s_red) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x < 32) {
+        t = threadIdx.x < kLossThreads / 32 ? s_red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_down_sync(0xffffffffu, t, off);
+    }
+    return t;
+}
+
+struct Window {
+    float w[2 * kR + 1];
+};
+
+__global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(const float* __restrict__ rgb, const float* __restrict__ gt,
+                                                           int W, int H, int keep, Window win,
+                                                           float* __restrict__ g_planes, double* __restrict__ ssim_sum) {
+    __shared__ float sx[kS][kS + 1], sy[kS][kS + 1];
+    __shared__ float h[5][kS][kT + 1];
+    __shared__ double s_red[kLossThreads / 32];
+    const int ch = blockIdx.z;
+    const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
+    const size_t plane = static_cast<size_t>(W) * H;
+    const float* X = rgb + ch * plane;
+    const float* Y = gt + ch * plane;
+    for (int i = threadIdx.x; i < kS * kS; i += kLossThreads) {
+        const int r = i / kS, c = i % kS;
+        const int gx = x0 + c - kR, gy = y0 + r - kR;
+        const bool in = gx >= 0 && gx < W && gy >= 0 && gy < keep;
+        sx[r][c] = in ? X[static_cast<size_t>(gy) * W + gx] : 0.0f;
+        sy[r][c] = in ? Y[static_cast<size_t>(gy) * W + gx] : 0.0f;
+    }
+    __syncthreads();
+    // horizontal pass over all staged rows
+    for (int i = threadIdx.x; i < kS * kT; i += kLossThreads) {
+        const int r = i / kT, c = i % kT;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 2 * kR + 1; ++t) {
+            const float xv = sx[r][c + t], yv = sy[r][c + t], w = win.w[t];
+            a0 = __fmaf_rn(w, xv, a0);
+            a1 = __fmaf_rn(w, yv, a1);
+            a2 = __fmaf_rn(w, xv * xv, a2);
+            a3 = __fmaf_rn(w, yv * yv, a3);
+            a4 = __fmaf_rn(w, xv * yv, a4);
+        }
+        h[0][r][c] = a0; h[1][r][c] = a1; h[2][r][c] = a2; h[3][r][c] = a3; h[4][r][c] = a4;
+    }
+    __syncthreads();
+    const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
+    double local = 0.0;
+    float* G = g_planes + static_cast<size_t>(ch) * 3 * plane;
+    for (int i = threadIdx.x; i < kT * kT; i += kLossThreads) {
+        const int r = i / kT, c = i % kT;
+        const int gx = x0 + c, gy = y0 + r;
+        if (gx >= W || gy >= keep) continue;
+        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int t = 0; t < 2 * kR + 1; ++t) {
+            const float w = win.w[t];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) m[q] = __fmaf_rn(w, h[q][r + t][c], m[q]);
+        }
+        const float mx = m[0], my = m[1];
+        const float var_x = m[2] - mx * mx, var_y = m[3] - my * my, cov = m[4] - mx * my;
+        const float a1 = 2.0f * mx * my + C1, a2 = 2.0f * cov + C2;
+        const float b1 = mx * mx + my * my + C1, b2 = var_x + var_y + C2;
+        const float denom = b1 * b2;
+        local += static_cast<double>(a1 * a2 / denom);
+        const float d_a1 = a2 / denom, d_a2 = a1 / denom;
+        const float d_b1 = -(a1 * a2) / (b1 * denom), d_b2 = -(a1 * a2) / (b2 * denom);
+        const size_t p = static_cast<size_t>(gy) * W + gx;
+        G[p] = d_a1 * 2.0f * my + d_b1 * 2.0f * mx + d_a2 * (-2.0f * my) + d_b2 * (-2.0f * mx);
+        G[plane + p] = d_b2;
+        G[2 * plane + p] = d_a2 * 2.0f;
+    }
+    const double s = block_sum(local, s_red);
+    if (threadIdx.x == 0) atomicAdd(ssim_sum + ch, s);
+}
+
+__global__ void __launch_bounds__(kLossThreads) k_ssim_bwd(const float* __restrict__ rgb, const float* __restrict__ gt,
+                                                           int W, int H, int keep, Window win,
+                                                           const float* __restrict__ g_planes, float l1_scale,
+                                                           float ssim_scale, float* __restrict__ d_image,
+                                                           double* __restrict__ abs_sum) {
+    __shared__ float sg[3][kS][kS + 1];
+    __shared__ float h[3][kS][kT + 1];
+    __shared__ double s_red[kLossThreads / 32];
+    const int ch = blockIdx.z;
+    const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
+    const size_t plane = static_cast<size_t>(W) * H;
+    const float* G = g_planes + static_cast<size_t>(ch) * 3 * plane;
+    if (ssim_scale != 0.0f) {
+        for (int i = threadIdx.x; i < kS * kS; i += kLossThreads) {
+            const int r = i / kS, c = i % kS;
+            const int gx = x0 + c - kR, gy = y0 + r - kR;
+            const bool in = gx >= 0 && gx < W && gy >= 0 && gy < keep;
+            const size_t p = static_cast<size_t>(gy) * W + gx;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) sg[q][r][c] = in ? G[q * plane + p] : 0.0f;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kS * kT; i += kLossThreads) {
+            const int r = i / kT, c = i % kT;
+            float a[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+            for (int t = 0; t < 2 * kR + 1; ++t) {
+                const float w = win.w[t];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) a[q] = __fmaf_rn(w, sg[q][r][c + t], a[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < 3; ++q) h[q][r][c] = a[q];
+        }
+        __syncthreads();
+    }
+    double local = 0.0;
+    for (int i = threadIdx.x; i < kT * kT; i += kLossThreads) {
+        const int r = i / kT, c = i % kT;
+        const int gx = x0 + c, gy = y0 + r;
+        if (gx >= W || gy >= H) continue;
+        const size_t p = ch * plane + static_cast<size_t>(gy) * W + gx;
+        float grad = 0.0f;
+        if (gy < keep) {
+            const float xv = rgb[p], yv = gt[p];
+            const float d = xv - yv;
+            local += fabs(static_cast<double>(d));
+            grad = d > 0.0f ? l1_scale : (d < 0.0f ? -l1_scale : 0.0f);
+            if (ssim_scale != 0.0f) {
+                float cm = 0.f, cxx = 0.f, cxy = 0.f;
+#pragma unroll
+                for (int t = 0; t < 2 * kR + 1; ++t) {
+                    const float w = win.w[t];
+                    cm = __fmaf_rn(w, h[0][r + t][c], cm);
+                    cxx = __fmaf_rn(w, h[1][r + t][c], cxx);
+                    cxy = __fmaf_rn(w, h[2][r + t][c], cxy);
+                }
+                grad -= ssim_scale * (cm + 2.0f * xv * cxx + yv * cxy);
+            }
+        }
+        d_image[p] = grad;
+    }
+    const double s = block_sum(local, s_red);
+    if (threadIdx.x == 0) atomicAdd(abs_sum, s);
+}
+
+}  // namespace
+
+void launch_loss(const float* rgb, const float* gt, int W, int H, int keep_rows, double lambda, float* d_image,
+                 float* g_planes, double* sums, cudaStream_t s) {
+    if (W <= 0 || H <= 0) return;
+    // 11-tap window (metrics.cpp:17-27), FP64 then rounded
+    Window win;
+    double w[2 * kR + 1], total = 0.0;
+    for (int i = 0; i < 2 * kR + 1; ++i) {
+        const double d = i - kR;
+        w[i] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
+        total += w[i];
+    }
+    for (int i = 0; i < 2 * kR + 1; ++i) win.w[i] = static_cast<float>(w[i] / total);
+    const double n = static_cast<double>(W) * keep_rows * 3.0;
+    const float l1_scale = n > 0 ? static_cast<float>((1.0 - lambda) / n) : 0.0f;
+    // d SSIM_mean / d pixel carries 1 / (3 n_px) (metrics.cpp:146), then * lambda (trainer.cpp:66)
+    const float ssim_scale = n > 0 ? static_cast<float>(lambda / n) : 0.0f;
+    OSB_CUDA_CHECK(cudaMemsetAsync(sums, 0, 4 * sizeof(double), s));
+    const dim3 grid((W + kT - 1) / kT, (H + kT - 1) / kT, 3);
+    if (lambda > 0.0 && keep_rows > 0) {
+        const dim3 gf((W + kT - 1) / kT, (keep_rows + kT - 1) / kT, 3);
+        k_ssim_fwd<<<gf, kLossThreads, 0, s>>>(rgb, gt, W, H, keep_rows, win, g_planes, sums + 1);
+        OSB_LAUNCHED(1);
+    }
+    k_ssim_bwd<<<grid, kLossThreads, 0, s>>>(rgb, gt, W, H, keep_rows, win, g_planes, l1_scale,
+                                             lambda > 0.0 ? ssim_scale : 0.0f, d_image, sums);
+    OSB_LAUNCHED(1);
+}
+
+}  // namespace osb

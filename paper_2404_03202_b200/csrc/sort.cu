@@ -5,15 +5,18 @@
 //   1. all Gaussians are stably radix-sorted by the 64-bit pattern of t_r (positive doubles order
 //      like their bit patterns; culled ones carry ~0 and sink to the end), with ids as values in
 //      ascending order -> (depth, id) order;
-//   2. instances are emitted in that order (exclusive scan of tiles_touched over it, fused with a
+//   2. instances are emitted in that order (exclusive scan of tiles_touched over it, then a
 //      load-balanced emission: every lane writes consecutive instances -> coalesced stores);
 //   3. a STABLE radix sort by tile id keeps the (depth, id) order inside every tile.
 // So each tile list equals the reference's sorted list element for element.
 //
-// Radix sort: LSD, 8-bit digits, one "onesweep" kernel per digit: per-warp match_any ranking,
-// per-block digit counts, decoupled look-back across blocks for the global digit offsets (dynamic
-// block ids guarantee forward progress), then a block-local sort in shared memory so the global
-// scatter writes runs of consecutive addresses. No host synchronization inside a sort.
+// Radix sort: LSD, 8-bit digits, reduce-then-scan per digit (no serial cross-block chain — at these
+// sizes every block is resident at once, so a decoupled look-back would serialise):
+//   upsweep   per-block digit counts (warp-private shared histograms)
+//   scan      per digit, exclusive prefix over blocks + the digit's global base
+//   downsweep per-warp match_any ranking (stable), block-local sort in shared memory, coalesced
+//             scatter of runs of equal digits.
+// No host synchronization inside a sort.
 #include "kernels.h"
 
 namespace osb {
@@ -24,9 +27,6 @@ constexpr int kRadixBits = 8;
 constexpr int kBins = 1 << kRadixBits;
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr uint32_t kFlagAgg = 1u << 30;
-constexpr uint32_t kFlagPrefix = 2u << 30;
-constexpr uint32_t kCountMask = (1u << 30) - 1;
 constexpr int kMaxPasses = 8;
 
 template <typename K>
@@ -39,6 +39,10 @@ template <>
 struct SortCfg<uint32_t> {
     static constexpr int kItems = 16;
 };
+template <typename K>
+__host__ __device__ constexpr int tile_keys() {
+    return kSortThreads * SortCfg<K>::kItems;
+}
 
 template <typename K>
 __global__ void __launch_bounds__(256) k_histogram(const K* __restrict__ keys, int n, int passes,
@@ -101,49 +105,65 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
     return r;
 }
 
-// Decoupled look-back: publish this block's aggregate for `slot`, return the exclusive prefix.
-__device__ __forceinline__ uint32_t lookback(uint32_t* status, uint32_t bid, size_t stride, size_t slot, uint32_t agg) {
-    uint32_t* my = status + static_cast<size_t>(bid) * stride + slot;
-    if (bid == 0) {
-        st_release(my, kFlagPrefix | agg);
-        return 0;
+// Per-block digit counts for one pass: counts[d * nblocks + b].
+template <typename K>
+__global__ void __launch_bounds__(kSortThreads) k_upsweep(const K* __restrict__ keys, int n, int shift, int nblocks,
+                                                          uint32_t* __restrict__ counts) {
+    constexpr int kTile = tile_keys<K>();
+    __shared__ uint32_t s_hist[kSortWarps][kBins];
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kSortWarps * kBins; i += kSortThreads) (&s_hist[0][0])[i] = 0;
+    __syncthreads();
+    const long base = static_cast<long>(blockIdx.x) * kTile;
+    const int count = static_cast<int>(min(static_cast<long>(kTile), static_cast<long>(n) - base));
+    for (int i = threadIdx.x; i < count; i += kSortThreads)
+        atomicAdd(&s_hist[warp][static_cast<uint32_t>((keys[base + i] >> shift) & (kBins - 1))], 1u);
+    __syncthreads();
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) c += s_hist[w][threadIdx.x];
+    counts[static_cast<size_t>(threadIdx.x) * nblocks + blockIdx.x] = c;
+}
+
+// One block per digit: offsets[d][b] = digit_base[d] + sum_{b' < b} counts[d][b'].
+__global__ void __launch_bounds__(kSortThreads) k_scan_counts(const uint32_t* __restrict__ counts, int nblocks,
+                                                              const uint32_t* __restrict__ digit_base,
+                                                              uint32_t* __restrict__ offsets) {
+    __shared__ uint32_t s_scan[kSortWarps + 1];
+    const int d = blockIdx.x;
+    const uint32_t* row = counts + static_cast<size_t>(d) * nblocks;
+    uint32_t* out = offsets + static_cast<size_t>(d) * nblocks;
+    uint32_t carry = digit_base[d];
+    for (int b0 = 0; b0 < nblocks; b0 += kSortThreads) {
+        const int b = b0 + threadIdx.x;
+        const uint32_t v = b < nblocks ? row[b] : 0u;
+        uint32_t total;
+        const uint32_t ex = block_exclusive_scan(v, s_scan, &total);
+        if (b < nblocks) out[b] = carry + ex;
+        carry += total;
+        __syncthreads();
     }
-    st_release(my, kFlagAgg | agg);
-    uint32_t exclusive = 0;
-    long p = static_cast<long>(bid) - 1;
-    while (true) {
-        const uint32_t s = ld_acquire(status + static_cast<size_t>(p) * stride + slot);
-        const uint32_t flag = s & ~kCountMask;
-        if (flag == 0) continue;
-        exclusive += s & kCountMask;
-        if (flag == kFlagPrefix) break;
-        --p;
-    }
-    st_release(my, kFlagPrefix | (exclusive + agg));
-    return exclusive;
 }
 
 template <typename K>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(const K* __restrict__ keys_in,
-                                                           const uint32_t* __restrict__ vals_in,
-                                                           K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-                                                           int n, int shift, const uint32_t* __restrict__ digit_base,
-                                                           uint32_t* __restrict__ status, uint32_t* __restrict__ counter) {
+__global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict__ keys_in,
+                                                            const uint32_t* __restrict__ vals_in,
+                                                            K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
+                                                            int n, int shift, int nblocks,
+                                                            const uint32_t* __restrict__ offsets) {
     constexpr int kItems = SortCfg<K>::kItems;
     constexpr int kTile = kSortThreads * kItems;
-    __shared__ uint32_t s_bid;
     __shared__ uint32_t s_warp[kSortWarps][kBins];
-    __shared__ uint32_t s_local[kBins];   // block-local start of each digit
-    __shared__ int s_global[kBins];       // global position - local position, per digit
+    __shared__ uint32_t s_local[kBins];  // block-local start of each digit
+    __shared__ int s_global[kBins];      // global position - local position, per digit
     __shared__ uint32_t s_scan[kSortWarps + 1];
     __shared__ K s_keys[kTile];
     __shared__ uint32_t s_vals[kTile];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) s_bid = atomicAdd(counter, 1u);
     for (int i = tid; i < kSortWarps * kBins; i += kSortThreads) (&s_warp[0][0])[i] = 0;
     __syncthreads();
-    const uint32_t bid = s_bid;
+    const uint32_t bid = blockIdx.x;
     const long block_base = static_cast<long>(bid) * kTile;
     const long base = block_base + static_cast<long>(warp) * 32 * kItems;
     const int count = static_cast<int>(min(static_cast<long>(kTile), static_cast<long>(n) - block_base));
@@ -189,8 +209,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K* __restrict__
     uint32_t total;
     const uint32_t local = block_exclusive_scan(cnt, s_scan, &total);
     s_local[d] = local;
-    const uint32_t excl = lookback(status, bid, kBins, d, cnt);
-    s_global[d] = static_cast<int>(digit_base[d] + excl) - static_cast<int>(local);
+    s_global[d] = static_cast<int>(offsets[static_cast<size_t>(d) * nblocks + bid]) - static_cast<int>(local);
     __syncthreads();
 
     // Block-local sort into shared memory.
@@ -220,30 +239,80 @@ __global__ void k_iota(uint32_t* v, int n) {
     if (i < n) v[i] = static_cast<uint32_t>(i);
 }
 
-// ---- fused exclusive scan of tiles_touched (depth order) + load-balanced instance emission ----
+// ---- scan of tiles_touched (depth order) + load-balanced instance emission ----------------------
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;  // ranks per block
 constexpr int kWarpRanks = 32 * kScanItems;            // ranks per warp
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __restrict__ touched,
-                                                            const uint32_t* __restrict__ order,
-                                                            const int4* __restrict__ rect, int n, int tiles_x,
-                                                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                                            uint32_t capacity, uint32_t* __restrict__ total,
-                                                            uint32_t* __restrict__ status,
-                                                            uint32_t* __restrict__ counter) {
-    __shared__ uint32_t s_bid;
+// Sum of touched over each block's ranks.
+__global__ void __launch_bounds__(kScanThreads) k_touch_sums(const uint32_t* __restrict__ touched,
+                                                             const uint32_t* __restrict__ order, int n,
+                                                             uint32_t* __restrict__ block_sums) {
     __shared__ uint32_t s_scan[kSortWarps + 1];
-    __shared__ uint32_t s_excl;
+    const long r0 = static_cast<long>(blockIdx.x) * kScanTile + threadIdx.x;
+    uint32_t local = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        const long r = r0 + i * kScanThreads;
+        if (r < n) local += touched[order[r]];
+    }
+    uint32_t total;
+    block_exclusive_scan(local, s_scan, &total);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
+}
+
+// Single block: exclusive scan of the block sums in place; *total = M.
+__global__ void __launch_bounds__(1024) k_scan_block_sums(uint32_t* __restrict__ sums, int nblocks,
+                                                          uint32_t* __restrict__ total) {
+    __shared__ uint32_t s_part[32];
+    __shared__ uint32_t s_carry;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < nblocks; b0 += 1024) {
+        const int b = b0 + threadIdx.x;
+        const uint32_t v = b < nblocks ? sums[b] : 0u;
+        uint32_t inc = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, off);
+            if (lane >= off) inc += t;
+        }
+        if (lane == 31) s_part[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t w = s_part[lane];
+            uint32_t wi = w;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, off);
+                if (lane >= off) wi += t;
+            }
+            s_part[lane] = wi - w;
+        }
+        __syncthreads();
+        const uint32_t carry = s_carry;
+        if (b < nblocks) sums[b] = carry + s_part[warp] + inc - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) s_carry = carry + s_part[warp] + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = s_carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restrict__ touched,
+                                                       const uint32_t* __restrict__ order,
+                                                       const int4* __restrict__ rect, int n, int tiles_x,
+                                                       const uint32_t* __restrict__ block_offsets,
+                                                       uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                       uint32_t capacity) {
+    __shared__ uint32_t s_scan[kSortWarps + 1];
     __shared__ uint32_t s_off[kScanTile + kSortWarps];  // per warp: kWarpRanks offsets + warp end
     __shared__ uint32_t s_gid[kScanTile];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_bid = atomicAdd(counter, 1u);
-    __syncthreads();
-    const uint32_t bid = s_bid;
     // thread owns ranks [r0, r0 + kScanItems) inside its warp's contiguous 256-rank chunk
-    const long r0 = static_cast<long>(bid) * kScanTile + warp * kWarpRanks + lane * kScanItems;
+    const long r0 = static_cast<long>(blockIdx.x) * kScanTile + warp * kWarpRanks + lane * kScanItems;
     uint32_t v[kScanItems];
     uint32_t g[kScanItems];
     uint32_t local = 0;
@@ -256,12 +325,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_emit(const uint32_t* __re
     }
     uint32_t agg;
     const uint32_t thread_excl = block_exclusive_scan(local, s_scan, &agg);
-    if (tid == 0) s_excl = lookback(status, bid, 1, 0, agg);
-    __syncthreads();
-    const uint32_t block_excl = s_excl;
-    if (static_cast<long>(bid + 1) * kScanTile >= n && tid == 0) *total = block_excl + agg;
+    const uint32_t block_excl = block_offsets[blockIdx.x];
 
-    // offsets (block-relative) of this thread's ranks, staged per warp
     uint32_t run = thread_excl;
     uint32_t* w_off = s_off + warp * (kWarpRanks + 1);
 #pragma unroll
@@ -304,12 +369,7 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, int m, uint2* __rest
     if (i == m - 1 || keys[i + 1] != k) ranges[k].y = i + 1;
 }
 
-template <typename K>
-constexpr int tile_keys() {
-    return kSortThreads * SortCfg<K>::kItems;
-}
-
-// Workspace: hist[8][256] | base[8][256] | counters[64] | status[passes][blocks][256]
+// Workspace: hist[8][256] | base[8][256] | counts[256][blocks] | offsets[256][blocks]
 template <typename K>
 bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n, int bits, void* ws,
                 cudaStream_t s) {
@@ -318,10 +378,9 @@ bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, 
     const int blocks = (n + tile_keys<K>() - 1) / tile_keys<K>();
     uint32_t* hist = static_cast<uint32_t*>(ws);
     uint32_t* base = hist + kMaxPasses * kBins;
-    uint32_t* counter = base + kMaxPasses * kBins;
-    uint32_t* status = counter + 64;
-    const size_t status_words = static_cast<size_t>(passes) * blocks * kBins;
-    OSB_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (2 * kMaxPasses * kBins + 64 + status_words), s));
+    uint32_t* counts = base + kMaxPasses * kBins;
+    uint32_t* offsets = counts + static_cast<size_t>(kBins) * blocks;
+    OSB_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kBins, s));
     const int hblocks = blocks < 148 * 4 ? blocks : 148 * 4;
     k_histogram<K><<<hblocks, 256, 0, s>>>(keys_in, n, passes, hist);
     k_scan_hist<<<passes, kBins, 0, s>>>(hist, base);
@@ -332,9 +391,11 @@ bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, 
         K* ko = flipped ? keys_in : keys_out;
         uint32_t* vi = flipped ? vals_out : vals_in;
         uint32_t* vo = flipped ? vals_in : vals_out;
-        k_onesweep<K><<<blocks, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, p * kRadixBits, base + p * kBins,
-                                                       status + static_cast<size_t>(p) * blocks * kBins, counter + p);
-        OSB_LAUNCHED(1);
+        const int shift = p * kRadixBits;
+        k_upsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, n, shift, blocks, counts);
+        k_scan_counts<<<kBins, kSortThreads, 0, s>>>(counts, blocks, base + p * kBins, offsets);
+        k_downsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, shift, blocks, offsets);
+        OSB_LAUNCHED(3);
         flipped = !flipped;
     }
     return flipped;
@@ -345,7 +406,7 @@ bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, 
 size_t radix_workspace_bytes(int n_max, int key_bytes) {
     const int tk = key_bytes == 8 ? tile_keys<uint64_t>() : tile_keys<uint32_t>();
     const size_t blocks = (static_cast<size_t>(n_max) + tk - 1) / tk;
-    return sizeof(uint32_t) * (2 * kMaxPasses * kBins + 64 + kMaxPasses * blocks * kBins) + 256;
+    return sizeof(uint32_t) * (2 * kMaxPasses * kBins + 2 * kBins * blocks) + 256;
 }
 
 bool radix_sort_u64(uint64_t* ki, uint64_t* ko, uint32_t* vi, uint32_t* vo, int n, int bits, void* ws,
@@ -375,12 +436,11 @@ void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4
         return;
     }
     const int blocks = (n + kScanTile - 1) / kScanTile;
-    uint32_t* counter = static_cast<uint32_t*>(ws);
-    uint32_t* status = counter + 64;
-    OSB_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * (blocks + 64), s));
-    k_scan_emit<<<blocks, kScanThreads, 0, s>>>(touched, order, rect, n, tiles_x, keys, vals, capacity, total, status,
-                                                 counter);
-    OSB_LAUNCHED(1);
+    uint32_t* sums = static_cast<uint32_t*>(ws);
+    k_touch_sums<<<blocks, kScanThreads, 0, s>>>(touched, order, n, sums);
+    k_scan_block_sums<<<1, 1024, 0, s>>>(sums, blocks, total);
+    k_emit<<<blocks, kScanThreads, 0, s>>>(touched, order, rect, n, tiles_x, sums, keys, vals, capacity);
+    OSB_LAUNCHED(3);
 }
 
 void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s) {

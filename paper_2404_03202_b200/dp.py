@@ -63,7 +63,7 @@ class GpuViewEngine:
     device; the target images stay resident. Adam zeroes the gradients it consumes."""
 
     def __init__(self, ctx, poses, targets: dict, width: int, height: int, config, extent: float = 1.0,
-                 mask_bottom_fraction: float = 0.0):
+                 mask_bottom_fraction: float = 0.0, lambda_ssim: float = 0.2):
         import torch
 
         self.ctx = ctx
@@ -73,13 +73,15 @@ class GpuViewEngine:
         self.config = config
         self.extent = extent
         self.mask = mask_bottom_fraction
+        self.lambda_ssim = lambda_ssim
         v = ctx.view()
         self._grads = torch.as_tensor(_CudaArray(v.grads, v.planes * v.stride), device="cuda")
 
     def accumulate_view(self, view_id: int):
         fr = self.ctx.render(self.poses[view_id], self.W, self.H)
         try:
-            _, dimg = self.ctx.l1_loss(fr, self.targets[view_id].data_ptr(), self.mask, want_value=False)
+            _, dimg = self.ctx.loss(fr, self.targets[view_id].data_ptr(), self.lambda_ssim, self.mask,
+                                    want_value=False)
             self.ctx.backward_device(fr, dimg, accumulate=True)
         finally:
             fr.free()

@@ -102,7 +102,8 @@ def _load():
         "osplat_gpu_reset_screen_stats": (S, [_vp]),
         "osplat_gpu_adam_step": (S, [_vp, _vp, C.c_double, C.c_long, C.c_int]),
         "osplat_gpu_l1_loss": (S, [_vp, _vp, _vp, C.c_double, C.POINTER(_vp), _dp]),
-        "osplat_gpu_train_view": (S, [_vp, _dp, C.c_int, C.c_int, _vp, C.c_int, C.c_double, _dp]),
+        "osplat_gpu_loss": (S, [_vp, _vp, _vp, C.c_double, C.c_double, C.POINTER(_vp), _dp]),
+        "osplat_gpu_train_view": (S, [_vp, _dp, C.c_int, C.c_int, _vp, C.c_int, C.c_double, C.c_double, _dp]),
         "osplat_gpu_launch_count": (C.c_longlong, []),
         "osplat_gpu_profile": (S, [_vp, C.c_int, C.c_int]),
         "osplat_gpu_profile_read": (S, [_vp, _dp, _lp, C.c_int]),
@@ -350,20 +351,26 @@ class Context:
         check(lib.osplat_gpu_adam_step(self.handle, config.handle if config else None, extent, iteration,
                                        int(zero_grad)))
 
-    def l1_loss(self, frame: Frame, gt_ptr: int, mask_bottom_fraction: float = 0.0, want_value=True):
+    def loss(self, frame: Frame, gt_ptr: int, lambda_ssim: float = 0.2, mask_bottom_fraction: float = 0.0,
+             want_value=True):
+        """loss() (trainer.cpp:25-71) against a device planar target; returns (value, d_image ptr)."""
         d = _vp()
         val = C.c_double(0.0)
-        check(lib.osplat_gpu_l1_loss(self.handle, frame.handle, C.c_void_p(gt_ptr), mask_bottom_fraction,
-                                     C.byref(d), C.byref(val) if want_value else None))
+        check(lib.osplat_gpu_loss(self.handle, frame.handle, C.c_void_p(gt_ptr), lambda_ssim, mask_bottom_fraction,
+                                  C.byref(d), C.byref(val) if want_value else None))
         return val.value, d.value
 
-    def train_view(self, pose12, width: int, height: int, gt, gt_on_device: bool, mask: float = 0.0) -> float:
-        """render -> L1 loss -> backward(accumulate); gt is a host numpy array (3,H,W) float32
-        or a device pointer (int)."""
+    def l1_loss(self, frame: Frame, gt_ptr: int, mask_bottom_fraction: float = 0.0, want_value=True):
+        return self.loss(frame, gt_ptr, 0.0, mask_bottom_fraction, want_value)
+
+    def train_view(self, pose12, width: int, height: int, gt, gt_on_device: bool, lambda_ssim: float = 0.2,
+                   mask: float = 0.0) -> float:
+        """render -> loss -> backward(accumulate); gt is a host numpy array (3,H,W) float32 or a
+        pointer (int) to host (gt_on_device False) or device memory."""
         t = transform_of(pose12)
         loss = C.c_double(0.0)
         ptr = C.c_void_p(gt) if isinstance(gt, int) else gt.ctypes.data_as(C.c_void_p)
-        check(lib.osplat_gpu_train_view(self.handle, _p(t), width, height, ptr, int(gt_on_device), mask,
+        check(lib.osplat_gpu_train_view(self.handle, _p(t), width, height, ptr, int(gt_on_device), lambda_ssim, mask,
                                         C.byref(loss)))
         return loss.value
 

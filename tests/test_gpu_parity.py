@@ -164,3 +164,37 @@ def test_context_adopts_caller_stream(legacy):
         kern = sum(v[0] for v in ctx.profile_read().values())
         assert kern > 0.0
         assert e0.elapsed_time(e1) >= 0.9 * kern, (e0.elapsed_time(e1), kern)
+
+
+def test_accumulate_and_logical_zero():
+    """backward(accumulate) sums views; a consuming Adam step / zero_grad makes the next backward
+    start from zero (the planes are overwritten, never read)."""
+    cloud = _scene("uniform", 4000, 13)
+    W, H = 256, 128
+    pa, pb = scenes.identity_pose(), scenes.random_pose(np.random.default_rng(3))
+    rng = np.random.default_rng(5)
+    da = rng.uniform(-1, 1, size=(H, W, 3)) / (W * H)
+    db = rng.uniform(-1, 1, size=(H, W, 3)) / (W * H)
+    ctx = native.Context(cloud)
+    fa, fb = ctx.render(pa, W, H), ctx.render(pb, W, H)
+    ctx.backward(fa, da)
+    ga = ctx.gradients()
+    ctx.backward(fb, db)
+    gb = ctx.gradients()
+    ctx.zero_grad()
+    ctx.backward(fa, da, accumulate=True)
+    ctx.backward(fb, db, accumulate=True)
+    gab = ctx.gradients()
+    for k in ("d_position", "d_sh", "d_rotation", "d_log_scale", "d_opacity_logit"):
+        ref = ga[k] + gb[k]
+        assert np.allclose(gab[k], ref, rtol=1e-5, atol=1e-7 * np.max(np.abs(ref))), k
+    ctx.adam_step(native.Config(), 1.0, 1, zero_grad=True)
+    fa.free()
+    fa = ctx.render(pa, W, H)
+    ctx.backward(fa, da, accumulate=True)
+    g1 = ctx.gradients()
+    ctx.backward(fa, da)  # reference overwrite semantics
+    g2 = ctx.gradients()
+    for k in ("d_position", "d_sh", "d_rotation", "d_log_scale", "d_opacity_logit"):
+        # K4a's FP32 atomics make the summation order run-dependent
+        assert np.allclose(g1[k], g2[k], rtol=1e-4, atol=1e-6 * np.max(np.abs(g2[k]))), k
