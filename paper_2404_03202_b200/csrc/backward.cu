@@ -61,25 +61,26 @@ __device__ __forceinline__ float warp_reduce9(const float (&v)[9], int lane, int
     return f;
 }
 
-__global__ void __launch_bounds__(kStage, 3) k_backward_pixels(const uint32_t* __restrict__ inst_gid,
-                                                               const uint2* __restrict__ ranges, PreprocessOut pp,
-                                                               int W, int H, int tiles_x, float bg0, float bg1,
-                                                               float bg2, FrameBuffers fb,
-                                                               const float* __restrict__ d_image,
-                                                               float4* __restrict__ acc) {
-    __shared__ StageSmem sm;
-    __shared__ int s_max_last;
+__global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint32_t* __restrict__ inst_gid,
+                                                                     const uint2* __restrict__ ranges, PreprocessOut pp,
+                                                                     int W, int H, int tiles_x, float bg0, float bg1,
+                                                                     float bg2, FrameBuffers fb,
+                                                                     const float* __restrict__ d_image,
+                                                                     float4* __restrict__ acc) {
+    __shared__ WarpStage stage[kTileWarps];
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
     const int px = tx * kTile + lx, py = ty * kTile + ly;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool inside = px < W && py < H;
     const uint2 range = ranges[tile];
     const double width = W;
     const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
     const float lxo = lx - 7.5f, lyo = ly - 7.5f;
+    const float r0 = 2.0f * warp - 7.5f;
     const float halfW = 0.5f * W, fW = static_cast<float>(W);
+    WarpStage& ws = stage[warp];
 
     const size_t pix = static_cast<size_t>(py) * W + px;
     const size_t plane = static_cast<size_t>(W) * H;
@@ -89,44 +90,41 @@ __global__ void __launch_bounds__(kStage, 3) k_backward_pixels(const uint32_t* _
     const float dl1 = inside ? d_image[plane + pix] : 0.0f;
     const float dl2 = inside ? d_image[2 * plane + pix] : 0.0f;
     const float bg_dot = bg0 * dl0 + bg1 * dl1 + bg2 * dl2;
-
-    if (threadIdx.x == 0) s_max_last = 0;
-    __syncthreads();
-    if (last > 0) atomicMax(&s_max_last, last);
-    __syncthreads();
-    const int max_last = s_max_last;
+    // this warp only walks the list up to its own furthest last_contrib
+    const int max_last = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(last)));
 
     float T_acc = T_final;
     float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;     // suffix colour
     float lc0 = 0.0f, lc1 = 0.0f, lc2 = 0.0f;  // last colour
     float last_a = 0.0f;
 
-    for (int hi = max_last; hi > 0; hi -= kStage) {
-        const int lo = hi > kStage ? hi - kStage : 0;
+    for (int hi = max_last; hi > 0; hi -= 32) {
+        const int lo = hi > 32 ? hi - 32 : 0;
         const int cnt = hi - lo;
-        __syncthreads();
-        if (threadIdx.x < cnt)
-            stage_splat(sm, threadIdx.x, inst_gid[range.x + lo + threadIdx.x], pp.pxy, pp.splat, xc, yc, width);
-        __syncthreads();
-        const int n_act = compact_for_warp(sm, cnt, warp, lane);
-        for (int t = n_act - 1; t >= 0; --t) {
-            const int j = sm.list[warp][t];
+        bool reach = false;
+        if (lane < cnt)
+            reach = stage_entry(ws, lane, inst_gid[range.x + lo + lane], pp.pxy, pp.splat, xc, yc, width, r0);
+        uint32_t bal = __ballot_sync(0xffffffffu, reach);
+        __syncwarp();
+        while (bal != 0u) {  // back to front; uniform over the warp (the reduction needs all lanes)
+            const int j = 31 - __clz(bal);
+            bal &= ~(1u << j);
             const int k = lo + j;
-            float v[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f, v5 = 0.f, v6 = 0.f, v7 = 0.f, v8 = 0.f;
             bool has = false;
             if (k < last) {
-                const float4 A = sm.a[j];
-                const float4 B = sm.b[j];
+                const float4 A = ws.a[j];
+                const float4 B = ws.b[j];
                 float dx, dy, power;
                 bool unc;
                 if (pair_power(A, B, lxo, lyo, halfW, fW, dx, dy, power, unc)) {
-                    const float4 Cc = sm.c[j];
+                    const float4 Cc = ws.c[j];
                     float alpha, g;
                     bool gate;
                     bool ok = true;
                     if (unc) {
                         Pair64 p;
-                        ok = pair_slow(sm.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
+                        ok = pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
                         alpha = static_cast<float>(p.alpha);
                         g = static_cast<float>(p.g);
                         gate = p.og < kAlphaMax;
@@ -137,7 +135,7 @@ __global__ void __launch_bounds__(kStage, 3) k_backward_pixels(const uint32_t* _
                         const float band = 0.99f * (1.5f * fabsf(B.w) + 1e-6f);
                         if (fabsf(og - 0.99f) <= band) {
                             Pair64 p;
-                            pair_slow(sm.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
+                            pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
                             gate = p.og < kAlphaMax;
                         } else {
                             gate = og < 0.99f;
@@ -149,9 +147,9 @@ __global__ void __launch_bounds__(kStage, 3) k_backward_pixels(const uint32_t* _
                         const float inv = __fdividef(1.0f, one_m);
                         T_acc = T_acc * inv;
                         const float wb = alpha * T_acc;
-                        v[0] = dl0 * wb;
-                        v[1] = dl1 * wb;
-                        v[2] = dl2 * wb;
+                        v0 = dl0 * wb;
+                        v1 = dl1 * wb;
+                        v2 = dl2 * wb;
                         const float oml = 1.0f - last_a;
                         s0 = __fmaf_rn(lc0, last_a, s0 * oml);
                         s1 = __fmaf_rn(lc1, last_a, s1 * oml);
@@ -163,35 +161,37 @@ __global__ void __launch_bounds__(kStage, 3) k_backward_pixels(const uint32_t* _
                         lc0 = Cc.x; lc1 = Cc.y; lc2 = Cc.z;
                         last_a = alpha;
                         if (gate) {
-                            v[3] = g * d_alpha;
+                            v3 = g * d_alpha;
                             const float d_power = -g * Cc.w * d_alpha;
                             const float qx = __fmaf_rn(2.0f * A.z, dx, B.x * dy);
                             const float qy = __fmaf_rn(B.x, dx, 2.0f * A.w * dy);
-                            v[4] = d_power * qx;
-                            v[5] = d_power * qy;
+                            v4 = d_power * qx;
+                            v5 = d_power * qy;
                             const float hp = 0.5f * d_power;
-                            v[6] = hp * dx * dx;
-                            v[7] = d_power * dx * dy;
-                            v[8] = hp * dy * dy;
+                            v6 = hp * dx * dx;
+                            v7 = d_power * dx * dy;
+                            v8 = hp * dy * dy;
                         }
                     }
                 }
             }
-            const uint32_t bal = __ballot_sync(0xffffffffu, has);
-            if (bal == 0u) continue;
-            float* a = reinterpret_cast<float*>(acc + 3 * static_cast<size_t>(sm.gid[j]));
-            if ((bal & (bal - 1u)) == 0u) {
+            const uint32_t hb = __ballot_sync(0xffffffffu, has);
+            if (hb == 0u) continue;
+            float* a = reinterpret_cast<float*>(acc + 3 * static_cast<size_t>(ws.gid[j]));
+            if ((hb & (hb - 1u)) == 0u) {
                 if (has) {
-                    red_add_v4(reinterpret_cast<float4*>(a), v[0], v[1], v[2], v[3]);
-                    red_add_v4(reinterpret_cast<float4*>(a) + 1, v[4], v[5], v[6], v[7]);
-                    red_add(a + 8, v[8]);
+                    red_add_v4(reinterpret_cast<float4*>(a), v0, v1, v2, v3);
+                    red_add_v4(reinterpret_cast<float4*>(a) + 1, v4, v5, v6, v7);
+                    red_add(a + 8, v8);
                 }
             } else {
+                const float v[9] = {v0, v1, v2, v3, v4, v5, v6, v7, v8};
                 int idx;
-                const float s = warp_reduce9(v, lane, &idx);
-                if (idx >= 0 && !(lane & 1)) red_add(a + idx, s);
+                const float sum = warp_reduce9(v, lane, &idx);
+                if (idx >= 0 && !(lane & 1)) red_add(a + idx, sum);
             }
         }
+        __syncwarp();
     }
 }
 
@@ -429,7 +429,7 @@ void launch_backward_pixels(const uint32_t* inst_gid, const uint2* ranges, const
                             float4* acc, cudaStream_t s) {
     const int tiles = tiles_x * tiles_y;
     if (tiles <= 0) return;
-    k_backward_pixels<<<tiles, kStage, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb, d_image,
+    k_backward_pixels<<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb, d_image,
                                                 acc);
     OSB_LAUNCHED(1);
 }

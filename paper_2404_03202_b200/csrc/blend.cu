@@ -1,14 +1,11 @@
 // blend.cu — K3: per-tile front-to-back alpha blending (proj/src/rasterizer.cpp:100-157).
 //
-// One 256-thread CTA per 16x16 tile, one pixel per thread. The tile list is walked in chunks of
-// 256 entries staged cooperatively into shared memory (FP64 centre -> tile-relative FP32 offsets,
-// seam-wrapped once per (entry, tile)). Each warp (2 pixel rows) then compacts the chunk to the
-// entries whose conservative alpha >= 1/255 extent reaches its rows and walks only those; the
-// dropped pairs are certain skips, so every decision is unchanged. The CTA leaves the list as soon
-// as all 256 pixels have terminated (__syncthreads_count).
-// FP32 fast path + FP64 guard (pair.cuh): power/alpha decisions near a threshold and T near the
-// 1e-4 stop are decided in FP64 exactly like the reference; a T decision inside the band replays
-// the pixel's prefix in FP64 and the pixel continues in FP64 ("exact mode").
+// One 256-thread CTA per 16x16 tile, one pixel per thread, warps independent (pair.cuh): each
+// warp walks the tile list 32 entries at a time, stages them lane-parallel, keeps the ones that can
+// reach its two rows and blends them in list order; it leaves the list as soon as its 32 pixels have
+// terminated. FP32 fast path + FP64 guard (pair.cuh): power/alpha decisions near a threshold and T
+// near the 1e-4 stop are decided in FP64 exactly like the reference; a T decision inside the band
+// replays the pixel's prefix in FP64 and the pixel continues in FP64 ("exact mode").
 #include "kernels.h"
 #include "pair.cuh"
 
@@ -16,21 +13,24 @@ namespace osb {
 
 namespace {
 
-__global__ void __launch_bounds__(kStage, 3) k_blend(const uint32_t* __restrict__ inst_gid,
-                                                     const uint2* __restrict__ ranges, PreprocessOut pp, int W, int H,
-                                                     int tiles_x, float bg0, float bg1, float bg2, FrameBuffers fb) {
-    __shared__ StageSmem sm;
+__global__ void __launch_bounds__(kTileThreads, 3) k_blend(const uint32_t* __restrict__ inst_gid,
+                                                           const uint2* __restrict__ ranges, PreprocessOut pp, int W,
+                                                           int H, int tiles_x, float bg0, float bg1, float bg2,
+                                                           FrameBuffers fb) {
+    __shared__ WarpStage stage[kTileWarps];
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
-    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
     const int px = tx * kTile + lx, py = ty * kTile + ly;
     const bool inside = px < W && py < H;
     const uint2 range = ranges[tile];
     const double width = W;
     const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
     const float lxo = lx - 7.5f, lyo = ly - 7.5f;
+    const float r0 = 2.0f * warp - 7.5f;
     const float halfW = 0.5f * W, fW = static_cast<float>(W);
+    WarpStage& ws = stage[warp];
 
     float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
     double T64 = 1.0;
@@ -39,27 +39,28 @@ __global__ void __launch_bounds__(kStage, 3) k_blend(const uint32_t* __restrict_
     int stop_at = static_cast<int>(range.y - range.x);  // entries evaluated (work counting)
     bool done = !inside;
 
-    for (uint32_t base = range.x; base < range.y; base += kStage) {
-        __syncthreads();
-        const uint32_t idx = base + threadIdx.x;
-        if (idx < range.y) stage_splat(sm, threadIdx.x, inst_gid[idx], pp.pxy, pp.splat, xc, yc, width);
-        if (__syncthreads_count(done) == kStage) break;
-        const int cnt = min(kStage, static_cast<int>(range.y - base));
-        const int n_act = compact_for_warp(sm, cnt, warp, lane);
-        for (int t = 0; t < n_act && !done; ++t) {
-            const int j = sm.list[warp][t];
-            const float4 A = sm.a[j];
-            const float4 B = sm.b[j];
+    for (uint32_t base = range.x; base < range.y; base += 32) {
+        if (__all_sync(0xffffffffu, done)) break;
+        const uint32_t idx = base + lane;
+        bool reach = false;
+        if (idx < range.y) reach = stage_entry(ws, lane, inst_gid[idx], pp.pxy, pp.splat, xc, yc, width, r0);
+        uint32_t bal = __ballot_sync(0xffffffffu, reach);
+        __syncwarp();
+        while (bal != 0u && !done) {
+            const int j = __ffs(bal) - 1;
+            bal &= bal - 1u;
+            const float4 A = ws.a[j];
+            const float4 B = ws.b[j];
             float dx, dy, power;
             bool unc;
             if (!pair_power(A, B, lxo, lyo, halfW, fW, dx, dy, power, unc)) continue;
-            const float4 Cc = sm.c[j];
+            const float4 Cc = ws.c[j];
             const uint32_t k = base + j;
             float alpha;
             double a64 = 0.0;
             if (unc || exact) {
                 Pair64 p;
-                if (!pair_slow(sm.gid[j], px, py, width, pp.pxy, pp.conic_o, &p)) continue;
+                if (!pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p)) continue;
                 a64 = p.alpha;
                 alpha = static_cast<float>(a64);
             } else {
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(kStage, 3) k_blend(const uint32_t* __restrict_
                     T64 = replay_T(inst_gid, range.x, k, px, py, width, pp.pxy, pp.conic_o);
                     if (!unc) {
                         Pair64 p;
-                        pair_slow(sm.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
+                        pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
                         a64 = p.alpha;
                     }
                     const double Tn64 = T64 * (1.0 - a64);
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(kStage, 3) k_blend(const uint32_t* __restrict_
             ++contrib;
             last = static_cast<int>(k - range.x) + 1;
         }
+        __syncwarp();
     }
     if (inside) {
         const size_t pix = static_cast<size_t>(py) * W + px;
@@ -157,7 +159,7 @@ void launch_blend(const uint32_t* inst_gid, const uint2* ranges, const Preproces
                   int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s) {
     const int tiles = tiles_x * tiles_y;
     if (tiles <= 0) return;
-    k_blend<<<tiles, kStage, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb);
+    k_blend<<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb);
     OSB_LAUNCHED(1);
 }
 

@@ -45,6 +45,7 @@ DeviceGuard::~DeviceGuard() { cudaSetDevice(prev); }
 PreprocessOut Frame::pp() const {
     PreprocessOut o;
     o.depth_key = depth_key.as<uint64_t>();
+    o.depth_key32 = depth_key32.as<uint32_t>();
     o.touched = touched.as<uint32_t>();
     o.rect = rect.as<int4>();
     o.pxy = pxy.as<double2>();
@@ -257,6 +258,7 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
         const size_t pixels = static_cast<size_t>(W) * H;
         const int tiles = f->tiles_x * f->tiles_y;
         f->depth_key.ensure(n * 8);
+        f->depth_key32.ensure(n * 4);
         f->touched.ensure(n * 4);
         f->rect.ensure(n * 16);
         f->pxy.ensure(n * 16);
@@ -288,24 +290,40 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
             launch_preprocess(params_.as<float>(), N, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
                               active_, f->pose, W, H, pp, stream_);
         }
-        // K2a: depth rank (stable by id)
+        // K2a: depth rank = (t_r, id) order. Fast path: stable 4-pass sort of the FP32-rounded
+        // t_r (monotone) + exact FP64 re-ordering inside runs of equal FP32 keys; a run longer
+        // than 32 is flagged and the frame falls back to the full 64-bit sort, decided at the one
+        // host synchronization of the frame below.
         f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(n), 8));
-        bool flipped;
-        {
+        uint32_t* long_run_flag = f->total.as<uint32_t>() + 1;
+        auto depth_rank = [&](bool full) -> const uint32_t* {
             Span sp(*this, kDepthSort);
-            OSB_CUDA_CHECK(cudaMemcpyAsync(f->okeys[0].as<uint64_t>(), pp.depth_key, n_ * 8,
-                                           cudaMemcpyDeviceToDevice, stream_));
             launch_iota(f->ovals[0].as<uint32_t>(), N, stream_);
-            flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(),
-                                     f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N, 64,
-                                     f->sort_ws.as<void>(), stream_);
-        }
-        const uint32_t* order = f->ovals[flipped ? 1 : 0].as<uint32_t>();
+            bool flipped;
+            if (full) {
+                OSB_CUDA_CHECK(cudaMemcpyAsync(f->okeys[0].as<uint64_t>(), pp.depth_key, n_ * 8,
+                                               cudaMemcpyDeviceToDevice, stream_));
+                flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(),
+                                         f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N, 64,
+                                         f->sort_ws.as<void>(), stream_);
+            } else {
+                uint32_t* k32[2] = {f->okeys[0].as<uint32_t>(), f->okeys[1].as<uint32_t>()};
+                OSB_CUDA_CHECK(cudaMemcpyAsync(k32[0], pp.depth_key32, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
+                OSB_CUDA_CHECK(cudaMemsetAsync(long_run_flag, 0, 4, stream_));
+                flipped = radix_sort_u32(k32[0], k32[1], f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N,
+                                         32, f->sort_ws.as<void>(), stream_);
+                launch_fix_runs(k32[flipped ? 1 : 0], f->ovals[flipped ? 1 : 0].as<uint32_t>(), pp.depth_key, N,
+                                long_run_flag, stream_);
+            }
+            return f->ovals[flipped ? 1 : 0].as<uint32_t>();
+        };
+        f->full_depth_sort = false;
+        const uint32_t* order = depth_rank(false);
         // K2b: scan of tiles_touched in depth order fused with the (tile, gid) emission. The
         // instance buffers keep their capacity across frames; only a frame that outgrows them pays
         // a second pass.
         uint32_t M = 0;
-        for (int attempt = 0; attempt < 2; ++attempt) {
+        for (int attempt = 0; attempt < 3; ++attempt) {
             const uint32_t cap = static_cast<uint32_t>(f->ikeys[0].capacity() / 4);
             {
                 Span sp(*this, kScan);
@@ -313,9 +331,15 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
                                  f->ivals[0].as<uint32_t>(), cap, f->total.as<uint32_t>(), f->scan_ws.as<void>(),
                                  stream_);
             }
-            OSB_CUDA_CHECK(cudaMemcpyAsync(&M, f->total.as<uint32_t>(), 4, cudaMemcpyDeviceToHost, stream_));
+            uint32_t host[2] = {0, 0};  // {M, long-run flag}
+            OSB_CUDA_CHECK(cudaMemcpyAsync(host, f->total.as<uint32_t>(), 8, cudaMemcpyDeviceToHost, stream_));
             OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
-            if (N == 0) M = 0;
+            M = N == 0 ? 0 : host[0];
+            if (host[1] != 0 && !f->full_depth_sort) {  // rare: redo the depth rank exactly, re-emit
+                f->full_depth_sort = true;
+                order = depth_rank(true);
+                continue;
+            }
             if (M <= cap && f->ikeys[0].capacity() > 0) break;
             const size_t want = (static_cast<size_t>(M) + M / 4 + 1024) * 4;
             for (int k = 0; k < 2; ++k) {

@@ -57,7 +57,8 @@ struct Frame {
     float bg[3] = {0, 0, 0};
     bool inst_in_alt = false;  // sorted instance gids live in inst_vals[1]
     // per Gaussian (K1 outputs)
-    DevBuf depth_key, touched, rect, pxy, conic_o, splat;
+    DevBuf depth_key, depth_key32, touched, rect, pxy, conic_o, splat;
+    bool full_depth_sort = false;  // set when the FP32-key fast path met a long run of equal keys
     // depth sort
     DevBuf okeys[2], ovals[2], offsets, total;
     // instances

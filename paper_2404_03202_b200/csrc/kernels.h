@@ -15,6 +15,7 @@ long long launches_total();
 // ---- K1 preprocess (preprocess.cu) --------------------------------------------------------
 struct PreprocessOut {
     uint64_t* depth_key;   // N: bit pattern of t_r (monotone), ~0 when culled
+    uint32_t* depth_key32; // N: bit pattern of (float)t_r (monotone, coarser), ~0 when culled
     uint32_t* touched;     // N: tile instances this Gaussian emits
     int4* rect;            // N: {tx0, tx1, ty0, ty1} (tx may wrap)
     double2* pxy;          // N: FP64 pixel centre
@@ -34,6 +35,10 @@ bool radix_sort_u64(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, ui
 bool radix_sort_u32(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
                     int bits, void* ws, cudaStream_t s);
 void launch_iota(uint32_t* v, int n, cudaStream_t s);
+// After a stable sort by the FP32-rounded depth: restore the exact (FP64 depth, id) order inside
+// runs of equal keys; a run longer than 32 sets *flag (caller falls back to the 64-bit sort).
+void launch_fix_runs(const uint32_t* keys, uint32_t* order, const uint64_t* depth_key, int n, uint32_t* flag,
+                     cudaStream_t s);
 // Exclusive scan of touched[order[r]] fused with the emission of (tile, gid) instances in depth
 // order; writes only instances below `capacity`; *total = M (device).
 size_t scan_workspace_bytes(int n);

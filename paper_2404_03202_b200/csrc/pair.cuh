@@ -1,12 +1,16 @@
 // pair.cuh — the per-(pixel, splat) evaluation shared by K3 (blend) and K4a (backward pixels).
 //
-// Shared-memory staging record per tile-list entry (3 x float4, broadcast reads):
+// Tile layout: one 256-thread CTA per 16x16 tile, one pixel per thread; warp w owns pixel rows
+// 2w and 2w+1. Warps are independent (no CTA barrier): each warp walks its tile's list in chunks
+// of 32 entries, stages a chunk lane-parallel into its own shared-memory slots, keeps (ballot) the
+// entries whose conservative alpha >= 1/255 extent (Splat32::ext_x/ext_y) reaches its two rows,
+// and evaluates only those — entries outside are certain skips of the FP32 classifier below, so
+// no decision changes. A warp stops as soon as its 32 pixels have terminated.
+//
+// Staged record per entry (3 x float4, broadcast reads):
 //   A = {cx, cy, ha, hc}   centre offset from the tile centre (FP64 -> FP32, seam-wrapped), 0.5 conic
 //   B = {b, plo, phi, dl}  conic b, pthr -/+ delta, delta (negative: per-pixel seam wrap needed)
 //   Cc = {r, g, bl, o}     colour, opacity
-// plus a warp mask: the 16x16 tile is 8 warps x 2 pixel rows; bit w is set when the entry's
-// conservative extent (Splat32::ext_x/ext_y) reaches a pixel centre of warp w. Entries outside are
-// certain skips in the FP32 classifier below, so dropping them per warp changes no decision.
 // The FP32 decision is "certain" outside the guard band and identical in K3 and K4a (same
 // instructions, --fmad=false, explicit FMAs), so the backward replays the forward's decisions.
 #pragma once
@@ -15,58 +19,41 @@
 
 namespace osb {
 
-constexpr int kStage = 256;
-constexpr int kStageWarps = kStage / 32;
+constexpr int kTileThreads = 256;
+constexpr int kTileWarps = kTileThreads / 32;
 constexpr float kLog2e = 1.4426950408889634f;
 
-struct StageSmem {
-    float4 a[kStage];
-    float4 b[kStage];
-    float4 c[kStage];
-    uint32_t gid[kStage];
-    uint8_t mask[kStage];
-    uint8_t list[kStageWarps][kStage];  // per-warp compacted entry indices
+struct WarpStage {
+    float4 a[32];
+    float4 b[32];
+    float4 c[32];
+    uint32_t gid[32];
 };
 
-// Stage entry j (Gaussian gid) for the tile centred at (xc, yc).
-__device__ __forceinline__ void stage_splat(StageSmem& sm, int j, uint32_t gid, const double2* __restrict__ pxy,
-                                            const Splat32* __restrict__ splat, double xc, double yc,
-                                            double width) {
+// Stage entry `gid` into this lane's slot for the tile centred at (xc, yc); returns whether the
+// entry can reach a pixel centre of the warp's rows (row offsets r0 = 2w - 7.5 and r0 + 1).
+__device__ __forceinline__ bool stage_entry(WarpStage& ws, int lane, uint32_t gid, const double2* __restrict__ pxy,
+                                            const Splat32* __restrict__ splat, double xc, double yc, double width,
+                                            float r0) {
     const double2 pp = pxy[gid];
     const float4* s4 = reinterpret_cast<const float4*>(splat + gid);
     const float4 s0 = s4[0], s1 = s4[1], s2 = s4[2];  // {ha,b,hc,o} {r,g,bl,pthr} {dl,ext_x,ext_y,-}
-    const double w0 = remainder(pp.x - xc, width);
-    const bool seam = fabs(w0) > 0.5 * width - 8.5;
+    // remainder(p.x - xc, W): the offset lies in (-W, W), where the IEEE remainder is one exact
+    // (Sterbenz) add/subtract of W, with ties at +-W/2 left unwrapped
+    double w0 = pp.x - xc;
+    const double half = 0.5 * width;
+    if (w0 > half) w0 -= width;
+    else if (w0 < -half) w0 += width;
+    const bool seam = fabs(w0) > half - 8.5;
     const float cx = static_cast<float>(w0), cy = static_cast<float>(pp.y - yc);
     const float dl = s2.x;
-    sm.a[j] = make_float4(cx, cy, s0.x, s0.z);
-    sm.b[j] = make_float4(s0.y, s1.w - dl, s1.w + dl, seam ? -dl : dl);
-    sm.c[j] = make_float4(s1.x, s1.y, s1.z, s0.w);
-    sm.gid[j] = gid;
-    uint32_t m = 0;
-    if (seam || fabsf(cx) <= 7.5f + s2.y) {
-        // pixel rows r (centre offset r - 7.5) with |cy - (r - 7.5)| <= ext_y
-        const float lo = cy - s2.z + 7.5f, hi = cy + s2.z + 7.5f;
-        const int rlo = lo <= 0.0f ? 0 : (lo > 15.0f ? 16 : static_cast<int>(ceilf(lo)));
-        const int rhi = hi >= 15.0f ? 15 : (hi < 0.0f ? -1 : static_cast<int>(floorf(hi)));
-        if (rlo <= rhi) m = ((2u << (rhi >> 1)) - 1u) & ~((1u << (rlo >> 1)) - 1u);
-    }
-    sm.mask[j] = static_cast<uint8_t>(m);
-}
-
-// Warp `warp` gathers the indices of the staged entries it can reach; returns how many.
-__device__ __forceinline__ int compact_for_warp(StageSmem& sm, int cnt, int warp, int lane) {
-    int n = 0;
-    const uint32_t lt = lanemask_lt();
-    for (int base = 0; base < cnt; base += 32) {
-        const int e = base + lane;
-        const bool act = e < cnt && ((sm.mask[e] >> warp) & 1u);
-        const uint32_t bal = __ballot_sync(0xffffffffu, act);
-        if (act) sm.list[warp][n + __popc(bal & lt)] = static_cast<uint8_t>(e);
-        n += __popc(bal);
-    }
-    __syncwarp();
-    return n;
+    ws.a[lane] = make_float4(cx, cy, s0.x, s0.z);
+    ws.b[lane] = make_float4(s0.y, s1.w - dl, s1.w + dl, seam ? -dl : dl);
+    ws.c[lane] = make_float4(s1.x, s1.y, s1.z, s0.w);
+    ws.gid[lane] = gid;
+    const bool cols = seam || fabsf(cx) <= 7.5f + s2.y;
+    const bool rows = cy - s2.z <= r0 + 1.0f && cy + s2.z >= r0;
+    return cols && rows;
 }
 
 // FP32 power for one pair. Returns false for a certain skip. `unc` is set when the FP32 result

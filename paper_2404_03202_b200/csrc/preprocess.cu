@@ -22,6 +22,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
     Proj64 pr;
     if (!project64(P, stride, pl, gid, pose, W, H, pr)) {
         out.depth_key[gid] = ~0ull;
+        out.depth_key32[gid] = ~0u;
         out.touched[gid] = 0;
         return;
     }
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
     if (!(delta < 1e30)) delta = 1e30;
 
     out.depth_key[gid] = static_cast<uint64_t>(__double_as_longlong(pr.t_r));
+    out.depth_key32[gid] = __float_as_uint(__double2float_rn(pr.t_r));  // monotone non-decreasing in t_r
     out.touched[gid] = touched;
     out.rect[gid] = make_int4(tx0, tx1, ty0, ty1);
     out.pxy[gid] = make_double2(pr.p[0], pr.p[1]);

@@ -450,3 +450,52 @@ void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStrea
 }
 
 }  // namespace osb
+
+namespace osb {
+
+namespace {
+
+constexpr int kMaxRun = 32;
+
+// Exact (FP64 depth, id) order inside runs of equal FP32-rounded depth keys (the stable FP32 sort
+// left each run in ascending id order). Runs longer than kMaxRun raise *flag: the caller then
+// redoes the depth rank with the full 64-bit sort.
+__global__ void k_fix_runs(const uint32_t* __restrict__ keys, uint32_t* __restrict__ order,
+                           const uint64_t* __restrict__ depth_key, int n, uint32_t* __restrict__ flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = keys[i];
+    if (k == 0xFFFFFFFFu) return;                     // culled tail: no instances, order irrelevant
+    if (i > 0 && keys[i - 1] == k) return;            // not a run start
+    if (i + 1 >= n || keys[i + 1] != k) return;       // run of one
+    int e = i + 1;
+    while (e < n && keys[e] == k && e - i <= kMaxRun) ++e;
+    if (e - i > kMaxRun) {
+        atomicExch(flag, 1u);
+        return;
+    }
+    for (int a = i + 1; a < e; ++a) {  // insertion sort by (depth bits, id)
+        const uint32_t g = order[a];
+        const uint64_t d = depth_key[g];
+        int b = a - 1;
+        while (b >= i) {
+            const uint32_t h = order[b];
+            const uint64_t dh = depth_key[h];
+            if (dh < d || (dh == d && h < g)) break;
+            order[b + 1] = h;
+            --b;
+        }
+        order[b + 1] = g;
+    }
+}
+
+}  // namespace
+
+void launch_fix_runs(const uint32_t* keys, uint32_t* order, const uint64_t* depth_key, int n, uint32_t* flag,
+                     cudaStream_t s) {
+    if (n <= 1) return;
+    k_fix_runs<<<(n + 255) / 256, 256, 0, s>>>(keys, order, depth_key, n, flag);
+    OSB_LAUNCHED(1);
+}
+
+}  // namespace osb

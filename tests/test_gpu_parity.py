@@ -198,3 +198,43 @@ def test_accumulate_and_logical_zero():
     for k in ("d_position", "d_sh", "d_rotation", "d_log_scale", "d_opacity_logit"):
         # K4a's FP32 atomics make the summation order run-dependent
         assert np.allclose(g1[k], g2[k], rtol=1e-4, atol=1e-6 * np.max(np.abs(g2[k]))), k
+
+
+def test_backward_with_background(oracle_port):
+    """The background term of d_alpha (gradients.cpp:142) and of the pixel colour."""
+    cloud = _scene("uniform", 3000, 17)
+    pose = scenes.random_pose(np.random.default_rng(19))
+    W, H, bg = 256, 128, (0.3, 0.6, 0.9)
+    d_image = np.random.default_rng(23).uniform(-1.0, 1.0, size=(H, W, 3)) / (W * H)
+    ctx = native.Context(cloud)
+    fr = ctx.render(pose, W, H, background=bg)
+    of = oracle_port.render(cloud, pose, W, H, bg, keep_handle=True)
+    assert np.max(np.abs(fr.image() - of.rgb)) <= IMAGE_ATOL
+    ctx.backward(fr, d_image)
+    g = ctx.gradients()
+    go = oracle_port.backward(of, d_image, cloud, pose)
+    oracle_port.free(of)
+    for k, (nbad, total, maxrel) in grads_close(g, go).items():
+        assert nbad <= max(2, total // 20000), (k, nbad, total, maxrel)
+
+
+@pytest.mark.parametrize("active", [0, 1, 2])
+def test_active_sh_degree(active, oracle_port):
+    """Renders and gradients with fewer active SH bands than stored (sh_warmup)."""
+    cloud = _scene("uniform", 2000, 29)
+    cloud.active_sh_degree = active
+    pose = scenes.identity_pose()
+    W, H = 192, 96
+    d_image = np.random.default_rng(31).uniform(-1.0, 1.0, size=(H, W, 3)) / (W * H)
+    ctx = native.Context(cloud)
+    fr = ctx.render(pose, W, H)
+    of = oracle_port.render(cloud, pose, W, H, keep_handle=True)
+    assert np.max(np.abs(fr.image() - of.rgb)) <= IMAGE_ATOL
+    ctx.backward(fr, d_image)
+    g = ctx.gradients()
+    go = oracle_port.backward(of, d_image, cloud, pose)
+    oracle_port.free(of)
+    bc_active = (active + 1) ** 2
+    assert np.all(g["d_sh"][:, bc_active:, :] == 0.0)
+    for k, (nbad, total, maxrel) in grads_close(g, go).items():
+        assert nbad <= max(2, total // 20000), (k, nbad, total, maxrel)
