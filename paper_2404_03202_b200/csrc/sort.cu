@@ -301,6 +301,14 @@ __global__ void __launch_bounds__(1024) k_scan_block_sums(uint32_t* __restrict__
     if (threadIdx.x == 0) *total = s_carry;
 }
 
+// Instance emission in depth order. Each thread owns 8 consecutive ranks; the warp's instance
+// range is produced in windows of 256 in shared memory — every lane writes the instances of its own
+// Gaussians that fall in the window (incremental tile walk, no search), then the warp copies the
+// window out with coalesced stores. Gaussians with more than kBigCount instances (full-row pole
+// splats) are emitted cooperatively by the whole warp instead, so no lane serialises them.
+constexpr int kWindow = 256;
+constexpr uint32_t kBigCount = 64;
+
 __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restrict__ touched,
                                                        const uint32_t* __restrict__ order,
                                                        const int4* __restrict__ rect, int n, int tiles_x,
@@ -308,13 +316,12 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
                                                        uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                        uint32_t capacity) {
     __shared__ uint32_t s_scan[kSortWarps + 1];
-    __shared__ uint32_t s_off[kScanTile + kSortWarps];  // per warp: kWarpRanks offsets + warp end
-    __shared__ uint32_t s_gid[kScanTile];
+    __shared__ uint32_t s_wk[kSortWarps][kWindow];
+    __shared__ uint32_t s_wv[kSortWarps][kWindow];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // thread owns ranks [r0, r0 + kScanItems) inside its warp's contiguous 256-rank chunk
     const long r0 = static_cast<long>(blockIdx.x) * kScanTile + warp * kWarpRanks + lane * kScanItems;
-    uint32_t v[kScanItems];
-    uint32_t g[kScanItems];
+    uint32_t v[kScanItems], g[kScanItems];
     uint32_t local = 0;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
@@ -326,37 +333,80 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
     uint32_t agg;
     const uint32_t thread_excl = block_exclusive_scan(local, s_scan, &agg);
     const uint32_t block_excl = block_offsets[blockIdx.x];
+    int4 rc[kScanItems];
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) rc[i] = v[i] > 0 ? rect[g[i]] : make_int4(0, 0, 0, 0);
+    uint32_t off[kScanItems];  // block-relative
+    {
+        uint32_t run = thread_excl;
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) {
+            off[i] = run;
+            run += v[i];
+        }
+    }
+    const uint32_t w_begin = __shfl_sync(0xffffffffu, thread_excl, 0);
+    const uint32_t w_end = __shfl_sync(0xffffffffu, thread_excl + local, 31);
 
-    uint32_t run = thread_excl;
-    uint32_t* w_off = s_off + warp * (kWarpRanks + 1);
+    // small Gaussians: lane-serial into the shared window, coalesced copy-out
+    for (uint32_t win = w_begin; win < w_end; win += kWindow) {
+        const uint32_t win_hi = min(win + kWindow, w_end);
+        for (int t = lane; t < kWindow; t += 32) s_wv[warp][t] = 0xFFFFFFFFu;  // big-Gaussian slots stay empty
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < kScanItems; ++i) {
+            if (v[i] == 0 || v[i] > kBigCount) continue;
+            const uint32_t s = max(off[i], win), e = min(off[i] + v[i], win_hi);
+            if (s >= e) continue;
+            const uint32_t wt = static_cast<uint32_t>(rc[i].y - rc[i].x + 1);
+            const uint32_t li = s - off[i];
+            uint32_t row = li / wt, col = li - row * wt;
+            for (uint32_t idx = s; idx < e; ++idx) {
+                int kx = rc[i].x + static_cast<int>(col);
+                kx = kx < 0 ? kx + tiles_x : (kx >= tiles_x ? kx - tiles_x : kx);
+                s_wk[warp][idx - win] = static_cast<uint32_t>((rc[i].z + static_cast<int>(row)) * tiles_x + kx);
+                s_wv[warp][idx - win] = g[i];
+                if (++col == wt) {
+                    col = 0;
+                    ++row;
+                }
+            }
+        }
+        __syncwarp();
+        for (uint32_t t = lane; t < win_hi - win; t += 32) {
+            const uint32_t out = block_excl + win + t;
+            const uint32_t gi = s_wv[warp][t];
+            if (out < capacity && gi != 0xFFFFFFFFu) {  // big Gaussians are emitted below
+                keys[out] = s_wk[warp][t];
+                vals[out] = gi;
+            }
+        }
+        __syncwarp();
+    }
+    // big Gaussians: the whole warp writes each one's instances
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
-        w_off[lane * kScanItems + i] = run;
-        s_gid[warp * kWarpRanks + lane * kScanItems + i] = g[i];
-        run += v[i];
-    }
-    if (lane == 31) w_off[kWarpRanks] = run;  // warp end
-    __syncwarp();
-    const uint32_t w_begin = w_off[0], w_end = w_off[kWarpRanks];
-    for (uint32_t j = w_begin + lane; j < w_end; j += 32) {
-        // owner: last q with w_off[q] <= j (binary search over the warp's 256 offsets)
-        int lo = 0, hi = kWarpRanks - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (w_off[mid] <= j) lo = mid;
-            else hi = mid - 1;
-        }
-        const uint32_t gid = s_gid[warp * kWarpRanks + lo];
-        const int4 rc = rect[gid];
-        const uint32_t li = j - w_off[lo];
-        const uint32_t wt = static_cast<uint32_t>(rc.y - rc.x + 1);
-        const uint32_t row = li / wt;
-        int kx = rc.x + static_cast<int>(li - row * wt);
-        kx = kx < 0 ? kx + tiles_x : (kx >= tiles_x ? kx - tiles_x : kx);
-        const uint32_t out = block_excl + j;
-        if (out < capacity) {
-            keys[out] = static_cast<uint32_t>((rc.z + static_cast<int>(row)) * tiles_x + kx);
-            vals[out] = gid;
+        uint32_t big = __ballot_sync(0xffffffffu, v[i] > kBigCount);
+        while (big) {
+            const int src = __ffs(big) - 1;
+            big &= big - 1u;
+            const uint32_t cnt = __shfl_sync(0xffffffffu, v[i], src);
+            const uint32_t o = __shfl_sync(0xffffffffu, off[i], src);
+            const uint32_t gi = __shfl_sync(0xffffffffu, g[i], src);
+            const int x0 = __shfl_sync(0xffffffffu, rc[i].x, src);
+            const int x1 = __shfl_sync(0xffffffffu, rc[i].y, src);
+            const int y0 = __shfl_sync(0xffffffffu, rc[i].z, src);
+            const uint32_t wt = static_cast<uint32_t>(x1 - x0 + 1);
+            for (uint32_t li = lane; li < cnt; li += 32) {
+                const uint32_t row = li / wt;
+                int kx = x0 + static_cast<int>(li - row * wt);
+                kx = kx < 0 ? kx + tiles_x : (kx >= tiles_x ? kx - tiles_x : kx);
+                const uint32_t out = block_excl + o + li;
+                if (out < capacity) {
+                    keys[out] = static_cast<uint32_t>((y0 + static_cast<int>(row)) * tiles_x + kx);
+                    vals[out] = gi;
+                }
+            }
         }
     }
 }

@@ -20,7 +20,7 @@ import numpy as np
 from .scenes import Cloud
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libosplat_b200.so")
+LIB_PATH = os.environ.get("OSPLAT_LIB", os.path.join(HERE, "libosplat_b200.so"))  # override: A/B builds
 
 OK, INVALID_ARGUMENT, IO, PARSE, VALIDATION, UNSUPPORTED, RUNTIME = range(7)
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "IO", 3: "PARSE", 4: "VALIDATION", 5: "UNSUPPORTED",
