@@ -71,14 +71,14 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const WarpPixel wp = warp_pixel(warp, lane);
+    const int lx = wp.lx, ly = wp.ly;
     const int px = tx * kTile + lx, py = ty * kTile + ly;
     const bool inside = px < W && py < H;
     const uint2 range = ranges[tile];
     const double width = W;
     const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
     const float lxo = lx - 7.5f, lyo = ly - 7.5f;
-    const float r0 = 2.0f * warp - 7.5f;
     const float halfW = 0.5f * W, fW = static_cast<float>(W);
     WarpStage& ws = stage[warp];
 
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
         const int cnt = hi - lo;
         bool reach = false;
         if (lane < cnt)
-            reach = stage_entry(ws, lane, inst_gid[range.x + lo + lane], pp.pxy, pp.splat, xc, yc, width, r0);
+            reach = stage_entry(ws, lane, inst_gid[range.x + lo + lane], pp.pxy, pp.splat, xc, yc, width, wp.r0, wp.c0);
         uint32_t bal = __ballot_sync(0xffffffffu, reach);
         __syncwarp();
         while (bal != 0u) {  // back to front; uniform over the warp (the reduction needs all lanes)

@@ -2,7 +2,7 @@
 //
 // One 256-thread CTA per 16x16 tile, one pixel per thread, warps independent (pair.cuh): each
 // warp walks the tile list 32 entries at a time, stages them lane-parallel, keeps the ones that can
-// reach its two rows and blends them in list order; it leaves the list as soon as its 32 pixels have
+// reach its 8x4 pixel block and blends them in list order; it leaves the list as soon as its 32 pixels have
 // terminated. FP32 fast path + FP64 guard (pair.cuh): power/alpha decisions near a threshold and T
 // near the 1e-4 stop are decided in FP64 exactly like the reference; a T decision inside the band
 // replays the pixel's prefix in FP64 and the pixel continues in FP64 ("exact mode").
@@ -21,14 +21,14 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_blend(const uint32_t* __res
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int lx = threadIdx.x & 15, ly = threadIdx.x >> 4;
+    const WarpPixel wp = warp_pixel(warp, lane);
+    const int lx = wp.lx, ly = wp.ly;
     const int px = tx * kTile + lx, py = ty * kTile + ly;
     const bool inside = px < W && py < H;
     const uint2 range = ranges[tile];
     const double width = W;
     const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
     const float lxo = lx - 7.5f, lyo = ly - 7.5f;
-    const float r0 = 2.0f * warp - 7.5f;
     const float halfW = 0.5f * W, fW = static_cast<float>(W);
     WarpStage& ws = stage[warp];
 
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_blend(const uint32_t* __res
         if (__all_sync(0xffffffffu, done)) break;
         const uint32_t idx = base + lane;
         bool reach = false;
-        if (idx < range.y) reach = stage_entry(ws, lane, inst_gid[idx], pp.pxy, pp.splat, xc, yc, width, r0);
+        if (idx < range.y) reach = stage_entry(ws, lane, inst_gid[idx], pp.pxy, pp.splat, xc, yc, width, wp.r0, wp.c0);
         uint32_t bal = __ballot_sync(0xffffffffu, reach);
         __syncwarp();
         while (bal != 0u && !done) {

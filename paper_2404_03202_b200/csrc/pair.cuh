@@ -1,9 +1,10 @@
 // pair.cuh — the per-(pixel, splat) evaluation shared by K3 (blend) and K4a (backward pixels).
 //
-// Tile layout: one 256-thread CTA per 16x16 tile, one pixel per thread; warp w owns pixel rows
-// 2w and 2w+1. Warps are independent (no CTA barrier): each warp walks its tile's list in chunks
+// Tile layout: one 256-thread CTA per 16x16 tile, one pixel per thread; warp w owns the 8x4 pixel
+// block at columns 8(w&1)..+7, rows 4(w>>1)..+3 (a square-ish block is touched by fewer splats than
+// a 16x2 strip of the same area). Warps are independent (no CTA barrier): each warp walks its tile's list in chunks
 // of 32 entries, stages a chunk lane-parallel into its own shared-memory slots, keeps (ballot) the
-// entries whose conservative alpha >= 1/255 extent (Splat32::ext_x/ext_y) reaches its two rows,
+// entries whose conservative alpha >= 1/255 extent (Splat32::ext_x/ext_y) reaches its pixel block,
 // and evaluates only those — entries outside are certain skips of the FP32 classifier below, so
 // no decision changes. A warp stops as soon as its 32 pixels have terminated.
 //
@@ -23,6 +24,21 @@ constexpr int kTileThreads = 256;
 constexpr int kTileWarps = kTileThreads / 32;
 constexpr float kLog2e = 1.4426950408889634f;
 
+// Pixel of (warp, lane) inside the tile, and the warp block's first row/column offset from the tile
+// centre.
+struct WarpPixel {
+    int lx, ly;
+    float r0, c0;
+};
+__device__ __forceinline__ WarpPixel warp_pixel(int warp, int lane) {
+    WarpPixel w;
+    w.lx = (warp & 1) * 8 + (lane & 7);
+    w.ly = (warp >> 1) * 4 + (lane >> 3);
+    w.r0 = static_cast<float>((warp >> 1) * 4) - 7.5f;
+    w.c0 = static_cast<float>((warp & 1) * 8) - 7.5f;
+    return w;
+}
+
 struct WarpStage {
     float4 a[32];
     float4 b[32];
@@ -31,10 +47,10 @@ struct WarpStage {
 };
 
 // Stage entry `gid` into this lane's slot for the tile centred at (xc, yc); returns whether the
-// entry can reach a pixel centre of the warp's rows (row offsets r0 = 2w - 7.5 and r0 + 1).
+// entry can reach a pixel centre of the warp's block (row offsets r0..r0+3, column offsets c0..c0+7).
 __device__ __forceinline__ bool stage_entry(WarpStage& ws, int lane, uint32_t gid, const double2* __restrict__ pxy,
                                             const Splat32* __restrict__ splat, double xc, double yc, double width,
-                                            float r0) {
+                                            float r0, float c0) {
     const double2 pp = pxy[gid];
     const float4* s4 = reinterpret_cast<const float4*>(splat + gid);
     const float4 s0 = s4[0], s1 = s4[1], s2 = s4[2];  // {ha,b,hc,o} {r,g,bl,pthr} {dl,ext_x,ext_y,-}
@@ -51,8 +67,8 @@ __device__ __forceinline__ bool stage_entry(WarpStage& ws, int lane, uint32_t gi
     ws.b[lane] = make_float4(s0.y, s1.w - dl, s1.w + dl, seam ? -dl : dl);
     ws.c[lane] = make_float4(s1.x, s1.y, s1.z, s0.w);
     ws.gid[lane] = gid;
-    const bool cols = seam || fabsf(cx) <= 7.5f + s2.y;
-    const bool rows = cy - s2.z <= r0 + 1.0f && cy + s2.z >= r0;
+    const bool cols = seam || (cx - s2.y <= c0 + 7.0f && cx + s2.y >= c0);
+    const bool rows = cy - s2.z <= r0 + 3.0f && cy + s2.z >= r0;
     return cols && rows;
 }
 
