@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
         const int cnt = hi - lo;
         bool reach = false;
         if (lane < cnt)
-            reach = stage_entry(ws, lane, inst_gid[range.x + lo + lane], pp.pxy, pp.splat, xc, yc, width, wp.r0, wp.c0);
+            reach = stage_entry(ws, lane, inst_gid[range.x + lo + lane], pp.pxy, pp.splat, xc, yc, width, wp.r0, wp.c0) != 0u;
         uint32_t bal = __ballot_sync(0xffffffffu, reach);
         __syncwarp();
         while (bal != 0u) {  // back to front; uniform over the warp (the reduction needs all lanes)

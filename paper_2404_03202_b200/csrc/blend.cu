@@ -2,7 +2,7 @@
 //
 // One 256-thread CTA per 16x16 tile, one pixel per thread, warps independent (pair.cuh): each
 // warp walks the tile list 32 entries at a time, stages them lane-parallel, keeps the ones that can
-// reach its 8x4 pixel block and blends them in list order; it leaves the list as soon as its 32 pixels have
+// reach its half-warp's 4x4 pixel block and blends them in list order; it leaves the list as soon as its 32 pixels have
 // terminated. FP32 fast path + FP64 guard (pair.cuh): power/alpha decisions near a threshold and T
 // near the 1e-4 stop are decided in FP64 exactly like the reference; a T decision inside the band
 // replays the pixel's prefix in FP64 and the pixel continues in FP64 ("exact mode").
@@ -42,9 +42,11 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_blend(const uint32_t* __res
     for (uint32_t base = range.x; base < range.y; base += 32) {
         if (__all_sync(0xffffffffu, done)) break;
         const uint32_t idx = base + lane;
-        bool reach = false;
+        uint32_t reach = 0u;
         if (idx < range.y) reach = stage_entry(ws, lane, inst_gid[idx], pp.pxy, pp.splat, xc, yc, width, wp.r0, wp.c0);
-        uint32_t bal = __ballot_sync(0xffffffffu, reach);
+        const uint32_t bal0 = __ballot_sync(0xffffffffu, reach & 1u);
+        const uint32_t bal1 = __ballot_sync(0xffffffffu, reach & 2u);
+        uint32_t bal = wp.half ? bal1 : bal0;  // this half-warp's entries; lanes loop independently
         __syncwarp();
         while (bal != 0u && !done) {
             const int j = __ffs(bal) - 1;

@@ -1,11 +1,11 @@
 // pair.cuh — the per-(pixel, splat) evaluation shared by K3 (blend) and K4a (backward pixels).
 //
 // Tile layout: one 256-thread CTA per 16x16 tile, one pixel per thread; warp w owns the 8x4 pixel
-// block at columns 8(w&1)..+7, rows 4(w>>1)..+3 (a square-ish block is touched by fewer splats than
-// a 16x2 strip of the same area). Warps are independent (no CTA barrier): each warp walks its tile's list in chunks
+// block at columns 8(w&1)..+7, rows 4(w>>1)..+3, and each half-warp one 4x4 quarter of it (small
+// square blocks are touched by far fewer splats than 16-pixel strips of the same area). Warps are independent (no CTA barrier): each warp walks its tile's list in chunks
 // of 32 entries, stages a chunk lane-parallel into its own shared-memory slots, keeps (ballot) the
-// entries whose conservative alpha >= 1/255 extent (Splat32::ext_x/ext_y) reaches its pixel block,
-// and evaluates only those — entries outside are certain skips of the FP32 classifier below, so
+// entries whose conservative alpha >= 1/255 extent (Splat32::ext_x/ext_y) reaches each half-warp's
+// 4x4 block (two ballots), and each half evaluates only its own — entries outside are certain skips of the FP32 classifier below, so
 // no decision changes. A warp stops as soon as its 32 pixels have terminated.
 //
 // Staged record per entry (3 x float4, broadcast reads):
@@ -27,13 +27,14 @@ constexpr float kLog2e = 1.4426950408889634f;
 // Pixel of (warp, lane) inside the tile, and the warp block's first row/column offset from the tile
 // centre.
 struct WarpPixel {
-    int lx, ly;
+    int lx, ly, half;
     float r0, c0;
 };
 __device__ __forceinline__ WarpPixel warp_pixel(int warp, int lane) {
     WarpPixel w;
-    w.lx = (warp & 1) * 8 + (lane & 7);
-    w.ly = (warp >> 1) * 4 + (lane >> 3);
+    w.half = lane >> 4;
+    w.lx = (warp & 1) * 8 + w.half * 4 + (lane & 3);
+    w.ly = (warp >> 1) * 4 + ((lane >> 2) & 3);
     w.r0 = static_cast<float>((warp >> 1) * 4) - 7.5f;
     w.c0 = static_cast<float>((warp & 1) * 8) - 7.5f;
     return w;
@@ -46,9 +47,10 @@ struct WarpStage {
     uint32_t gid[32];
 };
 
-// Stage entry `gid` into this lane's slot for the tile centred at (xc, yc); returns whether the
-// entry can reach a pixel centre of the warp's block (row offsets r0..r0+3, column offsets c0..c0+7).
-__device__ __forceinline__ bool stage_entry(WarpStage& ws, int lane, uint32_t gid, const double2* __restrict__ pxy,
+// Stage entry `gid` into this lane's slot for the tile centred at (xc, yc); returns a 2-bit mask:
+// bit h set when the entry can reach a pixel centre of half-warp h's block (row offsets r0..r0+3,
+// column offsets c0+4h..c0+4h+3).
+__device__ __forceinline__ uint32_t stage_entry(WarpStage& ws, int lane, uint32_t gid, const double2* __restrict__ pxy,
                                             const Splat32* __restrict__ splat, double xc, double yc, double width,
                                             float r0, float c0) {
     const double2 pp = pxy[gid];
@@ -67,9 +69,10 @@ __device__ __forceinline__ bool stage_entry(WarpStage& ws, int lane, uint32_t gi
     ws.b[lane] = make_float4(s0.y, s1.w - dl, s1.w + dl, seam ? -dl : dl);
     ws.c[lane] = make_float4(s1.x, s1.y, s1.z, s0.w);
     ws.gid[lane] = gid;
-    const bool cols = seam || (cx - s2.y <= c0 + 7.0f && cx + s2.y >= c0);
-    const bool rows = cy - s2.z <= r0 + 3.0f && cy + s2.z >= r0;
-    return cols && rows;
+    if (!(cy - s2.z <= r0 + 3.0f && cy + s2.z >= r0)) return 0u;
+    if (seam) return 3u;
+    const float lo = cx - s2.y, hi = cx + s2.y;
+    return (lo <= c0 + 3.0f && hi >= c0 ? 1u : 0u) | (lo <= c0 + 7.0f && hi >= c0 + 4.0f ? 2u : 0u);
 }
 
 // FP32 power for one pair. Returns false for a certain skip. `unc` is set when the FP32 result
