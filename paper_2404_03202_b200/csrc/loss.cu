@@ -4,6 +4,8 @@
 // 81-153), evaluated on the top `keep` rows (bottom-row mask) and its exact gradient.
 //
 // Two tiled kernels per image, one CTA per 32x32 output tile and colour channel:
+// Both passes are register-blocked (4 outputs per thread from 14 staged values) so shared-memory
+// traffic is ~3x lower than one output per thread.
 //   S1: x, y tile + 5-px halo -> smem; horizontal then vertical 11-tap passes for the five maps
 //       (mu_x, mu_y, E[xx], E[yy], E[xy]); per-pixel SSIM (block-reduced into one FP64 sum per
 //       channel) and its partials g_mu, g_sxx, g_sxy written as three planes.
@@ -20,6 +22,8 @@ constexpr int kT = 32;              // output tile
 constexpr int kR = 5;               // window radius
 constexpr int kS = kT + 2 * kR;     // staged tile with halo
 constexpr int kLossThreads = 256;
+constexpr int kO = 4;               // outputs per thread along a row (horizontal) or column (vertical)
+constexpr int kG = kT / kO;         // output groups per row / column
 
 __device__ __forceinline__ double block_sum(double v, double* s_red) {
 #pragma unroll
@@ -58,48 +62,72 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(const float* __restri
         sy[r][c] = in ? Y[static_cast<size_t>(gy) * W + gx] : 0.0f;
     }
     __syncthreads();
-    // horizontal pass over all staged rows
-    for (int i = threadIdx.x; i < kS * kT; i += kLossThreads) {
-        const int r = i / kT, c = i % kT;
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+    // horizontal pass over all staged rows; each thread produces 4 consecutive outputs of one row
+    // from 14 staged values (lanes on consecutive rows: conflict-free at the odd pitch)
+    for (int i = threadIdx.x; i < kS * kG; i += kLossThreads) {
+        const int r = i % kS, c0 = (i / kS) * kO;
+        float xv[kO + 2 * kR], yv[kO + 2 * kR];
 #pragma unroll
-        for (int t = 0; t < 2 * kR + 1; ++t) {
-            const float xv = sx[r][c + t], yv = sy[r][c + t], w = win.w[t];
-            a0 = __fmaf_rn(w, xv, a0);
-            a1 = __fmaf_rn(w, yv, a1);
-            a2 = __fmaf_rn(w, xv * xv, a2);
-            a3 = __fmaf_rn(w, yv * yv, a3);
-            a4 = __fmaf_rn(w, xv * yv, a4);
+        for (int j = 0; j < kO + 2 * kR; ++j) {
+            xv[j] = sx[r][c0 + j];
+            yv[j] = sy[r][c0 + j];
         }
-        h[0][r][c] = a0; h[1][r][c] = a1; h[2][r][c] = a2; h[3][r][c] = a3; h[4][r][c] = a4;
+#pragma unroll
+        for (int o = 0; o < kO; ++o) {
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+#pragma unroll
+            for (int t = 0; t < 2 * kR + 1; ++t) {
+                const float x = xv[o + t], y = yv[o + t], w = win.w[t];
+                a0 = __fmaf_rn(w, x, a0);
+                a1 = __fmaf_rn(w, y, a1);
+                a2 = __fmaf_rn(w, x * x, a2);
+                a3 = __fmaf_rn(w, y * y, a3);
+                a4 = __fmaf_rn(w, x * y, a4);
+            }
+            h[0][r][c0 + o] = a0; h[1][r][c0 + o] = a1; h[2][r][c0 + o] = a2; h[3][r][c0 + o] = a3;
+            h[4][r][c0 + o] = a4;
+        }
     }
     __syncthreads();
     const float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
     double local = 0.0;
     float* G = g_planes + static_cast<size_t>(ch) * 3 * plane;
-    for (int i = threadIdx.x; i < kT * kT; i += kLossThreads) {
-        const int r = i / kT, c = i % kT;
-        const int gx = x0 + c, gy = y0 + r;
-        if (gx >= W || gy >= keep) continue;
-        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    // vertical pass: each thread produces 4 consecutive rows of one column (lanes on consecutive
+    // columns)
+    for (int i = threadIdx.x; i < kT * kG; i += kLossThreads) {
+        const int c = i % kT, r0 = (i / kT) * kO;
+        const int gx = x0 + c;
+        float m[5][kO];
 #pragma unroll
-        for (int t = 0; t < 2 * kR + 1; ++t) {
-            const float w = win.w[t];
+        for (int q = 0; q < 5; ++q) {
+            float col[kO + 2 * kR];
 #pragma unroll
-            for (int q = 0; q < 5; ++q) m[q] = __fmaf_rn(w, h[q][r + t][c], m[q]);
+            for (int j = 0; j < kO + 2 * kR; ++j) col[j] = h[q][r0 + j][c];
+#pragma unroll
+            for (int o = 0; o < kO; ++o) {
+                float acc = 0.f;
+#pragma unroll
+                for (int t = 0; t < 2 * kR + 1; ++t) acc = __fmaf_rn(win.w[t], col[o + t], acc);
+                m[q][o] = acc;
+            }
         }
-        const float mx = m[0], my = m[1];
-        const float var_x = m[2] - mx * mx, var_y = m[3] - my * my, cov = m[4] - mx * my;
-        const float a1 = 2.0f * mx * my + C1, a2 = 2.0f * cov + C2;
-        const float b1 = mx * mx + my * my + C1, b2 = var_x + var_y + C2;
-        const float denom = b1 * b2;
-        local += static_cast<double>(a1 * a2 / denom);
-        const float d_a1 = a2 / denom, d_a2 = a1 / denom;
-        const float d_b1 = -(a1 * a2) / (b1 * denom), d_b2 = -(a1 * a2) / (b2 * denom);
-        const size_t p = static_cast<size_t>(gy) * W + gx;
-        G[p] = d_a1 * 2.0f * my + d_b1 * 2.0f * mx + d_a2 * (-2.0f * my) + d_b2 * (-2.0f * mx);
-        G[plane + p] = d_b2;
-        G[2 * plane + p] = d_a2 * 2.0f;
+#pragma unroll
+        for (int o = 0; o < kO; ++o) {
+            const int gy = y0 + r0 + o;
+            if (gx >= W || gy >= keep) continue;
+            const float mx = m[0][o], my = m[1][o];
+            const float var_x = m[2][o] - mx * mx, var_y = m[3][o] - my * my, cov = m[4][o] - mx * my;
+            const float a1 = 2.0f * mx * my + C1, a2 = 2.0f * cov + C2;
+            const float b1 = mx * mx + my * my + C1, b2 = var_x + var_y + C2;
+            const float denom = b1 * b2;
+            local += static_cast<double>(a1 * a2 / denom);
+            const float d_a1 = a2 / denom, d_a2 = a1 / denom;
+            const float d_b1 = -(a1 * a2) / (b1 * denom), d_b2 = -(a1 * a2) / (b2 * denom);
+            const size_t p = static_cast<size_t>(gy) * W + gx;
+            G[p] = d_a1 * 2.0f * my + d_b1 * 2.0f * mx + d_a2 * (-2.0f * my) + d_b2 * (-2.0f * mx);
+            G[plane + p] = d_b2;
+            G[2 * plane + p] = d_a2 * 2.0f;
+        }
     }
     const double s = block_sum(local, s_red);
     if (threadIdx.x == 0) atomicAdd(ssim_sum + ch, s);
@@ -127,45 +155,59 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_bwd(const float* __restri
             for (int q = 0; q < 3; ++q) sg[q][r][c] = in ? G[q * plane + p] : 0.0f;
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < kS * kT; i += kLossThreads) {
-            const int r = i / kT, c = i % kT;
-            float a[3] = {0.f, 0.f, 0.f};
+        for (int i = threadIdx.x; i < kS * kG; i += kLossThreads) {
+            const int r = i % kS, c0 = (i / kS) * kO;
 #pragma unroll
-            for (int t = 0; t < 2 * kR + 1; ++t) {
-                const float w = win.w[t];
+            for (int q = 0; q < 3; ++q) {
+                float row[kO + 2 * kR];
 #pragma unroll
-                for (int q = 0; q < 3; ++q) a[q] = __fmaf_rn(w, sg[q][r][c + t], a[q]);
+                for (int j = 0; j < kO + 2 * kR; ++j) row[j] = sg[q][r][c0 + j];
+#pragma unroll
+                for (int o = 0; o < kO; ++o) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int t = 0; t < 2 * kR + 1; ++t) acc = __fmaf_rn(win.w[t], row[o + t], acc);
+                    h[q][r][c0 + o] = acc;
+                }
             }
-#pragma unroll
-            for (int q = 0; q < 3; ++q) h[q][r][c] = a[q];
         }
         __syncthreads();
     }
     double local = 0.0;
-    for (int i = threadIdx.x; i < kT * kT; i += kLossThreads) {
-        const int r = i / kT, c = i % kT;
-        const int gx = x0 + c, gy = y0 + r;
-        if (gx >= W || gy >= H) continue;
-        const size_t p = ch * plane + static_cast<size_t>(gy) * W + gx;
-        float grad = 0.0f;
-        if (gy < keep) {
-            const float xv = rgb[p], yv = gt[p];
-            const float d = xv - yv;
-            local += fabs(static_cast<double>(d));
-            grad = d > 0.0f ? l1_scale : (d < 0.0f ? -l1_scale : 0.0f);
-            if (ssim_scale != 0.0f) {
-                float cm = 0.f, cxx = 0.f, cxy = 0.f;
+    for (int i = threadIdx.x; i < kT * kG; i += kLossThreads) {
+        const int c = i % kT, r0 = (i / kT) * kO;
+        const int gx = x0 + c;
+        float cv[3][kO];
+        if (ssim_scale != 0.0f) {
 #pragma unroll
-                for (int t = 0; t < 2 * kR + 1; ++t) {
-                    const float w = win.w[t];
-                    cm = __fmaf_rn(w, h[0][r + t][c], cm);
-                    cxx = __fmaf_rn(w, h[1][r + t][c], cxx);
-                    cxy = __fmaf_rn(w, h[2][r + t][c], cxy);
+            for (int q = 0; q < 3; ++q) {
+                float col[kO + 2 * kR];
+#pragma unroll
+                for (int j = 0; j < kO + 2 * kR; ++j) col[j] = h[q][r0 + j][c];
+#pragma unroll
+                for (int o = 0; o < kO; ++o) {
+                    float acc = 0.f;
+#pragma unroll
+                    for (int t = 0; t < 2 * kR + 1; ++t) acc = __fmaf_rn(win.w[t], col[o + t], acc);
+                    cv[q][o] = acc;
                 }
-                grad -= ssim_scale * (cm + 2.0f * xv * cxx + yv * cxy);
             }
         }
-        d_image[p] = grad;
+#pragma unroll
+        for (int o = 0; o < kO; ++o) {
+            const int gy = y0 + r0 + o;
+            if (gx >= W || gy >= H) continue;
+            const size_t p = ch * plane + static_cast<size_t>(gy) * W + gx;
+            float grad = 0.0f;
+            if (gy < keep) {
+                const float xv = rgb[p], yv = gt[p];
+                const float d = xv - yv;
+                local += fabs(static_cast<double>(d));
+                grad = d > 0.0f ? l1_scale : (d < 0.0f ? -l1_scale : 0.0f);
+                if (ssim_scale != 0.0f) grad -= ssim_scale * (cv[0][o] + 2.0f * xv * cv[1][o] + yv * cv[2][o]);
+            }
+            d_image[p] = grad;
+        }
     }
     const double s = block_sum(local, s_red);
     if (threadIdx.x == 0) atomicAdd(abs_sum, s);
