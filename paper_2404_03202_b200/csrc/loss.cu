@@ -24,6 +24,7 @@ constexpr int kS = kT + 2 * kR;     // staged tile with halo
 constexpr int kLossThreads = 256;
 constexpr int kO = 4;               // outputs per thread along a row (horizontal) or column (vertical)
 constexpr int kG = kT / kO;         // output groups per row / column
+constexpr int kStageIters = (kS * kS + kLossThreads - 1) / kLossThreads;
 
 __device__ __forceinline__ double block_sum(double v, double* s_red) {
 #pragma unroll
@@ -54,35 +55,44 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(const float* __restri
     const size_t plane = static_cast<size_t>(W) * H;
     const float* X = rgb + ch * plane;
     const float* Y = gt + ch * plane;
-    for (int i = threadIdx.x; i < kS * kS; i += kLossThreads) {
+#pragma unroll
+    for (int k = 0; k < kStageIters; ++k) {  // unrolled: all loads in flight before the stores
+        const int i = threadIdx.x + k * kLossThreads;
         const int r = i / kS, c = i % kS;
         const int gx = x0 + c - kR, gy = y0 + r - kR;
-        const bool in = gx >= 0 && gx < W && gy >= 0 && gy < keep;
-        sx[r][c] = in ? X[static_cast<size_t>(gy) * W + gx] : 0.0f;
-        sy[r][c] = in ? Y[static_cast<size_t>(gy) * W + gx] : 0.0f;
+        const bool in = i < kS * kS && gx >= 0 && gx < W && gy >= 0 && gy < keep;
+        const float xv = in ? X[static_cast<size_t>(gy) * W + gx] : 0.0f;
+        const float yv = in ? Y[static_cast<size_t>(gy) * W + gx] : 0.0f;
+        if (i < kS * kS) {
+            sx[r][c] = xv;
+            sy[r][c] = yv;
+        }
     }
     __syncthreads();
     // horizontal pass over all staged rows; each thread produces 4 consecutive outputs of one row
     // from 14 staged values (lanes on consecutive rows: conflict-free at the odd pitch)
     for (int i = threadIdx.x; i < kS * kG; i += kLossThreads) {
         const int r = i % kS, c0 = (i / kS) * kO;
-        float xv[kO + 2 * kR], yv[kO + 2 * kR];
+        float xv[kO + 2 * kR], yv[kO + 2 * kR], xx[kO + 2 * kR], yy[kO + 2 * kR], xy[kO + 2 * kR];
 #pragma unroll
         for (int j = 0; j < kO + 2 * kR; ++j) {
             xv[j] = sx[r][c0 + j];
             yv[j] = sy[r][c0 + j];
+            xx[j] = xv[j] * xv[j];
+            yy[j] = yv[j] * yv[j];
+            xy[j] = xv[j] * yv[j];
         }
 #pragma unroll
         for (int o = 0; o < kO; ++o) {
             float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
 #pragma unroll
             for (int t = 0; t < 2 * kR + 1; ++t) {
-                const float x = xv[o + t], y = yv[o + t], w = win.w[t];
-                a0 = __fmaf_rn(w, x, a0);
-                a1 = __fmaf_rn(w, y, a1);
-                a2 = __fmaf_rn(w, x * x, a2);
-                a3 = __fmaf_rn(w, y * y, a3);
-                a4 = __fmaf_rn(w, x * y, a4);
+                const float w = win.w[t];
+                a0 = __fmaf_rn(w, xv[o + t], a0);
+                a1 = __fmaf_rn(w, yv[o + t], a1);
+                a2 = __fmaf_rn(w, xx[o + t], a2);
+                a3 = __fmaf_rn(w, yy[o + t], a3);
+                a4 = __fmaf_rn(w, xy[o + t], a4);
             }
             h[0][r][c0 + o] = a0; h[1][r][c0 + o] = a1; h[2][r][c0 + o] = a2; h[3][r][c0 + o] = a3;
             h[4][r][c0 + o] = a4;
@@ -119,10 +129,13 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(const float* __restri
             const float var_x = m[2][o] - mx * mx, var_y = m[3][o] - my * my, cov = m[4][o] - mx * my;
             const float a1 = 2.0f * mx * my + C1, a2 = 2.0f * cov + C2;
             const float b1 = mx * mx + my * my + C1, b2 = var_x + var_y + C2;
-            const float denom = b1 * b2;
-            local += static_cast<double>(a1 * a2 / denom);
-            const float d_a1 = a2 / denom, d_a2 = a1 / denom;
-            const float d_b1 = -(a1 * a2) / (b1 * denom), d_b2 = -(a1 * a2) / (b2 * denom);
+            // two approximate reciprocals instead of five IEEE divisions (~1 ulp each)
+            const float ib1 = __fdividef(1.0f, b1), ib2 = __fdividef(1.0f, b2);
+            const float inv = ib1 * ib2;
+            const float S = a1 * a2 * inv;
+            local += static_cast<double>(S);
+            const float d_a1 = a2 * inv, d_a2 = a1 * inv;
+            const float d_b1 = -S * ib1, d_b2 = -S * ib2;
             const size_t p = static_cast<size_t>(gy) * W + gx;
             G[p] = d_a1 * 2.0f * my + d_b1 * 2.0f * mx + d_a2 * (-2.0f * my) + d_b2 * (-2.0f * mx);
             G[plane + p] = d_b2;
@@ -146,13 +159,20 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_bwd(const float* __restri
     const size_t plane = static_cast<size_t>(W) * H;
     const float* G = g_planes + static_cast<size_t>(ch) * 3 * plane;
     if (ssim_scale != 0.0f) {
-        for (int i = threadIdx.x; i < kS * kS; i += kLossThreads) {
+#pragma unroll
+        for (int k = 0; k < kStageIters; ++k) {
+            const int i = threadIdx.x + k * kLossThreads;
             const int r = i / kS, c = i % kS;
             const int gx = x0 + c - kR, gy = y0 + r - kR;
-            const bool in = gx >= 0 && gx < W && gy >= 0 && gy < keep;
+            const bool in = i < kS * kS && gx >= 0 && gx < W && gy >= 0 && gy < keep;
             const size_t p = static_cast<size_t>(gy) * W + gx;
+            float g[3];
 #pragma unroll
-            for (int q = 0; q < 3; ++q) sg[q][r][c] = in ? G[q * plane + p] : 0.0f;
+            for (int q = 0; q < 3; ++q) g[q] = in ? G[q * plane + p] : 0.0f;
+            if (i < kS * kS) {
+#pragma unroll
+                for (int q = 0; q < 3; ++q) sg[q][r][c] = g[q];
+            }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < kS * kG; i += kLossThreads) {
