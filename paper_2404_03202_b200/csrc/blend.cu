@@ -39,11 +39,14 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_blend(const uint32_t* __res
     int stop_at = static_cast<int>(range.y - range.x);  // entries evaluated (work counting)
     bool done = !inside;
 
+    uint32_t gid_next = range.x + lane < range.y ? inst_gid[range.x + lane] : 0u;  // ids one chunk ahead
     for (uint32_t base = range.x; base < range.y; base += 32) {
         if (__all_sync(0xffffffffu, done)) break;
         const uint32_t idx = base + lane;
+        const uint32_t gid = gid_next;
+        gid_next = idx + 32 < range.y ? inst_gid[idx + 32] : 0u;
         uint32_t reach = 0u;
-        if (idx < range.y) reach = stage_entry(ws, lane, inst_gid[idx], pp.pxy, pp.splat, xc, yc, width, wp.r0, wp.c0);
+        if (idx < range.y) reach = stage_entry(ws, lane, gid, pp.pxy, pp.splat, xc, yc, width, wp.r0, wp.c0);
         const uint32_t bal0 = __ballot_sync(0xffffffffu, reach & 1u);
         const uint32_t bal1 = __ballot_sync(0xffffffffu, reach & 2u);
         uint32_t bal = wp.half ? bal1 : bal0;  // this half-warp's entries; lanes loop independently
