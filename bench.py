@@ -392,7 +392,7 @@ def run_ours(args):
         "blend": ("fp32", fwd_pairs * INSTR_PER_FWD_PAIR / 1e12, "Tinstr/s", fp32_peak),
         "bwd_pixels": ("fp32", bwd_pairs * INSTR_PER_BWD_PAIR / 1e12, "Tinstr/s", fp32_peak),
         "preprocess": ("hbm", N * (44 + 12 * 16) / 1e9 + N * 44 / 1e9, "GB/s", peaks["hbm_gbs"]),
-        "adam": ("hbm", 32.0 * planes * view.stride / 1e9, "GB/s", peaks["hbm_gbs"]),
+        "adam": ("hbm", 28.0 * planes * view.stride / 1e9, "GB/s", peaks["hbm_gbs"]),  # p,g,m,v in; p,m,v out
         "bwd_gauss": ("hbm", N * 520 / 1e9, "GB/s", peaks["hbm_gbs"]),
         "tile_sort": ("hbm", instances * 32 / 1e9, "GB/s", peaks["hbm_gbs"]),
         "depth_sort": ("hbm", N * 12 * 2 * 8 / 1e9, "GB/s", peaks["hbm_gbs"]),

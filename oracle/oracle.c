@@ -11,6 +11,7 @@
 #include "oracle.h"
 
 #include <math.h>
+#include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
 #include <time.h>
@@ -957,6 +958,199 @@ double oracle_loss(const double* r, const double* gt, int w, int h, double lambd
     free(d_l1);
     free(d_ssim);
     return value;
+}
+
+/* ------------------------------------------------------------------ densification (trainer.cpp) */
+
+/* std::mt19937_64 (libstdc++ mersenne_twister_engine<uint64, 64, 312, 156, 31, 0xb5026f5aa96619e9,
+ * 29, 0x5555555555555555, 17, 0x71d67fffeda60000, 37, 0xfff7eee000000000, 43, 6364136223846793005>). */
+typedef struct {
+    uint64_t x[312];
+    int i;
+} mt64;
+
+static void mt64_seed(mt64* r, uint64_t seed) {
+    r->x[0] = seed;
+    for (int i = 1; i < 312; ++i) r->x[i] = 6364136223846793005ULL * (r->x[i - 1] ^ (r->x[i - 1] >> 62)) + (uint64_t)i;
+    r->i = 312;
+}
+
+static uint64_t mt64_next(mt64* r) {
+    if (r->i >= 312) {
+        const uint64_t upper = ~0ULL << 31, lower = ~upper;
+        for (int k = 0; k < 312; ++k) {
+            uint64_t y = (r->x[k] & upper) | (r->x[(k + 1) % 312] & lower);
+            r->x[k] = r->x[(k + 156) % 312] ^ (y >> 1) ^ ((y & 1ULL) ? 0xb5026f5aa96619e9ULL : 0ULL);
+        }
+        r->i = 0;
+    }
+    uint64_t z = r->x[r->i++];
+    z ^= (z >> 29) & 0x5555555555555555ULL;
+    z ^= (z << 17) & 0x71d67fffeda60000ULL;
+    z ^= (z << 37) & 0xfff7eee000000000ULL;
+    z ^= z >> 43;
+    return z;
+}
+
+/* std::generate_canonical<double, 53>: one 64-bit draw scaled by 2^-64, clamped below 1. */
+static double mt64_canonical(mt64* r) {
+    double v = (double)mt64_next(r) / 18446744073709551616.0;
+    return v >= 1.0 ? nextafter(1.0, 0.0) : v;
+}
+
+/* std::normal_distribution<double>(0, 1) in libstdc++: Marsaglia polar method, second value cached. */
+typedef struct {
+    mt64 eng;
+    int saved_ok;
+    double saved;
+} normal_rng;
+
+static double normal_next(normal_rng* g) {
+    if (g->saved_ok) {
+        g->saved_ok = 0;
+        return g->saved;
+    }
+    double x, y, r2;
+    do {
+        x = 2.0 * mt64_canonical(&g->eng) - 1.0;
+        y = 2.0 * mt64_canonical(&g->eng) - 1.0;
+        r2 = x * x + y * y;
+    } while (r2 > 1.0 || r2 == 0.0);
+    const double mult = sqrt(-2 * log(r2) / r2);
+    g->saved = x * mult;
+    g->saved_ok = 1;
+    return y * mult;
+}
+
+unsigned long long oracle_mix64(unsigned long long x) { /* trainer.cpp:300-306 */
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+static double max3(const double* v) { /* std::max({a, b, c}) */
+    double m = v[0];
+    if (m < v[1]) m = v[1];
+    if (m < v[2]) m = v[2];
+    return m;
+}
+
+static void copy_gaussian(const oracle_cloud* a, int i, const oracle_cloud* b, long j, int bc) {
+    memcpy(b->positions + 3 * j, a->positions + 3 * (size_t)i, 3 * sizeof(double));
+    memcpy(b->rotations + 4 * j, a->rotations + 4 * (size_t)i, 4 * sizeof(double));
+    memcpy(b->log_scales + 3 * j, a->log_scales + 3 * (size_t)i, 3 * sizeof(double));
+    b->opacity_logits[j] = a->opacity_logits[i];
+    memcpy(b->sh + (size_t)j * bc * 3, a->sh + (size_t)i * bc * 3, (size_t)bc * 3 * sizeof(double));
+}
+
+/* densify_and_prune (trainer.cpp:188-275). The extended list is [originals | clones | split
+ * children]; keep flags are decided on it and the survivors are compacted in order, together with
+ * the Adam moments (AdamState::append_zeros + filter, trainer.cpp:100-124). */
+int oracle_densify_and_prune(const oracle_cloud* in, const double* norm_sum, const long* hits,
+                             const double* max_radius, const oracle_adam* st_in, const oracle_densify_cfg* cfg,
+                             double extent, unsigned long long seed, int radius_active, oracle_cloud* out,
+                             oracle_adam* st_out, oracle_edit* summary) {
+    const double t0 = now_s();
+    const int n = in->n, bc = bc_of(in->sh_degree);
+    int* to_clone = (int*)malloc(sizeof(int) * (n > 0 ? n : 1));
+    int* to_split = (int*)malloc(sizeof(int) * (n > 0 ? n : 1));
+    long nc = 0, ns = 0;
+    for (int i = 0; i < n; ++i) {
+        const double g = hits[i] == 0 ? 0.0 : norm_sum[i] / (double)hits[i]; /* gradients.cpp:35-39 */
+        if (g < cfg->densify_grad_threshold) continue;
+        double s[3] = {exp(in->log_scales[3 * i]), exp(in->log_scales[3 * i + 1]), exp(in->log_scales[3 * i + 2])};
+        if (max3(s) > cfg->scale_split_threshold * extent) to_split[ns++] = i;
+        else to_clone[nc++] = i;
+    }
+    const long total = n + nc + 2 * ns;
+    oracle_cloud ext = {(int)total, in->sh_degree, in->active_sh_degree,
+                        (double*)malloc(sizeof(double) * 3 * total), (double*)malloc(sizeof(double) * 3 * bc * total),
+                        (double*)malloc(sizeof(double) * 4 * total), (double*)malloc(sizeof(double) * 3 * total),
+                        (double*)malloc(sizeof(double) * total)};
+    char* keep = (char*)malloc(total > 0 ? total : 1);
+    long* src = (long*)malloc(sizeof(long) * (total > 0 ? total : 1)); /* Adam source row, -1 = zeros */
+    for (int i = 0; i < n; ++i) {
+        copy_gaussian(in, i, &ext, i, bc);
+        keep[i] = 1;
+        src[i] = i;
+    }
+    long w = n;
+    for (long k = 0; k < nc; ++k, ++w) {
+        copy_gaussian(in, to_clone[k], &ext, w, bc);
+        keep[w] = 1;
+        src[w] = -1;
+    }
+    normal_rng rng;
+    mt64_seed(&rng.eng, seed);
+    rng.saved_ok = 0;
+    const double log_split = log(cfg->split_factor);
+    for (long k = 0; k < ns; ++k) {
+        const int p = to_split[k];
+        keep[p] = 0;
+        double qn[4], rot[9];
+        qnormalize(in->rotations + 4 * (size_t)p, qn);
+        quat_rot(qn, rot);
+        double s[3] = {exp(in->log_scales[3 * p]), exp(in->log_scales[3 * p + 1]), exp(in->log_scales[3 * p + 2])};
+        for (int child = 0; child < 2; ++child, ++w) {
+            double xi[3];
+            xi[0] = normal_next(&rng) * s[0];
+            xi[1] = normal_next(&rng) * s[1];
+            xi[2] = normal_next(&rng) * s[2];
+            copy_gaussian(in, p, &ext, w, bc);
+            double d[3];
+            m3v(rot, xi, d);
+            for (int c = 0; c < 3; ++c) {
+                ext.positions[3 * w + c] = in->positions[3 * (size_t)p + c] + d[c];
+                ext.log_scales[3 * w + c] = in->log_scales[3 * (size_t)p + c] - log_split;
+            }
+            keep[w] = 1;
+            src[w] = -1;
+        }
+    }
+    /* prune (trainer.cpp:244-262) */
+    long removed = 0;
+    for (long i = 0; i < total; ++i) {
+        if (keep[i]) {
+            const double o = 1.0 / (1.0 + exp(-ext.opacity_logits[i]));
+            double s[3] = {exp(ext.log_scales[3 * i]), exp(ext.log_scales[3 * i + 1]), exp(ext.log_scales[3 * i + 2])};
+            if (o < cfg->prune_opacity) keep[i] = 0;
+            else if (max3(s) > cfg->prune_scale_world * extent) keep[i] = 0;
+            else if (radius_active && i < n && max_radius[i] > cfg->prune_radius_px) keep[i] = 0;
+        }
+        if (!keep[i]) ++removed;
+    }
+    long o = 0;
+    for (long i = 0; i < total; ++i) {
+        if (!keep[i]) continue;
+        copy_gaussian(&ext, (int)i, out, o, bc);
+#define ADAM_ROW(F, K)                                                                                  \
+    if (src[i] >= 0) memcpy(st_out->F + (size_t)o * (K), st_in->F + (size_t)src[i] * (K), sizeof(double) * (K)); \
+    else memset(st_out->F + (size_t)o * (K), 0, sizeof(double) * (K));
+        ADAM_ROW(m_position, 3) ADAM_ROW(v_position, 3) ADAM_ROW(m_sh, 3 * bc) ADAM_ROW(v_sh, 3 * bc)
+        ADAM_ROW(m_rotation, 4) ADAM_ROW(v_rotation, 4) ADAM_ROW(m_scale, 3) ADAM_ROW(v_scale, 3)
+        ADAM_ROW(m_opacity, 1) ADAM_ROW(v_opacity, 1)
+#undef ADAM_ROW
+        ++o;
+    }
+    out->n = (int)o;
+    out->sh_degree = in->sh_degree;
+    out->active_sh_degree = in->active_sh_degree;
+    st_out->step = st_in->step;
+    summary->cloned = nc;
+    summary->split = ns;
+    summary->pruned = removed - ns;
+    summary->final_count = o;
+    free(ext.positions); free(ext.sh); free(ext.rotations); free(ext.log_scales); free(ext.opacity_logits);
+    free(keep); free(src); free(to_clone); free(to_split);
+    g_last_seconds = now_s() - t0;
+    return 0;
+}
+
+void oracle_reset_opacity(oracle_cloud* c, double ceiling) { /* trainer.cpp:277-280 */
+    const double cap = log(ceiling / (1.0 - ceiling));
+    for (int i = 0; i < c->n; ++i)
+        if (cap < c->opacity_logits[i]) c->opacity_logits[i] = cap;
 }
 
 void oracle_set_threads(int n) { (void)n; }

@@ -99,6 +99,33 @@ void oracle_adam_step(oracle_cloud* cloud, const oracle_grads* grads, oracle_ada
 double oracle_loss(const double* rendered, const double* gt, int width, int height,
                    double lambda_ssim, double mask_bottom_fraction, double* d_image);
 
+/* The TrainConfig fields densify_and_prune reads (proj/include/omnisplat/trainer.hpp:19-51). */
+typedef struct oracle_densify_cfg {
+    double densify_grad_threshold, scale_split_threshold, split_factor;
+    double prune_opacity, prune_scale_world, prune_radius_px;
+} oracle_densify_cfg;
+
+/* EditSummary (proj/include/omnisplat/trainer.hpp:93-98). */
+typedef struct oracle_edit {
+    long cloned, split, pruned, final_count;
+} oracle_edit;
+
+/* densify_and_prune() (proj/src/trainer.cpp:188-275) on a cloud of n Gaussians with its screen
+ * statistics (screen_norm_sum / screen_hits of the GradientBuffer), DensifyStats.max_radius_px and
+ * AdamState; the rng is std::mt19937_64(rng_seed). The edited cloud / state are written to `out` /
+ * `state_out`, whose arrays must hold 3n Gaussians (out->n is set). Returns 0. */
+int oracle_densify_and_prune(const oracle_cloud* in, const double* screen_norm_sum, const long* screen_hits,
+                             const double* max_radius_px, const oracle_adam* state_in,
+                             const oracle_densify_cfg* cfg, double scene_extent, unsigned long long rng_seed,
+                             int radius_prune_active, oracle_cloud* out, oracle_adam* state_out,
+                             oracle_edit* summary);
+
+/* reset_opacity() (proj/src/trainer.cpp:277-280): logits = min(logit, logit(ceiling)). */
+void oracle_reset_opacity(oracle_cloud* cloud, double ceiling);
+
+/* splitmix64 of the trainer's RNG streams (proj/src/trainer.cpp:300-306). */
+unsigned long long oracle_mix64(unsigned long long x);
+
 /* Wall time (steady clock, like eval.cpp:84-87) of the last render / backward / adam_step / loss
  * call, excluding the marshalling between these flat arrays and the implementation's types. */
 double oracle_last_seconds(void);

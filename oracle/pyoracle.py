@@ -106,6 +106,30 @@ class AdamConfig:
 
 
 @dataclass
+class DensifyConfig:
+    """TrainConfig densification fields with the reference defaults (trainer.hpp:19-51)."""
+    densify_grad_threshold: float = 2e-4
+    scale_split_threshold: float = 0.01
+    split_factor: float = 1.6
+    prune_opacity: float = 0.005
+    prune_scale_world: float = 0.1
+    prune_radius_px: float = 20.0
+
+
+class _DensifyCfg(C.Structure):
+    _fields_ = [(f, C.c_double) for f in ("densify_grad_threshold", "scale_split_threshold", "split_factor",
+                                          "prune_opacity", "prune_scale_world", "prune_radius_px")]
+
+
+class _Edit(C.Structure):
+    _fields_ = [("cloned", C.c_long), ("split", C.c_long), ("pruned", C.c_long), ("final_count", C.c_long)]
+
+
+ADAM_FIELDS = ("m_position", "v_position", "m_sh", "v_sh", "m_rotation", "v_rotation", "m_scale", "v_scale",
+               "m_opacity", "v_opacity")
+
+
+@dataclass
 class Frame:
     width: int
     height: int
@@ -161,6 +185,13 @@ class Oracle:
                                          C.POINTER(_AdamCfg), C.c_double, C.c_long]
         lib.oracle_loss.restype = C.c_double
         lib.oracle_loss.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double, _dp]
+        lib.oracle_densify_and_prune.restype = C.c_int
+        lib.oracle_densify_and_prune.argtypes = [C.POINTER(_Cloud), _dp, _lp, _dp, C.POINTER(_Adam),
+                                                 C.POINTER(_DensifyCfg), C.c_double, C.c_ulonglong, C.c_int,
+                                                 C.POINTER(_Cloud), C.POINTER(_Adam), C.POINTER(_Edit)]
+        lib.oracle_reset_opacity.argtypes = [C.POINTER(_Cloud), C.c_double]
+        lib.oracle_mix64.restype = C.c_ulonglong
+        lib.oracle_mix64.argtypes = [C.c_ulonglong]
         lib.oracle_set_threads.argtypes = [C.c_int]
         lib.oracle_threads.restype = C.c_int
         lib.oracle_kind.restype = C.c_char_p
@@ -271,6 +302,51 @@ class Oracle:
         d = np.zeros_like(r)
         v = self.lib.oracle_loss(_ptr(r), _ptr(g), W, H, lambda_ssim, mask_bottom_fraction, _ptr(d))
         return v, d
+
+
+    def densify_and_prune(self, cloud, norm_sum, hits, max_radius, state: AdamState, cfg: DensifyConfig,
+                          extent: float, seed: int, radius_prune_active: bool):
+        """densify_and_prune (trainer.cpp:188-275) -> (new cloud, new AdamState, summary dict)."""
+        import copy
+        n, bc = cloud.n, cloud.basis_count
+        keep = []
+        c = self._cloud(cloud, keep)
+        ns = np.ascontiguousarray(norm_sum, dtype=np.float64)
+        hi = np.ascontiguousarray(hits, dtype=np.int64)
+        mr = np.ascontiguousarray(max_radius, dtype=np.float64)
+        cap = max(3 * n, 1)
+        out = cloud.copy()
+        out.positions, out.sh = np.zeros((cap, 3)), np.zeros((cap, bc, 3))
+        out.rotations, out.log_scales, out.opacity_logits = np.zeros((cap, 4)), np.zeros((cap, 3)), np.zeros(cap)
+        oc = _Cloud(0, cloud.sh_degree, cloud.active_sh_degree,
+                    *[_ptr(a) for a in (out.positions, out.sh, out.rotations, out.log_scales, out.opacity_logits)])
+        sin = [np.ascontiguousarray(getattr(state, f), dtype=np.float64) for f in ADAM_FIELDS]
+        s_in = _Adam(*[_ptr(a) for a in sin], state.step)
+        so = AdamState.zeros(cap, bc)
+        s_out = _Adam(*[_ptr(getattr(so, f)) for f in ADAM_FIELDS], 0)
+        k = _DensifyCfg(*[getattr(cfg, f) for f, _ in _DensifyCfg._fields_])
+        e = _Edit()
+        self.lib.oracle_densify_and_prune(C.byref(c), _ptr(ns), _ptr(hi, _lp), _ptr(mr), C.byref(s_in), C.byref(k),
+                                          float(extent), C.c_ulonglong(seed), int(bool(radius_prune_active)),
+                                          C.byref(oc), C.byref(s_out), C.byref(e))
+        m = oc.n
+        out.positions, out.sh, out.rotations = out.positions[:m].copy(), out.sh[:m].copy(), out.rotations[:m].copy()
+        out.log_scales, out.opacity_logits = out.log_scales[:m].copy(), out.opacity_logits[:m].copy()
+        for f in ADAM_FIELDS:
+            setattr(so, f, getattr(so, f)[:m].copy())
+        so.step = s_out.step
+        return out, so, {"cloned": e.cloned, "split": e.split, "pruned": e.pruned, "final_count": e.final_count}
+
+    def reset_opacity(self, cloud, ceiling: float):
+        """reset_opacity (trainer.cpp:277-280); mutates cloud.opacity_logits in place."""
+        assert cloud.opacity_logits.dtype == np.float64 and cloud.opacity_logits.flags.c_contiguous
+        keep = []
+        c = self._cloud(cloud, keep)
+        c.opacity_logits = _ptr(cloud.opacity_logits)
+        self.lib.oracle_reset_opacity(C.byref(c), float(ceiling))
+
+    def mix64(self, x: int) -> int:
+        return int(self.lib.oracle_mix64(C.c_ulonglong(x & 0xFFFFFFFFFFFFFFFF)))
 
 
 def load(kind: str = "port") -> Oracle:

@@ -5,6 +5,7 @@
 // the reference sources are compiled where they lie and never copied into this repo.
 #include <chrono>
 #include <cstring>
+#include <random>
 #include <vector>
 
 #include "omnisplat/gradients.hpp"
@@ -271,6 +272,85 @@ double oracle_loss(const double* r, const double* gt, int w, int h, double lambd
     }
     if (d_image) std::memcpy(d_image, lr.d_image.data.data(), lr.d_image.data.size() * 8);
     return lr.value;
+}
+
+int oracle_densify_and_prune(const oracle_cloud* in, const double* norm_sum, const long* hits,
+                             const double* max_radius, const oracle_adam* st, const oracle_densify_cfg* cfg,
+                             double extent, unsigned long long seed, int radius_active, oracle_cloud* out,
+                             oracle_adam* st_out, oracle_edit* summary) {
+    GaussianCloud cloud = to_cloud(in);
+    const int bc = cloud.basis_count();
+    const std::size_t n = cloud.size();
+    GradientBuffer buf;
+    buf.resize(n, bc);
+    for (std::size_t i = 0; i < n; ++i) {
+        buf.screen_norm_sum[i] = norm_sum[i];
+        buf.screen_hits[i] = hits[i];
+    }
+    DensifyStats stats;
+    stats.resize(n);
+    for (std::size_t i = 0; i < n; ++i) stats.max_radius_px[i] = max_radius[i];
+    AdamState state;
+    state.step = st->step;
+    auto load = [&](std::vector<double>& v, const double* src, std::size_t k) { v.assign(src, src + k); };
+    load(state.m_position, st->m_position, n * 3);
+    load(state.v_position, st->v_position, n * 3);
+    load(state.m_sh, st->m_sh, n * 3 * bc);
+    load(state.v_sh, st->v_sh, n * 3 * bc);
+    load(state.m_rotation, st->m_rotation, n * 4);
+    load(state.v_rotation, st->v_rotation, n * 4);
+    load(state.m_scale, st->m_scale, n * 3);
+    load(state.v_scale, st->v_scale, n * 3);
+    load(state.m_opacity, st->m_opacity, n);
+    load(state.v_opacity, st->v_opacity, n);
+    TrainConfig tc;
+    tc.densify_grad_threshold = cfg->densify_grad_threshold;
+    tc.scale_split_threshold = cfg->scale_split_threshold;
+    tc.split_factor = cfg->split_factor;
+    tc.prune_opacity = cfg->prune_opacity;
+    tc.prune_scale_world = cfg->prune_scale_world;
+    tc.prune_radius_px = cfg->prune_radius_px;
+    std::mt19937_64 rng(seed);
+    EditSummary e;
+    {
+        Stopwatch sw;
+        e = densify_and_prune(cloud, buf, stats, state, tc, extent, rng, radius_active != 0);
+    }
+    out->n = static_cast<int>(cloud.size());
+    out->sh_degree = cloud.sh_degree;
+    out->active_sh_degree = cloud.active_sh_degree;
+    from_cloud(cloud, out);
+    st_out->step = state.step;
+    auto store = [](const std::vector<double>& v, double* dst) { std::memcpy(dst, v.data(), v.size() * 8); };
+    store(state.m_position, st_out->m_position);
+    store(state.v_position, st_out->v_position);
+    store(state.m_sh, st_out->m_sh);
+    store(state.v_sh, st_out->v_sh);
+    store(state.m_rotation, st_out->m_rotation);
+    store(state.v_rotation, st_out->v_rotation);
+    store(state.m_scale, st_out->m_scale);
+    store(state.v_scale, st_out->v_scale);
+    store(state.m_opacity, st_out->m_opacity);
+    store(state.v_opacity, st_out->v_opacity);
+    summary->cloned = e.cloned;
+    summary->split = e.split;
+    summary->pruned = e.pruned;
+    summary->final_count = static_cast<long>(e.final_count);
+    return 0;
+}
+
+void oracle_reset_opacity(oracle_cloud* c, double ceiling) {
+    GaussianCloud cloud = to_cloud(c);
+    reset_opacity(cloud, ceiling);
+    from_cloud(cloud, c);
+}
+
+unsigned long long oracle_mix64(unsigned long long x) {
+    // trainer.cpp:300-306 lives in an anonymous namespace there; restated for the RNG seeds
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
 }
 
 void oracle_set_threads(int n) { set_thread_count(n); }
