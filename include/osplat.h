@@ -145,6 +145,7 @@ typedef struct osplat_gpu_view {
     size_t n, stride;
     int planes, sh_degree, active_sh_degree;
     long adam_step;
+    float* max_radius_px; /* n: DensifyStats.max_radius_px (trainer.hpp:85-91) */
 } osplat_gpu_view;
 OSPLAT_API osplat_status osplat_gpu_view_buffers(osplat_gpu* ctx, osplat_gpu_view* view);
 
@@ -184,6 +185,59 @@ OSPLAT_API osplat_status osplat_gpu_l1_loss(osplat_gpu* ctx, const osplat_frame*
 OSPLAT_API osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
                                     const float* gt_planar, int gt_on_device, double lambda_ssim,
                                     double mask_bottom_fraction, double* loss);
+
+/* ---- densification control (trainer.cpp:180-280) ---- */
+/* EditSummary (trainer.hpp:93-98). */
+typedef struct osplat_edit_summary {
+    long cloned, split, pruned;
+    size_t final_count;
+} osplat_edit_summary;
+/* DensifyStats::observe (trainer.cpp:180-186): per-Gaussian max screen radius over the frames
+ * observed since the last densification. */
+OSPLAT_API osplat_status osplat_gpu_observe(osplat_gpu* ctx, const osplat_frame* frame);
+/* densify_and_prune (trainer.cpp:188-275) with the config's thresholds (NULL = defaults) on the
+ * accumulated screen statistics; the split offsets come from std::mt19937_64(rng_seed) through
+ * std::normal_distribution<double> exactly as in the reference (Trainer::run seeds it with
+ * mix64(seed ^ mix64(0x5eed + iteration)), trainer.cpp:370). The planes are reallocated: frames
+ * rendered before and device views taken before are invalid afterwards. Gradients, screen
+ * statistics and max radii restart at zero (GradientBuffer/DensifyStats::resize); Adam moments
+ * of kept Gaussians are carried, new ones start at zero. out may be NULL. */
+OSPLAT_API osplat_status osplat_gpu_densify_and_prune(osplat_gpu* ctx, const osplat_config* config, double scene_extent,
+                                                      unsigned long long rng_seed, int radius_prune_active,
+                                                      osplat_edit_summary* out);
+/* reset_opacity (trainer.cpp:277-280): opacity logits clamped to logit(ceiling). */
+OSPLAT_API osplat_status osplat_gpu_reset_opacity(osplat_gpu* ctx, double ceiling);
+/* Host copy of DensifyStats.max_radius_px (n doubles). */
+OSPLAT_API osplat_status osplat_gpu_max_radius(osplat_gpu* ctx, double* max_radius_px);
+/* splitmix64 of the trainer's RNG streams (trainer.cpp:300-306). */
+OSPLAT_API unsigned long long osplat_mix64(unsigned long long x);
+
+/* ---- optimizer-state sidecar and the training loop ---- */
+/* save/load_optimizer_state (dataio.cpp:479-527): the "OSPLADAM" v1 file of the reference
+ * (iteration, Adam step, basis count, ten moment arrays as doubles in AdamState layouts). Loading
+ * requires a cloud of the same size and basis count; *iteration receives the stored iteration. */
+OSPLAT_API osplat_status osplat_gpu_save_state(osplat_gpu* ctx, const char* path, long iteration);
+OSPLAT_API osplat_status osplat_gpu_load_state(osplat_gpu* ctx, const char* path, long* iteration);
+
+/* An H x W x 3 double image from host pixels (the Image of image.hpp) — training targets. */
+OSPLAT_API osplat_status osplat_image_create(int width, int height, const double* rgb, osplat_image** out);
+
+/* capi.h:58 */
+typedef void (*osplat_progress_fn)(void* user, long iteration, double loss, size_t gaussians);
+/* osplat_train (capi.cpp:190-234) on the device over an in-memory view set instead of a
+ * manifest dataset: views poses (row-major 4x4 world->camera, 16 doubles each) and images
+ * (equal sizes); is_test (NULL = all train) selects held-out views (the first one, else the
+ * first training view, is rendered for the PSNR of each log line). Trains the context's current
+ * cloud from start_iteration (Trainer::resume semantics; 0 = fresh) to config->iterations with
+ * Trainer::run's schedule (trainer.cpp:352-392): shuffled views per epoch, SH warm-up, loss,
+ * backward, densify/prune/opacity reset, Adam. scene_extent <= 0 uses the reference rule
+ * (trainer.cpp:282-298: camera centres, else the cloud's positions). With output_dir set it
+ * writes metrics.jsonl, checkpoint_%06ld.ply every checkpoint_interval, final.ply and
+ * final.adam like osplat_train; progress (may be NULL) is called on log iterations. */
+OSPLAT_API osplat_status osplat_gpu_train(osplat_gpu* ctx, const osplat_config* config, size_t views,
+                                          const double* transforms_cw, const osplat_image* const* images,
+                                          const uint8_t* is_test, double scene_extent, long start_iteration,
+                                          const char* output_dir, osplat_progress_fn progress, void* user);
 
 /* Profiling (bench.py roofline evidence). With timing on, every kernel family is bracketed by a
  * CUDA event pair on the context stream; with count_work on, K3 also writes per-pixel visited

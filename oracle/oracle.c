@@ -1022,6 +1022,12 @@ static double normal_next(normal_rng* g) {
     return y * mult;
 }
 
+void oracle_mt64_draws(unsigned long long seed, long count, unsigned long long* out) {
+    mt64 r;
+    mt64_seed(&r, seed);
+    for (long i = 0; i < count; ++i) out[i] = mt64_next(&r);
+}
+
 unsigned long long oracle_mix64(unsigned long long x) { /* trainer.cpp:300-306 */
     x += 0x9e3779b97f4a7c15ULL;
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;

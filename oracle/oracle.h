@@ -123,8 +123,18 @@ int oracle_densify_and_prune(const oracle_cloud* in, const double* screen_norm_s
 /* reset_opacity() (proj/src/trainer.cpp:277-280): logits = min(logit, logit(ceiling)). */
 void oracle_reset_opacity(oracle_cloud* cloud, double ceiling);
 
+/* count raw draws of std::mt19937_64(seed) (Trainer::pick_view's shuffle, trainer.cpp:340-352). */
+void oracle_mt64_draws(unsigned long long seed, long count, unsigned long long* out);
+
 /* splitmix64 of the trainer's RNG streams (proj/src/trainer.cpp:300-306). */
 unsigned long long oracle_mix64(unsigned long long x);
+
+/* Reference-only file writers (ref_shim.cpp; not in the restatement): save_checkpoint
+ * (dataio.cpp:347-382) and save_optimizer_state (dataio.cpp:479-495), for byte-level pins of the
+ * product's PLY and OSPLADAM writers. Return 0 on success. */
+int oracle_ref_save_checkpoint(const oracle_cloud* cloud, const char* path);
+int oracle_ref_save_optimizer_state(const oracle_adam* state, int n, int basis_count, long iteration,
+                                    const char* path);
 
 /* Wall time (steady clock, like eval.cpp:84-87) of the last render / backward / adam_step / loss
  * call, excluding the marshalling between these flat arrays and the implementation's types. */

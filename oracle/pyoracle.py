@@ -190,6 +190,7 @@ class Oracle:
                                                  C.POINTER(_DensifyCfg), C.c_double, C.c_ulonglong, C.c_int,
                                                  C.POINTER(_Cloud), C.POINTER(_Adam), C.POINTER(_Edit)]
         lib.oracle_reset_opacity.argtypes = [C.POINTER(_Cloud), C.c_double]
+        lib.oracle_mt64_draws.argtypes = [C.c_ulonglong, C.c_long, C.POINTER(C.c_ulonglong)]
         lib.oracle_mix64.restype = C.c_ulonglong
         lib.oracle_mix64.argtypes = [C.c_ulonglong]
         lib.oracle_set_threads.argtypes = [C.c_int]
@@ -347,6 +348,36 @@ class Oracle:
 
     def mix64(self, x: int) -> int:
         return int(self.lib.oracle_mix64(C.c_ulonglong(x & 0xFFFFFFFFFFFFFFFF)))
+
+    def save_checkpoint(self, cloud, path: str):
+        """Reference save_checkpoint (dataio.cpp:347-382); reference library only."""
+        keep = []
+        c = self._cloud(cloud, keep)
+        fn = self.lib.oracle_ref_save_checkpoint
+        fn.argtypes, fn.restype = [C.POINTER(_Cloud), C.c_char_p], C.c_int
+        assert fn(C.byref(c), path.encode()) == 0
+
+    def save_optimizer_state(self, state: AdamState, n: int, bc: int, iteration: int, path: str):
+        """Reference save_optimizer_state (dataio.cpp:479-495); reference library only."""
+        arrs = [np.ascontiguousarray(getattr(state, f), dtype=np.float64) for f in ADAM_FIELDS]
+        s = _Adam(*[_ptr(a) for a in arrs], state.step)
+        fn = self.lib.oracle_ref_save_optimizer_state
+        fn.argtypes, fn.restype = [C.POINTER(_Adam), C.c_int, C.c_int, C.c_long, C.c_char_p], C.c_int
+        assert fn(C.byref(s), n, bc, iteration, path.encode()) == 0
+
+    def mt64_draws(self, seed: int, count: int) -> list:
+        out = (C.c_ulonglong * max(count, 1))()
+        self.lib.oracle_mt64_draws(C.c_ulonglong(seed & 0xFFFFFFFFFFFFFFFF), count, out)
+        return [int(out[i]) for i in range(count)]
+
+    def epoch_order(self, train_indices, seed: int, epoch: int) -> list:
+        """Trainer::pick_view's per-epoch Fisher-Yates shuffle (trainer.cpp:340-352)."""
+        order = list(train_indices)
+        draws = self.mt64_draws(self.mix64(seed ^ self.mix64(epoch)), max(len(order) - 1, 0))
+        for k, i in enumerate(range(len(order), 1, -1)):
+            j = draws[k] % i
+            order[i - 1], order[j] = order[j], order[i - 1]
+        return order
 
 
 def load(kind: str = "port") -> Oracle:

@@ -8,6 +8,7 @@
 #include <random>
 #include <vector>
 
+#include "omnisplat/dataio.hpp"
 #include "omnisplat/gradients.hpp"
 #include "omnisplat/parallel.hpp"
 #include "omnisplat/rasterizer.hpp"
@@ -343,6 +344,43 @@ void oracle_reset_opacity(oracle_cloud* c, double ceiling) {
     GaussianCloud cloud = to_cloud(c);
     reset_opacity(cloud, ceiling);
     from_cloud(cloud, c);
+}
+
+int oracle_ref_save_checkpoint(const oracle_cloud* c, const char* path) {
+    try {
+        save_checkpoint(to_cloud(c), path);
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+
+int oracle_ref_save_optimizer_state(const oracle_adam* st, int n, int bc, long iteration, const char* path) {
+    AdamState s;
+    s.step = st->step;
+    const std::size_t N = static_cast<std::size_t>(n);
+    auto load = [&](std::vector<double>& v, const double* src, std::size_t k) { v.assign(src, src + k); };
+    load(s.m_position, st->m_position, N * 3);
+    load(s.v_position, st->v_position, N * 3);
+    load(s.m_sh, st->m_sh, N * 3 * bc);
+    load(s.v_sh, st->v_sh, N * 3 * bc);
+    load(s.m_rotation, st->m_rotation, N * 4);
+    load(s.v_rotation, st->v_rotation, N * 4);
+    load(s.m_scale, st->m_scale, N * 3);
+    load(s.v_scale, st->v_scale, N * 3);
+    load(s.m_opacity, st->m_opacity, N);
+    load(s.v_opacity, st->v_opacity, N);
+    try {
+        save_optimizer_state(s, iteration, bc, path);
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+
+void oracle_mt64_draws(unsigned long long seed, long count, unsigned long long* out) {
+    std::mt19937_64 rng(seed);
+    for (long i = 0; i < count; ++i) out[i] = rng();
 }
 
 unsigned long long oracle_mix64(unsigned long long x) {

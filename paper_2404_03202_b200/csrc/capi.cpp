@@ -2,10 +2,13 @@
 // (proj/src/capi.cpp) plus the device-resident extension. Error mapping follows
 // capi.cpp:41-81: typed errors -> osplat_status, "<ErrorCode>: message" in a thread-local
 // buffer that is cleared on success.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <charconv>
 #include <cstring>
+#include <filesystem>
 #include <fstream>
 #include <memory>
 #include <sstream>
@@ -14,6 +17,7 @@
 
 #include "../../include/osplat.h"
 #include "engine.h"
+#include "trainer.h"
 
 using osb::Engine;
 using osb::HostCloud;
@@ -38,6 +42,7 @@ struct osplat_config {
     long sh_warmup_interval = 1000;
     unsigned long long seed = 0;
     long checkpoint_interval = 0, log_interval = 100;
+    double background[3] = {0.0, 0.0, 0.0};  // JSON-only in the reference (dataio.cpp:611-615)
 };
 struct osplat_gpu {
     std::shared_ptr<Engine> engine;
@@ -99,11 +104,24 @@ osplat_status wrap(Fn&& fn) {
     } catch (const ApiError& e) {
         t_last_error = std::string(code_name(e.code)) + ": " + e.what();
         return map_code(e.code);
-    } catch (const std::invalid_argument& e) {
-        t_last_error = std::string("InvalidArgument: ") + e.what();
-        return OSPLAT_ERR_INVALID_ARGUMENT;
     } catch (const std::exception& e) {
-        t_last_error = e.what();
+        // engine / trainer errors carry the reference ErrorCode name as a "<Name>: " prefix
+        const std::string m = e.what();
+        static const Code all[] = {Code::ValidationError, Code::StateMismatch,     Code::DimensionMismatch,
+                                   Code::ParseError,      Code::UnsupportedFormat, Code::MissingProperty,
+                                   Code::VersionMismatch, Code::IoError,           Code::InvalidArgument};
+        for (Code c : all) {
+            const std::string prefix = std::string(code_name(c)) + ": ";
+            if (m.compare(0, prefix.size(), prefix) == 0) {
+                t_last_error = m;
+                return map_code(c);
+            }
+        }
+        if (dynamic_cast<const std::invalid_argument*>(&e)) {
+            t_last_error = "InvalidArgument: " + m;
+            return OSPLAT_ERR_INVALID_ARGUMENT;
+        }
+        t_last_error = m;
         return OSPLAT_ERR_RUNTIME;
     }
 }
@@ -334,6 +352,72 @@ void planar_to_hwc(const std::vector<float>& planar, int w, int h, double* out) 
     const size_t plane = static_cast<size_t>(w) * h;
     for (size_t i = 0; i < plane; ++i)
         for (int c = 0; c < 3; ++c) out[i * 3 + c] = planar[c * plane + i];
+}
+
+osb::TrainSettings settings_from(const osplat_config* c) {
+    const osplat_config d{};
+    if (!c) c = &d;
+    osb::TrainSettings t;
+    t.lambda_ssim = c->lambda_ssim;
+    t.iterations = c->iterations;
+    t.densify_until = c->densify_until;
+    t.densify_interval = c->densify_interval;
+    t.opacity_reset_interval = c->opacity_reset_interval;
+    t.densify_grad_threshold = c->densify_grad_threshold;
+    t.scale_split_threshold = c->scale_split_threshold;
+    t.split_factor = c->split_factor;
+    t.prune_opacity = c->prune_opacity;
+    t.prune_scale_world = c->prune_scale_world;
+    t.prune_radius_px = c->prune_radius_px;
+    t.opacity_reset_ceiling = c->opacity_reset_ceiling;
+    t.lr = hyper_from(c);
+    t.mask_bottom_fraction = c->mask_bottom_fraction;
+    t.sh_degree = c->sh_degree;
+    t.sh_warmup_interval = c->sh_warmup_interval;
+    t.seed = c->seed;
+    t.checkpoint_interval = c->checkpoint_interval;
+    t.log_interval = c->log_interval;
+    for (int k = 0; k < 3; ++k) t.background[k] = c->background[k];
+    // TrainConfig::validate (trainer.cpp:10-23) with the reference's error code
+    try {
+        t.validate();
+    } catch (const std::invalid_argument& e) {
+        std::string m = e.what();
+        const std::string prefix = "ValidationError: ";
+        if (m.compare(0, prefix.size(), prefix) == 0) m = m.substr(prefix.size());
+        throw ApiError(Code::ValidationError, m);
+    }
+    return t;
+}
+
+// nlohmann::json's number format (shortest round-trip digits; fixed notation for decimal exponents
+// in (-4, 15], ".0" on integral values, else d.ddde+XX) so metrics.jsonl matches the reference's
+// append_metrics_line (dataio.cpp:559-570) byte for byte.
+std::string json_number(double v) {
+    if (!std::isfinite(v)) return "null";
+    if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
+    char buf[64];
+    auto r = std::to_chars(buf, buf + sizeof(buf), v, std::chars_format::scientific);
+    std::string sci(buf, r.ptr);
+    std::string out;
+    if (sci[0] == '-') {
+        out = "-";
+        sci = sci.substr(1);
+    }
+    const size_t epos = sci.find('e');
+    std::string digits = sci.substr(0, epos);
+    digits.erase(std::remove(digits.begin(), digits.end(), '.'), digits.end());
+    const int exp10 = std::stoi(sci.substr(epos + 1));
+    const int k = static_cast<int>(digits.size());
+    const int n = exp10 + 1;  // position of the decimal point
+    if (k <= n && n <= 15) return out + digits + std::string(n - k, '0') + ".0";
+    if (0 < n && n <= 15) return out + digits.substr(0, n) + "." + digits.substr(n);
+    if (-4 < n && n <= 0) return out + "0." + std::string(-n, '0') + digits;
+    std::string m = k == 1 ? digits : digits.substr(0, 1) + "." + digits.substr(1);
+    const int e = n - 1;
+    char eb[16];
+    std::snprintf(eb, sizeof(eb), "e%c%02d", e < 0 ? '-' : '+', e < 0 ? -e : e);
+    return out + m + eb;
 }
 
 }  // namespace
@@ -643,6 +727,7 @@ osplat_status osplat_gpu_view_buffers(osplat_gpu* ctx, osplat_gpu_view* v) {
     v->sh_degree = e.sh_degree();
     v->active_sh_degree = e.active_sh_degree();
     v->adam_step = e.adam_step_count();
+    v->max_radius_px = e.max_radius();
     t_last_error.clear();
     return OSPLAT_OK;
 }
@@ -650,7 +735,7 @@ osplat_status osplat_gpu_view_buffers(osplat_gpu* ctx, osplat_gpu_view* v) {
 static void validate_frame(osplat_gpu* ctx, const osplat_frame* frame) {
     if (frame->engine.get() != ctx->engine.get())
         throw ApiError(Code::StateMismatch, "frame was rendered by another context");
-    if (static_cast<size_t>(frame->frame->n) != ctx->engine->n())
+    if (static_cast<size_t>(frame->frame->n) != ctx->engine->n() || frame->frame->generation != ctx->engine->generation())
         throw ApiError(Code::StateMismatch, "render output does not match the given scene");
 }
 
@@ -728,6 +813,166 @@ osplat_status osplat_gpu_zero_grad(osplat_gpu* ctx) {
 osplat_status osplat_gpu_reset_screen_stats(osplat_gpu* ctx) {
     if (!ctx) return invalid("osplat_gpu_reset_screen_stats: null context");
     return wrap([&] { ctx->engine->reset_screen_stats(); });
+}
+
+osplat_status osplat_gpu_observe(osplat_gpu* ctx, const osplat_frame* frame) {
+    if (!ctx || !frame) return invalid("osplat_gpu_observe: null argument");
+    return wrap([&] {
+        validate_frame(ctx, frame);
+        ctx->engine->observe(frame->frame);
+    });
+}
+
+static osb::DensifyArgs densify_args(const osplat_config* c, double extent, int radius_active) {
+    const osplat_config d{};
+    if (!c) c = &d;
+    if (c->densify_grad_threshold <= 0.0 || c->scale_split_threshold <= 0.0 || c->split_factor <= 0.0 ||
+        c->prune_opacity <= 0.0 || c->prune_scale_world <= 0.0 || c->prune_radius_px <= 0.0)
+        throw ApiError(Code::ValidationError, "densification thresholds must be positive");
+    osb::DensifyArgs a;
+    a.grad_threshold = c->densify_grad_threshold;
+    a.split_scale = c->scale_split_threshold * extent;
+    a.log_split = std::log(c->split_factor);
+    a.prune_opacity = c->prune_opacity;
+    a.prune_scale = c->prune_scale_world * extent;
+    a.prune_radius = c->prune_radius_px;
+    a.radius_active = radius_active != 0;
+    return a;
+}
+
+osplat_status osplat_gpu_densify_and_prune(osplat_gpu* ctx, const osplat_config* config, double extent,
+                                           unsigned long long rng_seed, int radius_prune_active,
+                                           osplat_edit_summary* out) {
+    if (!ctx) return invalid("osplat_gpu_densify_and_prune: null context");
+    return wrap([&] {
+        const osb::EditSummary e =
+            ctx->engine->densify_and_prune(densify_args(config, extent, radius_prune_active), rng_seed);
+        if (out) {
+            out->cloned = e.cloned;
+            out->split = e.split;
+            out->pruned = e.pruned;
+            out->final_count = e.final_count;
+        }
+    });
+}
+
+osplat_status osplat_gpu_reset_opacity(osplat_gpu* ctx, double ceiling) {
+    if (!ctx) return invalid("osplat_gpu_reset_opacity: null context");
+    if (!(ceiling > 0.0 && ceiling < 1.0)) return invalid("osplat_gpu_reset_opacity: ceiling must be in (0, 1)");
+    return wrap([&] { ctx->engine->reset_opacity(ceiling); });
+}
+
+osplat_status osplat_gpu_max_radius(osplat_gpu* ctx, double* out) {
+    if (!ctx || !out) return invalid("osplat_gpu_max_radius: null argument");
+    return wrap([&] {
+        Engine& e = *ctx->engine;
+        osb::DeviceGuard g(e.device());
+        std::vector<float> h(e.n());
+        if (!h.empty())
+            OSB_CUDA_CHECK(cudaMemcpyAsync(h.data(), e.max_radius(), h.size() * 4, cudaMemcpyDeviceToHost, e.stream()));
+        OSB_CUDA_CHECK(cudaStreamSynchronize(e.stream()));
+        for (size_t i = 0; i < h.size(); ++i) out[i] = h[i];
+    });
+}
+
+unsigned long long osplat_mix64(unsigned long long x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+osplat_status osplat_image_create(int width, int height, const double* rgb, osplat_image** out) {
+    if (!rgb || !out) return invalid("osplat_image_create: null argument");
+    if (width < 1 || height < 1) return invalid("osplat_image_create: image size must be positive");
+    return wrap([&] {
+        auto img = std::make_unique<osplat_image>();
+        img->width = width;
+        img->height = height;
+        img->data.assign(rgb, rgb + static_cast<size_t>(width) * height * 3);
+        *out = img.release();
+    });
+}
+
+osplat_status osplat_gpu_save_state(osplat_gpu* ctx, const char* path, long iteration) {
+    if (!ctx || !path) return invalid("osplat_gpu_save_state: null argument");
+    return wrap([&] { osb::save_optimizer_state(*ctx->engine, iteration, path); });
+}
+
+osplat_status osplat_gpu_load_state(osplat_gpu* ctx, const char* path, long* iteration) {
+    if (!ctx || !path) return invalid("osplat_gpu_load_state: null argument");
+    return wrap([&] {
+        const long it = osb::load_optimizer_state(*ctx->engine, path);
+        if (iteration) *iteration = it;
+    });
+}
+
+osplat_status osplat_gpu_train(osplat_gpu* ctx, const osplat_config* config, size_t views,
+                               const double* transforms_cw, const osplat_image* const* images, const uint8_t* is_test,
+                               double scene_extent, long start_iteration, const char* output_dir,
+                               osplat_progress_fn progress, void* user) {
+    if (!ctx || !transforms_cw || !images) return invalid("osplat_gpu_train: null argument");
+    if (views == 0) return invalid("osplat_gpu_train: no views");
+    return wrap([&] {
+        namespace fs = std::filesystem;
+        const osb::TrainSettings cfg = settings_from(config);
+        Engine& e = *ctx->engine;
+        if (cfg.sh_degree != e.sh_degree())
+            throw ApiError(Code::ValidationError, "config sh_degree does not match the cloud's");
+        const int W = images[0] ? images[0]->width : 0, H = images[0] ? images[0]->height : 0;
+        check_dims(W, H);
+        std::vector<double> poses(12 * views);
+        std::vector<int> train, test;
+        const size_t plane = static_cast<size_t>(W) * H;
+        std::vector<float> planar(views * 3 * plane);
+        for (size_t v = 0; v < views; ++v) {
+            checked_pose(transforms_cw + 16 * v, &poses[12 * v]);
+            const osplat_image* im = images[v];
+            if (!im) throw ApiError(Code::InvalidArgument, "null image");
+            if (im->width != W || im->height != H)
+                throw ApiError(Code::DimensionMismatch, "training images differ in size");
+            float* dst = planar.data() + v * 3 * plane;
+            for (size_t i = 0; i < plane; ++i)
+                for (int c = 0; c < 3; ++c) dst[c * plane + i] = static_cast<float>(im->data[3 * i + c]);
+            (is_test && is_test[v] ? test : train).push_back(static_cast<int>(v));
+        }
+        double extent = scene_extent;
+        if (!(extent > 0.0)) {
+            HostCloud c = e.download();
+            extent = osb::scene_extent(poses, c.positions);
+        }
+        osb::DeviceTrainer trainer(e, cfg, poses, planar.data(), W, H, train, test, extent);
+        planar.clear();
+        planar.shrink_to_fit();
+        std::string metrics_path;
+        if (output_dir) {
+            fs::create_directories(output_dir);
+            metrics_path = (fs::path(output_dir) / "metrics.jsonl").string();
+            std::ofstream(metrics_path, std::ios::trunc).close();
+        }
+        trainer.run(start_iteration, [&](const osb::IterationReport& r) {
+            // capi.cpp:207-224: metrics line + progress on log iterations, periodic checkpoints
+            if (r.logged) {
+                if (!metrics_path.empty()) {
+                    std::ofstream out(metrics_path, std::ios::app);
+                    if (!out) throw ApiError(Code::IoError, "cannot write " + metrics_path);
+                    out << "{\"gaussians\":" << r.gaussians << ",\"iteration\":" << r.iteration
+                        << ",\"loss\":" << json_number(r.loss) << ",\"psnr\":" << json_number(r.heldout_psnr) << "}\n";
+                }
+                if (progress) progress(user, r.iteration, r.loss, r.gaussians);
+            }
+            if (output_dir && cfg.checkpoint_interval > 0 && r.iteration % cfg.checkpoint_interval == 0 &&
+                r.iteration != cfg.iterations) {
+                char name[64];
+                std::snprintf(name, sizeof(name), "checkpoint_%06ld.ply", r.iteration);
+                save_checkpoint(e.download(), (fs::path(output_dir) / name).string());
+            }
+        });
+        if (output_dir) {
+            save_checkpoint(e.download(), (fs::path(output_dir) / "final.ply").string());
+            osb::save_optimizer_state(e, trainer.iteration(), (fs::path(output_dir) / "final.adam").string());
+        }
+    });
 }
 
 osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_config* config, double extent, long iteration,

@@ -6,6 +6,7 @@
 // allocate nothing.
 #include <cmath>
 #include <cstring>
+#include <random>
 #include <stdexcept>
 
 #include "engine.h"
@@ -51,6 +52,7 @@ PreprocessOut Frame::pp() const {
     o.pxy = pxy.as<double2>();
     o.conic_o = conic_o.as<double4>();
     o.splat = splat.as<Splat32>();
+    o.radius = radius.as<float>();
     return o;
 }
 
@@ -158,6 +160,7 @@ void Engine::upload(const HostCloud& c) {
     DeviceGuard g(device_);
     if (c.sh_degree < 0 || c.sh_degree > 3) throw std::invalid_argument("sh_degree must be in 0..3");
     n_ = c.n();
+    ++generation_;
     sh_degree_ = c.sh_degree;
     active_ = c.active_sh_degree < 0 ? 0 : (c.active_sh_degree > c.sh_degree ? c.sh_degree : c.active_sh_degree);
     const int bc = c.bc();
@@ -179,20 +182,27 @@ void Engine::upload(const HostCloud& c) {
     grads_.ensure(elems * 4);
     m_.ensure(elems * 4);
     v_.ensure(elems * 4);
-    acc_.ensure(stride_ * 48);
-    d_screen_.ensure(stride_ * 8);
-    norm_sum_.ensure(stride_ * 8);
-    hits_.ensure(stride_ * 4);
     loss_sum_.ensure(64);
     OSB_CUDA_CHECK(cudaMemcpyAsync(params_.as<float>(), host.data(), elems * 4, cudaMemcpyHostToDevice, stream_));
     OSB_CUDA_CHECK(cudaMemsetAsync(grads_.as<float>(), 0, elems * 4, stream_));
     OSB_CUDA_CHECK(cudaMemsetAsync(m_.as<float>(), 0, elems * 4, stream_));
     OSB_CUDA_CHECK(cudaMemsetAsync(v_.as<float>(), 0, elems * 4, stream_));
+    reset_per_gaussian_state();
+    grads_zero_ = true;
+    adam_step_ = 0;
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::reset_per_gaussian_state() {
+    acc_.ensure(stride_ * 48);
+    d_screen_.ensure(stride_ * 8);
+    norm_sum_.ensure(stride_ * 8);
+    hits_.ensure(stride_ * 4);
+    max_radius_.ensure(stride_ * 4);
     OSB_CUDA_CHECK(cudaMemsetAsync(d_screen_.as<float>(), 0, stride_ * 8, stream_));
     OSB_CUDA_CHECK(cudaMemsetAsync(norm_sum_.as<double>(), 0, stride_ * 8, stream_));
     OSB_CUDA_CHECK(cudaMemsetAsync(hits_.as<int>(), 0, stride_ * 4, stream_));
-    adam_step_ = 0;
-    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    OSB_CUDA_CHECK(cudaMemsetAsync(max_radius_.as<float>(), 0, stride_ * 4, stream_));
 }
 
 HostCloud Engine::download() {
@@ -249,6 +259,7 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
         f->tiles_x = (W + kTile - 1) / kTile;
         f->tiles_y = (H + kTile - 1) / kTile;
         f->n = static_cast<int>(n_);
+        f->generation = generation_;
         f->active_degree = active_;
         std::memcpy(f->pose12, pose12, sizeof(double) * 12);
         for (int i = 0; i < 9; ++i) f->pose.R[i] = pose12[i];
@@ -264,6 +275,7 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
         f->pxy.ensure(n * 16);
         f->conic_o.ensure(n * 32);
         f->splat.ensure(n * sizeof(Splat32));
+        f->radius.ensure(n * 4);
         for (int k = 0; k < 2; ++k) {
             f->okeys[k].ensure(n * 8);
             f->ovals[k].ensure(n * 4);
@@ -382,7 +394,7 @@ void Engine::release(Frame* f) {
 
 void Engine::backward(const Frame* f, const float* d_image, bool accumulate) {
     DeviceGuard g(device_);
-    if (static_cast<size_t>(f->n) != n_) throw std::logic_error("StateMismatch: render output does not match the cloud");
+    if (static_cast<size_t>(f->n) != n_ || f->generation != generation_) throw std::logic_error("StateMismatch: render output does not match the cloud");
     // K4b overwrites (no read of the gradient planes, zeros for culled Gaussians) when the buffer is
     // logically zero or the caller asks for reference overwrite semantics.
     const bool overwrite = !accumulate || grads_zero_;
@@ -515,6 +527,141 @@ void Engine::reset_screen_stats() {
     DeviceGuard g(device_);
     OSB_CUDA_CHECK(cudaMemsetAsync(norm_sum_.as<double>(), 0, stride_ * 8, stream_));
     OSB_CUDA_CHECK(cudaMemsetAsync(hits_.as<int>(), 0, stride_ * 4, stream_));
+}
+
+void Engine::observe(const Frame* f) {
+    DeviceGuard g(device_);
+    if (static_cast<size_t>(f->n) != n_ || f->generation != generation_) throw std::logic_error("StateMismatch: render output does not match the cloud");
+    launch_observe(f->radius.as<float>(), max_radius_.as<float>(), f->n, stream_);
+}
+
+void Engine::reset_opacity(double ceiling) {
+    DeviceGuard g(device_);
+    const Planes pl{(sh_degree_ + 1) * (sh_degree_ + 1)};
+    const double cap = std::log(ceiling / (1.0 - ceiling));  // logit (scene.hpp:58)
+    launch_reset_opacity(params_.as<float>() + static_cast<size_t>(pl.opacity()) * stride_, static_cast<int>(n_), cap,
+                         stream_);
+}
+
+EditSummary Engine::densify_and_prune(const DensifyArgs& a, unsigned long long rng_seed) {
+    DeviceGuard g(device_);
+    EditSummary e;
+    const int n = static_cast<int>(n_);
+    const int bc = (sh_degree_ + 1) * (sh_degree_ + 1);
+    DevBuf code, rank, ws, csrc, ssrc, normals, keep, dest;
+    int nc = 0, ns = 0;
+    if (n > 0) {
+        code.ensure(static_cast<size_t>(n) * 8);
+        rank.ensure(static_cast<size_t>(n) * 8);
+        ws.ensure(densify_scan_workspace_bytes(n));
+        launch_densify_mark(params_.as<float>(), n, static_cast<int>(stride_), bc, norm_sum_.as<double>(),
+                            hits_.as<int>(), a, code.as<unsigned long long>(), stream_);
+        launch_exclusive_scan_u64(code.as<unsigned long long>(), rank.as<unsigned long long>(), n, ws.as<void>(),
+                                  stream_);
+        const size_t nb = (static_cast<size_t>(n) + 1023) / 1024;
+        unsigned long long tot = 0;
+        OSB_CUDA_CHECK(cudaMemcpyAsync(&tot, ws.as<unsigned long long>() + nb, 8, cudaMemcpyDeviceToHost, stream_));
+        OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+        nc = static_cast<int>(tot & 0xffffffffull);
+        ns = static_cast<int>(tot >> 32);
+        csrc.ensure(static_cast<size_t>(nc) * 4);
+        ssrc.ensure(static_cast<size_t>(ns) * 4);
+        launch_densify_sources(code.as<unsigned long long>(), rank.as<unsigned long long>(), n, csrc.as<int>(),
+                               ssrc.as<int>(), stream_);
+    }
+    // The split children's offsets: the reference's own RNG stream (trainer.cpp:215, 227), drawn in
+    // its order (split parents ascending, child 0 then 1, x y z) -> bit-identical normals.
+    std::vector<double> xi(static_cast<size_t>(ns) * 6);
+    {
+        std::mt19937_64 rng(rng_seed);
+        std::normal_distribution<double> normal(0.0, 1.0);
+        for (double& x : xi) x = normal(rng);
+    }
+    normals.ensure(xi.size() * 8);
+    if (!xi.empty())
+        OSB_CUDA_CHECK(cudaMemcpyAsync(normals.as<double>(), xi.data(), xi.size() * 8, cudaMemcpyHostToDevice, stream_));
+    const long total = static_cast<long>(n) + nc + 2L * ns;
+    long kept = 0;
+    if (total > 0) {
+        keep.ensure(static_cast<size_t>(total) * 8);
+        dest.ensure(static_cast<size_t>(total) * 8);
+        ws.ensure(densify_scan_workspace_bytes(total));
+        launch_densify_keep(params_.as<float>(), n, static_cast<int>(stride_), bc, nc, total,
+                            code.as<unsigned long long>(), csrc.as<int>(), ssrc.as<int>(), max_radius_.as<float>(), a,
+                            keep.as<unsigned long long>(), stream_);
+        launch_exclusive_scan_u64(keep.as<unsigned long long>(), dest.as<unsigned long long>(), total, ws.as<void>(),
+                                  stream_);
+        const size_t nb = (static_cast<size_t>(total) + 1023) / 1024;
+        unsigned long long k = 0;
+        OSB_CUDA_CHECK(cudaMemcpyAsync(&k, ws.as<unsigned long long>() + nb, 8, cudaMemcpyDeviceToHost, stream_));
+        OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));  // also keeps xi alive until the copy is done
+        kept = static_cast<long>(k);
+    }
+    e.cloned = nc;
+    e.split = ns;
+    e.pruned = (total - kept) - ns;  // split parents are not "pruned" (trainer.cpp:262)
+    e.final_count = static_cast<size_t>(kept);
+    // gather into new planes (new stride), then swap them in
+    const size_t stride2 = ((kept > 0 ? static_cast<size_t>(kept) : 1) + 31) & ~size_t(31);
+    const size_t elems2 = static_cast<size_t>(planes_) * stride2;
+    DevBuf P2, M2, V2;
+    P2.ensure(elems2 * 4);
+    M2.ensure(elems2 * 4);
+    V2.ensure(elems2 * 4);
+    OSB_CUDA_CHECK(cudaMemsetAsync(P2.as<float>(), 0, elems2 * 4, stream_));
+    OSB_CUDA_CHECK(cudaMemsetAsync(M2.as<float>(), 0, elems2 * 4, stream_));
+    OSB_CUDA_CHECK(cudaMemsetAsync(V2.as<float>(), 0, elems2 * 4, stream_));
+    launch_densify_write(params_.as<float>(), m_.as<float>(), v_.as<float>(), n, static_cast<int>(stride_), bc, nc, total,
+                         keep.as<unsigned long long>(), dest.as<unsigned long long>(), csrc.as<int>(), ssrc.as<int>(),
+                         normals.as<double>(), a, P2.as<float>(), M2.as<float>(), V2.as<float>(),
+                         static_cast<int>(stride2), stream_);
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    params_.swap(P2);
+    m_.swap(M2);
+    v_.swap(V2);
+    n_ = static_cast<size_t>(kept);
+    stride_ = stride2;
+    ++generation_;
+    // GradientBuffer::resize + DensifyStats::resize (trainer.cpp:268-269): gradients and statistics restart
+    grads_.ensure(elems2 * 4);
+    grads_zero_ = true;
+    reset_per_gaussian_state();
+    return e;
+}
+
+double Engine::psnr(const Frame* f, const float* gt) {
+    DeviceGuard g(device_);
+    const long n = 3L * f->W * f->H;
+    scratch_.ensure(64);
+    launch_sq_err(f->rgb.as<float>(), gt, n, scratch_.as<double>(), stream_);
+    double sum = 0.0;
+    OSB_CUDA_CHECK(cudaMemcpyAsync(&sum, scratch_.as<double>(), 8, cudaMemcpyDeviceToHost, stream_));
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    const double cap = 99.0;  // kPsnrCap (metrics.hpp)
+    const double mse = sum / static_cast<double>(n);
+    if (mse <= 0.0) return cap;
+    const double v = 10.0 * std::log10(1.0 / mse);
+    return v < cap ? v : cap;
+}
+
+void Engine::read_adam(std::vector<float>& m, std::vector<float>& v) {
+    DeviceGuard g(device_);
+    const size_t elems = static_cast<size_t>(planes_) * stride_;
+    m.resize(elems);
+    v.resize(elems);
+    OSB_CUDA_CHECK(cudaMemcpyAsync(m.data(), m_.as<float>(), elems * 4, cudaMemcpyDeviceToHost, stream_));
+    OSB_CUDA_CHECK(cudaMemcpyAsync(v.data(), v_.as<float>(), elems * 4, cudaMemcpyDeviceToHost, stream_));
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
+void Engine::write_adam(const std::vector<float>& m, const std::vector<float>& v, long step) {
+    DeviceGuard g(device_);
+    const size_t elems = static_cast<size_t>(planes_) * stride_;
+    if (m.size() != elems || v.size() != elems) throw std::invalid_argument("write_adam: size mismatch");
+    OSB_CUDA_CHECK(cudaMemcpyAsync(m_.as<float>(), m.data(), elems * 4, cudaMemcpyHostToDevice, stream_));
+    OSB_CUDA_CHECK(cudaMemcpyAsync(v_.as<float>(), v.data(), elems * 4, cudaMemcpyHostToDevice, stream_));
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+    adam_step_ = step;
 }
 
 void Engine::synchronize() {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <memory>
+#include <utility>
 #include <vector>
 
 #include "kernels.h"
@@ -30,6 +31,10 @@ public:
     template <typename T>
     T* as() const { return static_cast<T*>(p_); }
     size_t capacity() const { return cap_; }
+    void swap(DevBuf& o) {
+        std::swap(p_, o.p_);
+        std::swap(cap_, o.cap_);
+    }
 
 private:
     void* p_ = nullptr;
@@ -49,15 +54,22 @@ enum KernelId { kPreprocess, kDepthSort, kScan, kEmit, kTileSort, kRanges, kBlen
                 kAdam, kKernelCount };
 const char* kernel_name(int id);
 
+// EditSummary (trainer.hpp:93-98).
+struct EditSummary {
+    long cloned = 0, split = 0, pruned = 0;
+    size_t final_count = 0;
+};
+
 struct Frame {
     int W = 0, H = 0, tiles_x = 0, tiles_y = 0, n = 0, active_degree = 0;
+    unsigned long generation = 0;  // Engine::generation() at render time (parameters' identity)
     uint32_t M = 0;
     double pose12[12];
     Pose pose;
     float bg[3] = {0, 0, 0};
     bool inst_in_alt = false;  // sorted instance gids live in inst_vals[1]
     // per Gaussian (K1 outputs)
-    DevBuf depth_key, depth_key32, touched, rect, pxy, conic_o, splat;
+    DevBuf depth_key, depth_key32, touched, rect, pxy, conic_o, splat, radius;
     bool full_depth_sort = false;  // set when the FP32-key fast path met a long run of equal keys
     // depth sort
     DevBuf okeys[2], ovals[2], offsets, total;
@@ -99,6 +111,16 @@ public:
     void materialize_grads();
     bool grads_zero() const { return grads_zero_; }
     void reset_screen_stats();
+    // Densification control (trainer.cpp:180-280): DensifyStats::observe of a rendered frame,
+    // densify_and_prune with the reference's RNG stream std::mt19937_64(rng_seed), reset_opacity.
+    void observe(const Frame* f);
+    EditSummary densify_and_prune(const DensifyArgs& a, unsigned long long rng_seed);
+    void reset_opacity(double ceiling);
+    // psnr (metrics.cpp:64-74) of a frame against a device planar FP32 image (synchronizes).
+    double psnr(const Frame* f, const float* gt_planar);
+    // Adam moments as raw planes (planes x stride floats each) and the step counter.
+    void read_adam(std::vector<float>& m, std::vector<float>& v);
+    void write_adam(const std::vector<float>& m, const std::vector<float>& v, long step);
     void synchronize();
     // CUDA-event timing per kernel family on the context stream, and per-pixel work counting.
     void set_profiling(bool timing, bool count_work);
@@ -108,6 +130,9 @@ public:
     cudaStream_t stream() const { return stream_; }
     int device() const { return device_; }
     size_t n() const { return n_; }
+    // Bumped whenever the Gaussian set is replaced (upload, densify): frames of an older
+    // generation no longer describe the cloud (StateMismatch).
+    unsigned long generation() const { return generation_; }
     size_t stride() const { return stride_; }
     int planes() const { return planes_; }
     int sh_degree() const { return sh_degree_; }
@@ -120,6 +145,7 @@ public:
     float2* d_screen() const { return d_screen_.as<float2>(); }
     double* norm_sum() const { return norm_sum_.as<double>(); }
     int* hits() const { return hits_.as<int>(); }
+    float* max_radius() const { return max_radius_.as<float>(); }
     float* d_image_buffer(size_t pixels);
     float* gt_buffer(size_t pixels);
     // Host target upload on a side stream (overlaps the render): upload -> wait_target() on the
@@ -133,9 +159,13 @@ private:
     cudaStream_t stream_;
     bool own_stream_;
     size_t n_ = 0, stride_ = 0;
+    unsigned long generation_ = 0;
     int planes_ = 0, sh_degree_ = 0, active_ = 0;
     long adam_step_ = 0;
-    DevBuf params_, grads_, m_, v_, acc_, d_screen_, norm_sum_, hits_, loss_sum_, d_image_, gt_, ssim_planes_;
+    DevBuf scratch_;
+    DevBuf params_, grads_, m_, v_, acc_, d_screen_, norm_sum_, hits_, max_radius_, loss_sum_, d_image_, gt_,
+        ssim_planes_;
+    void reset_per_gaussian_state();  // zero gradients' screen stats, d_screen, max radius (GradientBuffer::resize)
     double last_lambda_ = 0.0;
     bool grads_zero_ = true;
     std::vector<std::unique_ptr<Frame>> pool_;

@@ -21,6 +21,7 @@ struct PreprocessOut {
     double2* pxy;          // N: FP64 pixel centre
     double4* conic_o;      // N: FP64 conic a, b, c and opacity
     Splat32* splat;        // N: FP32 blend record (conic, opacity, colour, guard band, extents)
+    float* radius;         // N: screen radius ceil(3 sqrt(lambda_max)), -1 when culled (DensifyStats)
 };
 void launch_preprocess(const float* params, int n, int stride, int bc, int active_degree, const Pose& pose,
                        int W, int H, const PreprocessOut& out, cudaStream_t s);
@@ -86,6 +87,36 @@ void launch_adam(float* params, float* grads, float* m, float* v, const AdamArgs
 // of scratch (only used when lambda > 0).
 void launch_loss(const float* rgb, const float* gt, int W, int H, int keep_rows, double lambda, float* d_image,
                  float* g_planes, double* sums, cudaStream_t s);
+
+// sum over n of (a - b)^2 in FP64 -> *out (psnr's MSE numerator, metrics.cpp:64-74).
+void launch_sq_err(const float* a, const float* b, long n, double* out, cudaStream_t s);
+
+// ---- densification (densify.cu) -------------------------------------------------------------
+struct DensifyArgs {
+    double grad_threshold;  // densify_grad_threshold
+    double split_scale;     // scale_split_threshold * extent
+    double log_split;       // ln(split_factor)
+    double prune_opacity;
+    double prune_scale;     // prune_scale_world * extent
+    double prune_radius;    // prune_radius_px
+    int radius_active;
+};
+void launch_observe(const float* radius, float* max_radius, int n, cudaStream_t s);
+size_t densify_scan_workspace_bytes(long n);
+void launch_exclusive_scan_u64(const unsigned long long* in, unsigned long long* out, long n, void* ws,
+                               cudaStream_t s);  // ws[nblocks] = total
+void launch_densify_mark(const float* P, int n, int stride, int bc, const double* norm_sum, const int* hits,
+                         const DensifyArgs& a, unsigned long long* code, cudaStream_t s);
+void launch_densify_sources(const unsigned long long* code, const unsigned long long* rank, int n, int* clone_src,
+                            int* split_src, cudaStream_t s);
+void launch_densify_keep(const float* P, int n, int stride, int bc, int nc, long total, const unsigned long long* code,
+                         const int* clone_src, const int* split_src, const float* max_radius, const DensifyArgs& a,
+                         unsigned long long* keep, cudaStream_t s);
+void launch_densify_write(const float* P, const float* M, const float* V, int n, int stride, int bc, int nc, long total,
+                          const unsigned long long* keep, const unsigned long long* dest, const int* clone_src,
+                          const int* split_src, const double* normals, const DensifyArgs& a, float* P2, float* M2,
+                          float* V2, int stride2, cudaStream_t s);
+void launch_reset_opacity(float* opacity_plane, int n, double cap, cudaStream_t s);
 
 }  // namespace osb
 

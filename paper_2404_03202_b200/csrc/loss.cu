@@ -263,4 +263,30 @@ void launch_loss(const float* rgb, const float* gt, int W, int H, int keep_rows,
     OSB_LAUNCHED(1);
 }
 
+namespace {
+
+// sum (a - b)^2 in FP64 (metrics.cpp:64-74, psnr's MSE numerator), one atomic per block.
+__global__ void __launch_bounds__(256) k_sq_err(const float* __restrict__ a, const float* __restrict__ b, long n,
+                                                double* __restrict__ out) {
+    __shared__ double red[8];
+    double acc = 0.0;
+    for (long i = blockIdx.x * 256L + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * 256L) {
+        const double d = static_cast<double>(a[i]) - static_cast<double>(b[i]);
+        acc += d * d;
+    }
+    const double t = block_sum(acc, red);
+    if (threadIdx.x == 0) atomicAdd(out, t);
+}
+
+}  // namespace
+
+void launch_sq_err(const float* a, const float* b, long n, double* out, cudaStream_t s) {
+    OSB_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(double), s));
+    if (n <= 0) return;
+    long blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_sq_err<<<static_cast<int>(blocks), 256, 0, s>>>(a, b, n, out);
+    OSB_LAUNCHED(1);
+}
+
 }  // namespace osb

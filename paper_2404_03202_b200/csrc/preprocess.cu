@@ -24,6 +24,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
         out.depth_key[gid] = ~0ull;
         out.depth_key32[gid] = ~0u;
         out.touched[gid] = 0;
+        out.radius[gid] = -1.0f;
         return;
     }
 
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
     out.depth_key[gid] = static_cast<uint64_t>(__double_as_longlong(pr.t_r));
     out.depth_key32[gid] = __float_as_uint(__double2float_rn(pr.t_r));  // monotone non-decreasing in t_r
     out.touched[gid] = touched;
+    out.radius[gid] = static_cast<float>(radius);
     out.rect[gid] = make_int4(tx0, tx1, ty0, ty1);
     out.pxy[gid] = make_double2(pr.p[0], pr.p[1]);
     out.conic_o[gid] = make_double4(qa, qb, qc, pr.o);

@@ -53,7 +53,14 @@ class GpuView(C.Structure):
     _fields_ = [("params", _vp), ("grads", _vp), ("adam_m", _vp), ("adam_v", _vp), ("d_screen", _vp),
                 ("screen_norm_sum", _vp), ("screen_hits", _vp), ("n", C.c_size_t), ("stride", C.c_size_t),
                 ("planes", C.c_int), ("sh_degree", C.c_int), ("active_sh_degree", C.c_int),
-                ("adam_step", C.c_long)]
+                ("adam_step", C.c_long), ("max_radius_px", _vp)]
+
+
+class EditSummary(C.Structure):
+    _fields_ = [("cloned", C.c_long), ("split", C.c_long), ("pruned", C.c_long), ("final_count", C.c_size_t)]
+
+
+PROGRESS_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_long, C.c_double, C.c_size_t)
 
 
 def _load():
@@ -108,6 +115,16 @@ def _load():
         "osplat_gpu_profile": (S, [_vp, C.c_int, C.c_int]),
         "osplat_gpu_profile_read": (S, [_vp, _dp, _lp, C.c_int]),
         "osplat_kernel_name": (C.c_char_p, [C.c_int]),
+        "osplat_gpu_observe": (S, [_vp, _vp]),
+        "osplat_gpu_densify_and_prune": (S, [_vp, _vp, C.c_double, C.c_ulonglong, C.c_int, C.POINTER(EditSummary)]),
+        "osplat_gpu_reset_opacity": (S, [_vp, C.c_double]),
+        "osplat_gpu_max_radius": (S, [_vp, _dp]),
+        "osplat_mix64": (C.c_ulonglong, [C.c_ulonglong]),
+        "osplat_gpu_save_state": (S, [_vp, C.c_char_p, C.c_long]),
+        "osplat_gpu_load_state": (S, [_vp, C.c_char_p, _lp]),
+        "osplat_image_create": (S, [C.c_int, C.c_int, _dp, C.POINTER(_vp)]),
+        "osplat_gpu_train": (S, [_vp, _vp, C.c_size_t, _dp, C.POINTER(_vp), _u8p, C.c_double, C.c_long, C.c_char_p,
+                                 PROGRESS_FN, C.c_void_p]),
         "osplat_frame_work": (S, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     }
     for name, (res, args) in sig.items():
@@ -383,6 +400,62 @@ class Context:
         cnt = np.zeros(KERNEL_COUNT, dtype=np.int64)
         check(lib.osplat_gpu_profile_read(self.handle, _p(ms), _p(cnt, _lp), int(reset)))
         return {lib.osplat_kernel_name(i).decode(): (float(ms[i]), int(cnt[i])) for i in range(KERNEL_COUNT)}
+
+    # ---- densification control (trainer.cpp:180-280) and the training loop
+    def observe(self, frame: Frame):
+        check(lib.osplat_gpu_observe(self.handle, frame.handle))
+
+    def densify_and_prune(self, config: Config | None, extent: float, rng_seed: int, radius_prune_active: bool) -> dict:
+        e = EditSummary()
+        check(lib.osplat_gpu_densify_and_prune(self.handle, config.handle if config else None, extent,
+                                               C.c_ulonglong(rng_seed & 0xFFFFFFFFFFFFFFFF), int(radius_prune_active),
+                                               C.byref(e)))
+        self._refresh()
+        return {"cloned": e.cloned, "split": e.split, "pruned": e.pruned, "final_count": e.final_count}
+
+    def reset_opacity(self, ceiling: float):
+        check(lib.osplat_gpu_reset_opacity(self.handle, ceiling))
+
+    def max_radius(self) -> np.ndarray:
+        out = np.zeros(self.view().n)
+        check(lib.osplat_gpu_max_radius(self.handle, _p(out)))
+        return out
+
+    def save_state(self, path: str, iteration: int):
+        check(lib.osplat_gpu_save_state(self.handle, path.encode(), iteration))
+
+    def load_state(self, path: str) -> int:
+        it = C.c_long(0)
+        check(lib.osplat_gpu_load_state(self.handle, path.encode(), C.byref(it)))
+        return it.value
+
+    def train(self, config: Config | None, poses, images, is_test=None, extent: float = 0.0, start_iteration: int = 0,
+              output_dir: str | None = None, progress=None):
+        """osplat_gpu_train: Trainer::run over in-memory views (poses: list of pose12, images: list of
+        H x W x 3 float64 arrays). progress(iteration, loss, gaussians) on log iterations."""
+        views = len(poses)
+        T = np.ascontiguousarray(np.stack([transform_of(p) for p in poses]), dtype=np.float64)
+        handles = []
+        for im in images:
+            im = np.ascontiguousarray(im, dtype=np.float64)
+            h = _vp()
+            check(lib.osplat_image_create(im.shape[1], im.shape[0], _p(im), C.byref(h)))
+            handles.append(h)
+        arr = (_vp * views)(*handles)
+        flags = None if is_test is None else np.ascontiguousarray(is_test, dtype=np.uint8)
+        cb = PROGRESS_FN(lambda user, it, loss, n: progress(it, loss, n)) if progress else PROGRESS_FN()
+        try:
+            check(lib.osplat_gpu_train(self.handle, config.handle if config else None, views, _p(T), arr,
+                                       _p(flags, _u8p) if flags is not None else None, extent, start_iteration,
+                                       output_dir.encode() if output_dir else None, cb, None))
+        finally:
+            for h in handles:
+                lib.osplat_image_free(h)
+            self._refresh()
+
+    def _refresh(self):
+        v = self.view()
+        self.n, self.stride = v.n, v.stride
 
     def download(self) -> Cloud:
         h = _vp()

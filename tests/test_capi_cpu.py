@@ -87,6 +87,20 @@ def test_checkpoint_ply_roundtrip(tmp_path):
             assert body[5, props.index(f"f_rest_{bc - 1}")] == np.float32(cloud.sh[5, 1, 1])
 
 
+def test_checkpoint_ply_bytes_match_reference_writer(tmp_path, oracle_ref):
+    """Byte-identical to the reference's own save_checkpoint (dataio.cpp:347-382), and the
+    reference file loads back bit-exactly through osplat_cloud_load."""
+    for deg in (0, 2, 3):
+        cloud = scenes.random_cloud(np.random.default_rng(10 + deg), count=41, sh_degree=deg)
+        cloud.active_sh_degree = max(deg - 1, 0)
+        ours, ref = str(tmp_path / f"o{deg}.ply"), str(tmp_path / f"r{deg}.ply")
+        native.HostCloud.from_cloud(cloud).save(ours)
+        oracle_ref.save_checkpoint(cloud, ref)
+        assert open(ours, "rb").read() == open(ref, "rb").read(), deg
+        back = native.HostCloud.load(ref).to_cloud()
+        assert np.array_equal(back.sh, cloud.sh) and np.array_equal(back.positions, cloud.positions)
+
+
 def test_checkpoint_errors(tmp_path):
     with pytest.raises(native.OsplatError) as e:
         native.HostCloud.load(str(tmp_path / "missing.ply"))

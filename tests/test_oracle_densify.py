@@ -63,3 +63,11 @@ def test_mix64_and_reset_opacity(oracle_port, oracle_ref):
     oracle_ref.reset_opacity(b, 0.01)
     assert np.array_equal(a.opacity_logits, b.opacity_logits)
     assert np.max(a.opacity_logits) == np.log(0.01 / 0.99)
+
+
+def test_mt64_stream_and_epoch_order(oracle_port, oracle_ref):
+    for seed in (0, 5489, 2**64 - 3):
+        assert oracle_port.mt64_draws(seed, 700) == oracle_ref.mt64_draws(seed, 700)
+    assert oracle_port.mt64_draws(5489, 1) == [14514284786278117030]  # std::mt19937_64 default-seed value
+    order = oracle_port.epoch_order(list(range(10)), 7, 3)
+    assert sorted(order) == list(range(10)) and order == oracle_ref.epoch_order(list(range(10)), 7, 3)
