@@ -391,6 +391,14 @@ class Context:
                                         C.byref(loss)))
         return loss.value
 
+    def train_view_noloss(self, pose12, width: int, height: int, gt, gt_on_device: bool, lambda_ssim: float = 0.2,
+                          mask: float = 0.0):
+        """train_view without reading the loss back (no host synchronisation at the end)."""
+        t = transform_of(pose12)
+        ptr = C.c_void_p(gt) if isinstance(gt, int) else gt.ctypes.data_as(C.c_void_p)
+        check(lib.osplat_gpu_train_view(self.handle, _p(t), width, height, ptr, int(gt_on_device), lambda_ssim, mask,
+                                        None))
+
     def profile(self, timing: bool = True, count_work: bool = False):
         check(lib.osplat_gpu_profile(self.handle, int(timing), int(count_work)))
 
