@@ -176,15 +176,30 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// std::remainder(x, w) (rasterizer.cpp:13 wrap_dx) for |x| < 1.5 w, where the quotient rounds to
+// -1, 0 or +1 (a tie at |x| = w/2 rounds to the even 0) and x -/+ w is exact (Sterbenz). Centres
+// lie in [0, W] and pixel centres in (0, W), so |x| < W always; anything else takes the libm path.
+__device__ __forceinline__ double wrap_remainder(double x, double w) {
+    const double h = 0.5 * w;
+    if (!(fabs(x) < 1.5 * w)) return remainder(x, w);
+    if (x > h) return x - w;
+    if (x < -h) return x + w;
+    return x;
+}
+
 // Exact FP64 evaluation of one (pixel, splat) pair — proj/src/rasterizer.cpp:128-134 and
 // proj/src/gradients.cpp:125-132. Returns 0 when skipped; sx, sy are pixel centres.
 __device__ __forceinline__ int pair_fp64(double px, double py, double ca, double cb, double cc,
                                          double o, double sx, double sy, double width, double* g_out,
                                          double* alpha_out) {
-    double dx = remainder(px - sx, width);
+    double dx = wrap_remainder(px - sx, width);
     double dy = py - sy;
     double power = 0.5 * (ca * dx * dx + cc * dy * dy) + cb * dx * dy;
     if (power < 0.0) return 0;
+    // Certain skips first: an FP32 estimate of alpha (relative error < 1e-4 here: the FP64->FP32
+    // roundings of o and power plus ex2.approx) below 0.99/255 means the FP64 alpha is below
+    // 1/255 too, so the (costly) FP64 exp is only evaluated for pairs that can contribute.
+    if (static_cast<float>(o) * __expf(-static_cast<float>(power)) < 0.99f * static_cast<float>(kAlphaMin)) return 0;
     double g = exp(-power);
     double ab = o * g;
     double alpha = ab < kAlphaMax ? ab : kAlphaMax;
