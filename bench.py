@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--views-per-gpu", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-sweep", action="store_true", help="skip the render FPS sweep (pole/seam scenes)")
     return p.parse_args()
 
 
@@ -349,6 +350,46 @@ def run_ours(args):
     rprof = ctx.profile_read(reset=True)
     ctx.profile(timing=False)
 
+    # ---- render FPS sweep (BASELINE configs[2]): the uniform scene over 36 yaws x pitch {0, +-60 deg},
+    # and the pole-heavy (|lat| > 70 deg) and seam-heavy (|lon| > 160 deg) scenes at identity + yaws;
+    # per-frame device time (CUDA events), median and 5th-percentile FPS per variant
+    sweep = None
+    if rank == 0 and not args.no_sweep:
+        def frame_ms(c, poses_list):
+            out = []
+            for p in poses_list:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                c.render(p, W, H).free()
+                b.record(stream)
+                b.synchronize()
+                out.append(a.elapsed_time(b))
+            return out
+
+        def summary(ms):
+            fps = sorted(1e3 / np.asarray(ms))
+            return {"frames": len(ms), "fps_median": float(np.median(fps)), "fps_p5": float(np.percentile(fps, 5)),
+                    "ms_median": float(np.median(ms))}
+
+        yaw_pitch = [scenes.pose12(scenes.rot_x(np.radians(pt)) @ scenes.rot_y(np.radians(yw)))
+                     for pt in (0.0, 60.0, -60.0) for yw in range(0, 360, 10)]
+        frame_ms(ctx, yaw_pitch[:3])
+        sweep = {"uniform_36yaw_x3pitch": summary(frame_ms(ctx, yaw_pitch))}
+        ctx.profile(timing=False, count_work=True)
+        for variant in ("pole", "seam"):
+            vc = native.Context(scenes.synthetic_cloud(N, seed=1, variant=variant), device=local,
+                                stream=stream.cuda_stream)
+            vc.profile(timing=False, count_work=True)
+            fr = vc.render(scenes.identity_pose(), W, H)
+            fp, bp, inst = fr.work()
+            fr.free()
+            vc.profile(timing=False, count_work=False)
+            views = [scenes.pose12(scenes.rot_y(np.radians(yw))) for yw in range(0, 360, 30)]
+            frame_ms(vc, views[:2])
+            sweep[f"{variant}_heavy_12yaw"] = dict(summary(frame_ms(vc, views)), instances=inst, fwd_pairs=fp)
+            vc.free()
+        ctx.profile(timing=False, count_work=False)
+
     # ---- end to end through the public C ABI with host buffers
     e2e = None
     render_e2e = None
@@ -356,6 +397,12 @@ def run_ours(args):
         host_gt = {vi: torch.empty(3 * plane, dtype=torch.float32, pin_memory=True) for vi in my_views}
         for vi in my_views:
             host_gt[vi].copy_(gts[vi].cpu())
+        for _ in range(max(args.warmup, 3)):  # first use creates the copy stream and the target buffer
+            for vi in my_views:
+                ctx.train_view(poses[vi], W, H, host_gt[vi].data_ptr(), gt_on_device=False, lambda_ssim=LAMBDA_SSIM)
+            if world > 1:
+                dist.all_reduce(grads)
+            ctx.adam_step(cfg, extent, it[0], zero_grad=True)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
@@ -435,7 +482,7 @@ def run_ours(args):
                 "data": "synthetic", "config": workload_config(args, world),
                 "render_fps": {"value": 1e3 / render_ms, "ms_per_frame": render_ms, "frames": nframes,
                                "kernels_ms_per_frame": {k: v[0] / nframes for k, v in rprof.items() if v[1]},
-                               "e2e": render_e2e},
+                               "e2e": render_e2e, "sweep": sweep},
                 "work": {"fwd_pairs": fwd_pairs, "bwd_pairs": bwd_pairs, "instances": instances},
                 "kernels_ms_per_step": {k: v[0] / args.steps for k, v in prof.items() if v[1]},
                 "ms_per_step_profiled": ms_profiled / args.steps,

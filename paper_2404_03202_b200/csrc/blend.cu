@@ -51,72 +51,103 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_blend(const uint32_t* __res
         const uint32_t bal1 = __ballot_sync(0xffffffffu, reach & 2u);
         uint32_t bal = wp.half ? bal1 : bal0;  // this half-warp's entries; lanes loop independently
         __syncwarp();
-        while (bal != 0u && !done) {
-            const int j = __ffs(bal) - 1;
-            bal &= bal - 1u;
-            const float4 A = ws.a[j];
-            const float4 B = ws.b[j];
-            float dx, dy, power;
-            bool unc;
-            if (!pair_power(A, B, lxo, lyo, halfW, fW, dx, dy, power, unc)) continue;
-            const float4 Cc = ws.c[j];
-            const uint32_t k = base + j;
-            float alpha;
-            double a64 = 0.0;
-            if (unc || exact) {
-                Pair64 p;
-                if (!pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p)) continue;
-                a64 = p.alpha;
-                alpha = static_cast<float>(a64);
-            } else {
-                alpha = fminf(0.99f, Cc.w * ex2_approx(-power * kLog2e));
-            }
-            float w;
-            if (!exact) {
-                const float Tn = T * (1.0f - alpha);
-                if (Tn < kTHi) {
-                    if (Tn < kTLo) {
-                        done = true;
-                        stop_at = static_cast<int>(k - range.x) + 1;
+        // A lane whose FP32 transmittance lands inside the T band parks the entry (pend) and leaves
+        // the loop; the warp then replays each parked pixel's prefix cooperatively (warp_replay_T:
+        // 32 entries evaluated in parallel, product in list order) and the lane resumes.
+        bool pend = false, p_unc = false;
+        int pj = 0;
+        double p_a64 = 0.0;
+        for (;;) {
+            while (bal != 0u && !done && !pend) {
+                const int j = __ffs(bal) - 1;
+                bal &= bal - 1u;
+                const float4 A = ws.a[j];
+                const float4 B = ws.b[j];
+                float dx, dy, power;
+                bool unc;
+                if (!pair_power(A, B, lxo, lyo, halfW, fW, dx, dy, power, unc)) continue;
+                const float4 Cc = ws.c[j];
+                const uint32_t k = base + j;
+                float alpha;
+                double a64 = 0.0;
+                if (unc || exact) {
+                    Pair64 p;
+                    if (!pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p)) continue;
+                    a64 = p.alpha;
+                    alpha = static_cast<float>(a64);
+                } else {
+                    alpha = fminf(0.99f, Cc.w * ex2_approx(-power * kLog2e));
+                }
+                float w;
+                if (!exact) {
+                    const float Tn = T * (1.0f - alpha);
+                    if (Tn < kTHi) {
+                        if (Tn < kTLo) {
+                            done = true;
+                            stop_at = static_cast<int>(k - range.x) + 1;
+                            break;
+                        }
+                        pend = true;  // inside the band: decide in FP64 after an exact replay
+                        pj = j;
+                        p_unc = unc;
+                        p_a64 = a64;
                         break;
                     }
-                    // Inside the band: decide in FP64 from an exact replay of the prefix.
-                    T64 = replay_T(inst_gid, range.x, k, px, py, width, pp.pxy, pp.conic_o);
-                    if (!unc) {
-                        Pair64 p;
-                        pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
-                        a64 = p.alpha;
-                    }
+                    w = alpha * T;
+                    T = Tn;
+                } else {
                     const double Tn64 = T64 * (1.0 - a64);
                     if (Tn64 < kTStop) {
                         done = true;
                         stop_at = static_cast<int>(k - range.x) + 1;
                         break;
                     }
-                    exact = true;
                     w = static_cast<float>(a64 * T64);
                     T64 = Tn64;
                     T = static_cast<float>(Tn64);
-                } else {
-                    w = alpha * T;
-                    T = Tn;
                 }
-            } else {
+                c0 = __fmaf_rn(Cc.x, w, c0);
+                c1 = __fmaf_rn(Cc.y, w, c1);
+                c2 = __fmaf_rn(Cc.z, w, c2);
+                ++contrib;
+                last = static_cast<int>(k - range.x) + 1;
+            }
+            uint32_t pm = __ballot_sync(0xffffffffu, pend);
+            if (pm == 0u) break;
+            while (pm != 0u) {
+                const int L = __ffs(pm) - 1;
+                pm &= pm - 1u;
+                const uint32_t kL = __shfl_sync(0xffffffffu, base + pj, L);
+                const int pxL = __shfl_sync(0xffffffffu, px, L), pyL = __shfl_sync(0xffffffffu, py, L);
+                const double t = warp_replay_T(inst_gid, range.x, kL, pxL, pyL, width, pp.pxy, pp.conic_o, lane);
+                if (lane == L) T64 = t;
+            }
+            if (pend) {
+                pend = false;
+                const uint32_t k = base + pj;
+                double a64 = p_a64;
+                if (!p_unc) {
+                    Pair64 p;
+                    pair_slow(ws.gid[pj], px, py, width, pp.pxy, pp.conic_o, &p);
+                    a64 = p.alpha;
+                }
                 const double Tn64 = T64 * (1.0 - a64);
                 if (Tn64 < kTStop) {
                     done = true;
                     stop_at = static_cast<int>(k - range.x) + 1;
-                    break;
+                } else {
+                    exact = true;
+                    const float4 Cc = ws.c[pj];
+                    const float w = static_cast<float>(a64 * T64);
+                    T64 = Tn64;
+                    T = static_cast<float>(Tn64);
+                    c0 = __fmaf_rn(Cc.x, w, c0);
+                    c1 = __fmaf_rn(Cc.y, w, c1);
+                    c2 = __fmaf_rn(Cc.z, w, c2);
+                    ++contrib;
+                    last = static_cast<int>(k - range.x) + 1;
                 }
-                w = static_cast<float>(a64 * T64);
-                T64 = Tn64;
-                T = static_cast<float>(Tn64);
             }
-            c0 = __fmaf_rn(Cc.x, w, c0);
-            c1 = __fmaf_rn(Cc.y, w, c1);
-            c2 = __fmaf_rn(Cc.z, w, c2);
-            ++contrib;
-            last = static_cast<int>(k - range.x) + 1;
         }
         __syncwarp();
     }

@@ -127,4 +127,29 @@ static __device__ __noinline__ double replay_T(const uint32_t* __restrict__ inst
     return t;
 }
 
+// replay_T done by the whole warp for one pixel (px, py): lane l evaluates entries lo + 32 r + l in
+// FP64, then the factors are multiplied into t in list order (t * 1.0 == t for skipped entries,
+// so the product equals the sequential reference loop bit for bit). All lanes must call it
+// together; every lane returns the same t.
+__device__ __forceinline__ double warp_replay_T(const uint32_t* __restrict__ inst_gid, uint32_t lo, uint32_t k,
+                                                int px, int py, double width, const double2* __restrict__ pxy,
+                                                const double4* __restrict__ conic_o, int lane) {
+    double t = 1.0;
+    const double sx = px + 0.5, sy = py + 0.5;
+    for (uint32_t base = lo; base < k; base += 32) {
+        const uint32_t i = base + lane;
+        double f = 1.0;
+        if (i < k) {
+            const uint32_t g = __ldg(inst_gid + i);
+            const double2 pc = pxy[g];
+            const double4 co = conic_o[g];
+            double gg, a;
+            if (pair_fp64(pc.x, pc.y, co.x, co.y, co.z, co.w, sx, sy, width, &gg, &a)) f = 1.0 - a;
+        }
+        const int cnt = k - base < 32u ? static_cast<int>(k - base) : 32;
+        for (int q = 0; q < cnt; ++q) t = t * __shfl_sync(0xffffffffu, f, q);
+    }
+    return t;
+}
+
 }  // namespace osb

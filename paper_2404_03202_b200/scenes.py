@@ -182,3 +182,116 @@ def pose_to_transform(p12: np.ndarray) -> np.ndarray:
     t[:3, :3] = p12[:9].reshape(3, 3)
     t[:3, 3] = p12[9:]
     return t
+
+
+# ---------------------------------------------------------------------------- roaming scene (C5)
+
+def roaming_scene(n: int = 2_000_000, seed: int = 5, rooms: int = 3, sh_degree: int = 3) -> Cloud:
+    """360Roam-style synthetic interior: `rooms` connected 6 x 3 x 6 m rooms
+    in a row along +x (y up, floor at y = 0), Gaussians as flat discs on the walls / floor /
+    ceiling with procedural colour patterns (no two walls alike), plus volumetric blobs
+    (furniture) inside each room. Doorways (1.2 m wide, 2.2 m high) join neighbouring rooms."""
+    rng = np.random.default_rng(seed)
+    Lx, Ly, Lz = 6.0, 3.0, 6.0
+    n_blob = n // 6
+    n_surf = n - n_blob
+    # surface area per room: floor + ceiling 2*36, walls 4*18 (shared walls once)
+    pts, nrm = [], []
+    per = n_surf // rooms
+    for r in range(rooms):
+        x0 = r * Lx
+        u = rng.random((per, 2))
+        face = rng.choice(6, size=per, p=np.array([36, 36, 18, 18, 18, 18]) / 144.0)
+        p = np.zeros((per, 3))
+        nv = np.zeros((per, 3))
+        # 0 floor, 1 ceiling, 2 wall z=0, 3 wall z=Lz, 4 wall x=x0, 5 wall x=x0+Lx
+        for f, (ax, val, nn) in enumerate([(1, 0.0, (0, 1, 0)), (1, Ly, (0, -1, 0)), (2, 0.0, (0, 0, 1)),
+                                           (2, Lz, (0, 0, -1)), (0, x0, (1, 0, 0)), (0, x0 + Lx, (-1, 0, 0))]):
+            m = face == f
+            k = int(m.sum())
+            if ax == 1:
+                p[m] = np.stack([x0 + u[m, 0] * Lx, np.full(k, val), u[m, 1] * Lz], axis=1)
+            elif ax == 2:
+                p[m] = np.stack([x0 + u[m, 0] * Lx, u[m, 1] * Ly, np.full(k, val)], axis=1)
+            else:
+                p[m] = np.stack([np.full(k, val), u[m, 1] * Ly, u[m, 0] * Lz], axis=1)
+            nv[m] = nn
+        # doorways: drop wall points inside the openings between rooms
+        door = (((face == 4) & (r > 0)) | ((face == 5) & (r < rooms - 1))) & (np.abs(p[:, 2] - Lz / 2) < 0.6) & \
+               (p[:, 1] < 2.2)
+        pts.append(p[~door])
+        nrm.append(nv[~door])
+    P = np.concatenate(pts)
+    Nrm = np.concatenate(nrm)
+    ns = P.shape[0]
+    # blobs: clusters of small Gaussians (furniture / objects)
+    centres = np.stack([rng.uniform(0.5, rooms * Lx - 0.5, 40), rng.uniform(0.2, 1.5, 40), rng.uniform(0.5, Lz - 0.5, 40)], 1)
+    which = rng.integers(0, 40, n_blob)
+    B = centres[which] + rng.standard_normal((n_blob, 3)) * rng.uniform(0.1, 0.4, (40, 1))[which]
+    positions = np.concatenate([P, B])
+    total = positions.shape[0]
+    # surface discs: thin along the normal; rotation maps local z to the normal
+    spacing = np.sqrt(rooms * 144.0 / max(ns, 1))
+    ls = np.empty((total, 3))
+    ls[:ns, :2] = np.log(spacing * rng.uniform(0.6, 1.2, (ns, 2)))
+    ls[:ns, 2] = np.log(spacing * 0.1)
+    ls[ns:] = np.log(rng.uniform(0.005, 0.02, (total - ns, 1))) + 0.1 * rng.standard_normal((total - ns, 3))
+    q = np.zeros((total, 4))
+    z = np.array([0.0, 0.0, 1.0])
+    axis = np.cross(np.broadcast_to(z, Nrm.shape), Nrm)
+    s = np.linalg.norm(axis, axis=1)
+    c = Nrm @ z
+    ang = np.arctan2(s, c)
+    axis = np.where(s[:, None] > 1e-9, axis / np.maximum(s, 1e-12)[:, None], np.array([1.0, 0.0, 0.0]))
+    q[:ns, 0] = np.cos(ang / 2)
+    q[:ns, 1:] = axis * np.sin(ang / 2)[:, None]
+    q[:ns] = q[:ns] * np.where(q[:ns, :1] < 0, -1, 1)
+    qb = rng.standard_normal((total - ns, 4))
+    q[ns:] = qb / np.linalg.norm(qb, axis=1, keepdims=True)
+    # colour: per-face palettes modulated by stripes / checkers in world coordinates
+    base = rng.uniform(0.15, 0.85, (64, 3))
+    cell = (np.floor(positions[:, 0] / 0.75) + 7 * np.floor(positions[:, 1] / 0.5) + 13 * np.floor(positions[:, 2] / 0.75))
+    col = base[cell.astype(np.int64) % 64]
+    col = col * (0.8 + 0.2 * np.sin(positions[:, :1] * 9.0) * np.cos(positions[:, 2:] * 7.0))
+    col[ns:] = base[(which * 7) % 64] * rng.uniform(0.7, 1.1, (total - ns, 1))
+    bc = (sh_degree + 1) ** 2
+    sh = np.zeros((total, bc, 3))
+    sh[:, 0, :] = (np.clip(col, 0.02, 0.98) - 0.5) / 0.28209479177387814
+    if bc > 1:
+        sh[:, 1:4, :] = rng.uniform(-0.03, 0.03, (total, 3, 3))
+    opacity = _logit(np.concatenate([rng.uniform(0.85, 0.99, ns), rng.uniform(0.4, 0.95, total - ns)]))
+    return Cloud(positions, sh, q, ls, opacity, sh_degree, sh_degree).rounded()
+
+
+def roaming_poses(count: int = 200, seed: int = 6, rooms: int = 3) -> list:
+    """Panorama centres along a wandering path through the rooms at eye height (1.4-1.7 m), random
+    yaw; world->camera poses (camera y up)."""
+    rng = np.random.default_rng(seed)
+    t = np.linspace(0.0, 1.0, count)
+    x = 0.8 + t * (rooms * 6.0 - 1.6)
+    z = 3.0 + 1.8 * np.sin(t * rooms * 2.0 * np.pi) + rng.uniform(-0.3, 0.3, count)
+    y = rng.uniform(1.4, 1.7, count)
+    out = []
+    for k in range(count):
+        R = rot_y(rng.uniform(0.0, 2.0 * np.pi))
+        c = np.array([x[k], y[k], z[k]])
+        out.append(pose12(R, -(R @ c)))
+    return out
+
+
+def init_from_points(points: np.ndarray, rgb: np.ndarray, sh_degree: int = 3) -> Cloud:
+    """init_from_points (proj/src/scene.cpp:181-213): isotropic scale sqrt(mean of the 3 nearest
+    squared distances), identity rotation, opacity 0.1, DC colour from the point colour."""
+    from scipy.spatial import cKDTree
+
+    n = points.shape[0]
+    d, _ = cKDTree(points).query(points, k=4)
+    mean_sq = np.mean(d[:, 1:] ** 2, axis=1) if n > 1 else np.zeros(n)
+    ls = np.log(np.sqrt(np.maximum(mean_sq, 1e-7)))
+    bc = (sh_degree + 1) ** 2
+    sh = np.zeros((n, bc, 3))
+    sh[:, 0, :] = (rgb - 0.5) / 0.28209479177387814
+    q = np.zeros((n, 4))
+    q[:, 0] = 1.0
+    return Cloud(points.copy(), sh, q, np.repeat(ls[:, None], 3, axis=1), np.full(n, _logit(0.1)), sh_degree,
+                 0).rounded()
