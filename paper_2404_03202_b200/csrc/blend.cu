@@ -13,7 +13,7 @@ namespace osb {
 
 namespace {
 
-__global__ void __launch_bounds__(kTileThreads, 3) k_blend(const uint32_t* __restrict__ inst_gid,
+__global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __restrict__ inst_gid,
                                                            const uint2* __restrict__ ranges, PreprocessOut pp, int W,
                                                            int H, int tiles_x, float bg0, float bg1, float bg2,
                                                            FrameBuffers fb) {
