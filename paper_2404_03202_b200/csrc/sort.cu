@@ -243,7 +243,6 @@ __global__ void k_iota(uint32_t* v, int n) {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;  // ranks per block
-constexpr int kWarpRanks = 32 * kScanItems;            // ranks per warp
 
 // Sum of touched over each block's ranks.
 __global__ void __launch_bounds__(kScanThreads) k_touch_sums(const uint32_t* __restrict__ touched,
@@ -301,26 +300,23 @@ __global__ void __launch_bounds__(1024) k_scan_block_sums(uint32_t* __restrict__
     if (threadIdx.x == 0) *total = s_carry;
 }
 
-// Instance emission in depth order. Each thread owns 8 consecutive ranks; the warp's instance
-// range is produced in windows of 256 in shared memory — every lane writes the instances of its own
-// Gaussians that fall in the window (incremental tile walk, no search), then the warp copies the
-// window out with coalesced stores. Gaussians with more than kBigCount instances (full-row pole
-// splats) are emitted cooperatively by the whole warp instead, so no lane serialises them.
-constexpr int kWindow = 256;
-constexpr uint32_t kBigCount = 64;
+// Instance emission in depth order, balanced over OUTPUTS (the instance counts per rank are very
+// skewed: full-width pole splats emit hundreds of tiles): k_emit_prep writes, per depth rank, its
+// first output (exclusive scan), id and packed tile rectangle; k_emit gives every CTA exactly
+// kEmitTile consecutive outputs, finds the ranks covering them with two global binary searches,
+// stages their first-outputs in shared memory, and every thread emits 8 consecutive instances (one
+// shared-memory search, then a forward walk). Stores are 32-B runs per lane.
+constexpr int kEmitTile = kScanThreads * 8;
+constexpr int kEmitWindow = 2 * kEmitTile;  // ranks staged per CTA (more only with many empty ranks)
 
-__global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restrict__ touched,
-                                                       const uint32_t* __restrict__ order,
-                                                       const int4* __restrict__ rect, int n, int tiles_x,
-                                                       const uint32_t* __restrict__ block_offsets,
-                                                       uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                                       uint32_t capacity) {
+__global__ void __launch_bounds__(kScanThreads) k_emit_prep(const uint32_t* __restrict__ touched,
+                                                            const uint32_t* __restrict__ order,
+                                                            const int4* __restrict__ rect, int n,
+                                                            const uint32_t* __restrict__ block_offsets,
+                                                            uint32_t* __restrict__ rank_off,
+                                                            uint32_t* __restrict__ rank_gid, int2* __restrict__ rank_rc) {
     __shared__ uint32_t s_scan[kSortWarps + 1];
-    __shared__ uint32_t s_wk[kSortWarps][kWindow];
-    __shared__ uint32_t s_wv[kSortWarps][kWindow];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // thread owns ranks [r0, r0 + kScanItems) inside its warp's contiguous 256-rank chunk
-    const long r0 = static_cast<long>(blockIdx.x) * kScanTile + warp * kWarpRanks + lane * kScanItems;
+    const long r0 = static_cast<long>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
     uint32_t v[kScanItems], g[kScanItems];
     uint32_t local = 0;
 #pragma unroll
@@ -331,82 +327,75 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
         local += v[i];
     }
     uint32_t agg;
-    const uint32_t thread_excl = block_exclusive_scan(local, s_scan, &agg);
-    const uint32_t block_excl = block_offsets[blockIdx.x];
-    int4 rc[kScanItems];
-#pragma unroll
-    for (int i = 0; i < kScanItems; ++i) rc[i] = v[i] > 0 ? rect[g[i]] : make_int4(0, 0, 0, 0);
-    uint32_t off[kScanItems];  // block-relative
-    {
-        uint32_t run = thread_excl;
-#pragma unroll
-        for (int i = 0; i < kScanItems; ++i) {
-            off[i] = run;
-            run += v[i];
-        }
-    }
-    const uint32_t w_begin = __shfl_sync(0xffffffffu, thread_excl, 0);
-    const uint32_t w_end = __shfl_sync(0xffffffffu, thread_excl + local, 31);
-
-    // small Gaussians: lane-serial into the shared window, coalesced copy-out
-    for (uint32_t win = w_begin; win < w_end; win += kWindow) {
-        const uint32_t win_hi = min(win + kWindow, w_end);
-        for (int t = lane; t < kWindow; t += 32) s_wv[warp][t] = 0xFFFFFFFFu;  // big-Gaussian slots stay empty
-        __syncwarp();
-#pragma unroll
-        for (int i = 0; i < kScanItems; ++i) {
-            if (v[i] == 0 || v[i] > kBigCount) continue;
-            const uint32_t s = max(off[i], win), e = min(off[i] + v[i], win_hi);
-            if (s >= e) continue;
-            const uint32_t wt = static_cast<uint32_t>(rc[i].y - rc[i].x + 1);
-            const uint32_t li = s - off[i];
-            uint32_t row = li / wt, col = li - row * wt;
-            for (uint32_t idx = s; idx < e; ++idx) {
-                int kx = rc[i].x + static_cast<int>(col);
-                kx = kx < 0 ? kx + tiles_x : (kx >= tiles_x ? kx - tiles_x : kx);
-                s_wk[warp][idx - win] = static_cast<uint32_t>((rc[i].z + static_cast<int>(row)) * tiles_x + kx);
-                s_wv[warp][idx - win] = g[i];
-                if (++col == wt) {
-                    col = 0;
-                    ++row;
-                }
-            }
-        }
-        __syncwarp();
-        for (uint32_t t = lane; t < win_hi - win; t += 32) {
-            const uint32_t out = block_excl + win + t;
-            const uint32_t gi = s_wv[warp][t];
-            if (out < capacity && gi != 0xFFFFFFFFu) {  // big Gaussians are emitted below
-                keys[out] = s_wk[warp][t];
-                vals[out] = gi;
-            }
-        }
-        __syncwarp();
-    }
-    // big Gaussians: the whole warp writes each one's instances
+    uint32_t run = block_offsets[blockIdx.x] + block_exclusive_scan(local, s_scan, &agg);
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
-        uint32_t big = __ballot_sync(0xffffffffu, v[i] > kBigCount);
-        while (big) {
-            const int src = __ffs(big) - 1;
-            big &= big - 1u;
-            const uint32_t cnt = __shfl_sync(0xffffffffu, v[i], src);
-            const uint32_t o = __shfl_sync(0xffffffffu, off[i], src);
-            const uint32_t gi = __shfl_sync(0xffffffffu, g[i], src);
-            const int x0 = __shfl_sync(0xffffffffu, rc[i].x, src);
-            const int x1 = __shfl_sync(0xffffffffu, rc[i].y, src);
-            const int y0 = __shfl_sync(0xffffffffu, rc[i].z, src);
-            const uint32_t wt = static_cast<uint32_t>(x1 - x0 + 1);
-            for (uint32_t li = lane; li < cnt; li += 32) {
-                const uint32_t row = li / wt;
-                int kx = x0 + static_cast<int>(li - row * wt);
-                kx = kx < 0 ? kx + tiles_x : (kx >= tiles_x ? kx - tiles_x : kx);
-                const uint32_t out = block_excl + o + li;
-                if (out < capacity) {
-                    keys[out] = static_cast<uint32_t>((y0 + static_cast<int>(row)) * tiles_x + kx);
-                    vals[out] = gi;
-                }
-            }
+        const long r = r0 + i;
+        if (r >= n) break;
+        int2 rc = make_int2(0, 0);
+        if (v[i] > 0) {
+            const int4 q = rect[g[i]];
+            rc = make_int2((q.x & 0xFFFF) | ((q.y - q.x + 1) << 16), q.z);
+        }
+        rank_off[r] = run;
+        rank_gid[r] = g[i];
+        rank_rc[r] = rc;
+        run += v[i];
+    }
+}
+
+// last index e in [0, count) with off[e] <= o (off non-decreasing, off[0] <= o)
+__device__ __forceinline__ int owner_of(const uint32_t* off, int count, uint32_t o) {
+    int lo = 0, hi = count - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= o) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restrict__ rank_off,
+                                                       const uint32_t* __restrict__ rank_gid,
+                                                       const int2* __restrict__ rank_rc, int n,
+                                                       const uint32_t* __restrict__ total, int tiles_x,
+                                                       uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                       uint32_t capacity) {
+    __shared__ uint32_t s_off[kEmitWindow];
+    __shared__ int s_rb, s_w;
+    const uint32_t M = *total;
+    const uint32_t o_begin = static_cast<uint32_t>(blockIdx.x) * kEmitTile;
+    if (o_begin >= M) return;
+    const uint32_t o_end = min(o_begin + static_cast<uint32_t>(kEmitTile), M);
+    if (threadIdx.x == 0) {
+        const int rb = owner_of(rank_off, n, o_begin);
+        const int re = owner_of(rank_off, n, o_end - 1);
+        s_rb = rb;
+        s_w = re - rb + 1;
+    }
+    __syncthreads();
+    const int rb = s_rb, w = s_w;
+    const uint32_t* off = rank_off + rb;
+    if (w <= kEmitWindow) {
+        for (int i = threadIdx.x; i < w; i += kScanThreads) s_off[i] = off[i];
+        __syncthreads();
+        off = s_off;
+    }
+    uint32_t o = o_begin + threadIdx.x * 8;
+    if (o >= o_end) return;
+    int e = owner_of(off, w, o);
+    for (int q = 0; q < 8 && o < o_end; ++q, ++o) {
+        while (e + 1 < w && off[e + 1] <= o) ++e;
+        const int2 rc = rank_rc[rb + e];
+        const int x0 = static_cast<int>(static_cast<int16_t>(rc.x & 0xFFFF));
+        const uint32_t wt = static_cast<uint32_t>(rc.x) >> 16;
+        const uint32_t li = o - off[e];
+        const uint32_t row = li / wt;
+        int kx = x0 + static_cast<int>(li - row * wt);
+        kx = kx < 0 ? kx + tiles_x : (kx >= tiles_x ? kx - tiles_x : kx);
+        if (o < capacity) {
+            keys[o] = static_cast<uint32_t>((rc.y + static_cast<int>(row)) * tiles_x + kx);
+            vals[o] = rank_gid[rb + e];
         }
     }
 }
@@ -476,7 +465,7 @@ void launch_iota(uint32_t* v, int n, cudaStream_t s) {
 
 size_t scan_workspace_bytes(int n) {
     const size_t blocks = (static_cast<size_t>(n) + kScanTile - 1) / kScanTile;
-    return sizeof(uint32_t) * (blocks + 64);
+    return sizeof(uint32_t) * (blocks + 128) + (static_cast<size_t>(n) + 64) * 16 + 256;
 }
 
 void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
@@ -487,10 +476,19 @@ void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4
     }
     const int blocks = (n + kScanTile - 1) / kScanTile;
     uint32_t* sums = static_cast<uint32_t*>(ws);
+    uint32_t* rank_off = sums + ((blocks + 64 + 63) & ~63);
+    const size_t npad = (static_cast<size_t>(n) + 63) & ~size_t(63);  // keeps every array 256-B aligned
+    uint32_t* rank_gid = rank_off + npad;
+    int2* rank_rc = reinterpret_cast<int2*>(rank_gid + npad);
     k_touch_sums<<<blocks, kScanThreads, 0, s>>>(touched, order, n, sums);
     k_scan_block_sums<<<1, 1024, 0, s>>>(sums, blocks, total);
-    k_emit<<<blocks, kScanThreads, 0, s>>>(touched, order, rect, n, tiles_x, sums, keys, vals, capacity);
-    OSB_LAUNCHED(3);
+    k_emit_prep<<<blocks, kScanThreads, 0, s>>>(touched, order, rect, n, sums, rank_off, rank_gid, rank_rc);
+    // one CTA per kEmitTile outputs up to the capacity (CTAs past M exit; M > capacity is retried)
+    const long grid = (static_cast<long>(capacity) + kEmitTile - 1) / kEmitTile;
+    if (grid > 0)
+        k_emit<<<static_cast<int>(grid), kScanThreads, 0, s>>>(rank_off, rank_gid, rank_rc, n, total, tiles_x, keys,
+                                                               vals, capacity);
+    OSB_LAUNCHED(grid > 0 ? 4 : 3);
 }
 
 void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s) {
