@@ -510,6 +510,7 @@ osplat_status osplat_render(const osplat_cloud* cloud, const double transform_cw
         const size_t plane = static_cast<size_t>(width) * height;
         std::vector<float> host(plane * 3);
         try {
+            e.validate(f);
             OSB_CUDA_CHECK(cudaMemcpyAsync(host.data(), f->rgb.as<float>(), plane * 12, cudaMemcpyDeviceToHost,
                                            e.stream()));
             OSB_CUDA_CHECK(cudaStreamSynchronize(e.stream()));
@@ -589,6 +590,7 @@ int osplat_frame_height(const osplat_frame* f) { return f ? f->frame->H : 0; }
 osplat_status osplat_frame_image(const osplat_frame* frame, double* rgb) {
     if (!frame || !rgb) return invalid("osplat_frame_image: null argument");
     return wrap([&] {
+        frame->engine->validate(frame->frame);
         const osb::Frame& f = *frame->frame;
         osb::DeviceGuard g(frame->engine->device());
         const size_t plane = static_cast<size_t>(f.W) * f.H;
@@ -603,6 +605,7 @@ osplat_status osplat_frame_image(const osplat_frame* frame, double* rgb) {
 osplat_status osplat_frame_pixels(const osplat_frame* frame, float* rgb, float* T, int* contrib, int* last) {
     if (!frame) return invalid("osplat_frame_pixels: null frame");
     return wrap([&] {
+        frame->engine->validate(frame->frame);
         const osb::Frame& f = *frame->frame;
         osb::DeviceGuard g(frame->engine->device());
         cudaStream_t s = frame->engine->stream();
@@ -626,6 +629,7 @@ osplat_status osplat_frame_projections(const osplat_frame* frame, uint8_t* visib
                                        double* opacity, float* color, int32_t* rect, uint32_t* touched) {
     if (!frame) return invalid("osplat_frame_projections: null frame");
     return wrap([&] {
+        frame->engine->validate(frame->frame);
         const osb::Frame& f = *frame->frame;
         osb::DeviceGuard g(frame->engine->device());
         cudaStream_t s = frame->engine->stream();
@@ -676,6 +680,7 @@ osplat_status osplat_frame_tiles(const osplat_frame* frame, int* tiles_x, int* t
                                  uint32_t* ranges, uint32_t* gaussian_ids) {
     if (!frame) return invalid("osplat_frame_tiles: null frame");
     return wrap([&] {
+        frame->engine->validate(frame->frame);
         const osb::Frame& f = *frame->frame;
         osb::DeviceGuard g(frame->engine->device());
         cudaStream_t s = frame->engine->stream();
@@ -693,15 +698,16 @@ osplat_status osplat_frame_tiles(const osplat_frame* frame, int* tiles_x, int* t
 
 osplat_status osplat_frame_device(const osplat_frame* frame, osplat_frame_view* v) {
     if (!frame || !v) return invalid("osplat_frame_device: null argument");
-    const osb::Frame& f = *frame->frame;
-    v->rgb = f.rgb.as<float>();
-    v->transmittance = f.T.as<float>();
-    v->contributors = f.contrib.as<int>();
-    v->last_contrib = f.last.as<int>();
-    v->width = f.W;
-    v->height = f.H;
-    t_last_error.clear();
-    return OSPLAT_OK;
+    return wrap([&] {
+        frame->engine->validate(frame->frame);
+        const osb::Frame& f = *frame->frame;
+        v->rgb = f.rgb.as<float>();
+        v->transmittance = f.T.as<float>();
+        v->contributors = f.contrib.as<int>();
+        v->last_contrib = f.last.as<int>();
+        v->width = f.W;
+        v->height = f.H;
+    });
 }
 
 osplat_status osplat_gpu_view_buffers(osplat_gpu* ctx, osplat_gpu_view* v) {
@@ -745,6 +751,7 @@ osplat_status osplat_gpu_backward(osplat_gpu* ctx, const osplat_frame* frame, co
         validate_frame(ctx, frame);
         Engine& e = *ctx->engine;
         osb::DeviceGuard g(e.device());
+        frame->engine->validate(frame->frame);
         const osb::Frame& f = *frame->frame;
         const size_t plane = static_cast<size_t>(f.W) * f.H;
         std::vector<float> planar(plane * 3);
@@ -752,7 +759,7 @@ osplat_status osplat_gpu_backward(osplat_gpu* ctx, const osplat_frame* frame, co
             for (int c = 0; c < 3; ++c) planar[c * plane + i] = static_cast<float>(d_image[i * 3 + c]);
         float* dev = e.d_image_buffer(plane);
         OSB_CUDA_CHECK(cudaMemcpyAsync(dev, planar.data(), plane * 12, cudaMemcpyHostToDevice, e.stream()));
-        e.backward(&f, dev, accumulate != 0);
+        e.backward(frame->frame, dev, accumulate != 0);
         OSB_CUDA_CHECK(cudaStreamSynchronize(e.stream()));  // `planar` is pageable host memory
     });
 }
@@ -1051,6 +1058,7 @@ const char* osplat_kernel_name(int id) { return osb::kernel_name(id); }
 osplat_status osplat_frame_work(const osplat_frame* frame, uint64_t* fwd, uint64_t* bwd, uint64_t* instances) {
     if (!frame) return invalid("osplat_frame_work: null frame");
     return wrap([&] {
+        frame->engine->validate(frame->frame);
         const osb::Frame& f = *frame->frame;
         if (!f.count_work) throw ApiError(Code::StateMismatch, "frame was rendered without work counting");
         osb::DeviceGuard g(frame->engine->device());

@@ -43,6 +43,11 @@ DeviceGuard::DeviceGuard(int dev) {
 }
 DeviceGuard::~DeviceGuard() { cudaSetDevice(prev); }
 
+Frame::~Frame() {
+    if (ready) cudaEventDestroy(ready);
+    if (info_host) cudaFreeHost(info_host);
+}
+
 PreprocessOut Frame::pp() const {
     PreprocessOut o;
     o.depth_key = depth_key.as<uint64_t>();
@@ -265,122 +270,8 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
         for (int i = 0; i < 9; ++i) f->pose.R[i] = pose12[i];
         for (int i = 0; i < 3; ++i) f->pose.t[i] = pose12[9 + i];
         for (int i = 0; i < 3; ++i) f->bg[i] = static_cast<float>(bg ? bg[i] : 0.0);
-        const size_t n = n_ > 0 ? n_ : 1;
-        const size_t pixels = static_cast<size_t>(W) * H;
-        const int tiles = f->tiles_x * f->tiles_y;
-        f->depth_key.ensure(n * 8);
-        f->depth_key32.ensure(n * 4);
-        f->touched.ensure(n * 4);
-        f->rect.ensure(n * 16);
-        f->pxy.ensure(n * 16);
-        f->conic_o.ensure(n * 32);
-        f->splat.ensure(n * sizeof(Splat32));
-        f->radius.ensure(n * 4);
-        for (int k = 0; k < 2; ++k) {
-            f->okeys[k].ensure(n * 8);
-            f->ovals[k].ensure(n * 4);
-        }
-        f->offsets.ensure(n * 4);
-        f->total.ensure(16);
-        f->ranges.ensure(static_cast<size_t>(tiles) * 8);
-        f->rgb.ensure(pixels * 12);
-        f->T.ensure(pixels * 4);
-        f->contrib.ensure(pixels * 4);
-        f->last.ensure(pixels * 4);
-        f->count_work = count_work_;
-        if (count_work_) {
-            f->visited.ensure(pixels * 4);
-            f->work.ensure(16);
-        }
-        f->scan_ws.ensure(scan_workspace_bytes(static_cast<int>(n)));
-
-        const PreprocessOut pp = f->pp();
-        const int N = static_cast<int>(n_);
-        // K1
-        {
-            Span sp(*this, kPreprocess);
-            launch_preprocess(params_.as<float>(), N, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
-                              active_, f->pose, W, H, pp, stream_);
-        }
-        // K2a: depth rank = (t_r, id) order. Fast path: stable 4-pass sort of the FP32-rounded
-        // t_r (monotone) + exact FP64 re-ordering inside runs of equal FP32 keys; a run longer
-        // than 32 is flagged and the frame falls back to the full 64-bit sort, decided at the one
-        // host synchronization of the frame below.
-        f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(n), 8));
-        uint32_t* long_run_flag = f->total.as<uint32_t>() + 1;
-        auto depth_rank = [&](bool full) -> const uint32_t* {
-            Span sp(*this, kDepthSort);
-            launch_iota(f->ovals[0].as<uint32_t>(), N, stream_);
-            bool flipped;
-            if (full) {
-                OSB_CUDA_CHECK(cudaMemcpyAsync(f->okeys[0].as<uint64_t>(), pp.depth_key, n_ * 8,
-                                               cudaMemcpyDeviceToDevice, stream_));
-                flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(),
-                                         f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N, 64,
-                                         f->sort_ws.as<void>(), stream_);
-            } else {
-                uint32_t* k32[2] = {f->okeys[0].as<uint32_t>(), f->okeys[1].as<uint32_t>()};
-                OSB_CUDA_CHECK(cudaMemcpyAsync(k32[0], pp.depth_key32, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
-                OSB_CUDA_CHECK(cudaMemsetAsync(long_run_flag, 0, 4, stream_));
-                flipped = radix_sort_u32(k32[0], k32[1], f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N,
-                                         32, f->sort_ws.as<void>(), stream_);
-                launch_fix_runs(k32[flipped ? 1 : 0], f->ovals[flipped ? 1 : 0].as<uint32_t>(), pp.depth_key, N,
-                                long_run_flag, stream_);
-            }
-            return f->ovals[flipped ? 1 : 0].as<uint32_t>();
-        };
         f->full_depth_sort = false;
-        const uint32_t* order = depth_rank(false);
-        // K2b: scan of tiles_touched in depth order fused with the (tile, gid) emission. The
-        // instance buffers keep their capacity across frames; only a frame that outgrows them pays
-        // a second pass.
-        uint32_t M = 0;
-        for (int attempt = 0; attempt < 3; ++attempt) {
-            const uint32_t cap = static_cast<uint32_t>(f->ikeys[0].capacity() / 4);
-            {
-                Span sp(*this, kScan);
-                launch_scan_emit(pp.touched, order, pp.rect, N, f->tiles_x, f->ikeys[0].as<uint32_t>(),
-                                 f->ivals[0].as<uint32_t>(), cap, f->total.as<uint32_t>(), f->scan_ws.as<void>(),
-                                 stream_);
-            }
-            uint32_t host[2] = {0, 0};  // {M, long-run flag}
-            OSB_CUDA_CHECK(cudaMemcpyAsync(host, f->total.as<uint32_t>(), 8, cudaMemcpyDeviceToHost, stream_));
-            OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
-            M = N == 0 ? 0 : host[0];
-            if (host[1] != 0 && !f->full_depth_sort) {  // rare: redo the depth rank exactly, re-emit
-                f->full_depth_sort = true;
-                order = depth_rank(true);
-                continue;
-            }
-            if (M <= cap && f->ikeys[0].capacity() > 0) break;
-            const size_t want = (static_cast<size_t>(M) + M / 4 + 1024) * 4;
-            for (int k = 0; k < 2; ++k) {
-                f->ikeys[k].ensure(want);
-                f->ivals[k].ensure(want);
-            }
-        }
-        f->M = M;
-        const size_t m = M > 0 ? M : 1;
-        f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(m), 4));
-        {
-            Span sp(*this, kTileSort);
-            f->inst_in_alt = radix_sort_u32(f->ikeys[0].as<uint32_t>(), f->ikeys[1].as<uint32_t>(),
-                                            f->ivals[0].as<uint32_t>(), f->ivals[1].as<uint32_t>(),
-                                            static_cast<int>(M), bits_for(static_cast<uint64_t>(tiles)),
-                                            f->sort_ws.as<void>(), stream_);
-        }
-        {
-            Span sp(*this, kRanges);
-            OSB_CUDA_CHECK(cudaMemsetAsync(f->ranges.as<uint2>(), 0, static_cast<size_t>(tiles) * 8, stream_));
-            launch_ranges(f->ikeys[f->inst_in_alt ? 1 : 0].as<uint32_t>(), static_cast<int>(M),
-                          f->ranges.as<uint2>(), stream_);
-        }
-        // K3
-        {
-            Span sp(*this, kBlend);
-            launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(),
-                         stream_);
-        }
+        render_into(f);
     } catch (...) {
         free_.push_back(f);
         throw;
@@ -388,12 +279,168 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
     return f;
 }
 
-void Engine::release(Frame* f) {
-    if (f) free_.push_back(f);
+// The frame's kernels are all enqueued without a host synchronisation: the instance count M is only
+// known on the device when the tile sort runs, so the sort, ranges and blend cover min(M, capacity)
+// (device-side count, grids sized by the capacity). {M, long-run flag} are copied back
+// asynchronously; the first consumer of the frame (validate) checks them and, in the rare case of
+// an overflow or a long run of equal FP32 depth keys, grows the buffers / switches to the exact
+// 64-bit depth sort and renders the frame again.
+void Engine::render_into(Frame* f) {
+    const int W = f->W, H = f->H;
+    const size_t n = n_ > 0 ? n_ : 1;
+    const size_t pixels = static_cast<size_t>(W) * H;
+    const int tiles = f->tiles_x * f->tiles_y;
+    f->depth_key.ensure(n * 8);
+    f->depth_key32.ensure(n * 4);
+    f->touched.ensure(n * 4);
+    f->rect.ensure(n * 16);
+    f->pxy.ensure(n * 16);
+    f->conic_o.ensure(n * 32);
+    f->splat.ensure(n * sizeof(Splat32));
+    f->radius.ensure(n * 4);
+    for (int k = 0; k < 2; ++k) {
+        f->okeys[k].ensure(n * 8);
+        f->ovals[k].ensure(n * 4);
+    }
+    f->offsets.ensure(n * 4);
+    f->total.ensure(16);
+    f->ranges.ensure(static_cast<size_t>(tiles) * 8);
+    f->rgb.ensure(pixels * 12);
+    f->T.ensure(pixels * 4);
+    f->contrib.ensure(pixels * 4);
+    f->last.ensure(pixels * 4);
+    f->count_work = count_work_;
+    if (count_work_) {
+        f->visited.ensure(pixels * 4);
+        f->work.ensure(16);
+    }
+    f->scan_ws.ensure(scan_workspace_bytes(static_cast<int>(n)));
+    if (!f->info_host) OSB_CUDA_CHECK(cudaMallocHost(&f->info_host, 64));
+    if (!f->ready) OSB_CUDA_CHECK(cudaEventCreateWithFlags(&f->ready, cudaEventDisableTiming));
+
+    const PreprocessOut pp = f->pp();
+    const int N = static_cast<int>(n_);
+    // K1
+    {
+        Span sp(*this, kPreprocess);
+        launch_preprocess(params_.as<float>(), N, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
+                          active_, f->pose, W, H, pp, stream_);
+    }
+    // K2a: depth rank = (t_r, id) order. Fast path: stable sort of the FP32-rounded t_r (monotone)
+    // + exact FP64 re-ordering inside runs of equal FP32 keys; a run longer than 32 raises a flag
+    // and validate() renders the frame again with the full 64-bit sort.
+    f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(n), 8));
+    uint32_t* long_run_flag = f->total.as<uint32_t>() + 1;
+    const uint32_t* order;
+    {
+        Span sp(*this, kDepthSort);
+        launch_iota(f->ovals[0].as<uint32_t>(), N, stream_);
+        OSB_CUDA_CHECK(cudaMemsetAsync(long_run_flag, 0, 4, stream_));
+        bool flipped;
+        if (f->full_depth_sort) {
+            OSB_CUDA_CHECK(cudaMemcpyAsync(f->okeys[0].as<uint64_t>(), pp.depth_key, n_ * 8, cudaMemcpyDeviceToDevice,
+                                           stream_));
+            flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(), f->ovals[0].as<uint32_t>(),
+                                     f->ovals[1].as<uint32_t>(), N, 64, f->sort_ws.as<void>(), stream_);
+        } else {
+            uint32_t* k32[2] = {f->okeys[0].as<uint32_t>(), f->okeys[1].as<uint32_t>()};
+            OSB_CUDA_CHECK(cudaMemcpyAsync(k32[0], pp.depth_key32, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
+            flipped = radix_sort_u32(k32[0], k32[1], f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N, 32,
+                                     f->sort_ws.as<void>(), stream_);
+            launch_fix_runs(k32[flipped ? 1 : 0], f->ovals[flipped ? 1 : 0].as<uint32_t>(), pp.depth_key, N,
+                            long_run_flag, stream_);
+        }
+        order = f->ovals[flipped ? 1 : 0].as<uint32_t>();
+    }
+    // K2b: scan of tiles_touched in depth order + balanced (tile, gid) emission. A frame with no
+    // instance buffer yet sizes it first (one synchronous counting pass).
+    if (f->ikeys[0].capacity() == 0) {
+        launch_scan_emit(pp.touched, order, pp.rect, N, f->tiles_x, nullptr, nullptr, 0, f->total.as<uint32_t>(),
+                         f->scan_ws.as<void>(), stream_);
+        uint32_t host = 0;
+        OSB_CUDA_CHECK(cudaMemcpyAsync(&host, f->total.as<uint32_t>(), 4, cudaMemcpyDeviceToHost, stream_));
+        OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+        grow_instances(f, host);
+    }
+    const uint32_t cap = static_cast<uint32_t>(f->ikeys[0].capacity() / 4);
+    f->cap = cap;
+    {
+        Span sp(*this, kScan);
+        launch_scan_emit(pp.touched, order, pp.rect, N, f->tiles_x, f->ikeys[0].as<uint32_t>(),
+                         f->ivals[0].as<uint32_t>(), cap, f->total.as<uint32_t>(), f->scan_ws.as<void>(), stream_);
+    }
+    // {M, long-run flag} are final here: read them back now so validate() only waits for this
+    // point of the frame, not for the blend
+    OSB_CUDA_CHECK(cudaMemcpyAsync(f->info_host, f->total.as<uint32_t>(), 8, cudaMemcpyDeviceToHost, stream_));
+    OSB_CUDA_CHECK(cudaEventRecord(f->ready, stream_));
+    // K2c: stable sort by tile over min(M, cap) instances (count read on the device), tile ranges
+    f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(cap), 4));
+    {
+        Span sp(*this, kTileSort);
+        f->inst_in_alt = radix_sort_u32(f->ikeys[0].as<uint32_t>(), f->ikeys[1].as<uint32_t>(),
+                                        f->ivals[0].as<uint32_t>(), f->ivals[1].as<uint32_t>(), static_cast<int>(cap),
+                                        bits_for(static_cast<uint64_t>(tiles)), f->sort_ws.as<void>(), stream_,
+                                        f->total.as<uint32_t>());
+    }
+    {
+        Span sp(*this, kRanges);
+        OSB_CUDA_CHECK(cudaMemsetAsync(f->ranges.as<uint2>(), 0, static_cast<size_t>(tiles) * 8, stream_));
+        launch_ranges(f->ikeys[f->inst_in_alt ? 1 : 0].as<uint32_t>(), static_cast<int>(cap), f->ranges.as<uint2>(),
+                      stream_, f->total.as<uint32_t>());
+    }
+    // K3
+    {
+        Span sp(*this, kBlend);
+        launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(), stream_);
+    }
+    f->validated = false;
+    f->M = cap;  // provisional until validate()
 }
 
-void Engine::backward(const Frame* f, const float* d_image, bool accumulate) {
+void Engine::grow_instances(Frame* f, uint32_t M) {
+    const size_t want = (static_cast<size_t>(M) + M / 4 + 1024) * 4;
+    if (want <= f->ikeys[0].capacity()) return;
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));  // the buffers may still be in use
+    for (int k = 0; k < 2; ++k) {
+        f->ikeys[k].ensure(want);
+        f->ivals[k].ensure(want);
+    }
+}
+
+void Engine::validate(Frame* f) {
+    if (!f || f->validated) return;
     DeviceGuard g(device_);
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        OSB_CUDA_CHECK(cudaEventSynchronize(f->ready));
+        const uint32_t M = f->n == 0 ? 0u : f->info_host[0];
+        const bool long_run = f->info_host[1] != 0 && !f->full_depth_sort;
+        if (M <= f->cap && !long_run) {
+            f->M = M;
+            f->validated = true;
+            return;
+        }
+        if (long_run) f->full_depth_sort = true;
+        grow_instances(f, M);
+        render_into(f);
+    }
+    throw std::runtime_error("render: instance buffer sizing did not converge");
+}
+
+void Engine::release(Frame* f) {
+    if (!f) return;
+    // a frame released unread still tells the pool how large the instance buffers must be
+    if (!f->validated) {
+        DeviceGuard g(device_);
+        OSB_CUDA_CHECK(cudaEventSynchronize(f->ready));
+        if (f->n > 0 && f->info_host[0] > f->cap) grow_instances(f, f->info_host[0]);
+        f->validated = true;
+    }
+    free_.push_back(f);
+}
+
+void Engine::backward(Frame* f, const float* d_image, bool accumulate) {
+    DeviceGuard g(device_);
+    validate(f);
     if (static_cast<size_t>(f->n) != n_ || f->generation != generation_) throw std::logic_error("StateMismatch: render output does not match the cloud");
     // K4b overwrites (no read of the gradient planes, zeros for culled Gaussians) when the buffer is
     // logically zero or the caller asks for reference overwrite semantics.
@@ -454,8 +501,9 @@ void Engine::wait_target() { OSB_CUDA_CHECK(cudaStreamWaitEvent(stream_, target_
 
 void Engine::release_target() { OSB_CUDA_CHECK(cudaEventRecord(target_free_, stream_)); }
 
-double Engine::loss(const Frame* f, const float* gt, double lambda, double mask_bottom_fraction, bool want_value) {
+double Engine::loss(Frame* f, const float* gt, double lambda, double mask_bottom_fraction, bool want_value) {
     DeviceGuard g(device_);
+    validate(f);
     const size_t pixels = static_cast<size_t>(f->W) * f->H;
     float* dimg = d_image_buffer(pixels);
     const int masked = static_cast<int>(std::floor(mask_bottom_fraction * f->H));
@@ -529,8 +577,9 @@ void Engine::reset_screen_stats() {
     OSB_CUDA_CHECK(cudaMemsetAsync(hits_.as<int>(), 0, stride_ * 4, stream_));
 }
 
-void Engine::observe(const Frame* f) {
+void Engine::observe(Frame* f) {
     DeviceGuard g(device_);
+    validate(f);
     if (static_cast<size_t>(f->n) != n_ || f->generation != generation_) throw std::logic_error("StateMismatch: render output does not match the cloud");
     launch_observe(f->radius.as<float>(), max_radius_.as<float>(), f->n, stream_);
 }
@@ -629,8 +678,9 @@ EditSummary Engine::densify_and_prune(const DensifyArgs& a, unsigned long long r
     return e;
 }
 
-double Engine::psnr(const Frame* f, const float* gt) {
+double Engine::psnr(Frame* f, const float* gt) {
     DeviceGuard g(device_);
+    validate(f);
     const long n = 3L * f->W * f->H;
     scratch_.ensure(64);
     launch_sq_err(f->rgb.as<float>(), gt, n, scratch_.as<double>(), stream_);

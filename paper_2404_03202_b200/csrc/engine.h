@@ -71,6 +71,11 @@ struct Frame {
     // per Gaussian (K1 outputs)
     DevBuf depth_key, depth_key32, touched, rect, pxy, conic_o, splat, radius;
     bool full_depth_sort = false;  // set when the FP32-key fast path met a long run of equal keys
+    uint32_t cap = 0;              // instance capacity the frame was rendered with
+    bool validated = true;         // {M, long-run flag} checked (Engine::validate)
+    uint32_t* info_host = nullptr; // pinned {M, long-run flag}
+    cudaEvent_t ready = nullptr;   // recorded after the frame's kernels and the info read-back
+    ~Frame();
     // depth sort
     DevBuf okeys[2], ovals[2], offsets, total;
     // instances
@@ -96,11 +101,14 @@ public:
     void set_active_sh_degree(int d);
 
     Frame* render(const double pose12[12], int W, int H, const double bg[3]);
+    // First use of a frame's results: waits for its instance count and re-renders it in the rare
+    // case of an instance-buffer overflow or a long run of equal FP32 depth keys.
+    void validate(Frame* f);
     void release(Frame* f);
-    void backward(const Frame* f, const float* d_image_planar_dev, bool accumulate);
+    void backward(Frame* f, const float* d_image_planar_dev, bool accumulate);
     // loss() of trainer.cpp:25-71 on the device: d_image into d_image_buffer(); the value is read
     // back only when want_value (one 32-byte read, synchronizes the stream).
-    double loss(const Frame* f, const float* gt_planar_dev, double lambda_ssim, double mask_bottom_fraction,
+    double loss(Frame* f, const float* gt_planar_dev, double lambda_ssim, double mask_bottom_fraction,
                 bool want_value);
     double loss_value(const Frame* f, double mask_bottom_fraction);
     void adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad);
@@ -113,11 +121,11 @@ public:
     void reset_screen_stats();
     // Densification control (trainer.cpp:180-280): DensifyStats::observe of a rendered frame,
     // densify_and_prune with the reference's RNG stream std::mt19937_64(rng_seed), reset_opacity.
-    void observe(const Frame* f);
+    void observe(Frame* f);
     EditSummary densify_and_prune(const DensifyArgs& a, unsigned long long rng_seed);
     void reset_opacity(double ceiling);
     // psnr (metrics.cpp:64-74) of a frame against a device planar FP32 image (synchronizes).
-    double psnr(const Frame* f, const float* gt_planar);
+    double psnr(Frame* f, const float* gt_planar);
     // Adam moments as raw planes (planes x stride floats each) and the step counter.
     void read_adam(std::vector<float>& m, std::vector<float>& v);
     void write_adam(const std::vector<float>& m, const std::vector<float>& v, long step);
@@ -165,7 +173,9 @@ private:
     DevBuf scratch_;
     DevBuf params_, grads_, m_, v_, acc_, d_screen_, norm_sum_, hits_, max_radius_, loss_sum_, d_image_, gt_,
         ssim_planes_;
-    void reset_per_gaussian_state();  // zero gradients' screen stats, d_screen, max radius (GradientBuffer::resize)
+    void reset_per_gaussian_state();
+    void render_into(Frame* f);
+    void grow_instances(Frame* f, uint32_t M);  // zero gradients' screen stats, d_screen, max radius (GradientBuffer::resize)
     double last_lambda_ = 0.0;
     bool grads_zero_ = true;
     std::vector<std::unique_ptr<Frame>> pool_;

@@ -33,8 +33,9 @@ size_t radix_workspace_bytes(int n_max, int key_bytes);
 // the result ends up in *_out when the function returns true, in *_in otherwise.
 bool radix_sort_u64(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
                     int bits, void* ws, cudaStream_t s);
+// n_dev: optional device-side count (the sort covers min(n, *n_dev) elements; grids sized by n).
 bool radix_sort_u32(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
-                    int bits, void* ws, cudaStream_t s);
+                    int bits, void* ws, cudaStream_t s, const uint32_t* n_dev = nullptr);
 void launch_iota(uint32_t* v, int n, cudaStream_t s);
 // After a stable sort by the FP32-rounded depth: restore the exact (FP64 depth, id) order inside
 // runs of equal keys; a run longer than 32 sets *flag (caller falls back to the 64-bit sort).
@@ -45,7 +46,8 @@ void launch_fix_runs(const uint32_t* keys, uint32_t* order, const uint64_t* dept
 size_t scan_workspace_bytes(int n);
 void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
                       uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws, cudaStream_t s);
-void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s);
+void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s,
+                   const uint32_t* m_dev = nullptr);
 
 // ---- K3 blend (blend.cu) --------------------------------------------------------------------
 struct FrameBuffers {

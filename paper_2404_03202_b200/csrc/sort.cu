@@ -37,16 +37,25 @@ struct SortCfg<uint64_t> {
 };
 template <>
 struct SortCfg<uint32_t> {
-    static constexpr int kItems = 16;
+    static constexpr int kItems = 8;
 };
 template <typename K>
 __host__ __device__ constexpr int tile_keys() {
     return kSortThreads * SortCfg<K>::kItems;
 }
 
+// Element count of a sort: the host bound, or min(bound, *n_dev) when the count lives on the device
+// (the tile sort runs before the host knows M; the grid is sized for the buffer capacity).
+__device__ __forceinline__ int sort_count(int n_cap, const uint32_t* n_dev) {
+    if (!n_dev) return n_cap;
+    const uint32_t m = *n_dev;
+    return m < static_cast<uint32_t>(n_cap) ? static_cast<int>(m) : n_cap;
+}
+
 template <typename K>
-__global__ void __launch_bounds__(256) k_histogram(const K* __restrict__ keys, int n, int passes,
-                                                   uint32_t* __restrict__ hist /* passes x 256 */) {
+__global__ void __launch_bounds__(256) k_histogram(const K* __restrict__ keys, int n_cap, const uint32_t* n_dev,
+                                                   int passes, uint32_t* __restrict__ hist /* passes x 256 */) {
+    const int n = sort_count(n_cap, n_dev);
     __shared__ uint32_t s_hist[kMaxPasses][kBins];
     for (int i = threadIdx.x; i < passes * kBins; i += blockDim.x) (&s_hist[0][0])[i] = 0;
     __syncthreads();
@@ -107,15 +116,16 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
 
 // Per-block digit counts for one pass: counts[d * nblocks + b].
 template <typename K>
-__global__ void __launch_bounds__(kSortThreads) k_upsweep(const K* __restrict__ keys, int n, int shift, int nblocks,
-                                                          uint32_t* __restrict__ counts) {
+__global__ void __launch_bounds__(kSortThreads) k_upsweep(const K* __restrict__ keys, int n_cap, const uint32_t* n_dev,
+                                                          int shift, int nblocks, uint32_t* __restrict__ counts) {
+    const int n = sort_count(n_cap, n_dev);
     constexpr int kTile = tile_keys<K>();
     __shared__ uint32_t s_hist[kSortWarps][kBins];
     const int warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kSortWarps * kBins; i += kSortThreads) (&s_hist[0][0])[i] = 0;
     __syncthreads();
     const long base = static_cast<long>(blockIdx.x) * kTile;
-    const int count = static_cast<int>(min(static_cast<long>(kTile), static_cast<long>(n) - base));
+    const int count = static_cast<int>(max(0L, min(static_cast<long>(kTile), static_cast<long>(n) - base)));
     for (int i = threadIdx.x; i < count; i += kSortThreads)
         atomicAdd(&s_hist[warp][static_cast<uint32_t>((keys[base + i] >> shift) & (kBins - 1))], 1u);
     __syncthreads();
@@ -149,8 +159,10 @@ template <typename K>
 __global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict__ keys_in,
                                                             const uint32_t* __restrict__ vals_in,
                                                             K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
-                                                            int n, int shift, int nblocks,
+                                                            int n_cap, const uint32_t* n_dev, int shift, int nblocks,
                                                             const uint32_t* __restrict__ offsets) {
+    const int n = sort_count(n_cap, n_dev);
+    if (static_cast<long>(blockIdx.x) * kSortThreads * SortCfg<K>::kItems >= n) return;
     constexpr int kItems = SortCfg<K>::kItems;
     constexpr int kTile = kSortThreads * kItems;
     __shared__ uint32_t s_warp[kSortWarps][kBins];
@@ -400,7 +412,9 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
     }
 }
 
-__global__ void k_ranges(const uint32_t* __restrict__ keys, int m, uint2* __restrict__ ranges) {
+__global__ void k_ranges(const uint32_t* __restrict__ keys, int m_cap, const uint32_t* m_dev,
+                         uint2* __restrict__ ranges) {
+    const int m = sort_count(m_cap, m_dev);
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= m) return;
     const uint32_t k = keys[i];
@@ -410,8 +424,8 @@ __global__ void k_ranges(const uint32_t* __restrict__ keys, int m, uint2* __rest
 
 // Workspace: hist[8][256] | base[8][256] | counts[256][blocks] | offsets[256][blocks]
 template <typename K>
-bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n, int bits, void* ws,
-                cudaStream_t s) {
+bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n, const uint32_t* n_dev, int bits,
+                void* ws, cudaStream_t s) {
     if (n <= 1) return false;
     const int passes = (bits + kRadixBits - 1) / kRadixBits;
     const int blocks = (n + tile_keys<K>() - 1) / tile_keys<K>();
@@ -421,7 +435,7 @@ bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, 
     uint32_t* offsets = counts + static_cast<size_t>(kBins) * blocks;
     OSB_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kBins, s));
     const int hblocks = blocks < 148 * 4 ? blocks : 148 * 4;
-    k_histogram<K><<<hblocks, 256, 0, s>>>(keys_in, n, passes, hist);
+    k_histogram<K><<<hblocks, 256, 0, s>>>(keys_in, n, n_dev, passes, hist);
     k_scan_hist<<<passes, kBins, 0, s>>>(hist, base);
     OSB_LAUNCHED(2);
     bool flipped = false;
@@ -431,9 +445,9 @@ bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, 
         uint32_t* vi = flipped ? vals_out : vals_in;
         uint32_t* vo = flipped ? vals_in : vals_out;
         const int shift = p * kRadixBits;
-        k_upsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, n, shift, blocks, counts);
+        k_upsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, n, n_dev, shift, blocks, counts);
         k_scan_counts<<<kBins, kSortThreads, 0, s>>>(counts, blocks, base + p * kBins, offsets);
-        k_downsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, shift, blocks, offsets);
+        k_downsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, n_dev, shift, blocks, offsets);
         OSB_LAUNCHED(3);
         flipped = !flipped;
     }
@@ -443,18 +457,19 @@ bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, 
 }  // namespace
 
 size_t radix_workspace_bytes(int n_max, int key_bytes) {
-    const int tk = key_bytes == 8 ? tile_keys<uint64_t>() : tile_keys<uint32_t>();
+    (void)key_bytes;  // sized for the smaller tile of either key type (the buffer serves both sorts)
+    const int tk = tile_keys<uint64_t>() < tile_keys<uint32_t>() ? tile_keys<uint64_t>() : tile_keys<uint32_t>();
     const size_t blocks = (static_cast<size_t>(n_max) + tk - 1) / tk;
     return sizeof(uint32_t) * (2 * kMaxPasses * kBins + 2 * kBins * blocks) + 256;
 }
 
 bool radix_sort_u64(uint64_t* ki, uint64_t* ko, uint32_t* vi, uint32_t* vo, int n, int bits, void* ws,
                     cudaStream_t s) {
-    return radix_sort<uint64_t>(ki, ko, vi, vo, n, bits, ws, s);
+    return radix_sort<uint64_t>(ki, ko, vi, vo, n, nullptr, bits, ws, s);
 }
 bool radix_sort_u32(uint32_t* ki, uint32_t* ko, uint32_t* vi, uint32_t* vo, int n, int bits, void* ws,
-                    cudaStream_t s) {
-    return radix_sort<uint32_t>(ki, ko, vi, vo, n, bits, ws, s);
+                    cudaStream_t s, const uint32_t* n_dev) {
+    return radix_sort<uint32_t>(ki, ko, vi, vo, n, n_dev, bits, ws, s);
 }
 
 void launch_iota(uint32_t* v, int n, cudaStream_t s) {
@@ -491,9 +506,9 @@ void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4
     OSB_LAUNCHED(grid > 0 ? 4 : 3);
 }
 
-void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s) {
+void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s, const uint32_t* m_dev) {
     if (m <= 0) return;
-    k_ranges<<<(m + 255) / 256, 256, 0, s>>>(sorted_tiles, m, ranges);
+    k_ranges<<<(m + 255) / 256, 256, 0, s>>>(sorted_tiles, m, m_dev, ranges);
     OSB_LAUNCHED(1);
 }
 

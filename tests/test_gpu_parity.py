@@ -238,3 +238,34 @@ def test_active_sh_degree(active, oracle_port):
     assert np.all(g["d_sh"][:, bc_active:, :] == 0.0)
     for k, (nbad, total, maxrel) in grads_close(g, go).items():
         assert nbad <= max(2, total // 20000), (k, nbad, total, maxrel)
+
+
+def test_instance_buffer_growth_rerenders_exactly(oracle_port):
+    """Frames are enqueued without a host sync; a frame whose instances outgrow the pooled buffer
+    is re-rendered on first use (Engine::validate) and must still equal the oracle."""
+    cloud = scenes.synthetic_cloud(3000, seed=13)
+    ctx = native.Context(cloud)
+    ctx.render(scenes.identity_pose(), 64, 32).free()  # sizes the pooled frame for ~1/16 the instances
+    pose = scenes.random_pose(np.random.default_rng(4))
+    fr = ctx.render(pose, 512, 256)
+    of = oracle_port.render(cloud, pose, 512, 256)
+    nbad, first = compare_tiles(fr, of)
+    assert nbad == 0, (nbad, first)
+    assert np.max(np.abs(fr.image() - of.rgb)) <= IMAGE_ATOL
+    fr.free()
+
+
+def test_equal_depth_runs_fall_back_to_the_exact_sort(oracle_port):
+    """More than 32 Gaussians at bit-identical depth defeat the FP32-key fast path; the frame is
+    re-rendered with the 64-bit depth sort and the (depth, id) order stays exact."""
+    cloud = scenes.synthetic_cloud(2000, seed=14)
+    # 64 copies of one Gaussian's position (identical t_r), spread colours
+    cloud.positions[100:164] = cloud.positions[100]
+    cloud.sh[100:164, 0, :] = np.linspace(-0.4, 0.4, 64)[:, None]
+    ctx = native.Context(cloud)
+    pose = scenes.identity_pose()
+    fr = ctx.render(pose, 256, 128)
+    of = oracle_port.render(cloud, pose, 256, 128)
+    nbad, first = compare_tiles(fr, of)
+    assert nbad == 0, (nbad, first)
+    assert np.max(np.abs(fr.image() - of.rgb)) <= IMAGE_ATOL
