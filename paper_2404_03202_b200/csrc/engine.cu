@@ -327,7 +327,7 @@ void Engine::render_into(Frame* f) {
                           active_, f->pose, W, H, pp, stream_);
     }
     // K2a: depth rank = (t_r, id) order. Fast path: stable sort of the FP32-rounded t_r (monotone)
-    // + exact FP64 re-ordering inside runs of equal FP32 keys; a run longer than 32 raises a flag
+    // + exact FP64 re-ordering inside runs of equal keys; a run longer than 64 raises a flag
     // and validate() renders the frame again with the full 64-bit sort.
     f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(n), 8));
     uint32_t* long_run_flag = f->total.as<uint32_t>() + 1;
@@ -345,7 +345,7 @@ void Engine::render_into(Frame* f) {
         } else {
             uint32_t* k32[2] = {f->okeys[0].as<uint32_t>(), f->okeys[1].as<uint32_t>()};
             OSB_CUDA_CHECK(cudaMemcpyAsync(k32[0], pp.depth_key32, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
-            flipped = radix_sort_u32(k32[0], k32[1], f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N, 32,
+            flipped = radix_sort_u32(k32[0], k32[1], f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N, 24,
                                      f->sort_ws.as<void>(), stream_);
             launch_fix_runs(k32[flipped ? 1 : 0], f->ovals[flipped ? 1 : 0].as<uint32_t>(), pp.depth_key, N,
                             long_run_flag, stream_);

@@ -15,7 +15,7 @@ long long launches_total();
 // ---- K1 preprocess (preprocess.cu) --------------------------------------------------------
 struct PreprocessOut {
     uint64_t* depth_key;   // N: bit pattern of t_r (monotone), ~0 when culled
-    uint32_t* depth_key32; // N: bit pattern of (float)t_r (monotone, coarser), ~0 when culled
+    uint32_t* depth_key32; // N: 24-bit monotone depth key (FP32 bits above the near plane >> 4), 0xFFFFFF culled
     uint32_t* touched;     // N: tile instances this Gaussian emits
     int4* rect;            // N: {tx0, tx1, ty0, ty1} (tx may wrap)
     double2* pxy;          // N: FP64 pixel centre

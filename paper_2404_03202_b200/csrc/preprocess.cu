@@ -12,6 +12,18 @@ namespace osb {
 
 namespace {
 
+// 24-bit depth key for the 3-pass fast depth rank: the FP32 bit pattern of t_r (monotone for
+// positive values) above that of the near plane (t_r >= 0.01 for every visible Gaussian), with the
+// 4 lowest mantissa bits dropped (runs of equal keys are re-ordered exactly by k_fix_runs) and
+// clamped below the culled key. Monotone non-decreasing in t_r.
+constexpr uint32_t kDepthKeyCulled = 0xFFFFFFu;
+__device__ __forceinline__ uint32_t depth_key24(double t_r) {
+    const uint32_t bits = __float_as_uint(__double2float_rn(t_r));
+    const uint32_t near = 0x3C23D70Au;  // bits of 0.01f
+    const uint32_t k = bits > near ? (bits - near) >> 4 : 0u;
+    return k < kDepthKeyCulled - 1 ? k : kDepthKeyCulled - 1;
+}
+
 template <int DEG>
 __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P, int n, int stride, int bc, Pose pose,
                                                     int W, int H, PreprocessOut out) {
@@ -22,7 +34,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
     Proj64 pr;
     if (!project64(P, stride, pl, gid, pose, W, H, pr)) {
         out.depth_key[gid] = ~0ull;
-        out.depth_key32[gid] = ~0u;
+        out.depth_key32[gid] = kDepthKeyCulled;
         out.touched[gid] = 0;
         out.radius[gid] = -1.0f;
         return;
@@ -87,7 +99,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
     if (!(delta < 1e30)) delta = 1e30;
 
     out.depth_key[gid] = static_cast<uint64_t>(__double_as_longlong(pr.t_r));
-    out.depth_key32[gid] = __float_as_uint(__double2float_rn(pr.t_r));  // monotone non-decreasing in t_r
+    out.depth_key32[gid] = depth_key24(pr.t_r);
     out.touched[gid] = touched;
     out.radius[gid] = static_cast<float>(radius);
     out.rect[gid] = make_int4(tx0, tx1, ty0, ty1);

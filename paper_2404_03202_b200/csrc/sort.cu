@@ -518,7 +518,7 @@ namespace osb {
 
 namespace {
 
-constexpr int kMaxRun = 32;
+constexpr int kMaxRun = 64;
 
 // Exact (FP64 depth, id) order inside runs of equal FP32-rounded depth keys (the stable FP32 sort
 // left each run in ascending id order). Runs longer than kMaxRun raise *flag: the caller then
@@ -528,7 +528,7 @@ __global__ void k_fix_runs(const uint32_t* __restrict__ keys, uint32_t* __restri
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t k = keys[i];
-    if (k == 0xFFFFFFFFu) return;                     // culled tail: no instances, order irrelevant
+    if (k == 0xFFFFFFu) return;                       // culled tail: no instances, order irrelevant
     if (i > 0 && keys[i - 1] == k) return;            // not a run start
     if (i + 1 >= n || keys[i + 1] != k) return;       // run of one
     int e = i + 1;
