@@ -1,11 +1,11 @@
 // backward.cu — K4a (per-pixel, reverse order) and K4b (per-Gaussian chain rule, FP64).
 //
 // K4a replaces backward() pass 1 + pass 2 (proj/src/gradients.cpp:96-169): same CTA/tile layout
-// as K3 (warp-compacted entry lists, pair.cuh), list walked back to front from each pixel's
-// last_contrib. The 9 per-entry accumulators (d_colour 3, d_opacity, d_p 2, d_conic 3) of the
-// warp's pixels are combined with a reduce-scatter shuffle tree (12 shuffles instead of 45) and
-// added by one warp-wide red.global.add.f32 (9 lanes, 9 consecutive floats); an entry touched by
-// a single pixel of the warp is added directly by that lane. Pair decisions are the forward's;
+// and half-warp culling as K3 (pair.cuh), each 4x4 quarter walking its entries back to front from
+// each pixel's last_contrib. The 9 per-entry accumulators (d_colour 3, d_opacity, d_p 2, d_conic 3)
+// of a quarter's pixels are combined with a reduce-scatter shuffle tree inside the half-warp and
+// added by one red.global.add.f32 per value; an entry touched by a single pixel of the quarter is
+// added directly by that lane (2 x red.v4 + 1). Pair decisions are the forward's;
 // the 0.99 clamp gate (gradients.cpp:146) has its own FP64 guard.
 //
 // K4b replaces pass 3 (gradients.cpp:173-295): one thread per visible Gaussian, FP64 internals,
@@ -27,37 +27,37 @@ __device__ __forceinline__ void red_add(float* addr, float a) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(a) : "memory");
 }
 
-// Reduce-scatter of 9 values over the warp. Afterwards the lane pair (l, l^1) holds the full sum
-// of value *idx (or idx = -1 for a padding slot); levels split 9 -> 5 -> 3 -> 2 -> 1.
-__device__ __forceinline__ float warp_reduce9(const float (&v)[9], int lane, int* idx) {
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+// Reduce-scatter of 9 values inside each 16-lane half (xor 8, 4, 2, 1; 9 -> 5 -> 3 -> 2 -> 1 values
+// per lane, 10 shuffles): both halves reduce their own entry at once; afterwards lane l of a half
+// holds the half's sum of value *idx (-1: padding).
+__device__ __forceinline__ float half_reduce9(const float (&v)[9], int lane, int* idx) {
+    const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
     float a[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
         const float lo = v[i];
         const float hi = i + 5 < 9 ? v[i + 5] : 0.0f;
-        a[i] = (b4 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b4 ? lo : hi, 16);
+        a[i] = (b3 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b3 ? lo : hi, 8);
     }
     float c[3];
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         const float lo = a[i];
         const float hi = i + 3 < 5 ? a[i + 3] : 0.0f;
-        c[i] = (b3 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b3 ? lo : hi, 8);
+        c[i] = (b2 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b2 ? lo : hi, 4);
     }
     float e[2];
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         const float lo = c[i];
         const float hi = i + 2 < 3 ? c[i + 2] : 0.0f;
-        e[i] = (b2 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b2 ? lo : hi, 4);
+        e[i] = (b1 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b1 ? lo : hi, 2);
     }
-    float f = (b1 ? e[1] : e[0]) + __shfl_xor_sync(0xffffffffu, b1 ? e[0] : e[1], 2);
-    f += __shfl_xor_sync(0xffffffffu, f, 1);
-    const int i2 = (b2 ? 2 : 0) + (b1 ? 1 : 0);
-    const int i1 = (b3 ? 3 : 0) + i2;
-    const bool pad = (b2 && b1) || (b3 && i2 == 2) || (b4 && i1 == 4);
-    *idx = pad ? -1 : (b4 ? 5 : 0) + i1;
+    const float f = (b0 ? e[1] : e[0]) + __shfl_xor_sync(0xffffffffu, b0 ? e[0] : e[1], 1);
+    const int ic = (b1 ? 2 : 0) + (b0 ? 1 : 0);
+    const int ia = (b2 ? 3 : 0) + ic;
+    const bool pad = (b1 && b0) || (b2 && ic == 2) || (b3 && ia == 4);
+    *idx = pad ? -1 : (b3 ? 5 : 0) + ia;
     return f;
 }
 
@@ -98,21 +98,27 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
     float lc0 = 0.0f, lc1 = 0.0f, lc2 = 0.0f;  // last colour
     float last_a = 0.0f;
 
+    // Each 16-lane half owns a 4x4 pixel quarter and walks the entries that can reach it (the same
+    // half-warp culling as K3), back to front; the halves reduce their (different) entries at once.
+    const uint32_t halfmask = wp.half ? 0xFFFF0000u : 0x0000FFFFu;
     for (int hi = max_last; hi > 0; hi -= 32) {
         const int lo = hi > 32 ? hi - 32 : 0;
         const int cnt = hi - lo;
-        bool reach = false;
+        uint32_t reach = 0u;
         if (lane < cnt)
-            reach = stage_entry(ws, lane, inst_gid[range.x + lo + lane], pp.pxy, pp.splat, xc, yc, width, wp.r0, wp.c0) != 0u;
-        uint32_t bal = __ballot_sync(0xffffffffu, reach);
+            reach = stage_entry(ws, lane, inst_gid[range.x + lo + lane], pp.pxy, pp.splat, xc, yc, width, wp.r0, wp.c0);
+        const uint32_t bal0 = __ballot_sync(0xffffffffu, reach & 1u);
+        const uint32_t bal1 = __ballot_sync(0xffffffffu, reach & 2u);
+        uint32_t bal = wp.half ? bal1 : bal0;
         __syncwarp();
-        while (bal != 0u) {  // back to front; uniform over the warp (the reduction needs all lanes)
-            const int j = 31 - __clz(bal);
+        while (__any_sync(0xffffffffu, bal != 0u)) {  // back to front; warp-uniform (the reduction needs all lanes)
+            const bool live = bal != 0u;
+            const int j = live ? 31 - __clz(bal) : 0;
             bal &= ~(1u << j);
             const int k = lo + j;
             float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f, v5 = 0.f, v6 = 0.f, v7 = 0.f, v8 = 0.f;
             bool has = false;
-            if (k < last) {
+            if (live && k < last) {
                 const float4 A = ws.a[j];
                 const float4 B = ws.b[j];
                 float dx, dy, power;
@@ -175,20 +181,21 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
                     }
                 }
             }
-            const uint32_t hb = __ballot_sync(0xffffffffu, has);
-            if (hb == 0u) continue;
+            const uint32_t hb_all = __ballot_sync(0xffffffffu, has);
+            if (hb_all == 0u) continue;
+            const uint32_t hb = hb_all & halfmask;  // this half's contributing lanes
             float* a = reinterpret_cast<float*>(acc + 3 * static_cast<size_t>(ws.gid[j]));
-            if ((hb & (hb - 1u)) == 0u) {
-                if (has) {
-                    red_add_v4(reinterpret_cast<float4*>(a), v0, v1, v2, v3);
-                    red_add_v4(reinterpret_cast<float4*>(a) + 1, v4, v5, v6, v7);
-                    red_add(a + 8, v8);
-                }
-            } else {
+            const bool multi = (hb & (hb - 1u)) != 0u;
+            if (!multi && has) {  // a single pixel of this quarter: add directly
+                red_add_v4(reinterpret_cast<float4*>(a), v0, v1, v2, v3);
+                red_add_v4(reinterpret_cast<float4*>(a) + 1, v4, v5, v6, v7);
+                red_add(a + 8, v8);
+            }
+            if (__any_sync(0xffffffffu, multi)) {
                 const float v[9] = {v0, v1, v2, v3, v4, v5, v6, v7, v8};
                 int idx;
-                const float sum = warp_reduce9(v, lane, &idx);
-                if (idx >= 0 && !(lane & 1)) red_add(a + idx, sum);
+                const float sum = half_reduce9(v, lane, &idx);
+                if (multi && idx >= 0) red_add(a + idx, sum);
             }
         }
         __syncwarp();
