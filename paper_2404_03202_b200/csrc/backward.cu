@@ -61,6 +61,8 @@ __device__ __forceinline__ float half_reduce9(const float (&v)[9], int lane, int
     return f;
 }
 
+// BG: a non-black background adds the -T_final / (1 - alpha) * (bg . dL/dC) term (gradients.cpp:141).
+template <bool BG>
 __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint32_t* __restrict__ inst_gid,
                                                                      const uint2* __restrict__ ranges, PreprocessOut pp,
                                                                      int W, int H, int tiles_x, float bg0, float bg1,
@@ -138,13 +140,16 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
                         g = ex2_approx(-power * kLog2e);
                         const float og = Cc.w * g;
                         alpha = fminf(0.99f, og);
-                        const float band = 0.99f * (1.5f * fabsf(B.w) + 1e-6f);
-                        if (fabsf(og - 0.99f) <= band) {
-                            Pair64 p;
-                            pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
-                            gate = p.og < kAlphaMax;
-                        } else {
-                            gate = og < 0.99f;
+                        gate = true;  // o g <= o < 0.98 < 0.99 for all but the most opaque splats
+                        if (Cc.w >= 0.98f) {
+                            const float band = 0.99f * (1.5f * fabsf(B.w) + 1e-6f);
+                            if (fabsf(og - 0.99f) <= band) {
+                                Pair64 p;
+                                pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
+                                gate = p.og < kAlphaMax;
+                            } else {
+                                gate = og < 0.99f;
+                            }
                         }
                     }
                     if (ok) {
@@ -163,7 +168,8 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
                         float d_alpha = (Cc.x - s0) * dl0;
                         d_alpha = __fmaf_rn(Cc.y - s1, dl1, d_alpha);
                         d_alpha = __fmaf_rn(Cc.z - s2, dl2, d_alpha);
-                        d_alpha = d_alpha * T_acc - (T_final * inv) * bg_dot;
+                        d_alpha = d_alpha * T_acc;
+                        if (BG) d_alpha = d_alpha - (T_final * inv) * bg_dot;
                         lc0 = Cc.x; lc1 = Cc.y; lc2 = Cc.z;
                         last_a = alpha;
                         if (gate) {
@@ -436,8 +442,12 @@ void launch_backward_pixels(const uint32_t* inst_gid, const uint2* ranges, const
                             float4* acc, cudaStream_t s) {
     const int tiles = tiles_x * tiles_y;
     if (tiles <= 0) return;
-    k_backward_pixels<<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb, d_image,
-                                                acc);
+    if (bg[0] != 0.0f || bg[1] != 0.0f || bg[2] != 0.0f)
+        k_backward_pixels<true><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2],
+                                                               fb, d_image, acc);
+    else
+        k_backward_pixels<false><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1],
+                                                                bg[2], fb, d_image, acc);
     OSB_LAUNCHED(1);
 }
 
