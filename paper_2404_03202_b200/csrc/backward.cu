@@ -173,16 +173,15 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
                         lc0 = Cc.x; lc1 = Cc.y; lc2 = Cc.z;
                         last_a = alpha;
                         if (gate) {
+                            // dL/dpower times d, d d^T: K4b applies the conic once per Gaussian
+                            // (d_p = Q sum(dL/dpower d)) and the 1/2 of the conic diagonal
                             v3 = g * d_alpha;
                             const float d_power = -g * Cc.w * d_alpha;
-                            const float qx = __fmaf_rn(2.0f * A.z, dx, B.x * dy);
-                            const float qy = __fmaf_rn(B.x, dx, 2.0f * A.w * dy);
-                            v4 = d_power * qx;
-                            v5 = d_power * qy;
-                            const float hp = 0.5f * d_power;
-                            v6 = hp * dx * dx;
-                            v7 = d_power * dx * dy;
-                            v8 = hp * dy * dy;
+                            v4 = d_power * dx;
+                            v5 = d_power * dy;
+                            v6 = v4 * dx;
+                            v7 = v4 * dy;
+                            v8 = v5 * dy;
                         }
                     }
                 }
@@ -301,7 +300,11 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
     const float4 a0 = acc[3 * static_cast<size_t>(gid)];
     const float4 a1 = acc[3 * static_cast<size_t>(gid) + 1];
     const float4 a2 = acc[3 * static_cast<size_t>(gid) + 2];
-    const double d_p[2] = {a1.x, a1.y};
+    const double4 co = conic_o[gid];
+    // K4a accumulated sum(dL/dpower * d) and sum(dL/dpower * d d^T); dpower/dp = Q d with the
+    // FP64 conic (gradients.cpp:148-152), dpower/dconic = (d_x^2 / 2, d_x d_y, d_y^2 / 2)
+    const double sdx = a1.x, sdy = a1.y;
+    const double d_p[2] = {co.x * sdx + co.y * sdy, co.y * sdx + co.z * sdy};
 
     // screen-space gradient and densification statistics (gradients.cpp:180-183)
     const double ds0 = d_p[0] * W * 0.5, ds1 = d_p[1] * H * 0.5;
@@ -310,7 +313,6 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
     st.hits[gid] += 1;
 
     // opacity through the sigmoid (gradients.cpp:186-187)
-    const double4 co = conic_o[gid];
     const double o = co.w;
     put_grad<OVERWRITE>(G, stride, pl.opacity(), gid, static_cast<double>(a0.w) * o * (1.0 - o));
 
@@ -343,7 +345,8 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
 
     // covariance path (gradients.cpp:216-254)
     const double qa = co.x, qb = co.y, qc = co.z;
-    const double da = a1.z, db = 0.5 * static_cast<double>(a1.w), dc = a2.x;
+    const double da = 0.5 * static_cast<double>(a1.z), db = 0.5 * static_cast<double>(a1.w),
+                 dc = 0.5 * static_cast<double>(a2.x);
     const double m00 = qa * da + qb * db, m01 = qa * db + qb * dc;
     const double m10 = qb * da + qc * db, m11 = qb * db + qc * dc;
     const double dva = -(m00 * qa + m01 * qb);
