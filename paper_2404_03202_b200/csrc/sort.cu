@@ -196,7 +196,15 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict_
         const long idx = base + i * 32 + lane;
         const bool valid = idx < n;
         const uint32_t d = valid ? static_cast<uint32_t>((key[i] >> shift) & (kBins - 1)) : kBins;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        // lanes with the same digit: one ballot per digit bit (match.any has a long latency here)
+        uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int b = 0; b < kRadixBits; ++b) {
+            const bool bit = (d >> b) & 1u;
+            const uint32_t vote = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? vote : ~vote;
+        }
+        if (!valid) peers = 1u << lane;
         const int leader = __ffs(peers) - 1;
         uint32_t prev = 0;
         if (valid && lane == leader) {
