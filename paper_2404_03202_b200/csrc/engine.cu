@@ -52,6 +52,7 @@ PreprocessOut Frame::pp() const {
     PreprocessOut o;
     o.depth_key = depth_key.as<uint64_t>();
     o.depth_key32 = depth_key32.as<uint32_t>();
+    o.depth_range = depth_range.as<uint32_t>();
     o.touched = touched.as<uint32_t>();
     o.rect = rect.as<int4>();
     o.pxy = pxy.as<double2>();
@@ -292,6 +293,7 @@ void Engine::render_into(Frame* f) {
     const int tiles = f->tiles_x * f->tiles_y;
     f->depth_key.ensure(n * 8);
     f->depth_key32.ensure(n * 4);
+    f->depth_range.ensure(8);
     f->touched.ensure(n * 4);
     f->rect.ensure(n * 16);
     f->pxy.ensure(n * 16);
@@ -323,6 +325,7 @@ void Engine::render_into(Frame* f) {
     // K1
     {
         Span sp(*this, kPreprocess);
+        OSB_CUDA_CHECK(cudaMemsetAsync(pp.depth_range, 0xFF, 8, stream_));
         launch_preprocess(params_.as<float>(), N, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
                           active_, f->pose, W, H, pp, stream_);
     }
@@ -344,7 +347,7 @@ void Engine::render_into(Frame* f) {
                                      f->ovals[1].as<uint32_t>(), N, 64, f->sort_ws.as<void>(), stream_);
         } else {
             uint32_t* k32[2] = {f->okeys[0].as<uint32_t>(), f->okeys[1].as<uint32_t>()};
-            OSB_CUDA_CHECK(cudaMemcpyAsync(k32[0], pp.depth_key32, n_ * 4, cudaMemcpyDeviceToDevice, stream_));
+            launch_depth_key24(pp.depth_key32, pp.depth_range, N, k32[0], stream_);
             flipped = radix_sort_u32(k32[0], k32[1], f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N, 24,
                                      f->sort_ws.as<void>(), stream_);
             launch_fix_runs(k32[flipped ? 1 : 0], f->ovals[flipped ? 1 : 0].as<uint32_t>(), pp.depth_key, N,

@@ -69,7 +69,7 @@ struct Frame {
     float bg[3] = {0, 0, 0};
     bool inst_in_alt = false;  // sorted instance gids live in inst_vals[1]
     // per Gaussian (K1 outputs)
-    DevBuf depth_key, depth_key32, touched, rect, pxy, conic_o, splat, radius;
+    DevBuf depth_key, depth_key32, depth_range, touched, rect, pxy, conic_o, splat, radius;
     bool full_depth_sort = false;  // set when the FP32-key fast path met a long run of equal keys
     uint32_t cap = 0;              // instance capacity the frame was rendered with
     bool validated = true;         // {M, long-run flag} checked (Engine::validate)

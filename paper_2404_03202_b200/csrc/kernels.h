@@ -15,7 +15,8 @@ long long launches_total();
 // ---- K1 preprocess (preprocess.cu) --------------------------------------------------------
 struct PreprocessOut {
     uint64_t* depth_key;   // N: bit pattern of t_r (monotone), ~0 when culled
-    uint32_t* depth_key32; // N: 24-bit monotone depth key (FP32 bits above the near plane >> 4), 0xFFFFFF culled
+    uint32_t* depth_key32; // N: FP32 bit pattern of t_r (monotone), ~0 when culled
+    uint32_t* depth_range; // {min bits, ~max bits} over visible Gaussians (both atomicMin, init ~0)
     uint32_t* touched;     // N: tile instances this Gaussian emits
     int4* rect;            // N: {tx0, tx1, ty0, ty1} (tx may wrap)
     double2* pxy;          // N: FP64 pixel centre
@@ -37,6 +38,9 @@ bool radix_sort_u64(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, ui
 bool radix_sort_u32(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
                     int bits, void* ws, cudaStream_t s, const uint32_t* n_dev = nullptr);
 void launch_iota(uint32_t* v, int n, cudaStream_t s);
+// keys24[i] = (bits[i] - min) >> shift with the smallest shift that fits the visible range below
+// 0xFFFFFF (culled -> 0xFFFFFF): a monotone 24-bit depth key for the 3-pass fast depth rank.
+void launch_depth_key24(const uint32_t* bits, const uint32_t* range, int n, uint32_t* keys24, cudaStream_t s);
 // After a stable sort by the FP32-rounded depth: restore the exact (FP64 depth, id) order inside
 // runs of equal keys; a run longer than 32 sets *flag (caller falls back to the 64-bit sort).
 void launch_fix_runs(const uint32_t* keys, uint32_t* order, const uint64_t* depth_key, int n, uint32_t* flag,

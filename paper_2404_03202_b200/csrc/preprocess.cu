@@ -12,18 +12,6 @@ namespace osb {
 
 namespace {
 
-// 24-bit depth key for the 3-pass fast depth rank: the FP32 bit pattern of t_r (monotone for
-// positive values) above that of the near plane (t_r >= 0.01 for every visible Gaussian), with the
-// 4 lowest mantissa bits dropped (runs of equal keys are re-ordered exactly by k_fix_runs) and
-// clamped below the culled key. Monotone non-decreasing in t_r.
-constexpr uint32_t kDepthKeyCulled = 0xFFFFFFu;
-__device__ __forceinline__ uint32_t depth_key24(double t_r) {
-    const uint32_t bits = __float_as_uint(__double2float_rn(t_r));
-    const uint32_t near = 0x3C23D70Au;  // bits of 0.01f
-    const uint32_t k = bits > near ? (bits - near) >> 4 : 0u;
-    return k < kDepthKeyCulled - 1 ? k : kDepthKeyCulled - 1;
-}
-
 template <int DEG>
 __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P, int n, int stride, int bc, Pose pose,
                                                     int W, int H, PreprocessOut out) {
@@ -34,7 +22,7 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
     Proj64 pr;
     if (!project64(P, stride, pl, gid, pose, W, H, pr)) {
         out.depth_key[gid] = ~0ull;
-        out.depth_key32[gid] = kDepthKeyCulled;
+        out.depth_key32[gid] = 0xFFFFFFFFu;
         out.touched[gid] = 0;
         out.radius[gid] = -1.0f;
         return;
@@ -99,7 +87,16 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
     if (!(delta < 1e30)) delta = 1e30;
 
     out.depth_key[gid] = static_cast<uint64_t>(__double_as_longlong(pr.t_r));
-    out.depth_key32[gid] = depth_key24(pr.t_r);
+    // FP32 bits of t_r (monotone for positive values) and the frame's visible range of them (the
+    // depth-rank sort keys are these bits relative to the minimum, shifted into 24 bits)
+    const uint32_t dbits = __float_as_uint(__double2float_rn(pr.t_r));
+    out.depth_key32[gid] = dbits;
+    const uint32_t act = __activemask();
+    const uint32_t wmin = __reduce_min_sync(act, dbits), wmax = __reduce_max_sync(act, dbits);
+    if ((threadIdx.x & 31) == __ffs(act) - 1) {
+        atomicMin(out.depth_range, wmin);
+        atomicMin(out.depth_range + 1, ~wmax);
+    }
     out.touched[gid] = touched;
     out.radius[gid] = static_cast<float>(radius);
     out.rect[gid] = make_int4(tx0, tx1, ty0, ty1);

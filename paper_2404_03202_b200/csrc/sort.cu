@@ -254,6 +254,18 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict_
     }
 }
 
+__global__ void k_depth_key24(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ range, int n,
+                              uint32_t* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t lo = range[0], hi = ~range[1];
+    const uint32_t span = hi >= lo ? hi - lo : 0u;
+    int shift = 0;
+    while ((span >> shift) >= 0xFFFFFFu) ++shift;
+    const uint32_t b = bits[i];
+    out[i] = b == 0xFFFFFFFFu ? 0xFFFFFFu : (b - lo) >> shift;
+}
+
 __global__ void k_iota(uint32_t* v, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) v[i] = static_cast<uint32_t>(i);
@@ -478,6 +490,12 @@ bool radix_sort_u64(uint64_t* ki, uint64_t* ko, uint32_t* vi, uint32_t* vo, int 
 bool radix_sort_u32(uint32_t* ki, uint32_t* ko, uint32_t* vi, uint32_t* vo, int n, int bits, void* ws,
                     cudaStream_t s, const uint32_t* n_dev) {
     return radix_sort<uint32_t>(ki, ko, vi, vo, n, n_dev, bits, ws, s);
+}
+
+void launch_depth_key24(const uint32_t* bits, const uint32_t* range, int n, uint32_t* keys24, cudaStream_t s) {
+    if (n <= 0) return;
+    k_depth_key24<<<(n + 255) / 256, 256, 0, s>>>(bits, range, n, keys24);
+    OSB_LAUNCHED(1);
 }
 
 void launch_iota(uint32_t* v, int n, cudaStream_t s) {
