@@ -169,7 +169,8 @@ def workload_config(args, world):
             "gaussians": args.gaussians, "width": args.width, "height": args.height,
             "views_per_gpu_per_step": args.views_per_gpu, "sh_degree": 3, "scene": "synthetic uniform shell, seed 1",
             "lambda_ssim": LAMBDA_SSIM,
-            "parallelism": f"dp{world} (views split, Gaussians replicated, NCCL allreduce)",
+            "parallelism": f"dp{world} (views split, Gaussians replicated; N > 1: NCCL reduce-scatter of the "
+                           f"gradients, sharded Adam, all-gather of the parameters)",
             "l2": "inputs larger than L2: params + grads + Adam moments = 4 x 236 MB resident"}
 
 
@@ -265,8 +266,10 @@ def run_ours(args):
     it = [0]
     from paper_2404_03202_b200 import dp
     engine = dp.GpuViewEngine(ctx, poses, gts, W, H, cfg, extent, lambda_ssim=LAMBDA_SSIM)
-    trainer = dp.DataParallelTrainer(engine, rank, world, allreduce=(lambda t: dist.all_reduce(t)) if world > 1
-                                     else None)
+    # N > 1: sharded optimizer — reduce-scatter of the gradient planes, fused Adam on this rank's
+    # 1/N shard, all-gather of the parameters (NCCL, in place on the flat buffers)
+    rs, ag = dp.nccl_shard_collectives(dist) if world > 1 else (None, None)
+    trainer = dp.DataParallelTrainer(engine, rank, world, reduce_scatter=rs, all_gather=ag)
 
     def train_step():
         it[0] += 1
@@ -397,21 +400,24 @@ def run_ours(args):
         host_gt = {vi: torch.empty(3 * plane, dtype=torch.float32, pin_memory=True) for vi in my_views}
         for vi in my_views:
             host_gt[vi].copy_(gts[vi].cpu())
-        for _ in range(max(args.warmup, 3)):  # first use creates the copy stream and the target buffer
-            for vi in my_views:
-                ctx.train_view(poses[vi], W, H, host_gt[vi].data_ptr(), gt_on_device=False, lambda_ssim=LAMBDA_SSIM)
-            if world > 1:
-                dist.all_reduce(grads)
-            ctx.adam_step(cfg, extent, it[0], zero_grad=True)
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
+        def e2e_step():
             it[0] += 1
             for vi in my_views:
                 ctx.train_view(poses[vi], W, H, host_gt[vi].data_ptr(), gt_on_device=False, lambda_ssim=LAMBDA_SSIM)
             if world > 1:
-                dist.all_reduce(grads)
-            ctx.adam_step(cfg, extent, it[0], zero_grad=True)
+                b0, cnt = dp.shard_range(grads.numel(), rank, world)
+                rs(grads, b0, cnt)
+                ctx.adam_step(cfg, extent, it[0], zero_grad=True, begin=b0, count=cnt)
+                ag(engine.param_tensor(), b0, cnt)
+            else:
+                ctx.adam_step(cfg, extent, it[0], zero_grad=True)
+
+        for _ in range(max(args.warmup, 3)):  # first use creates the copy stream and the target buffer
+            e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
         barrier()
         e2e_s = max_over_ranks(time.perf_counter() - t0)
         e2e = {"value": world * V * args.steps / e2e_s, "unit": "views/s",

@@ -167,6 +167,11 @@ OSPLAT_API osplat_status osplat_gpu_reset_screen_stats(osplat_gpu* ctx);
  * (reference defaults). zero_grad != 0 clears the consumed gradients in the same pass. */
 OSPLAT_API osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_config* config, double scene_extent,
                                    long iteration, int zero_grad);
+/* The same step over the flat element range [begin, begin + count) of the planes x stride buffers
+ * (multiples of 4): a data-parallel rank's shard after a reduce-scatter of the gradients, followed
+ * by an all-gather of the parameters (sharded optimizer; every rank advances the step counter). */
+OSPLAT_API osplat_status osplat_gpu_adam_step_range(osplat_gpu* ctx, const osplat_config* config, double scene_extent,
+                                                    long iteration, int zero_grad, size_t begin, size_t count);
 
 /* loss() (trainer.cpp:25-71): (1 - lambda_ssim) L1 + lambda_ssim (1 - SSIM), SSIM 11x11 sigma 1.5
  * zero-padded (metrics.cpp:17-153), bottom rows masked, against a device planar FP32 target:

@@ -1,6 +1,7 @@
 // adam.cu — K5: fused Adam over every parameter plane (proj/src/trainer.cpp:128-178).
 //
-// Adam: one launch over the flat planes x stride FP32 buffers (p, g, m, v), float4 per thread,
+// Adam: one launch over the flat planes x stride FP32 buffers (p, g, m, v) — or the element range
+// [begin, begin + count) of them (the shard of a data-parallel rank) — float4 per thread,
 // per-plane learning rate from the kernel argument table (position / SH DC / SH rest / rotation /
 // log-scale / opacity groups), host-computed bias corrections (one global step, like the
 // reference's AdamState::step). Optionally zeroes the gradient it consumed (saves the separate
@@ -13,10 +14,10 @@ namespace {
 
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __restrict__ g, float4* __restrict__ m,
                                               float4* __restrict__ v, AdamArgs a) {
-    const long n4 = static_cast<long>(a.planes) * a.stride / 4;
+    const long n4 = (a.begin + a.count) / 4;
     const float b1 = 0.9f, b2 = 0.999f;
     const float ob1 = 1.0f - 0.9f, ob2 = 1.0f - 0.999f;
-    for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4;
+    for (long i = a.begin / 4 + blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4;
          i += static_cast<long>(gridDim.x) * blockDim.x) {
         const int plane = static_cast<int>((i * 4) / a.stride);
         const float lr = a.lr_plane[plane];
@@ -46,7 +47,7 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __
 }  // namespace
 
 void launch_adam(float* params, float* grads, float* m, float* v, const AdamArgs& a, cudaStream_t s) {
-    const long n4 = static_cast<long>(a.planes) * a.stride / 4;
+    const long n4 = a.count / 4;
     if (n4 <= 0) return;
     long blocks = (n4 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;

@@ -988,6 +988,12 @@ osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_config* config,
     return wrap([&] { ctx->engine->adam_step(hyper_from(config), extent, iteration, zero_grad != 0); });
 }
 
+osplat_status osplat_gpu_adam_step_range(osplat_gpu* ctx, const osplat_config* config, double extent, long iteration,
+                                         int zero_grad, size_t begin, size_t count) {
+    if (!ctx) return invalid("osplat_gpu_adam_step_range: null context");
+    return wrap([&] { ctx->engine->adam_step(hyper_from(config), extent, iteration, zero_grad != 0, begin, count); });
+}
+
 osplat_status osplat_gpu_loss(osplat_gpu* ctx, const osplat_frame* frame, const float* gt, double lambda_ssim,
                               double mask, const float** d_image, double* loss) {
     if (!ctx || !frame || !gt) return invalid("osplat_gpu_loss: null argument");

@@ -536,7 +536,8 @@ double Engine::loss_value(const Frame* f, double mask_bottom_fraction) {
     return value;
 }
 
-void Engine::adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad) {
+void Engine::adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad, size_t begin,
+                       size_t count) {
     DeviceGuard g(device_);
     adam_step_ += 1;
     const double bias1 = 1.0 - std::pow(0.9, static_cast<double>(adam_step_));
@@ -562,6 +563,12 @@ void Engine::adam_step(const TrainHyper& h, double extent, long iteration, bool 
     a.inv_bias2 = static_cast<float>(1.0 / bias2);
     a.planes = planes_;
     a.stride = static_cast<int>(stride_);
+    const size_t total = static_cast<size_t>(planes_) * stride_;
+    if (begin > total || (begin & 3) != 0) throw std::invalid_argument("adam_step: range start out of bounds");
+    if (count > total - begin) count = total - begin;
+    if ((count & 3) != 0) throw std::invalid_argument("adam_step: range length must be a multiple of 4");
+    a.begin = static_cast<long>(begin);
+    a.count = static_cast<long>(count);
     // Consumed gradients are not cleared in memory: the flag makes the next backward overwrite them.
     a.zero_grad = 0;
     materialize_grads();

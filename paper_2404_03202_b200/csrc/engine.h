@@ -111,7 +111,10 @@ public:
     double loss(Frame* f, const float* gt_planar_dev, double lambda_ssim, double mask_bottom_fraction,
                 bool want_value);
     double loss_value(const Frame* f, double mask_bottom_fraction);
-    void adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad);
+    // Adam over all planes, or over the flat element range [begin, begin + count) (multiples of 4;
+    // a data-parallel rank's shard after a reduce-scatter of the gradients).
+    void adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad, size_t begin = 0,
+                   size_t count = ~size_t(0));
     // Gradients are tracked as "logically zero" after zero_grad / a consuming Adam step, so the next
     // backward stores instead of read-modify-writes; materialize_grads() writes the zeros when the
     // buffer itself is about to be read (download, external views, Adam without a backward).

@@ -85,6 +85,7 @@ struct AdamArgs {
     float inv_bias1, inv_bias2;
     int planes, stride;
     int zero_grad;
+    long begin, count;  // flat element range (multiples of 4)
 };
 void launch_adam(float* params, float* grads, float* m, float* v, const AdamArgs& a, cudaStream_t s);
 // loss() of trainer.cpp:25-71 (loss.cu): (1 - lambda) L1 + lambda (1 - SSIM) over the top

@@ -35,16 +35,36 @@ class ViewEngine(Protocol):
     def adam_step(self, iteration: int) -> None: ...
 
 
-class DataParallelTrainer:
-    """Drives ViewEngine replicas: accumulate local views -> allreduce(sum) -> Adam."""
+def shard_range(size: int, rank: int, world: int) -> tuple[int, int]:
+    """[begin, begin + count) of a flat buffer of `size` elements owned by `rank` (equal shards,
+    multiples of 4 elements so the fused Adam's float4 sweep stays aligned)."""
+    if size % (4 * world):
+        raise ValueError(f"flat size {size} is not a multiple of 4 x world ({world})")
+    count = size // world
+    return rank * count, count
 
-    def __init__(self, engine: ViewEngine, rank: int, world: int, allreduce: Callable | None = None):
-        if world > 1 and allreduce is None:
-            raise ValueError("world > 1 needs an allreduce")
+
+class DataParallelTrainer:
+    """Drives ViewEngine replicas: accumulate local views -> exchange -> Adam.
+
+    Replicated optimizer (default): allreduce(sum) of the gradient buffer, then the identical fused
+    Adam on every rank. Sharded optimizer (``reduce_scatter`` and ``all_gather`` given): each rank
+    receives the summed gradients of its 1/world shard of the flat buffer, runs Adam on that shard
+    only (engine.adam_step_shard) and the parameters are all-gathered — the same bytes on the wire
+    as an allreduce, 1/world of the Adam traffic, and the same elementwise update (bit-identical to
+    the replicated step for the same summed gradients)."""
+
+    def __init__(self, engine: ViewEngine, rank: int, world: int, allreduce: Callable | None = None,
+                 reduce_scatter: Callable | None = None, all_gather: Callable | None = None):
+        if world > 1 and allreduce is None and (reduce_scatter is None or all_gather is None):
+            raise ValueError("world > 1 needs an allreduce or a reduce_scatter + all_gather pair")
         self.engine = engine
         self.rank = rank
         self.world = world
         self.allreduce = allreduce
+        self.reduce_scatter = reduce_scatter
+        self.all_gather = all_gather
+        self.sharded = world > 1 and reduce_scatter is not None and all_gather is not None
 
     def step(self, iteration: int, view_ids: Sequence[int]) -> float:
         loss = 0.0
@@ -52,9 +72,16 @@ class DataParallelTrainer:
             out = self.engine.accumulate_view(v)
             if out is not None:
                 loss += out
-        if self.world > 1:
-            self.allreduce(self.engine.grad_tensor())
-        self.engine.adam_step(iteration)
+        if self.sharded:
+            grads = self.engine.grad_tensor()
+            begin, count = shard_range(grads.numel(), self.rank, self.world)
+            self.reduce_scatter(grads, begin, count)  # grads[begin:begin+count] <- sum over ranks
+            self.engine.adam_step_shard(iteration, begin, count)
+            self.all_gather(self.engine.param_tensor(), begin, count)  # every rank's shard -> all
+        else:
+            if self.world > 1:
+                self.allreduce(self.engine.grad_tensor())
+            self.engine.adam_step(iteration)
         return loss
 
 
@@ -76,6 +103,7 @@ class GpuViewEngine:
         self.lambda_ssim = lambda_ssim
         v = ctx.view()
         self._grads = torch.as_tensor(_CudaArray(v.grads, v.planes * v.stride), device="cuda")
+        self._params = torch.as_tensor(_CudaArray(v.params, v.planes * v.stride), device="cuda")
 
     def accumulate_view(self, view_id: int):
         fr = self.ctx.render(self.poses[view_id], self.W, self.H)
@@ -93,6 +121,12 @@ class GpuViewEngine:
     def adam_step(self, iteration: int):
         self.ctx.adam_step(self.config, self.extent, iteration, zero_grad=True)
 
+    def adam_step_shard(self, iteration: int, begin: int, count: int):
+        self.ctx.adam_step(self.config, self.extent, iteration, zero_grad=True, begin=begin, count=count)
+
+    def param_tensor(self):
+        return self._params
+
 
 class _CudaArray:
     """__cuda_array_interface__ view of a device pointer (zero-copy torch interop)."""
@@ -100,3 +134,16 @@ class _CudaArray:
     def __init__(self, ptr: int, n: int, typestr: str = "<f4"):
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
                                          "strides": None}
+
+
+def nccl_shard_collectives(dist):
+    """reduce_scatter / all_gather callables over torch.distributed (NCCL on the GPU box), in place
+    on the flat buffers: the rank's shard is a view of the full tensor."""
+
+    def reduce_scatter(t, begin, count):
+        dist.reduce_scatter_tensor(t[begin:begin + count], t)
+
+    def all_gather(t, begin, count):
+        dist.all_gather_into_tensor(t, t[begin:begin + count])
+
+    return reduce_scatter, all_gather

@@ -108,6 +108,7 @@ def _load():
         "osplat_gpu_zero_grad": (S, [_vp]),
         "osplat_gpu_reset_screen_stats": (S, [_vp]),
         "osplat_gpu_adam_step": (S, [_vp, _vp, C.c_double, C.c_long, C.c_int]),
+        "osplat_gpu_adam_step_range": (S, [_vp, _vp, C.c_double, C.c_long, C.c_int, C.c_size_t, C.c_size_t]),
         "osplat_gpu_l1_loss": (S, [_vp, _vp, _vp, C.c_double, C.POINTER(_vp), _dp]),
         "osplat_gpu_loss": (S, [_vp, _vp, _vp, C.c_double, C.c_double, C.POINTER(_vp), _dp]),
         "osplat_gpu_train_view": (S, [_vp, _dp, C.c_int, C.c_int, _vp, C.c_int, C.c_double, C.c_double, _dp]),
@@ -364,9 +365,15 @@ class Context:
     def reset_screen_stats(self):
         check(lib.osplat_gpu_reset_screen_stats(self.handle))
 
-    def adam_step(self, config: Config | None, extent: float, iteration: int, zero_grad: bool = False):
-        check(lib.osplat_gpu_adam_step(self.handle, config.handle if config else None, extent, iteration,
-                                       int(zero_grad)))
+    def adam_step(self, config: Config | None, extent: float, iteration: int, zero_grad: bool = False,
+                  begin: int = 0, count: int | None = None):
+        """adam_step (trainer.cpp:143-178); with begin/count only that flat element range (a shard)."""
+        if begin == 0 and count is None:
+            check(lib.osplat_gpu_adam_step(self.handle, config.handle if config else None, extent, iteration,
+                                           int(zero_grad)))
+        else:
+            check(lib.osplat_gpu_adam_step_range(self.handle, config.handle if config else None, extent, iteration,
+                                                 int(zero_grad), begin, count if count is not None else 2**63))
 
     def loss(self, frame: Frame, gt_ptr: int, lambda_ssim: float = 0.2, mask_bottom_fraction: float = 0.0,
              want_value=True):

@@ -45,8 +45,54 @@ class OracleViewEngine:
         self.state = pyoracle.AdamState.zeros(n, bc)
         self.cfg = pyoracle.AdamConfig(iterations=100)
 
+    # --- flat parameters in the gradient layout (the sharded optimizer all-gathers them)
+    def _fields(self):
+        return [("positions", "d_position"), ("sh", "d_sh"), ("rotations", "d_rotation"),
+                ("log_scales", "d_log_scale"), ("opacity_logits", "d_opacity_logit")]
+
+    def param_tensor(self):
+        import torch
+        if getattr(self, "pflat", None) is None:
+            self.pflat = torch.from_numpy(self.params().copy())
+        return self.pflat
+
+    def _load_flat_params(self):
+        if getattr(self, "pflat", None) is None:
+            return
+        arr, o = self.pflat.numpy(), 0
+        for (cf, _), (_, shape) in zip(self._fields(), self.shapes):
+            sz = int(np.prod(shape))
+            setattr(self.cloud, cf, arr[o:o + sz].reshape(shape).copy())
+            o += sz
+
+    def adam_step_shard(self, iteration, begin, count):
+        """Adam on the flat element range only: the full elementwise step on copies, then the shard's
+        parameters / moments written back (other elements belong to other ranks)."""
+        import copy
+        self._load_flat_params()
+        old_cloud, old_state = self.cloud.copy(), copy.deepcopy(self.state)
+        self.adam_step(iteration)
+        new = self.params()
+        flat = self.param_tensor().numpy()
+        flat[begin:begin + count] = new[begin:begin + count]
+        # moments: keep this rank's shard of the new state, the old values elsewhere
+        offs = 0
+        for f, (_, shape) in zip(["m_position", "m_sh", "m_rotation", "m_scale", "m_opacity"], self.shapes):
+            sz = int(np.prod(shape))
+            lo, hi = max(begin, offs), min(begin + count, offs + sz)
+            for pre in ("m", "v"):
+                name = pre + f[1:]
+                a_new = getattr(self.state, name).ravel()
+                a_old = getattr(old_state, name).ravel().copy()
+                if lo < hi:
+                    a_old[lo - offs:hi - offs] = a_new[lo - offs:hi - offs]
+                setattr(self.state, name, a_old.reshape(getattr(old_state, name).shape))
+            offs += sz
+        self.cloud = old_cloud
+
     def accumulate_view(self, v):
         import torch
+        self._load_flat_params()
         f = self.oracle.render(self.cloud, self.poses[v], W, H, keep_handle=True)
         loss, d = self.oracle.loss(f.rgb, self.targets[v], 0.0, 0.0)
         g = self.oracle.backward(f, d, self.cloud, self.poses[v])
@@ -77,7 +123,7 @@ class OracleViewEngine:
                                c.opacity_logits.ravel()])
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, sharded=False):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -87,9 +133,25 @@ def _worker(rank, world, port, out_dir):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     eng = OracleViewEngine()
-    trainer = dp.DataParallelTrainer(eng, rank, world, allreduce=lambda t: dist.all_reduce(t))
+    if sharded:
+        import torch
+
+        def reduce_scatter(t, begin, count):  # gloo has no reduce_scatter: allreduce, keep the shard
+            dist.all_reduce(t)
+
+        def all_gather(t, begin, count):
+            parts = [torch.empty(count, dtype=t.dtype) for _ in range(world)]
+            dist.all_gather(parts, t[begin:begin + count].clone())
+            t.copy_(torch.cat(parts))
+
+        trainer = dp.DataParallelTrainer(eng, rank, world, reduce_scatter=reduce_scatter, all_gather=all_gather)
+        assert trainer.sharded
+    else:
+        trainer = dp.DataParallelTrainer(eng, rank, world, allreduce=lambda t: dist.all_reduce(t))
     for step in range(STEPS):
         trainer.step(step + 1, dp.views_for_rank(step, BATCH, N_VIEWS, rank, world))
+        if sharded:
+            eng._load_flat_params()
         np.save(os.path.join(out_dir, f"rank{rank}_step{step}.npy"), eng.params())
     dist.barrier()
     dist.destroy_process_group()
@@ -103,12 +165,16 @@ def test_view_partition():
     assert got == dp.batch_views(3, 8, 16) == sorted(dp.batch_views(3, 8, 16))
     with pytest.raises(ValueError):
         dp.DataParallelTrainer(object(), 0, 2, None)
+    assert dp.shard_range(2360, 0, 2) == (0, 1180) and dp.shard_range(2360, 1, 2) == (1180, 1180)
+    with pytest.raises(ValueError):
+        dp.shard_range(2362, 0, 2)
 
 
-def test_two_rank_gloo_matches_single_process(tmp_path, oracle_port):
+@pytest.mark.parametrize("sharded", [False, True], ids=["replicated_adam", "sharded_adam"])
+def test_two_rank_gloo_matches_single_process(tmp_path, oracle_port, sharded):
     import torch.multiprocessing as mp
     port = _free_port()
-    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, port, str(tmp_path), sharded), nprocs=2, join=True)
     single = OracleViewEngine()
     trainer = dp.DataParallelTrainer(single, 0, 1)
     for step in range(STEPS):
