@@ -269,3 +269,40 @@ def test_equal_depth_runs_fall_back_to_the_exact_sort(oracle_port):
     nbad, first = compare_tiles(fr, of)
     assert nbad == 0, (nbad, first)
     assert np.max(np.abs(fr.image() - of.rgb)) <= IMAGE_ATOL
+
+
+def test_adam_shards_equal_the_full_step():
+    """osplat_gpu_adam_step_range over the shards of a data-parallel world == the full fused Adam,
+    bit for bit (the sharded optimizer's update is elementwise)."""
+    import torch
+
+    from paper_2404_03202_b200 import dp
+    cloud = scenes.synthetic_cloud(3000, seed=15)
+    rng = np.random.default_rng(2)
+    cfg = native.Config(iterations=100)
+    d = rng.uniform(-1, 1, size=(64, 128, 3)) / (64 * 128)
+    world = 4
+    ctxs = [native.Context(cloud) for _ in range(world + 1)]
+    for c in ctxs:
+        fr = c.render(scenes.identity_pose(), 128, 64)
+        c.backward(fr, d)
+        fr.free()
+    grads = lambda c: torch.as_tensor(dp._CudaArray(c.view().grads, c.view().planes * c.view().stride),
+                                      device="cuda")
+    for c in ctxs[1:]:  # K4a's FP32 atomics make gradients order-dependent: give all the same ones
+        grads(c).copy_(grads(ctxs[0]))
+    torch.cuda.synchronize()
+    ctxs[0].adam_step(cfg, 1.0, 1)
+    flat = lambda c: torch.as_tensor(dp._CudaArray(c.view().params, c.view().planes * c.view().stride),
+                                     device="cuda").cpu().numpy()
+    full = flat(ctxs[0])
+    for r in range(world):
+        c = ctxs[1 + r]
+        b, n = dp.shard_range(full.size, r, world)
+        before = flat(c)
+        c.adam_step(cfg, 1.0, 1, begin=b, count=n)
+        after = flat(c)
+        assert np.array_equal(after[b:b + n], full[b:b + n]), r
+        outside = np.ones(full.size, dtype=bool)
+        outside[b:b + n] = False
+        assert np.array_equal(after[outside], before[outside]), r
