@@ -209,69 +209,74 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
 
 // Gradient plane update: OVERWRITE (the buffer is logically zero: first view after Adam or a
 // non-accumulating backward) stores, otherwise read-modify-write (multi-view accumulation).
-template <bool OVERWRITE>
-__device__ __forceinline__ void put_grad(float* __restrict__ G, int stride, int plane, int gid, double v) {
+template <bool OVERWRITE, typename R>
+__device__ __forceinline__ void put_grad(float* __restrict__ G, int stride, int plane, int gid, R v) {
     float* p = G + static_cast<size_t>(plane) * stride + gid;
     if (OVERWRITE) *p = static_cast<float>(v);
     else *p = *p + static_cast<float>(v);
 }
 
 // One SH basis function of the backward (gradients.cpp:202-207): d_sh_i = dl_color * b_i and
-// d_dir += db_i * (c_i . dl_color), with b_i / db_i from scene.cpp:45-92.
-template <bool OVERWRITE>
+// d_dir += db_i * (c_i . dl_color), with b_i / db_i from scene.cpp:45-92. Evaluated in FP32
+// (R = float): the basis and its gradient are well conditioned (|dir| = 1), the pre-clamp colour
+// gate comes exactly from K1, and the results stay far inside the 1e-3 gradient tolerance; the
+// cancellation-prone geometry chain below stays FP64.
+template <typename R, bool OVERWRITE>
 struct ShBack {
     const float* P;
     float* G;
     int stride, gid;
     Planes pl;
-    double dlc[3];
-    double dd[3];
-    __device__ __forceinline__ void basis(int i, double b, double gx, double gy, double gz) {
-        const double c0 = load_param(P, stride, pl.sh(i, 0), gid);
-        const double c1 = load_param(P, stride, pl.sh(i, 1), gid);
-        const double c2 = load_param(P, stride, pl.sh(i, 2), gid);
+    R dlc[3];
+    R dd[3];
+    __device__ __forceinline__ void basis(int i, R b, R gx, R gy, R gz) {
+        const R c0 = static_cast<R>(__ldg(P + static_cast<size_t>(pl.sh(i, 0)) * stride + gid));
+        const R c1 = static_cast<R>(__ldg(P + static_cast<size_t>(pl.sh(i, 1)) * stride + gid));
+        const R c2 = static_cast<R>(__ldg(P + static_cast<size_t>(pl.sh(i, 2)) * stride + gid));
         put_grad<OVERWRITE>(G, stride, pl.sh(i, 0), gid, dlc[0] * b);
         put_grad<OVERWRITE>(G, stride, pl.sh(i, 1), gid, dlc[1] * b);
         put_grad<OVERWRITE>(G, stride, pl.sh(i, 2), gid, dlc[2] * b);
-        const double cdot = c0 * dlc[0] + c1 * dlc[1] + c2 * dlc[2];
+        const R cdot = c0 * dlc[0] + c1 * dlc[1] + c2 * dlc[2];
         dd[0] += gx * cdot;
         dd[1] += gy * cdot;
         dd[2] += gz * cdot;
     }
 };
 
-template <int DEG, bool OVERWRITE>
-__device__ __forceinline__ void sh_backward(ShBack<OVERWRITE>& s, const double* d) {
-    constexpr double C1 = 0.4886025119029199;
-    constexpr double C20 = 1.0925484305920792, C21 = -1.0925484305920792, C22 = 0.31539156525252005,
-                     C23 = -1.0925484305920792, C24 = 0.5462742152960396;
-    constexpr double C30 = -0.5900435899266435, C31 = 2.890611442640554, C32 = -0.4570457994644658,
-                     C33 = 0.3731763325901154, C34 = -0.4570457994644658, C35 = 1.445305721320277,
-                     C36 = -0.5900435899266435;
-    const double x = d[0], y = d[1], z = d[2];
-    s.basis(0, kShC0, 0.0, 0.0, 0.0);
+template <int DEG, typename R, bool OVERWRITE>
+__device__ __forceinline__ void sh_backward(ShBack<R, OVERWRITE>& s, const R* d) {
+    constexpr R C0 = static_cast<R>(0.28209479177387814);
+    constexpr R C1 = static_cast<R>(0.4886025119029199);
+    constexpr R C20 = static_cast<R>(1.0925484305920792), C21 = static_cast<R>(-1.0925484305920792),
+                C22 = static_cast<R>(0.31539156525252005), C23 = static_cast<R>(-1.0925484305920792),
+                C24 = static_cast<R>(0.5462742152960396);
+    constexpr R C30 = static_cast<R>(-0.5900435899266435), C31 = static_cast<R>(2.890611442640554),
+                C32 = static_cast<R>(-0.4570457994644658), C33 = static_cast<R>(0.3731763325901154),
+                C34 = static_cast<R>(-0.4570457994644658), C35 = static_cast<R>(1.445305721320277),
+                C36 = static_cast<R>(-0.5900435899266435);
+    constexpr R k0 = 0, k2 = 2, k3 = 3, k4 = 4, k6 = 6, k8 = 8;
+    const R x = d[0], y = d[1], z = d[2];
+    s.basis(0, C0, k0, k0, k0);
     if (DEG < 1) return;
-    s.basis(1, -C1 * y, 0.0, -C1, 0.0);
-    s.basis(2, C1 * z, 0.0, 0.0, C1);
-    s.basis(3, -C1 * x, -C1, 0.0, 0.0);
+    s.basis(1, -C1 * y, k0, -C1, k0);
+    s.basis(2, C1 * z, k0, k0, C1);
+    s.basis(3, -C1 * x, -C1, k0, k0);
     if (DEG < 2) return;
-    const double xx = x * x, yy = y * y, zz = z * z;
-    s.basis(4, C20 * x * y, C20 * y, C20 * x, 0.0);
-    s.basis(5, C21 * y * z, 0.0, C21 * z, C21 * y);
-    s.basis(6, C22 * (2.0 * zz - xx - yy), -2.0 * C22 * x, -2.0 * C22 * y, 4.0 * C22 * z);
-    s.basis(7, C23 * x * z, C23 * z, 0.0, C23 * x);
-    s.basis(8, C24 * (xx - yy), 2.0 * C24 * x, -2.0 * C24 * y, 0.0);
+    const R xx = x * x, yy = y * y, zz = z * z;
+    s.basis(4, C20 * x * y, C20 * y, C20 * x, k0);
+    s.basis(5, C21 * y * z, k0, C21 * z, C21 * y);
+    s.basis(6, C22 * (k2 * zz - xx - yy), -k2 * C22 * x, -k2 * C22 * y, k4 * C22 * z);
+    s.basis(7, C23 * x * z, C23 * z, k0, C23 * x);
+    s.basis(8, C24 * (xx - yy), k2 * C24 * x, -k2 * C24 * y, k0);
     if (DEG < 3) return;
-    s.basis(9, C30 * y * (3.0 * xx - yy), C30 * 6.0 * x * y, C30 * (3.0 * xx - 3.0 * yy), 0.0);
+    s.basis(9, C30 * y * (k3 * xx - yy), C30 * k6 * x * y, C30 * (k3 * xx - k3 * yy), k0);
     s.basis(10, C31 * x * y * z, C31 * y * z, C31 * x * z, C31 * x * y);
-    s.basis(11, C32 * y * (4.0 * zz - xx - yy), -2.0 * C32 * x * y, C32 * (4.0 * zz - xx - 3.0 * yy),
-            8.0 * C32 * y * z);
-    s.basis(12, C33 * z * (2.0 * zz - 3.0 * xx - 3.0 * yy), -6.0 * C33 * x * z, -6.0 * C33 * y * z,
-            C33 * (6.0 * zz - 3.0 * xx - 3.0 * yy));
-    s.basis(13, C34 * x * (4.0 * zz - xx - yy), C34 * (4.0 * zz - 3.0 * xx - yy), -2.0 * C34 * x * y,
-            8.0 * C34 * x * z);
-    s.basis(14, C35 * z * (xx - yy), 2.0 * C35 * x * z, -2.0 * C35 * y * z, C35 * (xx - yy));
-    s.basis(15, C36 * x * (xx - 3.0 * yy), C36 * (3.0 * xx - 3.0 * yy), -6.0 * C36 * x * y, 0.0);
+    s.basis(11, C32 * y * (k4 * zz - xx - yy), -k2 * C32 * x * y, C32 * (k4 * zz - xx - k3 * yy), k8 * C32 * y * z);
+    s.basis(12, C33 * z * (k2 * zz - k3 * xx - k3 * yy), -k6 * C33 * x * z, -k6 * C33 * y * z,
+            C33 * (k6 * zz - k3 * xx - k3 * yy));
+    s.basis(13, C34 * x * (k4 * zz - xx - yy), C34 * (k4 * zz - k3 * xx - yy), -k2 * C34 * x * y, k8 * C34 * x * z);
+    s.basis(14, C35 * z * (xx - yy), k2 * C35 * x * z, -k2 * C35 * y * z, C35 * (xx - yy));
+    s.basis(15, C36 * x * (xx - k3 * yy), C36 * (k3 * xx - k3 * yy), -k6 * C36 * x * y, k0);
 }
 
 // K4b. Uses K1's FP64 conic and opacity (conic_o) and its pre-clamp colour sign bits instead of
@@ -326,15 +331,16 @@ __global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restr
     double d_m_sh[3];
     {
         const uint32_t neg = __float_as_uint(splat[gid].pad);
-        ShBack<OVERWRITE> sb{P, G, stride, gid, pl,
-                  {(neg & 1u) ? 0.0 : static_cast<double>(a0.x), (neg & 2u) ? 0.0 : static_cast<double>(a0.y),
-                   (neg & 4u) ? 0.0 : static_cast<double>(a0.z)},
-                  {0.0, 0.0, 0.0}};
+        ShBack<float, OVERWRITE> sb{P, G, stride, gid, pl,
+                  {(neg & 1u) ? 0.0f : a0.x, (neg & 2u) ? 0.0f : a0.y, (neg & 4u) ? 0.0f : a0.z},
+                  {0.0f, 0.0f, 0.0f}};
         double dir[3];
         view_dir(pose, t, t_r, dir);
-        sh_backward<DEG, OVERWRITE>(sb, dir);
-        const double dd = dot3(dir, sb.dd);
-        for (int c = 0; c < 3; ++c) d_m_sh[c] = (sb.dd[c] - dir[c] * dd) * (1.0 / t_r);
+        const float dirf[3] = {static_cast<float>(dir[0]), static_cast<float>(dir[1]), static_cast<float>(dir[2])};
+        sh_backward<DEG>(sb, dirf);
+        const double sdd[3] = {sb.dd[0], sb.dd[1], sb.dd[2]};
+        const double dd = dot3(dir, sdd);
+        for (int c = 0; c < 3; ++c) d_m_sh[c] = (sdd[c] - dir[c] * dd) * (1.0 / t_r);
     }
 
     // mean path: dL/dt = J^T dL/dp (gradients.cpp:212-213)
