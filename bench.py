@@ -179,8 +179,8 @@ def run_reference_arm(args):
     if rank != 0:
         return
     from paper_2404_03202_b200 import scenes
+    oracle, kind, cores = reference_oracle()  # puts oracle/ on sys.path
     import pyoracle
-    oracle, kind, cores = reference_oracle()
     N, W, H = args.gaussians, args.width, args.height
     cloud = scenes.synthetic_cloud(N, seed=1)
     poses = scenes.ring_poses(16, seed=2)
@@ -205,7 +205,8 @@ def run_reference_arm(args):
             "config": workload_config(args, 1),
             "cpu_baseline": {"value": value, "unit": "views/s", "cores": cores, "kind": kind,
                              "sample": f"{steps_run} full train step(s) of the workload on the host "
-                                       f"(reference render + loss + backward + adam_step, steady clock)"},
+                                       f"(reference render + loss + backward + adam_step, steady clock; loss "
+                                       f"target a black image — the loss cost does not depend on its values)"},
             "e2e": {"value": value, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
