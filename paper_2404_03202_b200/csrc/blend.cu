@@ -17,7 +17,11 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                                                            const uint2* __restrict__ ranges, PreprocessOut pp, int W,
                                                            int H, int tiles_x, float bg0, float bg1, float bg2,
                                                            FrameBuffers fb) {
+    // CTA-cooperative walk: the 8 warps stage 256 entries at once (warp w stages sub-chunk w, each
+    // entry once per tile instead of once per warp, with a 16-bit reach mask for all quarters), then
+    // every warp blends the 8 sub-chunks in list order; one barrier pair per 256 entries.
     __shared__ WarpStage stage[kTileWarps];
+    __shared__ uint16_t s_mask[kTileThreads];
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -30,7 +34,6 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
     const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
     const float lxo = lx - 7.5f, lyo = ly - 7.5f;
     const float halfW = 0.5f * W, fW = static_cast<float>(W);
-    WarpStage& ws = stage[warp];
 
     float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
     double T64 = 1.0;
@@ -39,18 +42,30 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
     int stop_at = static_cast<int>(range.y - range.x);  // entries evaluated (work counting)
     bool done = !inside;
 
-    uint32_t gid_next = range.x + lane < range.y ? inst_gid[range.x + lane] : 0u;  // ids one chunk ahead
-    for (uint32_t base = range.x; base < range.y; base += 32) {
-        if (__all_sync(0xffffffffu, done)) break;
-        const uint32_t idx = base + lane;
-        const uint32_t gid = gid_next;
-        gid_next = idx + 32 < range.y ? inst_gid[idx + 32] : 0u;
-        uint32_t reach = 0u;
-        if (idx < range.y) reach = stage_entry(ws, lane, gid, pp.pxy, pp.splat, xc, yc, width, wp.r0, wp.c0);
-        const uint32_t bal0 = __ballot_sync(0xffffffffu, reach & 1u);
-        const uint32_t bal1 = __ballot_sync(0xffffffffu, reach & 2u);
+    const int t = threadIdx.x;
+    uint32_t gid_next = range.x + t < range.y ? inst_gid[range.x + t] : 0u;  // ids one chunk ahead
+    for (uint32_t cbase = range.x; cbase < range.y; cbase += kTileThreads) {
+        if (!__syncthreads_or(!done)) break;  // every pixel of the tile has terminated
+        {
+            const uint32_t idx = cbase + t;
+            const uint32_t gid = gid_next;
+            gid_next = idx + kTileThreads < range.y ? inst_gid[idx + kTileThreads] : 0u;
+            uint32_t m = 0u;
+            if (idx < range.y) {
+                const float4* s4 = reinterpret_cast<const float4*>(pp.splat + gid);
+                m = stage_record16(stage[warp], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc, yc, width);
+            }
+            s_mask[t] = static_cast<uint16_t>(m);
+        }
+        __syncthreads();
+      for (int sub = 0; sub < kTileWarps; ++sub) {
+        const uint32_t base = cbase + 32 * sub;
+        if (base >= range.y || __all_sync(0xffffffffu, done)) break;
+        WarpStage& ws = stage[sub];
+        const uint32_t mk = s_mask[32 * sub + lane];
+        const uint32_t bal0 = __ballot_sync(0xffffffffu, (mk >> (2 * warp)) & 1u);
+        const uint32_t bal1 = __ballot_sync(0xffffffffu, (mk >> (2 * warp + 1)) & 1u);
         uint32_t bal = wp.half ? bal1 : bal0;  // this half-warp's entries; lanes loop independently
-        __syncwarp();
         // A lane whose FP32 transmittance lands inside the T band parks the entry (pend) and leaves
         // the loop; the warp then replays each parked pixel's prefix cooperatively (warp_replay_T:
         // 32 entries evaluated in parallel, product in list order) and the lane resumes.
@@ -150,6 +165,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
             }
         }
         __syncwarp();
+      }
+        __syncthreads();  // the stage is rewritten by the next chunk
     }
     if (inside) {
         const size_t pix = static_cast<size_t>(py) * W + px;

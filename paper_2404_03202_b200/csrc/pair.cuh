@@ -50,6 +50,53 @@ struct WarpStage {
 // Stage entry `gid` into this lane's slot for the tile centred at (xc, yc); returns a 2-bit mask:
 // bit h set when the entry can reach a pixel centre of half-warp h's block (row offsets r0..r0+3,
 // column offsets c0+4h..c0+4h+3).
+// 16-bit reach mask of a staged entry for the 16 4x4 quarters of its tile (quarter q = 2 warp +
+// half: columns 4 (2 (w & 1) + half) .. +3, rows 4 (w >> 1) .. +3), from the same conservative
+// alpha extents as stage_record's two-bit masks: a clear bit is a certain skip for every pixel of
+// that quarter.
+__device__ __forceinline__ uint32_t quarter_mask(const float4 A, float ext_x, float ext_y, bool seam) {
+    const float cx = A.x, cy = A.y;
+    uint32_t rows = 0u, cols = 0u;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const float r0 = 4.0f * r - 7.5f;
+        rows |= (cy - ext_y <= r0 + 3.0f && cy + ext_y >= r0) ? (1u << r) : 0u;
+    }
+    if (seam) {
+        cols = 0xFu;
+    } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const float c0 = 4.0f * c - 7.5f;
+            cols |= (cx - ext_x <= c0 + 3.0f && cx + ext_x >= c0) ? (1u << c) : 0u;
+        }
+    }
+    // quarter q: warp row = q >> 2, column group = q & 3 (= 2 (w & 1) + half)
+    uint32_t m = 0u;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+        if (rows & (1u << r)) m |= cols << (4 * r);
+    return m;
+}
+
+// stage_record for the CTA-cooperative walk: returns the 16-quarter reach mask (quarter_mask).
+__device__ __forceinline__ uint32_t stage_record16(WarpStage& ws, int lane, uint32_t gid, const double2 pp,
+                                                   const float4 s0, const float4 s1, const float4 s2, double xc,
+                                                   double yc, double width) {
+    double w0 = pp.x - xc;
+    const double half = 0.5 * width;
+    if (w0 > half) w0 -= width;
+    else if (w0 < -half) w0 += width;
+    const bool seam = fabs(w0) > half - 8.5;
+    const float cx = static_cast<float>(w0), cy = static_cast<float>(pp.y - yc);
+    const float dl = s2.x;
+    ws.a[lane] = make_float4(cx, cy, s0.x, s0.z);
+    ws.b[lane] = make_float4(s0.y, s1.w - dl, s1.w + dl, seam ? -dl : dl);
+    ws.c[lane] = make_float4(s1.x, s1.y, s1.z, s0.w);
+    ws.gid[lane] = gid;
+    return quarter_mask(make_float4(cx, cy, 0.0f, 0.0f), s2.y, s2.z, seam);
+}
+
 __device__ __forceinline__ uint32_t stage_entry(WarpStage& ws, int lane, uint32_t gid, const double2* __restrict__ pxy,
                                             const Splat32* __restrict__ splat, double xc, double yc, double width,
                                             float r0, float c0) {
