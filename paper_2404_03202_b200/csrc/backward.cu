@@ -69,7 +69,11 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
                                                                      float bg2, FrameBuffers fb,
                                                                      const float* __restrict__ d_image,
                                                                      float4* __restrict__ acc) {
+    // CTA-cooperative walk (as K3): 256 entries staged at once with 16-quarter reach masks, every
+    // warp then walks the 8 sub-chunks back to front.
     __shared__ WarpStage stage[kTileWarps];
+    __shared__ uint16_t s_mask[kTileThreads];
+    __shared__ int s_last[kTileWarps];
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -82,8 +86,6 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
     const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
     const float lxo = lx - 7.5f, lyo = ly - 7.5f;
     const float halfW = 0.5f * W, fW = static_cast<float>(W);
-    WarpStage& ws = stage[warp];
-
     const size_t pix = static_cast<size_t>(py) * W + px;
     const size_t plane = static_cast<size_t>(W) * H;
     const int last = inside ? fb.last[pix] : 0;
@@ -103,21 +105,37 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
     // Each 16-lane half owns a 4x4 pixel quarter and walks the entries that can reach it (the same
     // half-warp culling as K3), back to front; the halves reduce their (different) entries at once.
     const uint32_t halfmask = wp.half ? 0xFFFF0000u : 0x0000FFFFu;
-    for (int hi = max_last; hi > 0; hi -= 32) {
-        const int lo = hi > 32 ? hi - 32 : 0;
-        const int cnt = hi - lo;
-        uint32_t reach = 0u;
-        if (lane < cnt)
-            reach = stage_entry(ws, lane, inst_gid[range.x + lo + lane], pp.pxy, pp.splat, xc, yc, width, wp.r0, wp.c0);
-        const uint32_t bal0 = __ballot_sync(0xffffffffu, reach & 1u);
-        const uint32_t bal1 = __ballot_sync(0xffffffffu, reach & 2u);
+    if (lane == 0) s_last[warp] = max_last;
+    __syncthreads();
+    int cta_last = 0;
+#pragma unroll
+    for (int w = 0; w < kTileWarps; ++w) cta_last = max(cta_last, s_last[w]);
+    const int t = threadIdx.x;
+    for (int hi = cta_last; hi > 0; hi -= kTileThreads) {
+        const int lo = hi > kTileThreads ? hi - kTileThreads : 0;
+        {
+            uint32_t m = 0u;
+            if (lo + t < hi) {
+                const uint32_t gid = inst_gid[range.x + lo + t];
+                const float4* s4 = reinterpret_cast<const float4*>(pp.splat + gid);
+                m = stage_record16(stage[warp], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc, yc, width);
+            }
+            s_mask[t] = static_cast<uint16_t>(m);
+        }
+        __syncthreads();
+      for (int sub = kTileWarps - 1; sub >= 0; --sub) {
+        const int sbase = lo + 32 * sub;
+        if (sbase >= hi || sbase >= max_last) continue;  // no pixel of this warp reaches these entries
+        WarpStage& ws = stage[sub];
+        const uint32_t mk = s_mask[32 * sub + lane];
+        const uint32_t bal0 = __ballot_sync(0xffffffffu, (mk >> (2 * warp)) & 1u);
+        const uint32_t bal1 = __ballot_sync(0xffffffffu, (mk >> (2 * warp + 1)) & 1u);
         uint32_t bal = wp.half ? bal1 : bal0;
-        __syncwarp();
         while (__any_sync(0xffffffffu, bal != 0u)) {  // back to front; warp-uniform (the reduction needs all lanes)
             const bool live = bal != 0u;
             const int j = live ? 31 - __clz(bal) : 0;
             bal &= ~(1u << j);
-            const int k = lo + j;
+            const int k = sbase + j;
             float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f, v5 = 0.f, v6 = 0.f, v7 = 0.f, v8 = 0.f;
             bool has = false;
             if (live && k < last) {
@@ -204,6 +222,8 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
             }
         }
         __syncwarp();
+      }
+        __syncthreads();  // the stage is rewritten by the next chunk
     }
 }
 
