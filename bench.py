@@ -416,14 +416,16 @@ def run_ours(args):
         for _ in range(max(args.warmup, 3)):  # first use creates the copy stream and the target buffer
             e2e_step()
         barrier()
+        e2e_steps = max(3 * args.steps, 30)  # wall clock: enough steps to average out host jitter
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(e2e_steps):
             e2e_step()
         barrier()
         e2e_s = max_over_ranks(time.perf_counter() - t0)
-        e2e = {"value": world * V * args.steps / e2e_s, "unit": "views/s",
+        e2e = {"value": world * V * e2e_steps / e2e_s, "unit": "views/s", "steps": e2e_steps,
                "h2d_bytes_per_step": V * 3 * plane * 4, "d2h_bytes_per_step": V * 8,
-               "api": "osplat_gpu_train_view (pinned host target in, loss out) + osplat_gpu_adam_step"}
+               "api": "osplat_gpu_train_view (pinned host target in, loss out) + osplat_gpu_adam_step "
+                      "(N > 1: NCCL reduce-scatter + osplat_gpu_adam_step_range + all-gather)"}
         if rank == 0:
             hc = native.HostCloud.from_cloud(cloud)
             native.osplat_render(hc, poses[0], W, H)  # upload + warm

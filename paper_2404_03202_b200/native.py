@@ -128,7 +128,10 @@ def _load():
                                  PROGRESS_FN, C.c_void_p]),
         "osplat_frame_work": (S, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     }
+    ab_build = "OSPLAT_LIB" in os.environ  # A/B runs may load older builds without newer entry points
     for name, (res, args) in sig.items():
+        if ab_build and not hasattr(lib, name):
+            continue
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
