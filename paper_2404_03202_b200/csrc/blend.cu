@@ -1,11 +1,12 @@
 // blend.cu — K3: per-tile front-to-back alpha blending (proj/src/rasterizer.cpp:100-157).
 //
-// One 256-thread CTA per 16x16 tile, one pixel per thread, warps independent (pair.cuh): each
-// warp walks the tile list 32 entries at a time, stages them lane-parallel, keeps the ones that can
-// reach its half-warp's 4x4 pixel block and blends them in list order; it leaves the list as soon as its 32 pixels have
-// terminated. FP32 fast path + FP64 guard (pair.cuh): power/alpha decisions near a threshold and T
-// near the 1e-4 stop are decided in FP64 exactly like the reference; a T decision inside the band
-// replays the pixel's prefix in FP64 and the pixel continues in FP64 ("exact mode").
+// One 256-thread CTA per 16x16 tile, one pixel per thread. The CTA stages the tile list 256
+// entries at a time (each entry once, with a 16-quarter reach mask, pair.cuh), then each warp blends
+// the staged entries in list order, each half-warp only those that can reach its 4x4 quarter; a
+// warp stops as soon as its 32 pixels have terminated, the CTA when all have. FP32 fast path + FP64
+// guard (pair.cuh): power/alpha decisions near a threshold and T near the 1e-4 stop are decided in
+// FP64 exactly like the reference; a T decision inside the band replays the pixel's prefix in FP64
+// (warp-cooperatively) and the pixel continues in FP64 ("exact mode").
 #include "kernels.h"
 #include "pair.cuh"
 
