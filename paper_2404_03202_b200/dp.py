@@ -55,7 +55,8 @@ class DataParallelTrainer:
     the replicated step for the same summed gradients)."""
 
     def __init__(self, engine: ViewEngine, rank: int, world: int, allreduce: Callable | None = None,
-                 reduce_scatter: Callable | None = None, all_gather: Callable | None = None):
+                 reduce_scatter: Callable | None = None, all_gather: Callable | None = None,
+                 force_shard: bool = False):
         if world > 1 and allreduce is None and (reduce_scatter is None or all_gather is None):
             raise ValueError("world > 1 needs an allreduce or a reduce_scatter + all_gather pair")
         self.engine = engine
@@ -64,7 +65,8 @@ class DataParallelTrainer:
         self.allreduce = allreduce
         self.reduce_scatter = reduce_scatter
         self.all_gather = all_gather
-        self.sharded = world > 1 and reduce_scatter is not None and all_gather is not None
+        # force_shard: take the sharded path even at world 1 (tests of the collective plumbing)
+        self.sharded = (world > 1 or force_shard) and reduce_scatter is not None and all_gather is not None
 
     def step(self, iteration: int, view_ids: Sequence[int]) -> float:
         loss = 0.0

@@ -1,0 +1,68 @@
+"""GPU: the sharded-optimizer step through real NCCL collectives (world size 1 — the box has one
+GPU — with the sharded path forced): in-place reduce_scatter_tensor / all_gather_into_tensor on
+views of the flat planes, issued on the context's stream, give the same parameters as the
+replicated step."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_2404_03202_b200 import dp, native, scenes
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_sharded_step_over_nccl_matches_replicated():
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        stream = torch.cuda.Stream()
+        torch.cuda.set_stream(stream)
+        W, H = 256, 128
+        cloud = scenes.synthetic_cloud(5000, seed=21)
+        target = scenes.synthetic_cloud(5000, seed=22)
+        poses = scenes.ring_poses(4, seed=2)
+        tctx = native.Context(target, stream=stream.cuda_stream)
+        gts = {}
+        for v in range(4):
+            fr = tctx.render(poses[v], W, H)
+            t = torch.empty(3 * W * H, dtype=torch.float32, device="cuda")
+            t.copy_(torch.as_tensor(dp._CudaArray(fr.device().rgb, 3 * W * H), device="cuda"))
+            gts[v] = t
+            fr.free()
+        cfg = native.Config(iterations=100)
+        out = []
+        for sharded in (False, True):
+            ctx = native.Context(cloud, stream=stream.cuda_stream)
+            eng = dp.GpuViewEngine(ctx, poses, gts, W, H, cfg)
+            if sharded:
+                rs, ag = dp.nccl_shard_collectives(dist)
+                tr = dp.DataParallelTrainer(eng, 0, 1, reduce_scatter=rs, all_gather=ag, force_shard=True)
+                assert tr.sharded
+            else:
+                tr = dp.DataParallelTrainer(eng, 0, 1)
+            for it in range(1, 4):
+                tr.step(it, [0, 1, 2, 3])  # 4 views accumulated per step
+            torch.cuda.synchronize()
+            out.append(ctx.download())
+        a, b = out
+        for f in ("positions", "sh", "rotations", "log_scales", "opacity_logits"):
+            d = np.abs(getattr(a, f) - getattr(b, f))
+            # same math; K4a's FP32 atomics reorder sums run to run, which can flip the sign of
+            # noise-level gradients (Adam steps them by +-lr)
+            assert np.mean(d > 1e-6) < 2e-3, (f, np.mean(d > 1e-6))
+            assert np.max(d) <= 3 * 2 * 5e-2, f
+    finally:
+        dist.destroy_process_group()
