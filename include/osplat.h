@@ -124,6 +124,33 @@ OSPLAT_API osplat_status osplat_frame_projections(const osplat_frame* frame, uin
 OSPLAT_API osplat_status osplat_frame_tiles(const osplat_frame* frame, int* tiles_x, int* tiles_y, size_t* instances,
                                  uint32_t* ranges, uint32_t* gaussian_ids);
 
+/* Full SplatProjection records (rasterizer.hpp:31-41) of a frame: the visible Gaussians in
+ * ascending id (render()'s compaction, rasterizer.cpp:165-168), or for a frame of host projections
+ * (osplat_gpu_render_projected) the records as given. Call with NULL arrays to get *count. Arrays
+ * are per record: gaussian_id, p (2), cov (3), conic (3), radius, depth, color (3), alpha_base,
+ * t (3; zeros for host projections). Colour is the FP32 value the blend uses. */
+OSPLAT_API osplat_status osplat_frame_splats(const osplat_frame* frame, size_t* count, int32_t* gaussian_id,
+                                             double* p, double* cov, double* conic, double* radius, double* depth,
+                                             double* color, double* alpha_base, double* t);
+
+/* Replace the context's cloud (GaussianCloud assignment; Adam state and statistics reset). */
+OSPLAT_API osplat_status osplat_gpu_upload(osplat_gpu* ctx, const osplat_cloud* cloud);
+
+/* bin_to_tiles + blend_forward (rasterizer.cpp:57-157) over `count` host SplatProjection records
+ * (same per-record arrays as osplat_frame_splats; gaussian_id may be NULL = index; cov must be
+ * conic^-1, as project_gaussian produces it). tile_offsets == NULL: the device bins and sorts the
+ * records by (depth, gaussian_id) like bin_to_tiles (read the lists back with osplat_frame_tiles;
+ * its ids are then record indices). Otherwise the caller's TileGrid is blended as given:
+ * tile_offsets has tiles+1 entries (tiles = ceil(W/16) ceil(H/16)), tile_entries the concatenated
+ * record indices. The frame has no Gaussian parameters behind it: osplat_gpu_backward on it fails
+ * with a validation status (StateMismatch). Depth must be finite and >= 0. */
+OSPLAT_API osplat_status osplat_gpu_render_projected(osplat_gpu* ctx, size_t count, const int32_t* gaussian_id,
+                                                     const double* p, const double* cov, const double* conic,
+                                                     const double* radius, const double* depth, const double* color,
+                                                     const double* alpha_base, int width, int height,
+                                                     const double background[3], const uint32_t* tile_offsets,
+                                                     const int32_t* tile_entries, osplat_frame** out);
+
 /* Device views for zero-copy interop (e.g. wrapping as torch tensors for NCCL). */
 typedef struct osplat_frame_view {
     float* rgb;           /* 3 planes of H*W (R, G, B) */

@@ -63,9 +63,25 @@ inline void report(bool ok, const char* expr, const char* file, int line, bool f
     if (fatal) throw RequireFailed{};
 }
 
-inline int run_all() {
+// -tce=<names> skips test cases (comma-separated exact names), as doctest's --test-case-exclude.
+inline bool excluded(const char* name, int argc, char** argv) {
+    for (int i = 1; i < argc; ++i) {
+        std::string a = argv[i];
+        if (a.rfind("-tce=", 0) != 0) continue;
+        a = a.substr(5) + ",";
+        for (size_t at = 0, comma; (comma = a.find(',', at)) != std::string::npos; at = comma + 1)
+            if (a.compare(at, comma - at, name) == 0) return true;
+    }
+    return false;
+}
+
+inline int run_all(int argc = 0, char** argv = nullptr) {
     int cases_failed = 0, cases = 0;
     for (const Case& c : registry()) {
+        if (excluded(c.name, argc, argv)) {
+            std::printf("[SKIP] %s\n", c.name);
+            continue;
+        }
         ++cases;
         int before = failures();
         try {
@@ -111,5 +127,5 @@ inline int run_all() {
     } while (0)
 
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
-int main() { return ::doctest::detail::run_all(); }
+int main(int argc, char** argv) { return ::doctest::detail::run_all(argc, argv); }
 #endif

@@ -484,6 +484,51 @@ oracle_frame* oracle_reference_render(const oracle_cloud* c, const double pose[1
     return f;
 }
 
+oracle_frame* oracle_blend_projections(int n, const int* gid, const double* p, const double* cov,
+                                       const double* conic, const double* radius, const double* depth,
+                                       const double* color, const double* alpha, int W, int H, const double bg[3],
+                                       const long* offsets, const int* items) {
+    if (n < 0 || W < 1 || H < 1) return NULL;
+    oracle_frame* f = (oracle_frame*)calloc(1, sizeof(oracle_frame));
+    f->width = W; f->height = H;
+    for (int k = 0; k < 3; ++k) f->background[k] = bg ? bg[k] : 0.0;
+    for (int k = 0; k < 12; ++k) f->pose[k] = (k == 0 || k == 4 || k == 8) ? 1.0 : 0.0;
+    size_t px = (size_t)W * H;
+    f->rgb = (double*)calloc(px * 3, sizeof(double));
+    f->T = (double*)malloc(px * sizeof(double));
+    f->contrib = (int*)calloc(px, sizeof(int));
+    f->last = (int*)calloc(px, sizeof(int));
+    for (size_t i = 0; i < px; ++i) f->T[i] = 1.0;
+    f->nproj = n;
+    f->projections = (proj*)calloc((size_t)n + 1, sizeof(proj));
+    for (int i = 0; i < n; ++i) {
+        proj* pr = &f->projections[i];
+        pr->gaussian_id = gid ? gid[i] : i;
+        for (int k = 0; k < 2; ++k) pr->p[k] = p[2 * i + k];
+        for (int k = 0; k < 3; ++k) {
+            pr->cov[k] = cov[3 * i + k];
+            pr->conic[k] = conic[3 * i + k];
+            pr->color[k] = color[3 * i + k];
+        }
+        pr->radius = radius[i];
+        pr->depth = depth[i];
+        pr->alpha_base = alpha[i];
+    }
+    if (!offsets) {
+        bin_tiles(f);
+    } else {
+        f->tiles_x = (W + K_TILE - 1) / K_TILE;
+        f->tiles_y = (H + K_TILE - 1) / K_TILE;
+        const int tiles = f->tiles_x * f->tiles_y;
+        f->offsets = (long*)malloc(((size_t)tiles + 1) * sizeof(long));
+        memcpy(f->offsets, offsets, ((size_t)tiles + 1) * sizeof(long));
+        f->items = (int*)malloc((size_t)(offsets[tiles] > 0 ? offsets[tiles] : 1) * sizeof(int));
+        if (offsets[tiles] > 0) memcpy(f->items, items, (size_t)offsets[tiles] * sizeof(int));
+    }
+    blend(f);
+    return f;
+}
+
 void oracle_frame_free(oracle_frame* f) {
     if (!f) return;
     free(f->projections); free(f->offsets); free(f->items);

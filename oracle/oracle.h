@@ -70,6 +70,13 @@ oracle_frame* oracle_render(const oracle_cloud* cloud, const double pose[12], in
 oracle_frame* oracle_reference_render(const oracle_cloud* cloud, const double pose[12], int width,
                                       int height, const double background[3]);
 void oracle_frame_free(oracle_frame* frame);
+/* bin_to_tiles + blend_forward over n host SplatProjection records (rasterizer.cpp:57-157), arrays
+ * as oracle_frame_projections (t unused). offsets == NULL: bin_to_tiles builds the grid; otherwise
+ * offsets[tiles+1] / items[M] is the TileGrid to blend. */
+oracle_frame* oracle_blend_projections(int n, const int* gaussian_id, const double* p, const double* cov,
+                                       const double* conic, const double* radius, const double* depth,
+                                       const double* color, const double* alpha_base, int width, int height,
+                                       const double background[3], const long* offsets, const int* items);
 
 int oracle_frame_num_projections(const oracle_frame* frame);
 /* SplatProjection fields (proj/include/omnisplat/rasterizer.hpp:31-41); any pointer may be NULL. */

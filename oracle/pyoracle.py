@@ -171,6 +171,8 @@ class Oracle:
         lib.oracle_reference_render.restype = C.c_void_p
         lib.oracle_reference_render.argtypes = [C.POINTER(_Cloud), _dp, C.c_int, C.c_int, _dp]
         lib.oracle_frame_free.argtypes = [C.c_void_p]
+        lib.oracle_blend_projections.restype = C.c_void_p
+        lib.oracle_blend_projections.argtypes = [C.c_int, _ip] + [_dp] * 7 + [C.c_int, C.c_int, _dp, _lp, _ip]
         lib.oracle_frame_num_projections.restype = C.c_int
         lib.oracle_frame_num_projections.argtypes = [C.c_void_p]
         lib.oracle_frame_projections.argtypes = [C.c_void_p, _ip] + [_dp] * 8
@@ -232,6 +234,29 @@ class Oracle:
         finally:
             if not keep_handle:
                 self.lib.oracle_frame_free(h)
+
+    def blend_projections(self, splats: dict, width, height, background=(0.0, 0.0, 0.0), grid=None) -> Frame:
+        """bin_to_tiles + blend_forward over host SplatProjection records (rasterizer.cpp:57-157).
+        splats: dict of per-record arrays (gaussian_id, p, cov, conic, radius, depth, color, alpha_base);
+        grid: None, or (offsets [tiles+1], items [M]) = the TileGrid to blend."""
+        n = len(splats["depth"])
+        gid = np.ascontiguousarray(splats.get("gaussian_id", np.arange(n)), dtype=np.int32)
+        arrs = [np.ascontiguousarray(splats[k], dtype=np.float64)
+                for k in ("p", "cov", "conic", "radius", "depth", "color", "alpha_base")]
+        bg = np.ascontiguousarray(background, dtype=np.float64)
+        offs = items = None
+        if grid is not None:
+            offs = np.ascontiguousarray(grid[0], dtype=np.int64)
+            items = np.ascontiguousarray(grid[1] if len(grid[1]) else np.zeros(1), dtype=np.int32)
+        h = self.lib.oracle_blend_projections(n, _ptr(gid, _ip), *[_ptr(a) for a in arrs], width, height, _ptr(bg),
+                                              None if offs is None else _ptr(offs, _lp),
+                                              None if items is None else _ptr(items, _ip))
+        if not h:
+            raise RuntimeError("oracle blend_projections failed")
+        try:
+            return self._frame(h, width, height, False)
+        finally:
+            self.lib.oracle_frame_free(h)
 
     def _frame(self, h, W, H, keep_handle) -> Frame:
         lib = self.lib

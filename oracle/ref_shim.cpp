@@ -93,6 +93,44 @@ oracle_frame* oracle_render(const oracle_cloud* c, const double pose[12], int w,
     }
 }
 
+oracle_frame* oracle_blend_projections(int n, const int* gid, const double* p, const double* cov,
+                                       const double* conic, const double* radius, const double* depth,
+                                       const double* color, const double* alpha, int w, int h, const double bg[3],
+                                       const long* offsets, const int* items) {
+    try {
+        std::vector<SplatProjection> prs(static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i) {
+            SplatProjection& s = prs[i];
+            s.gaussian_id = gid ? gid[i] : i;
+            s.p = {p[2 * i], p[2 * i + 1]};
+            s.cov = {cov[3 * i], cov[3 * i + 1], cov[3 * i + 2]};
+            s.conic = {conic[3 * i], conic[3 * i + 1], conic[3 * i + 2]};
+            s.radius = radius[i];
+            s.depth = depth[i];
+            s.color = {color[3 * i], color[3 * i + 1], color[3 * i + 2]};
+            s.alpha_base = alpha[i];
+        }
+        EquirectCamera cam{w, h};
+        RenderSettings st;
+        if (bg) st.background = {bg[0], bg[1], bg[2]};
+        TileGrid grid;
+        if (offsets) {
+            grid.tile_size = 16;
+            grid.tiles_x = (w + 15) / 16;
+            grid.tiles_y = (h + 15) / 16;
+            grid.tiles.resize(static_cast<size_t>(grid.tile_count()));
+            for (int t = 0; t < grid.tile_count(); ++t) grid.tiles[t].assign(items + offsets[t], items + offsets[t + 1]);
+        } else {
+            grid = bin_to_tiles(prs, cam, 16);
+        }
+        auto* f = new oracle_frame;
+        f->out = blend_forward(std::move(grid), std::move(prs), cam, st);
+        return f;
+    } catch (...) {
+        return nullptr;
+    }
+}
+
 oracle_frame* oracle_reference_render(const oracle_cloud* c, const double pose[12], int w, int h,
                                       const double bg[3]) {
     try {

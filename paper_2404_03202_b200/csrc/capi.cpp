@@ -50,6 +50,8 @@ struct osplat_gpu {
 struct osplat_frame {
     std::shared_ptr<Engine> engine;
     osb::Frame* frame = nullptr;
+    // frames of host projections: device slot -> projection index, and the records' gaussian ids
+    std::vector<int32_t> slot_index, given_ids;
 };
 
 namespace {
@@ -693,6 +695,162 @@ osplat_status osplat_frame_tiles(const osplat_frame* frame, int* tiles_x, int* t
             OSB_CUDA_CHECK(cudaMemcpyAsync(gaussian_ids, f.inst_gid(), static_cast<size_t>(f.M) * 4,
                                            cudaMemcpyDeviceToHost, s));
         OSB_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (gaussian_ids && !frame->slot_index.empty())  // projection indices, like TileGrid
+            for (size_t i = 0; i < f.M; ++i) gaussian_ids[i] = static_cast<uint32_t>(frame->slot_index[gaussian_ids[i]]);
+    });
+}
+
+osplat_status osplat_gpu_upload(osplat_gpu* ctx, const osplat_cloud* cloud) {
+    if (!ctx || !cloud) return invalid("osplat_gpu_upload: null argument");
+    return wrap([&] { ctx->engine->upload(cloud->cloud); });
+}
+
+osplat_status osplat_gpu_render_projected(osplat_gpu* ctx, size_t count, const int32_t* gaussian_id, const double* p,
+                                          const double* cov, const double* conic, const double* radius,
+                                          const double* depth, const double* color, const double* alpha_base,
+                                          int width, int height, const double background[3],
+                                          const uint32_t* tile_offsets, const int32_t* tile_entries,
+                                          osplat_frame** out) {
+    if (!ctx || !out) return invalid("osplat_gpu_render_projected: null argument");
+    if (count && (!p || !cov || !conic || !radius || !depth || !color || !alpha_base))
+        return invalid("osplat_gpu_render_projected: null projection array");
+    return wrap([&] {
+        check_dims(width, height);
+        if (count > static_cast<size_t>(INT32_MAX / osb::kSplatPlanes))
+            throw ApiError(Code::InvalidArgument, "too many projections");
+        for (size_t i = 0; i < count; ++i) {
+            if (!std::isfinite(depth[i]) || depth[i] < 0.0)
+                throw ApiError(Code::InvalidArgument, "projection depth must be finite and >= 0");
+            if (!std::isfinite(p[2 * i]) || !std::isfinite(p[2 * i + 1]) || !std::isfinite(radius[i]) ||
+                radius[i] < 0.0 || radius[i] > 1e9)
+                throw ApiError(Code::InvalidArgument, "projection centre / radius out of range");
+        }
+        // device slots in (gaussian_id, index) order: K2's (depth, slot) order is then the
+        // reference's (depth, gaussian_id) comparator (rasterizer.cpp:88-93)
+        std::vector<int32_t> order(count);
+        for (size_t i = 0; i < count; ++i) order[i] = static_cast<int32_t>(i);
+        if (gaussian_id)
+            std::stable_sort(order.begin(), order.end(),
+                             [&](int32_t a, int32_t b) { return gaussian_id[a] < gaussian_id[b]; });
+        std::vector<double> planes(count * osb::kSplatPlanes);
+        auto put = [&](int plane, size_t slot, double v) { planes[plane * count + slot] = v; };
+        for (size_t s = 0; s < count; ++s) {
+            const size_t i = static_cast<size_t>(order[s]);
+            put(0, s, p[2 * i]);
+            put(1, s, p[2 * i + 1]);
+            for (int k = 0; k < 3; ++k) {
+                put(2 + k, s, cov[3 * i + k]);
+                put(5 + k, s, conic[3 * i + k]);
+                put(10 + k, s, color[3 * i + k]);
+            }
+            put(8, s, radius[i]);
+            put(9, s, depth[i]);
+            put(13, s, alpha_base[i]);
+        }
+        std::vector<uint2> ranges;
+        std::vector<uint32_t> slots;
+        if (tile_offsets) {
+            const size_t tiles = static_cast<size_t>((width + 15) / 16) * ((height + 15) / 16);
+            if (tile_offsets[0] != 0) throw ApiError(Code::InvalidArgument, "tile_offsets[0] must be 0");
+            std::vector<uint32_t> slot_of(count);
+            for (size_t s = 0; s < count; ++s) slot_of[order[s]] = static_cast<uint32_t>(s);
+            ranges.resize(tiles);
+            for (size_t t = 0; t < tiles; ++t) {
+                if (tile_offsets[t + 1] < tile_offsets[t])
+                    throw ApiError(Code::InvalidArgument, "tile_offsets must be non-decreasing");
+                ranges[t] = make_uint2(tile_offsets[t], tile_offsets[t + 1]);
+            }
+            const size_t M = tile_offsets[tiles];
+            if (M && !tile_entries) throw ApiError(Code::InvalidArgument, "null tile_entries");
+            slots.resize(M);
+            for (size_t e = 0; e < M; ++e) {
+                if (tile_entries[e] < 0 || static_cast<size_t>(tile_entries[e]) >= count)
+                    throw ApiError(Code::InvalidArgument, "tile entry out of range");
+                slots[e] = slot_of[tile_entries[e]];
+            }
+        }
+        const double zero[3] = {0, 0, 0};
+        auto fr = std::make_unique<osplat_frame>();
+        fr->engine = ctx->engine;
+        fr->slot_index = order;
+        if (fr->slot_index.empty()) fr->slot_index.push_back(0);  // marks a projection frame
+        fr->given_ids.resize(count);
+        for (size_t i = 0; i < count; ++i) fr->given_ids[i] = gaussian_id ? gaussian_id[i] : static_cast<int32_t>(i);
+        fr->frame = ctx->engine->render_projected(planes.data(), count, width, height, background ? background : zero,
+                                                  tile_offsets ? &ranges : nullptr, tile_offsets ? &slots : nullptr);
+        *out = fr.release();
+    });
+}
+
+osplat_status osplat_frame_splats(const osplat_frame* frame, size_t* count, int32_t* gaussian_id, double* p,
+                                  double* cov, double* conic, double* radius, double* depth, double* color,
+                                  double* alpha_base, double* t) {
+    if (!frame || !count) return invalid("osplat_frame_splats: null argument");
+    return wrap([&] {
+        Engine& e = *frame->engine;
+        e.validate(frame->frame);
+        const osb::Frame& f = *frame->frame;
+        osb::DeviceGuard g(e.device());
+        cudaStream_t s = e.stream();
+        const size_t n = static_cast<size_t>(f.n);
+        if (f.projected) {  // the imported records, in projection order
+            *count = n;
+            std::vector<double> planes(n * osb::kSplatPlanes);
+            if (n)
+                OSB_CUDA_CHECK(cudaMemcpyAsync(planes.data(), f.import.as<double>(), planes.size() * 8,
+                                               cudaMemcpyDeviceToHost, s));
+            OSB_CUDA_CHECK(cudaStreamSynchronize(s));
+            for (size_t slot = 0; slot < n; ++slot) {
+                const size_t i = static_cast<size_t>(frame->slot_index[slot]);
+                auto at = [&](int plane) { return planes[plane * n + slot]; };
+                if (gaussian_id) gaussian_id[i] = frame->given_ids[i];
+                for (int k = 0; k < 2; ++k) if (p) p[2 * i + k] = at(k);
+                for (int k = 0; k < 3; ++k) {
+                    if (cov) cov[3 * i + k] = at(2 + k);
+                    if (conic) conic[3 * i + k] = at(5 + k);
+                    if (color) color[3 * i + k] = at(10 + k);
+                    if (t) t[3 * i + k] = 0.0;
+                }
+                if (radius) radius[i] = at(8);
+                if (depth) depth[i] = at(9);
+                if (alpha_base) alpha_base[i] = at(13);
+            }
+            return;
+        }
+        std::vector<uint64_t> key(n);
+        std::vector<double2> pxy(n);
+        std::vector<double4> co(n);
+        std::vector<osb::Splat32> sp(n);
+        std::vector<float> rad(n);
+        if (n) {
+            OSB_CUDA_CHECK(cudaMemcpyAsync(key.data(), f.depth_key.as<void>(), n * 8, cudaMemcpyDeviceToHost, s));
+            OSB_CUDA_CHECK(cudaMemcpyAsync(pxy.data(), f.pxy.as<void>(), n * 16, cudaMemcpyDeviceToHost, s));
+            OSB_CUDA_CHECK(cudaMemcpyAsync(co.data(), f.conic_o.as<void>(), n * 32, cudaMemcpyDeviceToHost, s));
+            OSB_CUDA_CHECK(cudaMemcpyAsync(sp.data(), f.splat.as<void>(), n * sizeof(osb::Splat32),
+                                           cudaMemcpyDeviceToHost, s));
+            OSB_CUDA_CHECK(cudaMemcpyAsync(rad.data(), f.radius.as<void>(), n * 4, cudaMemcpyDeviceToHost, s));
+        }
+        OSB_CUDA_CHECK(cudaStreamSynchronize(s));
+        std::vector<double> detail;
+        const bool need_detail = cov || t;
+        if (need_detail) e.projection_detail(frame->frame, detail);
+        size_t v = 0;  // render()'s compaction: visible Gaussians in ascending id (rasterizer.cpp:165-168)
+        for (size_t i = 0; i < n; ++i) {
+            if (key[i] == ~0ull) continue;
+            if (gaussian_id) gaussian_id[v] = static_cast<int32_t>(i);
+            if (p) { p[2 * v] = pxy[i].x; p[2 * v + 1] = pxy[i].y; }
+            if (conic) { conic[3 * v] = co[i].x; conic[3 * v + 1] = co[i].y; conic[3 * v + 2] = co[i].z; }
+            if (alpha_base) alpha_base[v] = co[i].w;
+            if (radius) radius[v] = rad[i];
+            if (depth) { uint64_t b = key[i]; double d; std::memcpy(&d, &b, 8); depth[v] = d; }
+            if (color) { color[3 * v] = sp[i].r; color[3 * v + 1] = sp[i].g; color[3 * v + 2] = sp[i].bl; }
+            for (int k = 0; k < 3; ++k) {
+                if (cov) cov[3 * v + k] = detail[k * n + i];
+                if (t) t[3 * v + k] = detail[(3 + k) * n + i];
+            }
+            ++v;
+        }
+        *count = v;
     });
 }
 

@@ -272,6 +272,53 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
         for (int i = 0; i < 3; ++i) f->pose.t[i] = pose12[9 + i];
         for (int i = 0; i < 3; ++i) f->bg[i] = static_cast<float>(bg ? bg[i] : 0.0);
         f->full_depth_sort = false;
+        f->projected = f->given_grid = false;
+        render_into(f);
+    } catch (...) {
+        free_.push_back(f);
+        throw;
+    }
+    return f;
+}
+
+Frame* Engine::render_projected(const double* planes, size_t n, int W, int H, const double bg[3],
+                                const std::vector<uint2>* ranges, const std::vector<uint32_t>* slots) {
+    DeviceGuard g(device_);
+    if (n > static_cast<size_t>(INT32_MAX / kSplatPlanes)) throw std::invalid_argument("too many projections");
+    Frame* f;
+    if (!free_.empty()) {
+        f = free_.back();
+        free_.pop_back();
+    } else {
+        pool_.emplace_back(new Frame());
+        f = pool_.back().get();
+    }
+    try {
+        f->W = W;
+        f->H = H;
+        f->tiles_x = (W + kTile - 1) / kTile;
+        f->tiles_y = (H + kTile - 1) / kTile;
+        f->n = static_cast<int>(n);
+        f->generation = generation_;
+        f->active_degree = active_;
+        for (int i = 0; i < 12; ++i) f->pose12[i] = (i == 0 || i == 4 || i == 8) ? 1.0 : 0.0;
+        for (int i = 0; i < 9; ++i) f->pose.R[i] = f->pose12[i];
+        for (int i = 0; i < 3; ++i) f->pose.t[i] = 0.0;
+        for (int i = 0; i < 3; ++i) f->bg[i] = static_cast<float>(bg ? bg[i] : 0.0);
+        f->full_depth_sort = false;
+        f->projected = true;
+        f->given_grid = ranges != nullptr;
+        f->import.ensure(std::max<size_t>(n, 1) * kSplatPlanes * 8);
+        if (n)
+            OSB_CUDA_CHECK(cudaMemcpyAsync(f->import.as<double>(), planes, n * kSplatPlanes * 8, cudaMemcpyHostToDevice,
+                                           stream_));
+        if (f->given_grid) {
+            f->grid_ranges = *ranges;
+            f->grid_slots = *slots;
+        } else {
+            f->grid_ranges.clear();
+            f->grid_slots.clear();
+        }
         render_into(f);
     } catch (...) {
         free_.push_back(f);
@@ -288,7 +335,7 @@ Frame* Engine::render(const double pose12[12], int W, int H, const double bg[3])
 // 64-bit depth sort and renders the frame again.
 void Engine::render_into(Frame* f) {
     const int W = f->W, H = f->H;
-    const size_t n = n_ > 0 ? n_ : 1;
+    const size_t n = f->n > 0 ? static_cast<size_t>(f->n) : 1;
     const size_t pixels = static_cast<size_t>(W) * H;
     const int tiles = f->tiles_x * f->tiles_y;
     f->depth_key.ensure(n * 8);
@@ -321,13 +368,36 @@ void Engine::render_into(Frame* f) {
     if (!f->ready) OSB_CUDA_CHECK(cudaEventCreateWithFlags(&f->ready, cudaEventDisableTiming));
 
     const PreprocessOut pp = f->pp();
-    const int N = static_cast<int>(n_);
-    // K1
+    const int N = f->n;
+    // K1 (or the import of host projection records)
     {
         Span sp(*this, kPreprocess);
         OSB_CUDA_CHECK(cudaMemsetAsync(pp.depth_range, 0xFF, 8, stream_));
-        launch_preprocess(params_.as<float>(), N, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
-                          active_, f->pose, W, H, pp, stream_);
+        if (f->projected)
+            launch_import_projections(f->import.as<double>(), N, W, H, pp, stream_);
+        else
+            launch_preprocess(params_.as<float>(), N, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
+                              active_, f->pose, W, H, pp, stream_);
+    }
+    if (f->given_grid) {  // caller-supplied tile lists: no K2
+        const uint32_t M = static_cast<uint32_t>(f->grid_slots.size());
+        f->ivals[0].ensure(std::max<size_t>(M, 1) * 4);
+        if (M)
+            OSB_CUDA_CHECK(cudaMemcpyAsync(f->ivals[0].as<uint32_t>(), f->grid_slots.data(), size_t(M) * 4,
+                                           cudaMemcpyHostToDevice, stream_));
+        OSB_CUDA_CHECK(cudaMemcpyAsync(f->ranges.as<uint2>(), f->grid_ranges.data(), size_t(tiles) * 8,
+                                       cudaMemcpyHostToDevice, stream_));
+        f->inst_in_alt = false;
+        {
+            Span sp(*this, kBlend);
+            launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(),
+                         stream_);
+        }
+        // the host vectors are read by the copies above: finish them before the caller may free
+        OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+        f->cap = f->M = M;
+        f->validated = true;
+        return;
     }
     // K2a: depth rank = (t_r, id) order. Fast path: stable sort of the FP32-rounded t_r (monotone)
     // + exact FP64 re-ordering inside runs of equal keys; a run longer than 64 raises a flag
@@ -341,7 +411,7 @@ void Engine::render_into(Frame* f) {
         OSB_CUDA_CHECK(cudaMemsetAsync(long_run_flag, 0, 4, stream_));
         bool flipped;
         if (f->full_depth_sort) {
-            OSB_CUDA_CHECK(cudaMemcpyAsync(f->okeys[0].as<uint64_t>(), pp.depth_key, n_ * 8, cudaMemcpyDeviceToDevice,
+            OSB_CUDA_CHECK(cudaMemcpyAsync(f->okeys[0].as<uint64_t>(), pp.depth_key, size_t(N) * 8, cudaMemcpyDeviceToDevice,
                                            stream_));
             flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(), f->ovals[0].as<uint32_t>(),
                                      f->ovals[1].as<uint32_t>(), N, 64, f->sort_ws.as<void>(), stream_);
@@ -429,6 +499,22 @@ void Engine::validate(Frame* f) {
     throw std::runtime_error("render: instance buffer sizing did not converge");
 }
 
+void Engine::projection_detail(Frame* f, std::vector<double>& out) {
+    DeviceGuard g(device_);
+    validate(f);
+    if (f->projected || static_cast<size_t>(f->n) != n_ || f->generation != generation_)
+        throw std::logic_error("StateMismatch: render output does not match the cloud");
+    const size_t n = static_cast<size_t>(f->n);
+    out.assign(n * 6, 0.0);
+    if (!n) return;
+    DevBuf tmp;
+    tmp.ensure(n * 6 * 8);
+    launch_projection_detail(params_.as<float>(), f->n, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
+                             f->pose, f->W, f->H, tmp.as<double>(), stream_);
+    OSB_CUDA_CHECK(cudaMemcpyAsync(out.data(), tmp.as<double>(), n * 6 * 8, cudaMemcpyDeviceToHost, stream_));
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
 void Engine::release(Frame* f) {
     if (!f) return;
     // a frame released unread still tells the pool how large the instance buffers must be
@@ -444,7 +530,8 @@ void Engine::release(Frame* f) {
 void Engine::backward(Frame* f, const float* d_image, bool accumulate) {
     DeviceGuard g(device_);
     validate(f);
-    if (static_cast<size_t>(f->n) != n_ || f->generation != generation_) throw std::logic_error("StateMismatch: render output does not match the cloud");
+    if (f->projected || static_cast<size_t>(f->n) != n_ || f->generation != generation_)
+        throw std::logic_error("StateMismatch: render output does not match the cloud");
     // K4b overwrites (no read of the gradient planes, zeros for culled Gaussians) when the buffer is
     // logically zero or the caller asks for reference overwrite semantics.
     const bool overwrite = !accumulate || grads_zero_;
@@ -590,7 +677,8 @@ void Engine::reset_screen_stats() {
 void Engine::observe(Frame* f) {
     DeviceGuard g(device_);
     validate(f);
-    if (static_cast<size_t>(f->n) != n_ || f->generation != generation_) throw std::logic_error("StateMismatch: render output does not match the cloud");
+    if (f->projected || static_cast<size_t>(f->n) != n_ || f->generation != generation_)
+        throw std::logic_error("StateMismatch: render output does not match the cloud");
     launch_observe(f->radius.as<float>(), max_radius_.as<float>(), f->n, stream_);
 }
 

@@ -84,6 +84,12 @@ struct Frame {
     DevBuf rgb, T, contrib, last, visited, work;
     bool count_work = false;
     DevBuf sort_ws, scan_ws;
+    // Frames of host-supplied projections (render_projected): no Gaussian parameters behind them,
+    // so no backward; `grid_*` hold a caller-supplied tile grid (K2 skipped) when given_grid.
+    bool projected = false, given_grid = false;
+    DevBuf import;
+    std::vector<uint2> grid_ranges;
+    std::vector<uint32_t> grid_slots;
     const uint32_t* inst_gid() const { return ivals[inst_in_alt ? 1 : 0].as<uint32_t>(); }
     PreprocessOut pp() const;
     FrameBuffers fb() const;
@@ -101,9 +107,17 @@ public:
     void set_active_sh_degree(int d);
 
     Frame* render(const double pose12[12], int W, int H, const double bg[3]);
+    // bin_to_tiles + blend_forward over host SplatProjection records (kSplatPlanes FP64 planes of
+    // n, kernels.h): K2 bins and sorts them by (depth, slot) unless a tile grid is supplied
+    // (ranges per tile into `slots`, each a record index), then K3 blends.
+    Frame* render_projected(const double* planes, size_t n, int W, int H, const double bg[3],
+                            const std::vector<uint2>* ranges = nullptr, const std::vector<uint32_t>* slots = nullptr);
     // First use of a frame's results: waits for its instance count and re-renders it in the rare
     // case of an instance-buffer overflow or a long run of equal FP32 depth keys.
     void validate(Frame* f);
+    // cov (3 planes) and camera-space centre t (3 planes) of the frame's Gaussians (n each,
+    // zeros when culled): the SplatProjection fields K1 does not store.
+    void projection_detail(Frame* f, std::vector<double>& out);
     void release(Frame* f);
     void backward(Frame* f, const float* d_image_planar_dev, bool accumulate);
     // loss() of trainer.cpp:25-71 on the device: d_image into d_image_buffer(); the value is read

@@ -27,6 +27,16 @@ struct PreprocessOut {
 void launch_preprocess(const float* params, int n, int stride, int bc, int active_degree, const Pose& pose,
                        int W, int H, const PreprocessOut& out, cudaStream_t s);
 
+// Host-supplied SplatProjection records (rasterizer.hpp:31-41) as kSplatPlanes FP64 planes of n:
+// p.x, p.y, cov a, b, c, conic a, b, c, radius, depth, colour r, g, b, alpha_base. Writes the
+// same per-record outputs as K1 (depth must be finite and >= 0).
+constexpr int kSplatPlanes = 14;
+void launch_import_projections(const double* planes, int n, int W, int H, const PreprocessOut& out, cudaStream_t s);
+
+// cov (3 planes) then t (3 planes), n each, of every Gaussian; zeros when culled.
+void launch_projection_detail(const float* params, int n, int stride, int bc, const Pose& pose, int W, int H,
+                              double* out, cudaStream_t s);
+
 // ---- K2 duplicate + sort (sort.cu) ----------------------------------------------------------
 struct SortWorkspace;  // opaque, owned by the context
 size_t radix_workspace_bytes(int n_max, int key_bytes);

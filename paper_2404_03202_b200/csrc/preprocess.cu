@@ -12,6 +12,83 @@ namespace osb {
 
 namespace {
 
+// The record half of K1 shared with the projection import: tile rectangle (pole clamp, seam wrap),
+// depth keys, FP64 guard copy and the FP32 blend record with its guard band and extents.
+__device__ __forceinline__ void write_record(int gid, const double* p, const double* cov, const double* conic,
+                                             double o, double t_r, const double* col, uint32_t neg_bits,
+                                             double radius, int W, int H, const PreprocessOut& out) {
+    const double a = cov[0], b = cov[1], c = cov[2];
+    const double mid = 0.5 * (a + c);
+    const double dd2 = 0.25 * (a - c) * (a - c) + b * b;
+    const double dd = sqrt(dd2 > 0.0 ? dd2 : 0.0);
+    const double lmax = mid + dd;
+
+    // Tile rectangle with pole clamp and seam wrap (rasterizer.cpp:65-78).
+    const int tiles_x = (W + kTile - 1) / kTile;
+    const int tiles_y = (H + kTile - 1) / kTile;
+    int ty0 = static_cast<int>(floor((p[1] - radius) / kTile));
+    int ty1 = static_cast<int>(floor((p[1] + radius) / kTile));
+    ty0 = ty0 > 0 ? ty0 : 0;
+    ty1 = ty1 < tiles_y - 1 ? ty1 : tiles_y - 1;
+    int tx0 = static_cast<int>(floor((p[0] - radius) / kTile));
+    int tx1 = static_cast<int>(floor((p[0] + radius) / kTile));
+    if (tx1 - tx0 + 1 >= tiles_x) {
+        tx0 = 0;
+        tx1 = tiles_x - 1;
+    }
+    const uint32_t touched = ty0 > ty1 ? 0u : static_cast<uint32_t>((ty1 - ty0 + 1) * (tx1 - tx0 + 1));
+
+    // FP32 blend record and the guard band on `power` (DESIGN.md §3.2). Pairs with power within
+    // delta of pthr = ln(255 o) or of 0 are resolved by the FP64 path in K3/K4a.
+    const double qa = conic[0], qb = conic[1], qc = conic[2];
+    const double pthr = log(255.0 * o);
+    const double lmin = mid - dd;
+    const double lam_q_max = 1.0 / (lmin > 1e-300 ? lmin : 1e-300);
+    const double P_ = (pthr > 0.0 ? pthr : 0.0) + 1.0;
+    const double dmax = sqrt(2.0 * P_ * lmax);
+    const double tmax = 0.5 * (fabs(qa) + fabs(qb) + fabs(qc)) * dmax * dmax;
+    double delta = 0x1p-20 * (tmax + lam_q_max * dmax * (dmax + 16.0)) + 0x1p-21 * fabs(pthr) + 1e-6;
+    if (!(delta < 1e30)) delta = 1e30;
+
+    out.depth_key[gid] = static_cast<uint64_t>(__double_as_longlong(t_r));
+    // FP32 bits of t_r (monotone for positive values) and the frame's visible range of them (the
+    // depth-rank sort keys are these bits relative to the minimum, shifted into 24 bits)
+    const uint32_t dbits = __float_as_uint(__double2float_rn(t_r));
+    out.depth_key32[gid] = dbits;
+    const uint32_t act = __activemask();
+    const uint32_t wmin = __reduce_min_sync(act, dbits), wmax = __reduce_max_sync(act, dbits);
+    if ((threadIdx.x & 31) == __ffs(act) - 1) {
+        atomicMin(out.depth_range, wmin);
+        atomicMin(out.depth_range + 1, ~wmax);
+    }
+    out.touched[gid] = touched;
+    out.radius[gid] = static_cast<float>(radius);
+    out.rect[gid] = make_int4(tx0, tx1, ty0, ty1);
+    out.pxy[gid] = make_double2(p[0], p[1]);
+    out.conic_o[gid] = make_double4(qa, qb, qc, o);
+    Splat32 s;
+    s.ha = static_cast<float>(0.5 * qa);
+    s.b = static_cast<float>(qb);
+    s.hc = static_cast<float>(0.5 * qc);
+    s.o = static_cast<float>(o);
+    s.r = static_cast<float>(col[0]);
+    s.g = static_cast<float>(col[1]);
+    s.bl = static_cast<float>(col[2]);
+    s.pthr = static_cast<float>(pthr);
+    s.dl = static_cast<float>(delta);
+    // Bounding box of {d : 0.5 d^T Q d <= P} is |dx| <= sqrt(2 P cov_a), |dy| <= sqrt(2 P cov_c)
+    // (cov = Q^-1). With P = pthr + 3 delta (+ slack) every pixel outside has FP32 power
+    // > pthr + delta, i.e. a certain skip, so culling by these extents preserves every decision.
+    // (>= 0: only an imported record can have o < 1/255, and it never passes the alpha test)
+    const double Pext = fmax((pthr + 3.0 * delta) * (1.0 + 1e-4) + 1e-3, 0.0);
+    const double ex = sqrt(2.0 * Pext * (a > 0.0 ? a : 0.0)) * (1.0 + 1e-5) + 0.02;
+    const double ey = sqrt(2.0 * Pext * (c > 0.0 ? c : 0.0)) * (1.0 + 1e-5) + 0.02;
+    s.ext_x = ex < 1e30 ? static_cast<float>(ex) : 1e30f;
+    s.ext_y = ey < 1e30 ? static_cast<float>(ey) : 1e30f;
+    s.pad = __uint_as_float(neg_bits);  // K4b's colour-clamp gate
+    out.splat[gid] = s;
+}
+
 template <int DEG>
 __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P, int n, int stride, int bc, Pose pose,
                                                     int W, int H, PreprocessOut out) {
@@ -58,70 +135,38 @@ __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P,
     const double dd = sqrt(dd2 > 0.0 ? dd2 : 0.0);
     const double lmax = mid + dd;
     const double radius = ceil(3.0 * sqrt(lmax));
+    write_record(gid, pr.p, pr.cov, pr.conic, pr.o, pr.t_r, col, neg_bits, radius, W, H, out);
+}
 
-    // Tile rectangle with pole clamp and seam wrap (rasterizer.cpp:65-78).
-    const int tiles_x = (W + kTile - 1) / kTile;
-    const int tiles_y = (H + kTile - 1) / kTile;
-    int ty0 = static_cast<int>(floor((pr.p[1] - radius) / kTile));
-    int ty1 = static_cast<int>(floor((pr.p[1] + radius) / kTile));
-    ty0 = ty0 > 0 ? ty0 : 0;
-    ty1 = ty1 < tiles_y - 1 ? ty1 : tiles_y - 1;
-    int tx0 = static_cast<int>(floor((pr.p[0] - radius) / kTile));
-    int tx1 = static_cast<int>(floor((pr.p[0] + radius) / kTile));
-    if (tx1 - tx0 + 1 >= tiles_x) {
-        tx0 = 0;
-        tx1 = tiles_x - 1;
+
+// Host-supplied SplatProjection records (bin_to_tiles / blend_forward on host projections,
+// rasterizer.cpp:57-157): the same record half as K1, from FP64 planes instead of the parameters.
+__global__ void __launch_bounds__(256) k_import(const double* __restrict__ in, int n, int W, int H,
+                                                PreprocessOut out) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= n) return;
+    auto f = [&](int plane) { return in[static_cast<size_t>(plane) * n + gid]; };
+    const double p[2] = {f(0), f(1)};
+    const double cov[3] = {f(2), f(3), f(4)};
+    const double conic[3] = {f(5), f(6), f(7)};
+    const double col[3] = {f(10), f(11), f(12)};
+    write_record(gid, p, cov, conic, f(13), f(9), col, 0u, f(8), W, H, out);
+}
+
+// cov and t of every Gaussian (zeros when culled) for the full SplatProjection records of a frame
+// (osplat_frame_splats); the same project64 as K1, so bit-identical to what K1 used.
+__global__ void __launch_bounds__(128) k_detail(const float* __restrict__ P, int n, int stride, int bc, Pose pose,
+                                                int W, int H, double* __restrict__ out) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= n) return;
+    const Planes pl{bc};
+    Proj64 pr;
+    const bool vis = project64<false>(P, stride, pl, gid, pose, W, H, pr);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        out[static_cast<size_t>(k) * n + gid] = vis ? pr.cov[k] : 0.0;
+        out[static_cast<size_t>(3 + k) * n + gid] = vis ? pr.t[k] : 0.0;
     }
-    const uint32_t touched = ty0 > ty1 ? 0u : static_cast<uint32_t>((ty1 - ty0 + 1) * (tx1 - tx0 + 1));
-
-    // FP32 blend record and the guard band on `power` (DESIGN.md §3.2). Pairs with power within
-    // delta of pthr = ln(255 o) or of 0 are resolved by the FP64 path in K3/K4a.
-    const double qa = pr.conic[0], qb = pr.conic[1], qc = pr.conic[2];
-    const double pthr = log(255.0 * pr.o);
-    const double lmin = mid - dd;
-    const double lam_q_max = 1.0 / (lmin > 1e-300 ? lmin : 1e-300);
-    const double P_ = (pthr > 0.0 ? pthr : 0.0) + 1.0;
-    const double dmax = sqrt(2.0 * P_ * lmax);
-    const double tmax = 0.5 * (fabs(qa) + fabs(qb) + fabs(qc)) * dmax * dmax;
-    double delta = 0x1p-20 * (tmax + lam_q_max * dmax * (dmax + 16.0)) + 0x1p-21 * fabs(pthr) + 1e-6;
-    if (!(delta < 1e30)) delta = 1e30;
-
-    out.depth_key[gid] = static_cast<uint64_t>(__double_as_longlong(pr.t_r));
-    // FP32 bits of t_r (monotone for positive values) and the frame's visible range of them (the
-    // depth-rank sort keys are these bits relative to the minimum, shifted into 24 bits)
-    const uint32_t dbits = __float_as_uint(__double2float_rn(pr.t_r));
-    out.depth_key32[gid] = dbits;
-    const uint32_t act = __activemask();
-    const uint32_t wmin = __reduce_min_sync(act, dbits), wmax = __reduce_max_sync(act, dbits);
-    if ((threadIdx.x & 31) == __ffs(act) - 1) {
-        atomicMin(out.depth_range, wmin);
-        atomicMin(out.depth_range + 1, ~wmax);
-    }
-    out.touched[gid] = touched;
-    out.radius[gid] = static_cast<float>(radius);
-    out.rect[gid] = make_int4(tx0, tx1, ty0, ty1);
-    out.pxy[gid] = make_double2(pr.p[0], pr.p[1]);
-    out.conic_o[gid] = make_double4(qa, qb, qc, pr.o);
-    Splat32 s;
-    s.ha = static_cast<float>(0.5 * qa);
-    s.b = static_cast<float>(qb);
-    s.hc = static_cast<float>(0.5 * qc);
-    s.o = static_cast<float>(pr.o);
-    s.r = static_cast<float>(col[0]);
-    s.g = static_cast<float>(col[1]);
-    s.bl = static_cast<float>(col[2]);
-    s.pthr = static_cast<float>(pthr);
-    s.dl = static_cast<float>(delta);
-    // Bounding box of {d : 0.5 d^T Q d <= P} is |dx| <= sqrt(2 P cov_a), |dy| <= sqrt(2 P cov_c)
-    // (cov = Q^-1). With P = pthr + 3 delta (+ slack) every pixel outside has FP32 power
-    // > pthr + delta, i.e. a certain skip, so culling by these extents preserves every decision.
-    const double Pext = (pthr + 3.0 * delta) * (1.0 + 1e-4) + 1e-3;
-    const double ex = sqrt(2.0 * Pext * (a > 0.0 ? a : 0.0)) * (1.0 + 1e-5) + 0.02;
-    const double ey = sqrt(2.0 * Pext * (c > 0.0 ? c : 0.0)) * (1.0 + 1e-5) + 0.02;
-    s.ext_x = ex < 1e30 ? static_cast<float>(ex) : 1e30f;
-    s.ext_y = ey < 1e30 ? static_cast<float>(ey) : 1e30f;
-    s.pad = __uint_as_float(neg_bits);  // K4b's colour-clamp gate
-    out.splat[gid] = s;
 }
 
 }  // namespace
@@ -136,6 +181,19 @@ void launch_preprocess(const float* params, int n, int stride, int bc, int activ
         case 2: k_preprocess<2><<<blocks, 256, 0, s>>>(params, n, stride, bc, pose, W, H, out); break;
         default: k_preprocess<3><<<blocks, 256, 0, s>>>(params, n, stride, bc, pose, W, H, out); break;
     }
+    OSB_LAUNCHED(1);
+}
+
+void launch_import_projections(const double* planes, int n, int W, int H, const PreprocessOut& out, cudaStream_t s) {
+    if (n <= 0) return;
+    k_import<<<(n + 255) / 256, 256, 0, s>>>(planes, n, W, H, out);
+    OSB_LAUNCHED(1);
+}
+
+void launch_projection_detail(const float* params, int n, int stride, int bc, const Pose& pose, int W, int H,
+                              double* out, cudaStream_t s) {
+    if (n <= 0) return;
+    k_detail<<<(n + 127) / 128, 128, 0, s>>>(params, n, stride, bc, pose, W, H, out);
     OSB_LAUNCHED(1);
 }
 

@@ -127,6 +127,10 @@ def _load():
         "osplat_gpu_train": (S, [_vp, _vp, C.c_size_t, _dp, C.POINTER(_vp), _u8p, C.c_double, C.c_long, C.c_char_p,
                                  PROGRESS_FN, C.c_void_p]),
         "osplat_frame_work": (S, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+        "osplat_frame_splats": (S, [_vp, C.POINTER(C.c_size_t), _i32p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
+        "osplat_gpu_upload": (S, [_vp, _vp]),
+        "osplat_gpu_render_projected": (S, [_vp, C.c_size_t, _i32p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int,
+                                            C.c_int, _dp, _u32p, _i32p, C.POINTER(_vp)]),
     }
     ab_build = "OSPLAT_LIB" in os.environ  # A/B runs may load older builds without newer entry points
     for name, (res, args) in sig.items():
@@ -139,6 +143,8 @@ def _load():
 
 
 lib = _load()
+# osplat_frame_splats / osplat_gpu_render_projected per-record arrays, in argument order
+SPLAT_FIELDS = ("gaussian_id", "p", "cov", "conic", "radius", "depth", "color", "alpha_base", "t")
 KERNEL_COUNT = 11  # OSPLAT_KERNEL_COUNT
 EXPORTED = ("osplat_version osplat_last_error osplat_set_threads osplat_cloud_load osplat_cloud_save "
             "osplat_cloud_count osplat_cloud_free osplat_config_create osplat_config_set osplat_config_free "
@@ -291,6 +297,19 @@ class Frame:
         check(lib.osplat_frame_tiles(self.handle, None, None, None, _p(ranges, _u32p), _p(ids, _u32p)))
         return tx.value, ty.value, ranges, ids[:m.value]
 
+    def splats(self) -> dict:
+        """Full SplatProjection records (osplat_frame_splats): visible Gaussians in ascending id for a
+        render, the given records for a render_projected frame."""
+        n = C.c_size_t(0)
+        check(lib.osplat_frame_splats(self.handle, C.byref(n), *([None] * 9)))
+        k = n.value
+        out = dict(gaussian_id=np.zeros(k, dtype=np.int32), p=np.zeros((k, 2)), cov=np.zeros((k, 3)),
+                   conic=np.zeros((k, 3)), radius=np.zeros(k), depth=np.zeros(k), color=np.zeros((k, 3)),
+                   alpha_base=np.zeros(k), t=np.zeros((k, 3)))
+        ptrs = [_p(out["gaussian_id"], _i32p)] + [_p(out[f]) for f in SPLAT_FIELDS[1:]]
+        check(lib.osplat_frame_splats(self.handle, C.byref(n), *ptrs))
+        return out
+
     def work(self):
         """(forward pairs visited, backward pairs, tile instances) — needs count_work profiling."""
         f, b, m = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
@@ -342,6 +361,34 @@ class Context:
         bg = np.ascontiguousarray(background, dtype=np.float64)
         h = _vp()
         check(lib.osplat_gpu_render(self.handle, _p(t), width, height, _p(bg), C.byref(h)))
+        return Frame(self, h)
+
+    def upload(self, cloud: Cloud | HostCloud):
+        """Replace the device cloud (osplat_gpu_upload)."""
+        hc = cloud if isinstance(cloud, HostCloud) else HostCloud.from_cloud(cloud)
+        check(lib.osplat_gpu_upload(self.handle, hc.handle))
+        self._refresh()
+
+    def render_projected(self, splats: dict, width: int, height: int, background=(0.0, 0.0, 0.0),
+                         grid=None) -> Frame:
+        """bin_to_tiles + blend_forward over host SplatProjection records (a dict with the keys of
+        Frame.splats(); 't' is ignored). grid: None (bin on the device) or (ranges [tiles, 2],
+        entries [M]) as Frame.tiles() returns them for such a frame."""
+        k = len(splats["depth"])
+        ids = np.ascontiguousarray(splats.get("gaussian_id", np.arange(k)), dtype=np.int32)
+        arrs = [np.ascontiguousarray(splats[f], dtype=np.float64) for f in SPLAT_FIELDS[1:8]]
+        bg = np.ascontiguousarray(background, dtype=np.float64)
+        offs = ents = None
+        if grid is not None:
+            ranges, entries = grid
+            ranges = np.asarray(ranges, dtype=np.int64)
+            offs = np.ascontiguousarray(np.concatenate([[0], np.cumsum(ranges[:, 1] - ranges[:, 0])]), dtype=np.uint32)
+            ents = np.ascontiguousarray(np.concatenate([entries[a:b] for a, b in ranges] + [np.zeros(0)]),
+                                        dtype=np.int32)
+        h = _vp()
+        check(lib.osplat_gpu_render_projected(self.handle, k, _p(ids, _i32p), *[_p(a) for a in arrs], width, height,
+                                              _p(bg), None if offs is None else _p(offs, _u32p),
+                                              None if ents is None else _p(ents, _i32p), C.byref(h)))
         return Frame(self, h)
 
     def backward(self, frame: Frame, d_image: np.ndarray, accumulate: bool = False):
@@ -473,7 +520,8 @@ class Context:
 
     def _refresh(self):
         v = self.view()
-        self.n, self.stride = v.n, v.stride
+        self.n, self.stride, self.planes, self.sh_degree = v.n, v.stride, v.planes, v.sh_degree
+        self.basis_count = (v.sh_degree + 1) ** 2
 
     def download(self) -> Cloud:
         h = _vp()
