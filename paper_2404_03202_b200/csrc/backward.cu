@@ -302,7 +302,7 @@ __device__ __forceinline__ void sh_backward(ShBack<R, OVERWRITE>& s, const R* d)
 // K4b. Uses K1's FP64 conic and opacity (conic_o) and its pre-clamp colour sign bits instead of
 // re-deriving them; re-derives t, J, W-rotated J, Sigma3 and the rotation with K1's device code.
 template <int DEG, bool OVERWRITE>
-__global__ void __launch_bounds__(128) k_backward_gaussians(const float* __restrict__ P, int n, int stride, int bc,
+__global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __restrict__ P, int n, int stride, int bc,
                                                             Pose pose, int W, int H,
                                                             const uint64_t* __restrict__ depth_key,
                                                             const double4* __restrict__ conic_o,
