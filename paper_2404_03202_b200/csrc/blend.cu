@@ -33,8 +33,12 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
     const uint2 range = ranges[tile];
     const double width = W;
     const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
-    const float lxo = lx - 7.5f, lyo = ly - 7.5f;
+    float lxo = lx - 7.5f, lyo = ly - 7.5f;
+    // opaque to the compiler: kept in registers instead of being rematerialized from tid in the loop
+    asm volatile("mov.b32 %0, %0;" : "+f"(lxo));
+    asm volatile("mov.b32 %0, %0;" : "+f"(lyo));
     const float halfW = 0.5f * W, fW = static_cast<float>(W);
+    const uint32_t stage_s = pinned_smem_base(stage);
 
     float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
     double T64 = 1.0;
@@ -62,7 +66,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
       for (int sub = 0; sub < kTileWarps; ++sub) {
         const uint32_t base = cbase + 32 * sub;
         if (base >= range.y || __all_sync(0xffffffffu, done)) break;
-        WarpStage& ws = stage[sub];
+        const StageRef ws{stage_s + static_cast<uint32_t>(sub * sizeof(WarpStage))};
+        const int kofs = static_cast<int>(base - range.x) + 1;  // 1-based list position of entry j: kofs + j
         const uint32_t mk = s_mask[32 * sub + lane];
         const uint32_t bal0 = __ballot_sync(0xffffffffu, (mk >> (2 * warp)) & 1u);
         const uint32_t bal1 = __ballot_sync(0xffffffffu, (mk >> (2 * warp + 1)) & 1u);
@@ -77,18 +82,17 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
             while (bal != 0u && !done && !pend) {
                 const int j = __ffs(bal) - 1;
                 bal &= bal - 1u;
-                const float4 A = ws.a[j];
-                const float4 B = ws.b[j];
+                const float4 A = ws.a(j);
+                const float4 B = ws.b(j);
                 float dx, dy, power;
                 bool unc;
                 if (!pair_power(A, B, lxo, lyo, halfW, fW, dx, dy, power, unc)) continue;
-                const float4 Cc = ws.c[j];
-                const uint32_t k = base + j;
+                const float4 Cc = ws.c(j);
                 float alpha;
                 double a64 = 0.0;
                 if (unc || exact) {
                     Pair64 p;
-                    if (!pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p)) continue;
+                    if (!pair_slow(ws.gid(j), px, py, width, pp.pxy, pp.conic_o, &p)) continue;
                     a64 = p.alpha;
                     alpha = static_cast<float>(a64);
                 } else {
@@ -100,7 +104,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                     if (Tn < kTHi) {
                         if (Tn < kTLo) {
                             done = true;
-                            stop_at = static_cast<int>(k - range.x) + 1;
+                            stop_at = kofs + j;
                             break;
                         }
                         pend = true;  // inside the band: decide in FP64 after an exact replay
@@ -115,7 +119,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                     const double Tn64 = T64 * (1.0 - a64);
                     if (Tn64 < kTStop) {
                         done = true;
-                        stop_at = static_cast<int>(k - range.x) + 1;
+                        stop_at = kofs + j;
                         break;
                     }
                     w = static_cast<float>(a64 * T64);
@@ -126,7 +130,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                 c1 = __fmaf_rn(Cc.y, w, c1);
                 c2 = __fmaf_rn(Cc.z, w, c2);
                 ++contrib;
-                last = static_cast<int>(k - range.x) + 1;
+                last = kofs + j;
             }
             uint32_t pm = __ballot_sync(0xffffffffu, pend);
             if (pm == 0u) break;
@@ -140,20 +144,19 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
             }
             if (pend) {
                 pend = false;
-                const uint32_t k = base + pj;
                 double a64 = p_a64;
                 if (!p_unc) {
                     Pair64 p;
-                    pair_slow(ws.gid[pj], px, py, width, pp.pxy, pp.conic_o, &p);
+                    pair_slow(ws.gid(pj), px, py, width, pp.pxy, pp.conic_o, &p);
                     a64 = p.alpha;
                 }
                 const double Tn64 = T64 * (1.0 - a64);
                 if (Tn64 < kTStop) {
                     done = true;
-                    stop_at = static_cast<int>(k - range.x) + 1;
+                    stop_at = kofs + pj;
                 } else {
                     exact = true;
-                    const float4 Cc = ws.c[pj];
+                    const float4 Cc = ws.c(pj);
                     const float w = static_cast<float>(a64 * T64);
                     T64 = Tn64;
                     T = static_cast<float>(Tn64);
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                     c1 = __fmaf_rn(Cc.y, w, c1);
                     c2 = __fmaf_rn(Cc.z, w, c2);
                     ++contrib;
-                    last = static_cast<int>(k - range.x) + 1;
+                    last = kofs + pj;
                 }
             }
         }

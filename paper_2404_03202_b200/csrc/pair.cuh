@@ -47,6 +47,31 @@ struct WarpStage {
     uint32_t gid[32];
 };
 
+// Staged-record reads through a 32-bit shared-memory address computed (and pinned in a register)
+// once per kernel: indexing stage[sub].a[j] directly makes the compiler rebuild the shared window
+// base (S2R + LEA + 2 IMAD) on every iteration of the hot loops.
+struct StageRef {
+    uint32_t base;  // shared address of stage[sub]
+    __device__ __forceinline__ float4 a(int j) const { return ld4(base + 16u * j); }
+    __device__ __forceinline__ float4 b(int j) const { return ld4(base + 512u + 16u * j); }
+    __device__ __forceinline__ float4 c(int j) const { return ld4(base + 1024u + 16u * j); }
+    __device__ __forceinline__ uint32_t gid(int j) const {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + 1536u + 4u * j));
+        return v;
+    }
+    static __device__ __forceinline__ float4 ld4(uint32_t addr) {
+        float4 v;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+        return v;
+    }
+};
+__device__ __forceinline__ uint32_t pinned_smem_base(const void* p) {
+    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("mov.b32 %0, %0;" : "+r"(a));
+    return a;
+}
+
 // Stage entry `gid` into this lane's slot for the tile centred at (xc, yc); returns a 2-bit mask:
 // bit h set when the entry can reach a pixel centre of half-warp h's block (row offsets r0..r0+3,
 // column offsets c0+4h..c0+4h+3).
