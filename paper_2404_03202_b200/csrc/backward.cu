@@ -99,8 +99,6 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
 
     float T_acc = T_final;
     float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;     // suffix colour
-    float lc0 = 0.0f, lc1 = 0.0f, lc2 = 0.0f;  // last colour
-    float last_a = 0.0f;
 
     // Each 16-lane half owns a 4x4 pixel quarter and walks the entries that can reach it (the same
     // half-warp culling as K3), back to front; the halves reduce their (different) entries at once.
@@ -173,28 +171,29 @@ __global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint3
                     if (ok) {
                         has = true;
                         const float one_m = 1.0f - alpha;
-                        const float inv = __fdividef(1.0f, one_m);
+                        // 1 - alpha is in [0.01, 1]: MUFU.RCP directly (what __fdividef(1, x)
+                        // computes there, without its range-scaling instructions)
+                        float inv;
+                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));
                         T_acc = T_acc * inv;
                         const float wb = alpha * T_acc;
                         v0 = dl0 * wb;
                         v1 = dl1 * wb;
                         v2 = dl2 * wb;
-                        const float oml = 1.0f - last_a;
-                        s0 = __fmaf_rn(lc0, last_a, s0 * oml);
-                        s1 = __fmaf_rn(lc1, last_a, s1 * oml);
-                        s2 = __fmaf_rn(lc2, last_a, s2 * oml);
                         float d_alpha = (Cc.x - s0) * dl0;
                         d_alpha = __fmaf_rn(Cc.y - s1, dl1, d_alpha);
                         d_alpha = __fmaf_rn(Cc.z - s2, dl2, d_alpha);
                         d_alpha = d_alpha * T_acc;
                         if (BG) d_alpha = d_alpha - (T_final * inv) * bg_dot;
-                        lc0 = Cc.x; lc1 = Cc.y; lc2 = Cc.z;
-                        last_a = alpha;
+                        // suffix (colour of everything behind) now includes this entry
+                        s0 = __fmaf_rn(Cc.x, alpha, s0 * one_m);
+                        s1 = __fmaf_rn(Cc.y, alpha, s1 * one_m);
+                        s2 = __fmaf_rn(Cc.z, alpha, s2 * one_m);
                         if (gate) {
                             // dL/dpower times d, d d^T: K4b applies the conic once per Gaussian
                             // (d_p = Q sum(dL/dpower d)) and the 1/2 of the conic diagonal
                             v3 = g * d_alpha;
-                            const float d_power = -g * Cc.w * d_alpha;
+                            const float d_power = -Cc.w * v3;
                             v4 = d_power * dx;
                             v5 = d_power * dy;
                             v6 = v4 * dx;
