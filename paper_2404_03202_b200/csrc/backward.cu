@@ -63,7 +63,7 @@ __device__ __forceinline__ float half_reduce9(const float (&v)[9], int lane, int
 
 // BG: a non-black background adds the -T_final / (1 - alpha) * (bg . dL/dC) term (gradients.cpp:141).
 template <bool BG>
-__global__ void __launch_bounds__(kTileThreads, 3) k_backward_pixels(const uint32_t* __restrict__ inst_gid,
+__global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint32_t* __restrict__ inst_gid,
                                                                      const uint2* __restrict__ ranges, PreprocessOut pp,
                                                                      int W, int H, int tiles_x, float bg0, float bg1,
                                                                      float bg2, FrameBuffers fb,
