@@ -86,19 +86,23 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
     const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
     const float lxo = lx - 7.5f, lyo = ly - 7.5f;
     const float halfW = 0.5f * W, fW = static_cast<float>(W);
+    const float2 nlo = make_float2(-lxo, -lyo);
     const size_t pix = static_cast<size_t>(py) * W + px;
     const size_t plane = static_cast<size_t>(W) * H;
     const int last = inside ? fb.last[pix] : 0;
     const float T_final = inside ? fb.T[pix] : 0.0f;
     const float dl0 = inside ? d_image[pix] : 0.0f;
     const float dl1 = inside ? d_image[plane + pix] : 0.0f;
+    const float2 dl01 = make_float2(dl0, dl1);
     const float dl2 = inside ? d_image[2 * plane + pix] : 0.0f;
     const float bg_dot = bg0 * dl0 + bg1 * dl1 + bg2 * dl2;
     // this warp only walks the list up to its own furthest last_contrib
     const int max_last = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(last)));
 
     float T_acc = T_final;
-    float s0 = 0.0f, s1 = 0.0f, s2 = 0.0f;     // suffix colour
+    // negated suffix colour (-s): (Cc - s) is then one packed add; ns01 = (-s0, -s1)
+    float2 ns01 = make_float2(0.0f, 0.0f);
+    float ns2 = 0.0f;
 
     // Each 16-lane half owns a 4x4 pixel quarter and walks the entries that can reach it (the same
     // half-warp culling as K3), back to front; the halves reduce their (different) entries at once.
@@ -139,9 +143,10 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
             if (live && k < last) {
                 const float4 A = ws.a[j];
                 const float4 B = ws.b[j];
-                float dx, dy, power;
+                float2 d;
+                float power;
                 bool unc;
-                if (pair_power(A, B, lxo, lyo, halfW, fW, dx, dy, power, unc)) {
+                if (pair_power2(A, B, nlo, halfW, fW, d, power, unc)) {
                     const float4 Cc = ws.c[j];
                     float alpha, g;
                     bool gate;
@@ -177,28 +182,35 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
                         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));
                         T_acc = T_acc * inv;
                         const float wb = alpha * T_acc;
-                        v0 = dl0 * wb;
-                        v1 = dl1 * wb;
+                        const float2 v01 = __fmul2_rn(dl01, make_float2(wb, wb));
+                        v0 = v01.x;
+                        v1 = v01.y;
                         v2 = dl2 * wb;
-                        float d_alpha = (Cc.x - s0) * dl0;
-                        d_alpha = __fmaf_rn(Cc.y - s1, dl1, d_alpha);
-                        d_alpha = __fmaf_rn(Cc.z - s2, dl2, d_alpha);
+                        const float2 cs = __fadd2_rn(make_float2(Cc.x, Cc.y), ns01);  // Cc - s
+                        float d_alpha = cs.x * dl01.x;
+                        d_alpha = __fmaf_rn(cs.y, dl01.y, d_alpha);
+                        d_alpha = __fmaf_rn(Cc.z + ns2, dl2, d_alpha);
                         d_alpha = d_alpha * T_acc;
                         if (BG) d_alpha = d_alpha - (T_final * inv) * bg_dot;
                         // suffix (colour of everything behind) now includes this entry
-                        s0 = __fmaf_rn(Cc.x, alpha, s0 * one_m);
-                        s1 = __fmaf_rn(Cc.y, alpha, s1 * one_m);
-                        s2 = __fmaf_rn(Cc.z, alpha, s2 * one_m);
+                        // (-s) = fma(Cc, -alpha, (-s) (1 - alpha)): the exact negation of
+                        // fma(Cc, alpha, s (1 - alpha))
+                        const float nalpha = -alpha;
+                        ns01 = __ffma2_rn(make_float2(Cc.x, Cc.y), make_float2(nalpha, nalpha),
+                                          __fmul2_rn(ns01, make_float2(one_m, one_m)));
+                        ns2 = __fmaf_rn(Cc.z, nalpha, ns2 * one_m);
                         if (gate) {
                             // dL/dpower times d, d d^T: K4b applies the conic once per Gaussian
                             // (d_p = Q sum(dL/dpower d)) and the 1/2 of the conic diagonal
                             v3 = g * d_alpha;
                             const float d_power = -Cc.w * v3;
-                            v4 = d_power * dx;
-                            v5 = d_power * dy;
-                            v6 = v4 * dx;
-                            v7 = v4 * dy;
-                            v8 = v5 * dy;
+                            const float2 v45 = __fmul2_rn(d, make_float2(d_power, d_power));
+                            const float2 v67 = __fmul2_rn(d, make_float2(v45.x, v45.x));
+                            v4 = v45.x;
+                            v5 = v45.y;
+                            v6 = v67.x;
+                            v7 = v67.y;
+                            v8 = v45.y * d.y;
                         }
                     }
                 }

@@ -39,8 +39,10 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
     asm volatile("mov.b32 %0, %0;" : "+f"(lyo));
     const float halfW = 0.5f * W, fW = static_cast<float>(W);
     const uint32_t stage_s = pinned_smem_base(stage);
+    const float2 nlo = make_float2(-lxo, -lyo);
 
-    float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f;
+    float T = 1.0f, c2 = 0.0f;
+    float2 c01 = make_float2(0.0f, 0.0f);  // (c0, c1), updated with one packed FFMA2
     double T64 = 1.0;
     bool exact = false;
     int contrib = 0, last = 0;
@@ -84,9 +86,10 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                 bal &= bal - 1u;
                 const float4 A = ws.a(j);
                 const float4 B = ws.b(j);
-                float dx, dy, power;
+                float2 d;
+                float power;
                 bool unc;
-                if (!pair_power(A, B, lxo, lyo, halfW, fW, dx, dy, power, unc)) continue;
+                if (!pair_power2(A, B, nlo, halfW, fW, d, power, unc)) continue;
                 const float4 Cc = ws.c(j);
                 float alpha;
                 double a64 = 0.0;
@@ -126,8 +129,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                     T64 = Tn64;
                     T = static_cast<float>(Tn64);
                 }
-                c0 = __fmaf_rn(Cc.x, w, c0);
-                c1 = __fmaf_rn(Cc.y, w, c1);
+                c01 = __ffma2_rn(make_float2(Cc.x, Cc.y), make_float2(w, w), c01);
                 c2 = __fmaf_rn(Cc.z, w, c2);
                 ++contrib;
                 last = kofs + j;
@@ -160,8 +162,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                     const float w = static_cast<float>(a64 * T64);
                     T64 = Tn64;
                     T = static_cast<float>(Tn64);
-                    c0 = __fmaf_rn(Cc.x, w, c0);
-                    c1 = __fmaf_rn(Cc.y, w, c1);
+                    c01 = __ffma2_rn(make_float2(Cc.x, Cc.y), make_float2(w, w), c01);
                     c2 = __fmaf_rn(Cc.z, w, c2);
                     ++contrib;
                     last = kofs + pj;
@@ -175,8 +176,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
     if (inside) {
         const size_t pix = static_cast<size_t>(py) * W + px;
         const size_t plane = static_cast<size_t>(W) * H;
-        fb.rgb[pix] = __fmaf_rn(T, bg0, c0);
-        fb.rgb[plane + pix] = __fmaf_rn(T, bg1, c1);
+        fb.rgb[pix] = __fmaf_rn(T, bg0, c01.x);
+        fb.rgb[plane + pix] = __fmaf_rn(T, bg1, c01.y);
         fb.rgb[2 * plane + pix] = __fmaf_rn(T, bg2, c2);
         fb.T[pix] = T;
         fb.contrib[pix] = contrib;

@@ -167,6 +167,27 @@ __device__ __forceinline__ bool pair_power(const float4 A, const float4 B, float
     return true;
 }
 
+// pair_power with the paired FP32 operations issued as packed f32x2 instructions (FADD2 / FMUL2:
+// half the issue slots, each half rounded exactly like the scalar op, so every value and decision
+// is bit-identical to pair_power). nlo = (-lxo, -lyo).
+__device__ __forceinline__ bool pair_power2(const float4 A, const float4 B, float2 nlo, float halfW, float fW,
+                                            float2& d, float& power, bool& unc) {
+    d = __fadd2_rn(make_float2(A.x, A.y), nlo);  // (A.x - lxo, A.y - lyo)
+    unc = false;
+    if (B.w < 0.0f) {
+        if (d.x > halfW) d.x -= fW;
+        else if (d.x < -halfW) d.x += fW;
+        unc = fabsf(fabsf(d.x) - halfW) < 0.01f;
+    }
+    const float2 q = __fmul2_rn(make_float2(A.z, A.w), d);  // (A.z dx, A.w dy)
+    const float bdx = B.x * d.x;
+    power = __fmaf_rn(q.x, d.x, __fmaf_rn(q.y, d.y, bdx * d.y));
+    if (!(power <= B.z) && !unc) return false;
+    const float dl = fabsf(B.w);
+    unc = unc || power < dl || power > B.y;
+    return true;
+}
+
 struct Pair64 {
     double alpha, g, og;
 };
