@@ -5,7 +5,8 @@
 //
 // Two tiled kernels per image, one CTA per 32x32 output tile and colour channel:
 // Both passes are register-blocked (4 outputs per thread from 14 staged values) so shared-memory
-// traffic is ~3x lower than one output per thread.
+// traffic is ~3x lower than one output per thread, and maps are paired in float2 planes so two of
+// them advance per packed FFMA2 (half the FMA issue slots, bit-identical results).
 //   S1: x, y tile + 5-px halo -> smem; horizontal then vertical 11-tap passes for the five maps
 //       (mu_x, mu_y, E[xx], E[yy], E[xy]); per-pixel SSIM (block-reduced into one FP64 sum per
 //       channel) and its partials g_mu, g_sxx, g_sxy written as three planes.
@@ -47,8 +48,12 @@ struct Window {
 __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(const float* __restrict__ rgb, const float* __restrict__ gt,
                                                            int W, int H, int keep, Window win,
                                                            float* __restrict__ g_planes, double* __restrict__ ssim_sum) {
-    __shared__ float sx[kS][kS + 1], sy[kS][kS + 1];
-    __shared__ float h[5][kS][kT + 1];
+    // Maps are kept in (x, y)-paired float2 planes so both members of a pair go through one packed
+    // FFMA2 / FMUL2 (each half rounded exactly like the scalar op) and one 64-bit shared access.
+    // Odd pitches (in 8-byte words) keep the 64-bit accesses bank-conflict-free.
+    __shared__ float2 sxy[kS][kS + 1];                 // (x, y)
+    __shared__ float2 h01[kS][kT + 1], h23[kS][kT + 1];  // (mu_x, mu_y), (E[xx], E[yy]) after the row pass
+    __shared__ float h4[kS][kT + 1];                   // E[xy]
     __shared__ double s_red[kLossThreads / 32];
     const int ch = blockIdx.z;
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
@@ -63,39 +68,38 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(const float* __restri
         const bool in = i < kS * kS && gx >= 0 && gx < W && gy >= 0 && gy < keep;
         const float xv = in ? X[static_cast<size_t>(gy) * W + gx] : 0.0f;
         const float yv = in ? Y[static_cast<size_t>(gy) * W + gx] : 0.0f;
-        if (i < kS * kS) {
-            sx[r][c] = xv;
-            sy[r][c] = yv;
-        }
+        if (i < kS * kS) sxy[r][c] = make_float2(xv, yv);
     }
     __syncthreads();
+    float w[2 * kR + 1];
+#pragma unroll
+    for (int t = 0; t < 2 * kR + 1; ++t) w[t] = win.w[t];
     // horizontal pass over all staged rows; each thread produces 4 consecutive outputs of one row
-    // from 14 staged values (lanes on consecutive rows: conflict-free at the odd pitch)
+    // from 14 staged values (lanes on consecutive rows)
     for (int i = threadIdx.x; i < kS * kG; i += kLossThreads) {
         const int r = i % kS, c0 = (i / kS) * kO;
-        float xv[kO + 2 * kR], yv[kO + 2 * kR], xx[kO + 2 * kR], yy[kO + 2 * kR], xy[kO + 2 * kR];
+        float2 v[kO + 2 * kR], sq[kO + 2 * kR];
+        float xy[kO + 2 * kR];
 #pragma unroll
         for (int j = 0; j < kO + 2 * kR; ++j) {
-            xv[j] = sx[r][c0 + j];
-            yv[j] = sy[r][c0 + j];
-            xx[j] = xv[j] * xv[j];
-            yy[j] = yv[j] * yv[j];
-            xy[j] = xv[j] * yv[j];
+            v[j] = sxy[r][c0 + j];
+            sq[j] = __fmul2_rn(v[j], v[j]);  // (x x, y y)
+            xy[j] = v[j].x * v[j].y;
         }
 #pragma unroll
         for (int o = 0; o < kO; ++o) {
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+            float2 a01 = make_float2(0.f, 0.f), a23 = make_float2(0.f, 0.f);
+            float a4 = 0.f;
 #pragma unroll
             for (int t = 0; t < 2 * kR + 1; ++t) {
-                const float w = win.w[t];
-                a0 = __fmaf_rn(w, xv[o + t], a0);
-                a1 = __fmaf_rn(w, yv[o + t], a1);
-                a2 = __fmaf_rn(w, xx[o + t], a2);
-                a3 = __fmaf_rn(w, yy[o + t], a3);
-                a4 = __fmaf_rn(w, xy[o + t], a4);
+                const float2 wt = make_float2(w[t], w[t]);
+                a01 = __ffma2_rn(wt, v[o + t], a01);
+                a23 = __ffma2_rn(wt, sq[o + t], a23);
+                a4 = __fmaf_rn(w[t], xy[o + t], a4);
             }
-            h[0][r][c0 + o] = a0; h[1][r][c0 + o] = a1; h[2][r][c0 + o] = a2; h[3][r][c0 + o] = a3;
-            h[4][r][c0 + o] = a4;
+            h01[r][c0 + o] = a01;
+            h23[r][c0 + o] = a23;
+            h4[r][c0 + o] = a4;
         }
     }
     __syncthreads();
@@ -107,26 +111,45 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_fwd(const float* __restri
     for (int i = threadIdx.x; i < kT * kG; i += kLossThreads) {
         const int c = i % kT, r0 = (i / kT) * kO;
         const int gx = x0 + c;
-        float m[5][kO];
+        float2 m01[kO], m23[kO];
+        float m4[kO];
+        {
+            float2 col[kO + 2 * kR];
 #pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            float col[kO + 2 * kR];
+            for (int j = 0; j < kO + 2 * kR; ++j) col[j] = h01[r0 + j][c];
 #pragma unroll
-            for (int j = 0; j < kO + 2 * kR; ++j) col[j] = h[q][r0 + j][c];
+            for (int o = 0; o < kO; ++o) {
+                float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int t = 0; t < 2 * kR + 1; ++t) acc = __ffma2_rn(make_float2(w[t], w[t]), col[o + t], acc);
+                m01[o] = acc;
+            }
+#pragma unroll
+            for (int j = 0; j < kO + 2 * kR; ++j) col[j] = h23[r0 + j][c];
+#pragma unroll
+            for (int o = 0; o < kO; ++o) {
+                float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int t = 0; t < 2 * kR + 1; ++t) acc = __ffma2_rn(make_float2(w[t], w[t]), col[o + t], acc);
+                m23[o] = acc;
+            }
+            float c4[kO + 2 * kR];
+#pragma unroll
+            for (int j = 0; j < kO + 2 * kR; ++j) c4[j] = h4[r0 + j][c];
 #pragma unroll
             for (int o = 0; o < kO; ++o) {
                 float acc = 0.f;
 #pragma unroll
-                for (int t = 0; t < 2 * kR + 1; ++t) acc = __fmaf_rn(win.w[t], col[o + t], acc);
-                m[q][o] = acc;
+                for (int t = 0; t < 2 * kR + 1; ++t) acc = __fmaf_rn(w[t], c4[o + t], acc);
+                m4[o] = acc;
             }
         }
 #pragma unroll
         for (int o = 0; o < kO; ++o) {
             const int gy = y0 + r0 + o;
             if (gx >= W || gy >= keep) continue;
-            const float mx = m[0][o], my = m[1][o];
-            const float var_x = m[2][o] - mx * mx, var_y = m[3][o] - my * my, cov = m[4][o] - mx * my;
+            const float mx = m01[o].x, my = m01[o].y;
+            const float var_x = m23[o].x - mx * mx, var_y = m23[o].y - my * my, cov = m4[o] - mx * my;
             const float a1 = 2.0f * mx * my + C1, a2 = 2.0f * cov + C2;
             const float b1 = mx * mx + my * my + C1, b2 = var_x + var_y + C2;
             // two approximate reciprocals instead of five IEEE divisions (~1 ulp each)
@@ -151,13 +174,19 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_bwd(const float* __restri
                                                            const float* __restrict__ g_planes, float l1_scale,
                                                            float ssim_scale, float* __restrict__ d_image,
                                                            double* __restrict__ abs_sum) {
-    __shared__ float sg[3][kS][kS + 1];
-    __shared__ float h[3][kS][kT + 1];
+    // partial planes 0 and 1 paired in float2 (packed FFMA2), plane 2 scalar
+    __shared__ float2 sg01[kS][kS + 1];
+    __shared__ float sg2[kS][kS + 1];
+    __shared__ float2 h01[kS][kT + 1];
+    __shared__ float h2[kS][kT + 1];
     __shared__ double s_red[kLossThreads / 32];
     const int ch = blockIdx.z;
     const int x0 = blockIdx.x * kT, y0 = blockIdx.y * kT;
     const size_t plane = static_cast<size_t>(W) * H;
     const float* G = g_planes + static_cast<size_t>(ch) * 3 * plane;
+    float w[2 * kR + 1];
+#pragma unroll
+    for (int t = 0; t < 2 * kR + 1; ++t) w[t] = win.w[t];
     if (ssim_scale != 0.0f) {
 #pragma unroll
         for (int k = 0; k < kStageIters; ++k) {
@@ -170,25 +199,31 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_bwd(const float* __restri
 #pragma unroll
             for (int q = 0; q < 3; ++q) g[q] = in ? G[q * plane + p] : 0.0f;
             if (i < kS * kS) {
-#pragma unroll
-                for (int q = 0; q < 3; ++q) sg[q][r][c] = g[q];
+                sg01[r][c] = make_float2(g[0], g[1]);
+                sg2[r][c] = g[2];
             }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < kS * kG; i += kLossThreads) {
             const int r = i % kS, c0 = (i / kS) * kO;
+            float2 row[kO + 2 * kR];
+            float row2[kO + 2 * kR];
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                float row[kO + 2 * kR];
+            for (int j = 0; j < kO + 2 * kR; ++j) {
+                row[j] = sg01[r][c0 + j];
+                row2[j] = sg2[r][c0 + j];
+            }
 #pragma unroll
-                for (int j = 0; j < kO + 2 * kR; ++j) row[j] = sg[q][r][c0 + j];
+            for (int o = 0; o < kO; ++o) {
+                float2 acc = make_float2(0.f, 0.f);
+                float acc2 = 0.f;
 #pragma unroll
-                for (int o = 0; o < kO; ++o) {
-                    float acc = 0.f;
-#pragma unroll
-                    for (int t = 0; t < 2 * kR + 1; ++t) acc = __fmaf_rn(win.w[t], row[o + t], acc);
-                    h[q][r][c0 + o] = acc;
+                for (int t = 0; t < 2 * kR + 1; ++t) {
+                    acc = __ffma2_rn(make_float2(w[t], w[t]), row[o + t], acc);
+                    acc2 = __fmaf_rn(w[t], row2[o + t], acc2);
                 }
+                h01[r][c0 + o] = acc;
+                h2[r][c0 + o] = acc2;
             }
         }
         __syncthreads();
@@ -197,20 +232,27 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_bwd(const float* __restri
     for (int i = threadIdx.x; i < kT * kG; i += kLossThreads) {
         const int c = i % kT, r0 = (i / kT) * kO;
         const int gx = x0 + c;
-        float cv[3][kO];
+        float2 cv01[kO];
+        float cv2[kO];
         if (ssim_scale != 0.0f) {
+            float2 col[kO + 2 * kR];
+            float col2[kO + 2 * kR];
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                float col[kO + 2 * kR];
+            for (int j = 0; j < kO + 2 * kR; ++j) {
+                col[j] = h01[r0 + j][c];
+                col2[j] = h2[r0 + j][c];
+            }
 #pragma unroll
-                for (int j = 0; j < kO + 2 * kR; ++j) col[j] = h[q][r0 + j][c];
+            for (int o = 0; o < kO; ++o) {
+                float2 acc = make_float2(0.f, 0.f);
+                float acc2 = 0.f;
 #pragma unroll
-                for (int o = 0; o < kO; ++o) {
-                    float acc = 0.f;
-#pragma unroll
-                    for (int t = 0; t < 2 * kR + 1; ++t) acc = __fmaf_rn(win.w[t], col[o + t], acc);
-                    cv[q][o] = acc;
+                for (int t = 0; t < 2 * kR + 1; ++t) {
+                    acc = __ffma2_rn(make_float2(w[t], w[t]), col[o + t], acc);
+                    acc2 = __fmaf_rn(w[t], col2[o + t], acc2);
                 }
+                cv01[o] = acc;
+                cv2[o] = acc2;
             }
         }
 #pragma unroll
@@ -224,7 +266,7 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_bwd(const float* __restri
                 const float d = xv - yv;
                 local += fabs(static_cast<double>(d));
                 grad = d > 0.0f ? l1_scale : (d < 0.0f ? -l1_scale : 0.0f);
-                if (ssim_scale != 0.0f) grad -= ssim_scale * (cv[0][o] + 2.0f * xv * cv[1][o] + yv * cv[2][o]);
+                if (ssim_scale != 0.0f) grad -= ssim_scale * (cv01[o].x + 2.0f * xv * cv01[o].y + yv * cv2[o]);
             }
             d_image[p] = grad;
         }
