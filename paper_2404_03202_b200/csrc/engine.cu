@@ -26,12 +26,18 @@ DevBuf::~DevBuf() {
 
 void DevBuf::ensure(size_t bytes) {
     if (bytes <= cap_ && p_) return;
+    const size_t old_cap = p_ ? cap_ : 0;
     if (p_) {
         OSB_CUDA_CHECK(cudaFree(p_));
         p_ = nullptr;
-        cap_ = 0;
     }
+    cap_ = old_cap;
     size_t want = bytes < 256 ? 256 : bytes;
+    // a buffer that has to grow grows by at least 25%: a cloud densified every 100 iterations (or
+    // a frame whose instance count creeps up) reallocates O(log) times instead of at every step
+    // (cudaFree synchronises the device)
+    const size_t grown = cap_ + cap_ / 4;
+    if (cap_ > 0 && want < grown) want = grown;
     want = (want + 255) & ~size_t(255);
     OSB_CUDA_CHECK(cudaMalloc(&p_, want));
     cap_ = want;
@@ -695,7 +701,8 @@ EditSummary Engine::densify_and_prune(const DensifyArgs& a, unsigned long long r
     EditSummary e;
     const int n = static_cast<int>(n_);
     const int bc = (sh_degree_ + 1) * (sh_degree_ + 1);
-    DevBuf code, rank, ws, csrc, ssrc, normals, keep, dest;
+    DevBuf &code = dz_code_, &rank = dz_rank_, &ws = dz_ws_, &csrc = dz_csrc_, &ssrc = dz_ssrc_,
+           &normals = dz_normals_, &keep = dz_keep_, &dest = dz_dest_;  // persistent scratch (no per-call malloc/free)
     int nc = 0, ns = 0;
     if (n > 0) {
         code.ensure(static_cast<size_t>(n) * 8);
@@ -751,7 +758,7 @@ EditSummary Engine::densify_and_prune(const DensifyArgs& a, unsigned long long r
     // gather into new planes (new stride), then swap them in
     const size_t stride2 = ((kept > 0 ? static_cast<size_t>(kept) : 1) + 31) & ~size_t(31);
     const size_t elems2 = static_cast<size_t>(planes_) * stride2;
-    DevBuf P2, M2, V2;
+    DevBuf &P2 = spare_p_, &M2 = spare_m_, &V2 = spare_v_;  // double-buffered planes: the old ones become the spares
     P2.ensure(elems2 * 4);
     M2.ensure(elems2 * 4);
     V2.ensure(elems2 * 4);

@@ -190,6 +190,8 @@ private:
     DevBuf scratch_;
     DevBuf params_, grads_, m_, v_, acc_, d_screen_, norm_sum_, hits_, max_radius_, loss_sum_, d_image_, gt_,
         ssim_planes_;
+    // densify_and_prune scratch and the spare parameter / moment planes it writes into
+    DevBuf dz_code_, dz_rank_, dz_ws_, dz_csrc_, dz_ssrc_, dz_normals_, dz_keep_, dz_dest_, spare_p_, spare_m_, spare_v_;
     void reset_per_gaussian_state();
     void render_into(Frame* f);
     void grow_instances(Frame* f, uint32_t M);  // zero gradients' screen stats, d_screen, max radius (GradientBuffer::resize)
