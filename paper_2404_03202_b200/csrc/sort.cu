@@ -432,14 +432,31 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
     }
 }
 
-__global__ void k_ranges(const uint32_t* __restrict__ keys, int m_cap, const uint32_t* m_dev,
-                         uint2* __restrict__ ranges) {
+// Four sorted keys per thread (one 16-byte load + the two neighbours): a tile's range starts where
+// the key differs from its predecessor and ends where it differs from its successor.
+__global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, int m_cap, const uint32_t* m_dev,
+                                                uint2* __restrict__ ranges) {
     const int m = sort_count(m_cap, m_dev);
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
-    const uint32_t k = keys[i];
-    if (i == 0 || keys[i - 1] != k) ranges[k].x = i;
-    if (i == m - 1 || keys[i + 1] != k) ranges[k].y = i + 1;
+    const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+    if (i0 >= m) return;
+    uint32_t k[6];  // keys[i0 - 1 .. i0 + 4]
+    if (i0 + 4 <= m) {
+        const uint4 v = *reinterpret_cast<const uint4*>(keys + i0);
+        k[1] = v.x; k[2] = v.y; k[3] = v.z; k[4] = v.w;
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) k[1 + q] = i0 + q < m ? keys[i0 + q] : 0xFFFFFFFFu;
+    }
+    k[0] = i0 > 0 ? keys[i0 - 1] : 0xFFFFFFFFu;
+    k[5] = i0 + 4 < m ? keys[i0 + 4] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int i = i0 + q;
+        if (i >= m) break;
+        const uint32_t c = k[1 + q];
+        if (i == 0 || k[q] != c) ranges[c].x = i;
+        if (i == m - 1 || k[2 + q] != c) ranges[c].y = i + 1;
+    }
 }
 
 // Workspace: hist[8][256] | base[8][256] | counts[256][blocks] | offsets[256][blocks]
@@ -534,7 +551,7 @@ void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4
 
 void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s, const uint32_t* m_dev) {
     if (m <= 0) return;
-    k_ranges<<<(m + 255) / 256, 256, 0, s>>>(sorted_tiles, m, m_dev, ranges);
+    k_ranges<<<(m + 1023) / 1024, 256, 0, s>>>(sorted_tiles, m, m_dev, ranges);
     OSB_LAUNCHED(1);
 }
 
