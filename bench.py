@@ -467,6 +467,13 @@ def run_ours(args):
     roof["kernel"] = dominant
     roof["peak_source"] = (f"FP32 issue 148 SMs x 128 lanes x {clk_mhz:.0f} MHz (derived)" if roof.get("bound") ==
                            "fp32" else peaks["source"])
+    if roof.get("bound") == "fp32":
+        roof["model"] = (f"SURVEY.md 8(d): {INSTR_PER_BWD_PAIR} FP32-pipe instructions per backward pair (K4a), "
+                         f"{INSTR_PER_FWD_PAIR} per forward pair (K3), pairs counted on the reference's visit order")
+        roof["note"] = ("frac > 1 means the kernel does less FP32-pipe work than the per-pair model: the 4x4 "
+                        "quarter culling skips modeled pairs outright, K4a's 9 per-Gaussian accumulations per pair "
+                        "are L2 atomics (red.global.add), paired operations issue as FFMA2/FMUL2/FADD2; issue "
+                        "utilisation from ncu is in profiles/ncu_summary_*.txt")
 
     # ---- CPU baseline (rank 0, N == 1): the reference code on this host's cores
     cpu = None
