@@ -401,10 +401,18 @@ def run_ours(args):
         host_gt = {vi: torch.empty(3 * plane, dtype=torch.float32, pin_memory=True) for vi in my_views}
         for vi in my_views:
             host_gt[vi].copy_(gts[vi].cpu())
+        # pinned slots for every step's loss sums: each step's D2H read is enqueued (async), the
+        # host waits once at the end of the timed region and turns every step's sums into its loss
+        sums_host = torch.zeros((max(3 * args.steps, 30) + max(args.warmup, 3) + 8, len(my_views), 4),
+                                dtype=torch.float64, pin_memory=True)
+        losses = []
         def e2e_step():
             it[0] += 1
-            for vi in my_views:
-                ctx.train_view(poses[vi], W, H, host_gt[vi].data_ptr(), gt_on_device=False, lambda_ssim=LAMBDA_SSIM)
+            slot = sums_host[len(losses) % sums_host.shape[0]]
+            for k, vi in enumerate(my_views):
+                ctx.train_view_async(poses[vi], W, H, host_gt[vi].data_ptr(), gt_on_device=False,
+                                     sums_ptr=slot[k].data_ptr(), lambda_ssim=LAMBDA_SSIM)
+            losses.append(slot)
             if world > 1:
                 b0, cnt = dp.shard_range(grads.numel(), rank, world)
                 rs(grads, b0, cnt)
@@ -417,15 +425,23 @@ def run_ours(args):
             e2e_step()
         barrier()
         e2e_steps = max(3 * args.steps, 30)  # wall clock: enough steps to average out host jitter
+        ctx.synchronize()
+        losses.clear()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             e2e_step()
+        ctx.synchronize()  # every step's loss sums are on the host now
+        step_losses = [sum(native.loss_value(slot[k].numpy(), LAMBDA_SSIM, W, H) for k in range(len(my_views)))
+                       for slot in losses]
         barrier()
         e2e_s = max_over_ranks(time.perf_counter() - t0)
+        assert all(np.isfinite(step_losses)), "non-finite loss in the e2e run"
         e2e = {"value": world * V * e2e_steps / e2e_s, "unit": "views/s", "steps": e2e_steps,
-               "h2d_bytes_per_step": V * 3 * plane * 4, "d2h_bytes_per_step": V * 8,
-               "api": "osplat_gpu_train_view (pinned host target in, loss out) + osplat_gpu_adam_step "
-                      "(N > 1: NCCL reduce-scatter + osplat_gpu_adam_step_range + all-gather)"}
+               "h2d_bytes_per_step": V * 3 * plane * 4, "d2h_bytes_per_step": V * 32,
+               "loss_first_last": [step_losses[0], step_losses[-1]],
+               "api": "osplat_gpu_train_view_async (pinned host target in, loss sums out to pinned host every "
+                      "step, one wait at the end) + osplat_gpu_adam_step (N > 1: NCCL reduce-scatter + "
+                      "osplat_gpu_adam_step_range + all-gather)"}
         if rank == 0:
             hc = native.HostCloud.from_cloud(cloud)
             native.osplat_render(hc, poses[0], W, H)  # upload + warm

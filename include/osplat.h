@@ -217,6 +217,18 @@ OSPLAT_API osplat_status osplat_gpu_l1_loss(osplat_gpu* ctx, const osplat_frame*
 OSPLAT_API osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
                                     const float* gt_planar, int gt_on_device, double lambda_ssim,
                                     double mask_bottom_fraction, double* loss);
+/* osplat_gpu_train_view without the per-step wait: every kernel and copy of the step is enqueued on
+ * the context's stream and the call returns. loss_sums (4 doubles, pinned host memory; may be NULL)
+ * receives {L1 sum, SSIM sums r, g, b} once the stream reaches the end of the step — read them after
+ * osplat_gpu_synchronize and turn them into the loss with osplat_loss_value. A pipelined training
+ * loop (loss logged one step late) keeps the GPU busy while the host enqueues the next view. */
+OSPLAT_API osplat_status osplat_gpu_train_view_async(osplat_gpu* ctx, const double transform_cw[16], int width,
+                                                     int height, const float* gt, int gt_on_device,
+                                                     double lambda_ssim, double mask_bottom_fraction,
+                                                     double* loss_sums);
+/* (1 - l) L1 + l (1 - SSIM) from the sums of osplat_gpu_train_view_async (trainer.cpp:54-63). */
+OSPLAT_API double osplat_loss_value(const double sums[4], double lambda_ssim, int width, int height,
+                                    double mask_bottom_fraction);
 
 /* ---- densification control (trainer.cpp:180-280) ---- */
 /* EditSummary (trainer.hpp:93-98). */

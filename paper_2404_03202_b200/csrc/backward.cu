@@ -133,17 +133,14 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
         const uint32_t bal0 = __ballot_sync(0xffffffffu, (mk >> (2 * warp)) & 1u);
         const uint32_t bal1 = __ballot_sync(0xffffffffu, (mk >> (2 * warp + 1)) & 1u);
         uint32_t bal = wp.half ? bal1 : bal0;
-        {  // only the entries in front of this pixel's last contributor: j < last - sbase
-            const int lim = last - sbase;
-            bal &= lim >= 32 ? 0xFFFFFFFFu : (lim <= 0 ? 0u : (1u << lim) - 1u);
-        }
         while (__any_sync(0xffffffffu, bal != 0u)) {  // back to front; warp-uniform (the reduction needs all lanes)
             const bool live = bal != 0u;
             const int j = live ? 31 - __clz(bal) : 0;
             bal &= ~(1u << j);
+            const int k = sbase + j;
             float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f, v5 = 0.f, v6 = 0.f, v7 = 0.f, v8 = 0.f;
             bool has = false;
-            if (live) {
+            if (live && k < last) {
                 const float4 A = ws.a[j];
                 const float4 B = ws.b[j];
                 float2 d;

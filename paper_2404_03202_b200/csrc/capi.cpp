@@ -1171,9 +1171,37 @@ osplat_status osplat_gpu_l1_loss(osplat_gpu* ctx, const osplat_frame* frame, con
     return osplat_gpu_loss(ctx, frame, gt, 0.0, mask, d_image, loss);
 }
 
+namespace {
+osplat_status train_view_impl(osplat_gpu* ctx, const double transform_cw[16], int width, int height, const float* gt,
+                              int gt_on_device, double lambda_ssim, double mask, double* loss, double* sums_pinned);
+}
+
 osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
                                     const float* gt, int gt_on_device, double lambda_ssim, double mask,
                                     double* loss) {
+    return train_view_impl(ctx, transform_cw, width, height, gt, gt_on_device, lambda_ssim, mask, loss, nullptr);
+}
+
+osplat_status osplat_gpu_train_view_async(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
+                                          const float* gt, int gt_on_device, double lambda_ssim, double mask,
+                                          double* loss_sums) {
+    return train_view_impl(ctx, transform_cw, width, height, gt, gt_on_device, lambda_ssim, mask, nullptr,
+                           loss_sums ? loss_sums : nullptr);
+}
+
+double osplat_loss_value(const double sums[4], double lambda_ssim, int width, int height, double mask) {
+    // trainer.cpp:54-63, as Engine::loss_value
+    const int masked = static_cast<int>(std::floor(mask * height));
+    const double npx = static_cast<double>(width) * (height - masked);
+    const double n = npx * 3.0;
+    double value = (1.0 - lambda_ssim) * (sums[0] / n);
+    if (lambda_ssim > 0.0) value += lambda_ssim * (1.0 - ((sums[1] + sums[2] + sums[3]) / npx) / 3.0);
+    return value;
+}
+
+namespace {
+osplat_status train_view_impl(osplat_gpu* ctx, const double transform_cw[16], int width, int height, const float* gt,
+                              int gt_on_device, double lambda_ssim, double mask, double* loss, double* sums_pinned) {
     if (!ctx || !transform_cw || !gt) return invalid("osplat_gpu_train_view: null argument");
     if (lambda_ssim < 0.0 || lambda_ssim > 1.0) return invalid("osplat_gpu_train_view: lambda_ssim must be in [0, 1]");
     if (mask < 0.0 || mask >= 1.0) return invalid("osplat_gpu_train_view: mask_bottom_fraction must be in [0, 1)");
@@ -1199,6 +1227,7 @@ osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[1
                 // the L1 sum lives on the device; one 8-byte read completes the step
                 *loss = e.loss_value(f, mask);
             }
+            if (sums_pinned) e.loss_sums_async(sums_pinned);  // no wait: read after osplat_gpu_synchronize
         } catch (...) {
             e.release(f);
             throw;
@@ -1206,6 +1235,7 @@ osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[1
         e.release(f);
     });
 }
+}  // namespace
 
 osplat_status osplat_gpu_profile(osplat_gpu* ctx, int timing, int count_work) {
     if (!ctx) return invalid("osplat_gpu_profile: null context");

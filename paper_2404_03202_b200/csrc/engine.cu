@@ -629,6 +629,11 @@ double Engine::loss_value(const Frame* f, double mask_bottom_fraction) {
     return value;
 }
 
+void Engine::loss_sums_async(double* host) {
+    DeviceGuard g(device_);
+    OSB_CUDA_CHECK(cudaMemcpyAsync(host, loss_sum_.as<double>(), 32, cudaMemcpyDeviceToHost, stream_));
+}
+
 void Engine::adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad, size_t begin,
                        size_t count) {
     DeviceGuard g(device_);

@@ -125,6 +125,9 @@ public:
     double loss(Frame* f, const float* gt_planar_dev, double lambda_ssim, double mask_bottom_fraction,
                 bool want_value);
     double loss_value(const Frame* f, double mask_bottom_fraction);
+    // Enqueue a copy of the loss sums {L1, SSIM r, g, b} into host memory (pinned, or the copy is
+    // synchronous); valid once the stream has reached this point.
+    void loss_sums_async(double* host);
     // Adam over all planes, or over the flat element range [begin, begin + count) (multiples of 4;
     // a data-parallel rank's shard after a reduce-scatter of the gradients).
     void adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad, size_t begin = 0,

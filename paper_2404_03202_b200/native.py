@@ -129,6 +129,9 @@ def _load():
         "osplat_frame_work": (S, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
         "osplat_frame_splats": (S, [_vp, C.POINTER(C.c_size_t), _i32p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp]),
         "osplat_gpu_upload": (S, [_vp, _vp]),
+        "osplat_gpu_train_view_async": (S, [_vp, _dp, C.c_int, C.c_int, _vp, C.c_int, C.c_double, C.c_double,
+                                            C.c_void_p]),
+        "osplat_loss_value": (C.c_double, [_dp, C.c_double, C.c_int, C.c_int, C.c_double]),
         "osplat_gpu_render_projected": (S, [_vp, C.c_size_t, _i32p, _dp, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int,
                                             C.c_int, _dp, _u32p, _i32p, C.POINTER(_vp)]),
     }
@@ -158,6 +161,12 @@ def check(status: int):
 
 def _p(a, t=_dp):
     return a.ctypes.data_as(t)
+
+
+def loss_value(sums, lambda_ssim: float, width: int, height: int, mask: float = 0.0) -> float:
+    """osplat_loss_value: the loss from osplat_gpu_train_view_async's sums."""
+    a = np.ascontiguousarray(sums, dtype=np.float64)
+    return float(lib.osplat_loss_value(_p(a), lambda_ssim, width, height, mask))
 
 
 def version() -> str:
@@ -455,6 +464,16 @@ class Context:
         ptr = C.c_void_p(gt) if isinstance(gt, int) else gt.ctypes.data_as(C.c_void_p)
         check(lib.osplat_gpu_train_view(self.handle, _p(t), width, height, ptr, int(gt_on_device), lambda_ssim, mask,
                                         None))
+
+    def train_view_async(self, pose12, width: int, height: int, gt, gt_on_device: bool, sums_ptr: int | None,
+                         lambda_ssim: float = 0.2, mask: float = 0.0):
+        """osplat_gpu_train_view_async: the step is enqueued, nothing waited for; the 4 loss sums land
+        at sums_ptr (pinned host memory) once the stream gets there (osplat_loss_value turns them
+        into the loss after synchronize())."""
+        t = transform_of(pose12)
+        ptr = C.c_void_p(gt) if isinstance(gt, int) else gt.ctypes.data_as(C.c_void_p)
+        check(lib.osplat_gpu_train_view_async(self.handle, _p(t), width, height, ptr, int(gt_on_device), lambda_ssim,
+                                              mask, None if sums_ptr is None else C.c_void_p(sums_ptr)))
 
     def profile(self, timing: bool = True, count_work: bool = False):
         check(lib.osplat_gpu_profile(self.handle, int(timing), int(count_work)))

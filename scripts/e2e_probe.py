@@ -47,7 +47,31 @@ def main():
         ms = (time.perf_counter() - t0) / steps * 1e3
         print(f"{label:40s} {ms:7.3f} ms/step", flush=True)
 
-    run("host target + loss read-back", 20, host.data_ptr(), False, True)
+    run("host target + loss read-back", 40, host.data_ptr(), False, True)
+    sums = torch.zeros(4, dtype=torch.float64, pin_memory=True)
+
+    def run_async(label, steps, gt_ptr, on_device):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for it in range(steps):
+            ctx.train_view_async(poses[0], W, H, gt_ptr, on_device, sums.data_ptr(), 0.2)
+            ctx.adam_step(cfg, 1.0, it + 1, zero_grad=True)
+        ctx.synchronize()
+        ms = (time.perf_counter() - t0) / steps * 1e3
+        print(f"{label:40s} {ms:7.3f} ms/step", flush=True)
+
+    run_async("async: host target", 40, host.data_ptr(), False)
+    run_async("async: device target", 40, gt.data_ptr(), True)
+    # device time of the same step (CUDA events around 40 async steps)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for it in range(40):
+        ctx.train_view_async(poses[0], W, H, gt.data_ptr(), True, sums.data_ptr(), 0.2)
+        ctx.adam_step(cfg, 1.0, it + 1, zero_grad=True)
+    ev1.record(stream)
+    ev1.synchronize()
+    print(f"{'async device target, CUDA events':40s} {ev0.elapsed_time(ev1) / 40:7.3f} ms/step", flush=True)
     run("host target, no read-back", 20, host.data_ptr(), False, False)
     run("device target + loss read-back", 20, gt.data_ptr(), True, True)
     run("device target, no read-back", 20, gt.data_ptr(), True, False)

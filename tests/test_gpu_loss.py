@@ -38,3 +38,25 @@ class _Dev:
     def __init__(self, ptr, n):
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False), "version": 3,
                                          "strides": None}
+
+
+def test_train_view_async_matches_sync():
+    """osplat_gpu_train_view_async enqueues the step without waiting; its loss sums (pinned host)
+    give the same loss as the synchronous osplat_gpu_train_view, and the accumulated gradients agree."""
+    import torch
+    W, H = 256, 128
+    cloud = scenes.synthetic_cloud(4000, seed=5)
+    gt32, _, _, _ = native.Context(scenes.synthetic_cloud(4000, seed=6)).render(scenes.identity_pose(), W, H).pixels()
+    gt = np.ascontiguousarray(gt32.transpose(2, 0, 1))
+    pose = scenes.ring_poses(4, seed=2)[1]
+    a, b = native.Context(cloud), native.Context(cloud)
+    la = a.train_view(pose, W, H, gt, gt_on_device=False, lambda_ssim=0.2, mask=0.1)
+    sums = torch.zeros(4, dtype=torch.float64, pin_memory=True)
+    b.train_view_async(pose, W, H, gt, gt_on_device=False, sums_ptr=sums.data_ptr(), lambda_ssim=0.2, mask=0.1)
+    b.synchronize()
+    lb = native.loss_value(sums.numpy(), 0.2, W, H, 0.1)
+    assert abs(la - lb) <= 1e-12 * abs(la), (la, lb)
+    ga, gb = a.gradients(), b.gradients()
+    for k in ("d_position", "d_sh", "d_opacity_logit"):
+        scale = np.max(np.abs(ga[k]))
+        assert np.max(np.abs(ga[k] - gb[k])) <= 1e-4 * scale, k
