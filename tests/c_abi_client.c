@@ -66,6 +66,14 @@ int main(int argc, char** argv) {
         CHECK(osplat_gpu_adam_step(ctx, cfg, 1.0, 1, 1));
         printf("loss %.6f launches %lld\n", loss, osplat_gpu_launch_count());
         if (!(loss > 0.0)) return 6;
+        /* the pipelined variant: sums arrive after a synchronize (pageable memory here: the copy is
+         * then synchronous, which is allowed) */
+        double sums[4] = {0, 0, 0, 0};
+        CHECK(osplat_gpu_train_view_async(ctx, T, 128, 64, target, 0, 0.2, 0.0, sums));
+        CHECK(osplat_gpu_synchronize(ctx));
+        const double loss2 = osplat_loss_value(sums, 0.2, 128, 64, 0.0);
+        printf("async loss %.6f\n", loss2);
+        if (!(loss2 > 0.0)) return 7;
         free(target);
         osplat_gpu_free(ctx);
     }
