@@ -2,11 +2,13 @@
 //
 // Tile layout: one 256-thread CTA per 16x16 tile, one pixel per thread; warp w owns the 8x4 pixel
 // block at columns 8(w&1)..+7, rows 4(w>>1)..+3, and each half-warp one 4x4 quarter of it (small
-// square blocks are touched by far fewer splats than 16-pixel strips of the same area). Warps are independent (no CTA barrier): each warp walks its tile's list in chunks
-// of 32 entries, stages a chunk lane-parallel into its own shared-memory slots, keeps (ballot) the
-// entries whose conservative alpha >= 1/255 extent (Splat32::ext_x/ext_y) reaches each half-warp's
-// 4x4 block (two ballots), and each half evaluates only its own — entries outside are certain skips of the FP32 classifier below, so
-// no decision changes. A warp stops as soon as its 32 pixels have terminated.
+// square blocks are touched by far fewer splats than 16-pixel strips of the same area). The CTA
+// walks its tile's list 256 entries at a time: every thread stages one entry into shared memory
+// (stage_record16) with a 16-bit mask of the quarters its conservative alpha >= 1/255 extent
+// (Splat32::ext_x/ext_y) reaches; after one barrier every warp walks the staged entries, each
+// half-warp only those whose bit for its quarter is set (ballots) — entries outside are certain
+// skips of the FP32 classifier below, so no decision changes. K3 walks front to back and stops when
+// every pixel has terminated; K4a walks back to front from each warp's furthest last_contrib.
 //
 // Staged record per entry (3 x float4, broadcast reads):
 //   A = {cx, cy, ha, hc}   centre offset from the tile centre (FP64 -> FP32, seam-wrapped), 0.5 conic
@@ -122,54 +124,11 @@ __device__ __forceinline__ uint32_t stage_record16(WarpStage& ws, int lane, uint
     return quarter_mask(make_float4(cx, cy, 0.0f, 0.0f), s2.y, s2.z, seam);
 }
 
-__device__ __forceinline__ uint32_t stage_entry(WarpStage& ws, int lane, uint32_t gid, const double2* __restrict__ pxy,
-                                            const Splat32* __restrict__ splat, double xc, double yc, double width,
-                                            float r0, float c0) {
-    const double2 pp = pxy[gid];
-    const float4* s4 = reinterpret_cast<const float4*>(splat + gid);
-    const float4 s0 = s4[0], s1 = s4[1], s2 = s4[2];  // {ha,b,hc,o} {r,g,bl,pthr} {dl,ext_x,ext_y,-}
-    // remainder(p.x - xc, W): the offset lies in (-W, W), where the IEEE remainder is one exact
-    // (Sterbenz) add/subtract of W, with ties at +-W/2 left unwrapped
-    double w0 = pp.x - xc;
-    const double half = 0.5 * width;
-    if (w0 > half) w0 -= width;
-    else if (w0 < -half) w0 += width;
-    const bool seam = fabs(w0) > half - 8.5;
-    const float cx = static_cast<float>(w0), cy = static_cast<float>(pp.y - yc);
-    const float dl = s2.x;
-    ws.a[lane] = make_float4(cx, cy, s0.x, s0.z);
-    ws.b[lane] = make_float4(s0.y, s1.w - dl, s1.w + dl, seam ? -dl : dl);
-    ws.c[lane] = make_float4(s1.x, s1.y, s1.z, s0.w);
-    ws.gid[lane] = gid;
-    if (!(cy - s2.z <= r0 + 3.0f && cy + s2.z >= r0)) return 0u;
-    if (seam) return 3u;
-    const float lo = cx - s2.y, hi = cx + s2.y;
-    return (lo <= c0 + 3.0f && hi >= c0 ? 1u : 0u) | (lo <= c0 + 7.0f && hi >= c0 + 4.0f ? 2u : 0u);
-}
-
-// FP32 power for one pair. Returns false for a certain skip. `unc` is set when the FP32 result
-// is within the guard band of a threshold (power < 0, alpha < 1/255) or of the seam wrap tie.
-__device__ __forceinline__ bool pair_power(const float4 A, const float4 B, float lxo, float lyo, float halfW,
-                                           float fW, float& dx, float& dy, float& power, bool& unc) {
-    dx = A.x - lxo;
-    dy = A.y - lyo;
-    unc = false;
-    if (B.w < 0.0f) {
-        if (dx > halfW) dx -= fW;
-        else if (dx < -halfW) dx += fW;
-        unc = fabsf(fabsf(dx) - halfW) < 0.01f;
-    }
-    const float bdx = B.x * dx;
-    power = __fmaf_rn(A.z * dx, dx, __fmaf_rn(A.w * dy, dy, bdx * dy));
-    if (!(power <= B.z) && !unc) return false;
-    const float dl = fabsf(B.w);
-    unc = unc || power < dl || power > B.y;
-    return true;
-}
-
-// pair_power with the paired FP32 operations issued as packed f32x2 instructions (FADD2 / FMUL2:
-// half the issue slots, each half rounded exactly like the scalar op, so every value and decision
-// is bit-identical to pair_power). nlo = (-lxo, -lyo).
+// FP32 power for one pair (pixel centre offset (lxo, lyo) from the tile centre; nlo = (-lxo, -lyo)).
+// Returns false for a certain skip; `unc` is set when the FP32 result is within the guard band of a
+// threshold (power < 0, alpha < 1/255) or of the seam wrap tie. The paired operations issue as
+// packed f32x2 instructions (FADD2 / FMUL2: half the issue slots, each half rounded exactly like the
+// scalar op), and K3 and K4a run exactly this code, so the backward replays the forward's decisions.
 __device__ __forceinline__ bool pair_power2(const float4 A, const float4 B, float2 nlo, float halfW, float fW,
                                             float2& d, float& power, bool& unc) {
     d = __fadd2_rn(make_float2(A.x, A.y), nlo);  // (A.x - lxo, A.y - lyo)
@@ -204,20 +163,6 @@ static __device__ __noinline__ int pair_slow(uint32_t gid, int px, int py, doubl
     out->g = g;
     out->og = co.w * g;
     return 1;
-}
-
-// FP64 transmittance in front of list position `k` (exclusive), replaying the reference blend
-// (rasterizer.cpp:126-141) over list[lo, k).
-static __device__ __noinline__ double replay_T(const uint32_t* __restrict__ inst_gid, uint32_t lo, uint32_t k,
-                                               int px, int py, double width, const double2* __restrict__ pxy,
-                                               const double4* __restrict__ conic_o) {
-    double t = 1.0;
-    for (uint32_t i = lo; i < k; ++i) {
-        Pair64 p;
-        if (!pair_slow(inst_gid[i], px, py, width, pxy, conic_o, &p)) continue;
-        t = t * (1.0 - p.alpha);
-    }
-    return t;
 }
 
 // replay_T done by the whole warp for one pixel (px, py): lane l evaluates entries lo + 32 r + l in
