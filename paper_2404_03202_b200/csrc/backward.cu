@@ -242,12 +242,15 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
 }
 
 // Gradient plane update: OVERWRITE (the buffer is logically zero: first view after Adam or a
-// non-accumulating backward) stores, otherwise read-modify-write (multi-view accumulation).
+// non-accumulating backward) stores, otherwise adds (multi-view accumulation) with a
+// fire-and-forget red.global.add: one thread owns each element within a launch, so the sum is the
+// same single FP32 add as a read-modify-write, without 59 load -> store round trips in series (the
+// compiler cannot prove the planes distinct and would serialise them).
 template <bool OVERWRITE, typename R>
 __device__ __forceinline__ void put_grad(float* __restrict__ G, int stride, int plane, int gid, R v) {
     float* p = G + static_cast<size_t>(plane) * stride + gid;
     if (OVERWRITE) *p = static_cast<float>(v);
-    else *p = *p + static_cast<float>(v);
+    else red_add(p, static_cast<float>(v));
 }
 
 // One SH basis function of the backward (gradients.cpp:202-207): d_sh_i = dl_color * b_i and

@@ -187,7 +187,8 @@ def test_accumulate_and_logical_zero():
     gab = ctx.gradients()
     for k in ("d_position", "d_sh", "d_rotation", "d_log_scale", "d_opacity_logit"):
         ref = ga[k] + gb[k]
-        assert np.allclose(gab[k], ref, rtol=1e-5, atol=1e-7 * np.max(np.abs(ref))), k
+        # each backward is recomputed: K4a's FP32 atomics reorder its sums run to run
+        assert np.allclose(gab[k], ref, rtol=1e-4, atol=1e-6 * np.max(np.abs(ref))), k
     ctx.adam_step(native.Config(), 1.0, 1, zero_grad=True)
     fa.free()
     fa = ctx.render(pa, W, H)
