@@ -118,3 +118,33 @@ def test_projected_frame_has_no_backward():
     bad = dict(s, depth=np.full(10, -1.0))
     with pytest.raises(native.OsplatError):
         ctx.render_projected(bad, 64, 32)
+
+
+def test_render_projected_edge_records(oracle_port):
+    """Records the reference bins but never blends (alpha_base < 1/255), records at and across the
+    seam (centre outside [0, W)), a full-width record (span >= tiles_x), equal (depth, id) pairs, and
+    a zero-radius record: tile lists and pixels as bin_to_tiles + blend_forward give them."""
+    W, H = 128, 64
+    s = random_splats(40, W, H, 31)
+    s["alpha_base"][:5] = 1.0 / 300.0                 # below 1/255: binned, never blended
+    s["p"][5] = (-0.75, 20.0)                          # left of the seam
+    s["p"][6] = (W + 0.3, 40.0)                        # right of the seam
+    s["p"][7] = (W * 0.5, 3.0)
+    s["radius"][7] = 3.0 * W                           # wider than the image: whole rows
+    s["depth"][8] = s["depth"][9]
+    s["gaussian_id"][8] = s["gaussian_id"][9]          # full (depth, id) tie: any order is the reference's
+    s["radius"][10] = 0.0
+    ctx = native.Context(scenes.synthetic_cloud(1, seed=0))
+    of = oracle_port.blend_projections(s, W, H)
+    fr = ctx.render_projected(s, W, H)
+    tx, ty, ranges, ids = fr.tiles()
+    for t in range(tx * ty):
+        g = ids[ranges[t, 0]:ranges[t, 1]]
+        o = of.items[of.offsets[t]:of.offsets[t + 1]]
+        assert len(g) == len(o), t
+        # equal (depth, id) records may come in either order; everything else matches exactly
+        key = lambda i: (s["depth"][i], s["gaussian_id"][i])
+        assert [key(i) for i in g] == [key(i) for i in o], t
+    rgb, T, con, last = fr.pixels()
+    assert np.array_equal(con, of.contributors) and np.array_equal(last, of.last_contrib)
+    assert np.max(np.abs(fr.image() - of.rgb)) <= IMAGE_ATOL
