@@ -447,11 +447,15 @@ def run_ours(args):
             native.osplat_render(hc, poses[0], W, H)  # upload + warm
             t0 = time.perf_counter()
             nf = max(3, min(args.steps, 10))
+            checks = []
             for k in range(nf):
-                native.osplat_render(hc, poses[k % 16], W, H)
+                with native.osplat_image(hc, poses[k % 16], W, H) as px:  # osplat_render .. osplat_image_free
+                    checks.append(float(px[H // 2, ::64].sum()))  # read the host image
             render_e2e = {"value": nf / (time.perf_counter() - t0), "unit": "FPS",
-                          "api": "osplat_render (reference C ABI: host cloud -> host H x W x 3 double image)",
-                          "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 3 * plane * 4}
+                          "api": "osplat_render + osplat_image_pixels + osplat_image_free (reference C ABI: host "
+                                 "cloud -> host H x W x 3 double image)",
+                          "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 3 * plane * 8}
+            assert all(np.isfinite(checks))
 
     # ---- roofline of the dominant kernel family in the timed train steps
     clk_mhz = peaks["sm_max_mhz"]

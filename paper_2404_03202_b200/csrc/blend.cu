@@ -206,6 +206,25 @@ __global__ void k_work_count(const int* __restrict__ visited, const int* __restr
 
 }  // namespace
 
+namespace {
+__global__ void __launch_bounds__(256) k_planar_to_hwc_f64(const float* __restrict__ rgb, size_t plane,
+                                                           double* __restrict__ out) {
+    for (size_t i = blockIdx.x * 256ull + threadIdx.x; i < plane; i += static_cast<size_t>(gridDim.x) * 256ull) {
+        out[3 * i] = rgb[i];
+        out[3 * i + 1] = rgb[plane + i];
+        out[3 * i + 2] = rgb[2 * plane + i];
+    }
+}
+}  // namespace
+
+void launch_planar_to_hwc_f64(const float* rgb, size_t plane, double* out, cudaStream_t s) {
+    if (plane == 0) return;
+    size_t blocks = (plane + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_planar_to_hwc_f64<<<static_cast<int>(blocks), 256, 0, s>>>(rgb, plane, out);
+    OSB_LAUNCHED(1);
+}
+
 void launch_work_count(const FrameBuffers& fb, int pixels, unsigned long long* out, cudaStream_t s) {
     OSB_CUDA_CHECK(cudaMemsetAsync(out, 0, 16, s));
     if (pixels <= 0 || !fb.visited) return;

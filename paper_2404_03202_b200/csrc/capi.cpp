@@ -11,6 +11,7 @@
 #include <filesystem>
 #include <fstream>
 #include <memory>
+#include <mutex>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -26,10 +27,55 @@ struct osplat_cloud {
     HostCloud cloud;
     mutable std::shared_ptr<Engine> render_cache;  // device copy used by osplat_render
 };
+// H x W x 3 doubles. Images from osplat_render live in page-locked buffers recycled through a
+// small pool (no page faults, full-speed D2H); images built from host data use the heap.
 struct osplat_image {
     int width = 0, height = 0;
     std::vector<double> data;
+    double* pinned = nullptr;
+    size_t pinned_bytes = 0;
+    const double* px() const { return pinned ? pinned : data.data(); }
+    ~osplat_image();
 };
+
+namespace {
+struct PinnedPool {
+    std::mutex mu;
+    std::vector<std::pair<void*, size_t>> free;
+};
+PinnedPool& pinned_pool() {
+    static PinnedPool* p = new PinnedPool;  // never destroyed: buffers may be freed after main returns
+    return *p;
+}
+double* pinned_acquire(size_t bytes) {
+    PinnedPool& pool = pinned_pool();
+    {
+        std::lock_guard<std::mutex> lock(pool.mu);
+        for (size_t i = 0; i < pool.free.size(); ++i)
+            if (pool.free[i].second == bytes) {
+                void* p = pool.free[i].first;
+                pool.free.erase(pool.free.begin() + static_cast<long>(i));
+                return static_cast<double*>(p);
+            }
+    }
+    void* p = nullptr;
+    OSB_CUDA_CHECK(cudaMallocHost(&p, bytes));
+    return static_cast<double*>(p);
+}
+void pinned_release(void* p, size_t bytes) {
+    PinnedPool& pool = pinned_pool();
+    std::lock_guard<std::mutex> lock(pool.mu);
+    if (pool.free.size() < 4) {
+        pool.free.emplace_back(p, bytes);
+        return;
+    }
+    cudaFreeHost(p);
+}
+}  // namespace
+
+osplat_image::~osplat_image() {
+    if (pinned) pinned_release(pinned, pinned_bytes);
+}
 struct osplat_config {
     // TrainConfig (trainer.hpp:19-51) with the reference defaults
     double lambda_ssim = 0.2;
@@ -349,13 +395,6 @@ void check_dims(int w, int h) {
     if (static_cast<long long>(w) * h > (1ll << 30)) throw ApiError(Code::InvalidArgument, "image too large");
 }
 
-// planar FP32 (3 x H*W) -> interleaved H x W x 3 double
-void planar_to_hwc(const std::vector<float>& planar, int w, int h, double* out) {
-    const size_t plane = static_cast<size_t>(w) * h;
-    for (size_t i = 0; i < plane; ++i)
-        for (int c = 0; c < 3; ++c) out[i * 3 + c] = planar[c * plane + i];
-}
-
 osb::TrainSettings settings_from(const osplat_config* c) {
     const osplat_config d{};
     if (!c) c = &d;
@@ -508,31 +547,27 @@ osplat_status osplat_render(const osplat_cloud* cloud, const double transform_cw
         }
         Engine& e = *cloud->render_cache;
         const double bg[3] = {0.0, 0.0, 0.0};
-        osb::Frame* f = e.render(p12, width, height, bg);
         const size_t plane = static_cast<size_t>(width) * height;
-        std::vector<float> host(plane * 3);
+        auto img = std::make_unique<osplat_image>();
+        img->width = width;
+        img->height = height;
+        img->pinned_bytes = plane * 3 * sizeof(double);
+        img->pinned = pinned_acquire(img->pinned_bytes);
+        osb::Frame* f = e.render(p12, width, height, bg);
         try {
-            e.validate(f);
-            OSB_CUDA_CHECK(cudaMemcpyAsync(host.data(), f->rgb.as<float>(), plane * 12, cudaMemcpyDeviceToHost,
-                                           e.stream()));
-            OSB_CUDA_CHECK(cudaStreamSynchronize(e.stream()));
+            e.image_hwc(f, img->pinned);  // FP32 planes -> H x W x 3 doubles on the device, one D2H
         } catch (...) {
             e.release(f);
             throw;
         }
         e.release(f);
-        auto img = std::make_unique<osplat_image>();
-        img->width = width;
-        img->height = height;
-        img->data.resize(plane * 3);
-        planar_to_hwc(host, width, height, img->data.data());
         *out = img.release();
     });
 }
 
 int osplat_image_width(const osplat_image* image) { return image ? image->width : 0; }
 int osplat_image_height(const osplat_image* image) { return image ? image->height : 0; }
-const double* osplat_image_pixels(const osplat_image* image) { return image ? image->data.data() : nullptr; }
+const double* osplat_image_pixels(const osplat_image* image) { return image ? image->px() : nullptr; }
 void osplat_image_free(osplat_image* image) { delete image; }
 
 // ------------------------------------------------------------------ device-resident extension
@@ -592,15 +627,7 @@ int osplat_frame_height(const osplat_frame* f) { return f ? f->frame->H : 0; }
 osplat_status osplat_frame_image(const osplat_frame* frame, double* rgb) {
     if (!frame || !rgb) return invalid("osplat_frame_image: null argument");
     return wrap([&] {
-        frame->engine->validate(frame->frame);
-        const osb::Frame& f = *frame->frame;
-        osb::DeviceGuard g(frame->engine->device());
-        const size_t plane = static_cast<size_t>(f.W) * f.H;
-        std::vector<float> host(plane * 3);
-        OSB_CUDA_CHECK(cudaMemcpyAsync(host.data(), f.rgb.as<float>(), plane * 12, cudaMemcpyDeviceToHost,
-                                       frame->engine->stream()));
-        OSB_CUDA_CHECK(cudaStreamSynchronize(frame->engine->stream()));
-        planar_to_hwc(host, f.W, f.H, rgb);
+        frame->engine->image_hwc(frame->frame, rgb);
     });
 }
 
@@ -1098,7 +1125,7 @@ osplat_status osplat_gpu_train(osplat_gpu* ctx, const osplat_config* config, siz
                 throw ApiError(Code::DimensionMismatch, "training images differ in size");
             float* dst = planar.data() + v * 3 * plane;
             for (size_t i = 0; i < plane; ++i)
-                for (int c = 0; c < 3; ++c) dst[c * plane + i] = static_cast<float>(im->data[3 * i + c]);
+                for (int c = 0; c < 3; ++c) dst[c * plane + i] = static_cast<float>(im->px()[3 * i + c]);
             (is_test && is_test[v] ? test : train).push_back(static_cast<int>(v));
         }
         double extent = scene_extent;

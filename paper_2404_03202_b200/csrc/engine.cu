@@ -629,6 +629,17 @@ double Engine::loss_value(const Frame* f, double mask_bottom_fraction) {
     return value;
 }
 
+void Engine::image_hwc(Frame* f, double* host) {
+    DeviceGuard g(device_);
+    validate(f);
+    const size_t plane = static_cast<size_t>(f->W) * f->H;
+    hwc_.ensure(plane * 3 * sizeof(double));
+    launch_planar_to_hwc_f64(f->rgb.as<float>(), plane, hwc_.as<double>(), stream_);
+    OSB_CUDA_CHECK(cudaMemcpyAsync(host, hwc_.as<double>(), plane * 3 * sizeof(double), cudaMemcpyDeviceToHost,
+                                   stream_));
+    OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
+}
+
 void Engine::loss_sums_async(double* host) {
     DeviceGuard g(device_);
     OSB_CUDA_CHECK(cudaMemcpyAsync(host, loss_sum_.as<double>(), 32, cudaMemcpyDeviceToHost, stream_));

@@ -128,6 +128,9 @@ public:
     // Enqueue a copy of the loss sums {L1, SSIM r, g, b} into host memory (pinned, or the copy is
     // synchronous); valid once the stream has reached this point.
     void loss_sums_async(double* host);
+    // The frame's colour as H x W x 3 doubles (Image layout, image.hpp:10-23) in host memory:
+    // converted on the device, one D2H copy (full speed into pinned memory), synchronous.
+    void image_hwc(Frame* f, double* host);
     // Adam over all planes, or over the flat element range [begin, begin + count) (multiples of 4;
     // a data-parallel rank's shard after a reduce-scatter of the gradients).
     void adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad, size_t begin = 0,
@@ -192,7 +195,7 @@ private:
     long adam_step_ = 0;
     DevBuf scratch_;
     DevBuf params_, grads_, m_, v_, acc_, d_screen_, norm_sum_, hits_, max_radius_, loss_sum_, d_image_, gt_,
-        ssim_planes_;
+        ssim_planes_, hwc_;
     // densify_and_prune scratch and the spare parameter / moment planes it writes into
     DevBuf dz_code_, dz_rank_, dz_ws_, dz_csrc_, dz_ssrc_, dz_normals_, dz_keep_, dz_dest_, spare_p_, spare_m_, spare_v_;
     void reset_per_gaussian_state();

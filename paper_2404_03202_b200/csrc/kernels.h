@@ -73,6 +73,8 @@ struct FrameBuffers {
 };
 // Sums of per-pixel visited (forward pairs) and last_contrib (backward pairs) -> out[0], out[1].
 void launch_work_count(const FrameBuffers& fb, int pixels, unsigned long long* out, cudaStream_t s);
+// 3 FP32 planes -> interleaved H x W x 3 FP64 (the reference Image layout).
+void launch_planar_to_hwc_f64(const float* rgb, size_t plane, double* out, cudaStream_t s);
 void launch_blend(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H,
                   int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s);
 

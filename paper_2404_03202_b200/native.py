@@ -230,17 +230,32 @@ class HostCloud:
             self.handle = None
 
 
-def osplat_render(cloud: HostCloud, pose12, width: int, height: int) -> np.ndarray:
-    """The reference drop-in entry point (capi.h:73-74): host cloud in, H x W x 3 double out."""
-    t = transform_of(pose12)
-    img = _vp()
-    check(lib.osplat_render(cloud.handle, _p(t), width, height, C.byref(img)))
-    try:
-        w, h = lib.osplat_image_width(img), lib.osplat_image_height(img)
-        px = lib.osplat_image_pixels(img)
-        return np.ctypeslib.as_array(px, shape=(h, w, 3)).copy()
-    finally:
-        lib.osplat_image_free(img)
+def osplat_render(cloud: HostCloud, pose12, width: int, height: int, out: np.ndarray | None = None) -> np.ndarray:
+    """The reference drop-in entry point (capi.h:73-74): host cloud in, H x W x 3 double out
+    (copied into `out` when given, e.g. a viewer's reused frame buffer)."""
+    with osplat_image(cloud, pose12, width, height) as px:
+        if out is None:
+            return px.copy()
+        np.copyto(out, px)
+        return out
+
+
+class osplat_image:
+    """Context manager over an osplat_render result: a zero-copy numpy view of the osplat_image's
+    pixels, valid until the block exits (osplat_image_free)."""
+
+    def __init__(self, cloud: HostCloud, pose12, width: int, height: int):
+        self.cloud, self.t, self.size = cloud, transform_of(pose12), (width, height)
+        self.img = _vp()
+
+    def __enter__(self) -> np.ndarray:
+        check(lib.osplat_render(self.cloud.handle, _p(self.t), self.size[0], self.size[1], C.byref(self.img)))
+        w, h = lib.osplat_image_width(self.img), lib.osplat_image_height(self.img)
+        return np.ctypeslib.as_array(lib.osplat_image_pixels(self.img), shape=(h, w, 3))
+
+    def __exit__(self, *exc):
+        lib.osplat_image_free(self.img)
+        self.img = _vp()
 
 
 class Config:
