@@ -69,10 +69,13 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
                                                                      float bg2, FrameBuffers fb,
                                                                      const float* __restrict__ d_image,
                                                                      float4* __restrict__ acc) {
-    // CTA-cooperative walk (as K3): 256 entries staged at once with 16-quarter reach masks, every
-    // warp then walks the 8 sub-chunks back to front.
-    __shared__ WarpStage stage[kTileWarps];
-    __shared__ uint16_t s_mask[kTileThreads];
+    // CTA-cooperative walk (as K3): 512 entries staged at once with 16-quarter reach masks, every
+    // warp then walks the 16 sub-chunks back to front.
+    constexpr int kPer = 2;                       // entries staged per thread per round
+    constexpr int kChunk = kPer * kTileThreads;   // entries per round (one barrier pair)
+    constexpr int kSubs = kChunk / 32;
+    __shared__ WarpStage stage[kSubs];
+    __shared__ uint16_t s_mask[kChunk];
     __shared__ int s_last[kTileWarps];
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -113,19 +116,22 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
 #pragma unroll
     for (int w = 0; w < kTileWarps; ++w) cta_last = max(cta_last, s_last[w]);
     const int t = threadIdx.x;
-    for (int hi = cta_last; hi > 0; hi -= kTileThreads) {
-        const int lo = hi > kTileThreads ? hi - kTileThreads : 0;
-        {
+    for (int hi = cta_last; hi > 0; hi -= kChunk) {
+        const int lo = hi > kChunk ? hi - kChunk : 0;
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const int i = lo + t + e * kTileThreads;
             uint32_t m = 0u;
-            if (lo + t < hi) {
-                const uint32_t gid = inst_gid[range.x + lo + t];
+            if (i < hi) {
+                const uint32_t gid = inst_gid[range.x + i];
                 const float4* s4 = reinterpret_cast<const float4*>(pp.splat + gid);
-                m = stage_record16(stage[warp], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc, yc, width);
+                m = stage_record16(stage[warp + e * kTileWarps], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc, yc,
+                                   width);
             }
-            s_mask[t] = static_cast<uint16_t>(m);
+            s_mask[t + e * kTileThreads] = static_cast<uint16_t>(m);
         }
         __syncthreads();
-      for (int sub = kTileWarps - 1; sub >= 0; --sub) {
+      for (int sub = kSubs - 1; sub >= 0; --sub) {
         const int sbase = lo + 32 * sub;
         if (sbase >= hi || sbase >= max_last) continue;  // no pixel of this warp reaches these entries
         WarpStage& ws = stage[sub];
