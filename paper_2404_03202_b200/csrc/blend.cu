@@ -180,7 +180,8 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
         }
         __syncwarp();
       }
-        __syncthreads();  // the stage is rewritten by the next chunk
+        // no barrier here: the next round's __syncthreads_or is the one that orders this round's
+        // stage reads before the restaging
     }
     if (inside) {
         const size_t pix = static_cast<size_t>(py) * W + px;
