@@ -232,6 +232,17 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_bwd(const float* __restri
     for (int i = threadIdx.x; i < kT * kG; i += kLossThreads) {
         const int c = i % kT, r0 = (i / kT) * kO;
         const int gx = x0 + c;
+        // this thread's rendered / target pixels, loaded before the column convolution so their
+        // latency overlaps it (they were the kernel's dominant stall when loaded on use)
+        float xs[kO], ys[kO];
+#pragma unroll
+        for (int o = 0; o < kO; ++o) {
+            const int gy = y0 + r0 + o;
+            const bool in = gx < W && gy < keep;
+            const size_t p = ch * plane + static_cast<size_t>(in ? gy : 0) * W + (in ? gx : 0);
+            xs[o] = in ? rgb[p] : 0.0f;
+            ys[o] = in ? gt[p] : 0.0f;
+        }
         float2 cv01[kO];
         float cv2[kO];
         if (ssim_scale != 0.0f) {
@@ -262,7 +273,7 @@ __global__ void __launch_bounds__(kLossThreads) k_ssim_bwd(const float* __restri
             const size_t p = ch * plane + static_cast<size_t>(gy) * W + gx;
             float grad = 0.0f;
             if (gy < keep) {
-                const float xv = rgb[p], yv = gt[p];
+                const float xv = xs[o], yv = ys[o];
                 const float d = xv - yv;
                 local += fabs(static_cast<double>(d));
                 grad = d > 0.0f ? l1_scale : (d < 0.0f ? -l1_scale : 0.0f);
