@@ -345,6 +345,12 @@ __global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __re
         for (int q = pl.sh(active_n, 0); q < pl.sh(bc, 0); ++q) G[static_cast<size_t>(q) * stride + gid] = 0.0f;
     }
 
+    // the geometry parameters are loaded up front (their latency overlaps the SH backward below)
+    float lsf[3], qf[4];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) lsf[k] = __ldg(P + static_cast<size_t>(pl.lscale(k)) * stride + gid);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) qf[k] = __ldg(P + static_cast<size_t>(pl.rot(k)) * stride + gid);
     const float4 a0 = acc[3 * static_cast<size_t>(gid)];
     const float4 a1 = acc[3 * static_cast<size_t>(gid) + 1];
     const float4 a2 = acc[3 * static_cast<size_t>(gid) + 2];
@@ -413,9 +419,9 @@ __global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __re
             dsig[r * 3 + c] = dva * m0[r] * m0[c] + dvb * (m0[r] * m1[c] + m1[r] * m0[c]) + dvc * m1[r] * m1[c];
     double s[3], q[4], s3[9];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) s[k] = exp(load_param(P, stride, pl.lscale(k), gid));
+    for (int k = 0; k < 3; ++k) s[k] = exp(static_cast<double>(lsf[k]));
 #pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = load_param(P, stride, pl.rot(k), gid);
+    for (int k = 0; k < 4; ++k) q[k] = static_cast<double>(qf[k]);
     covariance3d(q, s, s3);
     double sm0[3], sm1[3];
     m3v(s3, m0, sm0);
