@@ -79,13 +79,20 @@ __device__ __forceinline__ void jacobian_equirect_grad(const double* t, double t
 template <bool kPixel = true>
 __device__ __forceinline__ bool project64(const float* __restrict__ P, int stride, const Planes& pl, int gid,
                                           const Pose& pose, int W, int H, Proj64& pr) {
+    // all 11 geometry parameters are loaded first: independent loads in flight together instead of
+    // each waiting behind the FP64 math that precedes its use
+    float lsf[3], qf[4];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) lsf[k] = __ldg(P + static_cast<size_t>(pl.lscale(k)) * stride + gid);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) qf[k] = __ldg(P + static_cast<size_t>(pl.rot(k)) * stride + gid);
+    const double logit = load_param(P, stride, pl.opacity(), gid);
     double m[3] = {load_param(P, stride, 0, gid), load_param(P, stride, 1, gid), load_param(P, stride, 2, gid)};
     world_to_camera(pose, m, pr.t, &pr.t_r);
     const double* t = pr.t;
     if (pr.t_r < kNear) return false;
     double rho = sqrt(t[0] * t[0] + t[2] * t[2]);
     if (rho <= kPole * pr.t_r) return false;
-    double logit = load_param(P, stride, pl.opacity(), gid);
     pr.o = 1.0 / (1.0 + exp(-logit));
     if (pr.o < kAlphaMin) return false;
 
@@ -103,9 +110,9 @@ __device__ __forceinline__ bool project64(const float* __restrict__ P, int strid
     jacobian_equirect(t, pr.t_r, W, H, pr.jac);
     m23_mul(pr.jac, pose.R, pr.m23);
 #pragma unroll
-    for (int k = 0; k < 3; ++k) pr.s[k] = exp(load_param(P, stride, pl.lscale(k), gid));
+    for (int k = 0; k < 3; ++k) pr.s[k] = exp(static_cast<double>(lsf[k]));
 #pragma unroll
-    for (int k = 0; k < 4; ++k) pr.q[k] = load_param(P, stride, pl.rot(k), gid);
+    for (int k = 0; k < 4; ++k) pr.q[k] = static_cast<double>(qf[k]);
     covariance3d(pr.q, pr.s, pr.s3);
     double sm0[3], sm1[3];
     m3v(pr.s3, pr.m23, sm0);
