@@ -221,7 +221,9 @@ OSPLAT_API osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double tra
  * the context's stream and the call returns. loss_sums (4 doubles, pinned host memory; may be NULL)
  * receives {L1 sum, SSIM sums r, g, b} once the stream reaches the end of the step — read them after
  * osplat_gpu_synchronize and turn them into the loss with osplat_loss_value. A pipelined training
- * loop (loss logged one step late) keeps the GPU busy while the host enqueues the next view. */
+ * loop (loss logged one step late) keeps the GPU busy while the host enqueues the next view.
+ * A host target (gt_on_device 0) is copied asynchronously when it is page-locked: keep it valid
+ * and unmodified until the stream has passed the step. */
 OSPLAT_API osplat_status osplat_gpu_train_view_async(osplat_gpu* ctx, const double transform_cw[16], int width,
                                                      int height, const float* gt, int gt_on_device,
                                                      double lambda_ssim, double mask_bottom_fraction,
