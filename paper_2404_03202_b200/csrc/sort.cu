@@ -277,16 +277,22 @@ constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;  // ranks per block
 
 // Sum of touched over each block's ranks.
+// Also leaves touched[order[r]] at ranked[r] (coalesced), so k_emit_prep does not gather it again.
 __global__ void __launch_bounds__(kScanThreads) k_touch_sums(const uint32_t* __restrict__ touched,
                                                              const uint32_t* __restrict__ order, int n,
-                                                             uint32_t* __restrict__ block_sums) {
+                                                             uint32_t* __restrict__ block_sums,
+                                                             uint32_t* __restrict__ ranked) {
     __shared__ uint32_t s_scan[kSortWarps + 1];
     const long r0 = static_cast<long>(blockIdx.x) * kScanTile + threadIdx.x;
     uint32_t local = 0;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
         const long r = r0 + i * kScanThreads;
-        if (r < n) local += touched[order[r]];
+        if (r < n) {
+            const uint32_t v = touched[order[r]];
+            ranked[r] = v;
+            local += v;
+        }
     }
     uint32_t total;
     block_exclusive_scan(local, s_scan, &total);
@@ -341,8 +347,8 @@ __global__ void __launch_bounds__(1024) k_scan_block_sums(uint32_t* __restrict__
 constexpr int kEmitTile = kScanThreads * 8;
 constexpr int kEmitWindow = 2 * kEmitTile;  // ranks staged per CTA (more only with many empty ranks)
 
-__global__ void __launch_bounds__(kScanThreads) k_emit_prep(const uint32_t* __restrict__ touched,
-                                                            const uint32_t* __restrict__ order,
+// rank_off[r] holds touched[order[r]] on entry (k_touch_sums) and the rank's first output on exit.
+__global__ void __launch_bounds__(kScanThreads) k_emit_prep(const uint32_t* __restrict__ order,
                                                             const int4* __restrict__ rect, int n,
                                                             const uint32_t* __restrict__ block_offsets,
                                                             uint32_t* __restrict__ rank_off,
@@ -355,7 +361,7 @@ __global__ void __launch_bounds__(kScanThreads) k_emit_prep(const uint32_t* __re
     for (int i = 0; i < kScanItems; ++i) {
         const long r = r0 + i;
         g[i] = r < n ? order[r] : 0u;
-        v[i] = r < n ? touched[g[i]] : 0u;
+        v[i] = r < n ? rank_off[r] : 0u;
         local += v[i];
     }
     uint32_t agg;
@@ -538,9 +544,9 @@ void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4
     const size_t npad = (static_cast<size_t>(n) + 63) & ~size_t(63);  // keeps every array 256-B aligned
     uint32_t* rank_gid = rank_off + npad;
     int2* rank_rc = reinterpret_cast<int2*>(rank_gid + npad);
-    k_touch_sums<<<blocks, kScanThreads, 0, s>>>(touched, order, n, sums);
+    k_touch_sums<<<blocks, kScanThreads, 0, s>>>(touched, order, n, sums, rank_off);
     k_scan_block_sums<<<1, 1024, 0, s>>>(sums, blocks, total);
-    k_emit_prep<<<blocks, kScanThreads, 0, s>>>(touched, order, rect, n, sums, rank_off, rank_gid, rank_rc);
+    k_emit_prep<<<blocks, kScanThreads, 0, s>>>(order, rect, n, sums, rank_off, rank_gid, rank_rc);
     // one CTA per kEmitTile outputs up to the capacity (CTAs past M exit; M > capacity is retried)
     const long grid = (static_cast<long>(capacity) + kEmitTile - 1) / kEmitTile;
     if (grid > 0)
