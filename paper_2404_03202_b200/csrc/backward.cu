@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
             if (i < hi) {
                 const uint32_t gid = inst_gid[range.x + i];
                 const float4* s4 = reinterpret_cast<const float4*>(pp.splat + gid);
-                m = stage_record16(stage[warp + e * kTileWarps], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc, yc,
+                m = stage_record16<true>(stage[warp + e * kTileWarps], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc, yc,
                                    width);
             }
             s_mask[t + e * kTileThreads] = static_cast<uint16_t>(m);

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
             uint32_t m = 0u;
             if (idx < range.y) {
                 const float4* s4 = reinterpret_cast<const float4*>(pp.splat + gid);
-                m = stage_record16(stage[warp + e * kTileWarps], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc,
+                m = stage_record16<false>(stage[warp + e * kTileWarps], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc,
                                    yc, width);
             }
             s_mask[t + e * kTileThreads] = static_cast<uint16_t>(m);
