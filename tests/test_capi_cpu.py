@@ -162,3 +162,18 @@ def test_no_silent_cpu_fallback_without_gpu():
     cloud = native.HostCloud.from_cloud(scenes.synthetic_cloud(10, seed=1))
     with pytest.raises(native.OsplatError):
         native.osplat_render(cloud, scenes.identity_pose(), 64, 32)
+
+
+def test_loss_value_from_sums_is_the_reference_formula():
+    """osplat_loss_value (host): (1 - l) L1/n + l (1 - mean SSIM) with the bottom-row mask
+    (trainer.cpp:54-63), from the device's four sums {sum |r - g|, SSIM sums r, g, b}."""
+    from paper_2404_03202_b200 import native
+    W, H = 64, 32
+    sums = np.array([123.25, 1500.5, 1490.0, 1510.75])
+    for lam, mask in ((0.0, 0.0), (0.2, 0.0), (0.2, 0.25), (1.0, 0.1)):
+        keep = H - int(np.floor(mask * H))
+        npx = W * keep
+        ref = (1 - lam) * sums[0] / (3 * npx)
+        if lam > 0:
+            ref += lam * (1 - (sums[1:].sum() / npx) / 3)
+        assert native.loss_value(sums, lam, W, H, mask) == pytest.approx(ref, rel=1e-15, abs=1e-15)
