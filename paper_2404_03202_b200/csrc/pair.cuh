@@ -3,9 +3,9 @@
 // Tile layout: one 256-thread CTA per 16x16 tile, one pixel per thread; warp w owns the 8x4 pixel
 // block at columns 8(w&1)..+7, rows 4(w>>1)..+3, and each half-warp one 4x4 quarter of it (small
 // square blocks are touched by far fewer splats than 16-pixel strips of the same area). The CTA
-// walks its tile's list 256 entries at a time: every thread stages one entry into shared memory
+// walks its tile's list 512 entries at a time: every thread stages two entries into shared memory
 // (stage_record16) with a 16-bit mask of the quarters its conservative alpha >= 1/255 extent
-// (Splat32::ext_x/ext_y) reaches; after one barrier every warp walks the staged entries, each
+// (Splat32::ext_x/ext_y; in K4a further cut by per-row ellipse intervals) reaches; after one barrier every warp walks the staged entries, each
 // half-warp only those whose bit for its quarter is set (ballots) — entries outside are certain
 // skips of the FP32 classifier below, so no decision changes. K3 walks front to back and stops when
 // every pixel has terminated; K4a walks back to front from each warp's furthest last_contrib.
