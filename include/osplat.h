@@ -11,7 +11,9 @@
  * streams and device buffers cross the boundary as void* / typed device pointers.
  *
  * Threading contract (same as the reference, SPEC.md exclusivity): an osplat_gpu context and the
- * frames it produced must not be used concurrently from two host threads. Calls are ordered on
+ * frames it produced must not be used concurrently from two host threads. osplat_render may be
+ * called from any number of threads on one osplat_cloud (the cloud is read-shared):
+ * the cloud's device copy is created once and concurrent renders of it are serialised. Calls are ordered on
  * the context's CUDA stream; every call that returns host data synchronizes that stream.
  */
 #ifndef OSPLAT_B200_H
@@ -75,6 +77,13 @@ OSPLAT_API int osplat_image_width(const osplat_image* image);
 OSPLAT_API int osplat_image_height(const osplat_image* image);
 OSPLAT_API const double* osplat_image_pixels(const osplat_image* image);
 OSPLAT_API void osplat_image_free(osplat_image* image);
+
+/* capi.h:90-92 — PSNR (dB, capped at 99) and SSIM (11x11, sigma 1.5, zero-padded; mean over pixels
+ * and channels) of two images of equal size, computed in FP64 on the GPU (metrics.cpp:17-79).
+ * Sizes differ -> OSPLAT_ERR_VALIDATION "DimensionMismatch: psnr: image sizes differ". Either
+ * output pointer may be NULL. Synchronous. */
+OSPLAT_API osplat_status osplat_metrics(const osplat_image* a, const osplat_image* b, double* out_psnr,
+                                        double* out_ssim);
 
 /* ======================================================================================
  * Part 2 — device-resident render / backward / step interface

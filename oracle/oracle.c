@@ -1005,6 +1005,27 @@ double oracle_loss(const double* r, const double* gt, int w, int h, double lambd
     return value;
 }
 
+/* psnr (metrics.cpp:64-74, capped at kPsnrCap = 99) and ssim (metrics.cpp:76-79) — osplat_metrics
+ * (capi.cpp:287-296). */
+void oracle_metrics(const double* a, const double* b, int w, int h, double* psnr, double* ssim) {
+    const size_t n = (size_t)w * h * 3;
+    double mse = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        double d = a[i] - b[i];
+        mse += d * d;
+    }
+    mse /= (double)n;
+    if (psnr) {
+        double v = 99.0;
+        if (mse > 0.0) {
+            v = 10.0 * log10(1.0 / mse);
+            if (v > 99.0) v = 99.0;
+        }
+        *psnr = v;
+    }
+    if (ssim) *ssim = ssim_grad(a, b, w, h, NULL);
+}
+
 /* ------------------------------------------------------------------ densification (trainer.cpp) */
 
 /* std::mt19937_64 (libstdc++ mersenne_twister_engine<uint64, 64, 312, 156, 31, 0xb5026f5aa96619e9,

@@ -106,6 +106,9 @@ void oracle_adam_step(oracle_cloud* cloud, const oracle_grads* grads, oracle_ada
 double oracle_loss(const double* rendered, const double* gt, int width, int height,
                    double lambda_ssim, double mask_bottom_fraction, double* d_image);
 
+/* psnr / ssim of two H x W x 3 images (metrics.cpp:64-79; osplat_metrics, capi.cpp:287-296). */
+void oracle_metrics(const double* a, const double* b, int width, int height, double* psnr, double* ssim);
+
 /* The TrainConfig fields densify_and_prune reads (proj/include/omnisplat/trainer.hpp:19-51). */
 typedef struct oracle_densify_cfg {
     double densify_grad_threshold, scale_split_threshold, split_factor;

@@ -187,6 +187,7 @@ class Oracle:
                                          C.POINTER(_AdamCfg), C.c_double, C.c_long]
         lib.oracle_loss.restype = C.c_double
         lib.oracle_loss.argtypes = [_dp, _dp, C.c_int, C.c_int, C.c_double, C.c_double, _dp]
+        lib.oracle_metrics.argtypes = [_dp, _dp, C.c_int, C.c_int, _dp, _dp]
         lib.oracle_densify_and_prune.restype = C.c_int
         lib.oracle_densify_and_prune.argtypes = [C.POINTER(_Cloud), _dp, _lp, _dp, C.POINTER(_Adam),
                                                  C.POINTER(_DensifyCfg), C.c_double, C.c_ulonglong, C.c_int,
@@ -329,6 +330,14 @@ class Oracle:
         v = self.lib.oracle_loss(_ptr(r), _ptr(g), W, H, lambda_ssim, mask_bottom_fraction, _ptr(d))
         return v, d
 
+    def metrics(self, a, b):
+        """(psnr, ssim) of two H x W x 3 images (metrics.cpp:64-79, osplat_metrics)."""
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        assert a.shape == b.shape and a.ndim == 3 and a.shape[2] == 3
+        ps, ss = C.c_double(0.0), C.c_double(0.0)
+        self.lib.oracle_metrics(_ptr(a), _ptr(b), a.shape[1], a.shape[0], C.byref(ps), C.byref(ss))
+        return ps.value, ss.value
 
     def densify_and_prune(self, cloud, norm_sum, hits, max_radius, state: AdamState, cfg: DensifyConfig,
                           extent: float, seed: int, radius_prune_active: bool):

@@ -10,6 +10,7 @@
 
 #include "omnisplat/dataio.hpp"
 #include "omnisplat/gradients.hpp"
+#include "omnisplat/metrics.hpp"
 #include "omnisplat/parallel.hpp"
 #include "omnisplat/rasterizer.hpp"
 #include "omnisplat/trainer.hpp"
@@ -311,6 +312,14 @@ double oracle_loss(const double* r, const double* gt, int w, int h, double lambd
     }
     if (d_image) std::memcpy(d_image, lr.d_image.data.data(), lr.d_image.data.size() * 8);
     return lr.value;
+}
+
+void oracle_metrics(const double* a, const double* b, int w, int h, double* out_psnr, double* out_ssim) {
+    Image x(w, h), y(w, h);
+    std::memcpy(x.data.data(), a, x.data.size() * 8);
+    std::memcpy(y.data.data(), b, y.data.size() * 8);
+    if (out_psnr) *out_psnr = psnr(x, y);
+    if (out_ssim) *out_ssim = ssim(x, y);
 }
 
 int oracle_densify_and_prune(const oracle_cloud* in, const double* norm_sum, const long* hits,

@@ -23,9 +23,15 @@
 using osb::Engine;
 using osb::HostCloud;
 
+// The reference's GaussianCloud is read-shared during rendering: any number of host
+// threads may call osplat_render on one const cloud at once. The device copy (render_cache) and
+// its Engine (stream, frame pool, staging buffers) are created once under render_mu, and each
+// render holds render_mu for its K1 -> K3 + copy-out, so concurrent callers are serialised on the
+// cloud's stream instead of racing on the Engine.
 struct osplat_cloud {
     HostCloud cloud;
     mutable std::shared_ptr<Engine> render_cache;  // device copy used by osplat_render
+    mutable std::mutex render_mu;
 };
 // H x W x 3 doubles. Images from osplat_render live in page-locked buffers recycled through a
 // small pool (no page faults, full-speed D2H); images built from host data use the heap.
@@ -471,7 +477,7 @@ void osplat_set_threads(int) {}
 
 osplat_status osplat_cloud_load(const char* path, osplat_cloud** out) {
     if (!path || !out) return invalid("osplat_cloud_load: null argument");
-    return wrap([&] { *out = new osplat_cloud{load_checkpoint(path), nullptr}; });
+    return wrap([&] { *out = new osplat_cloud{load_checkpoint(path), nullptr, {}}; });
 }
 
 osplat_status osplat_cloud_save(const osplat_cloud* cloud, const char* path) {
@@ -540,6 +546,7 @@ osplat_status osplat_render(const osplat_cloud* cloud, const double transform_cw
     return wrap([&] {
         double p12[12];
         checked_pose(transform_cw, p12);
+        std::lock_guard<std::mutex> lock(cloud->render_mu);
         if (!cloud->render_cache) {
             auto e = std::make_shared<Engine>(default_device(), nullptr);
             e->upload(cloud->cloud);
@@ -570,6 +577,49 @@ int osplat_image_height(const osplat_image* image) { return image ? image->heigh
 const double* osplat_image_pixels(const osplat_image* image) { return image ? image->px() : nullptr; }
 void osplat_image_free(osplat_image* image) { delete image; }
 
+// capi.cpp:287-296 -> psnr (metrics.cpp:64-74, capped at 99) and ssim (metrics.cpp:76-79) in FP64
+// on the device: both images are uploaded, three kernels (metrics.cu) reduce them, the four sums
+// come back and the host finishes the two formulas exactly as the reference does.
+osplat_status osplat_metrics(const osplat_image* a, const osplat_image* b, double* out_psnr, double* out_ssim) {
+    if (!a || !b) return invalid("osplat_metrics: null argument");
+    return wrap([&] {
+        if (a->width != b->width || a->height != b->height)
+            throw ApiError(Code::DimensionMismatch, "psnr: image sizes differ");
+        const int W = a->width, H = a->height;
+        const size_t px = static_cast<size_t>(W) * H;
+        osb::DeviceGuard g(default_device());
+        cudaStream_t s = nullptr;
+        OSB_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        void* buf = nullptr;
+        const size_t img_bytes = px * 3 * sizeof(double);
+        const size_t bytes = 2 * img_bytes + px * 15 * sizeof(double) + 4 * sizeof(double);
+        double sums[4] = {0, 0, 0, 0};
+        cudaError_t err = cudaMallocAsync(&buf, bytes, s);
+        if (err == cudaSuccess) {
+            double* da = static_cast<double*>(buf);
+            double* db = da + px * 3;
+            double* maps = db + px * 3;
+            double* dsum = maps + px * 15;
+            cudaMemcpyAsync(da, a->px(), img_bytes, cudaMemcpyHostToDevice, s);
+            cudaMemcpyAsync(db, b->px(), img_bytes, cudaMemcpyHostToDevice, s);
+            osb::launch_metrics_f64(da, db, W, H, maps, dsum, s);
+            cudaMemcpyAsync(sums, dsum, sizeof(sums), cudaMemcpyDeviceToHost, s);
+            cudaFreeAsync(buf, s);
+            err = cudaStreamSynchronize(s);
+        }
+        cudaStreamDestroy(s);
+        OSB_CUDA_CHECK(err);
+        const double n = static_cast<double>(px) * 3.0;
+        const double mse = sums[0] / n;
+        if (out_psnr) *out_psnr = mse <= 0.0 ? 99.0 : std::min(99.0, 10.0 * std::log10(1.0 / mse));
+        if (out_ssim) {
+            double total = 0.0;
+            for (int c = 0; c < 3; ++c) total += sums[1 + c] / static_cast<double>(px);
+            *out_ssim = total / 3.0;
+        }
+    });
+}
+
 // ------------------------------------------------------------------ device-resident extension
 
 osplat_status osplat_gpu_create(int device, void* stream, const osplat_cloud* cloud, osplat_gpu** out) {
@@ -592,7 +642,7 @@ osplat_status osplat_gpu_set_active_sh_degree(osplat_gpu* ctx, int degree) {
 
 osplat_status osplat_gpu_download(osplat_gpu* ctx, osplat_cloud** out) {
     if (!ctx || !out) return invalid("osplat_gpu_download: null argument");
-    return wrap([&] { *out = new osplat_cloud{ctx->engine->download(), nullptr}; });
+    return wrap([&] { *out = new osplat_cloud{ctx->engine->download(), nullptr, {}}; });
 }
 
 osplat_status osplat_gpu_synchronize(osplat_gpu* ctx) {

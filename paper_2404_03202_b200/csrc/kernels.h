@@ -110,6 +110,10 @@ void launch_loss(const float* rgb, const float* gt, int W, int H, int keep_rows,
 // sum over n of (a - b)^2 in FP64 -> *out (psnr's MSE numerator, metrics.cpp:64-74).
 void launch_sq_err(const float* a, const float* b, long n, double* out, cudaStream_t s);
 
+// osplat_metrics (metrics.cu): two H x W x 3 FP64 images -> sums[0] = sum (a - b)^2,
+// sums[1..3] = per-channel sums of the SSIM map (metrics.cpp:17-79). maps: 15 W H doubles.
+void launch_metrics_f64(const double* a, const double* b, int W, int H, double* maps, double* sums, cudaStream_t s);
+
 // ---- densification (densify.cu) -------------------------------------------------------------
 struct DensifyArgs {
     double grad_threshold;  // densify_grad_threshold

@@ -124,6 +124,7 @@ def _load():
         "osplat_gpu_save_state": (S, [_vp, C.c_char_p, C.c_long]),
         "osplat_gpu_load_state": (S, [_vp, C.c_char_p, _lp]),
         "osplat_image_create": (S, [C.c_int, C.c_int, _dp, C.POINTER(_vp)]),
+        "osplat_metrics": (S, [_vp, _vp, _dp, _dp]),
         "osplat_gpu_train": (S, [_vp, _vp, C.c_size_t, _dp, C.POINTER(_vp), _u8p, C.c_double, C.c_long, C.c_char_p,
                                  PROGRESS_FN, C.c_void_p]),
         "osplat_frame_work": (S, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
@@ -238,6 +239,26 @@ def osplat_render(cloud: HostCloud, pose12, width: int, height: int, out: np.nda
             return px.copy()
         np.copyto(out, px)
         return out
+
+
+def osplat_metrics(a: np.ndarray, b: np.ndarray) -> tuple[float, float]:
+    """The reference osplat_metrics (capi.h:90-92): (PSNR dB capped at 99, SSIM) of two H x W x 3
+    images, computed on the GPU through osplat_image handles."""
+    hs = []
+    try:
+        for im in (a, b):
+            im = np.ascontiguousarray(im, dtype=np.float64)
+            if im.ndim != 3 or im.shape[2] != 3:
+                raise ValueError("osplat_metrics: images must be H x W x 3")
+            h = _vp()
+            check(lib.osplat_image_create(im.shape[1], im.shape[0], _p(im), C.byref(h)))
+            hs.append(h)
+        ps, ss = C.c_double(0.0), C.c_double(0.0)
+        check(lib.osplat_metrics(hs[0], hs[1], C.byref(ps), C.byref(ss)))
+        return ps.value, ss.value
+    finally:
+        for h in hs:
+            lib.osplat_image_free(h)
 
 
 class osplat_image:

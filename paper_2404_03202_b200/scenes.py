@@ -78,7 +78,10 @@ def _directions(rng: np.random.Generator, n: int, variant: str) -> np.ndarray:
     return out[:n]
 
 
-def synthetic_cloud(n: int, seed: int = 1, variant: str = "uniform", sh_degree: int = 3) -> Cloud:
+def synthetic_cloud(n: int, seed: int = 1, variant: str = "uniform", sh_degree: int = 3,
+                    opacity_range=(0.05, 0.95), scale_mult: float = 1.0) -> Cloud:
+    """The §8(d) generator. `opacity_range` / `scale_mult` only reshape the same random draws
+    (stress scenes: near-opaque splats for the T < 1e-4 stop, oversized pole splats)."""
     rng = np.random.default_rng(seed)
     bc = (sh_degree + 1) ** 2
     dirs = _directions(rng, n, variant)
@@ -87,9 +90,9 @@ def synthetic_cloud(n: int, seed: int = 1, variant: str = "uniform", sh_degree: 
     q = rng.standard_normal((n, 4))
     q /= np.linalg.norm(q, axis=1, keepdims=True)
     sigma = np.sqrt(53.0 / max(n, 1))
-    base = np.log(sigma * rng.uniform(0.5, 1.5, size=(n, 1)))
+    base = np.log(scale_mult * sigma * rng.uniform(0.5, 1.5, size=(n, 1)))
     log_scales = base + 0.1 * rng.standard_normal((n, 3))
-    opacity_logits = _logit(rng.uniform(0.05, 0.95, size=n))
+    opacity_logits = _logit(rng.uniform(opacity_range[0], opacity_range[1], size=n))
     sh = np.empty((n, bc, 3))
     sh[:, 0, :] = rng.uniform(-0.4, 0.4, size=(n, 3))
     if bc > 1:

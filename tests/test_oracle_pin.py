@@ -136,3 +136,13 @@ def test_reference_unit_tests_pin_oracle(name):
         assert "test_rasterizer.cpp:80" in r.stdout
     else:
         assert r.returncode == 0 and not fails, r.stdout
+
+
+def test_metrics_restatement_bit_exact(oracle_port, oracle_ref):
+    """psnr / ssim (metrics.cpp:64-79, osplat_metrics) of the restatement == the reference."""
+    rng = np.random.default_rng(17)
+    for H, W in ((5, 7), (37, 53), (64, 128)):
+        a = rng.uniform(0, 1, (H, W, 3))
+        b = np.clip(a + rng.normal(0, 0.05, a.shape), 0, 1)
+        assert oracle_port.metrics(a, b) == oracle_ref.metrics(a, b)
+        assert oracle_port.metrics(a, a) == oracle_ref.metrics(a, a) == (99.0, 1.0)
