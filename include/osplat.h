@@ -196,11 +196,16 @@ OSPLAT_API osplat_status osplat_gpu_backward_device(osplat_gpu* ctx, const ospla
 OSPLAT_API osplat_status osplat_gpu_gradients(osplat_gpu* ctx, double* d_position, double* d_sh, double* d_rotation,
                                    double* d_log_scale, double* d_opacity_logit, double* d_screen,
                                    double* screen_norm_sum, long* screen_hits);
+/* zero_grad: the gradient planes become logically zero without a memory pass — the next backward
+ * stores instead of adding, and any read of the planes before that (osplat_gpu_gradients,
+ * osplat_gpu_view_buffers, whose caller may hand the planes to a collective) writes real zeros
+ * first. */
 OSPLAT_API osplat_status osplat_gpu_zero_grad(osplat_gpu* ctx);
 OSPLAT_API osplat_status osplat_gpu_reset_screen_stats(osplat_gpu* ctx);
 
 /* adam_step (trainer.hpp:80-81): one fused launch over all planes; config may be NULL
- * (reference defaults). zero_grad != 0 clears the consumed gradients in the same pass. */
+ * (reference defaults). zero_grad != 0 leaves the consumed gradients logically zero (see
+ * osplat_gpu_zero_grad). */
 OSPLAT_API osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_config* config, double scene_extent,
                                    long iteration, int zero_grad);
 /* The same step over the flat element range [begin, begin + count) of the planes x stride buffers

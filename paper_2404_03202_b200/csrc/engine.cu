@@ -562,6 +562,9 @@ void Engine::backward(Frame* f, const float* d_image, bool accumulate) {
 void Engine::materialize_grads() {
     if (!grads_zero_) return;
     OSB_CUDA_CHECK(cudaMemsetAsync(grads_.as<float>(), 0, static_cast<size_t>(planes_) * stride_ * 4, stream_));
+    // the planes now hold real zeros: a caller may write them directly (collectives, uploads) and
+    // the next consumer must not clear them again
+    grads_zero_ = false;
 }
 
 float* Engine::d_image_buffer(size_t pixels) {
@@ -689,6 +692,18 @@ void Engine::adam_step(const TrainHyper& h, double extent, long iteration, bool 
 }
 
 void Engine::zero_grad() { grads_zero_ = true; }
+
+void Engine::begin_training(bool fresh) {
+    DeviceGuard g(device_);
+    reset_per_gaussian_state();
+    grads_zero_ = true;
+    if (fresh) {
+        const size_t bytes = static_cast<size_t>(planes_) * stride_ * 4;
+        OSB_CUDA_CHECK(cudaMemsetAsync(m_.as<float>(), 0, bytes, stream_));
+        OSB_CUDA_CHECK(cudaMemsetAsync(v_.as<float>(), 0, bytes, stream_));
+        adam_step_ = 0;
+    }
+}
 
 void Engine::reset_screen_stats() {
     DeviceGuard g(device_);

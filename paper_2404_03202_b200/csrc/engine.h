@@ -142,6 +142,10 @@ public:
     void materialize_grads();
     bool grads_zero() const { return grads_zero_; }
     void reset_screen_stats();
+    // Trainer construction / resume (trainer.cpp:313-332): GradientBuffer and DensifyStats start
+    // from zero (screen statistics, d_screen, max radii, gradients); a fresh run (fresh = true)
+    // also restarts Adam (moments zero, step 0), a resume keeps the loaded optimizer state.
+    void begin_training(bool fresh);
     // Densification control (trainer.cpp:180-280): DensifyStats::observe of a rendered frame,
     // densify_and_prune with the reference's RNG stream std::mt19937_64(rng_seed), reset_opacity.
     void observe(Frame* f);

@@ -117,6 +117,9 @@ int DeviceTrainer::pick_view(long iteration) {
 
 void DeviceTrainer::run(long start_iteration, const std::function<void(const IterationReport&)>& hook) {
     DeviceGuard g(e_.device());
+    // the reference Trainer sizes (zeroes) GradientBuffer / DensifyStats / AdamState in its
+    // constructor (trainer.cpp:313-323); resume() then loads Adam (trainer.cpp:325-332)
+    e_.begin_training(start_iteration == 0);
     iteration_ = start_iteration;
     epoch_ = -1;
     const int heldout = test_.empty() ? train_[0] : test_[0];

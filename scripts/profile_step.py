@@ -2,6 +2,7 @@
 
     ncu --set full -k regex:k_blend -s 2 -c 1 -o gpurun_out/blend python scripts/profile_step.py
 """
+import json
 import os
 import sys
 
@@ -35,7 +36,17 @@ def main():
     for it in range(1, steps + 1):
         tr.step(it, [0])
     torch.cuda.synchronize()
-    print("done", native.launch_count(), "launches")
+    # the visited pairs of this workload's frame (after the captured launches): the per-pair
+    # instruction counts of profiles/ncu_kernels.json divide ncu's totals by these
+    ctx.profile(timing=False, count_work=True)
+    fr = ctx.render(poses[0], W, H)
+    fwd, bwd, inst = fr.work()
+    fr.free()
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "profile_work.json"), "w") as f:
+        json.dump({"gaussians": n, "width": W, "height": H, "variant": variant, "pose": "ring pose 0",
+                   "fwd_pairs": fwd, "bwd_pairs": bwd, "instances": inst}, f)
+    print("done", native.launch_count(), "launches", fwd, bwd, inst)
 
 
 if __name__ == "__main__":
