@@ -108,6 +108,12 @@ OSPLAT_API osplat_status osplat_gpu_create(int device, void* cuda_stream, const 
 OSPLAT_API void osplat_gpu_free(osplat_gpu* ctx);
 OSPLAT_API size_t osplat_gpu_count(const osplat_gpu* ctx);
 OSPLAT_API osplat_status osplat_gpu_set_active_sh_degree(osplat_gpu* ctx, int degree);
+/* Optional deterministic backward (the reference's pass 2 is a fixed-order tile reduction,
+ * gradients.cpp:162-169, so its gradients do not depend on the schedule): on != 0 makes every
+ * following backward of this context run K4a without atomics — per-instance partials, summed per
+ * Gaussian in a fixed order — so gradients are bit-identical run to run. Default off (K4a's
+ * warp-aggregated atomics: same values up to FP32 summation order, about half the cost). */
+OSPLAT_API osplat_status osplat_gpu_set_deterministic(osplat_gpu* ctx, int on);
 /* Download the current parameters into a new host cloud. */
 OSPLAT_API osplat_status osplat_gpu_download(osplat_gpu* ctx, osplat_cloud** out);
 OSPLAT_API osplat_status osplat_gpu_synchronize(osplat_gpu* ctx);

@@ -493,7 +493,240 @@ __global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __re
     }
 }
 
+
+
+// ---- deterministic mode (optional) ----------------------------------------------
+// K4a with a fixed summation order, the analogue of gradients.cpp:94-169 (per-tile accumulators,
+// then a fixed-order reduction): the tile walks its list 64 entries at a time (staged by the first
+// 64 threads, same records and masks as K4a); every quarter reduces an entry's 9 values over its 16
+// pixels with the same shuffle tree as K4a and stores the result in its own shared slot
+// part[quarter][entry]; after the round the 16 slots of every entry are summed in quarter order and
+// stored — no atomics — at the instance's emission index. The per-pair math is K4a's, instruction
+// for instruction (the pair classifier is shared through pair.cuh; the update below restates
+// K4a's body), so deterministic gradients equal K4a's up to FP32 summation order.
+constexpr int kDetChunk = 64;
+
+template <bool BG>
+__global__ void __launch_bounds__(kTileThreads) k_backward_pixels_det(
+    const uint32_t* __restrict__ inst_gid, const uint2* __restrict__ ranges, PreprocessOut pp, int W, int H,
+    int tiles_x, float bg0, float bg1, float bg2, FrameBuffers fb, const float* __restrict__ d_image,
+    const uint32_t* __restrict__ inv_rank, const uint32_t* __restrict__ rank_off, const int2* __restrict__ rank_rc,
+    float* __restrict__ inst_acc) {
+    __shared__ WarpStage stage[kDetChunk / 32];
+    __shared__ uint16_t s_mask[kDetChunk];
+    __shared__ float part[2 * kTileWarps][kDetChunk][9];
+    __shared__ int s_last[kTileWarps];
+    const int tile = blockIdx.x;
+    const int tx = tile % tiles_x, ty = tile / tiles_x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const WarpPixel wp = warp_pixel(warp, lane);
+    const int lx = wp.lx, ly = wp.ly;
+    const int px = tx * kTile + lx, py = ty * kTile + ly;
+    const bool inside = px < W && py < H;
+    const uint2 range = ranges[tile];
+    const double width = W;
+    const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
+    const float lxo = lx - 7.5f, lyo = ly - 7.5f;
+    const float halfW = 0.5f * W, fW = static_cast<float>(W);
+    const float2 nlo = make_float2(-lxo, -lyo);
+    const size_t pix = static_cast<size_t>(py) * W + px;
+    const size_t plane = static_cast<size_t>(W) * H;
+    const int last = inside ? fb.last[pix] : 0;
+    const float T_final = inside ? fb.T[pix] : 0.0f;
+    const float dl0 = inside ? d_image[pix] : 0.0f;
+    const float dl1 = inside ? d_image[plane + pix] : 0.0f;
+    const float2 dl01 = make_float2(dl0, dl1);
+    const float dl2 = inside ? d_image[2 * plane + pix] : 0.0f;
+    const float bg_dot = bg0 * dl0 + bg1 * dl1 + bg2 * dl2;
+    const int max_last = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(last)));
+    const int quarter = 2 * warp + wp.half;
+    float T_acc = T_final;
+    float2 ns01 = make_float2(0.0f, 0.0f);
+    float ns2 = 0.0f;
+    if (lane == 0) s_last[warp] = max_last;
+    __syncthreads();
+    int cta_last = 0;
+#pragma unroll
+    for (int w = 0; w < kTileWarps; ++w) cta_last = max(cta_last, s_last[w]);
+    const int t = threadIdx.x;
+    float* partf = &part[0][0][0];
+    for (int hi = cta_last; hi > 0; hi -= kDetChunk) {
+        const int lo = hi > kDetChunk ? hi - kDetChunk : 0;
+        for (int u = t; u < 2 * kTileWarps * kDetChunk * 9; u += kTileThreads) partf[u] = 0.0f;
+        if (t < kDetChunk) {
+            const int i = lo + t;
+            uint32_t m = 0u;
+            if (i < hi) {
+                const uint32_t gid = inst_gid[range.x + i];
+                const float4* s4 = reinterpret_cast<const float4*>(pp.splat + gid);
+                m = stage_record16<true>(stage[t >> 5], t & 31, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc, yc, width);
+            }
+            s_mask[t] = static_cast<uint16_t>(m);
+        }
+        __syncthreads();
+        for (int sub = kDetChunk / 32 - 1; sub >= 0; --sub) {
+            const int sbase = lo + 32 * sub;
+            if (sbase >= hi || sbase >= max_last) continue;
+            const WarpStage& ws = stage[sub];
+            const uint32_t mk = s_mask[32 * sub + lane];
+            const uint32_t bal0 = __ballot_sync(0xffffffffu, (mk >> (2 * warp)) & 1u);
+            const uint32_t bal1 = __ballot_sync(0xffffffffu, (mk >> (2 * warp + 1)) & 1u);
+            uint32_t bal = wp.half ? bal1 : bal0;
+            while (__any_sync(0xffffffffu, bal != 0u)) {
+                const bool live = bal != 0u;
+                const int j = live ? 31 - __clz(bal) : 0;
+                bal &= ~(1u << j);
+                const int k = sbase + j;
+                float v[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                bool has = false;
+                if (live && k < last) {
+                    const float4 A = ws.a[j];
+                    const float4 B = ws.b[j];
+                    float2 d;
+                    float power;
+                    bool unc;
+                    if (pair_power2(A, B, nlo, halfW, fW, d, power, unc)) {
+                        const float4 Cc = ws.c[j];
+                        float alpha, g;
+                        bool gate;
+                        bool ok = true;
+                        if (unc) {
+                            Pair64 p;
+                            ok = pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
+                            alpha = static_cast<float>(p.alpha);
+                            g = static_cast<float>(p.g);
+                            gate = p.og < kAlphaMax;
+                        } else {
+                            g = ex2_approx(-power * kLog2e);
+                            const float og = Cc.w * g;
+                            alpha = fminf(0.99f, og);
+                            gate = true;
+                            if (Cc.w >= 0.98f) {
+                                const float band = 0.99f * (1.5f * fabsf(B.w) + 1e-6f);
+                                if (fabsf(og - 0.99f) <= band) {
+                                    Pair64 p;
+                                    pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
+                                    gate = p.og < kAlphaMax;
+                                } else {
+                                    gate = og < 0.99f;
+                                }
+                            }
+                        }
+                        if (ok) {
+                            has = true;
+                            const float one_m = 1.0f - alpha;
+                            float inv;
+                            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));
+                            T_acc = T_acc * inv;
+                            const float wb = alpha * T_acc;
+                            const float2 v01 = __fmul2_rn(dl01, make_float2(wb, wb));
+                            v[0] = v01.x;
+                            v[1] = v01.y;
+                            v[2] = dl2 * wb;
+                            const float2 cs = __fadd2_rn(make_float2(Cc.x, Cc.y), ns01);
+                            float d_alpha = cs.x * dl01.x;
+                            d_alpha = __fmaf_rn(cs.y, dl01.y, d_alpha);
+                            d_alpha = __fmaf_rn(Cc.z + ns2, dl2, d_alpha);
+                            d_alpha = d_alpha * T_acc;
+                            if (BG) d_alpha = d_alpha - (T_final * inv) * bg_dot;
+                            const float nalpha = -alpha;
+                            ns01 = __ffma2_rn(make_float2(Cc.x, Cc.y), make_float2(nalpha, nalpha),
+                                              __fmul2_rn(ns01, make_float2(one_m, one_m)));
+                            ns2 = __fmaf_rn(Cc.z, nalpha, ns2 * one_m);
+                            if (gate) {
+                                v[3] = g * d_alpha;
+                                const float d_power = -Cc.w * v[3];
+                                const float2 v45 = __fmul2_rn(d, make_float2(d_power, d_power));
+                                const float2 v67 = __fmul2_rn(d, make_float2(v45.x, v45.x));
+                                v[4] = v45.x;
+                                v[5] = v45.y;
+                                v[6] = v67.x;
+                                v[7] = v67.y;
+                                v[8] = v45.y * d.y;
+                            }
+                        }
+                    }
+                }
+                const uint32_t hb_all = __ballot_sync(0xffffffffu, has);
+                if (hb_all == 0u) continue;
+                int idx;
+                const float sum = half_reduce9(v, lane, &idx);
+                // each quarter visits an entry at most once: its slot is written once per round
+                const uint32_t hb = hb_all & (wp.half ? 0xFFFF0000u : 0x0000FFFFu);
+                if (live && hb != 0u && idx >= 0) part[quarter][32 * sub + j][idx] = sum;
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        // fixed-order combination over the 16 quarters, stored at the emission index
+        for (int u = t; u < kDetChunk * 9; u += kTileThreads) {
+            const int j = u / 9, i = u - 9 * j;
+            if (lo + j >= hi) continue;
+            float acc_v = 0.0f;
+#pragma unroll
+            for (int q = 0; q < 2 * kTileWarps; ++q) acc_v += part[q][j][i];
+            const uint32_t gid = stage[j >> 5].gid[j & 31];
+            const uint32_t r = inv_rank[gid];
+            const int2 rc = rank_rc[r];
+            const int x0 = static_cast<int>(static_cast<int16_t>(rc.x & 0xFFFF));
+            const int wt = static_cast<int>(static_cast<uint32_t>(rc.x) >> 16);
+            int col = tx - x0;
+            col = ((col % tiles_x) + tiles_x) % tiles_x;
+            const size_t e = static_cast<size_t>(rank_off[r]) + static_cast<size_t>(ty - rc.y) * wt + col;
+            inst_acc[e * 9 + i] = acc_v;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_inv_rank(const uint32_t* __restrict__ rank_gid, int n, uint32_t* __restrict__ inv_rank) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) inv_rank[rank_gid[r]] = static_cast<uint32_t>(r);
+}
+
+// Pass 2: one thread per depth rank sums its instances in emission order (FP64) -> acc (FP32).
+__global__ void k_det_reduce(const uint32_t* __restrict__ rank_off, const uint32_t* __restrict__ rank_gid,
+                             const uint32_t* __restrict__ touched, int n, const float* __restrict__ inst_acc,
+                             float4* __restrict__ acc) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const uint32_t gid = rank_gid[r];
+    const uint32_t cnt = touched[gid];
+    if (cnt == 0u) return;
+    double s[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const float* p = inst_acc + static_cast<size_t>(rank_off[r]) * 9;
+    for (uint32_t li = 0; li < cnt; ++li, p += 9)
+#pragma unroll
+        for (int i = 0; i < 9; ++i) s[i] += static_cast<double>(p[i]);
+    float4* a = acc + 3 * static_cast<size_t>(gid);
+    a[0] = make_float4(static_cast<float>(s[0]), static_cast<float>(s[1]), static_cast<float>(s[2]),
+                       static_cast<float>(s[3]));
+    a[1] = make_float4(static_cast<float>(s[4]), static_cast<float>(s[5]), static_cast<float>(s[6]),
+                       static_cast<float>(s[7]));
+    a[2] = make_float4(static_cast<float>(s[8]), 0.0f, 0.0f, 0.0f);
+}
+
 }  // namespace
+
+void launch_backward_pixels_det(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H,
+                                int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb,
+                                const float* d_image, const EmitArrays& em, int n, uint32_t* inv_rank,
+                                float* inst_acc, float4* acc, cudaStream_t s) {
+    const int tiles = tiles_x * tiles_y;
+    if (tiles <= 0 || n <= 0) return;
+    k_inv_rank<<<(n + 255) / 256, 256, 0, s>>>(em.rank_gid, n, inv_rank);
+    if (bg[0] != 0.0f || bg[1] != 0.0f || bg[2] != 0.0f)
+        k_backward_pixels_det<true><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1],
+                                                                   bg[2], fb, d_image, inv_rank, em.rank_off,
+                                                                   em.rank_rc, inst_acc);
+    else
+        k_backward_pixels_det<false><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1],
+                                                                    bg[2], fb, d_image, inv_rank, em.rank_off,
+                                                                    em.rank_rc, inst_acc);
+    k_det_reduce<<<(n + 255) / 256, 256, 0, s>>>(em.rank_off, em.rank_gid, pp.touched, n, inst_acc, acc);
+    OSB_LAUNCHED(3);
+}
+
 
 void launch_backward_pixels(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H,
                             int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb, const float* d_image,

@@ -635,6 +635,13 @@ osplat_status osplat_gpu_create(int device, void* stream, const osplat_cloud* cl
 void osplat_gpu_free(osplat_gpu* ctx) { delete ctx; }
 size_t osplat_gpu_count(const osplat_gpu* ctx) { return ctx ? ctx->engine->n() : 0; }
 
+osplat_status osplat_gpu_set_deterministic(osplat_gpu* ctx, int on) {
+    if (!ctx) return invalid("osplat_gpu_set_deterministic: null context");
+    ctx->engine->set_deterministic(on != 0);
+    t_last_error.clear();
+    return OSPLAT_OK;
+}
+
 osplat_status osplat_gpu_set_active_sh_degree(osplat_gpu* ctx, int degree) {
     if (!ctx) return invalid("osplat_gpu_set_active_sh_degree: null context");
     return wrap([&] { ctx->engine->set_active_sh_degree(degree); });

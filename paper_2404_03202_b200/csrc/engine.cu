@@ -545,8 +545,18 @@ void Engine::backward(Frame* f, const float* d_image, bool accumulate) {
     const PreprocessOut pp = f->pp();
     {
         Span sp(*this, kBwdPixels);
-        launch_backward_pixels(f->inst_gid(), f->ranges.as<uint2>(), pp, f->W, f->H, f->tiles_x, f->tiles_y, f->bg,
-                               f->fb(), d_image, acc_.as<float4>(), stream_);
+        if (deterministic_) {
+            det_inst_.ensure(static_cast<size_t>(f->M) * 9 * sizeof(float) + 64);
+            det_rank_.ensure(static_cast<size_t>(f->n) * sizeof(uint32_t) + 64);
+            OSB_CUDA_CHECK(cudaMemsetAsync(det_inst_.as<float>(), 0, static_cast<size_t>(f->M) * 9 * sizeof(float),
+                                           stream_));
+            launch_backward_pixels_det(f->inst_gid(), f->ranges.as<uint2>(), pp, f->W, f->H, f->tiles_x, f->tiles_y,
+                                       f->bg, f->fb(), d_image, scan_emit_arrays(f->scan_ws.as<void>(), f->n), f->n,
+                                       det_rank_.as<uint32_t>(), det_inst_.as<float>(), acc_.as<float4>(), stream_);
+        } else {
+            launch_backward_pixels(f->inst_gid(), f->ranges.as<uint2>(), pp, f->W, f->H, f->tiles_x, f->tiles_y,
+                                   f->bg, f->fb(), d_image, acc_.as<float4>(), stream_);
+        }
     }
     ScreenStats st{d_screen_.as<float2>(), norm_sum_.as<double>(), hits_.as<int>()};
     if (!accumulate) OSB_CUDA_CHECK(cudaMemsetAsync(d_screen_.as<float2>(), 0, stride_ * 8, stream_));

@@ -120,6 +120,11 @@ public:
     void projection_detail(Frame* f, std::vector<double>& out);
     void release(Frame* f);
     void backward(Frame* f, const float* d_image_planar_dev, bool accumulate);
+    // Optional deterministic backward (gradients.cpp:94-169's fixed-order reduction): K4a without
+    // atomics, per-instance partials reduced per Gaussian in a fixed order — gradients bit-identical
+    // run to run, at roughly twice K4a's cost. Off by default.
+    void set_deterministic(bool on) { deterministic_ = on; }
+    bool deterministic() const { return deterministic_; }
     // loss() of trainer.cpp:25-71 on the device: d_image into d_image_buffer(); the value is read
     // back only when want_value (one 32-byte read, synchronizes the stream).
     double loss(Frame* f, const float* gt_planar_dev, double lambda_ssim, double mask_bottom_fraction,
@@ -207,6 +212,8 @@ private:
     void grow_instances(Frame* f, uint32_t M);  // zero gradients' screen stats, d_screen, max radius (GradientBuffer::resize)
     double last_lambda_ = 0.0;
     bool grads_zero_ = true;
+    bool deterministic_ = false;
+    DevBuf det_inst_, det_rank_;
     std::vector<std::unique_ptr<Frame>> pool_;
     std::vector<Frame*> free_;
     cudaStream_t copy_stream_ = nullptr;

@@ -58,6 +58,16 @@ void launch_fix_runs(const uint32_t* keys, uint32_t* order, const uint64_t* dept
 // Exclusive scan of touched[order[r]] fused with the emission of (tile, gid) instances in depth
 // order; writes only instances below `capacity`; *total = M (device).
 size_t scan_workspace_bytes(int n);
+// The per-depth-rank emission records launch_scan_emit leaves in its workspace (valid for the
+// frame's lifetime): first output (emission index of the rank's first instance), Gaussian id,
+// packed tile rectangle {x0 & 0xFFFF | width << 16, y0}. Instance li of rank r (row-major over its
+// rectangle, columns wrapped at the seam) has emission index rank_off[r] + li.
+struct EmitArrays {
+    const uint32_t* rank_off;
+    const uint32_t* rank_gid;
+    const int2* rank_rc;
+};
+EmitArrays scan_emit_arrays(void* ws, int n);
 void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
                       uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws, cudaStream_t s);
 void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s,
@@ -79,6 +89,15 @@ void launch_blend(const uint32_t* inst_gid, const uint2* ranges, const Preproces
                   int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s);
 
 // ---- K4 backward (backward.cu) --------------------------------------------------------------
+// Deterministic K4a (optional mode, gradients.cpp:94-169's fixed-order reduction): per tile the 16
+// quarters' partial sums of each entry are combined in a fixed order in shared memory and stored
+// (no atomics) at the instance's emission index in inst_acc (9 floats each, zeroed by the caller);
+// then one thread per depth rank sums its instances in emission order in FP64 into acc. Run to run
+// bit-identical gradients. inv_rank: n u32 of scratch.
+void launch_backward_pixels_det(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W,
+                                int H, int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb,
+                                const float* d_image, const EmitArrays& em, int n, uint32_t* inv_rank,
+                                float* inst_acc, float4* acc, cudaStream_t s);
 void launch_backward_pixels(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W,
                             int H, int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb,
                             const float* d_image, float4* acc, cudaStream_t s);

@@ -532,6 +532,18 @@ size_t scan_workspace_bytes(int n) {
     return sizeof(uint32_t) * (blocks + 128) + (static_cast<size_t>(n) + 64) * 16 + 256;
 }
 
+EmitArrays scan_emit_arrays(void* ws, int n) {
+    const int blocks = (n + kScanTile - 1) / kScanTile;
+    uint32_t* sums = static_cast<uint32_t*>(ws);
+    EmitArrays a;
+    uint32_t* rank_off = sums + ((blocks + 64 + 63) & ~63);
+    const size_t npad = (static_cast<size_t>(n) + 63) & ~size_t(63);
+    a.rank_off = rank_off;
+    a.rank_gid = rank_off + npad;
+    a.rank_rc = reinterpret_cast<const int2*>(rank_off + 2 * npad);
+    return a;
+}
+
 void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
                       uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws, cudaStream_t s) {
     if (n <= 0) {

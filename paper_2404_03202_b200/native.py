@@ -90,6 +90,7 @@ def _load():
         "osplat_gpu_free": (None, [_vp]),
         "osplat_gpu_count": (C.c_size_t, [_vp]),
         "osplat_gpu_set_active_sh_degree": (S, [_vp, C.c_int]),
+        "osplat_gpu_set_deterministic": (S, [_vp, C.c_int]),
         "osplat_gpu_download": (S, [_vp, C.POINTER(_vp)]),
         "osplat_gpu_synchronize": (S, [_vp]),
         "osplat_gpu_render": (S, [_vp, _dp, C.c_int, C.c_int, _dp, C.POINTER(_vp)]),
@@ -397,6 +398,10 @@ class Context:
         v = GpuView()
         check(lib.osplat_gpu_view_buffers(self.handle, C.byref(v)))
         return v
+
+    def set_deterministic(self, on: bool = True):
+        """Deterministic backward (fixed-order reduction, bit-identical gradients run to run)."""
+        check(lib.osplat_gpu_set_deterministic(self.handle, int(bool(on))))
 
     def set_active_sh_degree(self, d: int):
         check(lib.osplat_gpu_set_active_sh_degree(self.handle, d))
