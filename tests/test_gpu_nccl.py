@@ -66,3 +66,58 @@ def test_sharded_step_over_nccl_matches_replicated():
             assert np.max(d) <= 3 * 2 * 5e-2, f
     finally:
         dist.destroy_process_group()
+
+
+def test_densify_exchange_over_nccl_matches_replicated():
+    """Training iterations with DensifyStats::observe and a densify iteration (trainer.cpp:364-381)
+    through DataParallelTrainer over real NCCL (world 1, sharded path forced: stats allreduce,
+    moment all-gather, densify on the replica) == the replicated single-process path, bit for bit
+    (deterministic backward on both)."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        stream = torch.cuda.Stream()
+        torch.cuda.set_stream(stream)
+        W, H = 256, 128
+        cloud = scenes.synthetic_cloud(4000, seed=31)
+        target = scenes.synthetic_cloud(4000, seed=32)
+        poses = scenes.ring_poses(4, seed=3)
+        tctx = native.Context(target, stream=stream.cuda_stream)
+        gts = {}
+        for v in range(4):
+            fr = tctx.render(poses[v], W, H)
+            t = torch.empty(3 * W * H, dtype=torch.float32, device="cuda")
+            t.copy_(torch.as_tensor(dp._CudaArray(fr.device().rgb, 3 * W * H), device="cuda"))
+            gts[v] = t
+            fr.free()
+        cfg = native.Config(iterations=100, densify_grad_threshold=1e-7, prune_opacity=0.2)
+        out = []
+        for sharded in (False, True):
+            ctx = native.Context(cloud, stream=stream.cuda_stream)
+            ctx.set_deterministic(True)
+            eng = dp.GpuViewEngine(ctx, poses, gts, W, H, cfg, observe=True)
+            kw = dict(reduce_stats=dp.nccl_stats_reduce(dist))
+            if sharded:
+                rs, ag = dp.nccl_shard_collectives(dist)
+                tr = dp.DataParallelTrainer(eng, 0, 1, reduce_scatter=rs, all_gather=ag, force_shard=True, **kw)
+            else:
+                tr = dp.DataParallelTrainer(eng, 0, 1, **kw)
+            summary = None
+            for it in range(1, 5):
+                tr.accumulate([0, 1, 2, 3])
+                if it == 2:
+                    summary = tr.densify(cfg, 1.0, 77, radius_prune_active=False)
+                else:
+                    tr.apply(it)
+            torch.cuda.synchronize()
+            out.append((summary, ctx.download()))
+        (s0, a), (s1, b) = out
+        assert s0 == s1 and s0["cloned"] + s0["split"] > 0, (s0, s1)
+        assert a.n == b.n == s0["final_count"]
+        for f in ("positions", "sh", "rotations", "log_scales", "opacity_logits"):
+            assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    finally:
+        dist.destroy_process_group()
