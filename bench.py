@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--views-per-gpu", type=int, default=1)
     p.add_argument("--global-views", type=int, default=0,
                    help="fixed batch of B views per step split over the GPUs (strong scaling); 0 = weak")
+    p.add_argument("--torch-collectives", action="store_true",
+                   help="N > 1: exchange through torch.distributed (NCCL) instead of the library's own NCCL calls")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-sweep", action="store_true", help="skip the render FPS sweep (pole/seam scenes)")
@@ -348,25 +350,57 @@ def run_ours(args):
     extent = 1.0
     engine = dp.GpuViewEngine(ctx, poses, gts, W, H, cfg, extent, lambda_ssim=LAMBDA_SSIM)
     # N > 1: sharded optimizer — reduce-scatter of the gradient planes, fused Adam on this rank's
-    # 1/N shard, all-gather of the parameters (NCCL, in place on the flat buffers, on `stream`)
-    coll_ms = {"reduce_scatter": [], "all_gather": []}
+    # 1/N shard, all-gather of the parameters, in place on the flat buffers on `stream`. Default: the
+    # library's own NCCL communicator (osplat_gpu_dp_init / osplat_gpu_dp_step; torch.distributed
+    # only hands out the unique id); --torch-collectives: the same exchange through torch.distributed.
+    coll_ms = []
     timing_coll = [False]
+    native_dp = world > 1 and not args.torch_collectives
     rs = ag = None
-    if world > 1:
-        rs0, ag0 = dp.nccl_shard_collectives(dist)
+    if native_dp:
+        uid = [native.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.dp_init(world, rank, uid[0])
+        nccl["data_plane"] = "libosplat_b200 (ncclCommInitRank + ncclReduceScatter / ncclAllGather on the context stream)"
+    elif world > 1:
+        rs, ag = dp.nccl_shard_collectives(dist)
+        nccl["data_plane"] = "torch.distributed (reduce_scatter_tensor / all_gather_into_tensor)"
 
-        def timed(fn, key):
-            def call(t, b, c):
-                if not timing_coll[0]:
-                    return fn(t, b, c)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    class TimedEngine:
+        """Times each exchange (reduce-scatter + sharded Adam + all-gather) with events on `stream`."""
+
+        def __getattr__(self, name):
+            return getattr(engine, name)
+
+        def _timed(self, fn, *a):
+            if not timing_coll[0]:
+                return fn(*a)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn(*a)
+            e1.record(stream)
+            coll_ms.append((e0, e1))
+
+        def dp_step(self, iteration):
+            self._timed(engine.dp_step, iteration)
+
+    if world > 1 and not native_dp:
+        rs0, ag0 = rs, ag
+
+        def rs(t, b, c):
+            if timing_coll[0]:
+                e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                fn(t, b, c)
+                coll_ms.append([e0, None])
+            rs0(t, b, c)
+
+        def ag(t, b, c):
+            ag0(t, b, c)
+            if timing_coll[0]:
+                e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
-                coll_ms[key].append((e0, e1))
-            return call
-        rs, ag = timed(rs0, "reduce_scatter"), timed(ag0, "all_gather")
-    trainer = dp.DataParallelTrainer(engine, rank, world, reduce_scatter=rs, all_gather=ag)
+                coll_ms[-1][1] = e1
+    trainer = dp.DataParallelTrainer(TimedEngine(), rank, world, reduce_scatter=rs, all_gather=ag, native=native_dp)
     step_idx = [0]
 
     def train_step():
@@ -435,12 +469,13 @@ def run_ours(args):
     collectives = None
     if world > 1:
         flat_bytes = engine.grad_tensor().numel() * 4
+        ms = float(np.mean([a.elapsed_time(b) for a, b in coll_ms])) if coll_ms else None
         collectives = dict(nccl)
-        for key, evs in coll_ms.items():
-            ms = float(np.mean([a.elapsed_time(b) for a, b in evs])) if evs else None
-            # ring-equivalent bus bytes of a reduce-scatter / all-gather: (N - 1) / N x buffer
-            collectives[key] = {"ms": ms, "bytes": flat_bytes,
-                                "bus_gbs": (world - 1) / world * flat_bytes / (ms / 1e3) / 1e9 if ms else None}
+        # reduce-scatter + all-gather move the bytes of one ring allreduce: 2 (N - 1) / N x buffer
+        collectives["exchange"] = {"ms_per_step": ms, "buffer_bytes": flat_bytes,
+                                   "what": "reduce-scatter of the gradient planes + fused Adam on the 1/N shard + "
+                                           "all-gather of the parameters",
+                                   "bus_gbs": 2 * (world - 1) / world * flat_bytes / (ms / 1e3) / 1e9 if ms else None}
 
     # work counts of the profiled views (untimed renders with the device counters on)
     fwd_pairs = bwd_pairs = instances = 0
@@ -530,7 +565,9 @@ def run_ours(args):
                 ctx.train_view_async(poses[vi], W, H, host_gt[vi].data_ptr(), gt_on_device=False,
                                      sums_ptr=slot[k].data_ptr(), lambda_ssim=LAMBDA_SSIM)
             losses.append(slot)
-            if world > 1:
+            if native_dp:
+                ctx.dp_step(cfg, extent, s + 1)
+            elif world > 1:
                 b0, cnt = dp.shard_range(grads.numel(), rank, world)
                 rs(grads, b0, cnt)
                 ctx.adam_step(cfg, extent, s + 1, zero_grad=True, begin=b0, count=cnt)
@@ -557,8 +594,8 @@ def run_ours(args):
                "h2d_bytes_per_step": V * 3 * plane * 4, "d2h_bytes_per_step": V * 32,
                "loss_first_last": [step_losses[0], step_losses[-1]],
                "api": "osplat_gpu_train_view_async (pinned host target in, loss sums out to pinned host every "
-                      "step, one wait at the end) + osplat_gpu_adam_step (N > 1: NCCL reduce-scatter + "
-                      "osplat_gpu_adam_step_range + all-gather)"}
+                      "step, one wait at the end) + osplat_gpu_adam_step (N > 1: osplat_gpu_dp_step = NCCL "
+                      "reduce-scatter + sharded Adam + all-gather inside the library)"}
         if rank == 0:
             hc = native.HostCloud.from_cloud(cloud)
             native.osplat_render(hc, poses[0], W, H)  # upload + warm

@@ -220,6 +220,26 @@ OSPLAT_API osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_conf
 OSPLAT_API osplat_status osplat_gpu_adam_step_range(osplat_gpu* ctx, const osplat_config* config, double scene_extent,
                                                     long iteration, int zero_grad, size_t begin, size_t count);
 
+/* ---- §8(e) multi-view data parallelism inside the library: one process (context) per GPU, one
+ * NCCL communicator per context, every collective issued by the library on the context stream.
+ * NCCL is loaded at run time (libnccl.so.2; the one already mapped by the process if any);
+ * without it these calls return OSPLAT_ERR_UNSUPPORTED.
+ * osplat_nccl_unique_id: ncclGetUniqueId on one rank; the launcher hands the 128 bytes to every
+ * rank (any channel: torch.distributed, MPI, a file). osplat_gpu_dp_init: ncclCommInitRank
+ * (collective over the world). osplat_gpu_dp_step: the batch's exchange + optimizer step after
+ * every rank's backward(s) — in-place reduce-scatter of the gradient planes, fused Adam on this
+ * rank's 1/world shard, in-place all-gather of the parameters (= allreduce + replicated Adam, with
+ * 1/world of the Adam traffic; replicas bit-identical). With a communicator,
+ * osplat_gpu_densify_and_prune sums the screen statistics and maxes the radii over ranks and
+ * gathers the Adam moments first, osplat_gpu_save_state gathers the moments, and osplat_gpu_train
+ * trains a batch of `world` views per iteration (entry (j-1) world + rank of the reference's view
+ * stream on this rank; rank 0 writes the files): all of these are collectives — call them on
+ * every rank. */
+OSPLAT_API osplat_status osplat_nccl_unique_id(unsigned char id[128]);
+OSPLAT_API osplat_status osplat_gpu_dp_init(osplat_gpu* ctx, int world, int rank, const unsigned char id[128]);
+OSPLAT_API osplat_status osplat_gpu_dp_step(osplat_gpu* ctx, const osplat_config* config, double scene_extent,
+                                            long iteration);
+
 /* loss() (trainer.cpp:25-71): (1 - lambda_ssim) L1 + lambda_ssim (1 - SSIM), SSIM 11x11 sigma 1.5
  * zero-padded (metrics.cpp:17-153), bottom rows masked, against a device planar FP32 target:
  * writes dL/dC into the context's d_image buffer (returned through *d_image_planar) and the

@@ -1194,7 +1194,9 @@ osplat_status osplat_gpu_train(osplat_gpu* ctx, const osplat_config* config, siz
         planar.clear();
         planar.shrink_to_fit();
         std::string metrics_path;
-        if (output_dir) {
+        // data parallel: every rank runs the loop, rank 0 alone writes osplat_train's files
+        const bool writer = e.dp_rank() == 0;
+        if (output_dir && writer) {
             fs::create_directories(output_dir);
             metrics_path = (fs::path(output_dir) / "metrics.jsonl").string();
             std::ofstream(metrics_path, std::ios::trunc).close();
@@ -1210,7 +1212,7 @@ osplat_status osplat_gpu_train(osplat_gpu* ctx, const osplat_config* config, siz
                 }
                 if (progress) progress(user, r.iteration, r.loss, r.gaussians);
             }
-            if (output_dir && cfg.checkpoint_interval > 0 && r.iteration % cfg.checkpoint_interval == 0 &&
+            if (output_dir && writer && cfg.checkpoint_interval > 0 && r.iteration % cfg.checkpoint_interval == 0 &&
                 r.iteration != cfg.iterations) {
                 char name[64];
                 std::snprintf(name, sizeof(name), "checkpoint_%06ld.ply", r.iteration);
@@ -1218,8 +1220,11 @@ osplat_status osplat_gpu_train(osplat_gpu* ctx, const osplat_config* config, siz
             }
         });
         if (output_dir) {
-            save_checkpoint(e.download(), (fs::path(output_dir) / "final.ply").string());
-            osb::save_optimizer_state(e, trainer.iteration(), (fs::path(output_dir) / "final.adam").string());
+            e.dp_gather_moments();  // collective: every rank, before rank 0 writes the sidecar
+            if (writer) {
+                save_checkpoint(e.download(), (fs::path(output_dir) / "final.ply").string());
+                osb::save_optimizer_state(e, trainer.iteration(), (fs::path(output_dir) / "final.adam").string());
+            }
         }
     });
 }
@@ -1228,6 +1233,22 @@ osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_config* config,
                                    int zero_grad) {
     if (!ctx) return invalid("osplat_gpu_adam_step: null context");
     return wrap([&] { ctx->engine->adam_step(hyper_from(config), extent, iteration, zero_grad != 0); });
+}
+
+osplat_status osplat_nccl_unique_id(unsigned char id[128]) {
+    if (!id) return invalid("osplat_nccl_unique_id: null argument");
+    return wrap([&] { osb::nccl_unique_id(id); });
+}
+
+osplat_status osplat_gpu_dp_init(osplat_gpu* ctx, int world, int rank, const unsigned char id[128]) {
+    if (!ctx || !id) return invalid("osplat_gpu_dp_init: null argument");
+    if (world < 1 || rank < 0 || rank >= world) return invalid("osplat_gpu_dp_init: rank must be in [0, world)");
+    return wrap([&] { ctx->engine->dp_init(world, rank, id); });
+}
+
+osplat_status osplat_gpu_dp_step(osplat_gpu* ctx, const osplat_config* config, double extent, long iteration) {
+    if (!ctx) return invalid("osplat_gpu_dp_step: null context");
+    return wrap([&] { ctx->engine->dp_step(hyper_from(config), extent, iteration); });
 }
 
 osplat_status osplat_gpu_adam_step_range(osplat_gpu* ctx, const osplat_config* config, double extent, long iteration,

@@ -153,6 +153,7 @@ Engine::Engine(int device, cudaStream_t stream) : device_(device), stream_(strea
 Engine::~Engine() {
     cudaSetDevice(device_);
     cudaStreamSynchronize(stream_);
+    comm_.reset();
     pool_.clear();
     for (const Ev& ev : pending_) {
         cudaEventDestroy(ev.a);
@@ -739,6 +740,10 @@ void Engine::reset_opacity(double ceiling) {
 
 EditSummary Engine::densify_and_prune(const DensifyArgs& a, unsigned long long rng_seed) {
     DeviceGuard g(device_);
+    // data-parallel ranks: this rank's statistics are partial sums of its own views, its moments
+    // are current only on its shard — make both global first (comm.cpp)
+    dp_reduce_stats();
+    dp_gather_moments();
     EditSummary e;
     const int n = static_cast<int>(n_);
     const int bc = (sh_degree_ + 1) * (sh_degree_ + 1);
@@ -842,6 +847,7 @@ double Engine::psnr(Frame* f, const float* gt) {
 
 void Engine::read_adam(std::vector<float>& m, std::vector<float>& v) {
     DeviceGuard g(device_);
+    dp_gather_moments();  // a sharded optimizer's moments are current only on each rank's shard
     const size_t elems = static_cast<size_t>(planes_) * stride_;
     m.resize(elems);
     v.resize(elems);

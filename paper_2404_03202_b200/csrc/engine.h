@@ -95,6 +95,14 @@ struct Frame {
     FrameBuffers fb() const;
 };
 
+// NCCL communicator of a data-parallel rank (comm.cpp; NCCL is loaded at run time).
+struct Comm;
+struct CommDeleter {
+    void operator()(Comm* c) const;
+};
+void nccl_unique_id(unsigned char out[128]);  // ncclGetUniqueId
+int nccl_version();
+
 class Engine {
 public:
     Engine(int device, cudaStream_t stream);
@@ -162,6 +170,19 @@ public:
     void read_adam(std::vector<float>& m, std::vector<float>& v);
     void write_adam(const std::vector<float>& m, const std::vector<float>& v, long step);
     void synchronize();
+
+    // ---- multi-view data parallelism over NCCL (comm.cpp), one process (context) per GPU.
+    // dp_init: ncclCommInitRank on this context's device. dp_step: in-place reduce-scatter of the
+    // gradient planes, fused Adam on this rank's 1/world shard, in-place all-gather of the
+    // parameters, all on the context stream (sharded optimizer; replicas stay bit-identical).
+    // With a communicator, densify_and_prune first sums the screen statistics / maxes the radii
+    // over ranks and gathers the Adam moments; read_adam (the OSPLADAM sidecar) gathers them too.
+    void dp_init(int world, int rank, const unsigned char id[128]);
+    int dp_world() const;
+    int dp_rank() const;
+    void dp_step(const TrainHyper& h, double extent, long iteration);
+    void dp_gather_moments();
+    void dp_reduce_stats();
     // CUDA-event timing per kernel family on the context stream, and per-pixel work counting.
     void set_profiling(bool timing, bool count_work);
     void profile_read(double* ms, long* launches, bool reset);
@@ -213,6 +234,9 @@ private:
     double last_lambda_ = 0.0;
     bool grads_zero_ = true;
     bool deterministic_ = false;
+    std::unique_ptr<Comm, CommDeleter> comm_;
+    bool moments_sharded_ = false;  // Adam moments outside this rank's shard are stale
+    size_t dp_shard(size_t* begin) const;
     DevBuf det_inst_, det_rank_;
     std::vector<std::unique_ptr<Frame>> pool_;
     std::vector<Frame*> free_;

@@ -100,9 +100,11 @@ DeviceTrainer::DeviceTrainer(Engine& e, const TrainSettings& cfg, std::vector<do
     OSB_CUDA_CHECK(cudaStreamSynchronize(e_.stream()));
 }
 
-int DeviceTrainer::pick_view(long iteration) {
+int DeviceTrainer::pick_view(long iteration) { return view_at(iteration - 1); }
+
+int DeviceTrainer::view_at(long s) {
     const long n = static_cast<long>(train_.size());
-    const long epoch = (iteration - 1) / n;
+    const long epoch = s / n;
     if (epoch != epoch_) {
         epoch_ = epoch;
         order_ = train_;
@@ -112,7 +114,7 @@ int DeviceTrainer::pick_view(long iteration) {
             std::swap(order_[i - 1], order_[j]);
         }
     }
-    return order_[(iteration - 1) % n];
+    return order_[s % n];
 }
 
 void DeviceTrainer::run(long start_iteration, const std::function<void(const IterationReport&)>& hook) {
@@ -124,9 +126,14 @@ void DeviceTrainer::run(long start_iteration, const std::function<void(const Ite
     epoch_ = -1;
     const int heldout = test_.empty() ? train_[0] : test_[0];
     const double nan = std::numeric_limits<double>::quiet_NaN();
+    // data parallel (a communicator on the context, comm.cpp): iteration j trains a batch of `world`
+    // views — entries (j - 1) world .. j world - 1 of the reference's view stream, entry
+    // (j - 1) world + rank on this rank — then one exchange (sharded Adam, or the densify exchange);
+    // at world 1 this is Trainer::run exactly
+    const long world = e_.dp_world(), rank = e_.dp_rank();
     for (long j = iteration_ + 1; j <= cfg_.iterations; ++j) {
         iteration_ = j;
-        const int view = pick_view(j);
+        const int view = view_at((j - 1) * world + rank);
         if (j % cfg_.sh_warmup_interval == 0) {
             const int d = e_.active_sh_degree() + 1;
             e_.set_active_sh_degree(d < e_.sh_degree() ? d : e_.sh_degree());
@@ -154,7 +161,10 @@ void DeviceTrainer::run(long start_iteration, const std::function<void(const Ite
             if (j % cfg_.opacity_reset_interval == 0) e_.reset_opacity(cfg_.opacity_reset_ceiling);
         }
         // the densification edit rebuilds the parameter arrays: this iteration's gradients no longer apply
-        if (!rep.densified) e_.adam_step(cfg_.lr, extent_, j, true);
+        if (!rep.densified) {
+            if (world > 1) e_.dp_step(cfg_.lr, extent_, j);
+            else e_.adam_step(cfg_.lr, extent_, j, true);
+        }
         rep.gaussians = e_.n();
         rep.logged = log_now;
         rep.heldout_psnr = nan;

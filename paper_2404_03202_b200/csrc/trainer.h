@@ -49,6 +49,7 @@ public:
                   int width, int height, std::vector<int> train_indices, std::vector<int> test_indices,
                   double scene_extent);
     int pick_view(long iteration);  // trainer.cpp:340-354
+    int view_at(long stream_index);  // entry of the per-epoch shuffled view stream (0-based)
     long iteration() const { return iteration_; }
     double extent() const { return extent_; }
     // Runs iterations iteration()+1 .. cfg.iterations; hook(report) after every iteration.

@@ -64,8 +64,11 @@ class DataParallelTrainer:
 
     def __init__(self, engine: ViewEngine, rank: int, world: int, allreduce: Callable | None = None,
                  reduce_scatter: Callable | None = None, all_gather: Callable | None = None,
-                 reduce_stats: Callable | None = None, force_shard: bool = False):
-        if world > 1 and allreduce is None and (reduce_scatter is None or all_gather is None):
+                 reduce_stats: Callable | None = None, force_shard: bool = False, native: bool = False):
+        # native: the engine's context owns an NCCL communicator (Context.dp_init) and the library
+        # issues every collective itself (osplat_gpu_dp_step; densify / save exchange inside)
+        self.native = native
+        if world > 1 and not native and allreduce is None and (reduce_scatter is None or all_gather is None):
             raise ValueError("world > 1 needs an allreduce or a reduce_scatter + all_gather pair")
         self.engine = engine
         self.rank = rank
@@ -88,7 +91,9 @@ class DataParallelTrainer:
 
     def apply(self, iteration: int) -> None:
         """Gradient exchange + Adam (trainer.cpp:381 for the batch's summed gradients)."""
-        if self.sharded:
+        if self.native:
+            self.engine.dp_step(iteration)
+        elif self.sharded:
             grads = self.engine.grad_tensor()
             begin, count = shard_range(grads.numel(), self.rank, self.world)
             self.reduce_scatter(grads, begin, count)  # grads[begin:begin+count] <- sum over ranks
@@ -107,7 +112,7 @@ class DataParallelTrainer:
     def gather_optimizer_state(self) -> None:
         """Sharded optimizer: all-gather the Adam moments so every rank holds all of them (before
         densify_and_prune, which carries moments per Gaussian, or a save of the sidecar)."""
-        if not self.sharded:
+        if not self.sharded or self.native:
             return
         for t in self.engine.moment_tensors():
             begin, count = shard_range(t.numel(), self.rank, self.world)
@@ -116,7 +121,7 @@ class DataParallelTrainer:
     def densify(self, config, extent: float, seed: int, radius_prune_active: bool) -> dict:
         """densify_and_prune (trainer.cpp:188-275) on every replica after the stats exchange; the
         caller skips this iteration's Adam step, as Trainer::run does (trainer.cpp:379-381)."""
-        if self.world > 1:
+        if self.world > 1 and not self.native:
             if self.reduce_stats is None:
                 raise ValueError("densify at world > 1 needs reduce_stats")
             for t, op in self.engine.stat_tensors():
@@ -178,6 +183,9 @@ class GpuViewEngine:
 
     def adam_step(self, iteration: int):
         self.ctx.adam_step(self.config, self.extent, iteration, zero_grad=True)
+
+    def dp_step(self, iteration: int):
+        self.ctx.dp_step(self.config, self.extent, iteration)
 
     def adam_step_shard(self, iteration: int, begin: int, count: int):
         self.ctx.adam_step(self.config, self.extent, iteration, zero_grad=True, begin=begin, count=count)

@@ -91,6 +91,9 @@ def _load():
         "osplat_gpu_count": (C.c_size_t, [_vp]),
         "osplat_gpu_set_active_sh_degree": (S, [_vp, C.c_int]),
         "osplat_gpu_set_deterministic": (S, [_vp, C.c_int]),
+        "osplat_nccl_unique_id": (S, [C.POINTER(C.c_ubyte)]),
+        "osplat_gpu_dp_init": (S, [_vp, C.c_int, C.c_int, C.POINTER(C.c_ubyte)]),
+        "osplat_gpu_dp_step": (S, [_vp, _vp, C.c_double, C.c_long]),
         "osplat_gpu_download": (S, [_vp, C.POINTER(_vp)]),
         "osplat_gpu_synchronize": (S, [_vp]),
         "osplat_gpu_render": (S, [_vp, _dp, C.c_int, C.c_int, _dp, C.POINTER(_vp)]),
@@ -169,6 +172,13 @@ def loss_value(sums, lambda_ssim: float, width: int, height: int, mask: float = 
     """osplat_loss_value: the loss from osplat_gpu_train_view_async's sums."""
     a = np.ascontiguousarray(sums, dtype=np.float64)
     return float(lib.osplat_loss_value(_p(a), lambda_ssim, width, height, mask))
+
+
+def nccl_unique_id() -> bytes:
+    """osplat_nccl_unique_id: 128 bytes to hand to every rank's Context.dp_init."""
+    buf = (C.c_ubyte * 128)()
+    check(lib.osplat_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 def version() -> str:
@@ -398,6 +408,19 @@ class Context:
         v = GpuView()
         check(lib.osplat_gpu_view_buffers(self.handle, C.byref(v)))
         return v
+
+    def dp_init(self, world: int, rank: int, unique_id: bytes):
+        """osplat_gpu_dp_init: this context becomes rank `rank` of a `world`-GPU data-parallel job
+        (NCCL communicator owned by the library)."""
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
+        check(lib.osplat_gpu_dp_init(self.handle, world, rank, buf))
+
+    def dp_step(self, config: "Config | None", extent: float, iteration: int):
+        """osplat_gpu_dp_step: reduce-scatter of the gradients, Adam on this rank's shard,
+        all-gather of the parameters (NCCL, on the context stream)."""
+        check(lib.osplat_gpu_dp_step(self.handle, config.handle if config else None, extent, iteration))
 
     def set_deterministic(self, on: bool = True):
         """Deterministic backward (fixed-order reduction, bit-identical gradients run to run)."""

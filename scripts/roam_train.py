@@ -38,6 +38,10 @@ def main():
     ap.add_argument("--width", type=int, default=1520)
     ap.add_argument("--height", type=int, default=760)
     ap.add_argument("--out", default="/tmp/roam_out")
+    ap.add_argument("--prune-radius", type=float, default=20.0,
+                    help="TrainConfig prune_radius_px (reference default 20)")
+    ap.add_argument("--densify-grad", type=float, default=2e-4,
+                    help="TrainConfig densify_grad_threshold (reference default 2e-4)")
     args = ap.parse_args()
     W, H = args.width, args.height
     mask = 48.0 / 760.0
@@ -62,7 +66,8 @@ def main():
     prep_s = time.time() - t0
 
     ctx = native.Context(init)
-    cfg = native.Config(iterations=args.iterations, mask_bottom_fraction=mask, log_interval=1000)
+    cfg = native.Config(iterations=args.iterations, mask_bottom_fraction=mask, log_interval=1000,
+                        prune_radius_px=args.prune_radius, densify_grad_threshold=args.densify_grad)
     log = []
     t1 = time.time()
     ctx.train(cfg, poses, images, is_test=is_test, extent=0.0, output_dir=args.out,
@@ -78,6 +83,7 @@ def main():
     metrics = [json.loads(l) for l in open(os.path.join(args.out, "metrics.jsonl"))]
     print(json.dumps({
         "config": "C5 roaming scene (synthetic, 3 rooms), 1520x760 ERP, bottom 48 rows masked, osplat_gpu_train",
+        "prune_radius_px": args.prune_radius, "densify_grad_threshold": args.densify_grad,
         "gt_gaussians": gt.n, "views": args.views, "test_views": len(test), "init_gaussians": init.n,
         "iterations": args.iterations, "train_seconds": train_s, "iterations_per_s": args.iterations / train_s,
         "prep_seconds": prep_s, "final_gaussians": int(ctx.n), "heldout_psnr_mean": float(np.mean(ps)),
