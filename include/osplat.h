@@ -220,6 +220,25 @@ OSPLAT_API osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_conf
 OSPLAT_API osplat_status osplat_gpu_adam_step_range(osplat_gpu* ctx, const osplat_config* config, double scene_extent,
                                                     long iteration, int zero_grad, size_t begin, size_t count);
 
+/* ---- evaluation (capi.h:94-105, run_eval eval.cpp:63-116) over in-memory views: views poses
+ * (row-major 4x4 world->camera each) and images; is_test (NULL: none) marks the test split;
+ * split "test" (default when NULL), "train" or "all"; perspective_crop != 0 evaluates on the 6
+ * cube faces (H/2 x H/2, 90 degree FOV) of each panorama instead of the panorama. Render time per
+ * view on the steady clock around the render and its completion (the reference's FPS convention);
+ * PSNR / SSIM in FP64 on the device. Unknown split -> OSPLAT_ERR_INVALID_ARGUMENT, empty split ->
+ * OSPLAT_ERR_VALIDATION (EmptySplit). */
+typedef struct osplat_report osplat_report; /* capi.h — EvalReport (eval.hpp:28-35) */
+OSPLAT_API osplat_status osplat_gpu_eval(osplat_gpu* ctx, size_t views, const double* transforms_cw,
+                                         const osplat_image* const* images, const unsigned char* is_test,
+                                         const char* split, int perspective_crop, osplat_report** out);
+OSPLAT_API size_t osplat_report_view_count(const osplat_report* report);
+OSPLAT_API osplat_status osplat_report_view(const osplat_report* report, size_t index, int* frame_index,
+                                            double* psnr, double* ssim);
+OSPLAT_API osplat_status osplat_report_mean(const osplat_report* report, double* psnr, double* ssim,
+                                            double* seconds_per_frame, double* fps);
+OSPLAT_API const char* osplat_report_mode(const osplat_report* report);
+OSPLAT_API void osplat_report_free(osplat_report* report);
+
 /* ---- §8(e) multi-view data parallelism inside the library: one process (context) per GPU, one
  * NCCL communicator per context, every collective issued by the library on the context stream.
  * NCCL is loaded at run time (libnccl.so.2; the one already mapped by the process if any);

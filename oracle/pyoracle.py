@@ -339,6 +339,15 @@ class Oracle:
         self.lib.oracle_metrics(_ptr(a), _ptr(b), a.shape[1], a.shape[0], C.byref(ps), C.byref(ss))
         return ps.value, ss.value
 
+    def cube_crops(self, pano, size: int):
+        """The 6 cube-face perspective crops (eval.cpp:10-61) of an H x W x 3 panorama; reference only."""
+        pano = np.ascontiguousarray(pano, dtype=np.float64)
+        out = np.zeros((6, size, size, 3))
+        fn = self.lib.oracle_ref_cube_crops
+        fn.argtypes, fn.restype = [_dp, C.c_int, C.c_int, C.c_int, _dp], None
+        fn(_ptr(pano), pano.shape[1], pano.shape[0], size, _ptr(out))
+        return out
+
     def densify_and_prune(self, cloud, norm_sum, hits, max_radius, state: AdamState, cfg: DensifyConfig,
                           extent: float, seed: int, radius_prune_active: bool):
         """densify_and_prune (trainer.cpp:188-275) -> (new cloud, new AdamState, summary dict)."""

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "omnisplat/dataio.hpp"
+#include "omnisplat/eval.hpp"
 #include "omnisplat/gradients.hpp"
 #include "omnisplat/metrics.hpp"
 #include "omnisplat/parallel.hpp"
@@ -312,6 +313,17 @@ double oracle_loss(const double* r, const double* gt, int w, int h, double lambd
     }
     if (d_image) std::memcpy(d_image, lr.d_image.data.data(), lr.d_image.data.size() * 8);
     return lr.value;
+}
+
+// cube_faces(size) + perspective_crop (eval.cpp:10-61): the 6 S x S x 3 crops of an H x W x 3 panorama.
+void oracle_ref_cube_crops(const double* pano, int w, int h, int size, double* out) {
+    Image p(w, h);
+    std::memcpy(p.data.data(), pano, p.data.size() * 8);
+    const auto faces = cube_faces(size);
+    for (std::size_t k = 0; k < faces.size(); ++k) {
+        Image c = perspective_crop(p, faces[k]);
+        std::memcpy(out + k * c.data.size(), c.data.data(), c.data.size() * 8);
+    }
 }
 
 void oracle_metrics(const double* a, const double* b, int w, int h, double* out_psnr, double* out_ssim) {

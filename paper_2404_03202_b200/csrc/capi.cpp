@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <charconv>
+#include <chrono>
 #include <cstring>
 #include <filesystem>
 #include <fstream>
@@ -42,6 +43,17 @@ struct osplat_image {
     size_t pinned_bytes = 0;
     const double* px() const { return pinned ? pinned : data.data(); }
     ~osplat_image();
+};
+
+// EvalReport (eval.hpp:28-35)
+struct osplat_report {
+    struct View {
+        int frame_index;
+        double psnr, ssim;
+    };
+    std::vector<View> views;
+    double mean_psnr = 0.0, mean_ssim = 0.0, seconds_per_frame = 0.0, fps = 0.0;
+    std::string mode;
 };
 
 namespace {
@@ -110,7 +122,7 @@ namespace {
 
 // Reference ErrorCode subset used on this path (error.hpp:8-25) and its status mapping.
 enum class Code { ValidationError, StateMismatch, DimensionMismatch, ParseError, UnsupportedFormat, MissingProperty,
-                  VersionMismatch, IoError, InvalidArgument };
+                  VersionMismatch, IoError, InvalidArgument, EmptySplit };
 
 struct ApiError : std::runtime_error {
     Code code;
@@ -128,6 +140,7 @@ const char* code_name(Code c) {
         case Code::VersionMismatch: return "VersionMismatch";
         case Code::IoError: return "IoError";
         case Code::InvalidArgument: return "InvalidArgument";
+        case Code::EmptySplit: return "EmptySplit";
     }
     return "Unknown";
 }
@@ -138,6 +151,7 @@ osplat_status map_code(Code c) {  // capi.cpp:41-66
         case Code::MissingProperty: return OSPLAT_ERR_PARSE;
         case Code::ValidationError:
         case Code::DimensionMismatch:
+        case Code::EmptySplit:
         case Code::StateMismatch: return OSPLAT_ERR_VALIDATION;
         case Code::UnsupportedFormat:
         case Code::VersionMismatch: return OSPLAT_ERR_UNSUPPORTED;
@@ -1228,6 +1242,131 @@ osplat_status osplat_gpu_train(osplat_gpu* ctx, const osplat_config* config, siz
         }
     });
 }
+
+// osplat_eval (capi.cpp:298-306 -> run_eval, eval.cpp:63-116) over in-memory views: the split's
+// views rendered one by one, each render timed with the steady clock around the call and its
+// completion (the reference times render(); FPS = 1 / mean seconds), PSNR / SSIM against the
+// view's image in FP64 on the device — on the panorama, or averaged over the 6 cube-face
+// perspective crops of size H/2 (eval.cpp:10-19, 44-61).
+osplat_status osplat_gpu_eval(osplat_gpu* ctx, size_t views, const double* transforms_cw,
+                              const osplat_image* const* images, const unsigned char* is_test, const char* split,
+                              int perspective_crop, osplat_report** out) {
+    if (!ctx || !transforms_cw || !images || !out) return invalid("osplat_gpu_eval: null argument");
+    return wrap([&] {
+        const std::string sp = split ? split : "test";
+        std::vector<int> idx;
+        for (size_t v = 0; v < views; ++v) {
+            const bool test = is_test && is_test[v];
+            if (sp == "all" || (sp == "test" && test) || (sp == "train" && !test)) idx.push_back(static_cast<int>(v));
+        }
+        if (sp != "all" && sp != "test" && sp != "train") throw ApiError(Code::InvalidArgument, "unknown split: " + sp);
+        if (idx.empty()) throw ApiError(Code::EmptySplit, "split '" + sp + "' is empty");
+        Engine& e = *ctx->engine;
+        osb::DeviceGuard g(e.device());
+        auto rep = std::make_unique<osplat_report>();
+        rep->mode = perspective_crop ? "perspective-crop" : "omnidirectional";
+        const int W = images[idx[0]]->width, H = images[idx[0]]->height;
+        const size_t px = static_cast<size_t>(W) * H;
+        const int S = H / 2;  // cube_faces(dataset.cam.height / 2)
+        const size_t crop_px = static_cast<size_t>(S) * S;
+        const size_t big = std::max(px, crop_px);
+        osb::DevBuf gt, crops, maps, sums;
+        gt.ensure(px * 3 * sizeof(double));
+        crops.ensure(crop_px * 6 * sizeof(double) + 64);
+        maps.ensure(big * 15 * sizeof(double));
+        sums.ensure(4 * sizeof(double));
+        const double faces[6][2] = {{0.0, 0.0}, {osb::kPi / 2.0, 0.0}, {osb::kPi, 0.0}, {3.0 * osb::kPi / 2.0, 0.0},
+                                    {0.0, osb::kPi / 2.0}, {0.0, -osb::kPi / 2.0}};
+        auto metrics = [&](const double* a, const double* b, int w, int h, double* ps, double* ss) {
+            double hs[4];
+            osb::launch_metrics_f64(a, b, w, h, maps.as<double>(), sums.as<double>(), e.stream());
+            OSB_CUDA_CHECK(cudaMemcpyAsync(hs, sums.as<double>(), sizeof(hs), cudaMemcpyDeviceToHost, e.stream()));
+            OSB_CUDA_CHECK(cudaStreamSynchronize(e.stream()));
+            const double mse = hs[0] / (static_cast<double>(w) * h * 3.0);
+            *ps = mse <= 0.0 ? 99.0 : std::min(99.0, 10.0 * std::log10(1.0 / mse));
+            *ss = (hs[1] / (static_cast<double>(w) * h) + hs[2] / (static_cast<double>(w) * h) +
+                   hs[3] / (static_cast<double>(w) * h)) / 3.0;
+        };
+        double total = 0.0;
+        const double bg[3] = {0.0, 0.0, 0.0};
+        for (int v : idx) {
+            const osplat_image* im = images[v];
+            if (!im || im->width != W || im->height != H)
+                throw ApiError(Code::DimensionMismatch, "evaluation images differ in size");
+            double p12[12];
+            checked_pose(transforms_cw + 16 * static_cast<size_t>(v), p12);
+            OSB_CUDA_CHECK(cudaStreamSynchronize(e.stream()));
+            const auto t0 = std::chrono::steady_clock::now();
+            osb::Frame* f = e.render(p12, W, H, bg);
+            try {
+                e.validate(f);
+                OSB_CUDA_CHECK(cudaStreamSynchronize(e.stream()));
+                total += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+                OSB_CUDA_CHECK(cudaMemcpyAsync(gt.as<double>(), im->px(), px * 3 * sizeof(double),
+                                               cudaMemcpyHostToDevice, e.stream()));
+                const double* rgb = e.image_hwc_device(f);
+                osplat_report::View rv{v, 0.0, 0.0};
+                if (!perspective_crop) {
+                    metrics(rgb, gt.as<double>(), W, H, &rv.psnr, &rv.ssim);
+                } else {
+                    double* rc = crops.as<double>();
+                    double* gc = rc + crop_px * 3;
+                    for (const auto& fc : faces) {
+                        osb::launch_perspective_crop(rgb, W, H, S, fc[0], fc[1], rc, e.stream());
+                        osb::launch_perspective_crop(gt.as<double>(), W, H, S, fc[0], fc[1], gc, e.stream());
+                        double ps, ss;
+                        metrics(rc, gc, S, S, &ps, &ss);
+                        rv.psnr += ps;
+                        rv.ssim += ss;
+                    }
+                    rv.psnr /= 6.0;
+                    rv.ssim /= 6.0;
+                }
+                rep->views.push_back(rv);
+                rep->mean_psnr += rv.psnr;
+                rep->mean_ssim += rv.ssim;
+            } catch (...) {
+                e.release(f);
+                throw;
+            }
+            e.release(f);
+        }
+        rep->mean_psnr /= rep->views.size();
+        rep->mean_ssim /= rep->views.size();
+        rep->seconds_per_frame = total / rep->views.size();
+        rep->fps = rep->seconds_per_frame > 0.0 ? 1.0 / rep->seconds_per_frame : 0.0;
+        *out = rep.release();
+    });
+}
+
+size_t osplat_report_view_count(const osplat_report* report) { return report ? report->views.size() : 0; }
+
+osplat_status osplat_report_view(const osplat_report* report, size_t index, int* frame_index, double* psnr,
+                                 double* ssim) {
+    if (!report) return invalid("osplat_report_view: null report");
+    if (index >= report->views.size()) return invalid("osplat_report_view: index out of range");
+    const auto& v = report->views[index];
+    if (frame_index) *frame_index = v.frame_index;
+    if (psnr) *psnr = v.psnr;
+    if (ssim) *ssim = v.ssim;
+    t_last_error.clear();
+    return OSPLAT_OK;
+}
+
+osplat_status osplat_report_mean(const osplat_report* report, double* psnr, double* ssim, double* seconds_per_frame,
+                                 double* fps) {
+    if (!report) return invalid("osplat_report_mean: null report");
+    if (psnr) *psnr = report->mean_psnr;
+    if (ssim) *ssim = report->mean_ssim;
+    if (seconds_per_frame) *seconds_per_frame = report->seconds_per_frame;
+    if (fps) *fps = report->fps;
+    t_last_error.clear();
+    return OSPLAT_OK;
+}
+
+const char* osplat_report_mode(const osplat_report* report) { return report ? report->mode.c_str() : ""; }
+
+void osplat_report_free(osplat_report* report) { delete report; }
 
 osplat_status osplat_gpu_adam_step(osplat_gpu* ctx, const osplat_config* config, double extent, long iteration,
                                    int zero_grad) {

@@ -643,6 +643,15 @@ double Engine::loss_value(const Frame* f, double mask_bottom_fraction) {
     return value;
 }
 
+const double* Engine::image_hwc_device(Frame* f) {
+    DeviceGuard g(device_);
+    validate(f);
+    const size_t plane = static_cast<size_t>(f->W) * f->H;
+    hwc_.ensure(plane * 3 * sizeof(double));
+    launch_planar_to_hwc_f64(f->rgb.as<float>(), plane, hwc_.as<double>(), stream_);
+    return hwc_.as<double>();
+}
+
 void Engine::image_hwc(Frame* f, double* host) {
     DeviceGuard g(device_);
     validate(f);

@@ -144,6 +144,8 @@ public:
     // The frame's colour as H x W x 3 doubles (Image layout, image.hpp:10-23) in host memory:
     // converted on the device, one D2H copy (full speed into pinned memory), synchronous.
     void image_hwc(Frame* f, double* host);
+    // The same conversion into a device buffer owned by the engine (valid until the next call).
+    const double* image_hwc_device(Frame* f);
     // Adam over all planes, or over the flat element range [begin, begin + count) (multiples of 4;
     // a data-parallel rank's shard after a reduce-scatter of the gradients).
     void adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad, size_t begin = 0,

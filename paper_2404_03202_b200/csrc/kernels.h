@@ -132,6 +132,9 @@ void launch_sq_err(const float* a, const float* b, long n, double* out, cudaStre
 // osplat_metrics (metrics.cu): two H x W x 3 FP64 images -> sums[0] = sum (a - b)^2,
 // sums[1..3] = per-channel sums of the SSIM map (metrics.cpp:17-79). maps: 15 W H doubles.
 void launch_metrics_f64(const double* a, const double* b, int W, int H, double* maps, double* sums, cudaStream_t s);
+// perspective_crop (eval.cpp:21-61) of an H x W x 3 FP64 panorama into an S x S x 3 pinhole view.
+void launch_perspective_crop(const double* pano, int W, int H, int S, double yaw, double pitch, double* out,
+                             cudaStream_t s);
 
 // ---- densification (densify.cu) -------------------------------------------------------------
 struct DensifyArgs {

@@ -8,6 +8,7 @@
 //   k_metric_sq:   sum (a - b)^2 over all 3 H W values (psnr's MSE numerator, metrics.cpp:64-74).
 #include <cmath>
 
+#include "common.cuh"
 #include "kernels.h"
 
 namespace osb {
@@ -100,7 +101,51 @@ __global__ void __launch_bounds__(256) k_metric_sq(const double* __restrict__ a,
     if (threadIdx.x == 0) atomicAdd(out, t);
 }
 
+// perspective_crop (eval.cpp:21-61): pinhole S x S view of an H x W x 3 panorama, 90 degree field
+// of view, pitch about X then yaw about Y (cos / sin from the host, as the reference's libm gives
+// them), the ray projected with project_equirect (camera.cpp:25-39) and sampled bilinearly with the
+// seam wrapped horizontally and rows clamped.
+__global__ void k_perspective_crop(const double* __restrict__ pano, int W, int H, int S, double cp, double sp,
+                                   double cyw, double syw, double* __restrict__ out) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int y = blockIdx.y;
+    if (x >= S) return;
+    const double f = S * 0.5, c = S * 0.5;
+    const double dx = (x + 0.5 - c) / f, dy = (y + 0.5 - c) / f, dz = 1.0;
+    const double px = dx, py = cp * dy - sp * dz, pz = sp * dy + cp * dz;
+    const double tx = cyw * px + syw * pz, ty = py, tz = -syw * px + cyw * pz;
+    const double tr = sqrt(tx * tx + ty * ty + tz * tz);
+    double lon = atan2(tx, tz);
+    if (lon >= kPi) lon -= 2.0 * kPi;
+    double sine = ty / tr;
+    sine = sine < -1.0 ? -1.0 : (sine > 1.0 ? 1.0 : sine);
+    const double lat = asin(sine);
+    const double sx = lon / kPi, sy = 2.0 * lat / kPi;
+    const double gx = (sx + 1.0) * W * 0.5 - 0.5, gy = (sy + 1.0) * H * 0.5 - 0.5;
+    const int x0 = static_cast<int>(floor(gx)), y0 = static_cast<int>(floor(gy));
+    const double fx = gx - x0, fy = gy - y0;
+    const int xa = ((x0 % W) + W) % W, xb = (((x0 + 1) % W) + W) % W;
+    const int ya = min(max(y0, 0), H - 1), yb = min(max(y0 + 1, 0), H - 1);
+    for (int ch = 0; ch < 3; ++ch) {
+        const double v00 = pano[(static_cast<size_t>(ya) * W + xa) * 3 + ch];
+        const double v10 = pano[(static_cast<size_t>(ya) * W + xb) * 3 + ch];
+        const double v01 = pano[(static_cast<size_t>(yb) * W + xa) * 3 + ch];
+        const double v11 = pano[(static_cast<size_t>(yb) * W + xb) * 3 + ch];
+        out[(static_cast<size_t>(y) * S + x) * 3 + ch] =
+            (1 - fy) * ((1 - fx) * v00 + fx * v10) + fy * ((1 - fx) * v01 + fx * v11);
+    }
+}
+
 }  // namespace
+
+void launch_perspective_crop(const double* pano, int W, int H, int S, double yaw, double pitch, double* out,
+                             cudaStream_t s) {
+    if (S <= 0) return;
+    const dim3 grid((S + 127) / 128, S);
+    k_perspective_crop<<<grid, 128, 0, s>>>(pano, W, H, S, std::cos(pitch), std::sin(pitch), std::cos(yaw),
+                                            std::sin(yaw), out);
+    OSB_LAUNCHED(1);
+}
 
 void launch_metrics_f64(const double* a, const double* b, int W, int H, double* maps, double* sums, cudaStream_t s) {
     Win64 win;

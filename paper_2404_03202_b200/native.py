@@ -129,6 +129,12 @@ def _load():
         "osplat_gpu_load_state": (S, [_vp, C.c_char_p, _lp]),
         "osplat_image_create": (S, [C.c_int, C.c_int, _dp, C.POINTER(_vp)]),
         "osplat_metrics": (S, [_vp, _vp, _dp, _dp]),
+        "osplat_gpu_eval": (S, [_vp, C.c_size_t, _dp, C.POINTER(_vp), _u8p, C.c_char_p, C.c_int, C.POINTER(_vp)]),
+        "osplat_report_view_count": (C.c_size_t, [_vp]),
+        "osplat_report_view": (S, [_vp, C.c_size_t, _ip, _dp, _dp]),
+        "osplat_report_mean": (S, [_vp, _dp, _dp, _dp, _dp]),
+        "osplat_report_mode": (C.c_char_p, [_vp]),
+        "osplat_report_free": (None, [_vp]),
         "osplat_gpu_train": (S, [_vp, _vp, C.c_size_t, _dp, C.POINTER(_vp), _u8p, C.c_double, C.c_long, C.c_char_p,
                                  PROGRESS_FN, C.c_void_p]),
         "osplat_frame_work": (S, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
@@ -408,6 +414,39 @@ class Context:
         v = GpuView()
         check(lib.osplat_gpu_view_buffers(self.handle, C.byref(v)))
         return v
+
+    def eval(self, poses, images, is_test=None, split: str = "test", perspective_crop: bool = False) -> dict:
+        """osplat_gpu_eval (osplat_eval / run_eval over in-memory views): per-view PSNR / SSIM, means,
+        seconds per frame and FPS (render only, steady clock), mode."""
+        T = np.ascontiguousarray(np.stack([transform_of(p) for p in poses]), dtype=np.float64)
+        handles = []
+        try:
+            for im in images:
+                im = np.ascontiguousarray(im, dtype=np.float64)
+                h = _vp()
+                check(lib.osplat_image_create(im.shape[1], im.shape[0], _p(im), C.byref(h)))
+                handles.append(h)
+            arr = (_vp * len(handles))(*handles)
+            flags = None if is_test is None else np.ascontiguousarray(is_test, dtype=np.uint8)
+            rep = _vp()
+            check(lib.osplat_gpu_eval(self.handle, len(handles), _p(T), arr,
+                                      _p(flags, _u8p) if flags is not None else None, split.encode(),
+                                      int(perspective_crop), C.byref(rep)))
+        finally:
+            for h in handles:
+                lib.osplat_image_free(h)
+        try:
+            views = []
+            for i in range(lib.osplat_report_view_count(rep)):
+                fi, ps, ss = C.c_int(0), C.c_double(0), C.c_double(0)
+                check(lib.osplat_report_view(rep, i, C.byref(fi), C.byref(ps), C.byref(ss)))
+                views.append((fi.value, ps.value, ss.value))
+            mp, ms, spf, fps = C.c_double(0), C.c_double(0), C.c_double(0), C.c_double(0)
+            check(lib.osplat_report_mean(rep, C.byref(mp), C.byref(ms), C.byref(spf), C.byref(fps)))
+            return {"views": views, "mean_psnr": mp.value, "mean_ssim": ms.value, "seconds_per_frame": spf.value,
+                    "fps": fps.value, "mode": lib.osplat_report_mode(rep).decode()}
+        finally:
+            lib.osplat_report_free(rep)
 
     def dp_init(self, world: int, rank: int, unique_id: bytes):
         """osplat_gpu_dp_init: this context becomes rank `rank` of a `world`-GPU data-parallel job

@@ -17,7 +17,9 @@ HEADER = os.path.join(ROOT, "include", "osplat.h")
 REFERENCE_SYMBOLS = ["osplat_version", "osplat_last_error", "osplat_set_threads", "osplat_cloud_load",
                      "osplat_cloud_save", "osplat_cloud_count", "osplat_cloud_free", "osplat_config_create",
                      "osplat_config_set", "osplat_config_free", "osplat_render", "osplat_image_width",
-                     "osplat_image_height", "osplat_image_pixels", "osplat_image_free", "osplat_metrics"]
+                     "osplat_image_height", "osplat_image_pixels", "osplat_image_free", "osplat_metrics",
+                     "osplat_report_view_count", "osplat_report_view", "osplat_report_mean", "osplat_report_mode",
+                     "osplat_report_free"]
 
 
 def declared_symbols():

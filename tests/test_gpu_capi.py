@@ -72,3 +72,45 @@ def test_concurrent_osplat_render_on_one_cloud():
     assert len(results) == 4 * len(poses)
     for j, img in results.values():
         assert np.array_equal(img, expect[j])
+
+
+@pytest.mark.parametrize("crop", [False, True], ids=["omnidirectional", "perspective_crop"])
+def test_osplat_gpu_eval_matches_reference_metrics(crop, oracle_ref):
+    """osplat_gpu_eval (osplat_eval / run_eval, eval.cpp:63-116): per-view PSNR / SSIM of the GPU
+    render against each target equal the reference's psnr / ssim of the same images (on the
+    panorama, or averaged over its 6 cube-face crops made by the reference's perspective_crop)."""
+    cloud = scenes.synthetic_cloud(30_000, seed=5)
+    target = scenes.synthetic_cloud(30_000, seed=6)
+    poses = scenes.ring_poses(6, seed=7)
+    W, H = 256, 128
+    t = native.Context(target)
+    images = []
+    for p in poses:
+        fr = t.render(p, W, H)
+        images.append(fr.image())
+        fr.free()
+    is_test = [k % 2 == 0 for k in range(len(poses))]
+    ctx = native.Context(cloud)
+    rep = ctx.eval(poses, images, is_test, split="test", perspective_crop=crop)
+    assert rep["mode"] == ("perspective-crop" if crop else "omnidirectional")
+    assert [v[0] for v in rep["views"]] == [0, 2, 4]
+    assert rep["fps"] > 0 and abs(rep["fps"] * rep["seconds_per_frame"] - 1.0) < 1e-9
+    for fi, ps, ss in rep["views"]:
+        fr = ctx.render(poses[fi], W, H)
+        img = fr.image()
+        fr.free()
+        if crop:
+            rc, gc = oracle_ref.cube_crops(img, H // 2), oracle_ref.cube_crops(images[fi], H // 2)
+            ms = [oracle_ref.metrics(rc[k], gc[k]) for k in range(6)]
+            pr, sr = np.mean([m[0] for m in ms]), np.mean([m[1] for m in ms])
+        else:
+            pr, sr = oracle_ref.metrics(img, images[fi])
+        assert abs(ps - pr) <= 1e-8 * abs(pr) and abs(ss - sr) <= 1e-10, (fi, ps, pr, ss, sr)
+    assert abs(rep["mean_psnr"] - np.mean([v[1] for v in rep["views"]])) < 1e-9
+    assert len(ctx.eval(poses, images, is_test, split="all")["views"]) == 6
+    with pytest.raises(native.OsplatError) as e:
+        ctx.eval(poses, images, None, split="test")
+    assert e.value.status == native.VALIDATION and e.value.message.startswith("EmptySplit: ")
+    with pytest.raises(native.OsplatError) as e:
+        ctx.eval(poses, images, is_test, split="bogus")
+    assert e.value.status == native.INVALID_ARGUMENT
