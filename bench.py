@@ -561,10 +561,16 @@ def run_ours(args):
         def e2e_step():
             s = step_idx[0]
             slot = sums_host[len(losses) % sums_host.shape[0]]
-            for k, vi in enumerate(step_views(s, rank, world, V)):
+            views = step_views(s, rank, world, V)
+            losses.append(slot)
+            if world == 1 and V == 1:  # the reference's one-view iteration: backward + Adam fused
+                ctx.train_step_async(poses[views[0]], W, H, host_gt[views[0]].data_ptr(), False, slot[0].data_ptr(),
+                                     cfg, extent, s + 1, lambda_ssim=LAMBDA_SSIM)
+                step_idx[0] += 1
+                return
+            for k, vi in enumerate(views):
                 ctx.train_view_async(poses[vi], W, H, host_gt[vi].data_ptr(), gt_on_device=False,
                                      sums_ptr=slot[k].data_ptr(), lambda_ssim=LAMBDA_SSIM)
-            losses.append(slot)
             if native_dp:
                 ctx.dp_step(cfg, extent, s + 1)
             elif world > 1:
@@ -593,9 +599,10 @@ def run_ours(args):
         e2e = {"value": world * V * e2e_steps / e2e_s, "unit": "views/s", "steps": e2e_steps,
                "h2d_bytes_per_step": V * 3 * plane * 4, "d2h_bytes_per_step": V * 32,
                "loss_first_last": [step_losses[0], step_losses[-1]],
-               "api": "osplat_gpu_train_view_async (pinned host target in, loss sums out to pinned host every "
-                      "step, one wait at the end) + osplat_gpu_adam_step (N > 1: osplat_gpu_dp_step = NCCL "
-                      "reduce-scatter + sharded Adam + all-gather inside the library)"}
+               "api": "N = 1, one view: osplat_gpu_train_step_async (pinned host target in, render + loss + "
+                      "backward + Adam fused, loss sums out to pinned host every step, one wait at the end); "
+                      "otherwise osplat_gpu_train_view_async per view + osplat_gpu_adam_step (N > 1: "
+                      "osplat_gpu_dp_step = NCCL reduce-scatter + sharded Adam + all-gather inside the library)"}
         if rank == 0:
             hc = native.HostCloud.from_cloud(cloud)
             native.osplat_render(hc, poses[0], W, H)  # upload + warm

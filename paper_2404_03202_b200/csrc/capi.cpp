@@ -1020,6 +1020,15 @@ osplat_status osplat_gpu_backward(osplat_gpu* ctx, const osplat_frame* frame, co
     });
 }
 
+osplat_status osplat_gpu_backward_step(osplat_gpu* ctx, const osplat_frame* frame, const float* d_image_planar,
+                                       const osplat_config* config, double extent, long iteration) {
+    if (!ctx || !frame || !d_image_planar) return invalid("osplat_gpu_backward_step: null argument");
+    return wrap([&] {
+        validate_frame(ctx, frame);
+        ctx->engine->backward_step(frame->frame, d_image_planar, hyper_from(config), extent, iteration);
+    });
+}
+
 osplat_status osplat_gpu_backward_device(osplat_gpu* ctx, const osplat_frame* frame, const float* d_image_planar,
                                          int accumulate) {
     if (!ctx || !frame || !d_image_planar) return invalid("osplat_gpu_backward_device: null argument");
@@ -1416,14 +1425,29 @@ osplat_status osplat_gpu_l1_loss(osplat_gpu* ctx, const osplat_frame* frame, con
 }
 
 namespace {
+struct FusedStep {
+    const osplat_config* config;
+    double extent;
+    long iteration;
+};
 osplat_status train_view_impl(osplat_gpu* ctx, const double transform_cw[16], int width, int height, const float* gt,
-                              int gt_on_device, double lambda_ssim, double mask, double* loss, double* sums_pinned);
+                              int gt_on_device, double lambda_ssim, double mask, double* loss, double* sums_pinned,
+                              const FusedStep* step = nullptr);
 }
 
 osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
                                     const float* gt, int gt_on_device, double lambda_ssim, double mask,
                                     double* loss) {
     return train_view_impl(ctx, transform_cw, width, height, gt, gt_on_device, lambda_ssim, mask, loss, nullptr);
+}
+
+osplat_status osplat_gpu_train_step_async(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
+                                          const float* gt, int gt_on_device, double lambda_ssim, double mask,
+                                          const osplat_config* config, double extent, long iteration,
+                                          double* loss_sums) {
+    const FusedStep step{config, extent, iteration};
+    return train_view_impl(ctx, transform_cw, width, height, gt, gt_on_device, lambda_ssim, mask, nullptr, loss_sums,
+                           &step);
 }
 
 osplat_status osplat_gpu_train_view_async(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
@@ -1445,7 +1469,8 @@ double osplat_loss_value(const double sums[4], double lambda_ssim, int width, in
 
 namespace {
 osplat_status train_view_impl(osplat_gpu* ctx, const double transform_cw[16], int width, int height, const float* gt,
-                              int gt_on_device, double lambda_ssim, double mask, double* loss, double* sums_pinned) {
+                              int gt_on_device, double lambda_ssim, double mask, double* loss, double* sums_pinned,
+                              const FusedStep* step) {
     if (!ctx || !transform_cw || !gt) return invalid("osplat_gpu_train_view: null argument");
     if (lambda_ssim < 0.0 || lambda_ssim > 1.0) return invalid("osplat_gpu_train_view: lambda_ssim must be in [0, 1]");
     if (mask < 0.0 || mask >= 1.0) return invalid("osplat_gpu_train_view: mask_bottom_fraction must be in [0, 1)");
@@ -1466,7 +1491,10 @@ osplat_status train_view_impl(osplat_gpu* ctx, const double transform_cw[16], in
             (void)v;
             if (!gt_on_device) e.release_target();
             const size_t pixels = plane;
-            e.backward(f, e.d_image_buffer(pixels), true);
+            if (step)
+                e.backward_step(f, e.d_image_buffer(pixels), hyper_from(step->config), step->extent, step->iteration);
+            else
+                e.backward(f, e.d_image_buffer(pixels), true);
             if (loss) {
                 // the L1 sum lives on the device; one 8-byte read completes the step
                 *loss = e.loss_value(f, mask);
