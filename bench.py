@@ -303,11 +303,15 @@ class CudaArray:
 
 
 def run_ours(args):
+    rank, world, local = dist_env()
+    if os.environ.get("OSPLAT_BENCH_DRYRUN"):  # launcher test (tests/test_bench_cpu.py): report and exit
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local, "gpus": args.gpus,
+                          "master": f"{os.environ.get('MASTER_ADDR')}:{os.environ.get('MASTER_PORT')}"}), flush=True)
+        return
     import torch
     import torch.distributed as dist
     from paper_2404_03202_b200 import dp, native, scenes
 
-    rank, world, local = dist_env()
     if args.gpus != world:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if not torch.cuda.is_available():
@@ -627,13 +631,17 @@ def run_ours(args):
     planes = engine.grad_tensor().numel()
     # algorithmic bytes per launch; K3/K4a: pairs x the kernel's measured warp
     # instructions per pair (ncu, profiles/ncu_kernels.json) -> issue-slot utilisation
+    fused = world == 1 and V == 1  # the step runs osplat_gpu_backward_step (SH Adam inside bwd_gauss)
     hbm = {
         "preprocess": N * (44 + 12 * 16) + N * 44,
         "depth_sort": N * 12 * 2 * 8,
         "tile_sort": instances * 32,
         "loss": plane * 36,
-        "bwd_gauss": N * 520,
-        "adam": 28 * planes / (world if world > 1 else 1),  # sharded: this rank's 1/N of p, g, m, v
+        # fused: k_sh_adam reads / writes p, m, v of the 48 SH planes (1152 B) + position, colour
+        # gradient and view-direction sums (~60 B); K4b geometry ~240 B / Gaussian
+        "bwd_gauss": N * (1212 + 240) if fused else N * 520,
+        # p, g, m, v in, p, m, v out: all planes, the 11 geometry planes (fused), or this rank's 1/N
+        "adam": 28 * (11 * planes // 59 if fused else planes / world),
     }
     pairs = {"blend": fwd_pairs, "bwd_pixels": bwd_pairs}
     rooflines = {}

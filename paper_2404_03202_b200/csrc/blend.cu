@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
     float T = 1.0f, c2 = 0.0f;
     float2 c01 = make_float2(0.0f, 0.0f);  // (c0, c1), updated with one packed FFMA2
     double T64 = 1.0;
+    float Terr = 0.0f;  // bound on alpha-error propagation into T (exact mode: not needed)
     bool exact = false;
     int contrib = 0, last = 0;
     int stop_at = static_cast<int>(range.y - range.x);  // entries evaluated (work counting)
@@ -112,9 +113,24 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                 }
                 float w;
                 if (!exact) {
-                    const float Tn = T * (1.0f - alpha);
-                    if (Tn < kTHi) {
-                        if (Tn < kTLo) {
+                    const float one_m = 1.0f - alpha;
+                    const float Tn = T * one_m;
+                    // relative error bound of the FP32 T (common.cuh): alpha / (1 - alpha) x alpha's
+                    // relative error bound; the per-step rounding term is added from `contrib`
+                    float inv;
+                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));
+                    const float dlt = fabsf(B.w);
+                    Terr = __fmaf_rn(alpha * inv, __fmaf_rn(dlt, 1.001f + dlt, kAlphaErr), Terr);
+                    // Terr <= 0.2 and < 4e5 steps keep e <= 0.25: T_next >= kTPre is then certain
+                    bool near = Tn < kTPre || Terr > 0.2f;
+                    float em = 0.0f;
+                    if (near) {
+                        const float e = __fmaf_rn(static_cast<float>(contrib + 1), kTStep, Terr);
+                        em = __fmaf_rn(2.0f * e, e, e) + kTMargin;
+                        near = Tn < 1e-4f * (1.0f + em);
+                    }
+                    if (near) {
+                        if (Tn < 1e-4f * (1.0f - em)) {
                             done = true;
                             stop_at = kofs + j;
                             break;

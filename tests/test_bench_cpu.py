@@ -27,3 +27,25 @@ def test_ours_fails_loudly_without_a_gpu():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "1", "--warmup", "1"],
                          capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert out.returncode != 0 and "no CUDA device" in (out.stderr + out.stdout)
+
+
+def test_gpus_n_spawns_n_ranks():
+    """`bench.py --gpus N` outside torchrun launches N ranks itself with the torchrun environment
+    (RANK / LOCAL_RANK / WORLD_SIZE, MASTER_ADDR 127.0.0.1 and one shared port)."""
+    env = dict(os.environ, OSPLAT_BENCH_DRYRUN="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "3", "--steps", "1"],
+                         capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(l) for l in out.stdout.strip().splitlines()]
+    assert sorted(l["rank"] for l in lines) == [0, 1, 2]
+    assert all(l["world"] == 3 and l["gpus"] == 3 and l["local_rank"] == l["rank"] for l in lines)
+    assert len({l["master"] for l in lines}) == 1 and lines[0]["master"].startswith("127.0.0.1:")
+
+
+def test_gpus_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    env.pop("OSPLAT_BENCH_DRYRUN", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "1"],
+                         capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert out.returncode != 0 and "--gpus 4 but WORLD_SIZE=2" in (out.stderr + out.stdout)
