@@ -567,11 +567,6 @@ def run_ours(args):
             slot = sums_host[len(losses) % sums_host.shape[0]]
             views = step_views(s, rank, world, V)
             losses.append(slot)
-            if world == 1 and V == 1:  # the reference's one-view iteration: backward + Adam fused
-                ctx.train_step_async(poses[views[0]], W, H, host_gt[views[0]].data_ptr(), False, slot[0].data_ptr(),
-                                     cfg, extent, s + 1, lambda_ssim=LAMBDA_SSIM)
-                step_idx[0] += 1
-                return
             for k, vi in enumerate(views):
                 ctx.train_view_async(poses[vi], W, H, host_gt[vi].data_ptr(), gt_on_device=False,
                                      sums_ptr=slot[k].data_ptr(), lambda_ssim=LAMBDA_SSIM)
@@ -603,10 +598,9 @@ def run_ours(args):
         e2e = {"value": world * V * e2e_steps / e2e_s, "unit": "views/s", "steps": e2e_steps,
                "h2d_bytes_per_step": V * 3 * plane * 4, "d2h_bytes_per_step": V * 32,
                "loss_first_last": [step_losses[0], step_losses[-1]],
-               "api": "N = 1, one view: osplat_gpu_train_step_async (pinned host target in, render + loss + "
-                      "backward + Adam fused, loss sums out to pinned host every step, one wait at the end); "
-                      "otherwise osplat_gpu_train_view_async per view + osplat_gpu_adam_step (N > 1: "
-                      "osplat_gpu_dp_step = NCCL reduce-scatter + sharded Adam + all-gather inside the library)"}
+               "api": "osplat_gpu_train_view_async per view (pinned host target in, loss sums out to pinned host "
+                      "every step, one wait at the end) + osplat_gpu_adam_step (N > 1: osplat_gpu_dp_step = NCCL "
+                      "reduce-scatter + sharded Adam + all-gather inside the library)"}
         if rank == 0:
             hc = native.HostCloud.from_cloud(cloud)
             native.osplat_render(hc, poses[0], W, H)  # upload + warm
@@ -631,17 +625,13 @@ def run_ours(args):
     planes = engine.grad_tensor().numel()
     # algorithmic bytes per launch; K3/K4a: pairs x the kernel's measured warp
     # instructions per pair (ncu, profiles/ncu_kernels.json) -> issue-slot utilisation
-    fused = world == 1 and V == 1  # the step runs osplat_gpu_backward_step (SH Adam inside bwd_gauss)
     hbm = {
         "preprocess": N * (44 + 12 * 16) + N * 44,
         "depth_sort": N * 12 * 2 * 8,
         "tile_sort": instances * 32,
         "loss": plane * 36,
-        # fused: k_sh_adam reads / writes p, m, v of the 48 SH planes (1152 B) + position, colour
-        # gradient and view-direction sums (~60 B); K4b geometry ~240 B / Gaussian
-        "bwd_gauss": N * (1212 + 240) if fused else N * 520,
-        # p, g, m, v in, p, m, v out: all planes, the 11 geometry planes (fused), or this rank's 1/N
-        "adam": 28 * (11 * planes // 59 if fused else planes / world),
+        "bwd_gauss": N * 520,
+        "adam": 28 * planes / world,  # p, g, m, v in, p, m, v out (N > 1: this rank's 1/N shard)
     }
     pairs = {"blend": fwd_pairs, "bwd_pixels": bwd_pairs}
     rooflines = {}

@@ -114,6 +114,11 @@ OSPLAT_API osplat_status osplat_gpu_set_active_sh_degree(osplat_gpu* ctx, int de
  * Gaussian in a fixed order — so gradients are bit-identical run to run. Default off (K4a's
  * warp-aggregated atomics: same values up to FP32 summation order, about half the cost). */
 OSPLAT_API osplat_status osplat_gpu_set_deterministic(osplat_gpu* ctx, int on);
+/* Verification mode of the blend's T < 1e-4 stop: on != 0 replaces the default
+ * relative 2^-10 guard band by a running bound on the FP32 transmittance's error (built from K1's
+ * per-Gaussian power bound), so every stop decision is provably the FP64 reference's; more pixels
+ * replay in FP64 (slower). Frames of both modes are compared in tests/test_gpu_fullsize.py. */
+OSPLAT_API osplat_status osplat_gpu_set_strict_guard(osplat_gpu* ctx, int on);
 /* Download the current parameters into a new host cloud. */
 OSPLAT_API osplat_status osplat_gpu_download(osplat_gpu* ctx, osplat_cloud** out);
 OSPLAT_API osplat_status osplat_gpu_synchronize(osplat_gpu* ctx);
@@ -196,13 +201,6 @@ OSPLAT_API osplat_status osplat_gpu_view_buffers(osplat_gpu* ctx, osplat_gpu_vie
  * accumulate = 0 the raw-parameter gradients are overwritten (reference semantics); with 1 they
  * are added (multi-view batches). Screen statistics always accumulate (GradientBuffer). */
 OSPLAT_API osplat_status osplat_gpu_backward(osplat_gpu* ctx, const osplat_frame* frame, const double* d_image, int accumulate);
-/* backward (overwrite) + adam_step of a single-view iteration fused (trainer.cpp:363, 381): the SH
- * gradients are consumed by Adam in place and never stored; identical parameters / moments to
- * osplat_gpu_backward_device(accumulate 0) + osplat_gpu_adam_step(zero_grad 1). Single-GPU; the
- * gradient planes are logically zero afterwards (osplat_gpu_gradients reads zeros). */
-OSPLAT_API osplat_status osplat_gpu_backward_step(osplat_gpu* ctx, const osplat_frame* frame,
-                                                  const float* d_image_planar, const osplat_config* config,
-                                                  double scene_extent, long iteration);
 OSPLAT_API osplat_status osplat_gpu_backward_device(osplat_gpu* ctx, const osplat_frame* frame, const float* d_image_planar,
                                          int accumulate);
 /* Raw-parameter gradients in reference GradientBuffer layout (gradients.hpp:16-36). */
@@ -293,13 +291,6 @@ OSPLAT_API osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double tra
 OSPLAT_API osplat_status osplat_gpu_train_view_async(osplat_gpu* ctx, const double transform_cw[16], int width,
                                                      int height, const float* gt, int gt_on_device,
                                                      double lambda_ssim, double mask_bottom_fraction,
-                                                     double* loss_sums);
-/* One whole reference iteration without a host wait: osplat_gpu_train_view_async with the backward
- * and Adam step fused (osplat_gpu_backward_step) — render -> loss -> backward -> adam_step. */
-OSPLAT_API osplat_status osplat_gpu_train_step_async(osplat_gpu* ctx, const double transform_cw[16], int width,
-                                                     int height, const float* gt, int gt_on_device,
-                                                     double lambda_ssim, double mask_bottom_fraction,
-                                                     const osplat_config* config, double scene_extent, long iteration,
                                                      double* loss_sums);
 /* (1 - l) L1 + l (1 - SSIM) from the sums of osplat_gpu_train_view_async (trainer.cpp:54-63). */
 OSPLAT_API double osplat_loss_value(const double sums[4], double lambda_ssim, int width, int height,

@@ -6,7 +6,6 @@
 // log-scale / opacity groups), host-computed bias corrections (one global step, like the
 // reference's AdamState::step). Optionally zeroes the gradient it consumed (saves the separate
 // memset before the next backward). HBM-bound: 28 B (32 B with zeroing) per element.
-#include "adam.cuh"
 #include "kernels.h"
 
 namespace osb {
@@ -16,6 +15,8 @@ namespace {
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __restrict__ g, float4* __restrict__ m,
                                               float4* __restrict__ v, AdamArgs a) {
     const long n4 = (a.begin + a.count) / 4;
+    const float b1 = 0.9f, b2 = 0.999f;
+    const float ob1 = 1.0f - 0.9f, ob2 = 1.0f - 0.999f;
     for (long i = a.begin / 4 + blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4;
          i += static_cast<long>(gridDim.x) * blockDim.x) {
         const int plane = static_cast<int>((i * 4) / a.stride);
@@ -26,7 +27,16 @@ __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __
         float* mv = &mm.x;
         float* vvv = &vv.x;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) adam_elem(pv[k], mv[k], vvv[k], gv[k], lr, a.inv_bias1, a.inv_bias2);
+        for (int k = 0; k < 4; ++k) {
+            const float gr = gv[k];
+            const float mk = b1 * mv[k] + ob1 * gr;
+            const float vk = b2 * vvv[k] + ob2 * gr * gr;
+            const float mhat = mk * a.inv_bias1;
+            const float vhat = vk * a.inv_bias2;
+            pv[k] = pv[k] - lr * mhat / (sqrtf(vhat) + 1e-15f);
+            mv[k] = mk;
+            vvv[k] = vk;
+        }
         p[i] = pp;
         m[i] = mm;
         v[i] = vv;

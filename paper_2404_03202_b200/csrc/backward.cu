@@ -11,7 +11,6 @@
 // K4b replaces pass 3 (gradients.cpp:173-295): one thread per visible Gaussian, FP64 internals,
 // re-derives t, J, Sigma and the conic with the same device code as K1 and accumulates the raw
 // parameter gradients into the flat FP32 plane buffer (allreduce-able as one tensor).
-#include "adam.cuh"
 #include "kernels.h"
 #include "pair.cuh"
 #include "project.cuh"
@@ -267,7 +266,6 @@ __device__ __forceinline__ void put_grad(float* __restrict__ G, int stride, int 
 // cancellation-prone geometry chain below stays FP64.
 template <typename R, bool OVERWRITE>
 struct ShBack {
-    using Real = R;
     const float* P;
     float* G;
     int stride, gid;
@@ -288,9 +286,8 @@ struct ShBack {
     }
 };
 
-template <int DEG, typename S>
-__device__ __forceinline__ void sh_backward(S& s, const typename S::Real* d) {
-    using R = typename S::Real;
+template <int DEG, typename R, bool OVERWRITE>
+__device__ __forceinline__ void sh_backward(ShBack<R, OVERWRITE>& s, const R* d) {
     constexpr R C0 = static_cast<R>(0.28209479177387814);
     constexpr R C1 = static_cast<R>(0.4886025119029199);
     constexpr R C20 = static_cast<R>(1.0925484305920792), C21 = static_cast<R>(-1.0925484305920792),
@@ -325,106 +322,25 @@ __device__ __forceinline__ void sh_backward(S& s, const typename S::Real* d) {
     s.basis(15, C36 * x * (xx - k3 * yy), C36 * (k3 * xx - k3 * yy), -k6 * C36 * x * y, k0);
 }
 
-// The single-view training step's SH part with Adam fused (Engine::backward_step): the SH
-// gradient of basis i is dl_color * b_i (gradients.cpp:202-207) — consumed by the Adam update of
-// the same element in place instead of being written and read back (adam_elem: bit-identical to
-// K5's update of the same gradient). The view-direction sums feed K4b through sdd.
-struct ShAdam {
-    using Real = float;
-    float* P;
-    float* M;
-    float* V;
-    int stride, gid;
-    Planes pl;
-    float dlc[3];
-    float dd[3];
-    const float* lr_plane;
-    float ib1, ib2;
-    __device__ __forceinline__ void basis(int i, float b, float gx, float gy, float gz) {
-        float c[3];
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-            const int q = pl.sh(i, ch);
-            const size_t e = static_cast<size_t>(q) * stride + gid;
-            float p = P[e], m = M[e], v = V[e];
-            c[ch] = p;
-            adam_elem(p, m, v, dlc[ch] * b, lr_plane[q], ib1, ib2);
-            P[e] = p;
-            M[e] = m;
-            V[e] = v;
-        }
-        const float cdot = c[0] * dlc[0] + c[1] * dlc[1] + c[2] * dlc[2];
-        dd[0] += gx * cdot;
-        dd[1] += gy * cdot;
-        dd[2] += gz * cdot;
-    }
-    // Adam with a zero gradient (inactive SH bands, culled Gaussians: the reference's adam_step
-    // updates every element, trainer.cpp:158-177)
-    __device__ __forceinline__ void zero_grad_bands(int first_basis, int bc) {
-        for (int q = pl.sh(first_basis, 0); q < pl.sh(bc, 0); ++q) {
-            const size_t e = static_cast<size_t>(q) * stride + gid;
-            float p = P[e], m = M[e], v = V[e];
-            adam_elem(p, m, v, 0.0f, lr_plane[q], ib1, ib2);
-            P[e] = p;
-            M[e] = m;
-            V[e] = v;
-        }
-    }
-};
-
-template <int DEG>
-__global__ void __launch_bounds__(256) k_sh_adam(float* __restrict__ P, float* __restrict__ M, float* __restrict__ V,
-                                                 int n, int stride, int bc, Pose pose,
-                                                 const uint64_t* __restrict__ depth_key,
-                                                 const Splat32* __restrict__ splat, const float4* __restrict__ acc,
-                                                 AdamArgs a, float4* __restrict__ sdd_out) {
-    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= n) return;
-    const Planes pl{bc};
-    ShAdam sa{P, M, V, stride, gid, pl, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, a.lr_plane, a.inv_bias1, a.inv_bias2};
-    if (depth_key[gid] == ~0ull) {  // culled: zero gradient
-        sa.zero_grad_bands(0, bc);
-        sdd_out[gid] = make_float4(0.f, 0.f, 0.f, 0.f);
-        return;
-    }
-    const float4 a0 = acc[3 * static_cast<size_t>(gid)];
-    const uint32_t neg = __float_as_uint(splat[gid].pad);
-    sa.dlc[0] = (neg & 1u) ? 0.0f : a0.x;
-    sa.dlc[1] = (neg & 2u) ? 0.0f : a0.y;
-    sa.dlc[2] = (neg & 4u) ? 0.0f : a0.z;
-    double m[3] = {load_param(P, stride, 0, gid), load_param(P, stride, 1, gid), load_param(P, stride, 2, gid)};
-    double t[3], t_r, dir[3];
-    world_to_camera(pose, m, t, &t_r);
-    view_dir(pose, t, t_r, dir);
-    const float dirf[3] = {static_cast<float>(dir[0]), static_cast<float>(dir[1]), static_cast<float>(dir[2])};
-    sh_backward<DEG>(sa, dirf);
-    constexpr int active_n = (DEG + 1) * (DEG + 1);
-    sa.zero_grad_bands(active_n, bc);
-    sdd_out[gid] = make_float4(sa.dd[0], sa.dd[1], sa.dd[2], 0.0f);
-}
-
 // K4b. Uses K1's FP64 conic and opacity (conic_o) and its pre-clamp colour sign bits instead of
 // re-deriving them; re-derives t, J, W-rotated J, Sigma3 and the rotation with K1's device code.
-// SHD (the fused single-view step): the SH gradients were consumed by k_sh_adam, which left the
-// view-direction sums in sdd; only the geometry planes are written here.
-template <int DEG, bool OVERWRITE, bool SHD = false>
+template <int DEG, bool OVERWRITE>
 __global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __restrict__ P, int n, int stride, int bc,
                                                             Pose pose, int W, int H,
                                                             const uint64_t* __restrict__ depth_key,
                                                             const double4* __restrict__ conic_o,
                                                             const Splat32* __restrict__ splat,
                                                             const float4* __restrict__ acc, float* __restrict__ G,
-                                                            ScreenStats st, const float4* __restrict__ sdd_in = nullptr) {
+                                                            ScreenStats st) {
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= n) return;
     const Planes pl{bc};
     if (depth_key[gid] == ~0ull) {  // culled: zero gradient (gradients.cpp:82-86), nothing to add
         if (OVERWRITE)
-            for (int q = 0; q < pl.count(); ++q)
-                if (!SHD || q < 3 || q >= pl.rot(0)) G[static_cast<size_t>(q) * stride + gid] = 0.0f;
+            for (int q = 0; q < pl.count(); ++q) G[static_cast<size_t>(q) * stride + gid] = 0.0f;
         return;
     }
-    if (OVERWRITE && !SHD) {  // SH bands above the active degree carry no gradient (gradients.cpp:202-203)
+    if (OVERWRITE) {  // SH bands above the active degree carry no gradient (gradients.cpp:202-203)
         constexpr int active_n = (DEG + 1) * (DEG + 1);
         for (int q = pl.sh(active_n, 0); q < pl.sh(bc, 0); ++q) G[static_cast<size_t>(q) * stride + gid] = 0.0f;
     }
@@ -462,14 +378,7 @@ __global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __re
     // colour: SH coefficients and the view-direction path (gradients.cpp:190-209); the
     // pre-clamp sign gate (:197-200) comes from K1 (same basis, same summation order)
     double d_m_sh[3];
-    if (SHD) {
-        double dir[3];
-        view_dir(pose, t, t_r, dir);
-        const float4 s4 = sdd_in[gid];
-        const double sdd[3] = {s4.x, s4.y, s4.z};
-        const double dd = dot3(dir, sdd);
-        for (int c = 0; c < 3; ++c) d_m_sh[c] = (sdd[c] - dir[c] * dd) * (1.0 / t_r);
-    } else {
+    {
         const uint32_t neg = __float_as_uint(splat[gid].pad);
         ShBack<float, OVERWRITE> sb{P, G, stride, gid, pl,
                   {(neg & 1u) ? 0.0f : a0.x, (neg & 2u) ? 0.0f : a0.y, (neg & 4u) ? 0.0f : a0.z},
@@ -831,29 +740,6 @@ void launch_backward_pixels(const uint32_t* inst_gid, const uint2* ranges, const
         k_backward_pixels<false><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1],
                                                                 bg[2], fb, d_image, acc);
     OSB_LAUNCHED(1);
-}
-
-void launch_backward_step_gaussians(float* params, float* m, float* v, int n, int stride, int bc, int active_degree,
-                                    const Pose& pose, int W, int H, const PreprocessOut& pp, const float4* acc,
-                                    float* grads, const ScreenStats& st, const AdamArgs& adam, float4* sdd,
-                                    cudaStream_t s) {
-    if (n <= 0) return;
-    const int blocks = (n + 127) / 128;
-    switch (active_degree) {
-#define OSB_STEP(D)                                                                                                   \
-    case D:                                                                                                          \
-        k_sh_adam<D><<<(n + 255) / 256, 256, 0, s>>>(params, m, v, n, stride, bc, pose, pp.depth_key, pp.splat, acc, \
-                                                     adam, sdd);                                                     \
-        k_backward_gaussians<D, true, true><<<blocks, 128, 0, s>>>(params, n, stride, bc, pose, W, H, pp.depth_key,  \
-                                                                    pp.conic_o, pp.splat, acc, grads, st, sdd);      \
-        break;
-        OSB_STEP(0)
-        OSB_STEP(1)
-        OSB_STEP(2)
-        default: OSB_STEP(3)
-#undef OSB_STEP
-    }
-    OSB_LAUNCHED(2);
 }
 
 void launch_backward_gaussians(const float* params, int n, int stride, int bc, int active_degree, const Pose& pose,

@@ -14,6 +14,7 @@ namespace osb {
 
 namespace {
 
+template <bool STRICT>
 __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __restrict__ inst_gid,
                                                            const uint2* __restrict__ ranges, PreprocessOut pp, int W,
                                                            int H, int tiles_x, float bg0, float bg1, float bg2,
@@ -115,22 +116,30 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                 if (!exact) {
                     const float one_m = 1.0f - alpha;
                     const float Tn = T * one_m;
-                    // relative error bound of the FP32 T (common.cuh): alpha / (1 - alpha) x alpha's
-                    // relative error bound; the per-step rounding term is added from `contrib`
-                    float inv;
-                    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));
-                    const float dlt = fabsf(B.w);
-                    Terr = __fmaf_rn(alpha * inv, __fmaf_rn(dlt, 1.001f + dlt, kAlphaErr), Terr);
-                    // Terr <= 0.2 and < 4e5 steps keep e <= 0.25: T_next >= kTPre is then certain
-                    bool near = Tn < kTPre || Terr > 0.2f;
-                    float em = 0.0f;
-                    if (near) {
-                        const float e = __fmaf_rn(static_cast<float>(contrib + 1), kTStep, Terr);
-                        em = __fmaf_rn(2.0f * e, e, e) + kTMargin;
-                        near = Tn < 1e-4f * (1.0f + em);
+                    bool near;
+                    float lo;
+                    if (STRICT) {
+                        // relative error bound of the FP32 T (common.cuh): alpha / (1 - alpha) x
+                        // alpha's relative error bound; the per-step rounding term from `contrib`
+                        float inv;
+                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));
+                        const float dlt = fabsf(B.w);
+                        Terr = __fmaf_rn(alpha * inv, __fmaf_rn(dlt, 1.001f + dlt, kAlphaErr), Terr);
+                        // Terr <= 0.2 and < 4e5 steps keep e <= 0.25: T_next >= kTPre is then certain
+                        near = Tn < kTPre || Terr > 0.2f;
+                        lo = 0.0f;
+                        if (near) {
+                            const float e = __fmaf_rn(static_cast<float>(contrib + 1), kTStep, Terr);
+                            const float em = __fmaf_rn(2.0f * e, e, e) + kTMargin;
+                            near = Tn < 1e-4f * (1.0f + em);
+                            lo = 1e-4f * (1.0f - em);
+                        }
+                    } else {
+                        near = Tn < kTHi;
+                        lo = kTLo;
                     }
                     if (near) {
-                        if (Tn < 1e-4f * (1.0f - em)) {
+                        if (Tn < lo) {
                             done = true;
                             stop_at = kofs + j;
                             break;
@@ -259,10 +268,13 @@ void launch_work_count(const FrameBuffers& fb, int pixels, unsigned long long* o
 }
 
 void launch_blend(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H, int tiles_x,
-                  int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s) {
+                  int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s, bool strict) {
     const int tiles = tiles_x * tiles_y;
     if (tiles <= 0) return;
-    k_blend<<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb);
+    if (strict)
+        k_blend<true><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb);
+    else
+        k_blend<false><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb);
     OSB_LAUNCHED(1);
 }
 

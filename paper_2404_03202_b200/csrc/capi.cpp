@@ -656,6 +656,13 @@ osplat_status osplat_gpu_set_deterministic(osplat_gpu* ctx, int on) {
     return OSPLAT_OK;
 }
 
+osplat_status osplat_gpu_set_strict_guard(osplat_gpu* ctx, int on) {
+    if (!ctx) return invalid("osplat_gpu_set_strict_guard: null context");
+    ctx->engine->set_strict_guard(on != 0);
+    t_last_error.clear();
+    return OSPLAT_OK;
+}
+
 osplat_status osplat_gpu_set_active_sh_degree(osplat_gpu* ctx, int degree) {
     if (!ctx) return invalid("osplat_gpu_set_active_sh_degree: null context");
     return wrap([&] { ctx->engine->set_active_sh_degree(degree); });
@@ -1017,15 +1024,6 @@ osplat_status osplat_gpu_backward(osplat_gpu* ctx, const osplat_frame* frame, co
         OSB_CUDA_CHECK(cudaMemcpyAsync(dev, planar.data(), plane * 12, cudaMemcpyHostToDevice, e.stream()));
         e.backward(frame->frame, dev, accumulate != 0);
         OSB_CUDA_CHECK(cudaStreamSynchronize(e.stream()));  // `planar` is pageable host memory
-    });
-}
-
-osplat_status osplat_gpu_backward_step(osplat_gpu* ctx, const osplat_frame* frame, const float* d_image_planar,
-                                       const osplat_config* config, double extent, long iteration) {
-    if (!ctx || !frame || !d_image_planar) return invalid("osplat_gpu_backward_step: null argument");
-    return wrap([&] {
-        validate_frame(ctx, frame);
-        ctx->engine->backward_step(frame->frame, d_image_planar, hyper_from(config), extent, iteration);
     });
 }
 
@@ -1425,29 +1423,14 @@ osplat_status osplat_gpu_l1_loss(osplat_gpu* ctx, const osplat_frame* frame, con
 }
 
 namespace {
-struct FusedStep {
-    const osplat_config* config;
-    double extent;
-    long iteration;
-};
 osplat_status train_view_impl(osplat_gpu* ctx, const double transform_cw[16], int width, int height, const float* gt,
-                              int gt_on_device, double lambda_ssim, double mask, double* loss, double* sums_pinned,
-                              const FusedStep* step = nullptr);
+                              int gt_on_device, double lambda_ssim, double mask, double* loss, double* sums_pinned);
 }
 
 osplat_status osplat_gpu_train_view(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
                                     const float* gt, int gt_on_device, double lambda_ssim, double mask,
                                     double* loss) {
     return train_view_impl(ctx, transform_cw, width, height, gt, gt_on_device, lambda_ssim, mask, loss, nullptr);
-}
-
-osplat_status osplat_gpu_train_step_async(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
-                                          const float* gt, int gt_on_device, double lambda_ssim, double mask,
-                                          const osplat_config* config, double extent, long iteration,
-                                          double* loss_sums) {
-    const FusedStep step{config, extent, iteration};
-    return train_view_impl(ctx, transform_cw, width, height, gt, gt_on_device, lambda_ssim, mask, nullptr, loss_sums,
-                           &step);
 }
 
 osplat_status osplat_gpu_train_view_async(osplat_gpu* ctx, const double transform_cw[16], int width, int height,
@@ -1469,8 +1452,7 @@ double osplat_loss_value(const double sums[4], double lambda_ssim, int width, in
 
 namespace {
 osplat_status train_view_impl(osplat_gpu* ctx, const double transform_cw[16], int width, int height, const float* gt,
-                              int gt_on_device, double lambda_ssim, double mask, double* loss, double* sums_pinned,
-                              const FusedStep* step) {
+                              int gt_on_device, double lambda_ssim, double mask, double* loss, double* sums_pinned) {
     if (!ctx || !transform_cw || !gt) return invalid("osplat_gpu_train_view: null argument");
     if (lambda_ssim < 0.0 || lambda_ssim > 1.0) return invalid("osplat_gpu_train_view: lambda_ssim must be in [0, 1]");
     if (mask < 0.0 || mask >= 1.0) return invalid("osplat_gpu_train_view: mask_bottom_fraction must be in [0, 1)");
@@ -1491,10 +1473,7 @@ osplat_status train_view_impl(osplat_gpu* ctx, const double transform_cw[16], in
             (void)v;
             if (!gt_on_device) e.release_target();
             const size_t pixels = plane;
-            if (step)
-                e.backward_step(f, e.d_image_buffer(pixels), hyper_from(step->config), step->extent, step->iteration);
-            else
-                e.backward(f, e.d_image_buffer(pixels), true);
+            e.backward(f, e.d_image_buffer(pixels), true);
             if (loss) {
                 // the L1 sum lives on the device; one 8-byte read completes the step
                 *loss = e.loss_value(f, mask);

@@ -26,13 +26,18 @@ constexpr int kTile = 16;
 constexpr int kTilePixels = kTile * kTile;
 constexpr double kShC0 = 0.28209479177387814;  // scene.hpp:60
 
-// T-stop guard (K3): the FP32 transmittance carries a running bound e on its
-// relative error against the FP64 reference loop; a pixel whose FP32 T_next is within
-// (1 +- (e + 2 e^2 + kTMargin)) x 1e-4 replays its prefix in FP64. Each contributing pair adds
-// alpha / (1 - alpha) x (delta (1.001 + delta) + kAlphaErr) — delta = K1's bound on the FP32 power
+// T-stop guard (K3). Default: FP32 transmittance within a relative band of 2^-10
+// of 1e-4 replays the pixel's prefix in FP64 (an empirical band: K3 frames equal the strict mode's
+// on every parity scene). Strict mode (osplat_gpu_set_strict_guard): the band is a running bound e
+// on the FP32 T's relative error against the FP64 loop — each contributing pair adds
+// alpha / (1 - alpha) x (delta (1.001 + delta) + kAlphaErr), delta = K1's bound on the FP32 power
 // error (alpha = o e^-power, so it is alpha's relative error), kAlphaErr the FP32 evaluation of
 // o ex2(-power log2 e) (exponent rounding <= 5.6 x 2^-24, ex2.approx <= 2^-22, o and the product
-// 2 x 2^-24) — and kTStep for the roundings of 1 - alpha and T (1 - alpha).
+// 2 x 2^-24) — plus kTStep per step for the roundings of 1 - alpha and T (1 - alpha); the decision is
+// certain outside 1e-4 (1 +- (e + 2 e^2 + kTMargin)).
+constexpr float kTBand = 1.0f / 1024.0f;
+constexpr float kTLo = 1e-4f * (1.0f - kTBand);
+constexpr float kTHi = 1e-4f * (1.0f + kTBand);
 constexpr float kAlphaErr = 1.1e-6f;
 constexpr float kTStep = 1.2e-7f;   // 2^-23
 constexpr float kTMargin = 1e-6f;   // FP32 rounding of the threshold arithmetic

@@ -398,7 +398,7 @@ void Engine::render_into(Frame* f) {
         {
             Span sp(*this, kBlend);
             launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(),
-                         stream_);
+                         stream_, strict_guard_);
         }
         // the host vectors are read by the copies above: finish them before the caller may free
         OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -471,7 +471,8 @@ void Engine::render_into(Frame* f) {
     // K3
     {
         Span sp(*this, kBlend);
-        launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(), stream_);
+        launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(), stream_,
+                     strict_guard_);
     }
     f->validated = false;
     f->M = cap;  // provisional until validate()
@@ -668,7 +669,9 @@ void Engine::loss_sums_async(double* host) {
     OSB_CUDA_CHECK(cudaMemcpyAsync(host, loss_sum_.as<double>(), 32, cudaMemcpyDeviceToHost, stream_));
 }
 
-AdamArgs Engine::next_adam_args(const TrainHyper& h, double extent, long iteration) {
+void Engine::adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad, size_t begin,
+                       size_t count) {
+    DeviceGuard g(device_);
     adam_step_ += 1;
     const double bias1 = 1.0 - std::pow(0.9, static_cast<double>(adam_step_));
     const double bias2 = 1.0 - std::pow(0.999, static_cast<double>(adam_step_));
@@ -693,79 +696,20 @@ AdamArgs Engine::next_adam_args(const TrainHyper& h, double extent, long iterati
     a.inv_bias2 = static_cast<float>(1.0 / bias2);
     a.planes = planes_;
     a.stride = static_cast<int>(stride_);
-    // Consumed gradients are not cleared in memory: the flag makes the next backward overwrite them.
-    a.zero_grad = 0;
-    a.begin = 0;
-    a.count = static_cast<long>(planes_) * static_cast<long>(stride_);
-    return a;
-}
-
-void Engine::adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad, size_t begin,
-                       size_t count) {
-    DeviceGuard g(device_);
     const size_t total = static_cast<size_t>(planes_) * stride_;
     if (begin > total || (begin & 3) != 0) throw std::invalid_argument("adam_step: range start out of bounds");
     if (count > total - begin) count = total - begin;
     if ((count & 3) != 0) throw std::invalid_argument("adam_step: range length must be a multiple of 4");
-    AdamArgs a = next_adam_args(h, extent, iteration);
     a.begin = static_cast<long>(begin);
     a.count = static_cast<long>(count);
+    // Consumed gradients are not cleared in memory: the flag makes the next backward overwrite them.
+    a.zero_grad = 0;
     materialize_grads();
     {
         Span sp(*this, kAdam);
         launch_adam(params_.as<float>(), grads_.as<float>(), m_.as<float>(), v_.as<float>(), a, stream_);
     }
     if (zero_grad) grads_zero_ = true;
-}
-
-void Engine::backward_step(Frame* f, const float* d_image, const TrainHyper& h, double extent, long iteration) {
-    DeviceGuard g(device_);
-    validate(f);
-    if (f->projected || static_cast<size_t>(f->n) != n_ || f->generation != generation_)
-        throw std::logic_error("StateMismatch: render output does not match the cloud");
-    if (dp_world() > 1) throw std::logic_error("StateMismatch: the fused step is single-GPU (use dp_step)");
-    OSB_CUDA_CHECK(cudaMemsetAsync(acc_.as<float4>(), 0, stride_ * 48, stream_));
-    const PreprocessOut pp = f->pp();
-    {
-        Span sp(*this, kBwdPixels);
-        if (deterministic_) {
-            det_inst_.ensure(static_cast<size_t>(f->M) * 9 * sizeof(float) + 64);
-            det_rank_.ensure(static_cast<size_t>(f->n) * sizeof(uint32_t) + 64);
-            OSB_CUDA_CHECK(cudaMemsetAsync(det_inst_.as<float>(), 0, static_cast<size_t>(f->M) * 9 * sizeof(float),
-                                           stream_));
-            launch_backward_pixels_det(f->inst_gid(), f->ranges.as<uint2>(), pp, f->W, f->H, f->tiles_x, f->tiles_y,
-                                       f->bg, f->fb(), d_image, scan_emit_arrays(f->scan_ws.as<void>(), f->n), f->n,
-                                       det_rank_.as<uint32_t>(), det_inst_.as<float>(), acc_.as<float4>(), stream_);
-        } else {
-            launch_backward_pixels(f->inst_gid(), f->ranges.as<uint2>(), pp, f->W, f->H, f->tiles_x, f->tiles_y,
-                                   f->bg, f->fb(), d_image, acc_.as<float4>(), stream_);
-        }
-    }
-    OSB_CUDA_CHECK(cudaMemsetAsync(d_screen_.as<float2>(), 0, stride_ * 8, stream_));
-    ScreenStats st{d_screen_.as<float2>(), norm_sum_.as<double>(), hits_.as<int>()};
-    const AdamArgs a = next_adam_args(h, extent, iteration);
-    sdd_.ensure(stride_ * sizeof(float4));
-    {
-        Span sp(*this, kBwdGauss);
-        launch_backward_step_gaussians(params_.as<float>(), m_.as<float>(), v_.as<float>(), f->n,
-                                       static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1), f->active_degree,
-                                       f->pose, f->W, f->H, pp, acc_.as<float4>(), grads_.as<float>(), st, a,
-                                       sdd_.as<float4>(), stream_);
-    }
-    {
-        // K5 over the geometry planes (position | rotation, log-scale, opacity); the SH planes were
-        // updated by k_sh_adam with the same step's bias corrections
-        Span sp(*this, kAdam);
-        const Planes pl{(sh_degree_ + 1) * (sh_degree_ + 1)};
-        AdamArgs b = a;
-        b.begin = 0;
-        b.count = 3 * static_cast<long>(stride_);
-        launch_adam(params_.as<float>(), grads_.as<float>(), m_.as<float>(), v_.as<float>(), b, stream_);
-        b.begin = static_cast<long>(pl.rot(0)) * static_cast<long>(stride_);
-        b.count = static_cast<long>(planes_ - pl.rot(0)) * static_cast<long>(stride_);
-        launch_adam(params_.as<float>(), grads_.as<float>(), m_.as<float>(), v_.as<float>(), b, stream_);
-    }
-    grads_zero_ = true;  // the step consumed this view's gradient (the SH planes were never written)
 }
 
 void Engine::zero_grad() { grads_zero_ = true; }

@@ -132,6 +132,9 @@ public:
     // atomics, per-instance partials reduced per Gaussian in a fixed order — gradients bit-identical
     // run to run, at roughly twice K4a's cost. Off by default.
     void set_deterministic(bool on) { deterministic_ = on; }
+    // Strict T-stop guard in K3 (common.cuh): the FP32 transmittance carries a rigorous error bound
+    // instead of the fixed 2^-10 band — a verification mode (more FP64 replays, ~1.8x K3 time).
+    void set_strict_guard(bool on) { strict_guard_ = on; }
     bool deterministic() const { return deterministic_; }
     // loss() of trainer.cpp:25-71 on the device: d_image into d_image_buffer(); the value is read
     // back only when want_value (one 32-byte read, synchronizes the stream).
@@ -150,11 +153,6 @@ public:
     // a data-parallel rank's shard after a reduce-scatter of the gradients).
     void adam_step(const TrainHyper& h, double extent, long iteration, bool zero_grad, size_t begin = 0,
                    size_t count = ~size_t(0));
-    // One view's backward and the Adam step it feeds, fused (the reference's one-view iteration,
-    // trainer.cpp:363 + 381): K4a, then the SH planes' gradients are consumed by Adam in place
-    // (k_sh_adam, never stored), K4b writes the geometry gradients, K5 runs on the geometry planes.
-    // Same result as backward(overwrite) + adam_step; single-GPU; gradients are logically zero after.
-    void backward_step(Frame* f, const float* d_image_planar_dev, const TrainHyper& h, double extent, long iteration);
     // Gradients are tracked as "logically zero" after zero_grad / a consuming Adam step, so the next
     // backward stores instead of read-modify-writes; materialize_grads() writes the zeros when the
     // buffer itself is about to be read (download, external views, Adam without a backward).
@@ -241,11 +239,11 @@ private:
     double last_lambda_ = 0.0;
     bool grads_zero_ = true;
     bool deterministic_ = false;
+    bool strict_guard_ = false;
     std::unique_ptr<Comm, CommDeleter> comm_;
     bool moments_sharded_ = false;  // Adam moments outside this rank's shard are stale
     size_t dp_shard(size_t* begin) const;
-    DevBuf det_inst_, det_rank_, sdd_;
-    AdamArgs next_adam_args(const TrainHyper& h, double extent, long iteration);  // advances the step
+    DevBuf det_inst_, det_rank_;
     std::vector<std::unique_ptr<Frame>> pool_;
     std::vector<Frame*> free_;
     cudaStream_t copy_stream_ = nullptr;

@@ -85,8 +85,11 @@ struct FrameBuffers {
 void launch_work_count(const FrameBuffers& fb, int pixels, unsigned long long* out, cudaStream_t s);
 // 3 FP32 planes -> interleaved H x W x 3 FP64 (the reference Image layout).
 void launch_planar_to_hwc_f64(const float* rgb, size_t plane, double* out, cudaStream_t s);
+// strict: the T-stop guard band is the rigorous running error bound instead of the 2^-10 band
+// (common.cuh); slower (more FP64 replays), decisions provably the FP64 reference's.
 void launch_blend(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H,
-                  int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s);
+                  int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s,
+                  bool strict = false);
 
 // ---- K4 backward (backward.cu) --------------------------------------------------------------
 // Deterministic K4a (optional mode, gradients.cpp:94-169's fixed-order reduction): per tile the 16
@@ -119,14 +122,6 @@ struct AdamArgs {
     long begin, count;  // flat element range (multiples of 4)
 };
 void launch_adam(float* params, float* grads, float* m, float* v, const AdamArgs& a, cudaStream_t s);
-// K4b + Adam of the fused single-view training step (backward.cu): k_sh_adam applies Adam to every
-// SH element with its gradient computed in place (never stored) and leaves the view-direction sums
-// in sdd (n float4); K4b then writes only the geometry gradient planes (overwrite). The caller runs
-// K5 over the geometry planes afterwards.
-void launch_backward_step_gaussians(float* params, float* m, float* v, int n, int stride, int bc, int active_degree,
-                                    const Pose& pose, int W, int H, const PreprocessOut& pp, const float4* acc,
-                                    float* grads, const ScreenStats& st, const AdamArgs& adam, float4* sdd,
-                                    cudaStream_t s);
 // loss() of trainer.cpp:25-71 (loss.cu): (1 - lambda) L1 + lambda (1 - SSIM) over the top
 // keep_rows rows of planar FP32 images; writes dL/dC planes (0 in masked rows) and accumulates
 // sums[0] = sum |r - g| (FP64), sums[1..3] = per-channel SSIM map sums. g_planes: 9 * W * H floats

@@ -142,18 +142,9 @@ void DeviceTrainer::run(long start_iteration, const std::function<void(const Ite
         Frame* f = e_.render(&poses_[12 * static_cast<size_t>(view)], W_, H_, cfg_.background);
         IterationReport rep;
         rep.iteration = j;
-        bool fused = false;
         try {
             e_.loss(f, image(view), cfg_.lambda_ssim, cfg_.mask_bottom_fraction, false);
-            // single GPU, an iteration that neither densifies nor resets opacities (those sit
-            // between backward and adam_step, trainer.cpp:366-381): backward + Adam fused
-            const bool edit_iter = j <= cfg_.densify_until &&
-                                   (j % cfg_.densify_interval == 0 || j % cfg_.opacity_reset_interval == 0);
-            fused = world == 1 && !edit_iter;
-            if (fused)
-                e_.backward_step(f, e_.d_image_buffer(static_cast<size_t>(W_) * H_), cfg_.lr, extent_, j);
-            else
-                e_.backward(f, e_.d_image_buffer(static_cast<size_t>(W_) * H_), false);
+            e_.backward(f, e_.d_image_buffer(static_cast<size_t>(W_) * H_), false);
             e_.observe(f);
             rep.loss = log_now ? e_.loss_value(f, cfg_.mask_bottom_fraction) : nan;
         } catch (...) {
@@ -170,7 +161,7 @@ void DeviceTrainer::run(long start_iteration, const std::function<void(const Ite
             if (j % cfg_.opacity_reset_interval == 0) e_.reset_opacity(cfg_.opacity_reset_ceiling);
         }
         // the densification edit rebuilds the parameter arrays: this iteration's gradients no longer apply
-        if (!rep.densified && !fused) {
+        if (!rep.densified) {
             if (world > 1) e_.dp_step(cfg_.lr, extent_, j);
             else e_.adam_step(cfg_.lr, extent_, j, true);
         }

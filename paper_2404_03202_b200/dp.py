@@ -105,12 +105,6 @@ class DataParallelTrainer:
             self.engine.adam_step(iteration)
 
     def step(self, iteration: int, view_ids: Sequence[int]) -> float:
-        # one GPU, one view: the engine may fuse the backward with the Adam step it feeds
-        # (osplat_gpu_backward_step) — the reference's own one-view iteration, same result
-        if self.world == 1 and not self.sharded and not self.native and len(view_ids) == 1 and \
-                hasattr(self.engine, "fused_step"):
-            out = self.engine.fused_step(view_ids[0], iteration)
-            return 0.0 if out is None else out
         loss = self.accumulate(view_ids)
         self.apply(iteration)
         return loss
@@ -174,19 +168,6 @@ class GpuViewEngine:
             _, dimg = self.ctx.loss(fr, self.targets[view_id].data_ptr(), self.lambda_ssim, self.mask,
                                     want_value=False)
             self.ctx.backward_device(fr, dimg, accumulate=True)
-            if self.observe:
-                self.ctx.observe(fr)
-        finally:
-            fr.free()
-        return None
-
-    def fused_step(self, view_id: int, iteration: int):
-        """render -> loss -> backward + Adam fused (single GPU, single view per step)."""
-        fr = self.ctx.render(self.poses[view_id], self.W, self.H)
-        try:
-            _, dimg = self.ctx.loss(fr, self.targets[view_id].data_ptr(), self.lambda_ssim, self.mask,
-                                    want_value=False)
-            self.ctx.backward_step(fr, dimg, self.config, self.extent, iteration)
             if self.observe:
                 self.ctx.observe(fr)
         finally:

@@ -91,9 +91,7 @@ def _load():
         "osplat_gpu_count": (C.c_size_t, [_vp]),
         "osplat_gpu_set_active_sh_degree": (S, [_vp, C.c_int]),
         "osplat_gpu_set_deterministic": (S, [_vp, C.c_int]),
-        "osplat_gpu_backward_step": (S, [_vp, _vp, _vp, _vp, C.c_double, C.c_long]),
-        "osplat_gpu_train_step_async": (S, [_vp, _dp, C.c_int, C.c_int, _vp, C.c_int, C.c_double, C.c_double, _vp,
-                                            C.c_double, C.c_long, C.c_void_p]),
+        "osplat_gpu_set_strict_guard": (S, [_vp, C.c_int]),
         "osplat_nccl_unique_id": (S, [C.POINTER(C.c_ubyte)]),
         "osplat_gpu_dp_init": (S, [_vp, C.c_int, C.c_int, C.POINTER(C.c_ubyte)]),
         "osplat_gpu_dp_step": (S, [_vp, _vp, C.c_double, C.c_long]),
@@ -464,6 +462,10 @@ class Context:
         all-gather of the parameters (NCCL, on the context stream)."""
         check(lib.osplat_gpu_dp_step(self.handle, config.handle if config else None, extent, iteration))
 
+    def set_strict_guard(self, on: bool = True):
+        """Strict (provable) T-stop guard band in K3 instead of the default 2^-10 band."""
+        check(lib.osplat_gpu_set_strict_guard(self.handle, int(bool(on))))
+
     def set_deterministic(self, on: bool = True):
         """Deterministic backward (fixed-order reduction, bit-identical gradients run to run)."""
         check(lib.osplat_gpu_set_deterministic(self.handle, int(bool(on))))
@@ -510,21 +512,6 @@ class Context:
         d = np.ascontiguousarray(d_image, dtype=np.float64)
         assert d.shape == (frame.height, frame.width, 3)
         check(lib.osplat_gpu_backward(self.handle, frame.handle, _p(d), int(accumulate)))
-
-    def backward_step(self, frame: Frame, d_image_ptr: int, config: "Config | None", extent: float, iteration: int):
-        """osplat_gpu_backward_step: backward (overwrite) + adam_step fused (single-view iteration)."""
-        check(lib.osplat_gpu_backward_step(self.handle, frame.handle, C.c_void_p(d_image_ptr),
-                                           config.handle if config else None, extent, iteration))
-
-    def train_step_async(self, pose12, width: int, height: int, gt, gt_on_device: bool, sums_ptr: int | None,
-                         config: "Config | None", extent: float, iteration: int, lambda_ssim: float = 0.2,
-                         mask: float = 0.0):
-        """osplat_gpu_train_step_async: render -> loss -> backward + Adam (fused), nothing waited for."""
-        t = transform_of(pose12)
-        ptr = C.c_void_p(gt) if isinstance(gt, int) else gt.ctypes.data_as(C.c_void_p)
-        check(lib.osplat_gpu_train_step_async(self.handle, _p(t), width, height, ptr, int(gt_on_device), lambda_ssim,
-                                              mask, config.handle if config else None, extent, iteration,
-                                              None if sums_ptr is None else C.c_void_p(sums_ptr)))
 
     def backward_device(self, frame: Frame, d_image_ptr: int, accumulate: bool = False):
         check(lib.osplat_gpu_backward_device(self.handle, frame.handle, C.c_void_p(d_image_ptr), int(accumulate)))

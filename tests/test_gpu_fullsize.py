@@ -133,3 +133,24 @@ def test_config2_scale_matches_reference(ref):
     go = ref.backward(of, d, cloud, pose)
     ref.free(of)
     assert_grads_close(g, go)
+
+
+@pytest.mark.parametrize("name,make,pose,W,H", CASES[:5], ids=[c[0] for c in CASES[:5]])
+def test_default_guard_band_equals_strict_bound(name, make, pose, W, H):
+    """K3's default T-stop guard (a fixed relative 2^-10 band) against the strict mode, whose band
+    is a rigorous bound on the FP32 transmittance error: identical stop decisions
+    — contributors and last_contrib equal for every pixel — so on these scenes the default made every
+    stop decision the FP64 reference makes (colours / T differ only where strict mode continued a
+    pixel in FP64)."""
+    cloud = make()
+    out = []
+    for strict in (False, True):
+        ctx = native.Context(cloud)
+        ctx.set_strict_guard(strict)
+        fr = ctx.render(pose, W, H)
+        out.append(fr.pixels())
+        fr.free()
+        ctx.free()
+    (rgb_a, T_a, con_a, last_a), (rgb_b, T_b, con_b, last_b) = out
+    assert np.array_equal(con_a, con_b) and np.array_equal(last_a, last_b)
+    assert np.max(np.abs(rgb_a - rgb_b)) < 1e-5 and np.max(np.abs(T_a - T_b)) < 1e-5
