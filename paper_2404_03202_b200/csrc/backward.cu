@@ -19,6 +19,14 @@ namespace osb {
 
 namespace {
 
+#ifdef OSB_K4A_STATS
+// Instrumented build only (scripts/k4a_stats.py): K4a loop statistics per launch.
+__device__ unsigned long long g_k4a_stats[8];
+#define OSB_STAT(i, v) (st[i] += (v))
+#else
+#define OSB_STAT(i, v) ((void)0)
+#endif
+
 __device__ __forceinline__ void red_add_v4(float4* addr, float a, float b, float c, float d) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
@@ -116,8 +124,12 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
 #pragma unroll
     for (int w = 0; w < kTileWarps; ++w) cta_last = max(cta_last, s_last[w]);
     const int t = threadIdx.x;
+#ifdef OSB_K4A_STATS
+    unsigned long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
     for (int hi = cta_last; hi > 0; hi -= kChunk) {
         const int lo = hi > kChunk ? hi - kChunk : 0;
+        OSB_STAT(7, lane == 0 ? static_cast<unsigned long long>(hi - lo) : 0ull);
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
             const int i = lo + t + e * kTileThreads;
@@ -139,11 +151,15 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
         const uint32_t bal0 = __ballot_sync(0xffffffffu, (mk >> (2 * warp)) & 1u);
         const uint32_t bal1 = __ballot_sync(0xffffffffu, (mk >> (2 * warp + 1)) & 1u);
         uint32_t bal = wp.half ? bal1 : bal0;
+        OSB_STAT(0, 1);
         while (__any_sync(0xffffffffu, bal != 0u)) {  // back to front; warp-uniform (the reduction needs all lanes)
             const bool live = bal != 0u;
             const int j = live ? 31 - __clz(bal) : 0;
             bal &= ~(1u << j);
             const int k = sbase + j;
+            OSB_STAT(1, 1);
+            OSB_STAT(4, __popc(__ballot_sync(0xffffffffu, live)) / 16);
+            OSB_STAT(5, __popc(__ballot_sync(0xffffffffu, live && k < last)));
             float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f, v5 = 0.f, v6 = 0.f, v7 = 0.f, v8 = 0.f;
             bool has = false;
             if (live && k < last) {
@@ -222,7 +238,9 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
                 }
             }
             const uint32_t hb_all = __ballot_sync(0xffffffffu, has);
+            OSB_STAT(6, __popc(hb_all));
             if (hb_all == 0u) continue;
+            OSB_STAT(2, 1);
             const uint32_t hb = hb_all & halfmask;  // this half's contributing lanes
             float* a = reinterpret_cast<float*>(acc + 3 * static_cast<size_t>(ws.gid[j]));
             // up to 10 contributing pixels of this quarter add directly (3 red instructions per
@@ -235,6 +253,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
                 red_add(a + 8, v8);
             }
             if (__any_sync(0xffffffffu, multi)) {
+                OSB_STAT(3, 1);
                 const float v[9] = {v0, v1, v2, v3, v4, v5, v6, v7, v8};
                 int idx;
                 const float sum = half_reduce9(v, lane, &idx);
@@ -245,6 +264,10 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
       }
         __syncthreads();  // the stage is rewritten by the next chunk
     }
+#ifdef OSB_K4A_STATS
+    if (lane == 0)
+        for (int i = 0; i < 8; ++i) atomicAdd(&g_k4a_stats[i], st[i]);
+#endif
 }
 
 // Gradient plane update: OVERWRITE (the buffer is logically zero: first view after Adam or a
@@ -727,6 +750,16 @@ void launch_backward_pixels_det(const uint32_t* inst_gid, const uint2* ranges, c
     OSB_LAUNCHED(3);
 }
 
+
+#ifdef OSB_K4A_STATS
+extern "C" __attribute__((visibility("default"))) void osb_k4a_stats(unsigned long long out[8], int reset) {
+    cudaMemcpyFromSymbol(out, g_k4a_stats, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_k4a_stats, z, sizeof(z));
+    }
+}
+#endif
 
 void launch_backward_pixels(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H,
                             int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb, const float* d_image,
