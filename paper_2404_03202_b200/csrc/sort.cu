@@ -52,40 +52,6 @@ __device__ __forceinline__ int sort_count(int n_cap, const uint32_t* n_dev) {
     return m < static_cast<uint32_t>(n_cap) ? static_cast<int>(m) : n_cap;
 }
 
-template <typename K>
-__global__ void __launch_bounds__(256) k_histogram(const K* __restrict__ keys, int n_cap, const uint32_t* n_dev,
-                                                   int passes, uint32_t* __restrict__ hist /* passes x 256 */) {
-    const int n = sort_count(n_cap, n_dev);
-    __shared__ uint32_t s_hist[kMaxPasses][kBins];
-    for (int i = threadIdx.x; i < passes * kBins; i += blockDim.x) (&s_hist[0][0])[i] = 0;
-    __syncthreads();
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const K k = keys[i];
-        for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (p * kRadixBits)) & (kBins - 1)], 1u);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < passes * kBins; i += blockDim.x) {
-        const uint32_t v = (&s_hist[0][0])[i];
-        if (v) atomicAdd(&hist[i], v);
-    }
-}
-
-// Exclusive scan of each pass's 256 digit counts -> digit base offsets. One block per pass.
-__global__ void k_scan_hist(const uint32_t* __restrict__ hist, uint32_t* __restrict__ base) {
-    __shared__ uint32_t s[kBins];
-    const int p = blockIdx.x;
-    const int d = threadIdx.x;
-    s[d] = hist[p * kBins + d];
-    __syncthreads();
-    for (int off = 1; off < kBins; off <<= 1) {
-        const uint32_t v = d >= off ? s[d - off] : 0;
-        __syncthreads();
-        s[d] += v;
-        __syncthreads();
-    }
-    base[p * kBins + d] = s[d] - hist[p * kBins + d];
-}
-
 // 256-thread exclusive scan (returns exclusive prefix, *total = block sum).
 __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp, uint32_t* total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -114,36 +80,61 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
     return r;
 }
 
-// Per-block digit counts for one pass: counts[d * nblocks + b].
+// Per-block digit counts for one pass: counts[d * nblocks + b]. The first pass (hist != nullptr)
+// also accumulates every pass's global digit totals hist[p][d] (one read of the keys serves both).
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads) k_upsweep(const K* __restrict__ keys, int n_cap, const uint32_t* n_dev,
-                                                          int shift, int nblocks, uint32_t* __restrict__ counts) {
+                                                          int shift, int nblocks, uint32_t* __restrict__ counts,
+                                                          int passes, uint32_t* __restrict__ hist) {
     const int n = sort_count(n_cap, n_dev);
     constexpr int kTile = tile_keys<K>();
     __shared__ uint32_t s_hist[kSortWarps][kBins];
+    __shared__ uint32_t s_tot[kMaxPasses][kBins];
     const int warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kSortWarps * kBins; i += kSortThreads) (&s_hist[0][0])[i] = 0;
+    if (hist)
+        for (int i = threadIdx.x; i < kMaxPasses * kBins; i += kSortThreads) (&s_tot[0][0])[i] = 0;
     __syncthreads();
     const long base = static_cast<long>(blockIdx.x) * kTile;
     const int count = static_cast<int>(max(0L, min(static_cast<long>(kTile), static_cast<long>(n) - base)));
-    for (int i = threadIdx.x; i < count; i += kSortThreads)
-        atomicAdd(&s_hist[warp][static_cast<uint32_t>((keys[base + i] >> shift) & (kBins - 1))], 1u);
+    for (int i = threadIdx.x; i < count; i += kSortThreads) {
+        const K k = keys[base + i];
+        atomicAdd(&s_hist[warp][static_cast<uint32_t>((k >> shift) & (kBins - 1))], 1u);
+        if (hist)
+            for (int p = 1; p < passes; ++p)
+                atomicAdd(&s_tot[p][static_cast<uint32_t>((k >> (p * kRadixBits)) & (kBins - 1))], 1u);
+    }
     __syncthreads();
     uint32_t c = 0;
 #pragma unroll
     for (int w = 0; w < kSortWarps; ++w) c += s_hist[w][threadIdx.x];
     counts[static_cast<size_t>(threadIdx.x) * nblocks + blockIdx.x] = c;
+    if (hist) {
+        if (c) atomicAdd(&hist[threadIdx.x], c);
+        for (int p = 1; p < passes; ++p) {
+            const uint32_t t = s_tot[p][threadIdx.x];
+            if (t) atomicAdd(&hist[p * kBins + threadIdx.x], t);
+        }
+    }
 }
 
-// One block per digit: offsets[d][b] = digit_base[d] + sum_{b' < b} counts[d][b'].
+// One block per digit: offsets[d][b] = digit_base[d] + sum_{b' < b} counts[d][b'], the digit base
+// being the exclusive prefix of this pass's global digit totals.
 __global__ void __launch_bounds__(kSortThreads) k_scan_counts(const uint32_t* __restrict__ counts, int nblocks,
-                                                              const uint32_t* __restrict__ digit_base,
+                                                              const uint32_t* __restrict__ digit_totals,
                                                               uint32_t* __restrict__ offsets) {
     __shared__ uint32_t s_scan[kSortWarps + 1];
+    __shared__ uint32_t s_base;
     const int d = blockIdx.x;
+    {
+        uint32_t total;
+        const uint32_t ex = block_exclusive_scan(digit_totals[threadIdx.x], s_scan, &total);
+        if (static_cast<int>(threadIdx.x) == d) s_base = ex;
+        __syncthreads();
+    }
     const uint32_t* row = counts + static_cast<size_t>(d) * nblocks;
     uint32_t* out = offsets + static_cast<size_t>(d) * nblocks;
-    uint32_t carry = digit_base[d];
+    uint32_t carry = s_base;
     for (int b0 = 0; b0 < nblocks; b0 += kSortThreads) {
         const int b = b0 + threadIdx.x;
         const uint32_t v = b < nblocks ? row[b] : 0u;
@@ -422,18 +413,36 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
     uint32_t o = o_begin + threadIdx.x * 8;
     if (o >= o_end) return;
     int e = owner_of(off, w, o);
+    // the rank's record and the (row, column) of output o inside its rectangle: one division for
+    // the thread's first output, then stepped along the row-major walk; reloaded when the rank changes
+    int2 rc = rank_rc[rb + e];
+    uint32_t gid = rank_gid[rb + e];
+    uint32_t wt = static_cast<uint32_t>(rc.x) >> 16;
+    uint32_t li = o - off[e];
+    uint32_t row = li / wt, col = li - row * wt;
+    uint32_t next = e + 1 < w ? off[e + 1] : 0xFFFFFFFFu;
     for (int q = 0; q < 8 && o < o_end; ++q, ++o) {
-        while (e + 1 < w && off[e + 1] <= o) ++e;
-        const int2 rc = rank_rc[rb + e];
+        if (o >= next) {  // o belongs to a later rank (skip ranks without instances)
+            do {
+                ++e;
+                next = e + 1 < w ? off[e + 1] : 0xFFFFFFFFu;
+            } while (o >= next);
+            rc = rank_rc[rb + e];
+            gid = rank_gid[rb + e];
+            wt = static_cast<uint32_t>(rc.x) >> 16;
+            row = 0;
+            col = 0;
+        }
         const int x0 = static_cast<int>(static_cast<int16_t>(rc.x & 0xFFFF));
-        const uint32_t wt = static_cast<uint32_t>(rc.x) >> 16;
-        const uint32_t li = o - off[e];
-        const uint32_t row = li / wt;
-        int kx = x0 + static_cast<int>(li - row * wt);
+        int kx = x0 + static_cast<int>(col);
         kx = kx < 0 ? kx + tiles_x : (kx >= tiles_x ? kx - tiles_x : kx);
         if (o < capacity) {
             keys[o] = static_cast<uint32_t>((rc.y + static_cast<int>(row)) * tiles_x + kx);
-            vals[o] = rank_gid[rb + e];
+            vals[o] = gid;
+        }
+        if (++col == wt) {
+            col = 0;
+            ++row;
         }
     }
 }
@@ -465,7 +474,8 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ key
     }
 }
 
-// Workspace: hist[8][256] | base[8][256] | counts[256][blocks] | offsets[256][blocks]
+// Workspace: hist[8][256] (global digit totals per pass) | unused[8][256] | counts[256][blocks] |
+// offsets[256][blocks]
 template <typename K>
 bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n, const uint32_t* n_dev, int bits,
                 void* ws, cudaStream_t s) {
@@ -473,14 +483,9 @@ bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, 
     const int passes = (bits + kRadixBits - 1) / kRadixBits;
     const int blocks = (n + tile_keys<K>() - 1) / tile_keys<K>();
     uint32_t* hist = static_cast<uint32_t*>(ws);
-    uint32_t* base = hist + kMaxPasses * kBins;
-    uint32_t* counts = base + kMaxPasses * kBins;
+    uint32_t* counts = hist + 2 * kMaxPasses * kBins;
     uint32_t* offsets = counts + static_cast<size_t>(kBins) * blocks;
     OSB_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kBins, s));
-    const int hblocks = blocks < 148 * 4 ? blocks : 148 * 4;
-    k_histogram<K><<<hblocks, 256, 0, s>>>(keys_in, n, n_dev, passes, hist);
-    k_scan_hist<<<passes, kBins, 0, s>>>(hist, base);
-    OSB_LAUNCHED(2);
     bool flipped = false;
     for (int p = 0; p < passes; ++p) {
         K* ki = flipped ? keys_out : keys_in;
@@ -488,8 +493,9 @@ bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, 
         uint32_t* vi = flipped ? vals_out : vals_in;
         uint32_t* vo = flipped ? vals_in : vals_out;
         const int shift = p * kRadixBits;
-        k_upsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, n, n_dev, shift, blocks, counts);
-        k_scan_counts<<<kBins, kSortThreads, 0, s>>>(counts, blocks, base + p * kBins, offsets);
+        k_upsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, n, n_dev, shift, blocks, counts, passes,
+                                                     p == 0 ? hist : nullptr);
+        k_scan_counts<<<kBins, kSortThreads, 0, s>>>(counts, blocks, hist + p * kBins, offsets);
         k_downsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, n_dev, shift, blocks, offsets);
         OSB_LAUNCHED(3);
         flipped = !flipped;
