@@ -49,3 +49,16 @@ def test_gpus_must_match_world_size():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--steps", "1"],
                          capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
     assert out.returncode != 0 and "--gpus 4 but WORLD_SIZE=2" in (out.stderr + out.stdout)
+
+
+def test_reference_arm_never_maps_the_product_library(oracle_ref):
+    """The reference arm times only the reference's own code: the process must not even map
+    libosplat_b200.so (the package loads it lazily; bench.py's reference arm imports scenes only)."""
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '1', "
+            "'--gaussians', '500', '--width', '64', '--height', '32']; "
+            "runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "print('MAPPED', 'libosplat_b200' in maps, 'libref_oracle' in maps)")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == "MAPPED False True"
