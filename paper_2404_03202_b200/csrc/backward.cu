@@ -69,7 +69,51 @@ __device__ __forceinline__ float half_reduce9(const float (&v)[9], int lane, int
     return f;
 }
 
+// Shared per-CTA context of K4a's FP64 fallback: the slow path reads the FP64 records and recomputes
+// its pixel from the thread index, so none of it stays live in the hot loop's registers.
+struct K4aSlowCtx {
+    const double2* pxy;
+    const double4* conic_o;
+    double width;
+    int tiles_x;
+};
+__shared__ K4aSlowCtx s_k4a;
+
+// FP64 evaluation of instance `gid` at this thread's pixel (rasterizer.cpp:128-134) for K4a:
+// returns {alpha, g} with alpha = -1 when the pair does not contribute in FP64 and g negated when the
+// 0.99 clamp gate (gradients.cpp:146, o g < 0.99) is closed. Out of line: called for < 0.1 % of pairs.
+static __device__ __noinline__ float2 k4a_slow(uint32_t gid) {
+    const int tile = blockIdx.x;
+    const WarpPixel wp = warp_pixel(threadIdx.x >> 5, threadIdx.x & 31);
+    const int px = (tile % s_k4a.tiles_x) * kTile + wp.lx, py = (tile / s_k4a.tiles_x) * kTile + wp.ly;
+    const double2 pc = s_k4a.pxy[gid];
+    const double4 co = s_k4a.conic_o[gid];
+    double g, alpha;
+    if (!pair_fp64(pc.x, pc.y, co.x, co.y, co.z, co.w, px + 0.5, py + 0.5, s_k4a.width, &g, &alpha))
+        return make_float2(-1.0f, 0.0f);
+    const float gf = static_cast<float>(g);
+    return make_float2(static_cast<float>(alpha), co.w * g < kAlphaMax ? gf : -gf);
+}
+
+__device__ __forceinline__ uint32_t bfind_u32(uint32_t x) {  // index of the highest set bit, ~0u for 0
+    uint32_t r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+__device__ __forceinline__ uint32_t bit_u32(uint32_t j) {  // 1 << j, 0 for j >= 32 (PTX clamps the shift)
+    uint32_t r;
+    asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(j));
+    return r;
+}
+
 // BG: a non-black background adds the -T_final / (1 - alpha) * (bg . dL/dC) term (gradients.cpp:141).
+//
+// Hot loop (one entry per half-warp per iteration, back to front): branch-free for the common case.
+// Every lane evaluates the staged entry its half selected; a lane that does not contribute (no entry
+// left, entry at or past its last_contrib, certain FP32 skip, FP64 skip) carries alpha = 0 and g = 0,
+// which leaves T_acc and the suffix colour bit-identical (x * rcp(1) = x, fma(c, -0, s * 1) = s)
+// and makes all nine accumulated values zero. Only the FP64 fallback (pairs inside the guard band,
+// or the 0.99 clamp gate of a near-opaque splat) branches, warp-uniformly.
 template <bool BG>
 __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint32_t* __restrict__ inst_gid,
                                                                      const uint2* __restrict__ ranges, PreprocessOut pp,
@@ -95,7 +139,9 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
     const uint2 range = ranges[tile];
     const double width = W;
     const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
-    const float lxo = lx - 7.5f, lyo = ly - 7.5f;
+    float lxo = lx - 7.5f, lyo = ly - 7.5f;
+    asm volatile("mov.b32 %0, %0;" : "+f"(lxo));
+    asm volatile("mov.b32 %0, %0;" : "+f"(lyo));
     const float halfW = 0.5f * W, fW = static_cast<float>(W);
     const float2 nlo = make_float2(-lxo, -lyo);
     const size_t pix = static_cast<size_t>(py) * W + px;
@@ -109,6 +155,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
     const float bg_dot = bg0 * dl0 + bg1 * dl1 + bg2 * dl2;
     // this warp only walks the list up to its own furthest last_contrib
     const int max_last = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(last)));
+    const uint32_t stage_s = pinned_smem_base(stage);
 
     float T_acc = T_final;
     // negated suffix colour (-s): (Cc - s) is then one packed add; ns01 = (-s0, -s1)
@@ -119,6 +166,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
     // half-warp culling as K3), back to front; the halves reduce their (different) entries at once.
     const uint32_t halfmask = wp.half ? 0xFFFF0000u : 0x0000FFFFu;
     if (lane == 0) s_last[warp] = max_last;
+    if (threadIdx.x == 0) s_k4a = K4aSlowCtx{pp.pxy, pp.conic_o, width, tiles_x};
     __syncthreads();
     int cta_last = 0;
 #pragma unroll
@@ -139,6 +187,11 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
                 const float4* s4 = reinterpret_cast<const float4*>(pp.splat + gid);
                 m = stage_record16<true>(stage[warp + e * kTileWarps], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc, yc,
                                    width);
+            } else {
+                // finite filler: lanes with no entry left evaluate slot 31 with alpha forced to 0
+                WarpStage& w = stage[warp + e * kTileWarps];
+                w.a[lane] = w.b[lane] = w.c[lane] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                w.gid[lane] = 0u;
             }
             s_mask[t + e * kTileThreads] = static_cast<uint16_t>(m);
         }
@@ -146,115 +199,103 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
       for (int sub = kSubs - 1; sub >= 0; --sub) {
         const int sbase = lo + 32 * sub;
         if (sbase >= hi || sbase >= max_last) continue;  // no pixel of this warp reaches these entries
-        WarpStage& ws = stage[sub];
+        const StageRef ws{stage_s + static_cast<uint32_t>(sub * sizeof(WarpStage))};
         const uint32_t mk = s_mask[32 * sub + lane];
         const uint32_t bal0 = __ballot_sync(0xffffffffu, (mk >> (2 * warp)) & 1u);
         const uint32_t bal1 = __ballot_sync(0xffffffffu, (mk >> (2 * warp + 1)) & 1u);
         uint32_t bal = wp.half ? bal1 : bal0;
+        // entry j of this sub-chunk lies before this pixel's last_contrib iff j < kl
+        const uint32_t kl = static_cast<uint32_t>(min(max(last - sbase, 0), 32));
         OSB_STAT(0, 1);
         while (__any_sync(0xffffffffu, bal != 0u)) {  // back to front; warp-uniform (the reduction needs all lanes)
-            const bool live = bal != 0u;
-            const int j = live ? 31 - __clz(bal) : 0;
-            bal &= ~(1u << j);
-            const int k = sbase + j;
+            const uint32_t j = bfind_u32(bal);  // ~0u once this half has no entry left
+            bal &= ~bit_u32(j);
+            const uint32_t jj = j & 31u;
             OSB_STAT(1, 1);
-            OSB_STAT(4, __popc(__ballot_sync(0xffffffffu, live)) / 16);
-            OSB_STAT(5, __popc(__ballot_sync(0xffffffffu, live && k < last)));
-            float v0 = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f, v4 = 0.f, v5 = 0.f, v6 = 0.f, v7 = 0.f, v8 = 0.f;
-            bool has = false;
-            if (live && k < last) {
-                const float4 A = ws.a[j];
-                const float4 B = ws.b[j];
-                float2 d;
-                float power;
-                bool unc;
-                if (pair_power2(A, B, nlo, halfW, fW, d, power, unc)) {
-                    const float4 Cc = ws.c[j];
-                    float alpha, g;
-                    bool gate;
-                    bool ok = true;
+            const float4 A = ws.a(jj);
+            const float4 B = ws.b(jj);
+            const float4 Cc = ws.c(jj);
+            // FP32 power, exactly pair_power2's instructions (K3 makes the same decisions)
+            float2 d = __fadd2_rn(make_float2(A.x, A.y), nlo);
+            bool unc = false;
+            if (B.w < 0.0f) {
+                if (d.x > halfW) d.x -= fW;
+                else if (d.x < -halfW) d.x += fW;
+                unc = fabsf(fabsf(d.x) - halfW) < 0.01f;
+            }
+            const float2 q = __fmul2_rn(make_float2(A.z, A.w), d);
+            const float bdx = B.x * d.x;
+            const float power = __fmaf_rn(q.x, d.x, __fmaf_rn(q.y, d.y, bdx * d.y));
+            // candidate: an entry of this half before the pixel's last_contrib that is not a certain skip
+            const bool cand = j < kl && (power <= B.z || unc);
+            unc = unc || power < fabsf(B.w) || power > B.y;
+            float g = ex2_approx(-power * kLog2e);
+            const float og = Cc.w * g;
+            float alpha = fminf(0.99f, og);
+            // 0.99 clamp gate: certain in FP32 unless a near-opaque splat lands inside its guard band
+            bool gate = og < 0.99f;
+            const bool gchk = Cc.w >= 0.98f && fabsf(og - 0.99f) <= 0.99f * (1.5f * fabsf(B.w) + 1e-6f);
+            bool has = cand;
+            if (__any_sync(0xffffffffu, cand && (unc || gchk))) {
+                if (cand && (unc || gchk)) {
+                    const float2 r = k4a_slow(ws.gid(jj));
                     if (unc) {
-                        Pair64 p;
-                        ok = pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
-                        alpha = static_cast<float>(p.alpha);
-                        g = static_cast<float>(p.g);
-                        gate = p.og < kAlphaMax;
-                    } else {
-                        g = ex2_approx(-power * kLog2e);
-                        const float og = Cc.w * g;
-                        alpha = fminf(0.99f, og);
-                        gate = true;  // o g <= o < 0.98 < 0.99 for all but the most opaque splats
-                        if (Cc.w >= 0.98f) {
-                            const float band = 0.99f * (1.5f * fabsf(B.w) + 1e-6f);
-                            if (fabsf(og - 0.99f) <= band) {
-                                Pair64 p;
-                                pair_slow(ws.gid[j], px, py, width, pp.pxy, pp.conic_o, &p);
-                                gate = p.og < kAlphaMax;
-                            } else {
-                                gate = og < 0.99f;
-                            }
-                        }
+                        has = r.x >= 0.0f;
+                        alpha = r.x;
+                        g = fabsf(r.y);
                     }
-                    if (ok) {
-                        has = true;
-                        const float one_m = 1.0f - alpha;
-                        // 1 - alpha is in [0.01, 1]: MUFU.RCP directly (what __fdividef(1, x)
-                        // computes there, without its range-scaling instructions)
-                        float inv;
-                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));
-                        T_acc = T_acc * inv;
-                        const float wb = alpha * T_acc;
-                        const float2 v01 = __fmul2_rn(dl01, make_float2(wb, wb));
-                        v0 = v01.x;
-                        v1 = v01.y;
-                        v2 = dl2 * wb;
-                        const float2 cs = __fadd2_rn(make_float2(Cc.x, Cc.y), ns01);  // Cc - s
-                        float d_alpha = cs.x * dl01.x;
-                        d_alpha = __fmaf_rn(cs.y, dl01.y, d_alpha);
-                        d_alpha = __fmaf_rn(Cc.z + ns2, dl2, d_alpha);
-                        d_alpha = d_alpha * T_acc;
-                        if (BG) d_alpha = d_alpha - (T_final * inv) * bg_dot;
-                        // suffix (colour of everything behind) now includes this entry
-                        // (-s) = fma(Cc, -alpha, (-s) (1 - alpha)): the exact negation of
-                        // fma(Cc, alpha, s (1 - alpha))
-                        const float nalpha = -alpha;
-                        ns01 = __ffma2_rn(make_float2(Cc.x, Cc.y), make_float2(nalpha, nalpha),
-                                          __fmul2_rn(ns01, make_float2(one_m, one_m)));
-                        ns2 = __fmaf_rn(Cc.z, nalpha, ns2 * one_m);
-                        if (gate) {
-                            // dL/dpower times d, d d^T: K4b applies the conic once per Gaussian
-                            // (d_p = Q sum(dL/dpower d)) and the 1/2 of the conic diagonal
-                            v3 = g * d_alpha;
-                            const float d_power = -Cc.w * v3;
-                            const float2 v45 = __fmul2_rn(d, make_float2(d_power, d_power));
-                            const float2 v67 = __fmul2_rn(d, make_float2(v45.x, v45.x));
-                            v4 = v45.x;
-                            v5 = v45.y;
-                            v6 = v67.x;
-                            v7 = v67.y;
-                            v8 = v45.y * d.y;
-                        }
-                    }
+                    gate = r.y > 0.0f;
                 }
             }
+            OSB_STAT(5, __popc(__ballot_sync(0xffffffffu, j < kl)));
+            alpha = has ? alpha : 0.0f;
+            g = has && gate ? g : 0.0f;
+            const float one_m = 1.0f - alpha;
+            // 1 - alpha is in [0.01, 1]: MUFU.RCP directly (what __fdividef(1, x) computes there,
+            // without its range-scaling instructions); rcp(1) = 1 exactly
+            float inv;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));
+            T_acc = T_acc * inv;
+            const float wb = alpha * T_acc;
+            const float2 v01 = __fmul2_rn(dl01, make_float2(wb, wb));
+            const float v2 = dl2 * wb;
+            const float2 cs = __fadd2_rn(make_float2(Cc.x, Cc.y), ns01);  // Cc - s
+            float d_alpha = cs.x * dl01.x;
+            d_alpha = __fmaf_rn(cs.y, dl01.y, d_alpha);
+            d_alpha = __fmaf_rn(Cc.z + ns2, dl2, d_alpha);
+            d_alpha = d_alpha * T_acc;
+            if (BG) d_alpha = d_alpha - (T_final * inv) * bg_dot;
+            // suffix (colour of everything behind) now includes this entry:
+            // (-s) = fma(Cc, -alpha, (-s) (1 - alpha)), the exact negation of fma(Cc, alpha, s (1 - alpha))
+            const float nalpha = -alpha;
+            ns01 = __ffma2_rn(make_float2(Cc.x, Cc.y), make_float2(nalpha, nalpha),
+                              __fmul2_rn(ns01, make_float2(one_m, one_m)));
+            ns2 = __fmaf_rn(Cc.z, nalpha, ns2 * one_m);
+            // dL/dpower times d, d d^T: K4b applies the conic once per Gaussian
+            // (d_p = Q sum(dL/dpower d)) and the 1/2 of the conic diagonal
+            const float v3 = g * d_alpha;
+            const float d_power = -Cc.w * v3;
+            const float2 v45 = __fmul2_rn(d, make_float2(d_power, d_power));
+            const float2 v67 = __fmul2_rn(d, make_float2(v45.x, v45.x));
+            const float v8 = v45.y * d.y;
             const uint32_t hb_all = __ballot_sync(0xffffffffu, has);
             OSB_STAT(6, __popc(hb_all));
             if (hb_all == 0u) continue;
             OSB_STAT(2, 1);
             const uint32_t hb = hb_all & halfmask;  // this half's contributing lanes
-            float* a = reinterpret_cast<float*>(acc + 3 * static_cast<size_t>(ws.gid[j]));
+            float* a = reinterpret_cast<float*>(acc + 3 * static_cast<size_t>(ws.gid(jj)));
             // up to 10 contributing pixels of this quarter add directly (3 red instructions per
             // warp, the L2 absorbs the per-lane atomics); more are cheaper through the shuffle tree
             // (measured: always-tree 1.32 ms, <=10 direct 1.21 ms, always-direct 1.70 ms)
             const bool multi = __popc(hb) > 10;
             if (!multi && has) {
-                red_add_v4(reinterpret_cast<float4*>(a), v0, v1, v2, v3);
-                red_add_v4(reinterpret_cast<float4*>(a) + 1, v4, v5, v6, v7);
+                red_add_v4(reinterpret_cast<float4*>(a), v01.x, v01.y, v2, v3);
+                red_add_v4(reinterpret_cast<float4*>(a) + 1, v45.x, v45.y, v67.x, v67.y);
                 red_add(a + 8, v8);
             }
             if (__any_sync(0xffffffffu, multi)) {
                 OSB_STAT(3, 1);
-                const float v[9] = {v0, v1, v2, v3, v4, v5, v6, v7, v8};
+                const float v[9] = {v01.x, v01.y, v2, v3, v45.x, v45.y, v67.x, v67.y, v8};
                 int idx;
                 const float sum = half_reduce9(v, lane, &idx);
                 if (multi && idx >= 0) red_add(a + idx, sum);
