@@ -69,41 +69,19 @@ __device__ __forceinline__ float half_reduce9(const float (&v)[9], int lane, int
     return f;
 }
 
-// Shared per-CTA context of K4a's FP64 fallback: the slow path reads the FP64 records and recomputes
-// its pixel from the thread index, so none of it stays live in the hot loop's registers.
-struct K4aSlowCtx {
-    const double2* pxy;
-    const double4* conic_o;
-    double width;
-    int tiles_x;
-};
-__shared__ K4aSlowCtx s_k4a;
-
 // FP64 evaluation of instance `gid` at this thread's pixel (rasterizer.cpp:128-134) for K4a:
 // returns {alpha, g} with alpha = -1 when the pair does not contribute in FP64 and g negated when the
 // 0.99 clamp gate (gradients.cpp:146, o g < 0.99) is closed. Out of line: called for < 0.1 % of pairs.
 static __device__ __noinline__ float2 k4a_slow(uint32_t gid) {
-    const int tile = blockIdx.x;
-    const WarpPixel wp = warp_pixel(threadIdx.x >> 5, threadIdx.x & 31);
-    const int px = (tile % s_k4a.tiles_x) * kTile + wp.lx, py = (tile / s_k4a.tiles_x) * kTile + wp.ly;
-    const double2 pc = s_k4a.pxy[gid];
-    const double4 co = s_k4a.conic_o[gid];
+    int px, py;
+    slow_pixel(px, py);
+    const double2 pc = s_slow.pxy[gid];
+    const double4 co = s_slow.conic_o[gid];
     double g, alpha;
-    if (!pair_fp64(pc.x, pc.y, co.x, co.y, co.z, co.w, px + 0.5, py + 0.5, s_k4a.width, &g, &alpha))
+    if (!pair_fp64(pc.x, pc.y, co.x, co.y, co.z, co.w, px + 0.5, py + 0.5, s_slow.width, &g, &alpha))
         return make_float2(-1.0f, 0.0f);
     const float gf = static_cast<float>(g);
     return make_float2(static_cast<float>(alpha), co.w * g < kAlphaMax ? gf : -gf);
-}
-
-__device__ __forceinline__ uint32_t bfind_u32(uint32_t x) {  // index of the highest set bit, ~0u for 0
-    uint32_t r;
-    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
-    return r;
-}
-__device__ __forceinline__ uint32_t bit_u32(uint32_t j) {  // 1 << j, 0 for j >= 32 (PTX clamps the shift)
-    uint32_t r;
-    asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(j));
-    return r;
 }
 
 // BG: a non-black background adds the -T_final / (1 - alpha) * (bg . dL/dC) term (gradients.cpp:141).
@@ -166,7 +144,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
     // half-warp culling as K3), back to front; the halves reduce their (different) entries at once.
     const uint32_t halfmask = wp.half ? 0xFFFF0000u : 0x0000FFFFu;
     if (lane == 0) s_last[warp] = max_last;
-    if (threadIdx.x == 0) s_k4a = K4aSlowCtx{pp.pxy, pp.conic_o, width, tiles_x};
+    if (threadIdx.x == 0) s_slow = SlowCtx{pp.pxy, pp.conic_o, width, tiles_x};
     __syncthreads();
     int cta_last = 0;
 #pragma unroll

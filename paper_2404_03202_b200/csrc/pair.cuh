@@ -195,6 +195,34 @@ __device__ __forceinline__ bool pair_power2(const float4 A, const float4 B, floa
     return true;
 }
 
+// Per-CTA context of the out-of-line FP64 fallbacks (K3, K4a): they read the FP64 records and
+// recompute their pixel from the thread index, so none of it stays live in the hot loops' registers.
+struct SlowCtx {
+    const double2* pxy;
+    const double4* conic_o;
+    double width;
+    int tiles_x;
+};
+static __shared__ SlowCtx s_slow;
+
+__device__ __forceinline__ void slow_pixel(int& px, int& py) {
+    const int tile = blockIdx.x;
+    const WarpPixel wp = warp_pixel(threadIdx.x >> 5, threadIdx.x & 31);
+    px = (tile % s_slow.tiles_x) * kTile + wp.lx;
+    py = (tile / s_slow.tiles_x) * kTile + wp.ly;
+}
+
+__device__ __forceinline__ uint32_t bfind_u32(uint32_t x) {  // index of the highest set bit, ~0u for 0
+    uint32_t r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+__device__ __forceinline__ uint32_t bit_u32(uint32_t j) {  // 1 << j, 0 for j >= 32 (PTX clamps the shift)
+    uint32_t r;
+    asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(j));
+    return r;
+}
+
 struct Pair64 {
     double alpha, g, og;
 };
