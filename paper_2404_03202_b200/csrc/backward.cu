@@ -264,7 +264,10 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
             float* a = reinterpret_cast<float*>(acc + 3 * static_cast<size_t>(ws.gid(jj)));
             // up to 10 contributing pixels of this quarter add directly (3 red instructions per
             // warp, the L2 absorbs the per-lane atomics); more are cheaper through the shuffle tree
-            // (measured: always-tree 1.32 ms, <=10 direct 1.21 ms, always-direct 1.70 ms)
+            // (measured: always-tree 1.32 ms, <=10 direct 1.21 ms, always-direct 1.70 ms; with the
+            // branch-free loop: <=6 direct 0.988, <=10 0.954; one or two butterfly levels then direct
+            // adds by the group leaders 1.177 / 1.027; the tree's sums gathered into two red.v4 + one
+            // scalar per half 1.055 — the L2 absorbs nine scalar reds better than the extra shuffles)
             const bool multi = __popc(hb) > 10;
             if (!multi && has) {
                 red_add_v4(reinterpret_cast<float4*>(a), v01.x, v01.y, v2, v3);

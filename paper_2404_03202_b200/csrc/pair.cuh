@@ -121,8 +121,12 @@ __device__ __forceinline__ uint32_t ellipse_row_cols(float cx, float cy, float h
     const float det4 = fmaxf(4.0f * ha * hc - b * b - 1e-5f * (4.0f * ha * hc + b * b), 0.0f);
     const float q = 4.0f * ha * P - det4 * dys * dys;
     if (!(ha > 0.0f) || !(q >= 0.0f)) return ha > 0.0f ? 0u : cols_box;  // band misses / degenerate: keep box
-    const float inv2ha = 0.5f / ha;
-    const float hw = sqrtf(q) * inv2ha;
+    // MUFU approximations (relative error ~2^-22, far inside the 1e-3 relative slack below)
+    float rha, sq;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rha) : "f"(ha));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(sq) : "f"(q));
+    const float inv2ha = 0.5f * rha;
+    const float hw = sq * inv2ha;
     const float d1 = -b * dylo * inv2ha, d2 = -b * dyhi * inv2ha;
     const float slack = 1e-3f * (fabsf(cx) + fabsf(d1) + fabsf(d2) + hw) + 0.05f;
     const float xlo = cx - fmaxf(d1, d2) - hw - slack, xhi = cx - fminf(d1, d2) + hw + slack;
