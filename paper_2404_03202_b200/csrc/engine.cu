@@ -414,19 +414,16 @@ void Engine::render_into(Frame* f) {
     const uint32_t* order;
     {
         Span sp(*this, kDepthSort);
-        launch_iota(f->ovals[0].as<uint32_t>(), N, stream_);
         OSB_CUDA_CHECK(cudaMemsetAsync(long_run_flag, 0, 4, stream_));
         bool flipped;
         if (f->full_depth_sort) {
-            OSB_CUDA_CHECK(cudaMemcpyAsync(f->okeys[0].as<uint64_t>(), pp.depth_key, size_t(N) * 8, cudaMemcpyDeviceToDevice,
-                                           stream_));
             flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(), f->ovals[0].as<uint32_t>(),
-                                     f->ovals[1].as<uint32_t>(), N, 64, f->sort_ws.as<void>(), stream_);
+                                     f->ovals[1].as<uint32_t>(), N, 64, f->sort_ws.as<void>(), stream_, pp.depth_key,
+                                     true);
         } else {
             uint32_t* k32[2] = {f->okeys[0].as<uint32_t>(), f->okeys[1].as<uint32_t>()};
-            launch_depth_key24(pp.depth_key32, pp.depth_range, N, k32[0], stream_);
-            flipped = radix_sort_u32(k32[0], k32[1], f->ovals[0].as<uint32_t>(), f->ovals[1].as<uint32_t>(), N, 24,
-                                     f->sort_ws.as<void>(), stream_);
+            flipped = radix_sort_depth24(pp.depth_key32, pp.depth_range, k32[0], k32[1], f->ovals[0].as<uint32_t>(),
+                                         f->ovals[1].as<uint32_t>(), N, f->sort_ws.as<void>(), stream_);
             launch_fix_runs(k32[flipped ? 1 : 0], f->ovals[flipped ? 1 : 0].as<uint32_t>(), pp.depth_key, N,
                             long_run_flag, stream_);
         }
@@ -436,7 +433,7 @@ void Engine::render_into(Frame* f) {
     // instance buffer yet sizes it first (one synchronous counting pass).
     if (f->ikeys[0].capacity() == 0) {
         launch_scan_emit(pp.touched, order, pp.rect, N, f->tiles_x, nullptr, nullptr, 0, f->total.as<uint32_t>(),
-                         f->scan_ws.as<void>(), stream_);
+                         f->scan_ws.as<void>(), nullptr, stream_);
         uint32_t host = 0;
         OSB_CUDA_CHECK(cudaMemcpyAsync(&host, f->total.as<uint32_t>(), 4, cudaMemcpyDeviceToHost, stream_));
         OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -444,10 +441,12 @@ void Engine::render_into(Frame* f) {
     }
     const uint32_t cap = static_cast<uint32_t>(f->ikeys[0].capacity() / 4);
     f->cap = cap;
+    f->emit_first.ensure((static_cast<size_t>(emit_ctas(cap)) + 1) * 4);
     {
         Span sp(*this, kScan);
         launch_scan_emit(pp.touched, order, pp.rect, N, f->tiles_x, f->ikeys[0].as<uint32_t>(),
-                         f->ivals[0].as<uint32_t>(), cap, f->total.as<uint32_t>(), f->scan_ws.as<void>(), stream_);
+                         f->ivals[0].as<uint32_t>(), cap, f->total.as<uint32_t>(), f->scan_ws.as<void>(),
+                         f->emit_first.as<uint32_t>(), stream_);
     }
     // {M, long-run flag} are final here: read them back now so validate() only waits for this
     // point of the frame, not for the blend

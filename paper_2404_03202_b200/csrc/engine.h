@@ -83,7 +83,7 @@ struct Frame {
     // pixels
     DevBuf rgb, T, contrib, last, visited, work;
     bool count_work = false;
-    DevBuf sort_ws, scan_ws;
+    DevBuf sort_ws, scan_ws, emit_first;
     // Frames of host-supplied projections (render_projected): no Gaussian parameters behind them,
     // so no backward; `grid_*` hold a caller-supplied tile grid (K2 skipped) when given_grid.
     bool projected = false, given_grid = false;

@@ -42,15 +42,19 @@ struct SortWorkspace;  // opaque, owned by the context
 size_t radix_workspace_bytes(int n_max, int key_bytes);
 // Stable LSD radix sort of (key, value) pairs on bits [0, bits). keys/vals are double-buffered:
 // the result ends up in *_out when the function returns true, in *_in otherwise.
+// first_keys: the first pass reads its keys from there instead of keys_in (left untouched);
+// iota_vals: values are the element indices (vals_in is only a ping-pong buffer).
 bool radix_sort_u64(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
-                    int bits, void* ws, cudaStream_t s);
+                    int bits, void* ws, cudaStream_t s, const uint64_t* first_keys = nullptr, bool iota_vals = false);
 // n_dev: optional device-side count (the sort covers min(n, *n_dev) elements; grids sized by n).
 bool radix_sort_u32(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
                     int bits, void* ws, cudaStream_t s, const uint32_t* n_dev = nullptr);
-void launch_iota(uint32_t* v, int n, cudaStream_t s);
-// keys24[i] = (bits[i] - min) >> shift with the smallest shift that fits the visible range below
-// 0xFFFFFF (culled -> 0xFFFFFF): a monotone 24-bit depth key for the 3-pass fast depth rank.
-void launch_depth_key24(const uint32_t* bits, const uint32_t* range, int n, uint32_t* keys24, cudaStream_t s);
+// The fast depth rank: stable 3-pass sort of Gaussian ids 0..n-1 (no value input) by the 24-bit key
+// (bits[i] - min) >> shift, the smallest shift that fits the visible range below 0xFFFFFF (culled ->
+// 0xFFFFFF), computed on the fly by the first pass from K1's FP32 depth bits and their {min, ~max}
+// range; the keys end up in ki/ko like radix_sort_u32.
+bool radix_sort_depth24(const uint32_t* depth_bits, const uint32_t* range, uint32_t* ki, uint32_t* ko, uint32_t* vi,
+                        uint32_t* vo, int n, void* ws, cudaStream_t s);
 // After a stable sort by the FP32-rounded depth: restore the exact (FP64 depth, id) order inside
 // runs of equal keys; a run longer than 32 sets *flag (caller falls back to the 64-bit sort).
 void launch_fix_runs(const uint32_t* keys, uint32_t* order, const uint64_t* depth_key, int n, uint32_t* flag,
@@ -68,8 +72,11 @@ struct EmitArrays {
     const int2* rank_rc;
 };
 EmitArrays scan_emit_arrays(void* ws, int n);
+// cta_first: emit_ctas(capacity) + 1 words of scratch (first depth rank of every emission CTA).
+long emit_ctas(uint32_t capacity);
 void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
-                      uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws, cudaStream_t s);
+                      uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws,
+                      uint32_t* cta_first, cudaStream_t s);
 void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s,
                    const uint32_t* m_dev = nullptr);
 

@@ -44,6 +44,30 @@ __host__ __device__ constexpr int tile_keys() {
     return kSortThreads * SortCfg<K>::kItems;
 }
 
+// First pass of a sort may read its keys through a transform and take identity values:
+// key24 != nullptr: the 24-bit depth key (bits - min) >> shift of K1's FP32 depth bits (culled:
+// 0xFFFFFF), the range {min, ~max} of the visible bits at key24[0..1]; vals_in == nullptr: value =
+// element index (the depth rank sorts Gaussian ids 0..n-1).
+struct Key24 {
+    uint32_t lo = 0;
+    int shift = 0;
+    bool on = false;
+    __device__ explicit Key24(const uint32_t* range) {
+        if (!range) return;
+        on = true;
+        lo = range[0];
+        const uint32_t hi = ~range[1];
+        const uint32_t span = hi >= lo ? hi - lo : 0u;
+        while ((span >> shift) >= 0xFFFFFFu) ++shift;
+    }
+    template <typename K>
+    __device__ __forceinline__ K operator()(K b) const {
+        if (!on) return b;
+        const uint32_t u = static_cast<uint32_t>(b);
+        return static_cast<K>(u == 0xFFFFFFFFu ? 0xFFFFFFu : (u - lo) >> shift);
+    }
+};
+
 // Element count of a sort: the host bound, or min(bound, *n_dev) when the count lives on the device
 // (the tile sort runs before the host knows M; the grid is sized for the buffer capacity).
 __device__ __forceinline__ int sort_count(int n_cap, const uint32_t* n_dev) {
@@ -85,8 +109,10 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
 template <typename K>
 __global__ void __launch_bounds__(kSortThreads) k_upsweep(const K* __restrict__ keys, int n_cap, const uint32_t* n_dev,
                                                           int shift, int nblocks, uint32_t* __restrict__ counts,
-                                                          int passes, uint32_t* __restrict__ hist) {
+                                                          int passes, uint32_t* __restrict__ hist,
+                                                          const uint32_t* __restrict__ key24) {
     const int n = sort_count(n_cap, n_dev);
+    const Key24 xf(key24);
     constexpr int kTile = tile_keys<K>();
     __shared__ uint32_t s_hist[kSortWarps][kBins];
     __shared__ uint32_t s_tot[kMaxPasses][kBins];
@@ -98,7 +124,7 @@ __global__ void __launch_bounds__(kSortThreads) k_upsweep(const K* __restrict__ 
     const long base = static_cast<long>(blockIdx.x) * kTile;
     const int count = static_cast<int>(max(0L, min(static_cast<long>(kTile), static_cast<long>(n) - base)));
     for (int i = threadIdx.x; i < count; i += kSortThreads) {
-        const K k = keys[base + i];
+        const K k = xf(keys[base + i]);
         atomicAdd(&s_hist[warp][static_cast<uint32_t>((k >> shift) & (kBins - 1))], 1u);
         if (hist)
             for (int p = 1; p < passes; ++p)
@@ -130,19 +156,21 @@ __global__ void __launch_bounds__(kSortThreads) k_scan_counts(const uint32_t* __
         uint32_t total;
         const uint32_t ex = block_exclusive_scan(digit_totals[threadIdx.x], s_scan, &total);
         if (static_cast<int>(threadIdx.x) == d) s_base = ex;
-        __syncthreads();
+        __syncthreads();  // s_base visible; s_scan free for the next scan
     }
+    // each thread sums a contiguous run of blocks, one block-wide scan, then the run is written
     const uint32_t* row = counts + static_cast<size_t>(d) * nblocks;
     uint32_t* out = offsets + static_cast<size_t>(d) * nblocks;
-    uint32_t carry = s_base;
-    for (int b0 = 0; b0 < nblocks; b0 += kSortThreads) {
-        const int b = b0 + threadIdx.x;
-        const uint32_t v = b < nblocks ? row[b] : 0u;
-        uint32_t total;
-        const uint32_t ex = block_exclusive_scan(v, s_scan, &total);
-        if (b < nblocks) out[b] = carry + ex;
-        carry += total;
-        __syncthreads();
+    const int per = (nblocks + kSortThreads - 1) / kSortThreads;
+    const int b0 = threadIdx.x * per, b1 = min(b0 + per, nblocks);
+    uint32_t local = 0;
+    for (int b = b0; b < b1; ++b) local += row[b];
+    uint32_t total;
+    uint32_t run = s_base + block_exclusive_scan(local, s_scan, &total);
+    for (int b = b0; b < b1; ++b) {
+        const uint32_t v = row[b];
+        out[b] = run;
+        run += v;
     }
 }
 
@@ -151,8 +179,10 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict_
                                                             const uint32_t* __restrict__ vals_in,
                                                             K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                                                             int n_cap, const uint32_t* n_dev, int shift, int nblocks,
-                                                            const uint32_t* __restrict__ offsets) {
+                                                            const uint32_t* __restrict__ offsets,
+                                                            const uint32_t* __restrict__ key24) {
     const int n = sort_count(n_cap, n_dev);
+    const Key24 xf(key24);
     if (static_cast<long>(blockIdx.x) * kSortThreads * SortCfg<K>::kItems >= n) return;
     constexpr int kItems = SortCfg<K>::kItems;
     constexpr int kTile = kSortThreads * kItems;
@@ -179,8 +209,8 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict_
     for (int i = 0; i < kItems; ++i) {
         const long idx = base + i * 32 + lane;
         const bool valid = idx < n;
-        key[i] = valid ? keys_in[idx] : K(0);
-        val[i] = valid ? vals_in[idx] : 0u;
+        key[i] = valid ? xf(keys_in[idx]) : K(0);
+        val[i] = valid ? (vals_in ? vals_in[idx] : static_cast<uint32_t>(idx)) : 0u;
     }
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
@@ -243,23 +273,6 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict_
         keys_out[dst] = k;
         vals_out[dst] = s_vals[i];
     }
-}
-
-__global__ void k_depth_key24(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ range, int n,
-                              uint32_t* __restrict__ out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t lo = range[0], hi = ~range[1];
-    const uint32_t span = hi >= lo ? hi - lo : 0u;
-    int shift = 0;
-    while ((span >> shift) >= 0xFFFFFFu) ++shift;
-    const uint32_t b = bits[i];
-    out[i] = b == 0xFFFFFFFFu ? 0xFFFFFFu : (b - lo) >> shift;
-}
-
-__global__ void k_iota(uint32_t* v, int n) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) v[i] = static_cast<uint32_t>(i);
 }
 
 // ---- scan of tiles_touched (depth order) + load-balanced instance emission ----------------------
@@ -343,7 +356,8 @@ __global__ void __launch_bounds__(kScanThreads) k_emit_prep(const uint32_t* __re
                                                             const int4* __restrict__ rect, int n,
                                                             const uint32_t* __restrict__ block_offsets,
                                                             uint32_t* __restrict__ rank_off,
-                                                            uint32_t* __restrict__ rank_gid, int2* __restrict__ rank_rc) {
+                                                            uint32_t* __restrict__ rank_gid, int2* __restrict__ rank_rc,
+                                                            uint32_t* __restrict__ cta_first, int nctas) {
     __shared__ uint32_t s_scan[kSortWarps + 1];
     const long r0 = static_cast<long>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
     uint32_t v[kScanItems], g[kScanItems];
@@ -369,6 +383,12 @@ __global__ void __launch_bounds__(kScanThreads) k_emit_prep(const uint32_t* __re
         rank_off[r] = run;
         rank_gid[r] = g[i];
         rank_rc[r] = rc;
+        // the rank owning output b * kEmitTile starts k_emit's CTA b (no binary search there);
+        // entry nctas bounds the last CTA's window when M exceeds the capacity
+        if (v[i] > 0 && cta_first)
+            for (uint32_t b = (run + kEmitTile - 1) / kEmitTile; b <= (run + v[i] - 1) / kEmitTile &&
+                                                                  b <= static_cast<uint32_t>(nctas); ++b)
+                cta_first[b] = static_cast<uint32_t>(r);
         run += v[i];
     }
 }
@@ -389,7 +409,7 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
                                                        const int2* __restrict__ rank_rc, int n,
                                                        const uint32_t* __restrict__ total, int tiles_x,
                                                        uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                                       uint32_t capacity) {
+                                                       uint32_t capacity, const uint32_t* __restrict__ cta_first) {
     __shared__ uint32_t s_off[kEmitWindow];
     __shared__ int s_rb, s_w;
     const uint32_t M = *total;
@@ -397,8 +417,11 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
     if (o_begin >= M) return;
     const uint32_t o_end = min(o_begin + static_cast<uint32_t>(kEmitTile), M);
     if (threadIdx.x == 0) {
-        const int rb = owner_of(rank_off, n, o_begin);
-        const int re = owner_of(rank_off, n, o_end - 1);
+        // first rank from k_emit_prep; the owner of the next CTA's first output bounds the window
+        // (the last CTA searches: the culled ranks with no instances follow it)
+        const int rb = static_cast<int>(cta_first[blockIdx.x]);
+        const int re = o_end < M ? static_cast<int>(cta_first[blockIdx.x + 1])
+                                 : rb + owner_of(rank_off + rb, n - rb, o_end - 1);
         s_rb = rb;
         s_w = re - rb + 1;
     }
@@ -477,9 +500,13 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ key
 // Workspace: hist[8][256] (global digit totals per pass) | unused[8][256] | counts[256][blocks] |
 // offsets[256][blocks]
 template <typename K>
-bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n, const uint32_t* n_dev, int bits,
-                void* ws, cudaStream_t s) {
-    if (n <= 1) return false;
+bool radix_sort(const K* first_keys, const uint32_t* key24, K* keys_in, K* keys_out, const uint32_t* first_vals,
+                uint32_t* vals_in, uint32_t* vals_out, int n, const uint32_t* n_dev, int bits, void* ws,
+                cudaStream_t s) {
+    if (n <= 1) {
+        if (n == 1 && !first_vals) OSB_CUDA_CHECK(cudaMemsetAsync(vals_in, 0, sizeof(uint32_t), s));  // id 0
+        return false;
+    }
     const int passes = (bits + kRadixBits - 1) / kRadixBits;
     const int blocks = (n + tile_keys<K>() - 1) / tile_keys<K>();
     uint32_t* hist = static_cast<uint32_t*>(ws);
@@ -488,15 +515,16 @@ bool radix_sort(K* keys_in, K* keys_out, uint32_t* vals_in, uint32_t* vals_out, 
     OSB_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kBins, s));
     bool flipped = false;
     for (int p = 0; p < passes; ++p) {
-        K* ki = flipped ? keys_out : keys_in;
+        const K* ki = p == 0 ? first_keys : (flipped ? keys_out : keys_in);
         K* ko = flipped ? keys_in : keys_out;
-        uint32_t* vi = flipped ? vals_out : vals_in;
+        const uint32_t* vi = p == 0 ? first_vals : (flipped ? vals_out : vals_in);
         uint32_t* vo = flipped ? vals_in : vals_out;
+        const uint32_t* xf = p == 0 ? key24 : nullptr;
         const int shift = p * kRadixBits;
         k_upsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, n, n_dev, shift, blocks, counts, passes,
-                                                     p == 0 ? hist : nullptr);
+                                                     p == 0 ? hist : nullptr, xf);
         k_scan_counts<<<kBins, kSortThreads, 0, s>>>(counts, blocks, hist + p * kBins, offsets);
-        k_downsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, n_dev, shift, blocks, offsets);
+        k_downsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, n_dev, shift, blocks, offsets, xf);
         OSB_LAUNCHED(3);
         flipped = !flipped;
     }
@@ -513,25 +541,20 @@ size_t radix_workspace_bytes(int n_max, int key_bytes) {
 }
 
 bool radix_sort_u64(uint64_t* ki, uint64_t* ko, uint32_t* vi, uint32_t* vo, int n, int bits, void* ws,
-                    cudaStream_t s) {
-    return radix_sort<uint64_t>(ki, ko, vi, vo, n, nullptr, bits, ws, s);
+                    cudaStream_t s, const uint64_t* first_keys, bool iota_vals) {
+    return radix_sort<uint64_t>(first_keys ? first_keys : ki, nullptr, ki, ko, iota_vals ? nullptr : vi, vi, vo, n,
+                                nullptr, bits, ws, s);
 }
 bool radix_sort_u32(uint32_t* ki, uint32_t* ko, uint32_t* vi, uint32_t* vo, int n, int bits, void* ws,
                     cudaStream_t s, const uint32_t* n_dev) {
-    return radix_sort<uint32_t>(ki, ko, vi, vo, n, n_dev, bits, ws, s);
+    return radix_sort<uint32_t>(ki, nullptr, ki, ko, vi, vi, vo, n, n_dev, bits, ws, s);
+}
+bool radix_sort_depth24(const uint32_t* depth_bits, const uint32_t* range, uint32_t* ki, uint32_t* ko, uint32_t* vi,
+                        uint32_t* vo, int n, void* ws, cudaStream_t s) {
+    return radix_sort<uint32_t>(depth_bits, range, ki, ko, nullptr, vi, vo, n, nullptr, 24, ws, s);
 }
 
-void launch_depth_key24(const uint32_t* bits, const uint32_t* range, int n, uint32_t* keys24, cudaStream_t s) {
-    if (n <= 0) return;
-    k_depth_key24<<<(n + 255) / 256, 256, 0, s>>>(bits, range, n, keys24);
-    OSB_LAUNCHED(1);
-}
-
-void launch_iota(uint32_t* v, int n, cudaStream_t s) {
-    if (n <= 0) return;
-    k_iota<<<(n + 255) / 256, 256, 0, s>>>(v, n);
-    OSB_LAUNCHED(1);
-}
+long emit_ctas(uint32_t capacity) { return (static_cast<long>(capacity) + kEmitTile - 1) / kEmitTile; }
 
 size_t scan_workspace_bytes(int n) {
     const size_t blocks = (static_cast<size_t>(n) + kScanTile - 1) / kScanTile;
@@ -551,7 +574,8 @@ EmitArrays scan_emit_arrays(void* ws, int n) {
 }
 
 void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
-                      uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws, cudaStream_t s) {
+                      uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws,
+                      uint32_t* cta_first, cudaStream_t s) {
     if (n <= 0) {
         OSB_CUDA_CHECK(cudaMemsetAsync(total, 0, sizeof(uint32_t), s));
         return;
@@ -564,12 +588,13 @@ void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4
     int2* rank_rc = reinterpret_cast<int2*>(rank_gid + npad);
     k_touch_sums<<<blocks, kScanThreads, 0, s>>>(touched, order, n, sums, rank_off);
     k_scan_block_sums<<<1, 1024, 0, s>>>(sums, blocks, total);
-    k_emit_prep<<<blocks, kScanThreads, 0, s>>>(order, rect, n, sums, rank_off, rank_gid, rank_rc);
     // one CTA per kEmitTile outputs up to the capacity (CTAs past M exit; M > capacity is retried)
-    const long grid = (static_cast<long>(capacity) + kEmitTile - 1) / kEmitTile;
+    const long grid = keys ? emit_ctas(capacity) : 0;
+    k_emit_prep<<<blocks, kScanThreads, 0, s>>>(order, rect, n, sums, rank_off, rank_gid, rank_rc, cta_first,
+                                                static_cast<int>(grid));
     if (grid > 0)
         k_emit<<<static_cast<int>(grid), kScanThreads, 0, s>>>(rank_off, rank_gid, rank_rc, n, total, tiles_x, keys,
-                                                               vals, capacity);
+                                                               vals, capacity, cta_first);
     OSB_LAUNCHED(grid > 0 ? 4 : 3);
 }
 
