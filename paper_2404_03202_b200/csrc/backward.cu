@@ -11,6 +11,8 @@
 // K4b replaces pass 3 (gradients.cpp:173-295): one thread per visible Gaussian, FP64 internals,
 // re-derives t, J, Sigma and the conic with the same device code as K1 and accumulates the raw
 // parameter gradients into the flat FP32 plane buffer (allreduce-able as one tensor).
+#include <type_traits>
+
 #include "kernels.h"
 #include "pair.cuh"
 #include "project.cuh"
@@ -185,103 +187,110 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
         // entry j of this sub-chunk lies before this pixel's last_contrib iff j < kl
         const uint32_t kl = static_cast<uint32_t>(min(max(last - sbase, 0), 32));
         OSB_STAT(0, 1);
-        while (__any_sync(0xffffffffu, bal != 0u)) {  // back to front; warp-uniform (the reduction needs all lanes)
-            const uint32_t j = bfind_u32(bal);  // ~0u once this half has no entry left
-            bal &= ~bit_u32(j);
-            const uint32_t jj = j & 31u;
-            OSB_STAT(1, 1);
-            const float4 A = ws.a(jj);
-            const float4 B = ws.b(jj);
-            const float4 Cc = ws.c(jj);
-            // FP32 power, exactly pair_power2's instructions (K3 makes the same decisions)
-            float2 d = __fadd2_rn(make_float2(A.x, A.y), nlo);
-            bool unc = false;
-            if (B.w < 0.0f) {
-                if (d.x > halfW) d.x -= fW;
-                else if (d.x < -halfW) d.x += fW;
-                unc = fabsf(fabsf(d.x) - halfW) < 0.01f;
-            }
-            const float2 q = __fmul2_rn(make_float2(A.z, A.w), d);
-            const float bdx = B.x * d.x;
-            const float power = __fmaf_rn(q.x, d.x, __fmaf_rn(q.y, d.y, bdx * d.y));
-            // candidate: an entry of this half before the pixel's last_contrib that is not a certain skip
-            const bool cand = j < kl && (power <= B.z || unc);
-            unc = unc || power < fabsf(B.w) || power > B.y;
-            float g = ex2_approx(-power * kLog2e);
-            const float og = Cc.w * g;
-            float alpha = fminf(0.99f, og);
-            // 0.99 clamp gate: certain in FP32 unless a near-opaque splat lands inside its guard band
-            bool gate = og < 0.99f;
-            const bool gchk = Cc.w >= 0.98f && fabsf(og - 0.99f) <= 0.99f * (1.5f * fabsf(B.w) + 1e-6f);
-            bool has = cand;
-            if (__any_sync(0xffffffffu, cand && (unc || gchk))) {
-                if (cand && (unc || gchk)) {
-                    const float2 r = k4a_slow(ws.gid(jj));
-                    if (unc) {
-                        has = r.x >= 0.0f;
-                        alpha = r.x;
-                        g = fabsf(r.y);
+        // the per-pixel seam wrap only in sub-chunks that hold a seam-straddling entry (B.w < 0)
+        auto walk = [&](auto seam_tag) {
+            constexpr bool SEAM = decltype(seam_tag)::value;
+            while (__any_sync(0xffffffffu, bal != 0u)) {  // back to front; warp-uniform (the reduction needs all lanes)
+                const uint32_t j = bfind_u32(bal);  // ~0u once this half has no entry left
+                bal &= ~bit_u32(j);
+                const uint32_t jj = j & 31u;
+                OSB_STAT(1, 1);
+                const float4 A = ws.a(jj);
+                const float4 B = ws.b(jj);
+                const float4 Cc = ws.c(jj);
+                // FP32 power, exactly pair_power2's instructions (K3 makes the same decisions)
+                float2 d = __fadd2_rn(make_float2(A.x, A.y), nlo);
+                bool unc = false;
+                if (SEAM && B.w < 0.0f) {
+                    if (d.x > halfW) d.x -= fW;
+                    else if (d.x < -halfW) d.x += fW;
+                    unc = fabsf(fabsf(d.x) - halfW) < 0.01f;
+                }
+                const float2 q = __fmul2_rn(make_float2(A.z, A.w), d);
+                const float bdx = B.x * d.x;
+                const float power = __fmaf_rn(q.x, d.x, __fmaf_rn(q.y, d.y, bdx * d.y));
+                // candidate: an entry of this half before the pixel's last_contrib that is not a certain skip
+                const bool cand = j < kl && (power <= B.z || unc);
+                unc = unc || power < fabsf(B.w) || power > B.y;
+                float g = ex2_approx(-power * kLog2e);
+                const float og = Cc.w * g;
+                float alpha = fminf(0.99f, og);
+                // 0.99 clamp gate: certain in FP32 unless a near-opaque splat (o >= 0.98) lands inside its
+                // guard band — checked only behind the rare-path vote
+                bool gate = og < 0.99f;
+                bool has = cand;
+                if (__any_sync(0xffffffffu, cand && (unc || Cc.w >= 0.98f))) {
+                    const bool gchk = Cc.w >= 0.98f && fabsf(og - 0.99f) <= 0.99f * (1.5f * fabsf(B.w) + 1e-6f);
+                    if (cand && (unc || gchk)) {
+                        const float2 r = k4a_slow(ws.gid(jj));
+                        if (unc) {
+                            has = r.x >= 0.0f;
+                            alpha = r.x;
+                            g = fabsf(r.y);
+                        }
+                        gate = r.y > 0.0f;
                     }
-                    gate = r.y > 0.0f;
+                }
+                OSB_STAT(5, __popc(__ballot_sync(0xffffffffu, j < kl)));
+                alpha = has ? alpha : 0.0f;
+                g = has && gate ? g : 0.0f;
+                const float one_m = 1.0f - alpha;
+                // 1 - alpha is in [0.01, 1]: MUFU.RCP directly (what __fdividef(1, x) computes there,
+                // without its range-scaling instructions); rcp(1) = 1 exactly
+                float inv;
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));
+                T_acc = T_acc * inv;
+                const float wb = alpha * T_acc;
+                const float2 v01 = __fmul2_rn(dl01, make_float2(wb, wb));
+                const float v2 = dl2 * wb;
+                const float2 cs = __fadd2_rn(make_float2(Cc.x, Cc.y), ns01);  // Cc - s
+                float d_alpha = cs.x * dl01.x;
+                d_alpha = __fmaf_rn(cs.y, dl01.y, d_alpha);
+                d_alpha = __fmaf_rn(Cc.z + ns2, dl2, d_alpha);
+                d_alpha = d_alpha * T_acc;
+                if (BG) d_alpha = d_alpha - (T_final * inv) * bg_dot;
+                // suffix (colour of everything behind) now includes this entry:
+                // (-s) = fma(Cc, -alpha, (-s) (1 - alpha)), the exact negation of fma(Cc, alpha, s (1 - alpha))
+                const float nalpha = -alpha;
+                ns01 = __ffma2_rn(make_float2(Cc.x, Cc.y), make_float2(nalpha, nalpha),
+                                  __fmul2_rn(ns01, make_float2(one_m, one_m)));
+                ns2 = __fmaf_rn(Cc.z, nalpha, ns2 * one_m);
+                // dL/dpower times d, d d^T: K4b applies the conic once per Gaussian
+                // (d_p = Q sum(dL/dpower d)) and the 1/2 of the conic diagonal
+                const float v3 = g * d_alpha;
+                const float d_power = -Cc.w * v3;
+                const float2 v45 = __fmul2_rn(d, make_float2(d_power, d_power));
+                const float2 v67 = __fmul2_rn(d, make_float2(v45.x, v45.x));
+                const float v8 = v45.y * d.y;
+                const uint32_t hb_all = __ballot_sync(0xffffffffu, has);
+                OSB_STAT(6, __popc(hb_all));
+                if (hb_all == 0u) continue;
+                OSB_STAT(2, 1);
+                const uint32_t hb = hb_all & halfmask;  // this half's contributing lanes
+                float* a = reinterpret_cast<float*>(acc + 3 * static_cast<size_t>(ws.gid(jj)));
+                // up to 10 contributing pixels of this quarter add directly (3 red instructions per
+                // warp, the L2 absorbs the per-lane atomics); more are cheaper through the shuffle tree
+                // (measured: always-tree 1.32 ms, <=10 direct 1.21 ms, always-direct 1.70 ms; with the
+                // branch-free loop: <=6 direct 0.988, <=10 0.954; one or two butterfly levels then direct
+                // adds by the group leaders 1.177 / 1.027; the tree's sums gathered into two red.v4 + one
+                // scalar per half 1.055 — the L2 absorbs nine scalar reds better than the extra shuffles)
+                const bool multi = __popc(hb) > 10;
+                if (!multi && has) {
+                    red_add_v4(reinterpret_cast<float4*>(a), v01.x, v01.y, v2, v3);
+                    red_add_v4(reinterpret_cast<float4*>(a) + 1, v45.x, v45.y, v67.x, v67.y);
+                    red_add(a + 8, v8);
+                }
+                if (__any_sync(0xffffffffu, multi)) {
+                    OSB_STAT(3, 1);
+                    const float v[9] = {v01.x, v01.y, v2, v3, v45.x, v45.y, v67.x, v67.y, v8};
+                    int idx;
+                    const float sum = half_reduce9(v, lane, &idx);
+                    if (multi && idx >= 0) red_add(a + idx, sum);
                 }
             }
-            OSB_STAT(5, __popc(__ballot_sync(0xffffffffu, j < kl)));
-            alpha = has ? alpha : 0.0f;
-            g = has && gate ? g : 0.0f;
-            const float one_m = 1.0f - alpha;
-            // 1 - alpha is in [0.01, 1]: MUFU.RCP directly (what __fdividef(1, x) computes there,
-            // without its range-scaling instructions); rcp(1) = 1 exactly
-            float inv;
-            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(one_m));
-            T_acc = T_acc * inv;
-            const float wb = alpha * T_acc;
-            const float2 v01 = __fmul2_rn(dl01, make_float2(wb, wb));
-            const float v2 = dl2 * wb;
-            const float2 cs = __fadd2_rn(make_float2(Cc.x, Cc.y), ns01);  // Cc - s
-            float d_alpha = cs.x * dl01.x;
-            d_alpha = __fmaf_rn(cs.y, dl01.y, d_alpha);
-            d_alpha = __fmaf_rn(Cc.z + ns2, dl2, d_alpha);
-            d_alpha = d_alpha * T_acc;
-            if (BG) d_alpha = d_alpha - (T_final * inv) * bg_dot;
-            // suffix (colour of everything behind) now includes this entry:
-            // (-s) = fma(Cc, -alpha, (-s) (1 - alpha)), the exact negation of fma(Cc, alpha, s (1 - alpha))
-            const float nalpha = -alpha;
-            ns01 = __ffma2_rn(make_float2(Cc.x, Cc.y), make_float2(nalpha, nalpha),
-                              __fmul2_rn(ns01, make_float2(one_m, one_m)));
-            ns2 = __fmaf_rn(Cc.z, nalpha, ns2 * one_m);
-            // dL/dpower times d, d d^T: K4b applies the conic once per Gaussian
-            // (d_p = Q sum(dL/dpower d)) and the 1/2 of the conic diagonal
-            const float v3 = g * d_alpha;
-            const float d_power = -Cc.w * v3;
-            const float2 v45 = __fmul2_rn(d, make_float2(d_power, d_power));
-            const float2 v67 = __fmul2_rn(d, make_float2(v45.x, v45.x));
-            const float v8 = v45.y * d.y;
-            const uint32_t hb_all = __ballot_sync(0xffffffffu, has);
-            OSB_STAT(6, __popc(hb_all));
-            if (hb_all == 0u) continue;
-            OSB_STAT(2, 1);
-            const uint32_t hb = hb_all & halfmask;  // this half's contributing lanes
-            float* a = reinterpret_cast<float*>(acc + 3 * static_cast<size_t>(ws.gid(jj)));
-            // up to 10 contributing pixels of this quarter add directly (3 red instructions per
-            // warp, the L2 absorbs the per-lane atomics); more are cheaper through the shuffle tree
-            // (measured: always-tree 1.32 ms, <=10 direct 1.21 ms, always-direct 1.70 ms; with the
-            // branch-free loop: <=6 direct 0.988, <=10 0.954; one or two butterfly levels then direct
-            // adds by the group leaders 1.177 / 1.027; the tree's sums gathered into two red.v4 + one
-            // scalar per half 1.055 — the L2 absorbs nine scalar reds better than the extra shuffles)
-            const bool multi = __popc(hb) > 10;
-            if (!multi && has) {
-                red_add_v4(reinterpret_cast<float4*>(a), v01.x, v01.y, v2, v3);
-                red_add_v4(reinterpret_cast<float4*>(a) + 1, v45.x, v45.y, v67.x, v67.y);
-                red_add(a + 8, v8);
-            }
-            if (__any_sync(0xffffffffu, multi)) {
-                OSB_STAT(3, 1);
-                const float v[9] = {v01.x, v01.y, v2, v3, v45.x, v45.y, v67.x, v67.y, v8};
-                int idx;
-                const float sum = half_reduce9(v, lane, &idx);
-                if (multi && idx >= 0) red_add(a + idx, sum);
-            }
-        }
+        };
+        if (__any_sync(0xffffffffu, ws.b(lane).w < 0.0f)) walk(std::true_type{});
+        else walk(std::false_type{});
         __syncwarp();
       }
         __syncthreads();  // the stage is rewritten by the next chunk
