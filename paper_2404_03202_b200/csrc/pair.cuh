@@ -181,11 +181,13 @@ __device__ __forceinline__ uint32_t stage_record16(WarpStage& ws, int lane, uint
 // threshold (power < 0, alpha < 1/255) or of the seam wrap tie. The paired operations issue as
 // packed f32x2 instructions (FADD2 / FMUL2: half the issue slots, each half rounded exactly like the
 // scalar op), and K3 and K4a run exactly this code, so the backward replays the forward's decisions.
+// SEAM = false: the caller knows no staged entry straddles the seam (B.w >= 0), so the wrap is skipped.
+template <bool SEAM = true>
 __device__ __forceinline__ bool pair_power2(const float4 A, const float4 B, float2 nlo, float halfW, float fW,
                                             float2& d, float& power, bool& unc) {
     d = __fadd2_rn(make_float2(A.x, A.y), nlo);  // (A.x - lxo, A.y - lyo)
     unc = false;
-    if (B.w < 0.0f) {
+    if (SEAM && B.w < 0.0f) {
         if (d.x > halfW) d.x -= fW;
         else if (d.x < -halfW) d.x += fW;
         unc = fabsf(fabsf(d.x) - halfW) < 0.01f;
