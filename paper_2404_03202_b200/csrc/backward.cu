@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
     constexpr int kChunk = kPer * kTileThreads;   // entries per round (one barrier pair)
     constexpr int kSubs = kChunk / 32;
     __shared__ WarpStage stage[kSubs];
-    __shared__ uint32_t s_cm[kSubs * 16];  // contributor masks of the round (K3)
+    __shared__ uint16_t s_mask[kChunk];
     __shared__ int s_last[kTileWarps];
     const int tile = blockIdx.x;
     const int tx = tile % tiles_x, ty = tile / tiles_x;
@@ -155,38 +155,35 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
 #ifdef OSB_K4A_STATS
     unsigned long long st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
-    // rounds aligned to K3's 32-entry sub-chunks (the contributor masks are per sub-chunk)
-    const int L = static_cast<int>(range.y - range.x);
-    const uint32_t cm_base = cmask_base(tile, range.x);
-    for (int hi = (cta_last + 31) & ~31; hi > 0; hi -= kChunk) {
+    for (int hi = cta_last; hi > 0; hi -= kChunk) {
         const int lo = hi > kChunk ? hi - kChunk : 0;
         OSB_STAT(7, lane == 0 ? static_cast<unsigned long long>(hi - lo) : 0ull);
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
             const int i = lo + t + e * kTileThreads;
-            if (i < hi && i < L) {
+            uint32_t m = 0u;
+            if (i < hi) {
                 const uint32_t gid = inst_gid[range.x + i];
                 const float4* s4 = reinterpret_cast<const float4*>(pp.splat + gid);
-                stage_record16<false>(stage[warp + e * kTileWarps], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc, yc,
-                                      width);
+                m = stage_record16<true>(stage[warp + e * kTileWarps], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc, yc,
+                                   width);
             } else {
                 // finite filler: lanes with no entry left evaluate slot 31 with alpha forced to 0
                 WarpStage& w = stage[warp + e * kTileWarps];
                 w.a[lane] = w.b[lane] = w.c[lane] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                 w.gid[lane] = 0u;
             }
-        }
-        {  // the round's contributor masks (16 sub-chunks x 16 quarters, one word per thread)
-            const int sub = t >> 4;
-            s_cm[t] = lo + 32 * sub < min(hi, L) ? fb.cmask[(cm_base + (lo >> 5) + sub) * 16 + (t & 15)] : 0u;
+            s_mask[t + e * kTileThreads] = static_cast<uint16_t>(m);
         }
         __syncthreads();
       for (int sub = kSubs - 1; sub >= 0; --sub) {
         const int sbase = lo + 32 * sub;
         if (sbase >= hi || sbase >= max_last) continue;  // no pixel of this warp reaches these entries
         const StageRef ws{stage_s + static_cast<uint32_t>(sub * sizeof(WarpStage))};
-        // entries of this sub-chunk that contribute to at least one pixel of this half's quarter (K3)
-        uint32_t bal = s_cm[16 * sub + 2 * warp + wp.half];
+        const uint32_t mk = s_mask[32 * sub + lane];
+        const uint32_t bal0 = __ballot_sync(0xffffffffu, (mk >> (2 * warp)) & 1u);
+        const uint32_t bal1 = __ballot_sync(0xffffffffu, (mk >> (2 * warp + 1)) & 1u);
+        uint32_t bal = wp.half ? bal1 : bal0;
         // entry j of this sub-chunk lies before this pixel's last_contrib iff j < kl
         const uint32_t kl = static_cast<uint32_t>(min(max(last - sbase, 0), 32));
         OSB_STAT(0, 1);

@@ -14,14 +14,10 @@
 
 namespace osb {
 
-#ifndef OSB_K3_MINB
-#define OSB_K3_MINB 4
-#endif
-
 namespace {
 
 template <bool STRICT>
-__global__ void __launch_bounds__(kTileThreads, OSB_K3_MINB) k_blend(const uint32_t* __restrict__ inst_gid,
+__global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __restrict__ inst_gid,
                                                            const uint2* __restrict__ ranges, PreprocessOut pp, int W,
                                                            int H, int tiles_x, float bg0, float bg1, float bg2,
                                                            FrameBuffers fb) {
@@ -58,38 +54,21 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_MINB) k_blend(const uint3
     float Terr = 0.0f;  // bound on alpha-error propagation into T (exact mode: not needed)
     bool exact = false;
     int contrib = 0, last = 0;
-    // work counting (fb.visited): entries evaluated per pixel, stored at the stop (the whole list if
-    // the pixel never stops) — not kept in a register through the loop
+    int stop_at = static_cast<int>(range.y - range.x);  // entries evaluated (work counting)
     bool done = !inside;
 
     const int t = threadIdx.x;
-    // ids one round ahead, prefetched into shared memory with cp.async (each thread reads back only
-    // its own slots after a wait_group: no registers live across the blend loop)
-    __shared__ uint32_t s_gid[kChunk];
-    const uint32_t s_gid_t = static_cast<uint32_t>(__cvta_generic_to_shared(s_gid + t));
-    auto prefetch_ids = [&](uint32_t cb) {
+    uint32_t gid_next[kPer];  // ids one round ahead
 #pragma unroll
-        for (int e = 0; e < kPer; ++e) {
-            const uint32_t idx = cb + t + e * kTileThreads;
-            if (idx < range.y)
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s_gid_t + 4u * e * kTileThreads),
-                             "l"(inst_gid + idx)
-                             : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    prefetch_ids(range.x);
+    for (int e = 0; e < kPer; ++e)
+        gid_next[e] = range.x + t + e * kTileThreads < range.y ? inst_gid[range.x + t + e * kTileThreads] : 0u;
     for (uint32_t cbase = range.x; cbase < range.y; cbase += kChunk) {
         if (!__syncthreads_or(!done)) break;  // every pixel of the tile has terminated
-        asm volatile("cp.async.wait_all;" ::: "memory");
-        uint32_t gid_cur[kPer];
-#pragma unroll
-        for (int e = 0; e < kPer; ++e) gid_cur[e] = s_gid[t + e * kTileThreads];
-        prefetch_ids(cbase + kChunk);
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
             const uint32_t idx = cbase + t + e * kTileThreads;
-            const uint32_t gid = gid_cur[e];
+            const uint32_t gid = gid_next[e];
+            gid_next[e] = idx + kChunk < range.y ? inst_gid[idx + kChunk] : 0u;
             uint32_t m = 0u;
             if (idx < range.y) {
                 const float4* s4 = reinterpret_cast<const float4*>(pp.splat + gid);
@@ -112,7 +91,6 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_MINB) k_blend(const uint3
         // the loop; the warp then replays each parked pixel's prefix cooperatively (warp_replay_T:
         // 32 entries evaluated in parallel, product in list order) and the lane resumes.
         const bool seam = __any_sync(0xffffffffu, ws.b(lane).w < 0.0f);  // a seam-straddling entry here
-        uint32_t cbits = 0u;  // entries of this sub-chunk the pixel took (contributor mask for K4a)
         bool pend = false, p_unc = false;
         int pj = 0;
         double p_a64 = 0.0;
@@ -171,7 +149,7 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_MINB) k_blend(const uint3
                         if (near) {
                             if (Tn < lo) {
                                 done = true;
-                                if (fb.visited) fb.visited[py * W + px] = kofs + j;
+                                stop_at = kofs + j;
                                 break;
                             }
                             pend = true;  // inside the band: decide in FP64 after an exact replay
@@ -186,7 +164,7 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_MINB) k_blend(const uint3
                         const double Tn64 = T64 * (1.0 - a64);
                         if (Tn64 < kTStop) {
                             done = true;
-                            if (fb.visited) fb.visited[py * W + px] = kofs + j;
+                            stop_at = kofs + j;
                             break;
                         }
                         w = static_cast<float>(a64 * T64);
@@ -197,7 +175,6 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_MINB) k_blend(const uint3
                     c2 = __fmaf_rn(Cc.z, w, c2);
                     ++contrib;
                     last = kofs + j;
-                    cbits |= 1u << j;
                 }
             };
 if (seam) lanes(std::true_type{});
@@ -223,7 +200,7 @@ if (seam) lanes(std::true_type{});
                 const double Tn64 = T64 * (1.0 - a64);
                 if (Tn64 < kTStop) {
                     done = true;
-                    if (fb.visited) fb.visited[py * W + px] = kofs + pj;
+                    stop_at = kofs + pj;
                 } else {
                     exact = true;
                     const float4 Cc = ws.c(pj);
@@ -234,17 +211,7 @@ if (seam) lanes(std::true_type{});
                     c2 = __fmaf_rn(Cc.z, w, c2);
                     ++contrib;
                     last = kofs + pj;
-                    cbits |= 1u << pj;
                 }
-            }
-        }
-        {  // per-quarter contributor mask of this sub-chunk (OR over the half-warp)
-            const uint32_t q0 = __reduce_or_sync(0xffffffffu, wp.half ? 0u : cbits);
-            const uint32_t q1 = __reduce_or_sync(0xffffffffu, wp.half ? cbits : 0u);
-            if (lane == 0) {
-                uint32_t* cm = fb.cmask + (cmask_base(tile, range.x) + ((base - range.x) >> 5)) * 16 + 2 * warp;
-                cm[0] = q0;
-                cm[1] = q1;
             }
         }
         __syncwarp();
@@ -261,7 +228,7 @@ if (seam) lanes(std::true_type{});
         fb.T[pix] = T;
         fb.contrib[pix] = contrib;
         fb.last[pix] = last;
-        if (fb.visited && !done) fb.visited[pix] = static_cast<int>(range.y - range.x);
+        if (fb.visited) fb.visited[pix] = stop_at;
     }
 }
 

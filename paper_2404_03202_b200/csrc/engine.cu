@@ -75,7 +75,6 @@ FrameBuffers Frame::fb() const {
     b.contrib = contrib.as<int>();
     b.last = last.as<int>();
     b.visited = count_work ? visited.as<int>() : nullptr;
-    b.cmask = cmask.as<uint32_t>();
     return b;
 }
 
@@ -396,7 +395,6 @@ void Engine::render_into(Frame* f) {
         OSB_CUDA_CHECK(cudaMemcpyAsync(f->ranges.as<uint2>(), f->grid_ranges.data(), size_t(tiles) * 8,
                                        cudaMemcpyHostToDevice, stream_));
         f->inst_in_alt = false;
-        f->cmask.ensure(cmask_words(M, tiles) * 4);
         {
             Span sp(*this, kBlend);
             launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(),
@@ -470,7 +468,6 @@ void Engine::render_into(Frame* f) {
                       stream_, f->total.as<uint32_t>());
     }
     // K3
-    f->cmask.ensure(cmask_words(cap, tiles) * 4);
     {
         Span sp(*this, kBlend);
         launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(), stream_,

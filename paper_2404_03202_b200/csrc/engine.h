@@ -81,7 +81,7 @@ struct Frame {
     // instances
     DevBuf ikeys[2], ivals[2], ranges;
     // pixels
-    DevBuf rgb, T, contrib, last, visited, work, cmask;
+    DevBuf rgb, T, contrib, last, visited, work;
     bool count_work = false;
     DevBuf sort_ws, scan_ws, emit_first;
     // Frames of host-supplied projections (render_projected): no Gaussian parameters behind them,

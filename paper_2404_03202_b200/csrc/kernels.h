@@ -87,13 +87,7 @@ struct FrameBuffers {
     int* contrib;      // H*W
     int* last;         // H*W
     int* visited;      // H*W or nullptr: list entries evaluated per pixel (work counting only)
-    // Contributor masks written by K3 for K4a: for every 32-entry sub-chunk s of tile t's list and
-    // every 4x4 quarter q, bit j set iff entry 32 s + j contributes to at least one pixel of q;
-    // word (cmask_base(t, range.x) + s) * 16 + q. Sized cmask_words(M, tiles).
-    uint32_t* cmask;
 };
-__host__ __device__ inline uint32_t cmask_base(int tile, uint32_t range_x) { return (range_x >> 5) + tile; }
-inline size_t cmask_words(size_t instances, int tiles) { return ((instances >> 5) + tiles + 2) * 16; }
 // Sums of per-pixel visited (forward pairs) and last_contrib (backward pairs) -> out[0], out[1].
 void launch_work_count(const FrameBuffers& fb, int pixels, unsigned long long* out, cudaStream_t s);
 // 3 FP32 planes -> interleaved H x W x 3 FP64 (the reference Image layout).
