@@ -182,7 +182,8 @@ def workload_config(args, world, V):
             "lambda_ssim": LAMBDA_SSIM,
             "parallelism": f"dp{world} (views split, Gaussians replicated; N > 1: NCCL reduce-scatter of the "
                            f"gradients, sharded Adam, all-gather of the parameters)",
-            "l2": "inputs larger than L2: params + grads + Adam moments = 4 x 236 MB resident"}
+            "l2": f"inputs larger than L2: params + grads + Adam moments = 4 x "
+                  f"{args.gaussians * 59 * 4 / 1e6:.0f} MB resident"}
 
 
 # ------------------------------------------------------------------------------------------------ reference arm
