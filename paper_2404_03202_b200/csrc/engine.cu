@@ -433,7 +433,7 @@ void Engine::render_into(Frame* f) {
     // instance buffer yet sizes it first (one synchronous counting pass).
     if (f->ikeys[0].capacity() == 0) {
         launch_scan_emit(pp.touched, order, pp.rect, N, f->tiles_x, nullptr, nullptr, 0, f->total.as<uint32_t>(),
-                         f->scan_ws.as<void>(), nullptr, stream_);
+                         f->scan_ws.as<void>(), nullptr, nullptr, stream_);
         uint32_t host = 0;
         OSB_CUDA_CHECK(cudaMemcpyAsync(&host, f->total.as<uint32_t>(), 4, cudaMemcpyDeviceToHost, stream_));
         OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
@@ -442,24 +442,28 @@ void Engine::render_into(Frame* f) {
     const uint32_t cap = static_cast<uint32_t>(f->ikeys[0].capacity() / 4);
     f->cap = cap;
     f->emit_first.ensure((static_cast<size_t>(emit_ctas(cap)) + 1) * 4);
+    // the emission also does the tile sort's first upsweep (tiles <= 2^16: two 8-bit passes)
+    const int tile_bits = bits_for(static_cast<uint64_t>(tiles));
+    const bool fused_counts = tile_bits <= 16;
+    f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(cap), 4));
     {
         Span sp(*this, kScan);
+        if (fused_counts) tile_sort_prepare(f->sort_ws.as<void>(), stream_);
         launch_scan_emit(pp.touched, order, pp.rect, N, f->tiles_x, f->ikeys[0].as<uint32_t>(),
                          f->ivals[0].as<uint32_t>(), cap, f->total.as<uint32_t>(), f->scan_ws.as<void>(),
-                         f->emit_first.as<uint32_t>(), stream_);
+                         f->emit_first.as<uint32_t>(), fused_counts ? f->sort_ws.as<void>() : nullptr, stream_);
     }
     // {M, long-run flag} are final here: read them back now so validate() only waits for this
     // point of the frame, not for the blend
     OSB_CUDA_CHECK(cudaMemcpyAsync(f->info_host, f->total.as<uint32_t>(), 8, cudaMemcpyDeviceToHost, stream_));
     OSB_CUDA_CHECK(cudaEventRecord(f->ready, stream_));
     // K2c: stable sort by tile over min(M, cap) instances (count read on the device), tile ranges
-    f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(cap), 4));
     {
         Span sp(*this, kTileSort);
         f->inst_in_alt = radix_sort_u32(f->ikeys[0].as<uint32_t>(), f->ikeys[1].as<uint32_t>(),
                                         f->ivals[0].as<uint32_t>(), f->ivals[1].as<uint32_t>(), static_cast<int>(cap),
-                                        bits_for(static_cast<uint64_t>(tiles)), f->sort_ws.as<void>(), stream_,
-                                        f->total.as<uint32_t>());
+                                        tile_bits, f->sort_ws.as<void>(), stream_, f->total.as<uint32_t>(),
+                                        fused_counts);
     }
     {
         Span sp(*this, kRanges);

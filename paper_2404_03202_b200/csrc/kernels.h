@@ -47,8 +47,11 @@ size_t radix_workspace_bytes(int n_max, int key_bytes);
 bool radix_sort_u64(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
                     int bits, void* ws, cudaStream_t s, const uint64_t* first_keys = nullptr, bool iota_vals = false);
 // n_dev: optional device-side count (the sort covers min(n, *n_dev) elements; grids sized by n).
+// counts_ready (bits <= 16 only): the first pass's block counts and every pass's digit totals are
+// already in ws (launch_scan_emit with tile_sort_ws = ws after tile_sort_prepare(ws)).
 bool radix_sort_u32(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
-                    int bits, void* ws, cudaStream_t s, const uint32_t* n_dev = nullptr);
+                    int bits, void* ws, cudaStream_t s, const uint32_t* n_dev = nullptr, bool counts_ready = false);
+void tile_sort_prepare(void* ws, cudaStream_t s);
 // The fast depth rank: stable 3-pass sort of Gaussian ids 0..n-1 (no value input) by the 24-bit key
 // (bits[i] - min) >> shift, the smallest shift that fits the visible range below 0xFFFFFF (culled ->
 // 0xFFFFFF), computed on the fly by the first pass from K1's FP32 depth bits and their {min, ~max}
@@ -74,9 +77,11 @@ struct EmitArrays {
 EmitArrays scan_emit_arrays(void* ws, int n);
 // cta_first: emit_ctas(capacity) + 1 words of scratch (first depth rank of every emission CTA).
 long emit_ctas(uint32_t capacity);
+// tile_sort_ws (optional): the emission also writes the tile sort's first upsweep into that
+// radix_sort_u32 workspace (zeroed digit totals first: tile_sort_prepare), sized for `capacity`.
 void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
                       uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws,
-                      uint32_t* cta_first, cudaStream_t s);
+                      uint32_t* cta_first, void* tile_sort_ws, cudaStream_t s);
 void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s,
                    const uint32_t* m_dev = nullptr);
 

@@ -404,18 +404,34 @@ __device__ __forceinline__ int owner_of(const uint32_t* off, int count, uint32_t
     return lo;
 }
 
+// The emitted instances are staged in shared memory and written with 16-byte stores; with `counts`
+// the CTA also produces the tile sort's first-pass upsweep for its block (sort block b = emission
+// CTA b: both cover 2048 consecutive instances): the low-digit counts of its keys at counts[d *
+// nblocks + b] and both passes' global digit totals in hist (the tile sort then skips that upsweep).
 __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restrict__ rank_off,
                                                        const uint32_t* __restrict__ rank_gid,
                                                        const int2* __restrict__ rank_rc, int n,
                                                        const uint32_t* __restrict__ total, int tiles_x,
                                                        uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                                       uint32_t capacity, const uint32_t* __restrict__ cta_first) {
+                                                       uint32_t capacity, const uint32_t* __restrict__ cta_first,
+                                                       uint32_t* __restrict__ counts, uint32_t* __restrict__ hist,
+                                                       int nblocks) {
     __shared__ uint32_t s_off[kEmitWindow];
+    __shared__ __align__(16) uint32_t s_k[kEmitTile];
+    __shared__ __align__(16) uint32_t s_v[kEmitTile];
+    __shared__ uint32_t s_h0[kBins], s_h1[kBins];
     __shared__ int s_rb, s_w;
     const uint32_t M = *total;
     const uint32_t o_begin = static_cast<uint32_t>(blockIdx.x) * kEmitTile;
-    if (o_begin >= M) return;
+    if (o_begin >= M) {
+        if (counts) counts[static_cast<size_t>(threadIdx.x) * nblocks + blockIdx.x] = 0u;
+        return;
+    }
     const uint32_t o_end = min(o_begin + static_cast<uint32_t>(kEmitTile), M);
+    if (counts) {
+        s_h0[threadIdx.x] = 0u;
+        s_h1[threadIdx.x] = 0u;
+    }
     if (threadIdx.x == 0) {
         // first rank from k_emit_prep; the owner of the next CTA's first output bounds the window
         // (the last CTA searches: the culled ranks with no instances follow it)
@@ -434,39 +450,62 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
         off = s_off;
     }
     uint32_t o = o_begin + threadIdx.x * 8;
-    if (o >= o_end) return;
-    int e = owner_of(off, w, o);
-    // the rank's record and the (row, column) of output o inside its rectangle: one division for
-    // the thread's first output, then stepped along the row-major walk; reloaded when the rank changes
-    int2 rc = rank_rc[rb + e];
-    uint32_t gid = rank_gid[rb + e];
-    uint32_t wt = static_cast<uint32_t>(rc.x) >> 16;
-    uint32_t li = o - off[e];
-    uint32_t row = li / wt, col = li - row * wt;
-    uint32_t next = e + 1 < w ? off[e + 1] : 0xFFFFFFFFu;
-    for (int q = 0; q < 8 && o < o_end; ++q, ++o) {
-        if (o >= next) {  // o belongs to a later rank (skip ranks without instances)
-            do {
-                ++e;
-                next = e + 1 < w ? off[e + 1] : 0xFFFFFFFFu;
-            } while (o >= next);
-            rc = rank_rc[rb + e];
-            gid = rank_gid[rb + e];
-            wt = static_cast<uint32_t>(rc.x) >> 16;
-            row = 0;
-            col = 0;
+    if (o < o_end) {
+        int e = owner_of(off, w, o);
+        // the rank's record and the (row, column) of output o inside its rectangle: one division for
+        // the thread's first output, then stepped along the row-major walk; reloaded when the rank changes
+        int2 rc = rank_rc[rb + e];
+        uint32_t gid = rank_gid[rb + e];
+        uint32_t wt = static_cast<uint32_t>(rc.x) >> 16;
+        uint32_t li = o - off[e];
+        uint32_t row = li / wt, col = li - row * wt;
+        uint32_t next = e + 1 < w ? off[e + 1] : 0xFFFFFFFFu;
+        for (int q = 0; q < 8 && o < o_end; ++q, ++o) {
+            if (o >= next) {  // o belongs to a later rank (skip ranks without instances)
+                do {
+                    ++e;
+                    next = e + 1 < w ? off[e + 1] : 0xFFFFFFFFu;
+                } while (o >= next);
+                rc = rank_rc[rb + e];
+                gid = rank_gid[rb + e];
+                wt = static_cast<uint32_t>(rc.x) >> 16;
+                row = 0;
+                col = 0;
+            }
+            const int x0 = static_cast<int>(static_cast<int16_t>(rc.x & 0xFFFF));
+            int kx = x0 + static_cast<int>(col);
+            kx = kx < 0 ? kx + tiles_x : (kx >= tiles_x ? kx - tiles_x : kx);
+            const uint32_t key = static_cast<uint32_t>((rc.y + static_cast<int>(row)) * tiles_x + kx);
+            s_k[o - o_begin] = key;
+            s_v[o - o_begin] = gid;
+            if (counts && o < capacity) {
+                atomicAdd(&s_h0[key & (kBins - 1)], 1u);
+                atomicAdd(&s_h1[(key >> kRadixBits) & (kBins - 1)], 1u);
+            }
+            if (++col == wt) {
+                col = 0;
+                ++row;
+            }
         }
-        const int x0 = static_cast<int>(static_cast<int16_t>(rc.x & 0xFFFF));
-        int kx = x0 + static_cast<int>(col);
-        kx = kx < 0 ? kx + tiles_x : (kx >= tiles_x ? kx - tiles_x : kx);
-        if (o < capacity) {
-            keys[o] = static_cast<uint32_t>((rc.y + static_cast<int>(row)) * tiles_x + kx);
-            vals[o] = gid;
+    }
+    __syncthreads();
+    const uint32_t cnt = min(o_end, capacity) > o_begin ? min(o_end, capacity) - o_begin : 0u;
+    if (cnt == static_cast<uint32_t>(kEmitTile)) {  // full block: 16-byte stores
+        for (int i = threadIdx.x; i < kEmitTile / 4; i += kScanThreads) {
+            reinterpret_cast<uint4*>(keys + o_begin)[i] = reinterpret_cast<const uint4*>(s_k)[i];
+            reinterpret_cast<uint4*>(vals + o_begin)[i] = reinterpret_cast<const uint4*>(s_v)[i];
         }
-        if (++col == wt) {
-            col = 0;
-            ++row;
+    } else {
+        for (uint32_t i = threadIdx.x; i < cnt; i += kScanThreads) {
+            keys[o_begin + i] = s_k[i];
+            vals[o_begin + i] = s_v[i];
         }
+    }
+    if (counts) {
+        const uint32_t c0 = s_h0[threadIdx.x], c1 = s_h1[threadIdx.x];
+        counts[static_cast<size_t>(threadIdx.x) * nblocks + blockIdx.x] = c0;
+        if (c0) atomicAdd(&hist[threadIdx.x], c0);
+        if (c1) atomicAdd(&hist[kBins + threadIdx.x], c1);
     }
 }
 
@@ -502,7 +541,7 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ key
 template <typename K>
 bool radix_sort(const K* first_keys, const uint32_t* key24, K* keys_in, K* keys_out, const uint32_t* first_vals,
                 uint32_t* vals_in, uint32_t* vals_out, int n, const uint32_t* n_dev, int bits, void* ws,
-                cudaStream_t s) {
+                cudaStream_t s, bool counts_ready = false) {
     if (n <= 1) {
         if (n == 1 && !first_vals) OSB_CUDA_CHECK(cudaMemsetAsync(vals_in, 0, sizeof(uint32_t), s));  // id 0
         return false;
@@ -512,7 +551,7 @@ bool radix_sort(const K* first_keys, const uint32_t* key24, K* keys_in, K* keys_
     uint32_t* hist = static_cast<uint32_t*>(ws);
     uint32_t* counts = hist + 2 * kMaxPasses * kBins;
     uint32_t* offsets = counts + static_cast<size_t>(kBins) * blocks;
-    OSB_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kBins, s));
+    if (!counts_ready) OSB_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kBins, s));
     bool flipped = false;
     for (int p = 0; p < passes; ++p) {
         const K* ki = p == 0 ? first_keys : (flipped ? keys_out : keys_in);
@@ -521,11 +560,14 @@ bool radix_sort(const K* first_keys, const uint32_t* key24, K* keys_in, K* keys_
         uint32_t* vo = flipped ? vals_in : vals_out;
         const uint32_t* xf = p == 0 ? key24 : nullptr;
         const int shift = p * kRadixBits;
-        k_upsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, n, n_dev, shift, blocks, counts, passes,
-                                                     p == 0 ? hist : nullptr, xf);
+        if (!(p == 0 && counts_ready)) {
+            k_upsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, n, n_dev, shift, blocks, counts, passes,
+                                                         p == 0 ? hist : nullptr, xf);
+            OSB_LAUNCHED(1);
+        }
         k_scan_counts<<<kBins, kSortThreads, 0, s>>>(counts, blocks, hist + p * kBins, offsets);
         k_downsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, n_dev, shift, blocks, offsets, xf);
-        OSB_LAUNCHED(3);
+        OSB_LAUNCHED(2);
         flipped = !flipped;
     }
     return flipped;
@@ -546,8 +588,11 @@ bool radix_sort_u64(uint64_t* ki, uint64_t* ko, uint32_t* vi, uint32_t* vo, int 
                                 nullptr, bits, ws, s);
 }
 bool radix_sort_u32(uint32_t* ki, uint32_t* ko, uint32_t* vi, uint32_t* vo, int n, int bits, void* ws,
-                    cudaStream_t s, const uint32_t* n_dev) {
-    return radix_sort<uint32_t>(ki, nullptr, ki, ko, vi, vi, vo, n, n_dev, bits, ws, s);
+                    cudaStream_t s, const uint32_t* n_dev, bool counts_ready) {
+    return radix_sort<uint32_t>(ki, nullptr, ki, ko, vi, vi, vo, n, n_dev, bits, ws, s, counts_ready && bits <= 16);
+}
+void tile_sort_prepare(void* ws, cudaStream_t s) {
+    OSB_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * kMaxPasses * kBins, s));
 }
 bool radix_sort_depth24(const uint32_t* depth_bits, const uint32_t* range, uint32_t* ki, uint32_t* ko, uint32_t* vi,
                         uint32_t* vo, int n, void* ws, cudaStream_t s) {
@@ -575,7 +620,7 @@ EmitArrays scan_emit_arrays(void* ws, int n) {
 
 void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
                       uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws,
-                      uint32_t* cta_first, cudaStream_t s) {
+                      uint32_t* cta_first, void* tile_sort_ws, cudaStream_t s) {
     if (n <= 0) {
         OSB_CUDA_CHECK(cudaMemsetAsync(total, 0, sizeof(uint32_t), s));
         return;
@@ -592,9 +637,14 @@ void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4
     const long grid = keys ? emit_ctas(capacity) : 0;
     k_emit_prep<<<blocks, kScanThreads, 0, s>>>(order, rect, n, sums, rank_off, rank_gid, rank_rc, cta_first,
                                                 static_cast<int>(grid));
+    // the tile sort's workspace layout (radix_sort): hist[kMaxPasses][kBins] | .. | counts[kBins][blocks]
+    uint32_t* t_hist = static_cast<uint32_t*>(tile_sort_ws);
+    uint32_t* t_counts = t_hist ? t_hist + 2 * kMaxPasses * kBins : nullptr;
+    static_assert(kEmitTile == kSortThreads * SortCfg<uint32_t>::kItems, "emission CTA = tile-sort block");
     if (grid > 0)
         k_emit<<<static_cast<int>(grid), kScanThreads, 0, s>>>(rank_off, rank_gid, rank_rc, n, total, tiles_x, keys,
-                                                               vals, capacity, cta_first);
+                                                               vals, capacity, cta_first, t_counts, t_hist,
+                                                               static_cast<int>(grid));
     OSB_LAUNCHED(grid > 0 ? 4 : 3);
 }
 
