@@ -188,6 +188,15 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// Programmatic dependent launch (K2's chain of short kernels): a kernel launched with
+// launch_pdl waits for its predecessor's completion and memory (griddepcontrol.wait) before reading
+// anything the predecessor wrote, then lets its own successor be scheduled onto SMs as they free up
+// (griddepcontrol.launch_dependents) — the successor's launch and ramp overlap this kernel's tail.
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // std::remainder(x, w) (rasterizer.cpp:13 wrap_dx) for |x| < 1.5 w, where the quotient rounds to
 // -1, 0 or +1 (a tie at |x| = w/2 rounds to the even 0) and x -/+ w is exact (Sterbenz). Centres
 // lie in [0, W] and pixel centres in (0, W), so |x| < W always; anything else takes the libm path.

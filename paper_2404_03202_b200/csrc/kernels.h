@@ -200,4 +200,23 @@ struct CudaError : std::runtime_error {
         : std::runtime_error(std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
                              ") at " + file + ":" + std::to_string(line) + ": " + expr) {}
 };
+#ifndef OSB_PDL
+#define OSB_PDL 1
+#endif
+// Launch with programmatic stream serialization allowed (the kernel must start with pdl_begin()).
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = OSB_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    OSB_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 }  // namespace osb

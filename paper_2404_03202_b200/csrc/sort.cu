@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kSortThreads) k_upsweep(const K* __restrict__ 
                                                           int shift, int nblocks, uint32_t* __restrict__ counts,
                                                           int passes, uint32_t* __restrict__ hist,
                                                           const uint32_t* __restrict__ key24) {
+    pdl_begin();
     const int n = sort_count(n_cap, n_dev);
     const Key24 xf(key24);
     constexpr int kTile = tile_keys<K>();
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(kSortThreads) k_upsweep(const K* __restrict__ 
 __global__ void __launch_bounds__(kSortThreads) k_scan_counts(const uint32_t* __restrict__ counts, int nblocks,
                                                               const uint32_t* __restrict__ digit_totals,
                                                               uint32_t* __restrict__ offsets) {
+    pdl_begin();
     __shared__ uint32_t s_scan[kSortWarps + 1];
     __shared__ uint32_t s_base;
     const int d = blockIdx.x;
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict_
                                                             int n_cap, const uint32_t* n_dev, int shift, int nblocks,
                                                             const uint32_t* __restrict__ offsets,
                                                             const uint32_t* __restrict__ key24) {
+    pdl_begin();
     const int n = sort_count(n_cap, n_dev);
     const Key24 xf(key24);
     if (static_cast<long>(blockIdx.x) * kSortThreads * SortCfg<K>::kItems >= n) return;
@@ -286,6 +289,7 @@ __global__ void __launch_bounds__(kScanThreads) k_touch_sums(const uint32_t* __r
                                                              const uint32_t* __restrict__ order, int n,
                                                              uint32_t* __restrict__ block_sums,
                                                              uint32_t* __restrict__ ranked) {
+    pdl_begin();
     __shared__ uint32_t s_scan[kSortWarps + 1];
     const long r0 = static_cast<long>(blockIdx.x) * kScanTile + threadIdx.x;
     uint32_t local = 0;
@@ -306,6 +310,7 @@ __global__ void __launch_bounds__(kScanThreads) k_touch_sums(const uint32_t* __r
 // Single block: exclusive scan of the block sums in place; *total = M.
 __global__ void __launch_bounds__(1024) k_scan_block_sums(uint32_t* __restrict__ sums, int nblocks,
                                                           uint32_t* __restrict__ total) {
+    pdl_begin();
     __shared__ uint32_t s_part[32];
     __shared__ uint32_t s_carry;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -358,6 +363,7 @@ __global__ void __launch_bounds__(kScanThreads) k_emit_prep(const uint32_t* __re
                                                             uint32_t* __restrict__ rank_off,
                                                             uint32_t* __restrict__ rank_gid, int2* __restrict__ rank_rc,
                                                             uint32_t* __restrict__ cta_first, int nctas) {
+    pdl_begin();
     __shared__ uint32_t s_scan[kSortWarps + 1];
     const long r0 = static_cast<long>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
     uint32_t v[kScanItems], g[kScanItems];
@@ -416,6 +422,7 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
                                                        uint32_t capacity, const uint32_t* __restrict__ cta_first,
                                                        uint32_t* __restrict__ counts, uint32_t* __restrict__ hist,
                                                        int nblocks) {
+    pdl_begin();
     __shared__ uint32_t s_off[kEmitWindow];
     __shared__ __align__(16) uint32_t s_k[kEmitTile];
     __shared__ __align__(16) uint32_t s_v[kEmitTile];
@@ -513,6 +520,7 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
 // the key differs from its predecessor and ends where it differs from its successor.
 __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, int m_cap, const uint32_t* m_dev,
                                                 uint2* __restrict__ ranges) {
+    pdl_begin();
     const int m = sort_count(m_cap, m_dev);
     const int i0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
     if (i0 >= m) return;
@@ -561,12 +569,12 @@ bool radix_sort(const K* first_keys, const uint32_t* key24, K* keys_in, K* keys_
         const uint32_t* xf = p == 0 ? key24 : nullptr;
         const int shift = p * kRadixBits;
         if (!(p == 0 && counts_ready)) {
-            k_upsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, n, n_dev, shift, blocks, counts, passes,
-                                                         p == 0 ? hist : nullptr, xf);
+            launch_pdl(k_upsweep<K>, blocks, kSortThreads, s, ki, n, n_dev, shift, blocks, counts, passes,
+                       p == 0 ? hist : nullptr, xf);
             OSB_LAUNCHED(1);
         }
-        k_scan_counts<<<kBins, kSortThreads, 0, s>>>(counts, blocks, hist + p * kBins, offsets);
-        k_downsweep<K><<<blocks, kSortThreads, 0, s>>>(ki, vi, ko, vo, n, n_dev, shift, blocks, offsets, xf);
+        launch_pdl(k_scan_counts, kBins, kSortThreads, s, counts, blocks, hist + p * kBins, offsets);
+        launch_pdl(k_downsweep<K>, blocks, kSortThreads, s, ki, vi, ko, vo, n, n_dev, shift, blocks, offsets, xf);
         OSB_LAUNCHED(2);
         flipped = !flipped;
     }
@@ -631,26 +639,25 @@ void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4
     const size_t npad = (static_cast<size_t>(n) + 63) & ~size_t(63);  // keeps every array 256-B aligned
     uint32_t* rank_gid = rank_off + npad;
     int2* rank_rc = reinterpret_cast<int2*>(rank_gid + npad);
-    k_touch_sums<<<blocks, kScanThreads, 0, s>>>(touched, order, n, sums, rank_off);
-    k_scan_block_sums<<<1, 1024, 0, s>>>(sums, blocks, total);
+    launch_pdl(k_touch_sums, blocks, kScanThreads, s, touched, order, n, sums, rank_off);
+    launch_pdl(k_scan_block_sums, 1, 1024, s, sums, blocks, total);
     // one CTA per kEmitTile outputs up to the capacity (CTAs past M exit; M > capacity is retried)
     const long grid = keys ? emit_ctas(capacity) : 0;
-    k_emit_prep<<<blocks, kScanThreads, 0, s>>>(order, rect, n, sums, rank_off, rank_gid, rank_rc, cta_first,
-                                                static_cast<int>(grid));
+    launch_pdl(k_emit_prep, blocks, kScanThreads, s, order, rect, n, sums, rank_off, rank_gid, rank_rc, cta_first,
+               static_cast<int>(grid));
     // the tile sort's workspace layout (radix_sort): hist[kMaxPasses][kBins] | .. | counts[kBins][blocks]
     uint32_t* t_hist = static_cast<uint32_t*>(tile_sort_ws);
     uint32_t* t_counts = t_hist ? t_hist + 2 * kMaxPasses * kBins : nullptr;
     static_assert(kEmitTile == kSortThreads * SortCfg<uint32_t>::kItems, "emission CTA = tile-sort block");
     if (grid > 0)
-        k_emit<<<static_cast<int>(grid), kScanThreads, 0, s>>>(rank_off, rank_gid, rank_rc, n, total, tiles_x, keys,
-                                                               vals, capacity, cta_first, t_counts, t_hist,
-                                                               static_cast<int>(grid));
+        launch_pdl(k_emit, static_cast<int>(grid), kScanThreads, s, rank_off, rank_gid, rank_rc, n, total, tiles_x,
+                   keys, vals, capacity, cta_first, t_counts, t_hist, static_cast<int>(grid));
     OSB_LAUNCHED(grid > 0 ? 4 : 3);
 }
 
 void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s, const uint32_t* m_dev) {
     if (m <= 0) return;
-    k_ranges<<<(m + 1023) / 1024, 256, 0, s>>>(sorted_tiles, m, m_dev, ranges);
+    launch_pdl(k_ranges, (m + 1023) / 1024, 256, s, sorted_tiles, m, m_dev, ranges);
     OSB_LAUNCHED(1);
 }
 
@@ -667,6 +674,7 @@ constexpr int kMaxRun = 64;
 // redoes the depth rank with the full 64-bit sort.
 __global__ void k_fix_runs(const uint32_t* __restrict__ keys, uint32_t* __restrict__ order,
                            const uint64_t* __restrict__ depth_key, int n, uint32_t* __restrict__ flag) {
+    pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const uint32_t k = keys[i];
@@ -699,7 +707,7 @@ __global__ void k_fix_runs(const uint32_t* __restrict__ keys, uint32_t* __restri
 void launch_fix_runs(const uint32_t* keys, uint32_t* order, const uint64_t* depth_key, int n, uint32_t* flag,
                      cudaStream_t s) {
     if (n <= 1) return;
-    k_fix_runs<<<(n + 255) / 256, 256, 0, s>>>(keys, order, depth_key, n, flag);
+    launch_pdl(k_fix_runs, (n + 255) / 256, 256, s, keys, order, depth_key, n, flag);
     OSB_LAUNCHED(1);
 }
 
