@@ -14,6 +14,7 @@ namespace {
 
 __global__ void __launch_bounds__(256) k_adam(float4* __restrict__ p, float4* __restrict__ g, float4* __restrict__ m,
                                               float4* __restrict__ v, AdamArgs a) {
+    pdl_begin();
     const long n4 = (a.begin + a.count) / 4;
     const float b1 = 0.9f, b2 = 0.999f;
     const float ob1 = 1.0f - 0.9f, ob2 = 1.0f - 0.999f;
@@ -51,8 +52,8 @@ void launch_adam(float* params, float* grads, float* m, float* v, const AdamArgs
     if (n4 <= 0) return;
     long blocks = (n4 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    k_adam<<<static_cast<int>(blocks), 256, 0, s>>>(reinterpret_cast<float4*>(params), reinterpret_cast<float4*>(grads),
-                                                   reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), a);
+    launch_pdl(k_adam, static_cast<int>(blocks), 256, s, reinterpret_cast<float4*>(params),
+               reinterpret_cast<float4*>(grads), reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), a);
     OSB_LAUNCHED(1);
 }
 

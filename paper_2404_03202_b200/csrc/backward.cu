@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint3
                                                                      float bg2, FrameBuffers fb,
                                                                      const float* __restrict__ d_image,
                                                                      float4* __restrict__ acc) {
+    pdl_begin();
     // CTA-cooperative walk (as K3): 512 entries staged at once with 16-quarter reach masks, every
     // warp then walks the 16 sub-chunks back to front.
     constexpr int kPer = 2;                       // entries staged per thread per round
@@ -386,6 +387,7 @@ __global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __re
                                                             const Splat32* __restrict__ splat,
                                                             const float4* __restrict__ acc, float* __restrict__ G,
                                                             ScreenStats st) {
+    pdl_begin();
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= n) return;
     const Planes pl{bc};
@@ -798,11 +800,11 @@ void launch_backward_pixels(const uint32_t* inst_gid, const uint2* ranges, const
     const int tiles = tiles_x * tiles_y;
     if (tiles <= 0) return;
     if (bg[0] != 0.0f || bg[1] != 0.0f || bg[2] != 0.0f)
-        k_backward_pixels<true><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2],
-                                                               fb, d_image, acc);
+        launch_pdl(k_backward_pixels<true>, tiles, kTileThreads, s, inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1],
+                   bg[2], fb, d_image, acc);
     else
-        k_backward_pixels<false><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1],
-                                                                bg[2], fb, d_image, acc);
+        launch_pdl(k_backward_pixels<false>, tiles, kTileThreads, s, inst_gid, ranges, pp, W, H, tiles_x, bg[0],
+                   bg[1], bg[2], fb, d_image, acc);
     OSB_LAUNCHED(1);
 }
 
@@ -812,8 +814,8 @@ void launch_backward_gaussians(const float* params, int n, int stride, int bc, i
     if (n <= 0) return;
     const int blocks = (n + 127) / 128;
 #define OSB_K4B(D, O)                                                                                               \
-    k_backward_gaussians<D, O><<<blocks, 128, 0, s>>>(params, n, stride, bc, pose, W, H, pp.depth_key, pp.conic_o, \
-                                                      pp.splat, acc, grads, st)
+    launch_pdl(k_backward_gaussians<D, O>, blocks, 128, s, params, n, stride, bc, pose, W, H, pp.depth_key,       \
+               pp.conic_o, pp.splat, acc, grads, st)
     switch (active_degree * 2 + (overwrite ? 1 : 0)) {
         case 0: OSB_K4B(0, false); break;
         case 1: OSB_K4B(0, true); break;

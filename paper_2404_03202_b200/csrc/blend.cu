@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                                                            const uint2* __restrict__ ranges, PreprocessOut pp, int W,
                                                            int H, int tiles_x, float bg0, float bg1, float bg2,
                                                            FrameBuffers fb) {
+    pdl_begin();
     // CTA-cooperative walk: the 8 warps stage 512 entries at once (two per thread, each entry once
     // per tile instead of once per warp, with a 16-bit reach mask for all quarters), then every warp
     // blends the 16 sub-chunks in list order; one barrier pair per 512 entries (256: 0.56 ms,

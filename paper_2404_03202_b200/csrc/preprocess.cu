@@ -92,6 +92,7 @@ __device__ __forceinline__ void write_record(int gid, const double* p, const dou
 template <int DEG>
 __global__ void __launch_bounds__(256) k_preprocess(const float* __restrict__ P, int n, int stride, int bc, Pose pose,
                                                     int W, int H, PreprocessOut out) {
+    pdl_begin();
     constexpr int active_degree = DEG;  // compile-time: the SH loop unrolls into registers
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     if (gid >= n) return;
@@ -176,10 +177,10 @@ void launch_preprocess(const float* params, int n, int stride, int bc, int activ
     if (n <= 0) return;
     const int blocks = (n + 255) / 256;
     switch (active_degree) {
-        case 0: k_preprocess<0><<<blocks, 256, 0, s>>>(params, n, stride, bc, pose, W, H, out); break;
-        case 1: k_preprocess<1><<<blocks, 256, 0, s>>>(params, n, stride, bc, pose, W, H, out); break;
-        case 2: k_preprocess<2><<<blocks, 256, 0, s>>>(params, n, stride, bc, pose, W, H, out); break;
-        default: k_preprocess<3><<<blocks, 256, 0, s>>>(params, n, stride, bc, pose, W, H, out); break;
+        case 0: launch_pdl(k_preprocess<0>, blocks, 256, s, params, n, stride, bc, pose, W, H, out); break;
+        case 1: launch_pdl(k_preprocess<1>, blocks, 256, s, params, n, stride, bc, pose, W, H, out); break;
+        case 2: launch_pdl(k_preprocess<2>, blocks, 256, s, params, n, stride, bc, pose, W, H, out); break;
+        default: launch_pdl(k_preprocess<3>, blocks, 256, s, params, n, stride, bc, pose, W, H, out); break;
     }
     OSB_LAUNCHED(1);
 }
