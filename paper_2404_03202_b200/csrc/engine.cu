@@ -409,21 +409,23 @@ void Engine::render_into(Frame* f) {
     // K2a: depth rank = (t_r, id) order. Fast path: stable sort of the FP32-rounded t_r (monotone)
     // + exact FP64 re-ordering inside runs of equal keys; a run longer than 64 raises a flag
     // and validate() renders the frame again with the full 64-bit sort.
-    f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(n), 8));
+    // one workspace for both sorts, sized for both up front (the zeroed digit totals must survive)
+    f->sort_ws.ensure(std::max(radix_workspace_bytes(static_cast<int>(n), 8),
+                               radix_workspace_bytes(static_cast<int>(f->ikeys[0].capacity() / 4), 4)));
     uint32_t* long_run_flag = f->total.as<uint32_t>() + 1;
     const uint32_t* order;
     {
         Span sp(*this, kDepthSort);
-        OSB_CUDA_CHECK(cudaMemsetAsync(long_run_flag, 0, 4, stream_));
+        launch_k2_zero(f->sort_ws.as<void>(), long_run_flag, f->ranges.as<uint2>(), tiles, stream_);
         bool flipped;
         if (f->full_depth_sort) {
             flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(), f->ovals[0].as<uint32_t>(),
                                      f->ovals[1].as<uint32_t>(), N, 64, f->sort_ws.as<void>(), stream_, pp.depth_key,
-                                     true);
+                                     true, true);
         } else {
             uint32_t* k32[2] = {f->okeys[0].as<uint32_t>(), f->okeys[1].as<uint32_t>()};
             flipped = radix_sort_depth24(pp.depth_key32, pp.depth_range, k32[0], k32[1], f->ovals[0].as<uint32_t>(),
-                                         f->ovals[1].as<uint32_t>(), N, f->sort_ws.as<void>(), stream_);
+                                         f->ovals[1].as<uint32_t>(), N, f->sort_ws.as<void>(), stream_, true);
             launch_fix_runs(k32[flipped ? 1 : 0], f->ovals[flipped ? 1 : 0].as<uint32_t>(), pp.depth_key, N,
                             long_run_flag, stream_);
         }
@@ -445,10 +447,12 @@ void Engine::render_into(Frame* f) {
     // the emission also does the tile sort's first upsweep (tiles <= 2^16: two 8-bit passes)
     const int tile_bits = bits_for(static_cast<uint64_t>(tiles));
     const bool fused_counts = tile_bits <= 16;
+    const void* ws_zeroed = f->sort_ws.as<void>();
     f->sort_ws.ensure(radix_workspace_bytes(static_cast<int>(cap), 4));
     {
         Span sp(*this, kScan);
-        if (fused_counts) tile_sort_prepare(f->sort_ws.as<void>(), stream_);
+        // the first frame's instance buffer can grow the workspace: its tile slot is zeroed again
+        if (f->sort_ws.as<void>() != ws_zeroed) tile_sort_prepare(f->sort_ws.as<void>(), stream_);
         launch_scan_emit(pp.touched, order, pp.rect, N, f->tiles_x, f->ikeys[0].as<uint32_t>(),
                          f->ivals[0].as<uint32_t>(), cap, f->total.as<uint32_t>(), f->scan_ws.as<void>(),
                          f->emit_first.as<uint32_t>(), fused_counts ? f->sort_ws.as<void>() : nullptr, stream_);
@@ -463,11 +467,10 @@ void Engine::render_into(Frame* f) {
         f->inst_in_alt = radix_sort_u32(f->ikeys[0].as<uint32_t>(), f->ikeys[1].as<uint32_t>(),
                                         f->ivals[0].as<uint32_t>(), f->ivals[1].as<uint32_t>(), static_cast<int>(cap),
                                         tile_bits, f->sort_ws.as<void>(), stream_, f->total.as<uint32_t>(),
-                                        fused_counts);
+                                        fused_counts, true);
     }
     {
         Span sp(*this, kRanges);
-        OSB_CUDA_CHECK(cudaMemsetAsync(f->ranges.as<uint2>(), 0, static_cast<size_t>(tiles) * 8, stream_));
         launch_ranges(f->ikeys[f->inst_in_alt ? 1 : 0].as<uint32_t>(), static_cast<int>(cap), f->ranges.as<uint2>(),
                       stream_, f->total.as<uint32_t>());
     }

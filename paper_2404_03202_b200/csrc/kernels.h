@@ -45,19 +45,26 @@ size_t radix_workspace_bytes(int n_max, int key_bytes);
 // first_keys: the first pass reads its keys from there instead of keys_in (left untouched);
 // iota_vals: values are the element indices (vals_in is only a ping-pong buffer).
 bool radix_sort_u64(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
-                    int bits, void* ws, cudaStream_t s, const uint64_t* first_keys = nullptr, bool iota_vals = false);
+                    int bits, void* ws, cudaStream_t s, const uint64_t* first_keys = nullptr, bool iota_vals = false,
+                    bool hist_zeroed = false);
 // n_dev: optional device-side count (the sort covers min(n, *n_dev) elements; grids sized by n).
 // counts_ready (bits <= 16 only): the first pass's block counts and every pass's digit totals are
 // already in ws (launch_scan_emit with tile_sort_ws = ws after tile_sort_prepare(ws)).
+// tile_slot: the tile sort's digit totals live in the workspace's second slot, zeroed beforehand
+// (launch_k2_zero, or tile_sort_prepare after a workspace reallocation).
 bool radix_sort_u32(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
-                    int bits, void* ws, cudaStream_t s, const uint32_t* n_dev = nullptr, bool counts_ready = false);
+                    int bits, void* ws, cudaStream_t s, const uint32_t* n_dev = nullptr, bool counts_ready = false,
+                    bool tile_slot = false);
 void tile_sort_prepare(void* ws, cudaStream_t s);
+// Zero both digit-total slots of a sort workspace, the long-run flag and the tile ranges (one
+// chained launch at the start of K2; hist_zeroed / tile_slot sorts then skip their own memsets).
+void launch_k2_zero(void* sort_ws, uint32_t* long_run_flag, uint2* ranges, int tiles, cudaStream_t s);
 // The fast depth rank: stable 3-pass sort of Gaussian ids 0..n-1 (no value input) by the 24-bit key
 // (bits[i] - min) >> shift, the smallest shift that fits the visible range below 0xFFFFFF (culled ->
 // 0xFFFFFF), computed on the fly by the first pass from K1's FP32 depth bits and their {min, ~max}
 // range; the keys end up in ki/ko like radix_sort_u32.
 bool radix_sort_depth24(const uint32_t* depth_bits, const uint32_t* range, uint32_t* ki, uint32_t* ko, uint32_t* vi,
-                        uint32_t* vo, int n, void* ws, cudaStream_t s);
+                        uint32_t* vo, int n, void* ws, cudaStream_t s, bool hist_zeroed = false);
 // After a stable sort by the FP32-rounded depth: restore the exact (FP64 depth, id) order inside
 // runs of equal keys; a run longer than 32 sets *flag (caller falls back to the 64-bit sort).
 void launch_fix_runs(const uint32_t* keys, uint32_t* order, const uint64_t* depth_key, int n, uint32_t* flag,

@@ -549,17 +549,20 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ key
 template <typename K>
 bool radix_sort(const K* first_keys, const uint32_t* key24, K* keys_in, K* keys_out, const uint32_t* first_vals,
                 uint32_t* vals_in, uint32_t* vals_out, int n, const uint32_t* n_dev, int bits, void* ws,
-                cudaStream_t s, bool counts_ready = false) {
+                cudaStream_t s, bool counts_ready = false, int hist_slot = 0, bool hist_zeroed = false) {
     if (n <= 1) {
         if (n == 1 && !first_vals) OSB_CUDA_CHECK(cudaMemsetAsync(vals_in, 0, sizeof(uint32_t), s));  // id 0
         return false;
     }
     const int passes = (bits + kRadixBits - 1) / kRadixBits;
     const int blocks = (n + tile_keys<K>() - 1) / tile_keys<K>();
-    uint32_t* hist = static_cast<uint32_t*>(ws);
-    uint32_t* counts = hist + 2 * kMaxPasses * kBins;
+    // workspace: two digit-total slots hist[2][kMaxPasses][kBins] (depth rank: 0, tile sort: 1, so
+    // k_k2_zero can clear both before either runs) | counts[kBins][blocks] | offsets[kBins][blocks]
+    uint32_t* hist = static_cast<uint32_t*>(ws) + hist_slot * kMaxPasses * kBins;
+    uint32_t* counts = static_cast<uint32_t*>(ws) + 2 * kMaxPasses * kBins;
     uint32_t* offsets = counts + static_cast<size_t>(kBins) * blocks;
-    if (!counts_ready) OSB_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kBins, s));
+    if (!counts_ready && !hist_zeroed)
+        OSB_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kMaxPasses * kBins, s));
     bool flipped = false;
     for (int p = 0; p < passes; ++p) {
         const K* ki = p == 0 ? first_keys : (flipped ? keys_out : keys_in);
@@ -591,20 +594,42 @@ size_t radix_workspace_bytes(int n_max, int key_bytes) {
 }
 
 bool radix_sort_u64(uint64_t* ki, uint64_t* ko, uint32_t* vi, uint32_t* vo, int n, int bits, void* ws,
-                    cudaStream_t s, const uint64_t* first_keys, bool iota_vals) {
+                    cudaStream_t s, const uint64_t* first_keys, bool iota_vals, bool hist_zeroed) {
     return radix_sort<uint64_t>(first_keys ? first_keys : ki, nullptr, ki, ko, iota_vals ? nullptr : vi, vi, vo, n,
-                                nullptr, bits, ws, s);
+                                nullptr, bits, ws, s, false, 0, hist_zeroed);
 }
 bool radix_sort_u32(uint32_t* ki, uint32_t* ko, uint32_t* vi, uint32_t* vo, int n, int bits, void* ws,
-                    cudaStream_t s, const uint32_t* n_dev, bool counts_ready) {
-    return radix_sort<uint32_t>(ki, nullptr, ki, ko, vi, vi, vo, n, n_dev, bits, ws, s, counts_ready && bits <= 16);
+                    cudaStream_t s, const uint32_t* n_dev, bool counts_ready, bool tile_slot) {
+    return radix_sort<uint32_t>(ki, nullptr, ki, ko, vi, vi, vo, n, n_dev, bits, ws, s, counts_ready && bits <= 16,
+                                tile_slot ? 1 : 0, tile_slot);
 }
 void tile_sort_prepare(void* ws, cudaStream_t s) {
-    OSB_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * kMaxPasses * kBins, s));
+    OSB_CUDA_CHECK(cudaMemsetAsync(static_cast<uint32_t*>(ws) + kMaxPasses * kBins, 0,
+                                   sizeof(uint32_t) * kMaxPasses * kBins, s));
 }
 bool radix_sort_depth24(const uint32_t* depth_bits, const uint32_t* range, uint32_t* ki, uint32_t* ko, uint32_t* vi,
-                        uint32_t* vo, int n, void* ws, cudaStream_t s) {
-    return radix_sort<uint32_t>(depth_bits, range, ki, ko, nullptr, vi, vo, n, nullptr, 24, ws, s);
+                        uint32_t* vo, int n, void* ws, cudaStream_t s, bool hist_zeroed) {
+    return radix_sort<uint32_t>(depth_bits, range, ki, ko, nullptr, vi, vo, n, nullptr, 24, ws, s, false, 0,
+                                hist_zeroed);
+}
+
+namespace {
+// The frame's K2 scratch that must start at zero, in one chained kernel instead of separate memsets:
+// both digit-total slots of the sort workspace, the long-run flag and the tile ranges.
+__global__ void k_k2_zero(uint32_t* __restrict__ hist, int nhist, uint32_t* __restrict__ flag,
+                          uint2* __restrict__ ranges, int tiles) {
+    pdl_begin();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x, step = gridDim.x * blockDim.x;
+    for (int k = i; k < nhist; k += step) hist[k] = 0u;
+    for (int k = i; k < tiles; k += step) ranges[k] = make_uint2(0u, 0u);
+    if (i == 0) *flag = 0u;
+}
+}  // namespace
+
+void launch_k2_zero(void* sort_ws, uint32_t* long_run_flag, uint2* ranges, int tiles, cudaStream_t s) {
+    launch_pdl(k_k2_zero, 64, 256, s, static_cast<uint32_t*>(sort_ws), 2 * kMaxPasses * kBins, long_run_flag, ranges,
+               tiles);
+    OSB_LAUNCHED(1);
 }
 
 long emit_ctas(uint32_t capacity) { return (static_cast<long>(capacity) + kEmitTile - 1) / kEmitTile; }
@@ -646,8 +671,8 @@ void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4
     launch_pdl(k_emit_prep, blocks, kScanThreads, s, order, rect, n, sums, rank_off, rank_gid, rank_rc, cta_first,
                static_cast<int>(grid));
     // the tile sort's workspace layout (radix_sort): hist[kMaxPasses][kBins] | .. | counts[kBins][blocks]
-    uint32_t* t_hist = static_cast<uint32_t*>(tile_sort_ws);
-    uint32_t* t_counts = t_hist ? t_hist + 2 * kMaxPasses * kBins : nullptr;
+    uint32_t* t_hist = tile_sort_ws ? static_cast<uint32_t*>(tile_sort_ws) + kMaxPasses * kBins : nullptr;  // slot 1
+    uint32_t* t_counts = tile_sort_ws ? static_cast<uint32_t*>(tile_sort_ws) + 2 * kMaxPasses * kBins : nullptr;
     static_assert(kEmitTile == kSortThreads * SortCfg<uint32_t>::kItems, "emission CTA = tile-sort block");
     if (grid > 0)
         launch_pdl(k_emit, static_cast<int>(grid), kScanThreads, s, rank_off, rank_gid, rank_rc, n, total, tiles_x,
