@@ -631,11 +631,16 @@ def run_ours(args):
     # algorithmic bytes per launch; K3/K4a: pairs x the kernel's measured warp
     # instructions per pair (ncu, profiles/ncu_kernels.json) -> issue-slot utilisation
     hbm = {
-        "preprocess": N * (44 + 12 * 16) + N * 44,
+        # K1: the 59 parameter planes (236 B) in, the frame's per-Gaussian records out — depth keys 12,
+        # touched 4, rectangle 16, FP64 centre 16 + conic/opacity 32, FP32 blend record 48, radius 4 =
+        # 132 B per visible Gaussian (upper bound: every Gaussian counted as visible)
+        "preprocess": N * (236 + 132),
         "depth_sort": N * 12 * 2 * 8,
         "tile_sort": instances * 32,
         "loss": plane * 36,
-        "bwd_gauss": N * 520,
+        # K4b per visible Gaussian: parameters 236 + K4a accumulators 48 + K1 records (conic 32, blend
+        # record 48, depth key 8) in; gradient planes 236 + screen statistics 20 out (upper bound)
+        "bwd_gauss": N * (236 + 48 + 88 + 236 + 20),
         "adam": 28 * planes / world,  # p, g, m, v in, p, m, v out (N > 1: this rank's 1/N shard)
     }
     pairs = {"blend": fwd_pairs, "bwd_pixels": bwd_pairs}
