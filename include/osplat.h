@@ -246,8 +246,9 @@ OSPLAT_API void osplat_report_free(osplat_report* report);
 
 /* ---- §8(e) multi-view data parallelism inside the library: one process (context) per GPU, one
  * NCCL communicator per context, every collective issued by the library on the context stream.
- * NCCL is loaded at run time (libnccl.so.2; the one already mapped by the process if any);
- * without it these calls return OSPLAT_ERR_UNSUPPORTED.
+ * NCCL is loaded at run time (libnccl.so.2; the one already mapped by the process if any; the
+ * environment variable OSPLAT_NCCL_LIB names another library); without it these calls return
+ * OSPLAT_ERR_UNSUPPORTED.
  * osplat_nccl_unique_id: ncclGetUniqueId on one rank; the launcher hands the 128 bytes to every
  * rank (any channel: torch.distributed, MPI, a file). osplat_gpu_dp_init: ncclCommInitRank
  * (collective over the world). osplat_gpu_dp_step: the batch's exchange + optimizer step after

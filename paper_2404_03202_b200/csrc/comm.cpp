@@ -19,6 +19,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -56,10 +57,14 @@ NcclApi& api() {
     static NcclApi a;
     static std::once_flag once;
     std::call_once(once, [] {
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        // OSPLAT_NCCL_LIB: an explicit NCCL build (or the tests' in-process stand-in) instead of the
+        // libnccl.so.2 the process resolves
+        const char* path = std::getenv("OSPLAT_NCCL_LIB");
+        if (!path || !*path) path = "libnccl.so.2";
+        void* h = dlopen(path, RTLD_NOW | RTLD_GLOBAL);
         if (!h) {
             const char* e = dlerror();
-            a.error = std::string("cannot load libnccl.so.2: ") + (e ? e : "?");
+            a.error = std::string("cannot load ") + path + ": " + (e ? e : "?");
             return;
         }
         sym(h, "ncclGetUniqueId", a.getUniqueId, a.error);
