@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
                     last = kofs + j;
                 }
             };
-if (seam) lanes(std::true_type{});
+            if (seam) lanes(std::true_type{});
             else lanes(std::false_type{});
             uint32_t pm = __ballot_sync(0xffffffffu, pend);
             if (pm == 0u) break;
