@@ -18,7 +18,7 @@ namespace {
 
 template <bool STRICT>
 __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __restrict__ inst_gid,
-                                                           const uint2* __restrict__ ranges, PreprocessOut pp, int W,
+                                                           uint2* __restrict__ ranges, PreprocessOut pp, int W,
                                                            int H, int tiles_x, float bg0, float bg1, float bg2,
                                                            FrameBuffers fb) {
     pdl_begin();
@@ -38,7 +38,11 @@ __global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __res
     const int lx = wp.lx, ly = wp.ly;
     const int px = tx * kTile + lx, py = ty * kTile + ly;
     const bool inside = px < W && py < H;
-    const uint2 range = ranges[tile];
+    uint2 range = ranges[tile];
+    if (range.x > range.y) {  // an empty tile of the fused tile sort ({~0u, 0}): stored back as {0, 0}
+        range = make_uint2(0u, 0u);
+        if (threadIdx.x == 0) ranges[tile] = range;
+    }
     const double width = W;
     const double xc = tx * kTile + 8.0, yc = ty * kTile + 8.0;
     float lxo = lx - 7.5f, lyo = ly - 7.5f;
@@ -279,7 +283,7 @@ void launch_work_count(const FrameBuffers& fb, int pixels, unsigned long long* o
     OSB_LAUNCHED(1);
 }
 
-void launch_blend(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H, int tiles_x,
+void launch_blend(const uint32_t* inst_gid, uint2* ranges, const PreprocessOut& pp, int W, int H, int tiles_x,
                   int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s, bool strict) {
     const int tiles = tiles_x * tiles_y;
     if (tiles <= 0) return;

@@ -414,9 +414,11 @@ void Engine::render_into(Frame* f) {
                                radix_workspace_bytes(static_cast<int>(f->ikeys[0].capacity() / 4), 4)));
     uint32_t* long_run_flag = f->total.as<uint32_t>() + 1;
     const uint32_t* order;
+    const uint32_t* keys24 = nullptr;  // fast path: the sorted 24-bit keys (runs fixed in the emission)
     {
         Span sp(*this, kDepthSort);
-        launch_k2_zero(f->sort_ws.as<void>(), long_run_flag, f->ranges.as<uint2>(), tiles, stream_);
+        launch_k2_zero(f->sort_ws.as<void>(), long_run_flag, f->ranges.as<uint2>(), tiles, f->scan_ws.as<void>(),
+                       static_cast<int>(N), stream_);
         bool flipped;
         if (f->full_depth_sort) {
             flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(), f->ovals[0].as<uint32_t>(),
@@ -426,8 +428,7 @@ void Engine::render_into(Frame* f) {
             uint32_t* k32[2] = {f->okeys[0].as<uint32_t>(), f->okeys[1].as<uint32_t>()};
             flipped = radix_sort_depth24(pp.depth_key32, pp.depth_range, k32[0], k32[1], f->ovals[0].as<uint32_t>(),
                                          f->ovals[1].as<uint32_t>(), N, f->sort_ws.as<void>(), stream_, true);
-            launch_fix_runs(k32[flipped ? 1 : 0], f->ovals[flipped ? 1 : 0].as<uint32_t>(), pp.depth_key, N,
-                            long_run_flag, stream_);
+            keys24 = k32[flipped ? 1 : 0];
         }
         order = f->ovals[flipped ? 1 : 0].as<uint32_t>();
     }
@@ -435,9 +436,10 @@ void Engine::render_into(Frame* f) {
     // instance buffer yet sizes it first (one synchronous counting pass).
     if (f->ikeys[0].capacity() == 0) {
         launch_scan_emit(pp.touched, order, pp.rect, N, f->tiles_x, nullptr, nullptr, 0, f->total.as<uint32_t>(),
-                         f->scan_ws.as<void>(), nullptr, nullptr, stream_);
+                         f->scan_ws.as<void>(), nullptr, nullptr, stream_, keys24, pp.depth_key, long_run_flag);
         uint32_t host = 0;
         OSB_CUDA_CHECK(cudaMemcpyAsync(&host, f->total.as<uint32_t>(), 4, cudaMemcpyDeviceToHost, stream_));
+        scan_sums_reset(f->scan_ws.as<void>(), static_cast<int>(N), stream_);  // the emission below adds again
         OSB_CUDA_CHECK(cudaStreamSynchronize(stream_));
         grow_instances(f, host);
     }
@@ -455,24 +457,21 @@ void Engine::render_into(Frame* f) {
         if (f->sort_ws.as<void>() != ws_zeroed) tile_sort_prepare(f->sort_ws.as<void>(), stream_);
         launch_scan_emit(pp.touched, order, pp.rect, N, f->tiles_x, f->ikeys[0].as<uint32_t>(),
                          f->ivals[0].as<uint32_t>(), cap, f->total.as<uint32_t>(), f->scan_ws.as<void>(),
-                         f->emit_first.as<uint32_t>(), fused_counts ? f->sort_ws.as<void>() : nullptr, stream_);
+                         f->emit_first.as<uint32_t>(), fused_counts ? f->sort_ws.as<void>() : nullptr, stream_, keys24,
+                         pp.depth_key, long_run_flag);
     }
     // {M, long-run flag} are final here: read them back now so validate() only waits for this
     // point of the frame, not for the blend
     OSB_CUDA_CHECK(cudaMemcpyAsync(f->info_host, f->total.as<uint32_t>(), 8, cudaMemcpyDeviceToHost, stream_));
     OSB_CUDA_CHECK(cudaEventRecord(f->ready, stream_));
-    // K2c: stable sort by tile over min(M, cap) instances (count read on the device), tile ranges
+    // K2c: stable sort by tile over min(M, cap) instances (count read on the device); its last pass
+    // writes the tile ranges instead of the sorted keys
     {
         Span sp(*this, kTileSort);
         f->inst_in_alt = radix_sort_u32(f->ikeys[0].as<uint32_t>(), f->ikeys[1].as<uint32_t>(),
                                         f->ivals[0].as<uint32_t>(), f->ivals[1].as<uint32_t>(), static_cast<int>(cap),
                                         tile_bits, f->sort_ws.as<void>(), stream_, f->total.as<uint32_t>(),
-                                        fused_counts, true);
-    }
-    {
-        Span sp(*this, kRanges);
-        launch_ranges(f->ikeys[f->inst_in_alt ? 1 : 0].as<uint32_t>(), static_cast<int>(cap), f->ranges.as<uint2>(),
-                      stream_, f->total.as<uint32_t>());
+                                        fused_counts, true, f->ranges.as<uint2>());  // + the tile ranges
     }
     // K3
     {

@@ -52,23 +52,24 @@ bool radix_sort_u64(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, ui
 // already in ws (launch_scan_emit with tile_sort_ws = ws after tile_sort_prepare(ws)).
 // tile_slot: the tile sort's digit totals live in the workspace's second slot, zeroed beforehand
 // (launch_k2_zero, or tile_sort_prepare after a workspace reallocation).
+// ranges (tile sort): the last pass writes the tile ranges instead of the sorted keys (ranges must
+// start at {~0u, 0}: launch_k2_zero; empty tiles keep that and read as empty — K3 stores them back as
+// {0, 0}); keys_in / keys_out then hold no sorted result.
 bool radix_sort_u32(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
                     int bits, void* ws, cudaStream_t s, const uint32_t* n_dev = nullptr, bool counts_ready = false,
-                    bool tile_slot = false);
+                    bool tile_slot = false, uint2* ranges = nullptr);
 void tile_sort_prepare(void* ws, cudaStream_t s);
 // Zero both digit-total slots of a sort workspace, the long-run flag and the tile ranges (one
 // chained launch at the start of K2; hist_zeroed / tile_slot sorts then skip their own memsets).
-void launch_k2_zero(void* sort_ws, uint32_t* long_run_flag, uint2* ranges, int tiles, cudaStream_t s);
+// (+ the emission's block sums at the head of scan_ws, sized for n Gaussians)
+void launch_k2_zero(void* sort_ws, uint32_t* long_run_flag, uint2* ranges, int tiles, void* scan_ws, int n,
+                    cudaStream_t s);
 // The fast depth rank: stable 3-pass sort of Gaussian ids 0..n-1 (no value input) by the 24-bit key
 // (bits[i] - min) >> shift, the smallest shift that fits the visible range below 0xFFFFFF (culled ->
 // 0xFFFFFF), computed on the fly by the first pass from K1's FP32 depth bits and their {min, ~max}
 // range; the keys end up in ki/ko like radix_sort_u32.
 bool radix_sort_depth24(const uint32_t* depth_bits, const uint32_t* range, uint32_t* ki, uint32_t* ko, uint32_t* vi,
                         uint32_t* vo, int n, void* ws, cudaStream_t s, bool hist_zeroed = false);
-// After a stable sort by the FP32-rounded depth: restore the exact (FP64 depth, id) order inside
-// runs of equal keys; a run longer than 32 sets *flag (caller falls back to the 64-bit sort).
-void launch_fix_runs(const uint32_t* keys, uint32_t* order, const uint64_t* depth_key, int n, uint32_t* flag,
-                     cudaStream_t s);
 // Exclusive scan of touched[order[r]] fused with the emission of (tile, gid) instances in depth
 // order; writes only instances below `capacity`; *total = M (device).
 size_t scan_workspace_bytes(int n);
@@ -86,11 +87,15 @@ EmitArrays scan_emit_arrays(void* ws, int n);
 long emit_ctas(uint32_t capacity);
 // tile_sort_ws (optional): the emission also writes the tile sort's first upsweep into that
 // radix_sort_u32 workspace (zeroed digit totals first: tile_sort_prepare), sized for `capacity`.
+// depth_keys24 (fast depth rank): its sorted 24-bit keys — runs of equal keys are put in exact
+// (FP64 depth_key, id) order on the way (a run longer than 64 raises *long_run_flag: redo the depth
+// rank with the full 64-bit sort). The block sums in ws start at zero (launch_k2_zero; after a
+// counting pass: scan_sums_reset).
 void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
                       uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws,
-                      uint32_t* cta_first, void* tile_sort_ws, cudaStream_t s);
-void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s,
-                   const uint32_t* m_dev = nullptr);
+                      uint32_t* cta_first, void* tile_sort_ws, cudaStream_t s, const uint32_t* depth_keys24 = nullptr,
+                      const uint64_t* depth_key = nullptr, uint32_t* long_run_flag = nullptr);
+void scan_sums_reset(void* ws, int n, cudaStream_t s);
 
 // ---- K3 blend (blend.cu) --------------------------------------------------------------------
 struct FrameBuffers {
@@ -106,7 +111,8 @@ void launch_work_count(const FrameBuffers& fb, int pixels, unsigned long long* o
 void launch_planar_to_hwc_f64(const float* rgb, size_t plane, double* out, cudaStream_t s);
 // strict: the T-stop guard band is the rigorous running error bound instead of the 2^-10 band
 // (common.cuh); slower (more FP64 replays), decisions provably the FP64 reference's.
-void launch_blend(const uint32_t* inst_gid, const uint2* ranges, const PreprocessOut& pp, int W, int H,
+// ranges: read, and empty tiles left as {~0u, 0} by the fused tile sort are stored back as {0, 0}
+void launch_blend(const uint32_t* inst_gid, uint2* ranges, const PreprocessOut& pp, int W, int H,
                   int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s,
                   bool strict = false);
 

@@ -21,6 +21,8 @@
 
 namespace osb {
 
+int scan_block_count(int n);
+
 namespace {
 
 constexpr int kRadixBits = 8;
@@ -182,11 +184,14 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict_
                                                             K* __restrict__ keys_out, uint32_t* __restrict__ vals_out,
                                                             int n_cap, const uint32_t* n_dev, int shift, int nblocks,
                                                             const uint32_t* __restrict__ offsets,
-                                                            const uint32_t* __restrict__ key24) {
+                                                            const uint32_t* __restrict__ key24,
+                                                            uint2* __restrict__ ranges) {
     pdl_begin();
     const int n = sort_count(n_cap, n_dev);
     const Key24 xf(key24);
     if (static_cast<long>(blockIdx.x) * kSortThreads * SortCfg<K>::kItems >= n) return;
+    // this thread's digit offset (thread = digit), loaded with the keys instead of after the ranking
+    const uint32_t my_off = offsets[static_cast<size_t>(threadIdx.x) * nblocks + blockIdx.x];
     constexpr int kItems = SortCfg<K>::kItems;
     constexpr int kTile = kSortThreads * kItems;
     __shared__ uint32_t s_warp[kSortWarps][kBins];
@@ -253,7 +258,7 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict_
     uint32_t total;
     const uint32_t local = block_exclusive_scan(cnt, s_scan, &total);
     s_local[d] = local;
-    s_global[d] = static_cast<int>(offsets[static_cast<size_t>(d) * nblocks + bid]) - static_cast<int>(local);
+    s_global[d] = static_cast<int>(my_off) - static_cast<int>(local);
     __syncthreads();
 
     // Block-local sort into shared memory.
@@ -269,12 +274,33 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict_
     }
     __syncthreads();
     // Coalesced scatter: consecutive local positions of one digit are consecutive globally.
+    if (!ranges) {
+        for (int i = tid; i < count; i += kSortThreads) {
+            const K k = s_keys[i];
+            const uint32_t dd = static_cast<uint32_t>((k >> shift) & (kBins - 1));
+            const int dst = s_global[dd] + i;
+            keys_out[dst] = k;
+            vals_out[dst] = s_vals[i];
+        }
+        return;
+    }
+    // Last pass of the tile sort: the sorted keys are only needed for the tile ranges, so they are
+    // not stored; the ranges come from here. Inside this block's run of one digit the keys are in
+    // final (tile) order and consecutive globally, so a tile boundary between two neighbours of the
+    // run is a plain store; at the run's two ends the global neighbour belongs to another block, so
+    // the start / end are combined with atomicMin / atomicMax (ranges start at {~0u, 0}: k_k2_zero;
+    // the one plain store of a boundary is the extremum, so the order against the atomics is free).
     for (int i = tid; i < count; i += kSortThreads) {
-        const K k = s_keys[i];
-        const uint32_t dd = static_cast<uint32_t>((k >> shift) & (kBins - 1));
+        const uint32_t k = static_cast<uint32_t>(s_keys[i]);
+        const uint32_t dd = (k >> shift) & (kBins - 1);
+        const int lo = static_cast<int>(s_local[dd]);
+        const int hi = dd + 1 < kBins ? static_cast<int>(s_local[dd + 1]) : count;  // run of digit dd: [lo, hi)
         const int dst = s_global[dd] + i;
-        keys_out[dst] = k;
         vals_out[dst] = s_vals[i];
+        if (i == lo) atomicMin(&ranges[k].x, static_cast<uint32_t>(dst));
+        else if (static_cast<uint32_t>(s_keys[i - 1]) != k) ranges[k].x = static_cast<uint32_t>(dst);
+        if (i == hi - 1) atomicMax(&ranges[k].y, static_cast<uint32_t>(dst + 1));
+        else if (static_cast<uint32_t>(s_keys[i + 1]) != k) ranges[k].y = static_cast<uint32_t>(dst + 1);
     }
 }
 
@@ -283,12 +309,45 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;  // ranks per block
 
-// Sum of touched over each block's ranks.
-// Also leaves touched[order[r]] at ranked[r] (coalesced), so k_emit_prep does not gather it again.
+constexpr int kMaxRun = 64;
+
+// Exact (FP64 depth, id) order inside a run of equal FP32-rounded depth keys around rank r (the
+// stable FP32 sort left the run in ascending id order): the rank this element takes inside the run,
+// or -1 when the run is longer than kMaxRun (*flag raised: the caller redoes the depth rank with
+// the full 64-bit sort). O(run length) per member, every member places itself.
+__device__ __noinline__ int run_position(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ order,
+                                         const uint64_t* __restrict__ depth_key, int n, int r, uint32_t k,
+                                         uint32_t g, uint32_t* flag) {
+    int s = r, e = r + 1;
+    while (s > 0 && keys[s - 1] == k && r - s < kMaxRun) --s;
+    while (e < n && keys[e] == k && e - r <= kMaxRun) ++e;
+    if (e - s > kMaxRun) {
+        atomicExch(flag, 1u);
+        return -1;
+    }
+    const uint64_t d = depth_key[g];
+    int below = 0;
+    for (int a = s; a < e; ++a) {
+        const uint32_t h = order[a];
+        const uint64_t dh = depth_key[h];
+        below += (dh < d || (dh == d && h < g)) ? 1 : 0;
+    }
+    return s + below;
+}
+
+// Per depth rank r: the Gaussian that takes rank r (rank_gid) and its touched count (rank_off, read
+// by k_emit_prep), and the per-block sums of touched (atomics into sums zeroed by k_k2_zero).
+// keys (fast depth rank): the sorted 24-bit keys; every element of a run of equal keys places itself
+// at its exact (FP64 depth, id) position inside the run (replaces a separate run-fixing pass; a run
+// may straddle two blocks, so its elements add to the sum of the block they land in).
 __global__ void __launch_bounds__(kScanThreads) k_touch_sums(const uint32_t* __restrict__ touched,
                                                              const uint32_t* __restrict__ order, int n,
                                                              uint32_t* __restrict__ block_sums,
-                                                             uint32_t* __restrict__ ranked) {
+                                                             uint32_t* __restrict__ ranked,
+                                                             uint32_t* __restrict__ rank_gid,
+                                                             const uint32_t* __restrict__ keys,
+                                                             const uint64_t* __restrict__ depth_key,
+                                                             uint32_t* __restrict__ flag) {
     pdl_begin();
     __shared__ uint32_t s_scan[kSortWarps + 1];
     const long r0 = static_cast<long>(blockIdx.x) * kScanTile + threadIdx.x;
@@ -297,54 +356,25 @@ __global__ void __launch_bounds__(kScanThreads) k_touch_sums(const uint32_t* __r
     for (int i = 0; i < kScanItems; ++i) {
         const long r = r0 + i * kScanThreads;
         if (r < n) {
-            const uint32_t v = touched[order[r]];
-            ranked[r] = v;
-            local += v;
+            const uint32_t g = order[r];
+            long dst = r;
+            if (keys) {
+                const uint32_t k = keys[r];
+                if (k != 0xFFFFFFu && ((r > 0 && keys[r - 1] == k) || (r + 1 < n && keys[r + 1] == k))) {
+                    const int p = run_position(keys, order, depth_key, n, static_cast<int>(r), k, g, flag);
+                    if (p >= 0) dst = p;
+                }
+            }
+            const uint32_t v = touched[g];
+            ranked[dst] = v;
+            rank_gid[dst] = g;
+            if (dst / kScanTile == blockIdx.x) local += v;
+            else if (v) atomicAdd(&block_sums[dst / kScanTile], v);
         }
     }
     uint32_t total;
     block_exclusive_scan(local, s_scan, &total);
-    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
-}
-
-// Single block: exclusive scan of the block sums in place; *total = M.
-__global__ void __launch_bounds__(1024) k_scan_block_sums(uint32_t* __restrict__ sums, int nblocks,
-                                                          uint32_t* __restrict__ total) {
-    pdl_begin();
-    __shared__ uint32_t s_part[32];
-    __shared__ uint32_t s_carry;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    for (int b0 = 0; b0 < nblocks; b0 += 1024) {
-        const int b = b0 + threadIdx.x;
-        const uint32_t v = b < nblocks ? sums[b] : 0u;
-        uint32_t inc = v;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t t = __shfl_up_sync(0xffffffffu, inc, off);
-            if (lane >= off) inc += t;
-        }
-        if (lane == 31) s_part[warp] = inc;
-        __syncthreads();
-        if (warp == 0) {
-            const uint32_t w = s_part[lane];
-            uint32_t wi = w;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const uint32_t t = __shfl_up_sync(0xffffffffu, wi, off);
-                if (lane >= off) wi += t;
-            }
-            s_part[lane] = wi - w;
-        }
-        __syncthreads();
-        const uint32_t carry = s_carry;
-        if (b < nblocks) sums[b] = carry + s_part[warp] + inc - v;
-        __syncthreads();
-        if (threadIdx.x == 1023) s_carry = carry + s_part[warp] + inc;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *total = s_carry;
+    if (threadIdx.x == 0 && total) atomicAdd(&block_sums[blockIdx.x], total);
 }
 
 // Instance emission in depth order, balanced over OUTPUTS (the instance counts per rank are very
@@ -356,12 +386,14 @@ __global__ void __launch_bounds__(1024) k_scan_block_sums(uint32_t* __restrict__
 constexpr int kEmitTile = kScanThreads * 8;
 constexpr int kEmitWindow = 2 * kEmitTile;  // ranks staged per CTA (more only with many empty ranks)
 
-// rank_off[r] holds touched[order[r]] on entry (k_touch_sums) and the rank's first output on exit.
-__global__ void __launch_bounds__(kScanThreads) k_emit_prep(const uint32_t* __restrict__ order,
-                                                            const int4* __restrict__ rect, int n,
-                                                            const uint32_t* __restrict__ block_offsets,
+// rank_off[r] holds the touched count of rank r on entry (k_touch_sums) and the rank's first output
+// on exit. Each block derives its own exclusive prefix from the raw block sums (at most a few
+// thousand words: cheaper than a separate scan launch); the last block stores M = *total.
+__global__ void __launch_bounds__(kScanThreads) k_emit_prep(const int4* __restrict__ rect, int n,
+                                                            const uint32_t* __restrict__ block_sums,
                                                             uint32_t* __restrict__ rank_off,
-                                                            uint32_t* __restrict__ rank_gid, int2* __restrict__ rank_rc,
+                                                            const uint32_t* __restrict__ rank_gid,
+                                                            int2* __restrict__ rank_rc, uint32_t* __restrict__ total,
                                                             uint32_t* __restrict__ cta_first, int nctas) {
     pdl_begin();
     __shared__ uint32_t s_scan[kSortWarps + 1];
@@ -371,12 +403,17 @@ __global__ void __launch_bounds__(kScanThreads) k_emit_prep(const uint32_t* __re
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
         const long r = r0 + i;
-        g[i] = r < n ? order[r] : 0u;
+        g[i] = r < n ? rank_gid[r] : 0u;
         v[i] = r < n ? rank_off[r] : 0u;
         local += v[i];
     }
-    uint32_t agg;
-    uint32_t run = block_offsets[blockIdx.x] + block_exclusive_scan(local, s_scan, &agg);
+    uint32_t before = 0;
+    for (int b = threadIdx.x; b < static_cast<int>(blockIdx.x); b += kScanThreads) before += block_sums[b];
+    uint32_t agg, base_all;
+    block_exclusive_scan(before, s_scan, &base_all);
+    __syncthreads();  // s_scan is reused
+    uint32_t run = base_all + block_exclusive_scan(local, s_scan, &agg);
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *total = base_all + agg;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
         const long r = r0 + i;
@@ -387,7 +424,6 @@ __global__ void __launch_bounds__(kScanThreads) k_emit_prep(const uint32_t* __re
             rc = make_int2((q.x & 0xFFFF) | ((q.y - q.x + 1) << 16), q.z);
         }
         rank_off[r] = run;
-        rank_gid[r] = g[i];
         rank_rc[r] = rc;
         // the rank owning output b * kEmitTile starts k_emit's CTA b (no binary search there);
         // entry nctas bounds the last CTA's window when M exceeds the capacity
@@ -549,9 +585,12 @@ __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ key
 template <typename K>
 bool radix_sort(const K* first_keys, const uint32_t* key24, K* keys_in, K* keys_out, const uint32_t* first_vals,
                 uint32_t* vals_in, uint32_t* vals_out, int n, const uint32_t* n_dev, int bits, void* ws,
-                cudaStream_t s, bool counts_ready = false, int hist_slot = 0, bool hist_zeroed = false) {
+                cudaStream_t s, bool counts_ready = false, int hist_slot = 0, bool hist_zeroed = false,
+                uint2* ranges = nullptr) {
     if (n <= 1) {
         if (n == 1 && !first_vals) OSB_CUDA_CHECK(cudaMemsetAsync(vals_in, 0, sizeof(uint32_t), s));  // id 0
+        if (ranges && n == 1)
+            launch_pdl(k_ranges, 1, 256, s, reinterpret_cast<const uint32_t*>(keys_in), n, n_dev, ranges);
         return false;
     }
     const int passes = (bits + kRadixBits - 1) / kRadixBits;
@@ -577,7 +616,8 @@ bool radix_sort(const K* first_keys, const uint32_t* key24, K* keys_in, K* keys_
             OSB_LAUNCHED(1);
         }
         launch_pdl(k_scan_counts, kBins, kSortThreads, s, counts, blocks, hist + p * kBins, offsets);
-        launch_pdl(k_downsweep<K>, blocks, kSortThreads, s, ki, vi, ko, vo, n, n_dev, shift, blocks, offsets, xf);
+        launch_pdl(k_downsweep<K>, blocks, kSortThreads, s, ki, vi, ko, vo, n, n_dev, shift, blocks, offsets, xf,
+                   p == passes - 1 ? ranges : nullptr);
         OSB_LAUNCHED(2);
         flipped = !flipped;
     }
@@ -599,9 +639,9 @@ bool radix_sort_u64(uint64_t* ki, uint64_t* ko, uint32_t* vi, uint32_t* vo, int 
                                 nullptr, bits, ws, s, false, 0, hist_zeroed);
 }
 bool radix_sort_u32(uint32_t* ki, uint32_t* ko, uint32_t* vi, uint32_t* vo, int n, int bits, void* ws,
-                    cudaStream_t s, const uint32_t* n_dev, bool counts_ready, bool tile_slot) {
+                    cudaStream_t s, const uint32_t* n_dev, bool counts_ready, bool tile_slot, uint2* ranges) {
     return radix_sort<uint32_t>(ki, nullptr, ki, ko, vi, vi, vo, n, n_dev, bits, ws, s, counts_ready && bits <= 16,
-                                tile_slot ? 1 : 0, tile_slot);
+                                tile_slot ? 1 : 0, tile_slot, ranges);
 }
 void tile_sort_prepare(void* ws, cudaStream_t s) {
     OSB_CUDA_CHECK(cudaMemsetAsync(static_cast<uint32_t*>(ws) + kMaxPasses * kBins, 0,
@@ -617,18 +657,20 @@ namespace {
 // The frame's K2 scratch that must start at zero, in one chained kernel instead of separate memsets:
 // both digit-total slots of the sort workspace, the long-run flag and the tile ranges.
 __global__ void k_k2_zero(uint32_t* __restrict__ hist, int nhist, uint32_t* __restrict__ flag,
-                          uint2* __restrict__ ranges, int tiles) {
+                          uint2* __restrict__ ranges, int tiles, uint32_t* __restrict__ scan_sums, int nsums) {
     pdl_begin();
     const int i = blockIdx.x * blockDim.x + threadIdx.x, step = gridDim.x * blockDim.x;
     for (int k = i; k < nhist; k += step) hist[k] = 0u;
-    for (int k = i; k < tiles; k += step) ranges[k] = make_uint2(0u, 0u);
+    for (int k = i; k < nsums; k += step) scan_sums[k] = 0u;
+    for (int k = i; k < tiles; k += step) ranges[k] = make_uint2(~0u, 0u);  // atomicMin / atomicMax identities
     if (i == 0) *flag = 0u;
 }
 }  // namespace
 
-void launch_k2_zero(void* sort_ws, uint32_t* long_run_flag, uint2* ranges, int tiles, cudaStream_t s) {
+void launch_k2_zero(void* sort_ws, uint32_t* long_run_flag, uint2* ranges, int tiles, void* scan_ws, int n,
+                    cudaStream_t s) {
     launch_pdl(k_k2_zero, 64, 256, s, static_cast<uint32_t*>(sort_ws), 2 * kMaxPasses * kBins, long_run_flag, ranges,
-               tiles);
+               tiles, static_cast<uint32_t*>(scan_ws), scan_block_count(n));
     OSB_LAUNCHED(1);
 }
 
@@ -653,22 +695,23 @@ EmitArrays scan_emit_arrays(void* ws, int n) {
 
 void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
                       uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws,
-                      uint32_t* cta_first, void* tile_sort_ws, cudaStream_t s) {
+                      uint32_t* cta_first, void* tile_sort_ws, cudaStream_t s, const uint32_t* depth_keys24,
+                      const uint64_t* depth_key, uint32_t* long_run_flag) {
     if (n <= 0) {
         OSB_CUDA_CHECK(cudaMemsetAsync(total, 0, sizeof(uint32_t), s));
         return;
     }
     const int blocks = (n + kScanTile - 1) / kScanTile;
-    uint32_t* sums = static_cast<uint32_t*>(ws);
+    uint32_t* sums = static_cast<uint32_t*>(ws);  // zeroed by k_k2_zero (scan_sums_reset after a counting pass)
     uint32_t* rank_off = sums + ((blocks + 64 + 63) & ~63);
     const size_t npad = (static_cast<size_t>(n) + 63) & ~size_t(63);  // keeps every array 256-B aligned
     uint32_t* rank_gid = rank_off + npad;
     int2* rank_rc = reinterpret_cast<int2*>(rank_gid + npad);
-    launch_pdl(k_touch_sums, blocks, kScanThreads, s, touched, order, n, sums, rank_off);
-    launch_pdl(k_scan_block_sums, 1, 1024, s, sums, blocks, total);
+    launch_pdl(k_touch_sums, blocks, kScanThreads, s, touched, order, n, sums, rank_off, rank_gid, depth_keys24,
+               depth_key, long_run_flag);
     // one CTA per kEmitTile outputs up to the capacity (CTAs past M exit; M > capacity is retried)
     const long grid = keys ? emit_ctas(capacity) : 0;
-    launch_pdl(k_emit_prep, blocks, kScanThreads, s, order, rect, n, sums, rank_off, rank_gid, rank_rc, cta_first,
+    launch_pdl(k_emit_prep, blocks, kScanThreads, s, rect, n, sums, rank_off, rank_gid, rank_rc, total, cta_first,
                static_cast<int>(grid));
     // the tile sort's workspace layout (radix_sort): hist[kMaxPasses][kBins] | .. | counts[kBins][blocks]
     uint32_t* t_hist = tile_sort_ws ? static_cast<uint32_t*>(tile_sort_ws) + kMaxPasses * kBins : nullptr;  // slot 1
@@ -677,63 +720,14 @@ void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4
     if (grid > 0)
         launch_pdl(k_emit, static_cast<int>(grid), kScanThreads, s, rank_off, rank_gid, rank_rc, n, total, tiles_x,
                    keys, vals, capacity, cta_first, t_counts, t_hist, static_cast<int>(grid));
-    OSB_LAUNCHED(grid > 0 ? 4 : 3);
+    OSB_LAUNCHED(grid > 0 ? 3 : 2);
 }
 
-void launch_ranges(const uint32_t* sorted_tiles, int m, uint2* ranges, cudaStream_t s, const uint32_t* m_dev) {
-    if (m <= 0) return;
-    launch_pdl(k_ranges, (m + 1023) / 1024, 256, s, sorted_tiles, m, m_dev, ranges);
-    OSB_LAUNCHED(1);
-}
+int scan_block_count(int n) { return n > 0 ? (n + kScanTile - 1) / kScanTile : 0; }
 
-}  // namespace osb
-
-namespace osb {
-
-namespace {
-
-constexpr int kMaxRun = 64;
-
-// Exact (FP64 depth, id) order inside runs of equal FP32-rounded depth keys (the stable FP32 sort
-// left each run in ascending id order). Runs longer than kMaxRun raise *flag: the caller then
-// redoes the depth rank with the full 64-bit sort.
-__global__ void k_fix_runs(const uint32_t* __restrict__ keys, uint32_t* __restrict__ order,
-                           const uint64_t* __restrict__ depth_key, int n, uint32_t* __restrict__ flag) {
-    pdl_begin();
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t k = keys[i];
-    if (k == 0xFFFFFFu) return;                       // culled tail: no instances, order irrelevant
-    if (i > 0 && keys[i - 1] == k) return;            // not a run start
-    if (i + 1 >= n || keys[i + 1] != k) return;       // run of one
-    int e = i + 1;
-    while (e < n && keys[e] == k && e - i <= kMaxRun) ++e;
-    if (e - i > kMaxRun) {
-        atomicExch(flag, 1u);
-        return;
-    }
-    for (int a = i + 1; a < e; ++a) {  // insertion sort by (depth bits, id)
-        const uint32_t g = order[a];
-        const uint64_t d = depth_key[g];
-        int b = a - 1;
-        while (b >= i) {
-            const uint32_t h = order[b];
-            const uint64_t dh = depth_key[h];
-            if (dh < d || (dh == d && h < g)) break;
-            order[b + 1] = h;
-            --b;
-        }
-        order[b + 1] = g;
-    }
-}
-
-}  // namespace
-
-void launch_fix_runs(const uint32_t* keys, uint32_t* order, const uint64_t* depth_key, int n, uint32_t* flag,
-                     cudaStream_t s) {
-    if (n <= 1) return;
-    launch_pdl(k_fix_runs, (n + 255) / 256, 256, s, keys, order, depth_key, n, flag);
-    OSB_LAUNCHED(1);
+void scan_sums_reset(void* ws, int n, cudaStream_t s) {
+    const int blocks = scan_block_count(n);
+    if (blocks) OSB_CUDA_CHECK(cudaMemsetAsync(ws, 0, sizeof(uint32_t) * blocks, s));
 }
 
 }  // namespace osb
