@@ -636,7 +636,9 @@ def run_ours(args):
         # 132 B per visible Gaussian (upper bound: every Gaussian counted as visible)
         "preprocess": N * (236 + 132),
         "depth_sort": N * 12 * 2 * 8,
-        "tile_sort": instances * 32,
+        # two 8-byte (tile, id) passes in and out; the last pass stores ids only (its keys become the
+        # tile ranges): 8 + 8 + 8 + 4 = 28 B per instance
+        "tile_sort": instances * 28,
         "loss": plane * 36,
         # K4b per visible Gaussian: parameters 236 + K4a accumulators 48 + K1 records (conic 32, blend
         # record 48, depth key 8) in; gradient planes 236 + screen statistics 20 out (upper bound)

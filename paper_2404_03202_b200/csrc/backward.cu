@@ -95,7 +95,10 @@ static __device__ __noinline__ float2 k4a_slow(uint32_t gid) {
 // and makes all nine accumulated values zero. Only the FP64 fallback (pairs inside the guard band,
 // or the 0.99 clamp gate of a near-opaque splat) branches, warp-uniformly.
 template <bool BG>
-__global__ void __launch_bounds__(kTileThreads, 4) k_backward_pixels(const uint32_t* __restrict__ inst_gid,
+#ifndef OSB_K4A_CTAS
+#define OSB_K4A_CTAS 4  // CTAs per SM (64 registers)
+#endif
+__global__ void __launch_bounds__(kTileThreads, OSB_K4A_CTAS) k_backward_pixels(const uint32_t* __restrict__ inst_gid,
                                                                      const uint2* __restrict__ ranges, PreprocessOut pp,
                                                                      int W, int H, int tiles_x, float bg0, float bg1,
                                                                      float bg2, FrameBuffers fb,

@@ -17,7 +17,10 @@ namespace osb {
 namespace {
 
 template <bool STRICT>
-__global__ void __launch_bounds__(kTileThreads, 4) k_blend(const uint32_t* __restrict__ inst_gid,
+#ifndef OSB_K3_CTAS
+#define OSB_K3_CTAS 4  // CTAs per SM (64 registers)
+#endif
+__global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint32_t* __restrict__ inst_gid,
                                                            uint2* __restrict__ ranges, PreprocessOut pp, int W,
                                                            int H, int tiles_x, float bg0, float bg1, float bg2,
                                                            FrameBuffers fb) {
