@@ -335,8 +335,9 @@ __device__ __noinline__ int run_position(const uint32_t* __restrict__ keys, cons
     return s + below;
 }
 
-// Per depth rank r: the Gaussian that takes rank r (rank_gid) and its touched count (rank_off, read
-// by k_emit_prep), and the per-block sums of touched (atomics into sums zeroed by k_k2_zero).
+// Per depth rank r: the Gaussian that takes rank r (rank_gid), its touched count (rank_off, read
+// by k_emit_prep) and packed tile rectangle {x0 & 0xFFFF | width << 16, y0} (rank_rc; both gathers
+// issued together), and the per-block sums of touched (atomics into sums zeroed by k_k2_zero).
 // keys (fast depth rank): the sorted 24-bit keys; every element of a run of equal keys places itself
 // at its exact (FP64 depth, id) position inside the run (replaces a separate run-fixing pass; a run
 // may straddle two blocks, so its elements add to the sum of the block they land in).
@@ -345,6 +346,8 @@ __global__ void __launch_bounds__(kScanThreads) k_touch_sums(const uint32_t* __r
                                                              uint32_t* __restrict__ block_sums,
                                                              uint32_t* __restrict__ ranked,
                                                              uint32_t* __restrict__ rank_gid,
+                                                             const int4* __restrict__ rect,
+                                                             int2* __restrict__ rank_rc,
                                                              const uint32_t* __restrict__ keys,
                                                              const uint64_t* __restrict__ depth_key,
                                                              uint32_t* __restrict__ flag) {
@@ -366,8 +369,10 @@ __global__ void __launch_bounds__(kScanThreads) k_touch_sums(const uint32_t* __r
                 }
             }
             const uint32_t v = touched[g];
+            const int4 q = rect[g];  // stale for culled Gaussians (v = 0): not used then
             ranked[dst] = v;
             rank_gid[dst] = g;
+            rank_rc[dst] = v > 0 ? make_int2((q.x & 0xFFFF) | ((q.y - q.x + 1) << 16), q.z) : make_int2(0, 0);
             if (dst / kScanTile == blockIdx.x) local += v;
             else if (v) atomicAdd(&block_sums[dst / kScanTile], v);
         }
@@ -385,25 +390,24 @@ __global__ void __launch_bounds__(kScanThreads) k_touch_sums(const uint32_t* __r
 // shared-memory search, then a forward walk). Stores are 32-B runs per lane.
 constexpr int kEmitTile = kScanThreads * 8;
 constexpr int kEmitWindow = 2 * kEmitTile;  // ranks staged per CTA (more only with many empty ranks)
+constexpr int kEmitSmall = kEmitWindow / 4;  // windows up to this also stage their gid / rectangle records
+static_assert(4 * kEmitSmall * 4 <= kEmitWindow * 4, "off + gid + rc fit in the s_off space");
 
 // rank_off[r] holds the touched count of rank r on entry (k_touch_sums) and the rank's first output
 // on exit. Each block derives its own exclusive prefix from the raw block sums (at most a few
 // thousand words: cheaper than a separate scan launch); the last block stores M = *total.
-__global__ void __launch_bounds__(kScanThreads) k_emit_prep(const int4* __restrict__ rect, int n,
-                                                            const uint32_t* __restrict__ block_sums,
+__global__ void __launch_bounds__(kScanThreads) k_emit_prep(int n, const uint32_t* __restrict__ block_sums,
                                                             uint32_t* __restrict__ rank_off,
-                                                            const uint32_t* __restrict__ rank_gid,
-                                                            int2* __restrict__ rank_rc, uint32_t* __restrict__ total,
+                                                            uint32_t* __restrict__ total,
                                                             uint32_t* __restrict__ cta_first, int nctas) {
     pdl_begin();
     __shared__ uint32_t s_scan[kSortWarps + 1];
     const long r0 = static_cast<long>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
-    uint32_t v[kScanItems], g[kScanItems];
+    uint32_t v[kScanItems];
     uint32_t local = 0;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
         const long r = r0 + i;
-        g[i] = r < n ? rank_gid[r] : 0u;
         v[i] = r < n ? rank_off[r] : 0u;
         local += v[i];
     }
@@ -418,13 +422,7 @@ __global__ void __launch_bounds__(kScanThreads) k_emit_prep(const int4* __restri
     for (int i = 0; i < kScanItems; ++i) {
         const long r = r0 + i;
         if (r >= n) break;
-        int2 rc = make_int2(0, 0);
-        if (v[i] > 0) {
-            const int4 q = rect[g[i]];
-            rc = make_int2((q.x & 0xFFFF) | ((q.y - q.x + 1) << 16), q.z);
-        }
         rank_off[r] = run;
-        rank_rc[r] = rc;
         // the rank owning output b * kEmitTile starts k_emit's CTA b (no binary search there);
         // entry nctas bounds the last CTA's window when M exceeds the capacity
         if (v[i] > 0 && cta_first)
@@ -459,7 +457,7 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
                                                        uint32_t* __restrict__ counts, uint32_t* __restrict__ hist,
                                                        int nblocks) {
     pdl_begin();
-    __shared__ uint32_t s_off[kEmitWindow];
+    __shared__ __align__(16) uint32_t s_off[kEmitWindow];
     __shared__ __align__(16) uint32_t s_k[kEmitTile];
     __shared__ __align__(16) uint32_t s_v[kEmitTile];
     __shared__ uint32_t s_h0[kBins], s_h1[kBins];
@@ -487,7 +485,23 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
     __syncthreads();
     const int rb = s_rb, w = s_w;
     const uint32_t* off = rank_off + rb;
-    if (w <= kEmitWindow) {
+    const uint32_t* gidp = rank_gid + rb;
+    const int2* rcp = rank_rc + rb;
+    if (w <= kEmitSmall) {
+        // the window's whole records in shared memory (one coalesced load phase instead of a
+        // dependent global load at every rank change of the walk): off | gid | rc in s_off's space
+        uint32_t* s_gid = s_off + kEmitSmall;
+        int2* s_rc = reinterpret_cast<int2*>(s_off + 2 * kEmitSmall);
+        for (int i = threadIdx.x; i < w; i += kScanThreads) {
+            s_off[i] = off[i];
+            s_gid[i] = gidp[i];
+            s_rc[i] = rcp[i];
+        }
+        __syncthreads();
+        off = s_off;
+        gidp = s_gid;
+        rcp = s_rc;
+    } else if (w <= kEmitWindow) {
         for (int i = threadIdx.x; i < w; i += kScanThreads) s_off[i] = off[i];
         __syncthreads();
         off = s_off;
@@ -497,8 +511,8 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
         int e = owner_of(off, w, o);
         // the rank's record and the (row, column) of output o inside its rectangle: one division for
         // the thread's first output, then stepped along the row-major walk; reloaded when the rank changes
-        int2 rc = rank_rc[rb + e];
-        uint32_t gid = rank_gid[rb + e];
+        int2 rc = rcp[e];
+        uint32_t gid = gidp[e];
         uint32_t wt = static_cast<uint32_t>(rc.x) >> 16;
         uint32_t li = o - off[e];
         uint32_t row = li / wt, col = li - row * wt;
@@ -509,8 +523,8 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
                     ++e;
                     next = e + 1 < w ? off[e + 1] : 0xFFFFFFFFu;
                 } while (o >= next);
-                rc = rank_rc[rb + e];
-                gid = rank_gid[rb + e];
+                rc = rcp[e];
+                gid = gidp[e];
                 wt = static_cast<uint32_t>(rc.x) >> 16;
                 row = 0;
                 col = 0;
@@ -707,12 +721,11 @@ void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4
     const size_t npad = (static_cast<size_t>(n) + 63) & ~size_t(63);  // keeps every array 256-B aligned
     uint32_t* rank_gid = rank_off + npad;
     int2* rank_rc = reinterpret_cast<int2*>(rank_gid + npad);
-    launch_pdl(k_touch_sums, blocks, kScanThreads, s, touched, order, n, sums, rank_off, rank_gid, depth_keys24,
-               depth_key, long_run_flag);
+    launch_pdl(k_touch_sums, blocks, kScanThreads, s, touched, order, n, sums, rank_off, rank_gid, rect, rank_rc,
+               depth_keys24, depth_key, long_run_flag);
     // one CTA per kEmitTile outputs up to the capacity (CTAs past M exit; M > capacity is retried)
     const long grid = keys ? emit_ctas(capacity) : 0;
-    launch_pdl(k_emit_prep, blocks, kScanThreads, s, rect, n, sums, rank_off, rank_gid, rank_rc, total, cta_first,
-               static_cast<int>(grid));
+    launch_pdl(k_emit_prep, blocks, kScanThreads, s, n, sums, rank_off, total, cta_first, static_cast<int>(grid));
     // the tile sort's workspace layout (radix_sort): hist[kMaxPasses][kBins] | .. | counts[kBins][blocks]
     uint32_t* t_hist = tile_sort_ws ? static_cast<uint32_t*>(tile_sort_ws) + kMaxPasses * kBins : nullptr;  // slot 1
     uint32_t* t_counts = tile_sort_ws ? static_cast<uint32_t*>(tile_sort_ws) + 2 * kMaxPasses * kBins : nullptr;

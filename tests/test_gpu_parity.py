@@ -268,6 +268,36 @@ def test_equal_depth_runs_fall_back_to_the_exact_sort(oracle_port):
     assert np.max(np.abs(fr.image() - of.rgb)) <= IMAGE_ATOL
 
 
+def test_depth_runs_straddling_emission_blocks(oracle_port):
+    """Runs of FP32-equal depth keys: groups of 2..40 Gaussians moved off one position along a
+    tangent by permuted multiples of 5e-5 (FP64-distinct depths that round to one FP32 value, in
+    an order unrelated to their ids) put ~98 % of the depth ranks in 1,331 runs of up to 21, four
+    of them straddling the 2048-rank blocks of the emission scan: every member places itself at its
+    exact (FP64 depth, id) position inside its run (k_touch_sums) and the tile lists stay the
+    oracle's."""
+    rng = np.random.default_rng(21)
+    cloud = scenes.synthetic_cloud(9000, seed=21)
+    P = cloud.positions.copy()
+    i = 0
+    while i < 9000:
+        L = int(rng.integers(2, 41))
+        idx = np.arange(i, min(i + L, 9000))
+        e = np.cross(P[i], [0.3, 1.0, 0.2])
+        e /= np.linalg.norm(e)
+        P[idx] = P[i] + (5e-5 * rng.permutation(len(idx)))[:, None] * e
+        i += L
+    cloud.positions = P
+    cloud = cloud.rounded()  # the device holds FP32 parameters: the oracle sees the same values
+    ctx = native.Context(cloud)
+    pose = scenes.identity_pose()
+    fr = ctx.render(pose, 384, 192)
+    of = oracle_port.render(cloud, pose, 384, 192)
+    nbad, first = compare_tiles(fr, of)
+    assert nbad == 0, (nbad, first)
+    assert np.max(np.abs(fr.image() - of.rgb)) <= IMAGE_ATOL
+    fr.free()
+
+
 def test_adam_shards_equal_the_full_step():
     """osplat_gpu_adam_step_range over the shards of a data-parallel world == the full fused Adam,
     bit for bit (the sharded optimizer's update is elementwise)."""
