@@ -76,18 +76,19 @@ __device__ __forceinline__ void jacobian_equirect_grad(const double* t, double t
 
 // project_gaussian (rasterizer.cpp:17-55) minus the SH colour. Returns false when culled
 // (t_r < 0.01, pole-degenerate, opacity < 1/255).
-template <bool kPixel = true>
-__device__ __forceinline__ bool project64(const float* __restrict__ P, int stride, const Planes& pl, int gid,
-                                          const Pose& pose, int W, int H, Proj64& pr) {
+// ld(plane) returns this Gaussian's FP32 parameter of that plane (global memory, or K1's shared-
+// memory staging of its CTA's parameter tile).
+template <bool kPixel = true, typename Ld>
+__device__ __forceinline__ bool project64(Ld ld, const Planes& pl, const Pose& pose, int W, int H, Proj64& pr) {
     // all 11 geometry parameters are loaded first: independent loads in flight together instead of
     // each waiting behind the FP64 math that precedes its use
     float lsf[3], qf[4];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) lsf[k] = __ldg(P + static_cast<size_t>(pl.lscale(k)) * stride + gid);
+    for (int k = 0; k < 3; ++k) lsf[k] = ld(pl.lscale(k));
 #pragma unroll
-    for (int k = 0; k < 4; ++k) qf[k] = __ldg(P + static_cast<size_t>(pl.rot(k)) * stride + gid);
-    const double logit = load_param(P, stride, pl.opacity(), gid);
-    double m[3] = {load_param(P, stride, 0, gid), load_param(P, stride, 1, gid), load_param(P, stride, 2, gid)};
+    for (int k = 0; k < 4; ++k) qf[k] = ld(pl.rot(k));
+    const double logit = static_cast<double>(ld(pl.opacity()));
+    double m[3] = {static_cast<double>(ld(0)), static_cast<double>(ld(1)), static_cast<double>(ld(2))};
     world_to_camera(pose, m, pr.t, &pr.t_r);
     const double* t = pr.t;
     if (pr.t_r < kNear) return false;
@@ -126,6 +127,13 @@ __device__ __forceinline__ bool project64(const float* __restrict__ P, int strid
     pr.conic[1] = -b / det;
     pr.conic[2] = a / det;
     return true;
+}
+
+template <bool kPixel = true>
+__device__ __forceinline__ bool project64(const float* __restrict__ P, int stride, const Planes& pl, int gid,
+                                          const Pose& pose, int W, int H, Proj64& pr) {
+    return project64<kPixel>([&](int plane) { return __ldg(P + static_cast<size_t>(plane) * stride + gid); }, pl,
+                             pose, W, H, pr);
 }
 
 // View direction W^T t / t_r (rasterizer.cpp:51).
