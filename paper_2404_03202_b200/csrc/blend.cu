@@ -17,6 +17,9 @@ namespace osb {
 namespace {
 
 template <bool STRICT>
+#ifndef OSB_K3_ELLIPSE
+#define OSB_K3_ELLIPSE false  // K3 stages box masks (per-row ellipse intervals: measured slower in K3)
+#endif
 #ifndef OSB_K3_CTAS
 #define OSB_K3_CTAS 4  // CTAs per SM (64 registers)
 #endif
@@ -80,7 +83,7 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint3
             uint32_t m = 0u;
             if (idx < range.y) {
                 const float4* s4 = reinterpret_cast<const float4*>(pp.splat + gid);
-                m = stage_record16<false>(stage[warp + e * kTileWarps], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc,
+                m = stage_record16<OSB_K3_ELLIPSE>(stage[warp + e * kTileWarps], lane, gid, pp.pxy[gid], s4[0], s4[1], s4[2], xc,
                                    yc, width);
             }
             s_mask[t + e * kTileThreads] = static_cast<uint16_t>(m);
