@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K4A_CTAS) k_backward_pixels(
     __shared__ WarpStage stage[kSubs];
     __shared__ uint16_t s_mask[kChunk];
     __shared__ int s_last[kTileWarps];
-    const int tile = blockIdx.x;
+    const int tile = block_tile(tiles_x, (H + kTile - 1) / kTile);
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const WarpPixel wp = warp_pixel(warp, lane);
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K4A_CTAS) k_backward_pixels(
     // half-warp culling as K3), back to front; the halves reduce their (different) entries at once.
     const uint32_t halfmask = wp.half ? 0xFFFF0000u : 0x0000FFFFu;
     if (lane == 0) s_last[warp] = max_last;
-    if (threadIdx.x == 0) s_slow = SlowCtx{pp.pxy, pp.conic_o, width, tiles_x};
+    if (threadIdx.x == 0) s_slow = SlowCtx{pp.pxy, pp.conic_o, width, tiles_x, tile};
     __syncthreads();
     int cta_last = 0;
 #pragma unroll
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(kTileThreads) k_backward_pixels_det(
     __shared__ uint16_t s_mask[kDetChunk];
     __shared__ float part[2 * kTileWarps][kDetChunk][9];
     __shared__ int s_last[kTileWarps];
-    const int tile = blockIdx.x;
+    const int tile = block_tile(tiles_x, (H + kTile - 1) / kTile);
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const WarpPixel wp = warp_pixel(warp, lane);

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint3
     constexpr int kSubs = kChunk / 32;
     __shared__ WarpStage stage[kSubs];
     __shared__ uint16_t s_mask[kChunk];
-    const int tile = blockIdx.x;
+    const int tile = block_tile(tiles_x, (H + kTile - 1) / kTile);
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const WarpPixel wp = warp_pixel(warp, lane);

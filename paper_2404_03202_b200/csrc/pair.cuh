@@ -201,6 +201,22 @@ __device__ __forceinline__ bool pair_power2(const float4 A, const float4 B, floa
     return true;
 }
 
+// Tile of this CTA (K3 / K4a: one CTA per 16x16 tile), row-major. OSB_TILE_ORDER 1 launches the
+// tile rows from the two image edges inwards (rows 0, R-1, 1, R-2, ...) so the long pole-row lists
+// do not form the grid's tail (a list-scheduling model predicted -8 % for pole-heavy views); measured
+// slower — K3 0.558 -> 0.571 ms, pole-heavy 603 -> 581 FPS: the CTAs in flight then cover two bands
+// of rows instead of one, and the neighbouring tiles' shared splat records hit in L2 less often.
+#ifndef OSB_TILE_ORDER
+#define OSB_TILE_ORDER 0
+#endif
+__device__ __forceinline__ int block_tile(int tiles_x, int tiles_y) {
+    const int b = blockIdx.x;
+    if (OSB_TILE_ORDER == 0) return b;
+    const int ri = b / tiles_x, col = b - ri * tiles_x;
+    const int row = (ri & 1) ? tiles_y - 1 - (ri >> 1) : (ri >> 1);
+    return row * tiles_x + col;
+}
+
 // Per-CTA context of the out-of-line FP64 fallbacks (K3, K4a): they read the FP64 records and
 // recompute their pixel from the thread index, so none of it stays live in the hot loops' registers.
 struct SlowCtx {
@@ -208,11 +224,12 @@ struct SlowCtx {
     const double4* conic_o;
     double width;
     int tiles_x;
+    int tile;
 };
 static __shared__ SlowCtx s_slow;
 
 __device__ __forceinline__ void slow_pixel(int& px, int& py) {
-    const int tile = blockIdx.x;
+    const int tile = s_slow.tile;
     const WarpPixel wp = warp_pixel(threadIdx.x >> 5, threadIdx.x & 31);
     px = (tile % s_slow.tiles_x) * kTile + wp.lx;
     py = (tile / s_slow.tiles_x) * kTile + wp.ly;
