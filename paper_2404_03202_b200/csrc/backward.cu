@@ -42,26 +42,46 @@ __device__ __forceinline__ void red_add(float* addr, float a) {
 // holds the half's sum of value *idx (-1: padding).
 __device__ __forceinline__ float half_reduce9(const float (&v)[9], int lane, int* idx) {
     const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2, b0 = lane & 1;
-    float a[5];
+    // the adds of a stage issue in pairs as packed FADD2 (each half rounded like the scalar add)
+    float k[5], r[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
         const float lo = v[i];
         const float hi = i + 5 < 9 ? v[i + 5] : 0.0f;
-        a[i] = (b3 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b3 ? lo : hi, 8);
+        k[i] = b3 ? hi : lo;
+        r[i] = __shfl_xor_sync(0xffffffffu, b3 ? lo : hi, 8);
     }
-    float c[3];
+    float a[5];
+    {
+        const float2 s01 = __fadd2_rn(make_float2(k[0], k[1]), make_float2(r[0], r[1]));
+        const float2 s23 = __fadd2_rn(make_float2(k[2], k[3]), make_float2(r[2], r[3]));
+        a[0] = s01.x; a[1] = s01.y; a[2] = s23.x; a[3] = s23.y;
+        a[4] = k[4] + r[4];
+    }
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         const float lo = a[i];
         const float hi = i + 3 < 5 ? a[i + 3] : 0.0f;
-        c[i] = (b2 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b2 ? lo : hi, 4);
+        k[i] = b2 ? hi : lo;
+        r[i] = __shfl_xor_sync(0xffffffffu, b2 ? lo : hi, 4);
     }
-    float e[2];
+    float c[3];
+    {
+        const float2 s01 = __fadd2_rn(make_float2(k[0], k[1]), make_float2(r[0], r[1]));
+        c[0] = s01.x; c[1] = s01.y;
+        c[2] = k[2] + r[2];
+    }
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
         const float lo = c[i];
         const float hi = i + 2 < 3 ? c[i + 2] : 0.0f;
-        e[i] = (b1 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b1 ? lo : hi, 2);
+        k[i] = b1 ? hi : lo;
+        r[i] = __shfl_xor_sync(0xffffffffu, b1 ? lo : hi, 2);
+    }
+    float e[2];
+    {
+        const float2 s01 = __fadd2_rn(make_float2(k[0], k[1]), make_float2(r[0], r[1]));
+        e[0] = s01.x; e[1] = s01.y;
     }
     const float f = (b0 ? e[1] : e[0]) + __shfl_xor_sync(0xffffffffu, b0 ? e[0] : e[1], 1);
     const int ic = (b1 ? 2 : 0) + (b0 ? 1 : 0);
