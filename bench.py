@@ -496,24 +496,29 @@ def run_ours(args):
     fwd_pairs, bwd_pairs, instances = fwd_pairs / nviews, bwd_pairs / nviews, instances / nviews
     ctx.zero_grad()
 
-    # ---- render-only FPS (K1 -> K3), same scene, device time
+    # ---- render-only FPS (K1 -> K3), device time: the synthetic scene as generated (a fresh context
+    # holding the seed-1 cloud the training started from), so the number does not depend on how
+    # many train steps ran before it
     barrier()
-    nframes = max(args.steps, 16)
+    rctx = native.Context(cloud, device=local, stream=stream.cuda_stream)
+    for k in range(3):
+        rctx.render(poses[k % N_POSES], W, H).free()
+    nframes = max(args.steps, 4 * N_POSES)
     r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     r0.record(stream)
     for k in range(nframes):
-        ctx.render(poses[k % N_POSES], W, H).free()
+        rctx.render(poses[k % N_POSES], W, H).free()
     r1.record(stream)
     barrier()
     render_ms = max_over_ranks(r0.elapsed_time(r1)) / nframes
     # the same frames again with per-kernel CUDA events (the split; its total includes the events)
-    ctx.profile(timing=True)
-    ctx.profile_read(reset=True)
+    rctx.profile(timing=True)
+    rctx.profile_read(reset=True)
     for k in range(nframes):
-        ctx.render(poses[k % N_POSES], W, H).free()
+        rctx.render(poses[k % N_POSES], W, H).free()
     barrier()
-    rprof = ctx.profile_read(reset=True)
-    ctx.profile(timing=False)
+    rprof = rctx.profile_read(reset=True)
+    rctx.profile(timing=False)
 
     # ---- render FPS sweep (BASELINE configs[2]): the uniform scene over 36 yaws x pitch {0, +-60 deg},
     # and the pole-heavy (|lat| > 70 deg) and seam-heavy (|lon| > 160 deg) scenes over 12 yaws;
@@ -538,8 +543,8 @@ def run_ours(args):
 
         yaw_pitch = [scenes.pose12(scenes.rot_x(np.radians(pt)) @ scenes.rot_y(np.radians(yw)))
                      for pt in (0.0, 60.0, -60.0) for yw in range(0, 360, 10)]
-        frame_ms(ctx, yaw_pitch[:3])
-        sweep = {"uniform_36yaw_x3pitch": summary(frame_ms(ctx, yaw_pitch))}
+        frame_ms(rctx, yaw_pitch[:3])
+        sweep = {"uniform_36yaw_x3pitch": summary(frame_ms(rctx, yaw_pitch))}
         for variant in ("pole", "seam"):
             vc = native.Context(scenes.synthetic_cloud(N, seed=1, variant=variant), device=local,
                                 stream=stream.cuda_stream)
@@ -552,6 +557,7 @@ def run_ours(args):
             frame_ms(vc, views[:2])
             sweep[f"{variant}_heavy_12yaw"] = dict(summary(frame_ms(vc, views)), instances=inst, fwd_pairs=fp)
             vc.free()
+    rctx.free()
 
     # ---- end to end through the public C ABI with host buffers
     e2e = None
