@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K4A_CTAS) k_backward_pixels(
             constexpr bool SEAM = decltype(seam_tag)::value;
             while (__any_sync(0xffffffffu, bal != 0u)) {  // back to front; warp-uniform (the reduction needs all lanes)
                 const uint32_t j = bfind_u32(bal);  // ~0u once this half has no entry left
-                bal &= ~bit_u32(j);
+                bal &= below_u32(j);  // j is bal's highest set bit: clear it (~0u: bal is already 0)
                 const uint32_t jj = j & 31u;
                 OSB_STAT(1, 1);
                 const float4 A = ws.a(jj);

@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint3
     for (int e = 0; e < kPer; ++e)
         gid_next[e] = range.x + t + e * kTileThreads < range.y ? inst_gid[range.x + t + e * kTileThreads] : 0u;
     for (uint32_t cbase = range.x; cbase < range.y; cbase += kChunk) {
-        if (!__syncthreads_or(!done)) break;  // every pixel of the tile has terminated
+        // every pixel of the tile has terminated (no barrier before the first round: nothing staged yet)
+        if (cbase != range.x && !__syncthreads_or(!done)) break;
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
             const uint32_t idx = cbase + t + e * kTileThreads;

@@ -240,6 +240,11 @@ __device__ __forceinline__ uint32_t bfind_u32(uint32_t x) {  // index of the hig
     asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
     return r;
 }
+__device__ __forceinline__ uint32_t below_u32(uint32_t j) {  // (1 << j) - 1, all ones for j >= 32 (one BMSK)
+    uint32_t r;
+    asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(r) : "r"(j));
+    return r;
+}
 __device__ __forceinline__ uint32_t bit_u32(uint32_t j) {  // 1 << j, 0 for j >= 32 (PTX clamps the shift)
     uint32_t r;
     asm("shl.b32 %0, 1, %1;" : "=r"(r) : "r"(j));
