@@ -376,6 +376,13 @@ void Engine::render_into(Frame* f) {
 
     const PreprocessOut pp = f->pp();
     const int N = f->n;
+    // one workspace for both sorts, sized for both up front (the zeroed digit totals must survive)
+    f->sort_ws.ensure(std::max(radix_workspace_bytes(static_cast<int>(n), 8),
+                               radix_workspace_bytes(static_cast<int>(f->ikeys[0].capacity() / 4), 4)));
+    uint32_t* long_run_flag = f->total.as<uint32_t>() + 1;
+    // K1 clears the frame's K2 scratch on the way (an import of host records or an empty cloud: a
+    // separate k_k2_zero below)
+    const bool k1_zeroes = !f->projected && N > 0 && !f->given_grid;
     // K1 (or the import of host projection records)
     {
         Span sp(*this, kPreprocess);
@@ -384,7 +391,10 @@ void Engine::render_into(Frame* f) {
             launch_import_projections(f->import.as<double>(), N, W, H, pp, stream_);
         else
             launch_preprocess(params_.as<float>(), N, static_cast<int>(stride_), (sh_degree_ + 1) * (sh_degree_ + 1),
-                              active_, f->pose, W, H, pp, stream_);
+                              active_, f->pose, W, H, pp, stream_,
+                              k1_zeroes ? k2_scratch(f->sort_ws.as<void>(), long_run_flag, f->ranges.as<uint2>(), tiles,
+                                                     f->scan_ws.as<void>(), N)
+                                        : K2Scratch{});
     }
     if (f->given_grid) {  // caller-supplied tile lists: no K2
         const uint32_t M = static_cast<uint32_t>(f->grid_slots.size());
@@ -409,16 +419,13 @@ void Engine::render_into(Frame* f) {
     // K2a: depth rank = (t_r, id) order. Fast path: stable sort of the FP32-rounded t_r (monotone)
     // + exact FP64 re-ordering inside runs of equal keys; a run longer than 64 raises a flag
     // and validate() renders the frame again with the full 64-bit sort.
-    // one workspace for both sorts, sized for both up front (the zeroed digit totals must survive)
-    f->sort_ws.ensure(std::max(radix_workspace_bytes(static_cast<int>(n), 8),
-                               radix_workspace_bytes(static_cast<int>(f->ikeys[0].capacity() / 4), 4)));
-    uint32_t* long_run_flag = f->total.as<uint32_t>() + 1;
     const uint32_t* order;
     const uint32_t* keys24 = nullptr;  // fast path: the sorted 24-bit keys (runs fixed in the emission)
     {
         Span sp(*this, kDepthSort);
-        launch_k2_zero(f->sort_ws.as<void>(), long_run_flag, f->ranges.as<uint2>(), tiles, f->scan_ws.as<void>(),
-                       static_cast<int>(N), stream_);
+        if (!k1_zeroes)
+            launch_k2_zero(f->sort_ws.as<void>(), long_run_flag, f->ranges.as<uint2>(), tiles, f->scan_ws.as<void>(),
+                           static_cast<int>(N), stream_);
         bool flipped;
         if (f->full_depth_sort) {
             flipped = radix_sort_u64(f->okeys[0].as<uint64_t>(), f->okeys[1].as<uint64_t>(), f->ovals[0].as<uint32_t>(),

@@ -24,8 +24,20 @@ struct PreprocessOut {
     Splat32* splat;        // N: FP32 blend record (conic, opacity, colour, guard band, extents)
     float* radius;         // N: screen radius ceil(3 sqrt(lambda_max)), -1 when culled (DensifyStats)
 };
+// The frame's K2 scratch that must start at zero (launch_k2_zero's job); with zero.hist set, K1
+// clears it on the way (one launch less in the K2 chain).
+struct K2Scratch {
+    uint32_t* hist = nullptr;  // both digit-total slots of the sort workspace
+    int nhist = 0;
+    uint32_t* flag = nullptr;  // long-run flag
+    uint2* ranges = nullptr;   // tile ranges -> {~0u, 0}
+    int tiles = 0;
+    uint32_t* sums = nullptr;  // emission block sums
+    int nsums = 0;
+};
+K2Scratch k2_scratch(void* sort_ws, uint32_t* long_run_flag, uint2* ranges, int tiles, void* scan_ws, int n);
 void launch_preprocess(const float* params, int n, int stride, int bc, int active_degree, const Pose& pose,
-                       int W, int H, const PreprocessOut& out, cudaStream_t s);
+                       int W, int H, const PreprocessOut& out, cudaStream_t s, const K2Scratch& zero = K2Scratch{});
 
 // Host-supplied SplatProjection records (rasterizer.hpp:31-41) as kSplatPlanes FP64 planes of n:
 // p.x, p.y, cov a, b, c, conic a, b, c, radius, depth, colour r, g, b, alpha_base. Writes the

@@ -109,7 +109,22 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
         : "memory");
 }
 
+#ifndef OSB_K1_LAZY_BAND
+#define OSB_K1_LAZY_BAND 1e-9  // (A/B: a huge band re-sums every channel in the backward's order)
+#endif
 constexpr int kPreThreads = 128;  // Gaussians per CTA = one 512-B row per parameter plane
+
+// 0.5 + sum_k c_k b_k(dir) in the backward's order (gradients.cpp:197-198) for one colour channel;
+// coef points at basis 0's coefficient, basis k's is 3 * kPreThreads floats further (plane 3 + 3k + c).
+// Out of line: only evaluated when the forward sum lies within 1e-9 of zero.
+static __device__ __noinline__ double backward_order_sum(const double* dir, int degree, const float* coef) {
+    double basis[16];
+    sh_basis(dir, degree, basis);
+    const int nb = (degree + 1) * (degree + 1);
+    double r = 0.5;
+    for (int k = 0; k < nb; ++k) r += static_cast<double>(coef[3 * kPreThreads * k]) * basis[k];
+    return r;
+}
 
 // K1: one thread per Gaussian. The CTA's parameter tile (the active planes x 128 Gaussians: 59 rows
 // of 512 B at SH degree 3) is staged into shared memory by TMA bulk copies issued by one thread
@@ -117,8 +132,10 @@ constexpr int kPreThreads = 128;  // Gaussians per CTA = one 512-B row per param
 // instead of 59 dependent-latency global loads per thread (the parameter loads were K1's
 // dominant stall: 30 % of its samples).
 template <int DEG>
+// (80 registers, 6 CTAs / SM; capped at 72 / 64 registers it spills: render 0.832 -> 0.845 / 0.851 ms)
 __global__ void __launch_bounds__(kPreThreads) k_preprocess(const float* __restrict__ P, int n, int stride, int bc,
-                                                            Pose pose, int W, int H, PreprocessOut out) {
+                                                            Pose pose, int W, int H, PreprocessOut out,
+                                                            K2Scratch zero) {
     constexpr int active_degree = DEG;  // compile-time: the SH loop unrolls into registers
     constexpr int nb = (active_degree + 1) * (active_degree + 1);
     constexpr int kRows = 3 + 3 * nb + 8;  // position | active SH | rotation, log-scale, opacity
@@ -146,6 +163,13 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(const float* __restr
         }
     }
     __syncthreads();  // the barrier's initialisation is visible to every thread
+    if (zero.hist) {  // the frame's K2 scratch, cleared while the tile's copies are in flight
+        const int gi = blockIdx.x * kPreThreads + threadIdx.x, step = gridDim.x * kPreThreads;
+        for (int k = gi; k < zero.nhist; k += step) zero.hist[k] = 0u;
+        for (int k = gi; k < zero.tiles; k += step) zero.ranges[k] = make_uint2(~0u, 0u);
+        for (int k = gi; k < zero.nsums; k += step) zero.sums[k] = 0u;
+        if (gi == 0) *zero.flag = 0u;
+    }
     mbar_wait_parity(&s_bar, 0);
     const int gid = g0 + threadIdx.x;
     if (gid >= n) return;
@@ -168,18 +192,23 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(const float* __restr
     double basis[16];
     sh_basis(dir, active_degree, basis);
     double col[3] = {0.0, 0.0, 0.0};
-    double raw_b[3] = {0.5, 0.5, 0.5};  // backward's pre-clamp sum order (gradients.cpp:197-198)
 #pragma unroll
     for (int k = 0; k < nb; ++k) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const double term = static_cast<double>(s_par[pl.sh(k, c)][t]) * basis[k];
-            col[c] += term;
-            raw_b[c] += term;
-        }
+        for (int c = 0; c < 3; ++c) col[c] += static_cast<double>(s_par[pl.sh(k, c)][t]) * basis[k];
     }
-    const uint32_t neg_bits = (raw_b[0] < 0.0 ? 1u : 0u) | (raw_b[1] < 0.0 ? 2u : 0u) | (raw_b[2] < 0.0 ? 4u : 0u);
     col[0] += 0.5; col[1] += 0.5; col[2] += 0.5;
+    // K4b's colour-clamp gate: the sign of the backward's pre-clamp sum, 0.5 + terms in basis order
+    // (gradients.cpp:197-198). It differs from the forward sum (terms, then + 0.5) by rounding only
+    // (|difference| < 1e-13 for any colour this model produces), so it is re-summed in the backward's
+    // order only when the forward sum lies within 1e-9 of zero.
+    uint32_t neg_bits = 0u;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        bool neg = col[c] < 0.0;
+        if (fabs(col[c]) < OSB_K1_LAZY_BAND) neg = backward_order_sum(dir, active_degree, &s_par[pl.sh(0, c)][t]) < 0.0;
+        neg_bits |= neg ? (1u << c) : 0u;
+    }
     col[0] = col[0] > 0.0 ? col[0] : 0.0;
     col[1] = col[1] > 0.0 ? col[1] : 0.0;
     col[2] = col[2] > 0.0 ? col[2] : 0.0;
@@ -228,14 +257,14 @@ __global__ void __launch_bounds__(128) k_detail(const float* __restrict__ P, int
 }  // namespace
 
 void launch_preprocess(const float* params, int n, int stride, int bc, int active_degree, const Pose& pose,
-                       int W, int H, const PreprocessOut& out, cudaStream_t s) {
+                       int W, int H, const PreprocessOut& out, cudaStream_t s, const K2Scratch& zero) {
     if (n <= 0) return;
     const int blocks = (n + kPreThreads - 1) / kPreThreads;
     switch (active_degree) {
-        case 0: launch_pdl(k_preprocess<0>, blocks, kPreThreads, s, params, n, stride, bc, pose, W, H, out); break;
-        case 1: launch_pdl(k_preprocess<1>, blocks, kPreThreads, s, params, n, stride, bc, pose, W, H, out); break;
-        case 2: launch_pdl(k_preprocess<2>, blocks, kPreThreads, s, params, n, stride, bc, pose, W, H, out); break;
-        default: launch_pdl(k_preprocess<3>, blocks, kPreThreads, s, params, n, stride, bc, pose, W, H, out); break;
+        case 0: launch_pdl(k_preprocess<0>, blocks, kPreThreads, s, params, n, stride, bc, pose, W, H, out, zero); break;
+        case 1: launch_pdl(k_preprocess<1>, blocks, kPreThreads, s, params, n, stride, bc, pose, W, H, out, zero); break;
+        case 2: launch_pdl(k_preprocess<2>, blocks, kPreThreads, s, params, n, stride, bc, pose, W, H, out, zero); break;
+        default: launch_pdl(k_preprocess<3>, blocks, kPreThreads, s, params, n, stride, bc, pose, W, H, out, zero); break;
     }
     OSB_LAUNCHED(1);
 }

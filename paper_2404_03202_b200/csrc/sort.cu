@@ -681,6 +681,18 @@ __global__ void k_k2_zero(uint32_t* __restrict__ hist, int nhist, uint32_t* __re
 }
 }  // namespace
 
+K2Scratch k2_scratch(void* sort_ws, uint32_t* long_run_flag, uint2* ranges, int tiles, void* scan_ws, int n) {
+    K2Scratch z;
+    z.hist = static_cast<uint32_t*>(sort_ws);
+    z.nhist = 2 * kMaxPasses * kBins;
+    z.flag = long_run_flag;
+    z.ranges = ranges;
+    z.tiles = tiles;
+    z.sums = static_cast<uint32_t*>(scan_ws);
+    z.nsums = scan_block_count(n);
+    return z;
+}
+
 void launch_k2_zero(void* sort_ws, uint32_t* long_run_flag, uint2* ranges, int tiles, void* scan_ws, int n,
                     cudaStream_t s) {
     launch_pdl(k_k2_zero, 64, 256, s, static_cast<uint32_t*>(sort_ws), 2 * kMaxPasses * kBins, long_run_flag, ranges,
