@@ -7,15 +7,18 @@
 //      ascending order -> (depth, id) order;
 //   2. instances are emitted in that order (exclusive scan of tiles_touched over it, then a
 //      load-balanced emission: every lane writes consecutive instances -> coalesced stores);
-//   3. a STABLE radix sort by tile id keeps the (depth, id) order inside every tile.
-// So each tile list equals the reference's sorted list element for element.
+//   3. a STABLE radix sort by tile id keeps the (depth, id) order inside every tile; its last pass
+//      writes the per-tile ranges instead of the sorted keys.
+// So each tile list equals the reference's sorted list element for element. The fast depth rank
+// sorts 24-bit FP32-derived keys instead and restores the exact (FP64 depth, id) order inside runs
+// of equal keys on the way into the emission (k_touch_sums).
 //
 // Radix sort: LSD, 8-bit digits, reduce-then-scan per digit (no serial cross-block chain — at these
 // sizes every block is resident at once, so a decoupled look-back would serialise):
 //   upsweep   per-block digit counts (warp-private shared histograms)
 //   scan      per digit, exclusive prefix over blocks + the digit's global base
-//   downsweep per-warp match_any ranking (stable), block-local sort in shared memory, coalesced
-//             scatter of runs of equal digits.
+//   downsweep stable per-warp ranking (one ballot per digit bit), block-local sort in shared
+//             memory, coalesced scatter of runs of equal digits.
 // No host synchronization inside a sort.
 #include "kernels.h"
 
@@ -566,8 +569,10 @@ __global__ void __launch_bounds__(kScanThreads) k_emit(const uint32_t* __restric
     }
 }
 
-// Four sorted keys per thread (one 16-byte load + the two neighbours): a tile's range starts where
-// the key differs from its predecessor and ends where it differs from its successor.
+// Tile ranges from stored sorted keys — only for a one-instance "sort" now (the tile sort's last
+// downsweep writes the ranges otherwise). Four keys per thread (one 16-byte load + the two
+// neighbours): a range starts where the key differs from its predecessor, ends where it differs from
+// its successor.
 __global__ void __launch_bounds__(256) k_ranges(const uint32_t* __restrict__ keys, int m_cap, const uint32_t* m_dev,
                                                 uint2* __restrict__ ranges) {
     pdl_begin();
