@@ -192,21 +192,28 @@ __global__ void __launch_bounds__(kPreThreads) k_preprocess(const float* __restr
     double basis[16];
     sh_basis(dir, active_degree, basis);
     double col[3] = {0.0, 0.0, 0.0};
+    float cmax = 0.0f;  // largest |coefficient| (FP32, one register: K1 is bound by its FP64 pipe)
 #pragma unroll
     for (int k = 0; k < nb; ++k) {
 #pragma unroll
-        for (int c = 0; c < 3; ++c) col[c] += static_cast<double>(s_par[pl.sh(k, c)][t]) * basis[k];
+        for (int c = 0; c < 3; ++c) {
+            const float coef = s_par[pl.sh(k, c)][t];
+            col[c] += static_cast<double>(coef) * basis[k];
+            cmax = fmaxf(cmax, fabsf(coef));
+        }
     }
     col[0] += 0.5; col[1] += 0.5; col[2] += 0.5;
     // K4b's colour-clamp gate: the sign of the backward's pre-clamp sum, 0.5 + terms in basis order
-    // (gradients.cpp:197-198). It differs from the forward sum (terms, then + 0.5) by rounding only
-    // (|difference| < 1e-13 for any colour this model produces), so it is re-summed in the backward's
-    // order only when the forward sum lies within 1e-9 of zero.
+    // (gradients.cpp:197-198). The two orders differ by rounding only: at most 17 roundings of partial
+    // sums bounded by S = 0.5 + sum |c_k b_k| <= 0.5 + 48 max|c_k| (|b_k| <= 3 on the unit sphere), i.e.
+    // < 2e-15 S. So the sign is re-summed in the backward's order (out of line) only when the forward
+    // sum lies within max(1e-9, 1e-14 S) of zero.
     uint32_t neg_bits = 0u;
+    const double band = fmax(OSB_K1_LAZY_BAND, 1e-14 * (0.5 + 48.0 * static_cast<double>(cmax)));
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         bool neg = col[c] < 0.0;
-        if (fabs(col[c]) < OSB_K1_LAZY_BAND) neg = backward_order_sum(dir, active_degree, &s_par[pl.sh(0, c)][t]) < 0.0;
+        if (fabs(col[c]) < band) neg = backward_order_sum(dir, active_degree, &s_par[pl.sh(0, c)][t]) < 0.0;
         neg_bits |= neg ? (1u << c) : 0u;
     }
     col[0] = col[0] > 0.0 ? col[0] : 0.0;
