@@ -115,6 +115,9 @@ static __device__ __noinline__ float2 k4a_slow(uint32_t gid) {
 // and makes all nine accumulated values zero. Only the FP64 fallback (pairs inside the guard band,
 // or the 0.99 clamp gate of a near-opaque splat) branches, warp-uniformly.
 template <bool BG>
+#ifndef OSB_K4A_DIRECT
+#define OSB_K4A_DIRECT 10  // a quarter's entry with at most this many contributing pixels: direct atomics
+#endif
 #ifndef OSB_K4A_CTAS
 #define OSB_K4A_CTAS 4  // CTAs per SM (64 registers)
 #endif
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K4A_CTAS) k_backward_pixels(
                 // branch-free loop: <=6 direct 0.988, <=10 0.954; one or two butterfly levels then direct
                 // adds by the group leaders 1.177 / 1.027; the tree's sums gathered into two red.v4 + one
                 // scalar per half 1.055 — the L2 absorbs nine scalar reds better than the extra shuffles)
-                const bool multi = __popc(hb) > 10;
+                const bool multi = __popc(hb) > OSB_K4A_DIRECT;
                 if (!multi && has) {
                     red_add_v4(reinterpret_cast<float4*>(a), v01.x, v01.y, v2, v3);
                     red_add_v4(reinterpret_cast<float4*>(a) + 1, v45.x, v45.y, v67.x, v67.y);
