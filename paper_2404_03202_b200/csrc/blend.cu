@@ -16,13 +16,17 @@ namespace osb {
 
 namespace {
 
-template <bool STRICT>
+#ifdef OSB_K3_STATS
+// Instrumented build only (scripts/k4a_stats.py --k3): K3 lane-loop statistics per launch.
+__device__ unsigned long long g_k3_stats[5];
+#endif
 #ifndef OSB_K3_ELLIPSE
 #define OSB_K3_ELLIPSE false  // K3 stages box masks (per-row ellipse intervals: measured slower in K3)
 #endif
 #ifndef OSB_K3_CTAS
 #define OSB_K3_CTAS 4  // CTAs per SM (64 registers)
 #endif
+template <bool STRICT>
 __global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint32_t* __restrict__ inst_gid,
                                                            uint2* __restrict__ ranges, PreprocessOut pp, int W,
                                                            int H, int tiles_x, float bg0, float bg1, float bg2,
@@ -69,6 +73,9 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint3
     bool done = !inside;
 
     const int t = threadIdx.x;
+#ifdef OSB_K3_STATS
+    unsigned long long st[5] = {0, 0, 0, 0, 0};
+#endif
     uint32_t gid_next[kPer];  // ids one round ahead
 #pragma unroll
     for (int e = 0; e < kPer; ++e)
@@ -115,12 +122,25 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint3
                 while (bal != 0u && !done && !pend) {
                     const int j = __ffs(bal) - 1;
                     bal &= bal - 1u;
+#ifdef OSB_K3_STATS
+                    {
+                        const uint32_t am = __activemask();
+                        if (lane == __ffs(am) - 1) {
+                            st[0] += 1;  // warp iterations
+                            st[4] += ((am & 0xFFFFu) != 0u) + ((am >> 16) != 0u);  // live halves
+                        }
+                        st[1] += 1;  // lanes evaluating
+                    }
+#endif
                     const float4 A = ws.a(j);
                     const float4 B = ws.b(j);
                     float2 d;
                     float power;
                     bool unc;
                     if (!pair_power2<SEAM>(A, B, nlo, halfW, fW, d, power, unc)) continue;
+#ifdef OSB_K3_STATS
+                    st[2] += 1;  // lanes past the power test
+#endif
                     const float4 Cc = ws.c(j);
                     float alpha;
                     double a64 = 0.0;
@@ -185,6 +205,9 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint3
                     }
                     c01 = __ffma2_rn(make_float2(Cc.x, Cc.y), make_float2(w, w), c01);
                     c2 = __fmaf_rn(Cc.z, w, c2);
+#ifdef OSB_K3_STATS
+                    st[3] += 1;  // lanes contributing
+#endif
                     ++contrib;
                     last = kofs + j;
                 }
@@ -231,6 +254,9 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint3
         // no barrier here: the next round's __syncthreads_or is the one that orders this round's
         // stage reads before the restaging
     }
+#ifdef OSB_K3_STATS
+    for (int q = 0; q < 5; ++q) atomicAdd(&g_k3_stats[q], st[q]);
+#endif
     if (inside) {
         const size_t pix = static_cast<size_t>(py) * W + px;
         const size_t plane = static_cast<size_t>(W) * H;
@@ -300,5 +326,15 @@ void launch_blend(const uint32_t* inst_gid, uint2* ranges, const PreprocessOut& 
         k_blend<false><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb);
     OSB_LAUNCHED(1);
 }
+
+#ifdef OSB_K3_STATS
+extern "C" __attribute__((visibility("default"))) void osb_k3_stats(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, g_k3_stats, sizeof(unsigned long long) * 5);
+    if (reset) {
+        unsigned long long z[5] = {0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_k3_stats, z, sizeof(z));
+    }
+}
+#endif
 
 }  // namespace osb

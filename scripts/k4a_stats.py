@@ -30,8 +30,16 @@ def main():
     lib.osb_k4a_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
     out = (C.c_ulonglong * 8)()
     lib.osb_k4a_stats(out, 1)
+    k3 = (C.c_ulonglong * 5)()
+    has_k3 = hasattr(lib, "osb_k3_stats")
+    if has_k3:
+        lib.osb_k3_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+        lib.osb_k3_stats(k3, 1)
     ctx.profile(timing=False, count_work=True)
     fr = ctx.render(poses[0], W, H)
+    ctx.synchronize()
+    if has_k3:
+        lib.osb_k3_stats(k3, 1)
     _, dimg = ctx.loss(fr, gt.data_ptr(), 0.2, 0.0, want_value=False)
     ctx.backward_device(fr, dimg)
     fwd, bwd, inst = fr.work()
@@ -39,6 +47,9 @@ def main():
     lib.osb_k4a_stats(out, 1)
     st = {n: int(out[i]) for i, n in enumerate(NAMES)}
     st.update(bwd_pairs=bwd, fwd_pairs=fwd, instances=inst)
+    if has_k3:
+        st.update({f"k3_{n}": int(k3[i]) for i, n in enumerate(
+            ["warp_iterations", "lanes_evaluated", "lanes_past_power", "lanes_contributing", "live_halves"])})
     print(json.dumps(st))
 
 
