@@ -30,7 +30,7 @@ template <bool STRICT>
 __global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint32_t* __restrict__ inst_gid,
                                                            uint2* __restrict__ ranges, PreprocessOut pp, int W,
                                                            int H, int tiles_x, float bg0, float bg1, float bg2,
-                                                           FrameBuffers fb) {
+                                                           FrameBuffers fb, int tile0) {
     pdl_begin();
     // CTA-cooperative walk: the 8 warps stage 512 entries at once (two per thread, each entry once
     // per tile instead of once per warp, with a 16-bit reach mask for all quarters), then every warp
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint3
     constexpr int kSubs = kChunk / 32;
     __shared__ WarpStage stage[kSubs];
     __shared__ uint16_t s_mask[kChunk];
-    const int tile = block_tile(tiles_x, (H + kTile - 1) / kTile);
+    const int tile = tile0 + block_tile(tiles_x, (H + kTile - 1) / kTile);  // tile0: banded launches
     const int tx = tile % tiles_x, ty = tile / tiles_x;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const WarpPixel wp = warp_pixel(warp, lane);
@@ -291,9 +291,9 @@ __global__ void k_work_count(const int* __restrict__ visited, const int* __restr
 }  // namespace
 
 namespace {
-__global__ void __launch_bounds__(256) k_planar_to_hwc_f64(const float* __restrict__ rgb, size_t plane,
-                                                           double* __restrict__ out) {
-    for (size_t i = blockIdx.x * 256ull + threadIdx.x; i < plane; i += static_cast<size_t>(gridDim.x) * 256ull) {
+__global__ void __launch_bounds__(256) k_planar_to_hwc_f64(const float* __restrict__ rgb, size_t plane, size_t p0,
+                                                           size_t p1, double* __restrict__ out) {
+    for (size_t i = p0 + blockIdx.x * 256ull + threadIdx.x; i < p1; i += static_cast<size_t>(gridDim.x) * 256ull) {
         out[3 * i] = rgb[i];
         out[3 * i + 1] = rgb[plane + i];
         out[3 * i + 2] = rgb[2 * plane + i];
@@ -301,11 +301,12 @@ __global__ void __launch_bounds__(256) k_planar_to_hwc_f64(const float* __restri
 }
 }  // namespace
 
-void launch_planar_to_hwc_f64(const float* rgb, size_t plane, double* out, cudaStream_t s) {
-    if (plane == 0) return;
-    size_t blocks = (plane + 255) / 256;
+void launch_planar_to_hwc_f64(const float* rgb, size_t plane, double* out, cudaStream_t s, size_t p0, size_t p1) {
+    if (p1 == static_cast<size_t>(-1)) p1 = plane;
+    if (p1 <= p0) return;
+    size_t blocks = (p1 - p0 + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    k_planar_to_hwc_f64<<<static_cast<int>(blocks), 256, 0, s>>>(rgb, plane, out);
+    k_planar_to_hwc_f64<<<static_cast<int>(blocks), 256, 0, s>>>(rgb, plane, p0, p1, out);
     OSB_LAUNCHED(1);
 }
 
@@ -317,13 +318,17 @@ void launch_work_count(const FrameBuffers& fb, int pixels, unsigned long long* o
 }
 
 void launch_blend(const uint32_t* inst_gid, uint2* ranges, const PreprocessOut& pp, int W, int H, int tiles_x,
-                  int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s, bool strict) {
-    const int tiles = tiles_x * tiles_y;
+                  int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s, bool strict, int row0,
+                  int row1) {
+    if (row1 < 0 || row1 > tiles_y) row1 = tiles_y;
+    const int tile0 = row0 * tiles_x, tiles = (row1 - row0) * tiles_x;
     if (tiles <= 0) return;
     if (strict)
-        k_blend<true><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb);
+        k_blend<true><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb,
+                                                     tile0);
     else
-        k_blend<false><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb);
+        k_blend<false><<<tiles, kTileThreads, 0, s>>>(inst_gid, ranges, pp, W, H, tiles_x, bg[0], bg[1], bg[2], fb,
+                                                      tile0);
     OSB_LAUNCHED(1);
 }
 

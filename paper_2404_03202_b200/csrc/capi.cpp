@@ -574,13 +574,9 @@ osplat_status osplat_render(const osplat_cloud* cloud, const double transform_cw
         img->height = height;
         img->pinned_bytes = plane * 3 * sizeof(double);
         img->pinned = pinned_acquire(img->pinned_bytes);
-        osb::Frame* f = e.render(p12, width, height, bg);
-        try {
-            e.image_hwc(f, img->pinned);  // FP32 planes -> H x W x 3 doubles on the device, one D2H
-        } catch (...) {
-            e.release(f);
-            throw;
-        }
+        // FP32 planes -> H x W x 3 doubles on the device, copied to the pinned image band by band
+        // while the rest of the frame blends
+        osb::Frame* f = e.render_hwc(p12, width, height, bg, img->pinned);
         e.release(f);
         *out = img.release();
     });

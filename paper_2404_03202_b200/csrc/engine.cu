@@ -160,6 +160,11 @@ Engine::~Engine() {
         cudaEventDestroy(ev.b);
     }
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
+    if (d2h_stream_) {
+        cudaStreamSynchronize(d2h_stream_);
+        cudaStreamDestroy(d2h_stream_);
+    }
+    for (cudaEvent_t e : band_ev_) cudaEventDestroy(e);
     if (copy_stream_) {
         cudaStreamSynchronize(copy_stream_);
         cudaEventDestroy(target_ready_);
@@ -340,7 +345,11 @@ Frame* Engine::render_projected(const double* planes, size_t n, int W, int H, co
 // asynchronously; the first consumer of the frame (validate) checks them and, in the rare case of
 // an overflow or a long run of equal FP32 depth keys, grows the buffers / switches to the exact
 // 64-bit depth sort and renders the frame again.
+#ifndef OSB_HWC_BANDS
+#define OSB_HWC_BANDS 8  // render_hwc: bands of tile rows (the D2H of 50 MB of doubles is the bound)
+#endif
 void Engine::render_into(Frame* f) {
+    ++renders_;
     const int W = f->W, H = f->H;
     const size_t n = f->n > 0 ? static_cast<size_t>(f->n) : 1;
     const size_t pixels = static_cast<size_t>(W) * H;
@@ -480,11 +489,36 @@ void Engine::render_into(Frame* f) {
                                         tile_bits, f->sort_ws.as<void>(), stream_, f->total.as<uint32_t>(),
                                         fused_counts, true, f->ranges.as<uint2>());  // + the tile ranges
     }
-    // K3
+    // K3 (render_hwc: in bands of tile rows, each band's host copy queued behind it on the D2H stream)
     {
         Span sp(*this, kBlend);
-        launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(), stream_,
-                     strict_guard_);
+        if (!hwc_host_) {
+            launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(),
+                         stream_, strict_guard_);
+        } else {
+            constexpr int kBands = OSB_HWC_BANDS;
+            const size_t plane = pixels;
+            hwc_.ensure(plane * 3 * sizeof(double));
+            if (!d2h_stream_) OSB_CUDA_CHECK(cudaStreamCreateWithFlags(&d2h_stream_, cudaStreamNonBlocking));
+            while (band_ev_.size() < static_cast<size_t>(kBands)) {
+                cudaEvent_t e;
+                OSB_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                band_ev_.push_back(e);
+            }
+            for (int b = 0; b < kBands; ++b) {
+                const int r0 = f->tiles_y * b / kBands, r1 = f->tiles_y * (b + 1) / kBands;
+                if (r1 <= r0) continue;
+                launch_blend(f->inst_gid(), f->ranges.as<uint2>(), pp, W, H, f->tiles_x, f->tiles_y, f->bg, f->fb(),
+                             stream_, strict_guard_, r0, r1);
+                OSB_CUDA_CHECK(cudaEventRecord(band_ev_[b], stream_));
+                OSB_CUDA_CHECK(cudaStreamWaitEvent(d2h_stream_, band_ev_[b], 0));
+                const size_t p0 = static_cast<size_t>(r0) * kTile * W;
+                const size_t p1 = std::min(static_cast<size_t>(r1) * kTile, static_cast<size_t>(H)) * W;
+                launch_planar_to_hwc_f64(f->rgb.as<float>(), plane, hwc_.as<double>(), d2h_stream_, p0, p1);
+                OSB_CUDA_CHECK(cudaMemcpyAsync(hwc_host_ + 3 * p0, hwc_.as<double>() + 3 * p0,
+                                               (p1 - p0) * 3 * sizeof(double), cudaMemcpyDeviceToHost, d2h_stream_));
+            }
+        }
     }
     f->validated = false;
     f->M = cap;  // provisional until validate()
@@ -663,6 +697,31 @@ const double* Engine::image_hwc_device(Frame* f) {
     hwc_.ensure(plane * 3 * sizeof(double));
     launch_planar_to_hwc_f64(f->rgb.as<float>(), plane, hwc_.as<double>(), stream_);
     return hwc_.as<double>();
+}
+
+Frame* Engine::render_hwc(const double pose12[12], int W, int H, const double bg[3], double* host) {
+    DeviceGuard g(device_);
+    hwc_host_ = host;
+    Frame* f = nullptr;
+    try {
+        f = render(pose12, W, H, bg);
+    } catch (...) {
+        hwc_host_ = nullptr;
+        if (d2h_stream_) cudaStreamSynchronize(d2h_stream_);
+        throw;
+    }
+    hwc_host_ = nullptr;
+    try {
+        const unsigned long before = renders_;
+        validate(f);  // a re-render (instance overflow, long depth run) blends in one launch, no copies
+        OSB_CUDA_CHECK(cudaStreamSynchronize(d2h_stream_));
+        if (renders_ != before) image_hwc(f, host);  // the banded copies held the first attempt
+    } catch (...) {
+        if (d2h_stream_) cudaStreamSynchronize(d2h_stream_);
+        release(f);
+        throw;
+    }
+    return f;
 }
 
 void Engine::image_hwc(Frame* f, double* host) {

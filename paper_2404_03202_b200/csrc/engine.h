@@ -147,6 +147,10 @@ public:
     // The frame's colour as H x W x 3 doubles (Image layout, image.hpp:10-23) in host memory:
     // converted on the device, one D2H copy (full speed into pinned memory), synchronous.
     void image_hwc(Frame* f, double* host);
+    // render + image_hwc with the host copy overlapped: K3 blends the frame in bands of tile rows
+    // and each band is converted and copied to `host` (pinned) on a side stream while the next band
+    // blends. Returns the frame (validated; its image is in `host`).
+    Frame* render_hwc(const double pose12[12], int W, int H, const double bg[3], double* host);
     // The same conversion into a device buffer owned by the engine (valid until the next call).
     const double* image_hwc_device(Frame* f);
     // Adam over all planes, or over the flat element range [begin, begin + count) (multiples of 4;
@@ -247,6 +251,12 @@ private:
     std::vector<std::unique_ptr<Frame>> pool_;
     std::vector<Frame*> free_;
     cudaStream_t copy_stream_ = nullptr;
+    // render_hwc: the host image of the frame being rendered (nullptr otherwise), its D2H stream and
+    // band events; renders_ counts render_into calls (a validate() re-render is detected by it)
+    double* hwc_host_ = nullptr;
+    cudaStream_t d2h_stream_ = nullptr;
+    std::vector<cudaEvent_t> band_ev_;
+    unsigned long renders_ = 0;
     cudaEvent_t target_ready_ = nullptr, target_free_ = nullptr;
 
     // profiler

@@ -120,13 +120,17 @@ struct FrameBuffers {
 // Sums of per-pixel visited (forward pairs) and last_contrib (backward pairs) -> out[0], out[1].
 void launch_work_count(const FrameBuffers& fb, int pixels, unsigned long long* out, cudaStream_t s);
 // 3 FP32 planes -> interleaved H x W x 3 FP64 (the reference Image layout).
-void launch_planar_to_hwc_f64(const float* rgb, size_t plane, double* out, cudaStream_t s);
+// pixels [p0, p1) of the planar FP32 image into H x W x 3 doubles (the whole image by default)
+void launch_planar_to_hwc_f64(const float* rgb, size_t plane, double* out, cudaStream_t s, size_t p0 = 0,
+                              size_t p1 = static_cast<size_t>(-1));
 // strict: the T-stop guard band is the rigorous running error bound instead of the 2^-10 band
 // (common.cuh); slower (more FP64 replays), decisions provably the FP64 reference's.
 // ranges: read, and empty tiles left as {~0u, 0} by the fused tile sort are stored back as {0, 0}
+// tile rows [row0, row1) only (row1 < 0: to the last row): a frame can be blended in bands so the
+// host copy of one band overlaps the blending of the next (Engine::render_hwc).
 void launch_blend(const uint32_t* inst_gid, uint2* ranges, const PreprocessOut& pp, int W, int H,
                   int tiles_x, int tiles_y, const float bg[3], const FrameBuffers& fb, cudaStream_t s,
-                  bool strict = false);
+                  bool strict = false, int row0 = 0, int row1 = -1);
 
 // ---- K4 backward (backward.cu) --------------------------------------------------------------
 // Deterministic K4a (optional mode, gradients.cpp:94-169's fixed-order reduction): per tile the 16

@@ -130,6 +130,24 @@ def test_osplat_render_c_abi_matches_frame(oracle_port):
     assert np.max(np.abs(img - of.rgb)) <= IMAGE_ATOL
 
 
+def test_osplat_render_banded_copy_and_rerender(oracle_port):
+    """osplat_render blends in bands of tile rows and copies each band to the host image while the
+    next blends (Engine::render_hwc); an odd-sized image (partial last tile row) and a frame whose
+    instances outgrow the pooled buffer (re-rendered on validation, then copied again) must both
+    equal the oracle."""
+    cloud = _scene("uniform", 4_000, 15)
+    hc = native.HostCloud.from_cloud(cloud)
+    pose = scenes.random_pose(np.random.default_rng(3))
+    small = native.osplat_render(hc, pose, 64, 32)  # sizes the cloud's pooled frame small
+    of_small = oracle_port.render(cloud, pose, 64, 32)
+    assert np.max(np.abs(small - of_small.rgb)) <= IMAGE_ATOL
+    for W, H in ((520, 250), (512, 256)):  # the first outgrows the pool and is re-rendered
+        img = native.osplat_render(hc, pose, W, H)
+        of = oracle_port.render(cloud, pose, W, H)
+        assert img.shape == (H, W, 3)
+        assert np.max(np.abs(img - of.rgb)) <= IMAGE_ATOL, (W, H)
+
+
 def test_empty_and_culled_clouds():
     empty = scenes.synthetic_cloud(0, seed=1)
     ctx = native.Context(empty)
