@@ -475,8 +475,8 @@ __global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __re
     }
 
     // mean path: dL/dt = J^T dL/dp (gradients.cpp:212-213)
-    double jac[6];
-    jacobian_equirect(t, t_r, W, H, jac);
+    double jac[6], jg[18];
+    jacobian_equirect_and_grad_fast(t, t_r, W, H, jac, jg);
     double d_t[3] = {jac[0] * d_p[0] + jac[3] * d_p[1], jac[1] * d_p[0] + jac[4] * d_p[1],
                      jac[2] * d_p[0] + jac[5] * d_p[1]};
 
@@ -504,7 +504,12 @@ __global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __re
     for (int k = 0; k < 3; ++k) s[k] = exp(static_cast<double>(lsf[k]));
 #pragma unroll
     for (int k = 0; k < 4; ++k) q[k] = static_cast<double>(qf[k]);
-    covariance3d(q, s, s3);
+    // normalised once, by one reciprocal (a few ulp from the reference's divisions; the gradients'
+    // tolerance allows it), for Sigma, the rotation and the normalisation's gradient below
+    const double inv_n = 1.0 / qnorm(q);
+    double qu[4];
+    qu[0] = q[0] * inv_n; qu[1] = q[1] * inv_n; qu[2] = q[2] * inv_n; qu[3] = q[3] * inv_n;
+    covariance3d_unit(qu, s, s3);
     double sm0[3], sm1[3];
     m3v(s3, m0, sm0);
     m3v(s3, m1, sm1);
@@ -521,8 +526,6 @@ __global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __re
         for (int b = 0; b < 3; ++b) Rt[a * 3 + b] = pose.R[b * 3 + a];
     double djac[6];
     m23_mul(dm, Rt, djac);
-    double jg[18];
-    jacobian_equirect_grad(t, t_r, W, H, jg);
 #pragma unroll
     for (int r = 0; r < 6; ++r) {
         const double dj = djac[r];
@@ -535,8 +538,7 @@ __global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __re
     for (int c = 0; c < 3; ++c) put_grad<OVERWRITE>(G, stride, c, gid, dpos[c] + d_m_sh[c]);
 
     // Sigma3 -> quaternion (through normalisation) and log-scales (gradients.cpp:260-293)
-    double qu[4], rot[9];
-    qnormalize(q, qu);
+    double rot[9];
     quat_rot(qu, rot);
     double drot[9];
 #pragma unroll
@@ -561,10 +563,9 @@ __global__ void __launch_bounds__(128, 4) k_backward_gaussians(const float* __re
         for (int i = 0; i < 9; ++i) v += drot[i] * rg[k][i];
         dqu[k] = v;
     }
-    const double qn = qnorm(q);
     const double qdot = qu[0] * dqu[0] + qu[1] * dqu[1] + qu[2] * dqu[2] + qu[3] * dqu[3];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) put_grad<OVERWRITE>(G, stride, pl.rot(k), gid, (dqu[k] - qu[k] * qdot) / qn);
+    for (int k = 0; k < 4; ++k) put_grad<OVERWRITE>(G, stride, pl.rot(k), gid, (dqu[k] - qu[k] * qdot) * inv_n);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const double rk[3] = {rot[k], rot[3 + k], rot[6 + k]};

@@ -116,10 +116,17 @@ __device__ __forceinline__ void qnormalize(const double* q, double* o) {
     double n = qnorm(q);
     o[0] = q[0] / n; o[1] = q[1] / n; o[2] = q[2] / n; o[3] = q[3] / n;
 }
+// Sigma = R diag(s^2) R^T from an already normalised quaternion (K4b: normalised once, by a
+// reciprocal, for both Sigma and the rotation gradient).
+__device__ __forceinline__ void covariance3d_unit(const double* qu, const double* s, double* sig);
 // Sigma = R diag(s^2) R^T (scene.cpp:94-102), returned as the mirrored symmetric 3x3.
 __device__ __forceinline__ void covariance3d(const double* q, const double* s, double* sig) {
-    double qu[4], r[9];
+    double qu[4];
     qnormalize(q, qu);
+    covariance3d_unit(qu, s, sig);
+}
+__device__ __forceinline__ void covariance3d_unit(const double* qu, const double* s, double* sig) {
+    double r[9];
     quat_rot(qu, r);
     double s2[3] = {s[0] * s[0], s[1] * s[1], s[2] * s[2]};
     double f[9];

@@ -74,6 +74,41 @@ __device__ __forceinline__ void jacobian_equirect_grad(const double* t, double t
     g[17] = -base * ty * (1.0 - 2.0 * tz * tz / r2 - tz * tz / u);
 }
 
+// K4b's J and dJ/dt together, with one reciprocal per denominator instead of ~20 FP64 divisions:
+// within a few ulp of the two functions above (K4b only produces gradients, held to 1e-3 relative;
+// K1 keeps the divisions, whose results feed exact tile decisions).
+__device__ __forceinline__ void jacobian_equirect_and_grad_fast(const double* t, double t_r, int W, int H, double* j,
+                                                                double* g) {
+    const double tx = t[0], ty = t[1], tz = t[2];
+    const double u = tx * tx + tz * tz;
+    const double rho = sqrt(u);
+    const double r2 = t_r * t_r;
+    const double inv_u = 1.0 / u, inv_r2 = 1.0 / r2, inv_rho = 1.0 / rho;
+    const double wf = W / (2.0 * kPi);
+    const double hf = H / kPi;
+    j[0] = wf * tz * inv_u;
+    j[1] = 0.0;
+    j[2] = -wf * tx * inv_u;
+    const double base = hf * inv_r2 * inv_rho;  // hf / (r2 rho)
+    j[3] = -base * tx * ty;
+    j[4] = hf * rho * inv_r2;
+    j[5] = -base * tz * ty;
+    const double inv_u2 = inv_u * inv_u;
+    g[0] = -2.0 * wf * tx * tz * inv_u2; g[1] = 0.0; g[2] = wf * (tx * tx - tz * tz) * inv_u2;
+    g[3] = 0.0; g[4] = 0.0; g[5] = 0.0;
+    g[6] = g[2]; g[7] = 0.0; g[8] = -g[0];
+    const double a = 2.0 * inv_r2;
+    g[9] = -base * ty * (1.0 - a * tx * tx - tx * tx * inv_u);
+    g[10] = -base * tx * (1.0 - a * ty * ty);
+    g[11] = base * tx * ty * tz * (a + inv_u);
+    g[12] = base * tx * (1.0 - a * u);
+    g[13] = -2.0 * hf * rho * ty * inv_r2 * inv_r2;
+    g[14] = base * tz * (1.0 - a * u);
+    g[15] = g[11];
+    g[16] = -base * tz * (1.0 - a * ty * ty);
+    g[17] = -base * ty * (1.0 - a * tz * tz - tz * tz * inv_u);
+}
+
 // project_gaussian (rasterizer.cpp:17-55) minus the SH colour. Returns false when culled
 // (t_r < 0.01, pole-degenerate, opacity < 1/255).
 // ld(plane) returns this Gaussian's FP32 parameter of that plane (global memory, or K1's shared-
