@@ -195,6 +195,26 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
+// ---- TMA bulk staging (cp.async.bulk + mbarrier): K1 / K4b stage their CTA's parameter tile ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "MBAR_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 // Programmatic dependent launch (K2's chain of short kernels): a kernel launched with
 // launch_pdl waits for its predecessor's completion and memory (griddepcontrol.wait) before reading
 // anything the predecessor wrote, then lets its own successor be scheduled onto SMs as they free up

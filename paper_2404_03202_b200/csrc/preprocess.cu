@@ -89,26 +89,6 @@ __device__ __forceinline__ void write_record(int gid, const double* p, const dou
     out.splat[gid] = s;
 }
 
-// ---- TMA bulk staging of the CTA's parameter tile (cp.async.bulk + mbarrier) ----------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "MBAR_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra MBAR_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
 #ifndef OSB_K1_LAZY_BAND
 #define OSB_K1_LAZY_BAND 1e-9  // (A/B: a huge band re-sums every channel in the backward's order)
 #endif
