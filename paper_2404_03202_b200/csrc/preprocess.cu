@@ -41,13 +41,16 @@ __device__ __forceinline__ void write_record(int gid, const double* p, const dou
     // FP32 blend record and the guard band on `power`. Pairs with power within
     // delta of pthr = ln(255 o) or of 0 are resolved by the FP64 path in K3/K4a.
     const double qa = conic[0], qb = conic[1], qc = conic[2];
-    const double pthr = log(255.0 * o);
+    // ln(255 o) only places the FP32 classifier's band, never a decision itself: FP32 logf (<= 1 ulp,
+    // < 5e-7 absolute below ln 255 + the argument's rounding 6e-8) instead of the FP64 log, its error
+    // added to the band below (+1e-6)
+    const double pthr = static_cast<double>(logf(static_cast<float>(255.0 * o)));
     const double lmin = mid - dd;
     const double lam_q_max = 1.0 / (lmin > 1e-300 ? lmin : 1e-300);
     const double P_ = (pthr > 0.0 ? pthr : 0.0) + 1.0;
     const double dmax = sqrt(2.0 * P_ * lmax);
     const double tmax = 0.5 * (fabs(qa) + fabs(qb) + fabs(qc)) * dmax * dmax;
-    double delta = 0x1p-20 * (tmax + lam_q_max * dmax * (dmax + 16.0)) + 0x1p-21 * fabs(pthr) + 1e-6;
+    double delta = 0x1p-20 * (tmax + lam_q_max * dmax * (dmax + 16.0)) + 0x1p-21 * fabs(pthr) + 2e-6;
     if (!(delta < 1e30)) delta = 1e30;
 
     out.depth_key[gid] = static_cast<uint64_t>(__double_as_longlong(t_r));
@@ -81,8 +84,9 @@ __device__ __forceinline__ void write_record(int gid, const double* p, const dou
     // > pthr + delta, i.e. a certain skip, so culling by these extents preserves every decision.
     // (>= 0: only an imported record can have o < 1/255, and it never passes the alpha test)
     const double Pext = fmax((pthr + 3.0 * delta) * (1.0 + 1e-4) + 1e-3, 0.0);
-    const double ex = sqrt(2.0 * Pext * (a > 0.0 ? a : 0.0)) * (1.0 + 1e-5) + 0.02;
-    const double ey = sqrt(2.0 * Pext * (c > 0.0 ? c : 0.0)) * (1.0 + 1e-5) + 0.02;
+    // (FP32 sqrt of the FP32-rounded argument: relative error ~1e-7, inside the 1e-5 slack)
+    const double ex = static_cast<double>(sqrtf(static_cast<float>(2.0 * Pext * (a > 0.0 ? a : 0.0)))) * (1.0 + 1e-5) + 0.02;
+    const double ey = static_cast<double>(sqrtf(static_cast<float>(2.0 * Pext * (c > 0.0 ? c : 0.0)))) * (1.0 + 1e-5) + 0.02;
     s.ext_x = ex < 1e30 ? static_cast<float>(ex) : 1e30f;
     s.ext_y = ey < 1e30 ? static_cast<float>(ey) : 1e30f;
     s.pad = __uint_as_float(neg_bits);  // K4b's colour-clamp gate
