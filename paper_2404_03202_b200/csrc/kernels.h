@@ -63,9 +63,9 @@ bool radix_sort_u64(uint64_t* keys_in, uint64_t* keys_out, uint32_t* vals_in, ui
 // counts_ready (bits <= 16 only): the first pass's block counts and every pass's digit totals are
 // already in ws (launch_scan_emit with tile_sort_ws = ws after tile_sort_prepare(ws)).
 // tile_slot: the tile sort's digit totals live in the workspace's second slot, zeroed beforehand
-// (launch_k2_zero, or tile_sort_prepare after a workspace reallocation).
+// (K1 / launch_k2_zero, or tile_sort_prepare after a workspace reallocation).
 // ranges (tile sort): the last pass writes the tile ranges instead of the sorted keys (ranges must
-// start at {~0u, 0}: launch_k2_zero; empty tiles keep that and read as empty — K3 stores them back as
+// start at {~0u, 0}: K1 / launch_k2_zero; empty tiles keep that and read as empty — K3 stores them back as
 // {0, 0}); keys_in / keys_out then hold no sorted result.
 bool radix_sort_u32(uint32_t* keys_in, uint32_t* keys_out, uint32_t* vals_in, uint32_t* vals_out, int n,
                     int bits, void* ws, cudaStream_t s, const uint32_t* n_dev = nullptr, bool counts_ready = false,
@@ -101,7 +101,7 @@ long emit_ctas(uint32_t capacity);
 // radix_sort_u32 workspace (zeroed digit totals first: tile_sort_prepare), sized for `capacity`.
 // depth_keys24 (fast depth rank): its sorted 24-bit keys — runs of equal keys are put in exact
 // (FP64 depth_key, id) order on the way (a run longer than 64 raises *long_run_flag: redo the depth
-// rank with the full 64-bit sort). The block sums in ws start at zero (launch_k2_zero; after a
+// rank with the full 64-bit sort). The block sums in ws start at zero (K1 / launch_k2_zero; after a
 // counting pass: scan_sums_reset).
 void launch_scan_emit(const uint32_t* touched, const uint32_t* order, const int4* rect, int n, int tiles_x,
                       uint32_t* keys, uint32_t* vals, uint32_t capacity, uint32_t* total, void* ws,

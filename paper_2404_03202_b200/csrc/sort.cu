@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kSortThreads) k_downsweep(const K* __restrict_
     // not stored; the ranges come from here. Inside this block's run of one digit the keys are in
     // final (tile) order and consecutive globally, so a tile boundary between two neighbours of the
     // run is a plain store; at the run's two ends the global neighbour belongs to another block, so
-    // the start / end are combined with atomicMin / atomicMax (ranges start at {~0u, 0}: k_k2_zero;
+    // the start / end are combined with atomicMin / atomicMax (ranges start at {~0u, 0}: K1 or k_k2_zero;
     // the one plain store of a boundary is the extremum, so the order against the atomics is free).
     for (int i = tid; i < count; i += kSortThreads) {
         const uint32_t k = static_cast<uint32_t>(s_keys[i]);
@@ -340,7 +340,7 @@ __device__ __noinline__ int run_position(const uint32_t* __restrict__ keys, cons
 
 // Per depth rank r: the Gaussian that takes rank r (rank_gid), its touched count (rank_off, read
 // by k_emit_prep) and packed tile rectangle {x0 & 0xFFFF | width << 16, y0} (rank_rc; both gathers
-// issued together), and the per-block sums of touched (atomics into sums zeroed by k_k2_zero).
+// issued together), and the per-block sums of touched (atomics into sums zeroed by K1 or k_k2_zero).
 // keys (fast depth rank): the sorted 24-bit keys; every element of a run of equal keys places itself
 // at its exact (FP64 depth, id) position inside the run (replaces a separate run-fixing pass; a run
 // may straddle two blocks, so its elements add to the sum of the block they land in).
