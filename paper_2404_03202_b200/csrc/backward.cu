@@ -302,18 +302,22 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K4A_CTAS) k_backward_pixels(
                 // branch-free loop: <=6 direct 0.988, <=10 0.954; one or two butterfly levels then direct
                 // adds by the group leaders 1.177 / 1.027; the tree's sums gathered into two red.v4 + one
                 // scalar per half 1.055 — the L2 absorbs nine scalar reds better than the extra shuffles)
-                const bool multi = __popc(hb) > OSB_K4A_DIRECT;
-                if (!multi && has) {
-                    red_add_v4(reinterpret_cast<float4*>(a), v01.x, v01.y, v2, v3);
-                    red_add_v4(reinterpret_cast<float4*>(a) + 1, v45.x, v45.y, v67.x, v67.y);
-                    red_add(a + 8, v8);
-                }
-                if (__any_sync(0xffffffffu, multi)) {
+                // warp-uniform choice: when either half has more than OSB_K4A_DIRECT contributing
+                // pixels both halves go through the tree (its shuffles serve both halves at once, so
+                // the other half's reduction is free and saves its direct atomics)
+                const bool multi = __any_sync(0xffffffffu, __popc(hb) > OSB_K4A_DIRECT);
+                if (!multi) {
+                    if (has) {
+                        red_add_v4(reinterpret_cast<float4*>(a), v01.x, v01.y, v2, v3);
+                        red_add_v4(reinterpret_cast<float4*>(a) + 1, v45.x, v45.y, v67.x, v67.y);
+                        red_add(a + 8, v8);
+                    }
+                } else {
                     OSB_STAT(3, 1);
                     const float v[9] = {v01.x, v01.y, v2, v3, v45.x, v45.y, v67.x, v67.y, v8};
                     int idx;
                     const float sum = half_reduce9(v, lane, &idx);
-                    if (multi && idx >= 0) red_add(a + idx, sum);
+                    if (hb != 0u && idx >= 0) red_add(a + idx, sum);
                 }
             }
         };
