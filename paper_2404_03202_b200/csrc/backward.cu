@@ -4,8 +4,9 @@
 // and half-warp culling as K3 (pair.cuh), each 4x4 quarter walking its entries back to front from
 // each pixel's last_contrib. The 9 per-entry accumulators (d_colour 3, d_opacity, d_p 2, d_conic 3)
 // of a quarter's pixels are combined with a reduce-scatter shuffle tree inside the half-warp and
-// added by one red.global.add.f32 per value; an entry touched by at most 10 pixels of the quarter
-// is added directly by those lanes (2 x red.v4 + 1 each). Pair decisions are the forward's;
+// added by one red.global.add.f32 per value; when neither half of the warp has more than 10
+// contributing pixels (warp-uniform choice) the contributing lanes add directly (2 x red.v4 + 1
+// each). Pair decisions are the forward's;
 // the 0.99 clamp gate (gradients.cpp:146) has its own FP64 guard.
 //
 // K4b replaces pass 3 (gradients.cpp:173-295): one thread per visible Gaussian, FP64 internals,
