@@ -4,9 +4,8 @@
 // and half-warp culling as K3 (pair.cuh), each 4x4 quarter walking its entries back to front from
 // each pixel's last_contrib. The 9 per-entry accumulators (d_colour 3, d_opacity, d_p 2, d_conic 3)
 // of a quarter's pixels are combined with a reduce-scatter shuffle tree inside the half-warp and
-// added by one red.global.add.f32 per value; when neither half of the warp has more than 10
-// contributing pixels (warp-uniform choice) the contributing lanes add directly (2 x red.v4 + 1
-// each). Pair decisions are the forward's;
+// added by one red.global.add.f32 per value; when the warp has at most 14 contributing lanes
+// (warp-uniform choice) they add directly (2 x red.v4 + 1 each). Pair decisions are the forward's;
 // the 0.99 clamp gate (gradients.cpp:146) has its own FP64 guard.
 //
 // K4b replaces pass 3 (gradients.cpp:173-295): one thread per visible Gaussian, FP64 internals,
@@ -116,6 +115,9 @@ static __device__ __noinline__ float2 k4a_slow(uint32_t gid) {
 // and makes all nine accumulated values zero. Only the FP64 fallback (pairs inside the guard band,
 // or the 0.99 clamp gate of a near-opaque splat) branches, warp-uniformly.
 template <bool BG>
+#ifndef OSB_K4A_TOTAL
+#define OSB_K4A_TOTAL 14  // tree when the warp has more contributing lanes (0: either half > OSB_K4A_DIRECT)
+#endif
 #ifndef OSB_K4A_DIRECT
 #define OSB_K4A_DIRECT 10  // a quarter's entry with at most this many contributing pixels: direct atomics
 #endif
@@ -303,10 +305,16 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K4A_CTAS) k_backward_pixels(
                 // branch-free loop: <=6 direct 0.988, <=10 0.954; one or two butterfly levels then direct
                 // adds by the group leaders 1.177 / 1.027; the tree's sums gathered into two red.v4 + one
                 // scalar per half 1.055 — the L2 absorbs nine scalar reds better than the extra shuffles)
-                // warp-uniform choice: when either half has more than OSB_K4A_DIRECT contributing
-                // pixels both halves go through the tree (its shuffles serve both halves at once, so
-                // the other half's reduction is free and saves its direct atomics)
+                // warp-uniform choice: when the warp has more than OSB_K4A_TOTAL contributing lanes
+                // both halves go through the tree (its shuffles serve both halves at once, so the
+                // other half's reduction is free and saves its direct atomics)
+#if OSB_K4A_TOTAL
+                // measured: the warp's total > 8 / 10 / 12 / 14 / 16 / 20: 0.848 / 0.832 / 0.820 /
+                // 0.814 / 0.829 / 0.954 ms; either half > 10: 0.835 ms
+                const bool multi = __popc(hb_all) > OSB_K4A_TOTAL;
+#else
                 const bool multi = __any_sync(0xffffffffu, __popc(hb) > OSB_K4A_DIRECT);
+#endif
                 if (!multi) {
                     if (has) {
                         red_add_v4(reinterpret_cast<float4*>(a), v01.x, v01.y, v2, v3);
