@@ -115,6 +115,9 @@ static __device__ __noinline__ float2 k4a_slow(uint32_t gid) {
 // and makes all nine accumulated values zero. Only the FP64 fallback (pairs inside the guard band,
 // or the 0.99 clamp gate of a near-opaque splat) branches, warp-uniformly.
 template <bool BG>
+#ifndef OSB_K4A_PER
+#define OSB_K4A_PER 2  // entries staged per thread per round (512-entry rounds)
+#endif
 #ifndef OSB_K4A_TOTAL
 #define OSB_K4A_TOTAL 14  // tree when the warp has more contributing lanes (0: either half > OSB_K4A_DIRECT)
 #endif
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K4A_CTAS) k_backward_pixels(
     pdl_begin();
     // CTA-cooperative walk (as K3): 512 entries staged at once with 16-quarter reach masks, every
     // warp then walks the 16 sub-chunks back to front.
-    constexpr int kPer = 2;                       // entries staged per thread per round
+    constexpr int kPer = OSB_K4A_PER;                      // entries staged per thread per round
     constexpr int kChunk = kPer * kTileThreads;   // entries per round (one barrier pair)
     constexpr int kSubs = kChunk / 32;
     __shared__ WarpStage stage[kSubs];

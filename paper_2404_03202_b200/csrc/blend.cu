@@ -20,6 +20,9 @@ namespace {
 // Instrumented build only (scripts/k4a_stats.py --k3): K3 lane-loop statistics per launch.
 __device__ unsigned long long g_k3_stats[5];
 #endif
+#ifndef OSB_K3_PER
+#define OSB_K3_PER 2  // entries staged per thread per round (512-entry rounds)
+#endif
 #ifndef OSB_K3_ELLIPSE
 #define OSB_K3_ELLIPSE false  // K3 stages box masks (per-row ellipse intervals: measured slower in K3)
 #endif
@@ -36,7 +39,7 @@ __global__ void __launch_bounds__(kTileThreads, OSB_K3_CTAS) k_blend(const uint3
     // per tile instead of once per warp, with a 16-bit reach mask for all quarters), then every warp
     // blends the 16 sub-chunks in list order; one barrier pair per 512 entries (256: 0.56 ms,
     // 512: 0.51 ms, 768: 0.53 ms — the barrier wait of the slowest warp is paid less often).
-    constexpr int kPer = 2;                       // entries staged per thread per round
+    constexpr int kPer = OSB_K3_PER;                      // entries staged per thread per round
     constexpr int kChunk = kPer * kTileThreads;   // entries per round (one barrier pair)
     constexpr int kSubs = kChunk / 32;
     __shared__ WarpStage stage[kSubs];
